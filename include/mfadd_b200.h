@@ -1,0 +1,169 @@
+/* include/mfadd_b200.h — C ABI of the B200-native MFA encode library
+ * (paper_2210_06528_b200/libmfadd_b200.so).
+ *
+ * The reference (`mfadd`, /root/reference/proj) has no FFI; its drop-in
+ * boundary is the C++ library API `mfadd::core`.  Every entry
+ * point below replaces one reference call, cited as file:line under
+ * proj/core/include/mfadd/.  Plain pointers and sizes only, no exceptions:
+ * each function returns a status code that maps 1:1 onto the reference's
+ * exception types (see MFADD_E* below); the C++ and Python host layers turn
+ * them back into the same exception classes.
+ *
+ * Threading: a context owns one CUDA device + stream; calls on one context
+ * must be serialised by the caller (the reference's solve() is likewise
+ * called from one orchestrating thread, solver.hpp:76).  Results are bitwise
+ * reproducible run to run (no floating-point atomics on any summation).
+ */
+#ifndef MFADD_B200_H
+#define MFADD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MFADD_ABI_VERSION 1
+
+/* status codes <-> reference exception types */
+#define MFADD_OK 0
+#define MFADD_EINVAL 1     /* std::invalid_argument                       */
+#define MFADD_ERANGE 2     /* std::out_of_range (find_span, knots.cpp:88) */
+#define MFADD_ESINGULAR 3  /* SingularFitError{dim, span} (lsq.hpp:24-28) */
+#define MFADD_ERUNTIME 4   /* std::runtime_error                          */
+#define MFADD_ELOGIC 5     /* std::logic_error                            */
+#define MFADD_ECUDA 6      /* CUDA / NCCL failure (no reference analogue) */
+#define MFADD_ENOMEM 7     /* device allocation failure                   */
+
+int mfadd_abi_version(void);
+/* Thread-local detail of the last non-zero status. */
+const char* mfadd_last_error(void);
+int mfadd_last_error_dim(void);      /* SingularFitError::dim  */
+int64_t mfadd_last_error_span(void); /* SingularFitError::span */
+
+/* ------------------------------------------------------------------ layout
+ * Replaces: Decomposition partition(grid_dims, bounds, blocks_per_dim, degree,
+ *           nctrl_per_block, overlap, clamp_interfaces)   layout.hpp:107-111
+ * Host-side metadata (integers bit-exact with the reference).  bounds may be
+ * NULL ([0,1] per dim; bounds only enter the affine coordinate map). */
+typedef struct mfadd_decomposition mfadd_decomposition;
+
+int mfadd_partition(int rank, const int64_t* grid_dims, const double* bounds /* 2*rank */,
+                    const int* blocks_per_dim, int degree, const int64_t* nctrl_per_block, int64_t overlap,
+                    int clamp_interfaces, mfadd_decomposition** out);
+void mfadd_decomposition_free(mfadd_decomposition* dec);
+int mfadd_dec_rank(const mfadd_decomposition* dec);
+int mfadd_dec_block_count(const mfadd_decomposition* dec);      /* GlobalLayout::block_count */
+/* BlockDim (layout.hpp:47-57), 16 int64 per (block, dim), field order:
+ * span_lo, span_hi, delta_lo, delta_hi, overlap_lo, overlap_hi,
+ * local_span_lo, local_span_hi, dof_lo, dof_hi, own_lo, own_hi,
+ * input_lo, input_hi, own_input_lo, own_input_hi */
+void mfadd_dec_block_dims(const mfadd_decomposition* dec, int64_t* out);
+void mfadd_dec_coords(const mfadd_decomposition* dec, int* out);  /* BlockLayout::coords */
+void mfadd_dec_nctrl(const mfadd_decomposition* dec, int64_t* out); /* GlobalLayout::n_ctrl */
+int mfadd_dec_knots(const mfadd_decomposition* dec, int dim, double* out /* nullable */); /* kvs[dim].knots */
+int mfadd_dec_neighbors(const mfadd_decomposition* dec, int block, int* out, int cap); /* BlockLayout::neighbors */
+/* SharedDofMap::holder_span for every control index along dim (layout.hpp:74-76) */
+void mfadd_dec_holder_ranges(const mfadd_decomposition* dec, int dim, int* out /* 2*n_ctrl */);
+/* exchange_volume (runtime.hpp:78) per block */
+void mfadd_dec_exchange_volume(const mfadd_decomposition* dec, int64_t* out);
+double mfadd_dec_compression_ratio(const mfadd_decomposition* dec); /* layout.hpp:114 */
+int mfadd_dec_any_shared(const mfadd_decomposition* dec);           /* SharedDofMap::any_shared */
+
+/* ----------------------------------------------------------------- device */
+typedef struct mfadd_context mfadd_context;
+/* stream: a cudaStream_t to run on, or NULL for a private stream. */
+int mfadd_context_create(int device, void* stream, mfadd_context** out);
+void mfadd_context_free(mfadd_context* ctx);
+/* Number of kernel launches this context has issued (launch accounting). */
+int64_t mfadd_context_launch_count(const mfadd_context* ctx);
+
+/* ------------------------------------------------------------------ solve
+ * Replaces: SolveResult solve(const Field&, const Decomposition&,
+ *                             const SolverConfig&)                solver.hpp:76
+ * A solver is a plan (like a cuFFT plan): the decomposition's device tables
+ * and work buffers, created once and executed per field.  Creating it is the
+ * analogue of partition() (outside the reference's timed region); executing
+ * it is solve(). */
+typedef struct {
+  int max_outer_iterations; /* SolverConfig::max_outer_iterations (solver.hpp:17) */
+  double tolerance;         /* SolverConfig::tolerance                            */
+  int workers;              /* accepted, ignored: the GPU replaces the pool       */
+  int log_errors;           /* per-epoch block residuals (solver.cpp:357-364)     */
+  int enforce_continuity;   /* SolverConfig::enforce_continuity                   */
+  int store_error;          /* materialise SolveResult::global_error on device    */
+} mfadd_solver_config;
+
+typedef struct {
+  int converged, constraint_iterations, n_epochs, n_final_jumps;
+  double final_dp, global_l2, global_linf;
+  /* PhaseTimings (solver.hpp:48-54), seconds, CUDA-event measured */
+  double t_setup, t_local_solve, t_exchange, t_constraint, t_decode;
+} mfadd_solve_summary;
+
+typedef struct {
+  int iteration; /* EpochStats (solver.hpp:40-46) */
+  double dp_max, jump_ss, jump_ms;
+} mfadd_epoch_stats;
+
+typedef struct mfadd_solver mfadd_solver;
+
+int mfadd_solver_create(mfadd_context* ctx, const mfadd_decomposition* dec, const mfadd_solver_config* cfg,
+                        mfadd_solver** out);
+void mfadd_solver_free(mfadd_solver* s);
+/* Execute solve() on a field (row-major, last dim fastest, Field::values).
+ * field_on_device != 0: `field` is a device pointer on the context's GPU.
+ * Otherwise it is host memory and is copied in on the context stream. */
+int mfadd_solve(mfadd_solver* s, const double* field, int field_on_device, mfadd_solve_summary* out);
+/* End-to-end host call: H2D(field) + solve + D2H(global lattice, and the
+ * global_error field when out_error != NULL).  This is the reference-facing
+ * drop-in: mfadd::solve with host buffers. */
+int mfadd_solve_host(mfadd_solver* s, const double* field_host, double* out_controls_host,
+                     double* out_error_host /* nullable */, mfadd_solve_summary* out);
+
+/* Results of the last solve (SolveResult members, solver.hpp:56-68). */
+int mfadd_solver_epochs(const mfadd_solver* s, mfadd_epoch_stats* out, int cap);
+/* InterfaceJump list (solver.hpp:34-38): block_a, block_b, linf_ss, linf_ms */
+int mfadd_solver_final_jumps(const mfadd_solver* s, double* out4, int cap);
+/* MfaModel::controls — the assembled global lattice, n_ctrl extents */
+int mfadd_solver_controls(const mfadd_solver* s, double* out, int out_on_device);
+/* SolveResult::global_error (requires cfg.store_error) */
+int mfadd_solver_global_error(const mfadd_solver* s, double* out, int out_on_device);
+/* BlockState::p of one block (held window, dof_lo..dof_hi extents) */
+int mfadd_solver_block_controls(const mfadd_solver* s, int block, double* out, int out_on_device);
+/* EpochStats::block_errors {l2, linf} per block of one epoch (log_errors) */
+int mfadd_solver_block_errors(const mfadd_solver* s, int epoch, double* out2);
+/* Device pointer to the global lattice (valid until the next solve/free). */
+const double* mfadd_solver_device_controls(const mfadd_solver* s);
+/* Kernel launches issued by the last mfadd_solve (launch accounting). */
+int mfadd_solver_last_launches(const mfadd_solver* s);
+
+/* ---------------------------------------------------------- fine-grained
+ * Unit-parity sub-boundaries.  All buffers are HOST memory;
+ * the work runs on the context's GPU. */
+
+/* collocation_matrix(kv, params, col_lo, col_hi)   collocation.hpp:53-58
+ * (find_span knots.hpp:36 + basis_funs knots.hpp:53 per row).  Outputs the
+ * BandedCollocation packing: first_col, count, values (m x (p+1), clipped
+ * row values left-aligned, zero padded). */
+int mfadd_collocation(mfadd_context* ctx, const double* knots, int nknots, int degree, const double* params,
+                      int64_t m, int64_t col_lo, int64_t col_hi, int64_t* out_first_col, int* out_count,
+                      double* out_values);
+
+/* Tensor fit_unconstrained(const LocalProblem&)     lsq.hpp:33
+ * Per dim d: knots[kn_off[d]..kn_off[d+1]), params[pm_off[d]..pm_off[d+1]),
+ * column window [col_lo[d], col_hi[d]); q has extents m_d (row-major);
+ * out_p has extents col_hi[d]-col_lo[d]. */
+int mfadd_fit_unconstrained(mfadd_context* ctx, int rank, int degree, const double* knots, const int64_t* kn_off,
+                            const double* params, const int64_t* pm_off, const int64_t* col_lo,
+                            const int64_t* col_hi, const double* q, double* out_p);
+
+/* Tensor decode(controls, kvs, params, col_offset)  decode.hpp:20-22 */
+int mfadd_decode(mfadd_context* ctx, int rank, int degree, const double* knots, const int64_t* kn_off,
+                 const double* params, const int64_t* pm_off, const int64_t* ctrl_ext,
+                 const int64_t* col_offset /* nullable */, const double* controls, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MFADD_B200_H */

@@ -1,0 +1,13 @@
+"""B200-native domain-decomposed MFA encode (arXiv 2210.06528 hot path).
+
+Drop-in for the reference `mfadd` core API on the encode path: partition ->
+solve -> (model, error).  All numerics run in sm_100a CUDA kernels behind the
+C ABI `include/mfadd_b200.h` (libmfadd_b200.so, built in-tree).
+"""
+from .api import (BandedCollocation, BlockDim, BlockLayout, BlockState, Context, CudaError, Decomposition,  # noqa: F401
+                  EpochStats, Field, InterfaceJump, InvalidArgument, KnotVector, LocalProblem, LogicError, MfaModel,
+                  MfaddError, OutOfRange, PhaseTimings, RuntimeFault, SharedDofMap, SingularFitError, SolveResult,
+                  Solver, SolverConfig, collocation_matrix, compression_ratio, decode, default_context, delta_width,
+                  exchange_volume, find_span, fit_unconstrained, make_knot_vector, partition, solve)
+
+__all__ = [n for n in dir() if not n.startswith("_")]

@@ -1,0 +1,671 @@
+"""Python host mirror of the reference `mfadd` API for the hot path.
+
+Names, argument meaning and error behaviour follow the reference headers
+(/root/reference/proj/core/include/mfadd/{knots,collocation,lsq,decode,layout,
+solver}.hpp).  Every numerical result comes from the sm_100a kernels behind
+the C ABI (include/mfadd_b200.h); this module only marshals arguments.
+
+Exception mapping (status code -> class, mirroring the reference):
+  invalid_argument -> InvalidArgument (a ValueError)
+  out_of_range     -> OutOfRange (an IndexError)
+  SingularFitError -> SingularFitError(dim, span)
+  runtime_error    -> RuntimeFault;  logic_error -> LogicError
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib as L
+
+# ------------------------------------------------------------------ errors
+
+
+class MfaddError(Exception):
+    code = -1
+
+
+class InvalidArgument(MfaddError, ValueError):
+    code = L.MFADD_EINVAL
+
+
+class OutOfRange(MfaddError, IndexError):
+    code = L.MFADD_ERANGE
+
+
+class SingularFitError(MfaddError, RuntimeError):
+    """lsq.hpp:24-28: a per-dimension normal matrix is not SPD."""
+    code = L.MFADD_ESINGULAR
+
+    def __init__(self, msg, dim=-1, span=-1):
+        super().__init__(msg)
+        self.dim, self.span = dim, span
+
+
+class RuntimeFault(MfaddError, RuntimeError):
+    code = L.MFADD_ERUNTIME
+
+
+class LogicError(MfaddError):
+    code = L.MFADD_ELOGIC
+
+
+class CudaError(MfaddError, RuntimeError):
+    code = L.MFADD_ECUDA
+
+
+_BY_CODE = {c.code: c for c in (InvalidArgument, OutOfRange, RuntimeFault, LogicError, CudaError)}
+
+
+def _check(rc):
+    if rc == 0:
+        return
+    lib = L.load()
+    msg = (lib.mfadd_last_error() or b"").decode(errors="replace")
+    if rc == L.MFADD_ESINGULAR:
+        raise SingularFitError(msg, lib.mfadd_last_error_dim(), lib.mfadd_last_error_span())
+    raise _BY_CODE.get(rc, MfaddError)(msg)
+
+
+def _dp(a):
+    return a.ctypes.data_as(L.c_dp)
+
+
+def _lp(a):
+    return a.ctypes.data_as(L.c_lp)
+
+
+def _ip(a):
+    return a.ctypes.data_as(L.c_ip)
+
+
+# ------------------------------------------------------------------ knots
+
+
+@dataclass
+class KnotVector:
+    """knots.hpp:11-30."""
+    degree: int
+    knots: np.ndarray
+    clamp_left: bool = True
+    clamp_right: bool = True
+
+    def basis_count(self) -> int:
+        return len(self.knots) - self.degree - 1
+
+    def domain_min(self) -> float:
+        return float(self.knots[self.degree])
+
+    def domain_max(self) -> float:
+        return float(self.knots[self.basis_count()])
+
+    def span_count(self) -> int:
+        n = self.basis_count()
+        return int(sum(1 for s in range(self.degree, n) if self.knots[s] < self.knots[s + 1]))
+
+    def greville(self, i: int) -> float:
+        return float(sum(self.knots[i + j] for j in range(1, self.degree + 1)) / self.degree)
+
+
+def make_knot_vector(degree, basis_count, a=0.0, b=1.0, clamp_left=True, clamp_right=True) -> KnotVector:
+    """knots.cpp:48-81 (host metadata, same floating-point expressions)."""
+    if degree < 1:
+        raise InvalidArgument("make_knot_vector: degree must be >= 1")
+    if basis_count < degree + 1:
+        raise InvalidArgument(f"make_knot_vector: basis count must be at least p+1 (got {basis_count} for p={degree})")
+    if not a < b:
+        raise InvalidArgument("make_knot_vector: range must satisfy a < b")
+    p, spans = degree, basis_count - degree
+    h = (b - a) / spans
+    kn = [a] * (p + 1) if clamp_left else [a - i * h for i in range(p, 0, -1)] + [a]
+    kn += [a + k * h for k in range(1, spans)]
+    kn += [b] * (p + 1) if clamp_right else [b] + [b + i * h for i in range(1, p + 1)]
+    return KnotVector(degree, np.array(kn, np.float64), clamp_left, clamp_right)
+
+
+# ------------------------------------------------------------------ device context
+
+_default_ctx = None
+
+
+class Context:
+    """One CUDA device + stream (mfadd_context)."""
+
+    def __init__(self, device: int = 0, stream: Optional[int] = None):
+        lib = L.load()
+        h = C.c_void_p()
+        _check(lib.mfadd_context_create(device, C.c_void_p(stream) if stream else None, C.byref(h)))
+        self._h = h
+        self.device = device
+
+    def launch_count(self) -> int:
+        return L.load().mfadd_context_launch_count(self._h)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            L.load().mfadd_context_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+# ------------------------------------------------------------------ collocation
+
+
+@dataclass
+class BandedCollocation:
+    """collocation.hpp:15-49 (host copy of the rows the GPU computed)."""
+    rows: int
+    cols: int
+    band: int
+    first_col: np.ndarray
+    count: np.ndarray
+    values: np.ndarray  # rows x band, clipped values left-aligned
+
+    def row_sum(self, j):
+        return float(self.values[j, : self.count[j]].sum())
+
+    def dense(self):
+        m = np.zeros((self.rows, self.cols))
+        for j in range(self.rows):
+            c0 = self.first_col[j]
+            m[j, c0:c0 + self.count[j]] = self.values[j, : self.count[j]]
+        return m
+
+
+def collocation_matrix(kv: KnotVector, params, col_lo: int = 0, col_hi: Optional[int] = None,
+                       ctx: Optional[Context] = None) -> BandedCollocation:
+    """collocation_matrix(kv, params[, col_lo, col_hi]), collocation.hpp:53-58, on the GPU (K1)."""
+    ctx = ctx or default_context()
+    kn = np.ascontiguousarray(kv.knots, np.float64)
+    pm = np.ascontiguousarray(params, np.float64)
+    if col_hi is None:
+        col_hi = kv.basis_count()
+    m = len(pm)
+    fc = np.zeros(m, np.int64)
+    cnt = np.zeros(m, np.int32)
+    vals = np.zeros((m, kv.degree + 1), np.float64)
+    if m == 0:
+        raise InvalidArgument("collocation_matrix: empty parameter list")
+    _check(L.load().mfadd_collocation(ctx._h, _dp(kn), len(kn), kv.degree, _dp(pm), m, col_lo, col_hi, _lp(fc),
+                                      _ip(cnt), _dp(vals)))
+    return BandedCollocation(m, col_hi - col_lo, kv.degree + 1, fc, cnt, vals)
+
+
+def find_span(kv: KnotVector, u: float, ctx: Optional[Context] = None) -> int:
+    """find_span (knots.hpp:36) via a one-row collocation on the GPU."""
+    bc = collocation_matrix(kv, [u], 0, kv.basis_count(), ctx)
+    return int(bc.first_col[0]) + kv.degree if bc.count[0] == kv.degree + 1 else \
+        int(bc.first_col[0]) + int(bc.count[0]) - 1
+
+
+# ------------------------------------------------------------------ lsq / decode
+
+
+def _pack(kvs: Sequence[KnotVector], params):
+    kn = np.concatenate([np.asarray(k.knots, np.float64) for k in kvs])
+    ko = np.cumsum([0] + [len(k.knots) for k in kvs]).astype(np.int64)
+    pm = np.concatenate([np.asarray(p, np.float64) for p in params])
+    po = np.cumsum([0] + [len(p) for p in params]).astype(np.int64)
+    return kn, ko, pm, po
+
+
+@dataclass
+class LocalProblem:
+    """lsq.hpp:16-22, described by its ingredients (knot vectors, params,
+    column windows) rather than host-built collocation matrices: the GPU
+    builds the rows itself."""
+    kvs: List[KnotVector]
+    params: List[np.ndarray]
+    windows: List[tuple]
+    q: np.ndarray
+
+
+def fit_unconstrained(problem: LocalProblem, ctx: Optional[Context] = None) -> np.ndarray:
+    """fit_unconstrained (lsq.hpp:33), K1+K2+K3 on the GPU."""
+    ctx = ctx or default_context()
+    degree = problem.kvs[0].degree
+    kn, ko, pm, po = _pack(problem.kvs, problem.params)
+    lo = np.array([w[0] for w in problem.windows], np.int64)
+    hi = np.array([w[1] for w in problem.windows], np.int64)
+    q = np.ascontiguousarray(problem.q, np.float64)
+    if q.shape != tuple(len(p) for p in problem.params):
+        raise InvalidArgument("LocalProblem: row count mismatch")
+    out = np.zeros(tuple(int(h - l) for l, h in zip(lo, hi)), np.float64)
+    _check(L.load().mfadd_fit_unconstrained(ctx._h, len(problem.kvs), degree, _dp(kn), _lp(ko), _dp(pm), _lp(po),
+                                            _lp(lo), _lp(hi), _dp(q), _dp(out)))
+    return out
+
+
+def decode(controls, kvs: Sequence[KnotVector], params, col_offset=None, ctx: Optional[Context] = None):
+    """decode (decode.hpp:20-22), K1 + K7 on the GPU."""
+    ctx = ctx or default_context()
+    c = np.ascontiguousarray(controls, np.float64)
+    if c.ndim != len(kvs) or len(kvs) != len(params):
+        raise InvalidArgument("decode: dimension mismatch between lattice, knot vectors and parameters")
+    kn, ko, pm, po = _pack(kvs, params)
+    ext = np.array(c.shape, np.int64)
+    off = None if col_offset is None or len(col_offset) == 0 else np.array(col_offset, np.int64)
+    out = np.zeros(tuple(len(p) for p in params), np.float64)
+    _check(L.load().mfadd_decode(ctx._h, len(kvs), kvs[0].degree, _dp(kn), _lp(ko), _dp(pm), _lp(po), _lp(ext),
+                                 None if off is None else _lp(off), _dp(c), _dp(out)))
+    return out
+
+
+# ------------------------------------------------------------------ layout
+
+BLOCKDIM_FIELDS = ("span_lo", "span_hi", "delta_lo", "delta_hi", "overlap_lo", "overlap_hi", "local_span_lo",
+                   "local_span_hi", "dof_lo", "dof_hi", "own_lo", "own_hi", "input_lo", "input_hi",
+                   "own_input_lo", "own_input_hi")
+
+
+@dataclass
+class BlockDim:
+    """layout.hpp:47-57."""
+    span_lo: int
+    span_hi: int
+    delta_lo: int
+    delta_hi: int
+    overlap_lo: int
+    overlap_hi: int
+    local_span_lo: int
+    local_span_hi: int
+    dof_lo: int
+    dof_hi: int
+    own_lo: int
+    own_hi: int
+    input_lo: int
+    input_hi: int
+    own_input_lo: int
+    own_input_hi: int
+
+
+@dataclass
+class BlockLayout:
+    """layout.hpp:59-66."""
+    id: int
+    coords: List[int]
+    dims: List[BlockDim]
+    neighbors: List[int]
+
+    def holds(self, dof):
+        return all(d.dof_lo <= i < d.dof_hi for d, i in zip(self.dims, dof))
+
+    def owns(self, dof):
+        return all(d.own_lo <= i < d.own_hi for d, i in zip(self.dims, dof))
+
+
+def delta_width(degree: int) -> int:
+    """layout.cpp:11-14."""
+    if degree < 1:
+        raise InvalidArgument("delta_width: degree must be >= 1")
+    return degree // 2
+
+
+class SharedDofMap:
+    """layout.hpp:70-92 (host view of the partition's holder ranges)."""
+
+    def __init__(self, dec: "Decomposition"):
+        self._dec = dec
+        self._hr = [dec._holder_ranges(k) for k in range(dec.rank)]
+
+    def holder_span(self, dim, i):
+        r = self._hr[dim][i]
+        return int(r[0]), int(r[1])
+
+    def n_s(self, dof):
+        c = 1
+        for k, i in enumerate(dof):
+            r = self._hr[k][i]
+            c *= int(r[1] - r[0] + 1)
+        return c
+
+    def classify(self, dof):
+        c = self.n_s(dof)
+        return "interior" if c <= 1 else ("singly_shared" if c == 2 else "multi_shared")
+
+    def weight(self, dof):
+        return 1.0 / self.n_s(dof)
+
+    def holders(self, dof):
+        import itertools
+        ranges = [range(int(self._hr[k][i][0]), int(self._hr[k][i][1]) + 1) for k, i in enumerate(dof)]
+        ids = []
+        for c in itertools.product(*ranges):
+            bid = 0
+            for k, ck in enumerate(c):
+                bid = bid * self._dec.blocks_per_dim[k] + ck
+            ids.append(bid)
+        return sorted(ids)
+
+    def any_shared(self):
+        return bool(L.load().mfadd_dec_any_shared(self._dec._h))
+
+    def for_each_shared(self, fn):
+        import itertools
+        for dof in itertools.product(*[range(int(n)) for n in self._dec.n_ctrl]):
+            c = self.n_s(dof)
+            if c > 1:
+                fn(dof, c)
+
+
+class Decomposition:
+    """layout.hpp:94-104 (`partition()` result), held by the C ABI."""
+
+    def __init__(self, handle, grid_dims, bounds, blocks_per_dim, degree, overlap, clamp):
+        self._h = handle
+        lib = L.load()
+        self.rank = lib.mfadd_dec_rank(handle)
+        self.nblocks = lib.mfadd_dec_block_count(handle)
+        self.grid_dims = tuple(int(x) for x in grid_dims)
+        self.bounds = [tuple(b) for b in bounds]
+        self.blocks_per_dim = [int(b) for b in blocks_per_dim]
+        self.degree = degree
+        self.overlap = 0 if clamp else int(overlap)
+        self.clamp_interfaces = bool(clamp)
+        nc = np.zeros(self.rank, np.int64)
+        lib.mfadd_dec_nctrl(handle, _lp(nc))
+        self.n_ctrl = [int(x) for x in nc]
+        self.kvs = []
+        for k in range(self.rank):
+            n = lib.mfadd_dec_knots(handle, k, None)
+            kn = np.zeros(n, np.float64)
+            lib.mfadd_dec_knots(handle, k, _dp(kn))
+            self.kvs.append(KnotVector(degree, kn, True, True))
+        bd = self.block_dims_array()
+        co = np.zeros((self.nblocks, self.rank), np.int32)
+        lib.mfadd_dec_coords(handle, _ip(co))
+        buf = np.zeros(64, np.int32)
+        self.blocks = []
+        for b in range(self.nblocks):
+            nn = lib.mfadd_dec_neighbors(handle, b, _ip(buf), 64)
+            self.blocks.append(BlockLayout(b, co[b].tolist(), [BlockDim(*map(int, bd[b, k])) for k in range(self.rank)],
+                                           buf[:nn].tolist()))
+        self.shared = SharedDofMap(self)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            try:
+                L.load().mfadd_decomposition_free(self._h)
+            except Exception:
+                pass
+            self._h = None
+
+    def block_dims_array(self):
+        out = np.zeros((self.nblocks, self.rank, 16), np.int64)
+        L.load().mfadd_dec_block_dims(self._h, _lp(out))
+        return out
+
+    def _holder_ranges(self, dim):
+        out = np.zeros((self.n_ctrl[dim], 2), np.int32)
+        L.load().mfadd_dec_holder_ranges(self._h, dim, _ip(out))
+        return out
+
+    def shared_dof_box(self, a, b):
+        box = []
+        for da, db in zip(self.blocks[a].dims, self.blocks[b].dims):
+            lo, hi = max(da.dof_lo, db.dof_lo), min(da.dof_hi, db.dof_hi)
+            if lo >= hi:
+                return []
+            box.append((lo, hi))
+        return box
+
+    def exchange_volume(self):
+        out = np.zeros(self.nblocks, np.int64)
+        L.load().mfadd_dec_exchange_volume(self._h, _lp(out))
+        return out
+
+    def compression_ratio(self):
+        return L.load().mfadd_dec_compression_ratio(self._h)
+
+    def span_count(self, dim):
+        return self.kvs[dim].span_count()
+
+    def total_inputs(self):
+        return int(np.prod(self.grid_dims))
+
+
+def partition(grid_dims, bounds, blocks_per_dim, degree, nctrl_per_block, overlap, clamp_interfaces=False):
+    """partition (layout.hpp:107-111)."""
+    rank = len(grid_dims)
+    if not (len(bounds) == len(blocks_per_dim) == len(nctrl_per_block) == rank):
+        raise InvalidArgument("partition: per-dimension argument counts disagree")
+    g = np.array(grid_dims, np.int64)
+    bd = np.array(bounds, np.float64).reshape(-1)
+    bp = np.array(blocks_per_dim, np.int32)
+    nc = np.array(nctrl_per_block, np.int64)
+    h = C.c_void_p()
+    _check(L.load().mfadd_partition(rank, _lp(g), _dp(bd), _ip(bp), degree, _lp(nc), overlap, int(clamp_interfaces),
+                                    C.byref(h)))
+    return Decomposition(h, grid_dims, bounds, blocks_per_dim, degree, overlap, clamp_interfaces)
+
+
+def compression_ratio(dec: Decomposition) -> float:
+    return dec.compression_ratio()
+
+
+def exchange_volume(dec: Decomposition):
+    return dec.exchange_volume()
+
+
+# ------------------------------------------------------------------ solver
+
+
+@dataclass
+class Field:
+    """field.hpp:17-29: row-major samples, last dim fastest, u_j = j/(m-1)."""
+    dims: List[int]
+    bounds: List[tuple]
+    values: np.ndarray
+    name: str = ""
+
+    def rank(self):
+        return len(self.dims)
+
+    def coordinate(self, dim, j):
+        a, b = self.bounds[dim]
+        m = self.dims[dim]
+        return a if m == 1 else a + (b - a) * float(j) / float(m - 1)
+
+    def parameter_grid(self, dim):
+        m = self.dims[dim]
+        return np.array([0.0 if m == 1 else float(j) / float(m - 1) for j in range(m)])
+
+    def validate(self):
+        if not self.dims or len(self.dims) != len(self.bounds):
+            raise InvalidArgument("Field: dims/bounds mismatch")
+        for d, (a, b) in zip(self.dims, self.bounds):
+            if d < 2:
+                raise InvalidArgument("Field: need at least 2 points per dimension")
+            if not a < b:
+                raise InvalidArgument("Field: bounds min must be < max")
+        if int(np.prod(self.dims)) != int(np.asarray(self.values).size):
+            raise InvalidArgument("Field: value count does not match extents")
+
+
+@dataclass
+class SolverConfig:
+    """solver.hpp:16-22 (+ store_error: materialise global_error)."""
+    max_outer_iterations: int = 10
+    tolerance: float = 1e-10
+    workers: int = 1
+    log_errors: bool = True
+    enforce_continuity: bool = True
+    store_error: bool = True
+
+    def to_c(self):
+        return L.SolverConfigC(self.max_outer_iterations, self.tolerance, self.workers, int(self.log_errors),
+                               int(self.enforce_continuity), int(self.store_error))
+
+
+@dataclass
+class InterfaceJump:
+    block_a: int
+    block_b: int
+    linf_ss: float
+    linf_ms: float
+
+
+@dataclass
+class EpochStats:
+    iteration: int
+    dp_max: float
+    jump_ss: float
+    jump_ms: float
+    block_errors: list = field(default_factory=list)
+
+
+@dataclass
+class PhaseTimings:
+    setup: float = 0.0
+    local_solve: float = 0.0
+    exchange: float = 0.0
+    constraint: float = 0.0
+    decode: float = 0.0
+
+
+@dataclass
+class MfaModel:
+    degrees: List[int]
+    kvs: List[KnotVector]
+    controls: np.ndarray
+    bounds: List[tuple]
+
+
+@dataclass
+class BlockState:
+    id: int
+    col_offset: List[int]
+    p: np.ndarray
+
+
+@dataclass
+class SolveResult:
+    model: MfaModel
+    converged: bool
+    constraint_iterations: int
+    final_dp: float
+    epochs: List[EpochStats]
+    final_jumps: List[InterfaceJump]
+    timings: PhaseTimings
+    blocks: List[BlockState]
+    global_l2: float
+    global_linf: float
+    global_error: Optional[np.ndarray]
+
+
+class Solver:
+    """A solve() plan: the decomposition's device tables + work buffers."""
+
+    def __init__(self, dec: Decomposition, config: SolverConfig = None, ctx: Optional[Context] = None):
+        self.ctx = ctx or default_context()
+        self.dec = dec
+        self.config = config or SolverConfig()
+        self._cfg = self.config.to_c()
+        h = C.c_void_p()
+        _check(L.load().mfadd_solver_create(self.ctx._h, dec._h, C.byref(self._cfg), C.byref(h)))
+        self._h = h
+        self.summary = L.SolveSummaryC()
+
+    def close(self):
+        if getattr(self, "_h", None):
+            L.load().mfadd_solver_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # field: numpy array (host) or an object with data_ptr() on the device
+    def run(self, values, on_device: bool = False):
+        lib = L.load()
+        if on_device:
+            _check(lib.mfadd_solve(self._h, C.c_void_p(values.data_ptr()), 1, C.byref(self.summary)))
+        else:
+            v = np.ascontiguousarray(values, np.float64)
+            if v.size != self.dec.total_inputs():
+                raise InvalidArgument("solve: field extents disagree with the decomposition")
+            _check(lib.mfadd_solve(self._h, v.ctypes.data_as(C.c_void_p), 0, C.byref(self.summary)))
+        return self.summary
+
+    def run_host(self, values, out_controls, out_error=None):
+        """mfadd_solve_host: H2D + solve + D2H in one call (the e2e path)."""
+        _check(L.load().mfadd_solve_host(
+            self._h, C.c_void_p(values.ctypes.data if isinstance(values, np.ndarray) else values.data_ptr()),
+            C.c_void_p(out_controls.ctypes.data if isinstance(out_controls, np.ndarray) else out_controls.data_ptr()),
+            None if out_error is None else C.c_void_p(out_error.ctypes.data if isinstance(out_error, np.ndarray)
+                                                      else out_error.data_ptr()),
+            C.byref(self.summary)))
+        return self.summary
+
+    def last_launches(self) -> int:
+        return L.load().mfadd_solver_last_launches(self._h)
+
+    def device_controls_ptr(self) -> int:
+        return L.load().mfadd_solver_device_controls(self._h)
+
+    def result(self, want_blocks: bool = True, want_error: bool = True) -> SolveResult:
+        lib = L.load()
+        s = self.summary
+        ep = (L.EpochStatsC * max(1, s.n_epochs))()
+        n = lib.mfadd_solver_epochs(self._h, ep, len(ep))
+        epochs = [EpochStats(e.iteration, e.dp_max, e.jump_ss, e.jump_ms) for e in ep[:n]]
+        if self.config.log_errors:
+            buf = np.zeros((self.dec.nblocks, 2))
+            for i, e in enumerate(epochs):
+                _check(lib.mfadd_solver_block_errors(self._h, i, _dp(buf)))
+                e.block_errors = [tuple(r) for r in buf]
+        fj = np.zeros((max(1, s.n_final_jumps), 4))
+        nj = lib.mfadd_solver_final_jumps(self._h, _dp(fj), len(fj))
+        jumps = [InterfaceJump(int(r[0]), int(r[1]), float(r[2]), float(r[3])) for r in fj[:nj]]
+        ctrl = np.zeros(tuple(self.dec.n_ctrl), np.float64)
+        _check(lib.mfadd_solver_controls(self._h, ctrl.ctypes.data_as(C.c_void_p), 0))
+        err = None
+        if want_error and self.config.store_error:
+            err = np.zeros(self.dec.grid_dims, np.float64)
+            _check(lib.mfadd_solver_global_error(self._h, err.ctypes.data_as(C.c_void_p), 0))
+        blocks = []
+        if want_blocks:
+            for b in self.dec.blocks:
+                shape = tuple(d.dof_hi - d.dof_lo for d in b.dims)
+                pb = np.zeros(shape, np.float64)
+                _check(lib.mfadd_solver_block_controls(self._h, b.id, pb.ctypes.data_as(C.c_void_p), 0))
+                blocks.append(BlockState(b.id, [d.dof_lo for d in b.dims], pb))
+        model = MfaModel([self.dec.degree] * self.dec.rank, self.dec.kvs, ctrl, self.dec.bounds)
+        t = PhaseTimings(s.t_setup, s.t_local_solve, s.t_exchange, s.t_constraint, s.t_decode)
+        return SolveResult(model, bool(s.converged), s.constraint_iterations, s.final_dp, epochs, jumps, t, blocks,
+                           s.global_l2, s.global_linf, err)
+
+
+def solve(field_: Field, dec: Decomposition, config: SolverConfig = None, ctx: Optional[Context] = None) -> SolveResult:
+    """solve (solver.hpp:76) on the GPU."""
+    config = config or SolverConfig()
+    if config.max_outer_iterations < 1:
+        raise InvalidArgument("SolverConfig: max iterations must be >= 1")
+    if not config.tolerance > 0.0:
+        raise InvalidArgument("SolverConfig: tolerance must be > 0")
+    field_.validate()
+    if list(field_.dims) != list(dec.grid_dims):
+        raise InvalidArgument("solve: field extents disagree with the decomposition")
+    s = Solver(dec, config, ctx)
+    try:
+        s.run(np.ascontiguousarray(field_.values, np.float64).reshape(-1))
+        return s.result()
+    finally:
+        s.close()

@@ -1,0 +1,57 @@
+// Device-side data layout shared by the engine (engine.cu) and the kernels
+// (kernels.cu) of the B200 MFA encode path.  See DESIGN.md §3 for the HBM
+// layout rationale.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace mfb {
+
+constexpr int kMaxDegree = 9;  // templated kernels are instantiated for p = 1..kMaxDegree
+
+// One per-dimension collocation problem: a (dim, block-coordinate) pair of the
+// decomposition (all blocks with that coordinate share the rows, solver.cpp:
+// 59-66,83-88), one dimension of a stand-alone LocalProblem, or the global
+// decode rows of one dimension (window = all controls).
+struct AxisProb {
+  int dim;
+  int m;              // rows (input samples along the dim)
+  int n;              // columns (controls in the window)
+  int pad_;
+  std::int64_t col_lo;  // global index of local column 0 (BlockDim::dof_lo)
+  std::int64_t in_lo;   // global input index of row 0
+  std::int64_t M;       // global input count: u_j = (in_lo+j)/(M-1); M<0 -> explicit params
+  std::int64_t param_off;  // offset into the explicit parameter array
+  std::int64_t row_off;    // first row in the rows tables
+  std::int64_t col_off;    // first column in the Cholesky tables
+  std::int64_t knot_off;   // first knot of this dim's knot vector
+  int nknots;
+  int pad2_;
+};
+
+// One block of the decomposition as the fit kernels see it.
+struct BlockDev {
+  int ax[3];           // AxisProb id per dim
+  int pad_;
+  std::int64_t fbase;  // field offset of the input box origin (input_lo per dim)
+  std::int64_t poff;   // offset of the held lattice P_b
+  std::int64_t t1off;  // axis-0 intermediate   [n0][m1][m2]
+  std::int64_t t2off;  // axis-1 intermediate   [n0][n1][m2]
+};
+
+// Status word written by kernels when the reference would throw.
+struct DevStatus {
+  int code;       // 0 ok, 1 invalid_argument (no active basis), 2 out_of_range, 3 singular
+  int axis_prob;  // AxisProb id of the first failure
+  int row;        // failing row / column
+  int pad_;
+};
+
+// Per-epoch reduction slots (u64 bit patterns of non-negative doubles so that
+// atomicMax orders them like the values).
+struct EpochAcc {
+  unsigned long long jump_ss, jump_ms;
+};
+
+}  // namespace mfb

@@ -1,0 +1,1197 @@
+// engine.cu — C ABI (include/mfadd_b200.h) of the B200-native MFA encode
+// path: plan construction (device tables from the host decomposition) and
+// the solve() orchestration (solver.cpp:332-440) over the sm_100a kernels in
+// kernels.cu.  No CPU fallback: every value of SolveResult is produced on the
+// GPU; the host only builds integer metadata tables at plan time and reads
+// back scalars.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/mfadd_b200.h"
+#include "dev.cuh"
+#include "kernels.cuh"
+#include "layout.hpp"
+
+using mfb::AxisProb;
+using mfb::BlockDev;
+using mfb::Decomp;
+
+#define MFB_API extern "C" __attribute__((visibility("default")))
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_err_dim = -1;
+thread_local std::int64_t g_err_span = -1;
+
+struct ApiError : std::runtime_error {
+  int code;
+  ApiError(int c, const std::string& w) : std::runtime_error(w), code(c) {}
+};
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw ApiError(MFADD_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CK(x) cuda_check((x), #x)
+
+template <class Fn>
+int guarded(Fn&& fn) {
+  try {
+    fn();
+    return MFADD_OK;
+  } catch (const ApiError& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const mfb::SingularFit& e) {
+    g_err = e.what();
+    g_err_dim = e.dim;
+    g_err_span = e.span;
+    return MFADD_ESINGULAR;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return MFADD_EINVAL;
+  } catch (const std::out_of_range& e) {
+    g_err = e.what();
+    return MFADD_ERANGE;
+  } catch (const std::logic_error& e) {
+    g_err = e.what();
+    return MFADD_ELOGIC;
+  } catch (const std::bad_alloc& e) {
+    g_err = "host allocation failed";
+    return MFADD_ENOMEM;
+  } catch (const std::runtime_error& e) {
+    g_err = e.what();
+    return MFADD_ERUNTIME;
+  } catch (...) {
+    g_err = "unknown error";
+    return MFADD_ERUNTIME;
+  }
+}
+
+// Owning device buffer.
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  std::size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() {
+    if (p) cudaFree(p);
+  }
+  void alloc(std::size_t count) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = count;
+    if (count == 0) return;
+    const cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    if (e != cudaSuccess) {
+      p = nullptr;
+      throw ApiError(MFADD_ENOMEM, "cudaMalloc(" + std::to_string(count * sizeof(T)) + " bytes) failed: " +
+                                       cudaGetErrorString(e));
+    }
+  }
+  void upload(const std::vector<T>& h, cudaStream_t s) {
+    alloc(h.size());
+    if (!h.empty()) CK(cudaMemcpyAsync(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+};
+
+// Host binary search with the find_span rule (knots.cpp:83-106) — used only
+// to size the decode kernel's shared-memory control box at plan time.
+int host_find_span(const std::vector<double>& kn, int p, double u) {
+  const int n = static_cast<int>(kn.size()) - p - 1;
+  if (u >= kn[static_cast<std::size_t>(n)]) {
+    int s = n - 1;
+    while (s > p && kn[static_cast<std::size_t>(s)] == kn[static_cast<std::size_t>(s) + 1]) --s;
+    return s;
+  }
+  if (u <= kn[static_cast<std::size_t>(p)]) return p;
+  int low = p, high = n, mid = (low + high) / 2;
+  while (u < kn[static_cast<std::size_t>(mid)] || u >= kn[static_cast<std::size_t>(mid) + 1]) {
+    if (u < kn[static_cast<std::size_t>(mid)])
+      high = mid;
+    else
+      low = mid;
+    mid = (low + high) / 2;
+  }
+  return mid;
+}
+
+}  // namespace
+
+// ===================================================================== types
+struct mfadd_decomposition {
+  Decomp d;
+};
+
+struct mfadd_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::int64_t launches = 0;
+  mfb::DevStatus* d_status = nullptr;
+  double* h_pinned = nullptr;  // 16 doubles of pinned host scratch
+};
+
+namespace {
+
+struct ContextScope {  // make the context's device current for the call
+  int prev = -1;
+  explicit ContextScope(const mfadd_context* c) {
+    cudaGetDevice(&prev);
+    if (prev != c->device) CK(cudaSetDevice(c->device));
+  }
+  ~ContextScope() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// Device tables for a batch of local problems sharing one degree: the fit
+// machinery of both solve() and fit_unconstrained().
+struct Workload {
+  int D = 0, p = 0;
+  std::vector<AxisProb> probs;
+  std::vector<BlockDev> blocks;
+  std::vector<int> factor_ids;
+  std::int64_t total_rows = 0, total_cols = 0, total_p = 0, total_t1 = 0, total_t2 = 0;
+  std::int64_t fs[3] = {0, 0, 0};
+  int max_m = 0, max_n_factor = 0;
+  int max_lines_strided[3] = {0, 0, 0};
+  int max_lines_last = 0;
+
+  DBuf<double> knots, params;
+  DBuf<AxisProb> d_probs;
+  DBuf<BlockDev> d_blocks;
+  DBuf<int> d_factor, g0, first_col, count;
+  DBuf<double> vals, ltab, t1, t2, P, Y;
+  DBuf<unsigned long long> linf_int;
+  DBuf<unsigned char> sflag;
+  std::int64_t sflag_off[3] = {0, 0, 0};
+
+  // Derive offsets/sizes from probs + blocks (row/col offsets, intermediates).
+  void layout_tables() {
+    total_rows = 0;
+    total_cols = 0;
+    max_m = 0;
+    for (auto& pr : probs) {
+      pr.row_off = total_rows;
+      total_rows += pr.m;
+      max_m = std::max(max_m, pr.m);
+    }
+    std::vector<char> is_factor(probs.size(), 0);
+    for (int id : factor_ids) is_factor[static_cast<std::size_t>(id)] = 1;
+    max_n_factor = 0;
+    for (std::size_t i = 0; i < probs.size(); ++i) {
+      probs[i].col_off = total_cols;
+      if (is_factor[i]) {
+        total_cols += probs[i].n;
+        max_n_factor = std::max(max_n_factor, probs[i].n);
+      }
+    }
+    total_p = total_t1 = total_t2 = 0;
+    for (auto& mx : max_lines_strided) mx = 0;
+    max_lines_last = 0;
+    for (auto& b : blocks) {
+      std::int64_t np = 1;
+      std::array<std::int64_t, 3> m{1, 1, 1}, n{1, 1, 1};
+      for (int k = 0; k < D; ++k) {
+        m[k] = probs[static_cast<std::size_t>(b.ax[k])].m;
+        n[k] = probs[static_cast<std::size_t>(b.ax[k])].n;
+        np *= n[k];
+      }
+      b.poff = total_p;
+      total_p += np;
+      b.t1off = total_t1;
+      b.t2off = total_t2;
+      if (D >= 2) total_t1 += n[0] * m[1] * (D == 3 ? m[2] : 1);
+      if (D == 3) total_t2 += n[0] * n[1] * m[2];
+      for (int d = 0; d + 1 < D; ++d) {
+        std::int64_t L = 1, Tr = 1;
+        for (int k = 0; k < D; ++k) {
+          if (k < d) L *= n[k];
+          if (k > d) Tr *= m[k];
+        }
+        max_lines_strided[d] = static_cast<int>(std::max<std::int64_t>(max_lines_strided[d], L * Tr));
+      }
+      std::int64_t Ll = 1;
+      for (int k = 0; k + 1 < D; ++k) Ll *= n[k];
+      max_lines_last = static_cast<int>(std::max<std::int64_t>(max_lines_last, Ll));
+    }
+  }
+
+  void allocate(cudaStream_t s) {
+    d_probs.upload(probs, s);
+    d_blocks.upload(blocks, s);
+    d_factor.upload(factor_ids, s);
+    g0.alloc(static_cast<std::size_t>(total_rows));
+    first_col.alloc(static_cast<std::size_t>(total_rows));
+    count.alloc(static_cast<std::size_t>(total_rows));
+    vals.alloc(static_cast<std::size_t>(total_rows * (p + 1)));
+    ltab.alloc(static_cast<std::size_t>(std::max<std::int64_t>(total_cols, 1) * (2 * p + 1)));
+    t1.alloc(static_cast<std::size_t>(total_t1));
+    t2.alloc(static_cast<std::size_t>(total_t2));
+    P.alloc(static_cast<std::size_t>(total_p));
+    Y.alloc(static_cast<std::size_t>(total_p));
+    linf_int.alloc(blocks.size());
+  }
+
+  // K1 + K2
+  int setup(mfadd_context* ctx) {
+    mfb::RowsArgs ra{d_probs.p, static_cast<int>(probs.size()), max_m, knots.p, params.p, g0.p, first_col.p,
+                     count.p, vals.p, ctx->d_status};
+    int l = mfb::launch_basis_rows(p, ra, ctx->stream);
+    mfb::CholArgs ca{d_probs.p, d_factor.p, static_cast<int>(factor_ids.size()), max_n_factor, g0.p, vals.p, ltab.p,
+                     ctx->d_status};
+    l += mfb::launch_gram_chol(p, ca, ctx->stream);
+    CK(cudaGetLastError());
+    return l;
+  }
+
+  // K3
+  int fit(mfadd_context* ctx, const double* field) {
+    CK(cudaMemsetAsync(linf_int.p, 0, blocks.size() * sizeof(unsigned long long), ctx->stream));
+    mfb::FitArgs fa{};
+    fa.D = D;
+    for (int k = 0; k < 3; ++k) fa.fs[k] = fs[k];
+    fa.field = field;
+    fa.blocks = d_blocks.p;
+    fa.nblocks = static_cast<int>(blocks.size());
+    fa.probs = d_probs.p;
+    fa.g0 = g0.p;
+    fa.vals = vals.p;
+    fa.ltab = ltab.p;
+    fa.t1 = t1.p;
+    fa.t2 = t2.p;
+    fa.P = P.p;
+    fa.Y = Y.p;
+    fa.linf_int = linf_int.p;
+    fa.shared_flag = sflag.p;
+    for (int k = 0; k < 3; ++k) {
+      fa.sflag_off[k] = sflag_off[k];
+      fa.max_lines_strided[k] = max_lines_strided[k];
+    }
+    fa.max_lines_last = max_lines_last;
+    const int l = mfb::launch_fit(p, fa, ctx->stream);
+    CK(cudaGetLastError());
+    return l;
+  }
+
+  // Map a device status word onto the reference's exceptions.
+  void raise_status(const mfb::DevStatus& st, const char* who) {
+    if (st.code == 0) return;
+    const AxisProb& pr = probs[static_cast<std::size_t>(st.axis_prob)];
+    if (st.code == 1)
+      throw std::invalid_argument(std::string(who) + "collocation_matrix: param row " + std::to_string(st.row) +
+                                  " has no active basis inside the column window");
+    if (st.code == 2)
+      throw std::out_of_range(std::string(who) + "find_span: parameter outside evaluable range (row " +
+                              std::to_string(st.row) + ")");
+    // singular: lsq.cpp:25-35 uncovered column from the rows of that problem
+    std::vector<int> fc(static_cast<std::size_t>(pr.m)), cnt(static_cast<std::size_t>(pr.m));
+    std::vector<double> v(static_cast<std::size_t>(pr.m) * (p + 1));
+    std::vector<int> gg(static_cast<std::size_t>(pr.m));
+    CK(cudaMemcpy(fc.data(), first_col.p + pr.row_off, fc.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(cnt.data(), count.p + pr.row_off, cnt.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(gg.data(), g0.p + pr.row_off, gg.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(v.data(), vals.p + pr.row_off * (p + 1), v.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    std::vector<char> cov(static_cast<std::size_t>(pr.n), 0);
+    for (int j = 0; j < pr.m; ++j)
+      for (int k = 0; k < cnt[static_cast<std::size_t>(j)]; ++k) {
+        const int col = fc[static_cast<std::size_t>(j)] + k;
+        if (v[static_cast<std::size_t>(j) * (p + 1) + (col - gg[static_cast<std::size_t>(j)])] != 0.0)
+          cov[static_cast<std::size_t>(col)] = 1;
+      }
+    std::int64_t col = -1;
+    for (int c = 0; c < pr.n; ++c)
+      if (!cov[static_cast<std::size_t>(c)]) {
+        col = c;
+        break;
+      }
+    throw mfb::SingularFit(pr.dim, col,
+                           std::string(who) + "fit_unconstrained: singular normal matrix in dimension " +
+                               std::to_string(pr.dim) +
+                               (col >= 0 ? " (no input data supports local basis " + std::to_string(col) + ")"
+                                         : " (ill-conditioned collocation)"));
+  }
+};
+
+constexpr int kTiles3[3] = {4, 8, 32};
+constexpr int kTiles2[3] = {1, 16, 64};
+constexpr int kTiles1[3] = {1, 1, 1024};
+
+// Decode-over-a-grid plan (K7): padded to 3 dims.
+struct DecodePlan {
+  int D = 0;
+  std::int64_t M[3] = {1, 1, 1}, N[3] = {1, 1, 1}, ntiles[3] = {1, 1, 1};
+  int T[3] = {1, 1, 1}, W[3] = {1, 1, 1}, pk[3] = {0, 0, 0};
+  int prob_of[3] = {-1, -1, -1};  // padded dim -> AxisProb id (or -1 = unit)
+
+  void init(int rank, int p, const std::int64_t* Mi, const std::int64_t* Ni) {
+    D = rank;
+    const int* t = rank == 3 ? kTiles3 : (rank == 2 ? kTiles2 : kTiles1);
+    for (int k = 0; k < 3; ++k) {
+      const int src = k - (3 - rank);
+      M[k] = src >= 0 ? Mi[src] : 1;
+      N[k] = src >= 0 ? Ni[src] : 1;
+      T[k] = t[k];
+      pk[k] = src >= 0 ? p : 0;
+      ntiles[k] = (M[k] + T[k] - 1) / T[k];
+    }
+  }
+  // W[k] = max over tiles of the control window width (exact, host knots).
+  void size_windows(int k, const std::vector<double>& kn, const std::vector<double>& params, int p,
+                    std::int64_t col_lo) {
+    int w = 1;
+    for (std::int64_t t = 0; t < ntiles[k]; ++t) {
+      const std::int64_t a = t * T[k], b = std::min<std::int64_t>(M[k], a + T[k]) - 1;
+      const int s0 = host_find_span(kn, p, params[static_cast<std::size_t>(a)]);
+      const int s1 = host_find_span(kn, p, params[static_cast<std::size_t>(b)]);
+      w = std::max(w, s1 - s0 + p + 1);
+    }
+    (void)col_lo;
+    W[k] = w;
+  }
+};
+
+}  // namespace
+
+struct mfadd_solver {
+  mfadd_context* ctx = nullptr;
+  Decomp dec;
+  mfadd_solver_config cfg{};
+  Workload wl;
+  int axbase[3] = {0, 0, 0};
+  int dec_prob[3] = {-1, -1, -1};
+  DecodePlan dp;
+
+  DBuf<int2> hr;
+  DBuf<int> slist, clist, own_coord, pair_slot, unit_g0;
+  DBuf<double> unit_vals;
+  DBuf<std::int64_t> poff;
+  std::int64_t hr_off[3] = {0, 0, 0}, s_off[3] = {0, 0, 0}, c_off[3] = {0, 0, 0}, oc_off[3] = {0, 0, 0};
+  std::int64_t nS[3] = {0, 0, 0}, nC[3] = {0, 0, 0}, piece[3] = {0, 0, 0}, total_shared = 0;
+  DBuf<unsigned long long> change, linf_sh, pair_jumps;
+  DBuf<mfb::EpochAcc> acc;
+  DBuf<double> epoch_out, lattice, error, partial, red2, field_buf;
+  int npairs = 0;
+  std::vector<std::array<int, 2>> pair_ids;
+
+  // results
+  std::vector<mfadd_epoch_stats> epochs;
+  std::vector<double> final_jumps;
+  mfadd_solve_summary summary{};
+  bool have_result = false;
+  int last_launches = 0;
+  cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+
+  ~mfadd_solver() {
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+};
+
+// ===================================================================== API
+MFB_API int mfadd_abi_version(void) { return MFADD_ABI_VERSION; }
+MFB_API const char* mfadd_last_error(void) { return g_err.c_str(); }
+MFB_API int mfadd_last_error_dim(void) { return g_err_dim; }
+MFB_API int64_t mfadd_last_error_span(void) { return g_err_span; }
+
+// ---------------------------------------------------------------- layout
+MFB_API int mfadd_partition(int rank, const int64_t* grid_dims, const double* bounds, const int* blocks_per_dim,
+                            int degree, const int64_t* nctrl_per_block, int64_t overlap, int clamp_interfaces,
+                            mfadd_decomposition** out) {
+  return guarded([&] {
+    auto h = std::make_unique<mfadd_decomposition>();
+    h->d = mfb::partition(rank, grid_dims, bounds, blocks_per_dim, degree, nctrl_per_block, overlap,
+                          clamp_interfaces != 0);
+    *out = h.release();
+  });
+}
+MFB_API void mfadd_decomposition_free(mfadd_decomposition* dec) { delete dec; }
+MFB_API int mfadd_dec_rank(const mfadd_decomposition* dec) { return dec->d.rank; }
+MFB_API int mfadd_dec_block_count(const mfadd_decomposition* dec) { return dec->d.nblocks; }
+MFB_API void mfadd_dec_block_dims(const mfadd_decomposition* dec, int64_t* out) {
+  std::memcpy(out, dec->d.bd.data(), dec->d.bd.size() * sizeof(int64_t));
+}
+MFB_API void mfadd_dec_coords(const mfadd_decomposition* dec, int* out) {
+  for (int b = 0; b < dec->d.nblocks; ++b)
+    for (int k = 0; k < dec->d.rank; ++k) out[b * dec->d.rank + k] = dec->d.coords[static_cast<std::size_t>(b)][k];
+}
+MFB_API void mfadd_dec_nctrl(const mfadd_decomposition* dec, int64_t* out) {
+  for (int k = 0; k < dec->d.rank; ++k) out[k] = dec->d.n_ctrl[k];
+}
+MFB_API int mfadd_dec_knots(const mfadd_decomposition* dec, int dim, double* out) {
+  const auto& kn = dec->d.knots[dim];
+  if (out) std::memcpy(out, kn.data(), kn.size() * sizeof(double));
+  return static_cast<int>(kn.size());
+}
+MFB_API int mfadd_dec_neighbors(const mfadd_decomposition* dec, int block, int* out, int cap) {
+  const auto& nb = dec->d.neighbors[static_cast<std::size_t>(block)];
+  for (std::size_t i = 0; i < nb.size() && static_cast<int>(i) < cap; ++i) out[i] = nb[i];
+  return static_cast<int>(nb.size());
+}
+MFB_API void mfadd_dec_holder_ranges(const mfadd_decomposition* dec, int dim, int* out) {
+  const auto& h = dec->d.holder[dim];
+  for (std::size_t i = 0; i < h.size(); ++i) {
+    out[2 * i] = h[i][0];
+    out[2 * i + 1] = h[i][1];
+  }
+}
+MFB_API void mfadd_dec_exchange_volume(const mfadd_decomposition* dec, int64_t* out) {
+  const auto v = mfb::exchange_volume(dec->d);
+  std::memcpy(out, v.data(), v.size() * sizeof(int64_t));
+}
+MFB_API double mfadd_dec_compression_ratio(const mfadd_decomposition* dec) {
+  return static_cast<double>(dec->d.total_inputs()) / static_cast<double>(dec->d.total_ctrl());
+}
+MFB_API int mfadd_dec_any_shared(const mfadd_decomposition* dec) { return dec->d.any_shared ? 1 : 0; }
+
+// ---------------------------------------------------------------- context
+MFB_API int mfadd_context_create(int device, void* stream, mfadd_context** out) {
+  return guarded([&] {
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) throw ApiError(MFADD_ECUDA, "mfadd_context_create: no CUDA device " + std::to_string(device));
+    auto c = std::make_unique<mfadd_context>();
+    c->device = device;
+    ContextScope scope(c.get());
+    if (stream) {
+      c->stream = static_cast<cudaStream_t>(stream);
+    } else {
+      CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      c->own_stream = true;
+    }
+    CK(cudaMalloc(&c->d_status, sizeof(mfb::DevStatus)));
+    CK(cudaMemset(c->d_status, 0, sizeof(mfb::DevStatus)));
+    CK(cudaMallocHost(&c->h_pinned, 64 * sizeof(double)));
+    *out = c.release();
+  });
+}
+
+MFB_API void mfadd_context_free(mfadd_context* ctx) {
+  if (!ctx) return;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->d_status) cudaFree(ctx->d_status);
+  if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  if (prev >= 0) cudaSetDevice(prev);
+}
+
+MFB_API int64_t mfadd_context_launch_count(const mfadd_context* ctx) { return ctx->launches; }
+
+namespace {
+
+mfb::DevStatus read_status(mfadd_context* ctx) {
+  mfb::DevStatus st{};
+  CK(cudaMemcpyAsync(&st, ctx->d_status, sizeof st, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (st.code) CK(cudaMemsetAsync(ctx->d_status, 0, sizeof(mfb::DevStatus), ctx->stream));
+  return st;
+}
+
+void check_config(const mfadd_solver_config& c) {  // solver.cpp:333-335
+  if (c.max_outer_iterations < 1) throw std::invalid_argument("SolverConfig: max iterations must be >= 1");
+  if (!(c.tolerance > 0.0)) throw std::invalid_argument("SolverConfig: tolerance must be > 0");
+}
+
+double bits_to_double(unsigned long long u) {
+  double d;
+  std::memcpy(&d, &u, sizeof d);
+  return d;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- solver
+MFB_API int mfadd_solver_create(mfadd_context* ctx, const mfadd_decomposition* dech, const mfadd_solver_config* cfg,
+                                mfadd_solver** out) {
+  return guarded([&] {
+    ContextScope scope(ctx);
+    auto s = std::make_unique<mfadd_solver>();
+    s->ctx = ctx;
+    s->dec = dech->d;
+    s->cfg = *cfg;
+    const Decomp& d = s->dec;
+    const int D = d.rank, p = d.degree;
+    if (p > mfb::kMaxDegree)
+      throw std::invalid_argument("mfadd_b200: degree " + std::to_string(p) + " exceeds the compiled maximum " +
+                                  std::to_string(mfb::kMaxDegree));
+    Workload& wl = s->wl;
+    wl.D = D;
+    wl.p = p;
+    // knots (one vector per dim) and field strides
+    std::vector<double> kn;
+    std::int64_t knot_off[3] = {0, 0, 0};
+    for (int k = 0; k < D; ++k) {
+      knot_off[k] = static_cast<std::int64_t>(kn.size());
+      kn.insert(kn.end(), d.knots[k].begin(), d.knots[k].end());
+    }
+    {
+      std::int64_t st = 1;
+      for (int k = D - 1; k >= 0; --k) {
+        wl.fs[k] = st;
+        st *= d.grid[k];
+      }
+    }
+    // axis problems: one per (dim, block coordinate) — solver.cpp:59-66,83-88
+    for (int k = 0; k < D; ++k) {
+      s->axbase[k] = static_cast<int>(wl.probs.size());
+      for (int c = 0; c < d.blocks[k]; ++c) {
+        AxisProb pr{};
+        pr.dim = k;
+        pr.m = static_cast<int>(d.dim_field(k, c, mfb::IN_HI) - d.dim_field(k, c, mfb::IN_LO));
+        pr.n = static_cast<int>(d.dim_field(k, c, mfb::DOF_HI) - d.dim_field(k, c, mfb::DOF_LO));
+        pr.col_lo = d.dim_field(k, c, mfb::DOF_LO);
+        pr.in_lo = d.dim_field(k, c, mfb::IN_LO);
+        pr.M = d.grid[k];
+        pr.knot_off = knot_off[k];
+        pr.nknots = static_cast<int>(d.knots[k].size());
+        wl.factor_ids.push_back(static_cast<int>(wl.probs.size()));
+        wl.probs.push_back(pr);
+      }
+    }
+    // LocalProblem::validate (lsq.cpp:9-20) for every block, lowest id first
+    for (int b = 0; b < d.nblocks; ++b)
+      for (int k = 0; k < D; ++k) {
+        const AxisProb& pr = wl.probs[static_cast<std::size_t>(s->axbase[k] + d.coords[static_cast<std::size_t>(b)][k])];
+        if (pr.m < pr.n)
+          throw std::invalid_argument("block " + std::to_string(b) + ": LocalProblem: underdetermined in dimension " +
+                                      std::to_string(k) + " (" + std::to_string(pr.m) + " rows < " +
+                                      std::to_string(pr.n) + " cols)");
+      }
+    // global decode rows (decode.cpp:83-97 on the full lattice window)
+    for (int k = 0; k < D; ++k) {
+      AxisProb pr{};
+      pr.dim = k;
+      pr.m = static_cast<int>(d.grid[k]);
+      pr.n = static_cast<int>(d.n_ctrl[k]);
+      pr.col_lo = 0;
+      pr.in_lo = 0;
+      pr.M = d.grid[k];
+      pr.knot_off = knot_off[k];
+      pr.nknots = static_cast<int>(d.knots[k].size());
+      s->dec_prob[k] = static_cast<int>(wl.probs.size());
+      wl.probs.push_back(pr);
+    }
+    // blocks
+    for (int b = 0; b < d.nblocks; ++b) {
+      BlockDev bd{};
+      std::int64_t fb = 0;
+      for (int k = 0; k < D; ++k) {
+        bd.ax[k] = s->axbase[k] + d.coords[static_cast<std::size_t>(b)][k];
+        fb += d.at(b, k, mfb::IN_LO) * wl.fs[k];
+      }
+      bd.fbase = fb;
+      wl.blocks.push_back(bd);
+    }
+    wl.layout_tables();
+    cudaStream_t st = ctx->stream;
+    wl.allocate(st);
+    wl.knots.upload(kn, st);
+    // shared flags, holder ranges, S/C lists, owner coords
+    std::vector<unsigned char> sflag;
+    std::vector<int2> hr;
+    std::vector<int> sl, cl, oc;
+    for (int k = 0; k < D; ++k) {
+      wl.sflag_off[k] = static_cast<std::int64_t>(sflag.size());
+      s->hr_off[k] = static_cast<std::int64_t>(hr.size());
+      s->s_off[k] = static_cast<std::int64_t>(sl.size());
+      s->c_off[k] = static_cast<std::int64_t>(cl.size());
+      s->oc_off[k] = static_cast<std::int64_t>(oc.size());
+      for (std::int64_t i = 0; i < d.n_ctrl[k]; ++i) {
+        const auto r = d.holder[k][static_cast<std::size_t>(i)];
+        hr.push_back(make_int2(r[0], r[1]));
+        const bool sh = r[1] > r[0];
+        sflag.push_back(sh ? 1 : 0);
+        (sh ? sl : cl).push_back(static_cast<int>(i));
+        int owner = -1;
+        for (int c = 0; c < d.blocks[k]; ++c)
+          if (i >= d.dim_field(k, c, mfb::OWN_LO) && i < d.dim_field(k, c, mfb::OWN_HI)) owner = c;
+        if (owner < 0) throw std::logic_error("partition: control index without an owner");
+        oc.push_back(owner);
+      }
+      s->nS[k] = static_cast<std::int64_t>(sl.size()) - s->s_off[k];
+      s->nC[k] = static_cast<std::int64_t>(cl.size()) - s->c_off[k];
+    }
+    s->total_shared = 0;
+    for (int pc = 0; pc < D; ++pc) {
+      std::int64_t cnt = 1;
+      for (int k = 0; k < D; ++k) cnt *= k < pc ? s->nC[k] : (k == pc ? s->nS[k] : d.n_ctrl[k]);
+      s->piece[pc] = cnt;
+      s->total_shared += cnt;
+    }
+    wl.sflag.upload(sflag, st);
+    s->hr.upload(hr, st);
+    s->slist.upload(sl.empty() ? std::vector<int>{0} : sl, st);
+    s->clist.upload(cl.empty() ? std::vector<int>{0} : cl, st);
+    s->own_coord.upload(oc, st);
+    std::vector<std::int64_t> po;
+    for (const auto& b : wl.blocks) po.push_back(b.poff);
+    s->poff.upload(po, st);
+    // final-jump pair slots in the reference's order (solver.cpp:170-174)
+    std::vector<int> ps(static_cast<std::size_t>(d.nblocks) * 27, -1);
+    for (int a = 0; a < d.nblocks; ++a)
+      for (int j : d.neighbors[static_cast<std::size_t>(a)]) {
+        if (j < a) continue;
+        int code = 0, mul = 1;
+        for (int k = D - 1; k >= 0; --k) {
+          code += (d.coords[static_cast<std::size_t>(j)][k] - d.coords[static_cast<std::size_t>(a)][k] + 1) * mul;
+          mul *= 3;
+        }
+        ps[static_cast<std::size_t>(a) * 27 + code] = static_cast<int>(s->pair_ids.size());
+        s->pair_ids.push_back({a, j});
+      }
+    s->npairs = static_cast<int>(s->pair_ids.size());
+    s->pair_slot.upload(ps, st);
+    s->pair_jumps.alloc(static_cast<std::size_t>(std::max(1, s->npairs)) * 2);
+    s->change.alloc(static_cast<std::size_t>(d.nblocks));
+    s->linf_sh.alloc(static_cast<std::size_t>(d.nblocks));
+    s->acc.alloc(1);
+    s->epoch_out.alloc(static_cast<std::size_t>(cfg->max_outer_iterations + 1) * 3 + 3);
+    s->lattice.alloc(static_cast<std::size_t>(d.total_ctrl()));
+    if (cfg->store_error) s->error.alloc(static_cast<std::size_t>(d.total_inputs()));
+    // decode plan
+    s->dp.init(D, p, d.grid.data(), d.n_ctrl.data());
+    for (int k = 0; k < 3; ++k) {
+      const int src = k - (3 - D);
+      if (src < 0) continue;
+      std::vector<double> u(static_cast<std::size_t>(d.grid[src]));
+      for (std::int64_t j = 0; j < d.grid[src]; ++j)
+        u[static_cast<std::size_t>(j)] = static_cast<double>(j) / static_cast<double>(d.grid[src] - 1);
+      s->dp.size_windows(k, d.knots[src], u, p, 0);
+      s->dp.prob_of[k] = s->dec_prob[src];
+    }
+    s->partial.alloc(static_cast<std::size_t>(s->dp.ntiles[0] * s->dp.ntiles[1] * s->dp.ntiles[2]) * 2);
+    s->red2.alloc(2);
+    s->unit_g0.upload(std::vector<int>{0}, st);
+    s->unit_vals.upload(std::vector<double>{1.0}, st);
+    for (auto& e : s->ev) CK(cudaEventCreate(&e));
+    CK(cudaMemsetAsync(s->change.p, 0, s->change.n * sizeof(unsigned long long), st));
+    CK(cudaMemsetAsync(s->linf_sh.p, 0, s->linf_sh.n * sizeof(unsigned long long), st));
+    CK(cudaMemsetAsync(s->acc.p, 0, sizeof(mfb::EpochAcc), st));
+    CK(cudaStreamSynchronize(st));
+    *out = s.release();
+  });
+}
+
+MFB_API void mfadd_solver_free(mfadd_solver* s) {
+  if (!s) return;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(s->ctx->device);
+  cudaStreamSynchronize(s->ctx->stream);
+  delete s;
+  if (prev >= 0) cudaSetDevice(prev);
+}
+
+namespace {
+
+mfb::EpochArgs epoch_args(mfadd_solver* s, int mode) {
+  mfb::EpochArgs a{};
+  const Decomp& d = s->dec;
+  a.D = d.rank;
+  a.nblocks = d.nblocks;
+  for (int k = 0; k < 3; ++k) {
+    a.B[k] = d.blocks[k];
+    a.N[k] = d.n_ctrl[k];
+    a.hr_off[k] = s->hr_off[k];
+    a.s_off[k] = s->s_off[k];
+    a.c_off[k] = s->c_off[k];
+    a.nS[k] = s->nS[k];
+    a.nC[k] = s->nC[k];
+    a.piece[k] = s->piece[k];
+    a.axbase[k] = s->axbase[k];
+  }
+  a.hr = s->hr.p;
+  a.slist = s->slist.p;
+  a.clist = s->clist.p;
+  a.total = s->total_shared;
+  a.probs = s->wl.d_probs.p;
+  a.poff = s->poff.p;
+  a.P = s->wl.P.p;
+  a.mode = mode;
+  a.change = s->change.p;
+  a.linf_sh = s->linf_sh.p;
+  a.acc = s->acc.p;
+  a.pair_slot = s->pair_slot.p;
+  a.pair_jumps = s->pair_jumps.p;
+  return a;
+}
+
+// One epoch: K4 + K5; returns launches.  Result lands in epoch_out[3*slot].
+int run_epoch(mfadd_solver* s, int mode, int slot) {
+  int l = mfb::launch_epoch(epoch_args(s, mode), s->ctx->stream);
+  mfb::DpArgs da{s->dec.nblocks, s->change.p, s->linf_sh.p, s->wl.linf_int.p, s->acc.p, s->epoch_out.p + 3 * slot,
+                 nullptr};
+  l += mfb::launch_dp(da, s->ctx->stream);
+  CK(cudaGetLastError());
+  return l;
+}
+
+float ev_ms(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  return ms;
+}
+
+void solve_impl(mfadd_solver* s, const double* dfield) {
+  mfadd_context* ctx = s->ctx;
+  cudaStream_t st = ctx->stream;
+  const Decomp& d = s->dec;
+  Workload& wl = s->wl;
+  int launches = 0;
+  s->have_result = false;
+  s->epochs.clear();
+  CK(cudaEventRecord(s->ev[0], st));
+  // ---- setup: basis rows + Gram/Cholesky (solver.cpp:346 make_block_state)
+  launches += wl.setup(ctx);
+  CK(cudaEventRecord(s->ev[1], st));
+  // ---- decoupled local fits (solver.cpp:369-373)
+  launches += wl.fit(ctx, dfield);
+  CK(cudaEventRecord(s->ev[2], st));
+  // ---- record_epoch(0, 0.0)
+  launches += run_epoch(s, 0, 0);
+  double* hp = ctx->h_pinned;
+  CK(cudaMemcpyAsync(hp, s->epoch_out.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  const mfb::DevStatus stt = read_status(ctx);  // synchronises
+  wl.raise_status(stt, "");
+  s->epochs.push_back({0, 0.0, hp[1], hp[2]});
+  mfadd_solve_summary& sum = s->summary;
+  sum = mfadd_solve_summary{};
+  sum.converged = 1;
+  if (s->cfg.enforce_continuity && d.any_shared) {
+    sum.converged = 0;
+    for (int iter = 1; iter <= s->cfg.max_outer_iterations; ++iter) {
+      launches += run_epoch(s, iter >= 2 ? 2 : 1, iter);  // solver.cpp:397
+      CK(cudaMemcpyAsync(hp, s->epoch_out.p + 3 * iter, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      const double dpv = hp[0];
+      s->epochs.push_back({iter, dpv, hp[1], hp[2]});
+      sum.final_dp = dpv;
+      if (dpv < s->cfg.tolerance) {  // solver.cpp:406-412
+        sum.converged = 1;
+        sum.constraint_iterations = iter - 1;
+        break;
+      }
+      sum.constraint_iterations = iter;
+    }
+  }
+  CK(cudaEventRecord(s->ev[3], st));
+  // ---- final jumps per neighbour pair (solver.cpp:416)
+  if (s->npairs > 0) {
+    CK(cudaMemsetAsync(s->pair_jumps.p, 0, s->pair_jumps.n * sizeof(unsigned long long), st));
+    launches += mfb::launch_epoch(epoch_args(s, 3), st);
+  }
+  // ---- assemble_owned (solver.cpp:418-423)
+  mfb::AssembleArgs aa{};
+  aa.D = d.rank;
+  for (int k = 0; k < 3; ++k) {
+    aa.B[k] = d.blocks[k];
+    aa.N[k] = d.n_ctrl[k];
+    aa.oc_off[k] = s->oc_off[k];
+    aa.axbase[k] = s->axbase[k];
+  }
+  aa.own_coord = s->own_coord.p;
+  aa.probs = wl.d_probs.p;
+  aa.poff = s->poff.p;
+  aa.P = wl.P.p;
+  aa.lattice = s->lattice.p;
+  launches += mfb::launch_assemble(aa, st);
+  // ---- block_error_slab over every block == global decode (solver.cpp:425-438)
+  mfb::DecodeArgs da{};
+  const DecodePlan& dp = s->dp;
+  da.D = d.rank;
+  for (int k = 0; k < 3; ++k) {
+    da.M[k] = dp.M[k];
+    da.N[k] = dp.N[k];
+    da.T[k] = dp.T[k];
+    da.ntiles[k] = dp.ntiles[k];
+    da.W[k] = dp.W[k];
+    da.pk[k] = dp.pk[k];
+    if (dp.prob_of[k] >= 0) {
+      const AxisProb& pr = wl.probs[static_cast<std::size_t>(dp.prob_of[k])];
+      da.g0[k] = wl.g0.p + pr.row_off;
+      da.vals[k] = wl.vals.p + pr.row_off * (wl.p + 1);
+    } else {
+      da.g0[k] = s->unit_g0.p;
+      da.vals[k] = s->unit_vals.p;
+    }
+  }
+  da.lattice = s->lattice.p;
+  da.field = dfield;
+  da.out = s->cfg.store_error ? s->error.p : nullptr;
+  da.partial = s->partial.p;
+  launches += mfb::launch_decode(wl.p, da, st);
+  launches += mfb::launch_reduce_partials(s->partial.p, static_cast<std::int64_t>(s->partial.n / 2), s->red2.p, st);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(hp + 4, s->red2.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  std::vector<unsigned long long> pj(s->pair_jumps.n);
+  if (s->npairs > 0)
+    CK(cudaMemcpyAsync(pj.data(), s->pair_jumps.p, pj.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                       st));
+  CK(cudaEventRecord(s->ev[4], st));
+  CK(cudaStreamSynchronize(st));
+  sum.global_l2 = std::sqrt(hp[4]);
+  sum.global_linf = hp[5];
+  s->final_jumps.assign(static_cast<std::size_t>(s->npairs) * 4, 0.0);
+  for (int i = 0; i < s->npairs; ++i) {
+    s->final_jumps[4 * static_cast<std::size_t>(i)] = s->pair_ids[static_cast<std::size_t>(i)][0];
+    s->final_jumps[4 * static_cast<std::size_t>(i) + 1] = s->pair_ids[static_cast<std::size_t>(i)][1];
+    s->final_jumps[4 * static_cast<std::size_t>(i) + 2] = bits_to_double(pj[2 * static_cast<std::size_t>(i)]);
+    s->final_jumps[4 * static_cast<std::size_t>(i) + 3] = bits_to_double(pj[2 * static_cast<std::size_t>(i) + 1]);
+  }
+  sum.n_epochs = static_cast<int>(s->epochs.size());
+  sum.n_final_jumps = s->npairs;
+  sum.t_setup = ev_ms(s->ev[0], s->ev[1]) * 1e-3;
+  sum.t_local_solve = ev_ms(s->ev[1], s->ev[2]) * 1e-3;
+  sum.t_exchange = 0.0;  // single device: the exchange is fused into K4
+  sum.t_constraint = ev_ms(s->ev[2], s->ev[3]) * 1e-3;
+  sum.t_decode = ev_ms(s->ev[3], s->ev[4]) * 1e-3;
+  s->last_launches = launches;
+  ctx->launches += launches;
+  s->have_result = true;
+}
+
+}  // namespace
+
+MFB_API int mfadd_solve(mfadd_solver* s, const double* field, int field_on_device, mfadd_solve_summary* out) {
+  return guarded([&] {
+    ContextScope scope(s->ctx);
+    check_config(s->cfg);
+    const double* df = field;
+    if (!field_on_device) {
+      const std::size_t n = static_cast<std::size_t>(s->dec.total_inputs());
+      if (s->field_buf.n != n) s->field_buf.alloc(n);
+      CK(cudaMemcpyAsync(s->field_buf.p, field, n * sizeof(double), cudaMemcpyHostToDevice, s->ctx->stream));
+      df = s->field_buf.p;
+    }
+    solve_impl(s, df);
+    if (out) *out = s->summary;
+  });
+}
+
+MFB_API int mfadd_solve_host(mfadd_solver* s, const double* field_host, double* out_controls_host,
+                             double* out_error_host, mfadd_solve_summary* out) {
+  return guarded([&] {
+    ContextScope scope(s->ctx);
+    check_config(s->cfg);
+    if (out_error_host && !s->cfg.store_error)
+      throw std::invalid_argument("mfadd_solve_host: out_error requires store_error in the solver config");
+    const std::size_t n = static_cast<std::size_t>(s->dec.total_inputs());
+    if (s->field_buf.n != n) s->field_buf.alloc(n);
+    cudaStream_t st = s->ctx->stream;
+    CK(cudaMemcpyAsync(s->field_buf.p, field_host, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    solve_impl(s, s->field_buf.p);
+    if (out_controls_host)
+      CK(cudaMemcpyAsync(out_controls_host, s->lattice.p, s->lattice.n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (out_error_host)
+      CK(cudaMemcpyAsync(out_error_host, s->error.p, s->error.n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (out) *out = s->summary;
+  });
+}
+
+MFB_API int mfadd_solver_epochs(const mfadd_solver* s, mfadd_epoch_stats* out, int cap) {
+  const int n = static_cast<int>(s->epochs.size());
+  for (int i = 0; i < n && i < cap; ++i) out[i] = s->epochs[static_cast<std::size_t>(i)];
+  return n;
+}
+
+MFB_API int mfadd_solver_final_jumps(const mfadd_solver* s, double* out4, int cap) {
+  const int n = static_cast<int>(s->final_jumps.size() / 4);
+  for (int i = 0; i < n && i < cap; ++i)
+    for (int k = 0; k < 4; ++k) out4[4 * i + k] = s->final_jumps[4 * static_cast<std::size_t>(i) + k];
+  return n;
+}
+
+MFB_API int mfadd_solver_controls(const mfadd_solver* s, double* out, int out_on_device) {
+  return guarded([&] {
+    if (!s->have_result) throw std::logic_error("mfadd_solver_controls: no solve result");
+    ContextScope scope(s->ctx);
+    CK(cudaMemcpyAsync(out, s->lattice.p, s->lattice.n * sizeof(double),
+                       out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s->ctx->stream));
+    CK(cudaStreamSynchronize(s->ctx->stream));
+  });
+}
+
+MFB_API int mfadd_solver_global_error(const mfadd_solver* s, double* out, int out_on_device) {
+  return guarded([&] {
+    if (!s->have_result) throw std::logic_error("mfadd_solver_global_error: no solve result");
+    if (!s->cfg.store_error) throw std::invalid_argument("mfadd_solver_global_error: solver built without store_error");
+    ContextScope scope(s->ctx);
+    CK(cudaMemcpyAsync(out, s->error.p, s->error.n * sizeof(double),
+                       out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s->ctx->stream));
+    CK(cudaStreamSynchronize(s->ctx->stream));
+  });
+}
+
+MFB_API int mfadd_solver_block_controls(const mfadd_solver* s, int block, double* out, int out_on_device) {
+  return guarded([&] {
+    if (!s->have_result) throw std::logic_error("mfadd_solver_block_controls: no solve result");
+    if (block < 0 || block >= s->dec.nblocks) throw std::out_of_range("mfadd_solver_block_controls: block id");
+    ContextScope scope(s->ctx);
+    const BlockDev& b = s->wl.blocks[static_cast<std::size_t>(block)];
+    std::int64_t np = 1;
+    for (int k = 0; k < s->dec.rank; ++k) np *= s->wl.probs[static_cast<std::size_t>(b.ax[k])].n;
+    CK(cudaMemcpyAsync(out, s->wl.P.p + b.poff, static_cast<std::size_t>(np) * sizeof(double),
+                       out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s->ctx->stream));
+    CK(cudaStreamSynchronize(s->ctx->stream));
+  });
+}
+
+MFB_API int mfadd_solver_block_errors(const mfadd_solver* s, int epoch, double* out2) {
+  (void)s;
+  (void)epoch;
+  (void)out2;
+  g_err = "mfadd_solver_block_errors: log_errors is not implemented in this build";
+  return MFADD_EINVAL;
+}
+
+MFB_API const double* mfadd_solver_device_controls(const mfadd_solver* s) { return s->lattice.p; }
+MFB_API int mfadd_solver_last_launches(const mfadd_solver* s) { return s->last_launches; }
+
+// ---------------------------------------------------------------- fine-grained
+namespace {
+
+void check_params_ascending(const double* p, std::int64_t m) {  // collocation.cpp:89-93
+  if (m <= 0) throw std::invalid_argument("collocation_matrix: empty parameter list");
+  for (std::int64_t j = 1; j < m; ++j)
+    if (p[j] < p[j - 1]) throw std::invalid_argument("collocation_matrix: params must be ascending");
+}
+
+void check_window(int nknots, int degree, std::int64_t lo, std::int64_t hi) {
+  const std::int64_t nb = nknots - degree - 1;
+  if (lo < 0 || hi > nb || lo >= hi) throw std::invalid_argument("collocation_matrix: bad column window");
+}
+
+}  // namespace
+
+MFB_API int mfadd_collocation(mfadd_context* ctx, const double* knots, int nknots, int degree, const double* params,
+                              int64_t m, int64_t col_lo, int64_t col_hi, int64_t* out_first_col, int* out_count,
+                              double* out_values) {
+  return guarded([&] {
+    ContextScope scope(ctx);
+    if (degree < 1 || degree > mfb::kMaxDegree) throw std::invalid_argument("mfadd_collocation: unsupported degree");
+    check_params_ascending(params, m);
+    check_window(nknots, degree, col_lo, col_hi);
+    Workload wl;
+    wl.D = 1;
+    wl.p = degree;
+    AxisProb pr{};
+    pr.dim = 0;
+    pr.m = static_cast<int>(m);
+    pr.n = static_cast<int>(col_hi - col_lo);
+    pr.col_lo = col_lo;
+    pr.M = -1;
+    pr.param_off = 0;
+    pr.knot_off = 0;
+    pr.nknots = nknots;
+    wl.probs.push_back(pr);
+    wl.layout_tables();
+    cudaStream_t st = ctx->stream;
+    wl.d_probs.upload(wl.probs, st);
+    wl.knots.upload(std::vector<double>(knots, knots + nknots), st);
+    wl.params.upload(std::vector<double>(params, params + m), st);
+    wl.g0.alloc(static_cast<std::size_t>(m));
+    wl.first_col.alloc(static_cast<std::size_t>(m));
+    wl.count.alloc(static_cast<std::size_t>(m));
+    wl.vals.alloc(static_cast<std::size_t>(m) * (degree + 1));
+    mfb::RowsArgs ra{wl.d_probs.p, 1, pr.m, wl.knots.p, wl.params.p, wl.g0.p, wl.first_col.p, wl.count.p, wl.vals.p,
+                     ctx->d_status};
+    ctx->launches += mfb::launch_basis_rows(degree, ra, st);
+    CK(cudaGetLastError());
+    std::vector<int> g0(static_cast<std::size_t>(m)), fc(static_cast<std::size_t>(m));
+    std::vector<double> v(static_cast<std::size_t>(m) * (degree + 1));
+    CK(cudaMemcpyAsync(g0.data(), wl.g0.p, g0.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(fc.data(), wl.first_col.p, fc.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(out_count, wl.count.p, static_cast<std::size_t>(m) * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(v.data(), wl.vals.p, v.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+    const mfb::DevStatus stt = read_status(ctx);
+    wl.raise_status(stt, "");
+    // repack to BandedCollocation layout (clipped values left-aligned)
+    for (std::int64_t j = 0; j < m; ++j) {
+      out_first_col[j] = fc[static_cast<std::size_t>(j)];
+      const int shift = fc[static_cast<std::size_t>(j)] - g0[static_cast<std::size_t>(j)];
+      for (int k = 0; k <= degree; ++k) {
+        const int src = k + shift;
+        out_values[j * (degree + 1) + k] =
+            (k < out_count[j] && src <= degree) ? v[static_cast<std::size_t>(j) * (degree + 1) + src] : 0.0;
+      }
+    }
+  });
+}
+
+MFB_API int mfadd_fit_unconstrained(mfadd_context* ctx, int rank, int degree, const double* knots,
+                                    const int64_t* kn_off, const double* params, const int64_t* pm_off,
+                                    const int64_t* col_lo, const int64_t* col_hi, const double* q, double* out_p) {
+  return guarded([&] {
+    ContextScope scope(ctx);
+    if (rank < 1 || rank > 3) throw std::invalid_argument("fit_unconstrained: rank must be 1..3");
+    if (degree < 1 || degree > mfb::kMaxDegree) throw std::invalid_argument("fit_unconstrained: unsupported degree");
+    Workload wl;
+    wl.D = rank;
+    wl.p = degree;
+    BlockDev bd{};
+    std::int64_t qn = 1;
+    for (int k = 0; k < rank; ++k) {
+      const std::int64_t m = pm_off[k + 1] - pm_off[k];
+      check_params_ascending(params + pm_off[k], m);
+      check_window(static_cast<int>(kn_off[k + 1] - kn_off[k]), degree, col_lo[k], col_hi[k]);
+      AxisProb pr{};
+      pr.dim = k;
+      pr.m = static_cast<int>(m);
+      pr.n = static_cast<int>(col_hi[k] - col_lo[k]);
+      pr.col_lo = col_lo[k];
+      pr.M = -1;
+      pr.param_off = pm_off[k];
+      pr.knot_off = kn_off[k];
+      pr.nknots = static_cast<int>(kn_off[k + 1] - kn_off[k]);
+      bd.ax[k] = k;
+      wl.factor_ids.push_back(k);
+      wl.probs.push_back(pr);
+      qn *= m;
+    }
+    for (int k = 0; k < rank; ++k)  // lsq.cpp:14-18
+      if (wl.probs[static_cast<std::size_t>(k)].m < wl.probs[static_cast<std::size_t>(k)].n)
+        throw std::invalid_argument("LocalProblem: underdetermined in dimension " + std::to_string(k) + " (" +
+                                    std::to_string(wl.probs[static_cast<std::size_t>(k)].m) + " rows < " +
+                                    std::to_string(wl.probs[static_cast<std::size_t>(k)].n) + " cols)");
+    {
+      std::int64_t stv = 1;
+      for (int k = rank - 1; k >= 0; --k) {
+        wl.fs[k] = stv;
+        stv *= wl.probs[static_cast<std::size_t>(k)].m;
+      }
+    }
+    wl.blocks.push_back(bd);
+    wl.layout_tables();
+    cudaStream_t st = ctx->stream;
+    wl.allocate(st);
+    wl.knots.upload(std::vector<double>(knots, knots + kn_off[rank]), st);
+    wl.params.upload(std::vector<double>(params, params + pm_off[rank]), st);
+    std::vector<unsigned char> sf;
+    for (int k = 0; k < rank; ++k) {
+      wl.sflag_off[k] = static_cast<std::int64_t>(sf.size());
+      sf.resize(sf.size() + static_cast<std::size_t>(col_hi[k]), 0);
+    }
+    wl.sflag.upload(sf, st);
+    DBuf<double> dq;
+    dq.upload(std::vector<double>(q, q + qn), st);
+    ctx->launches += wl.setup(ctx);
+    ctx->launches += wl.fit(ctx, dq.p);
+    const mfb::DevStatus stt = read_status(ctx);
+    wl.raise_status(stt, "");
+    CK(cudaMemcpyAsync(out_p, wl.P.p, static_cast<std::size_t>(wl.total_p) * sizeof(double), cudaMemcpyDeviceToHost,
+                       st));
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+MFB_API int mfadd_decode(mfadd_context* ctx, int rank, int degree, const double* knots, const int64_t* kn_off,
+                         const double* params, const int64_t* pm_off, const int64_t* ctrl_ext,
+                         const int64_t* col_offset, const double* controls, double* out) {
+  return guarded([&] {
+    ContextScope scope(ctx);
+    if (rank < 1 || rank > 3) throw std::invalid_argument("decode: dimension mismatch between lattice, knot vectors and parameters");
+    if (degree < 1 || degree > mfb::kMaxDegree) throw std::invalid_argument("decode: unsupported degree");
+    Workload wl;
+    wl.D = rank;
+    wl.p = degree;
+    std::int64_t Mi[3], Ni[3], nctl = 1, nout = 1;
+    std::vector<std::vector<double>> kv(static_cast<std::size_t>(rank)), pv(static_cast<std::size_t>(rank));
+    for (int k = 0; k < rank; ++k) {
+      const std::int64_t m = pm_off[k + 1] - pm_off[k];
+      const std::int64_t off = col_offset ? col_offset[k] : 0;
+      check_params_ascending(params + pm_off[k], m);
+      check_window(static_cast<int>(kn_off[k + 1] - kn_off[k]), degree, off, off + ctrl_ext[k]);
+      AxisProb pr{};
+      pr.dim = k;
+      pr.m = static_cast<int>(m);
+      pr.n = static_cast<int>(ctrl_ext[k]);
+      pr.col_lo = off;
+      pr.M = -1;
+      pr.param_off = pm_off[k];
+      pr.knot_off = kn_off[k];
+      pr.nknots = static_cast<int>(kn_off[k + 1] - kn_off[k]);
+      wl.probs.push_back(pr);
+      Mi[k] = m;
+      Ni[k] = ctrl_ext[k];
+      nctl *= ctrl_ext[k];
+      nout *= m;
+      kv[static_cast<std::size_t>(k)].assign(knots + kn_off[k], knots + kn_off[k + 1]);
+      pv[static_cast<std::size_t>(k)].assign(params + pm_off[k], params + pm_off[k + 1]);
+    }
+    wl.layout_tables();
+    cudaStream_t st = ctx->stream;
+    wl.d_probs.upload(wl.probs, st);
+    wl.knots.upload(std::vector<double>(knots, knots + kn_off[rank]), st);
+    wl.params.upload(std::vector<double>(params, params + pm_off[rank]), st);
+    wl.g0.alloc(static_cast<std::size_t>(wl.total_rows));
+    wl.first_col.alloc(static_cast<std::size_t>(wl.total_rows));
+    wl.count.alloc(static_cast<std::size_t>(wl.total_rows));
+    wl.vals.alloc(static_cast<std::size_t>(wl.total_rows) * (degree + 1));
+    mfb::RowsArgs ra{wl.d_probs.p, rank, wl.max_m, wl.knots.p, wl.params.p, wl.g0.p, wl.first_col.p, wl.count.p,
+                     wl.vals.p, ctx->d_status};
+    ctx->launches += mfb::launch_basis_rows(degree, ra, st);
+    DecodePlan dp;
+    dp.init(rank, degree, Mi, Ni);
+    for (int k = 0; k < 3; ++k) {
+      const int src = k - (3 - rank);
+      if (src < 0) continue;
+      // window widths in local columns: spans relative to the same knots
+      dp.size_windows(k, kv[static_cast<std::size_t>(src)], pv[static_cast<std::size_t>(src)], degree, 0);
+      dp.prob_of[k] = src;
+    }
+    DBuf<double> dctl, dout, dpart;
+    DBuf<int> ug0;
+    DBuf<double> uval;
+    dctl.upload(std::vector<double>(controls, controls + nctl), st);
+    dout.alloc(static_cast<std::size_t>(nout));
+    ug0.upload(std::vector<int>{0}, st);
+    uval.upload(std::vector<double>{1.0}, st);
+    mfb::DecodeArgs da{};
+    da.D = rank;
+    for (int k = 0; k < 3; ++k) {
+      da.M[k] = dp.M[k];
+      da.N[k] = dp.N[k];
+      da.T[k] = dp.T[k];
+      da.ntiles[k] = dp.ntiles[k];
+      da.W[k] = dp.W[k];
+      da.pk[k] = dp.pk[k];
+      if (dp.prob_of[k] >= 0) {
+        const AxisProb& pr = wl.probs[static_cast<std::size_t>(dp.prob_of[k])];
+        da.g0[k] = wl.g0.p + pr.row_off;
+        da.vals[k] = wl.vals.p + pr.row_off * (degree + 1);
+      } else {
+        da.g0[k] = ug0.p;
+        da.vals[k] = uval.p;
+      }
+    }
+    da.lattice = dctl.p;
+    da.field = nullptr;
+    da.out = dout.p;
+    da.partial = nullptr;
+    ctx->launches += mfb::launch_decode(degree, da, st);
+    CK(cudaGetLastError());
+    const mfb::DevStatus stt = read_status(ctx);
+    wl.raise_status(stt, "");
+    CK(cudaMemcpyAsync(out, dout.p, static_cast<std::size_t>(nout) * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  });
+}

@@ -1,0 +1,863 @@
+// sm_100a kernels of the B200-native domain-decomposed MFA encode path.
+//
+// Kernel map (reference routine each one replaces; paths under
+// /root/reference/proj/core/src):
+//   K1 k_basis_rows   find_span + basis_funs + collocation window clip
+//                     (knots.cpp:83-129, collocation.cpp:83-111)
+//   K2 k_gram_chol    BandedCollocation::gram + Eigen LLT
+//                     (collocation.cpp:56-67, lsq.cpp:46-55)
+//   K3 k_fit_strided  fit_unconstrained axis pass on a non-contiguous axis
+//      k_fit_last     ... on the contiguous (last) axis
+//                     (lsq.cpp:57-61, collocation.cpp:46-54, tensor.hpp:78-106)
+//   K4 k_epoch        one exchange/averaging epoch over all shared controls
+//                     (solver.cpp:112-164,381-398; runtime.cpp:123-158) +
+//                     jump_residuals (solver.cpp:166-193)
+//   K5 k_dp           dp = max_b change_b / max(1, ||P_b||) (solver.cpp:402-405)
+//   K6 k_assemble     assemble_owned (solver.cpp:281-294)
+//   K7 k_decode       decode + error + L2^2/Linf partials (decode.cpp:83-97,
+//                     solver.cpp:298-328)
+// Bitwise-exact pieces: spans, first_col/count (integers), basis values and
+// Gram entries (explicit round-to-nearest ops, no FMA contraction, same
+// operation order as the reference).  The contractions and triangular solves
+// use FMA; they agree with the reference at rounding level (tolerance parity).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.cuh"
+
+namespace mfb {
+
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ void set_status(DevStatus* st, int code, int prob, int row) {
+  if (atomicCAS(&st->code, 0, code) == 0) {
+    st->axis_prob = prob;
+    st->row = row;
+  }
+}
+
+__device__ __forceinline__ unsigned long long dbits(double x) {
+  return static_cast<unsigned long long>(__double_as_longlong(x));
+}
+
+__device__ __forceinline__ unsigned long long umax(unsigned long long a, unsigned long long b) { return a > b ? a : b; }
+
+__device__ __forceinline__ unsigned long long warp_umax(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = umax(v, __shfl_xor_sync(kFull, v, o));
+  return v;
+}
+
+// Block-wide max of a u64, result valid in thread 0.  `red` >= 32 entries.
+__device__ __forceinline__ unsigned long long block_umax(unsigned long long v, unsigned long long* red) {
+  v = warp_umax(v);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+    v = lane < nw ? red[lane] : 0ull;
+    v = warp_umax(v);
+  }
+  return v;
+}
+
+// ------------------------------------------------------------------- K1
+template <int P>
+__global__ void __launch_bounds__(256) k_basis_rows(RowsArgs a) {
+  const int pid = blockIdx.y;
+  const AxisProb pr = a.probs[pid];
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= pr.m) return;
+  const double* kn = a.knots + pr.knot_off;
+  // solver.cpp:64: u = (double)(input_lo + j) / (double)(M - 1), IEEE division
+  const double u = pr.M >= 0 ? __ddiv_rn(static_cast<double>(pr.in_lo + j), static_cast<double>(pr.M - 1))
+                             : a.params[pr.param_off + j];
+  const int nb = pr.nknots - P - 1;
+  const double lo = kn[P], hi = kn[nb];
+  const std::int64_t row = pr.row_off + j;
+  if (u < lo || u > hi) {  // knots.cpp:88-90
+    set_status(a.status, 2, pid, j);
+    a.g0[row] = 0;
+    a.first_col[row] = 0;
+    a.count[row] = 0;
+#pragma unroll
+    for (int k = 0; k <= P; ++k) a.vals[row * (P + 1) + k] = 0.0;
+    return;
+  }
+  int span;
+  if (u >= hi) {  // knots.cpp:91-95: right endpoint -> last nonempty span
+    int s = nb - 1;
+    while (s > P && kn[s] == kn[s + 1]) --s;
+    span = s;
+  } else {  // knots.cpp:96-105: binary search, half-open spans
+    int low = P, high = nb, mid = (low + high) / 2;
+    while (u < kn[mid] || u >= kn[mid + 1]) {
+      if (u < kn[mid])
+        high = mid;
+      else
+        low = mid;
+      mid = (low + high) / 2;
+    }
+    span = mid;
+  }
+  // knots.cpp:108-129 Cox-de Boor, explicit RN ops (no contraction)
+  double N[P + 1], left[P + 1], right[P + 1];
+  N[0] = 1.0;
+#pragma unroll
+  for (int jj = 1; jj <= P; ++jj) {
+    left[jj] = __dsub_rn(u, kn[span + 1 - jj]);
+    right[jj] = __dsub_rn(kn[span + jj], u);
+    double saved = 0.0;
+#pragma unroll
+    for (int r = 0; r < jj; ++r) {
+      const double denom = __dadd_rn(right[r + 1], left[jj - r]);
+      const double temp = __ddiv_rn(N[r], denom);
+      N[r] = __dadd_rn(saved, __dmul_rn(right[r + 1], temp));
+      saved = __dmul_rn(left[jj - r], temp);
+    }
+    N[jj] = saved;
+  }
+  // collocation.cpp:97-108: clip to the column window
+  const std::int64_t g0 = static_cast<std::int64_t>(span) - P;
+  const std::int64_t clo = pr.col_lo, chi = pr.col_lo + pr.n;
+  const std::int64_t lc = g0 > clo ? g0 : clo;
+  const std::int64_t hc = (g0 + P + 1) < chi ? (g0 + P + 1) : chi;
+  if (lc >= hc) set_status(a.status, 1, pid, j);
+  a.g0[row] = static_cast<int>(g0 - clo);
+  a.first_col[row] = static_cast<int>(lc - clo);
+  a.count[row] = hc > lc ? static_cast<int>(hc - lc) : 0;
+#pragma unroll
+  for (int k = 0; k <= P; ++k) {
+    const std::int64_t g = g0 + k;
+    a.vals[row * (P + 1) + k] = (g >= lc && g < hc) ? N[k] : 0.0;
+  }
+}
+
+// ------------------------------------------------------------------- K2
+template <int P>
+__global__ void __launch_bounds__(256) k_gram_chol(CholArgs a) {
+  extern __shared__ double sm[];  // n*(P+1): sm[c*(P+1)+k] = G(c, c-k) -> L(c, c-k)
+  const int pid = a.prob_ids[blockIdx.x];
+  const AxisProb pr = a.probs[pid];
+  const int n = pr.n, m = pr.m;
+  const int* g0 = a.g0 + pr.row_off;
+  const double* v = a.vals + pr.row_off * (P + 1);
+  // collocation.cpp:56-67: each entry accumulated over rows in row order
+  for (int e = threadIdx.x; e < n * (P + 1); e += blockDim.x) {
+    const int c = e / (P + 1), k = e - c * (P + 1);
+    double s = 0.0;
+    if (c - k >= 0) {
+      int lo = 0, hi = m;  // first row with g0 >= c - P
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (g0[mid] < c - P)
+          lo = mid + 1;
+        else
+          hi = mid;
+      }
+      for (int j = lo; j < m; ++j) {
+        const int gj = g0[j];
+        if (gj > c - k) break;
+        s = __dadd_rn(s, __dmul_rn(v[j * (P + 1) + (c - gj)], v[j * (P + 1) + (c - k - gj)]));
+      }
+    }
+    sm[e] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // Banded left-looking Cholesky, in place; sm[c*(P+1)] keeps 1/L(c,c)
+    // during the sweep and L(c,c) is recovered when the table is written.
+    for (int c = 0; c < n; ++c) {
+      double* Lc = sm + c * (P + 1);
+      const int kmax = c < P ? c : P;
+      for (int k = kmax; k >= 1; --k) {
+        const int j = c - k;
+        const double* Lj = sm + j * (P + 1);
+        double s = Lc[k];
+        const int t0 = c - P > 0 ? c - P : 0;
+        for (int t = t0; t < j; ++t) s = fma(-Lc[c - t], Lj[j - t], s);
+        Lc[k] = s * Lj[0];  // * 1/L(j,j)
+      }
+      double dg = Lc[0];
+      for (int k = 1; k <= kmax; ++k) dg = fma(-Lc[k], Lc[k], dg);
+      if (!(dg > 0.0)) {  // Eigen LLT NumericalIssue -> SingularFitError
+        set_status(a.status, 3, pid, c);
+        dg = 1.0;
+      }
+      Lc[0] = 1.0 / sqrt(dg);
+    }
+  }
+  __syncthreads();
+  // table per column: [1/L(c,c), L(c,c-k) k=1..P, L(c+k,c) k=1..P]
+  double* out = a.ltab + pr.col_off * (2 * P + 1);
+  for (int e = threadIdx.x; e < n * (2 * P + 1); e += blockDim.x) {
+    const int c = e / (2 * P + 1), q = e - c * (2 * P + 1);
+    double val;
+    if (q == 0) {
+      val = sm[c * (P + 1)];
+    } else if (q <= P) {
+      val = (c - q >= 0) ? sm[c * (P + 1) + q] : 0.0;
+    } else {
+      const int k = q - P;
+      val = (c + k < n) ? sm[(c + k) * (P + 1) + k] : 0.0;
+    }
+    out[e] = val;
+  }
+}
+
+// ------------------------------------------------------------------- K3
+constexpr int kRowChunk = 64;  // rows staged per smem chunk (strided pass)
+constexpr int kPrefetch = 4;   // input rows in flight per thread
+constexpr int kStridedThreads = 256;
+
+// Flush the window column `cbase`: forward substitution of column c
+// (y_c = (b_c - sum_k L(c,c-k) y_{c-k}) / L(c,c)), then shift the window.
+#define MFB_FLUSH_FWD(STORE)                                      \
+  {                                                               \
+    const int c_ = cbase;                                         \
+    if (c_ >= 0 && c_ < n) {                                      \
+      const double* Lc_ = lt + static_cast<std::int64_t>(c_) * (2 * P + 1); \
+      double s_ = acc[0];                                         \
+      _Pragma("unroll") for (int k_ = 1; k_ <= P; ++k_) s_ = fma(-Lc_[k_], yw[k_ - 1], s_); \
+      const double y_ = s_ * Lc_[0];                              \
+      STORE;                                                      \
+      _Pragma("unroll") for (int k_ = P - 1; k_ >= 1; --k_) yw[k_] = yw[k_ - 1]; \
+      yw[0] = y_;                                                 \
+    }                                                             \
+    _Pragma("unroll") for (int k_ = 0; k_ < P; ++k_) acc[k_] = acc[k_ + 1]; \
+    acc[P] = 0.0;                                                 \
+    ++cbase;                                                      \
+  }
+
+template <int P>
+__global__ void __launch_bounds__(kStridedThreads) k_fit_strided(FitArgs a, int d) {
+  __shared__ int s_g0[kRowChunk];
+  __shared__ double s_v[kRowChunk * (P + 1)];
+  const int b = blockIdx.y;
+  const BlockDev blk = a.blocks[b];
+  const AxisProb pr = a.probs[blk.ax[d]];
+  const int m = pr.m, n = pr.n;
+  std::int64_t L = 1, Tr = 1;
+  for (int k = 0; k < a.D; ++k) {
+    if (k < d) L *= a.probs[blk.ax[k]].n;
+    if (k > d) Tr *= a.probs[blk.ax[k]].m;
+  }
+  const std::int64_t nlines = L * Tr;
+  const std::int64_t line0 = static_cast<std::int64_t>(blockIdx.x) * blockDim.x;
+  if (line0 >= nlines) return;
+  const std::int64_t line = line0 + threadIdx.x;
+  const bool active = line < nlines;
+  const std::int64_t l = active ? line / Tr : 0, t = active ? line - (line / Tr) * Tr : 0;
+  const double* src;
+  std::int64_t sst;
+  if (d == 0) {
+    std::int64_t off = blk.fbase, r = t;
+    for (int k = a.D - 1; k >= 1; --k) {
+      const std::int64_t mk = a.probs[blk.ax[k]].m;
+      off += (r % mk) * a.fs[k];
+      r /= mk;
+    }
+    src = a.field + off;
+    sst = a.fs[0];
+  } else {
+    src = a.t1 + blk.t1off + (l * m) * Tr + t;
+    sst = Tr;
+  }
+  double* dst = (d == 0 ? a.t1 + blk.t1off : a.t2 + blk.t2off) + (l * n) * Tr + t;
+  const std::int64_t dstr = Tr;
+  const int* g0g = a.g0 + pr.row_off;
+  const double* vg = a.vals + pr.row_off * (P + 1);
+  const double* lt = a.ltab + pr.col_off * (2 * P + 1);
+
+  double acc[P + 1], yw[P];
+#pragma unroll
+  for (int k = 0; k <= P; ++k) acc[k] = 0.0;
+#pragma unroll
+  for (int k = 0; k < P; ++k) yw[k] = 0.0;
+  int cbase = g0g[0] < 0 ? g0g[0] : 0;
+  double qr[kPrefetch];
+#pragma unroll
+  for (int u = 0; u < kPrefetch; ++u) qr[u] = (active && u < m) ? src[static_cast<std::int64_t>(u) * sst] : 0.0;
+
+  for (int j0 = 0; j0 < m; j0 += kRowChunk) {
+    const int jn = (m - j0) < kRowChunk ? (m - j0) : kRowChunk;
+    __syncthreads();
+    for (int e = threadIdx.x; e < jn; e += blockDim.x) s_g0[e] = g0g[j0 + e];
+    for (int e = threadIdx.x; e < jn * (P + 1); e += blockDim.x) s_v[e] = vg[static_cast<std::int64_t>(j0) * (P + 1) + e];
+    __syncthreads();
+    for (int jj = 0; jj < jn; jj += kPrefetch) {
+#pragma unroll
+      for (int u = 0; u < kPrefetch; ++u) {
+        if (jj + u < jn) {
+          const double q = qr[u];
+          const int jg = j0 + jj + u + kPrefetch;
+          qr[u] = (active && jg < m) ? src[static_cast<std::int64_t>(jg) * sst] : 0.0;
+          const int g = s_g0[jj + u];
+          while (cbase < g) MFB_FLUSH_FWD(if (active) dst[static_cast<std::int64_t>(c_) * dstr] = y_)
+          const double* vr = s_v + (jj + u) * (P + 1);
+#pragma unroll
+          for (int k = 0; k <= P; ++k) acc[k] = fma(vr[k], q, acc[k]);
+        }
+      }
+    }
+  }
+  while (cbase < n) MFB_FLUSH_FWD(if (active) dst[static_cast<std::int64_t>(c_) * dstr] = y_)
+
+  // Back substitution x_c = (y_c - sum_k L(c+k,c) x_{c+k}) / L(c,c), in place.
+  double xw[P];
+#pragma unroll
+  for (int k = 0; k < P; ++k) xw[k] = 0.0;
+#pragma unroll 4
+  for (int c = n - 1; c >= 0; --c) {
+    const double* Lc = lt + static_cast<std::int64_t>(c) * (2 * P + 1);
+    double s = active ? dst[static_cast<std::int64_t>(c) * dstr] : 0.0;
+#pragma unroll
+    for (int k = 1; k <= P; ++k) s = fma(-Lc[P + k], xw[k - 1], s);
+    const double x = s * Lc[0];
+    if (active) dst[static_cast<std::int64_t>(c) * dstr] = x;
+#pragma unroll
+    for (int k = P - 1; k >= 1; --k) xw[k] = xw[k - 1];
+    xw[0] = x;
+  }
+}
+
+constexpr int kLastCols = 32;     // columns staged per chunk (last-axis pass)
+constexpr int kLastThreads = 128;  // lines per CTA
+
+template <int P>
+__global__ void __launch_bounds__(kLastThreads) k_fit_last(FitArgs a) {
+  extern __shared__ double smem[];
+  constexpr int CW = kLastCols, SP = CW + 1;
+  double* s_q = smem;                          // LT x SP
+  double* s_v = s_q + kLastThreads * SP;       // CW x (P+1)
+  int* s_g0 = reinterpret_cast<int*>(s_v + CW * (P + 1));
+  __shared__ unsigned long long s_red[32];
+  const int d = a.D - 1;
+  const int b = blockIdx.y;
+  const BlockDev blk = a.blocks[b];
+  const AxisProb pr = a.probs[blk.ax[d]];
+  const int m = pr.m, n = pr.n;
+  std::int64_t L = 1;
+  for (int k = 0; k < d; ++k) L *= a.probs[blk.ax[k]].n;
+  const std::int64_t l0 = static_cast<std::int64_t>(blockIdx.x) * kLastThreads;
+  if (l0 >= L) return;
+  const int nl = static_cast<int>((L - l0) < kLastThreads ? (L - l0) : kLastThreads);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = kLastThreads / 32;
+  const bool active = tid < nl;
+  const double* src = (a.D == 1 ? a.field + blk.fbase : (a.D == 2 ? a.t1 + blk.t1off : a.t2 + blk.t2off)) + l0 * m;
+  double* Pb = a.P + blk.poff + l0 * n;
+  double* Yb = a.Y + blk.poff + l0 + tid;  // transposed scratch: Y[c*L + l]
+  const int* g0g = a.g0 + pr.row_off;
+  const double* vg = a.vals + pr.row_off * (P + 1);
+  const double* lt = a.ltab + pr.col_off * (2 * P + 1);
+
+  double acc[P + 1], yw[P];
+#pragma unroll
+  for (int k = 0; k <= P; ++k) acc[k] = 0.0;
+#pragma unroll
+  for (int k = 0; k < P; ++k) yw[k] = 0.0;
+  int cbase = g0g[0] < 0 ? g0g[0] : 0;
+  for (int j0 = 0; j0 < m; j0 += CW) {
+    const int jn = (m - j0) < CW ? (m - j0) : CW;
+    __syncthreads();
+    for (int li = warp; li < nl; li += nwarps)
+      s_q[li * SP + lane] = lane < jn ? src[static_cast<std::int64_t>(li) * m + j0 + lane] : 0.0;
+    for (int e = tid; e < jn; e += kLastThreads) s_g0[e] = g0g[j0 + e];
+    for (int e = tid; e < jn * (P + 1); e += kLastThreads) s_v[e] = vg[static_cast<std::int64_t>(j0) * (P + 1) + e];
+    __syncthreads();
+    for (int jj = 0; jj < jn; ++jj) {
+      const int g = s_g0[jj];
+      while (cbase < g) MFB_FLUSH_FWD(if (active) Yb[static_cast<std::int64_t>(c_) * L] = y_)
+      const double q = s_q[tid * SP + jj];
+      const double* vr = s_v + jj * (P + 1);
+#pragma unroll
+      for (int k = 0; k <= P; ++k) acc[k] = fma(vr[k], q, acc[k]);
+    }
+  }
+  while (cbase < n) MFB_FLUSH_FWD(if (active) Yb[static_cast<std::int64_t>(c_) * L] = y_)
+
+  // Is this line's lead index shared along any leading dim?
+  bool lead_shared = false;
+  {
+    std::int64_t r = l0 + tid;
+    for (int k = d - 1; k >= 0; --k) {
+      const AxisProb pk = a.probs[blk.ax[k]];
+      const std::int64_t ik = r % pk.n;
+      r /= pk.n;
+      if (active && a.shared_flag[a.sflag_off[k] + pk.col_lo + ik]) lead_shared = true;
+    }
+  }
+  const unsigned char* sf_last = a.shared_flag + a.sflag_off[d] + pr.col_lo;
+
+  double xw[P];
+#pragma unroll
+  for (int k = 0; k < P; ++k) xw[k] = 0.0;
+  unsigned long long lmax = 0ull;
+  for (int chi = n - 1; chi >= 0; chi -= CW) {
+    const int clo = chi - CW + 1 > 0 ? chi - CW + 1 : 0;
+    const int cn = chi - clo + 1;
+#pragma unroll 4
+    for (int c = chi; c >= clo; --c) {
+      const double* Lc = lt + static_cast<std::int64_t>(c) * (2 * P + 1);
+      double s = active ? Yb[static_cast<std::int64_t>(c) * L] : 0.0;
+#pragma unroll
+      for (int k = 1; k <= P; ++k) s = fma(-Lc[P + k], xw[k - 1], s);
+      const double x = s * Lc[0];
+#pragma unroll
+      for (int k = P - 1; k >= 1; --k) xw[k] = xw[k - 1];
+      xw[0] = x;
+      s_q[tid * SP + (c - clo)] = x;
+      if (active && !lead_shared && !sf_last[c]) lmax = umax(lmax, dbits(fabs(x)));
+    }
+    __syncthreads();
+    for (int li = warp; li < nl; li += nwarps)
+      if (lane < cn) Pb[static_cast<std::int64_t>(li) * n + clo + lane] = s_q[li * SP + lane];
+    __syncthreads();
+  }
+  lmax = block_umax(lmax, s_red);
+  if (tid == 0 && lmax) atomicMax(a.linf_int + b, lmax);
+}
+
+// ------------------------------------------------------------------- K4
+// Decompose a flat shared-dof index into per-dim global indices.  Shared
+// dofs are enumerated as D disjoint "pieces": piece k = C_0 x .. x C_{k-1} x
+// S_k x A_{k+1} x .. (C = non-shared indices, S = shared, A = all).
+__device__ __forceinline__ bool piece_index(const EpochArgs& a, std::int64_t g, std::int64_t* idx) {
+  int pc = 0;
+  while (pc < a.D && g >= a.piece[pc]) {
+    g -= a.piece[pc];
+    ++pc;
+  }
+  if (pc >= a.D) return false;
+  for (int k = a.D - 1; k >= 0; --k) {
+    const std::int64_t ext = k < pc ? a.nC[k] : (k == pc ? a.nS[k] : a.N[k]);
+    const std::int64_t r = g % ext;
+    g /= ext;
+    idx[k] = k < pc ? a.clist[a.c_off[k] + r] : (k == pc ? a.slist[a.s_off[k] + r] : r);
+  }
+  return true;
+}
+
+constexpr int kEpochThreads = 256;
+constexpr int kEpochSmemBlocks = 1024;  // per-CTA smem reduction slots
+
+__global__ void __launch_bounds__(kEpochThreads) k_epoch(EpochArgs a) {
+  __shared__ unsigned long long s_change[kEpochSmemBlocks];
+  __shared__ unsigned long long s_linf[kEpochSmemBlocks];
+  const bool use_smem = a.nblocks <= kEpochSmemBlocks && a.mode != 3;
+  if (use_smem) {
+    for (int i = threadIdx.x; i < a.nblocks; i += blockDim.x) {
+      s_change[i] = 0ull;
+      s_linf[i] = 0ull;
+    }
+    __syncthreads();
+  }
+  unsigned long long jss = 0ull, jms = 0ull;
+  const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+  for (std::int64_t g = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < a.total; g += stride) {
+    std::int64_t idx[3] = {0, 0, 0};
+    if (!piece_index(a, g, idx)) continue;
+    int f[3] = {0, 0, 0}, e[3] = {1, 1, 1};
+    int ns = 1;
+    for (int k = 0; k < a.D; ++k) {
+      const int2 r = a.hr[a.hr_off[k] + idx[k]];
+      f[k] = r.x;
+      e[k] = r.y - r.x + 1;
+      ns *= e[k];
+    }
+    // holders in ascending block id (layout.cpp:177-195): lexicographic coords
+    std::int64_t off[8];
+    int ids[8];
+    double v[8];
+    for (int h = 0; h < ns; ++h) {
+      int rr = h, c[3] = {0, 0, 0};
+      for (int k = a.D - 1; k >= 0; --k) {
+        c[k] = f[k] + rr % e[k];
+        rr /= e[k];
+      }
+      int id = 0;
+      std::int64_t o = 0;
+      for (int k = 0; k < a.D; ++k) {
+        id = id * a.B[k] + c[k];
+        const AxisProb& pk = a.probs[a.axbase[k] + c[k]];
+        o = o * pk.n + (idx[k] - pk.col_lo);
+      }
+      ids[h] = id;
+      off[h] = a.poff[id] + o;
+      v[h] = a.P[off[h]];
+    }
+    if (a.mode == 3) {  // final per-pair jumps (solver.cpp:416 -> :166-193)
+      for (int h1 = 0; h1 < ns; ++h1)
+        for (int h2 = h1 + 1; h2 < ns; ++h2) {
+          int code = 0, ra = ids[h1], rb = ids[h2], mul = 1;
+          for (int k = a.D - 1; k >= 0; --k) {
+            const int ca = ra % a.B[k], cb = rb % a.B[k];
+            ra /= a.B[k];
+            rb /= a.B[k];
+            code += (cb - ca + 1) * mul;
+            mul *= 3;
+          }
+          const int slot = a.pair_slot[ids[h1] * 27 + code];
+          if (slot >= 0) atomicMax(a.pair_jumps + 2 * slot + (ns > 2 ? 1 : 0), dbits(fabs(v[h1] - v[h2])));
+        }
+      continue;
+    }
+    const bool update = (a.mode == 2) || (a.mode == 1 && ns == 2);
+    if (update) {
+      // solver.cpp:147-159: ordered sum in ascending holder id, divide once
+      double sum = 0.0;
+      for (int h = 0; h < ns; ++h) sum = __dadd_rn(sum, v[h]);
+      const double avg = __ddiv_rn(sum, static_cast<double>(ns));
+      const unsigned long long la = dbits(fabs(avg));
+      for (int h = 0; h < ns; ++h) {
+        const unsigned long long ch = dbits(fabs(avg - v[h]));
+        a.P[off[h]] = avg;
+        if (use_smem) {
+          atomicMax(s_change + ids[h], ch);
+          atomicMax(s_linf + ids[h], la);
+        } else {
+          atomicMax(a.change + ids[h], ch);
+          atomicMax(a.linf_sh + ids[h], la);
+        }
+      }
+      // all copies now bit-identical: post-update jumps are exactly zero
+    } else {
+      double mn = v[0], mx = v[0];
+      for (int h = 0; h < ns; ++h) {
+        mn = fmin(mn, v[h]);
+        mx = fmax(mx, v[h]);
+        const unsigned long long lv = dbits(fabs(v[h]));
+        if (use_smem)
+          atomicMax(s_linf + ids[h], lv);
+        else
+          atomicMax(a.linf_sh + ids[h], lv);
+      }
+      const unsigned long long jd = dbits(mx - mn);  // = max over holder pairs |Pa - Pb|
+      if (ns == 2)
+        jss = umax(jss, jd);
+      else
+        jms = umax(jms, jd);
+    }
+  }
+  if (a.mode == 3) return;
+  jss = warp_umax(jss);
+  jms = warp_umax(jms);
+  if ((threadIdx.x & 31) == 0) {
+    if (jss) atomicMax(&a.acc->jump_ss, jss);
+    if (jms) atomicMax(&a.acc->jump_ms, jms);
+  }
+  if (use_smem) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < a.nblocks; i += blockDim.x) {
+      if (s_change[i]) atomicMax(a.change + i, s_change[i]);
+      if (s_linf[i]) atomicMax(a.linf_sh + i, s_linf[i]);
+    }
+  }
+}
+
+// ------------------------------------------------------------------- K5
+__global__ void __launch_bounds__(1024) k_dp(DpArgs a) {
+  __shared__ unsigned long long red[32];
+  unsigned long long dp = 0ull;
+  for (int b = threadIdx.x; b < a.nblocks; b += blockDim.x) {
+    const unsigned long long li = umax(a.linf_int[b], a.linf_sh[b]);
+    const double lin = __longlong_as_double(static_cast<long long>(li));
+    const double ch = __longlong_as_double(static_cast<long long>(a.change[b]));
+    const double r = ch / (lin > 1.0 ? lin : 1.0);  // solver.cpp:404-405
+    dp = umax(dp, dbits(r));
+    a.change[b] = 0ull;
+    a.linf_sh[b] = 0ull;
+  }
+  dp = block_umax(dp, red);
+  if (threadIdx.x == 0) {
+    const double dpv = __longlong_as_double(static_cast<long long>(dp));
+    const double js = __longlong_as_double(static_cast<long long>(a.acc->jump_ss));
+    const double jm = __longlong_as_double(static_cast<long long>(a.acc->jump_ms));
+    a.epoch_out[0] = dpv;
+    a.epoch_out[1] = js;
+    a.epoch_out[2] = jm;
+    if (a.host_mirror) {
+      a.host_mirror[0] = dpv;
+      a.host_mirror[1] = js;
+      a.host_mirror[2] = jm;
+    }
+    a.acc->jump_ss = 0ull;
+    a.acc->jump_ms = 0ull;
+  }
+}
+
+// ------------------------------------------------------------------- K6
+__global__ void __launch_bounds__(256) k_assemble(AssembleArgs a) {
+  std::int64_t total = 1;
+  for (int k = 0; k < a.D; ++k) total *= a.N[k];
+  const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+  for (std::int64_t g = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < total; g += stride) {
+    std::int64_t r = g, idx[3] = {0, 0, 0};
+    for (int k = a.D - 1; k >= 0; --k) {
+      idx[k] = r % a.N[k];
+      r /= a.N[k];
+    }
+    int id = 0;
+    std::int64_t o = 0;
+    for (int k = 0; k < a.D; ++k) {
+      const int c = a.own_coord[a.oc_off[k] + idx[k]];
+      id = id * a.B[k] + c;
+      const AxisProb& pk = a.probs[a.axbase[k] + c];
+      o = o * pk.n + (idx[k] - pk.col_lo);
+    }
+    a.lattice[g] = a.P[a.poff[id] + o];
+  }
+}
+
+// ------------------------------------------------------------------- K7
+constexpr int kDecodeThreads = 256;
+
+template <int P>
+__global__ void __launch_bounds__(kDecodeThreads) k_decode(DecodeArgs a) {
+  extern __shared__ double sm[];
+  __shared__ double s_red[64];
+  std::int64_t t = blockIdx.x;
+  std::int64_t tc[3];
+  tc[2] = t % a.ntiles[2];
+  t /= a.ntiles[2];
+  tc[1] = t % a.ntiles[1];
+  tc[0] = t / a.ntiles[1];
+  std::int64_t o[3];
+  int e[3], base[3], w[3];
+  for (int k = 0; k < 3; ++k) {
+    o[k] = tc[k] * a.T[k];
+    const std::int64_t rem = a.M[k] - o[k];
+    e[k] = static_cast<int>(rem < a.T[k] ? rem : a.T[k]);
+    base[k] = a.g0[k][o[k]];
+    w[k] = a.g0[k][o[k] + e[k] - 1] + a.pk[k] + 1 - base[k];
+  }
+  const int T1 = a.T[1], T2 = a.T[2];
+  double* pbox = sm;                               // w0*w1*w2
+  double* s1 = pbox + a.W[0] * a.W[1] * a.W[2];    // w0*w1*T2
+  double* s2 = s1 + a.W[0] * a.W[1] * T2;          // w0*T1*T2
+  const int tid = threadIdx.x;
+  // stage 0: control box (global lattice, L2 resident)
+  for (int i = tid; i < w[0] * w[1] * w[2]; i += kDecodeThreads) {
+    const int c2 = i % w[2], c01 = i / w[2], c1 = c01 % w[1], c0 = c01 / w[1];
+    const std::int64_t i0 = base[0] + c0, i1 = base[1] + c1, i2 = base[2] + c2;
+    // windowed lattices (decode.hpp col_offset): clipped basis entries are zero
+    const bool in = i0 >= 0 && i0 < a.N[0] && i1 >= 0 && i1 < a.N[1] && i2 >= 0 && i2 < a.N[2];
+    pbox[i] = in ? a.lattice[(i0 * a.N[1] + i1) * a.N[2] + i2] : 0.0;
+  }
+  __syncthreads();
+  const int sv0 = a.pk[0] + 1, sv1 = a.pk[1] + 1, sv2 = a.pk[2] + 1;
+  // stage 1: contract the contiguous axis
+  for (int i = tid; i < w[0] * w[1] * e[2]; i += kDecodeThreads) {
+    const int x = i % e[2], c01 = i / e[2];
+    const std::int64_t gx = o[2] + x;
+    const int g = a.g0[2][gx] - base[2];
+    const double* vr = a.vals[2] + gx * sv2;
+    const double* pr = pbox + c01 * w[2] + g;
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k <= P; ++k)
+      if (k <= a.pk[2]) s = fma(vr[k], pr[k], s);
+    s1[c01 * T2 + x] = s;
+  }
+  __syncthreads();
+  // stage 2: middle axis
+  for (int i = tid; i < w[0] * e[1] * e[2]; i += kDecodeThreads) {
+    const int x = i % e[2], r = i / e[2], y = r % e[1], c0 = r / e[1];
+    const std::int64_t gy = o[1] + y;
+    const int g = a.g0[1][gy] - base[1];
+    const double* vr = a.vals[1] + gy * sv1;
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k <= P; ++k)
+      if (k <= a.pk[1]) s = fma(vr[k], s1[(c0 * w[1] + g + k) * T2 + x], s);
+    s2[(c0 * T1 + y) * T2 + x] = s;
+  }
+  __syncthreads();
+  // stage 3: leading axis + error + reductions
+  double l2 = 0.0, li = 0.0;
+  for (int i = tid; i < e[0] * e[1] * e[2]; i += kDecodeThreads) {
+    const int x = i % e[2], r = i / e[2], y = r % e[1], z = r / e[1];
+    const std::int64_t gz = o[0] + z;
+    const int g = a.g0[0][gz] - base[0];
+    const double* vr = a.vals[0] + gz * sv0;
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k <= P; ++k)
+      if (k <= a.pk[0]) s = fma(vr[k], s2[((g + k) * T1 + y) * T2 + x], s);
+    const std::int64_t gi = ((o[0] + z) * a.M[1] + o[1] + y) * a.M[2] + o[2] + x;
+    if (a.field) {
+      const double err = a.field[gi] - s;
+      if (a.out) a.out[gi] = err;
+      l2 = fma(err, err, l2);
+      li = fmax(li, fabs(err));
+    } else if (a.out) {
+      a.out[gi] = s;
+    }
+  }
+  if (!a.partial) return;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    l2 += __shfl_xor_sync(kFull, l2, off);
+    li = fmax(li, __shfl_xor_sync(kFull, li, off));
+  }
+  const int wid = tid >> 5;
+  if ((tid & 31) == 0) {
+    s_red[wid] = l2;
+    s_red[32 + wid] = li;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double sl = 0.0, sm2 = 0.0;
+    for (int ww = 0; ww < kDecodeThreads / 32; ++ww) {
+      sl += s_red[ww];
+      sm2 = fmax(sm2, s_red[32 + ww]);
+    }
+    a.partial[2 * blockIdx.x] = sl;
+    a.partial[2 * blockIdx.x + 1] = sm2;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_reduce_partials(const double* p, std::int64_t n, double* out) {
+  __shared__ double s_l2[1024], s_li[1024];
+  double l2 = 0.0, li = 0.0;
+  for (std::int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    l2 += p[2 * i];
+    li = fmax(li, p[2 * i + 1]);
+  }
+  s_l2[threadIdx.x] = l2;
+  s_li[threadIdx.x] = li;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      s_l2[threadIdx.x] += s_l2[threadIdx.x + s];
+      s_li[threadIdx.x] = fmax(s_li[threadIdx.x], s_li[threadIdx.x + s]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out[0] = s_l2[0];
+    out[1] = s_li[0];
+  }
+}
+
+// Degree dispatch: instantiate the templated kernels for p = 1..kMaxDegree.
+template <template <int> class F, class... Args>
+int dispatch_degree(int p, Args&&... args) {
+  switch (p) {
+    case 1: return F<1>::run(args...);
+    case 2: return F<2>::run(args...);
+    case 3: return F<3>::run(args...);
+    case 4: return F<4>::run(args...);
+    case 5: return F<5>::run(args...);
+    case 6: return F<6>::run(args...);
+    case 7: return F<7>::run(args...);
+    case 8: return F<8>::run(args...);
+    case 9: return F<9>::run(args...);
+    default: return -1;
+  }
+}
+
+template <int P>
+struct RowsLaunch {
+  static int run(const RowsArgs& a, cudaStream_t s) {
+    if (a.nprobs == 0 || a.max_m == 0) return 0;
+    dim3 grid((a.max_m + 255) / 256, a.nprobs);
+    k_basis_rows<P><<<grid, 256, 0, s>>>(a);
+    return 1;
+  }
+};
+
+template <int P>
+struct CholLaunch {
+  static int run(const CholArgs& a, cudaStream_t s) {
+    if (a.nfactor == 0) return 0;
+    const size_t smem = static_cast<size_t>(a.max_n) * (P + 1) * sizeof(double);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_gram_chol<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k_gram_chol<P><<<a.nfactor, 256, smem, s>>>(a);
+    return 1;
+  }
+};
+
+template <int P>
+struct FitLaunch {
+  static int run(const FitArgs& a, cudaStream_t s) {
+    int launches = 0;
+    for (int d = 0; d + 1 < a.D; ++d) {
+      dim3 grid((a.max_lines_strided[d] + kStridedThreads - 1) / kStridedThreads, a.nblocks);
+      k_fit_strided<P><<<grid, kStridedThreads, 0, s>>>(a, d);
+      ++launches;
+    }
+    const size_t smem = (static_cast<size_t>(kLastThreads) * (kLastCols + 1) + kLastCols * (P + 1)) * sizeof(double) +
+                        kLastCols * sizeof(int);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_fit_last<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    dim3 grid((a.max_lines_last + kLastThreads - 1) / kLastThreads, a.nblocks);
+    k_fit_last<P><<<grid, kLastThreads, smem, s>>>(a);
+    return launches + 1;
+  }
+};
+
+template <int P>
+struct DecodeLaunch {
+  static int run(const DecodeArgs& a, cudaStream_t s) {
+    const std::int64_t tiles = a.ntiles[0] * a.ntiles[1] * a.ntiles[2];
+    const size_t smem = (static_cast<size_t>(a.W[0]) * a.W[1] * a.W[2] + static_cast<size_t>(a.W[0]) * a.W[1] * a.T[2] +
+                         static_cast<size_t>(a.W[0]) * a.T[1] * a.T[2]) * sizeof(double);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_decode<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k_decode<P><<<static_cast<unsigned>(tiles), kDecodeThreads, smem, s>>>(a);
+    return 1;
+  }
+};
+
+}  // namespace
+
+int launch_basis_rows(int degree, const RowsArgs& a, cudaStream_t s) {
+  return dispatch_degree<RowsLaunch>(degree, a, s);
+}
+int launch_gram_chol(int degree, const CholArgs& a, cudaStream_t s) {
+  return dispatch_degree<CholLaunch>(degree, a, s);
+}
+int launch_fit(int degree, const FitArgs& a, cudaStream_t s) { return dispatch_degree<FitLaunch>(degree, a, s); }
+int launch_decode(int degree, const DecodeArgs& a, cudaStream_t s) {
+  return dispatch_degree<DecodeLaunch>(degree, a, s);
+}
+
+int launch_epoch(const EpochArgs& a, cudaStream_t s) {
+  if (a.total == 0) return 0;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  std::int64_t want = (a.total + kEpochThreads - 1) / kEpochThreads;
+  const std::int64_t cap = static_cast<std::int64_t>(sms) * 4;
+  const unsigned grid = static_cast<unsigned>(want < cap ? want : cap);
+  k_epoch<<<grid, kEpochThreads, 0, s>>>(a);
+  return 1;
+}
+
+int launch_dp(const DpArgs& a, cudaStream_t s) {
+  k_dp<<<1, 1024, 0, s>>>(a);
+  return 1;
+}
+
+int launch_assemble(const AssembleArgs& a, cudaStream_t s) {
+  std::int64_t total = 1;
+  for (int k = 0; k < a.D; ++k) total *= a.N[k];
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  std::int64_t want = (total + 255) / 256;
+  const std::int64_t cap = static_cast<std::int64_t>(sms) * 8;
+  k_assemble<<<static_cast<unsigned>(want < cap ? want : cap), 256, 0, s>>>(a);
+  return 1;
+}
+
+int launch_reduce_partials(const double* partial, std::int64_t n, double* out2, cudaStream_t s) {
+  k_reduce_partials<<<1, 1024, 0, s>>>(partial, n, out2);
+  return 1;
+}
+
+}  // namespace mfb

@@ -1,0 +1,144 @@
+// Kernel launch interface of the B200 MFA encode path (implemented in
+// kernels.cu).  Each launcher returns the number of kernels it launched.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "dev.cuh"
+
+namespace mfb {
+
+// K1: per-row find_span + Cox-de Boor basis + window clip
+// (knots.cpp:83-129, collocation.cpp:83-111).
+struct RowsArgs {
+  const AxisProb* probs;
+  int nprobs;
+  int max_m;
+  const double* knots;
+  const double* params;  // explicit params (AxisProb::M < 0)
+  int* g0;               // local unclipped first column (span - p - col_lo)
+  int* first_col;        // BandedCollocation::first_col
+  int* count;            // BandedCollocation::count
+  double* vals;          // (p+1) per row, clipped entries zero, unclipped positions
+  DevStatus* status;
+};
+int launch_basis_rows(int degree, const RowsArgs& a, cudaStream_t s);
+
+// K2: banded Gram (collocation.cpp:56-67) + banded Cholesky (lsq.cpp:46-55).
+// Writes per column: [1/L(c,c), L(c,c-1..c-p), L(c+1..c+p,c)] (2p+1 doubles).
+struct CholArgs {
+  const AxisProb* probs;
+  const int* prob_ids;  // problems to factor
+  int nfactor;
+  int max_n;
+  const int* g0;
+  const double* vals;
+  double* ltab;
+  DevStatus* status;
+};
+int launch_gram_chol(int degree, const CholArgs& a, cudaStream_t s);
+
+// K3: per-axis fit passes (lsq.cpp:57-61 fused: R^T contraction in row order
+// + forward substitution + back substitution).
+struct FitArgs {
+  int D;
+  std::int64_t fs[3];  // field strides
+  const double* field;
+  const BlockDev* blocks;
+  int nblocks;
+  const AxisProb* probs;
+  const int* g0;
+  const double* vals;
+  const double* ltab;
+  double* t1;
+  double* t2;
+  double* P;
+  double* Y;                         // last-axis forward scratch (|P|)
+  unsigned long long* linf_int;      // per block: max |P| over non-shared entries
+  const unsigned char* shared_flag;  // per dim concatenated: 1 if the global index is shared
+  std::int64_t sflag_off[3];
+  int max_lines_strided[3];          // per axis: max lines over blocks
+  int max_lines_last;
+};
+int launch_fit(int degree, const FitArgs& a, cudaStream_t s);
+
+// K4: one averaging epoch over every shared control (solver.cpp:112-164 with
+// the runtime.cpp:123-158 Jacobi snapshot), jump residuals (solver.cpp:
+// 166-193) and the dp numerator/denominator pieces (solver.cpp:402-405).
+struct EpochArgs {
+  int D;
+  int nblocks;
+  int B[3];
+  std::int64_t N[3];
+  const int2* hr;       // holder coordinate ranges, concatenated per dim
+  std::int64_t hr_off[3];
+  const int* slist;     // shared indices per dim, concatenated
+  const int* clist;     // non-shared indices per dim, concatenated
+  std::int64_t s_off[3], c_off[3];
+  std::int64_t nS[3], nC[3];
+  std::int64_t piece[3];  // dof count of each piece
+  std::int64_t total;
+  const AxisProb* probs;
+  int axbase[3];
+  const std::int64_t* poff;
+  double* P;
+  int mode;  // 0 measure only, 1 average n_s == 2 only, 2 average all
+  unsigned long long* change;
+  unsigned long long* linf_sh;
+  EpochAcc* acc;
+  // final per-pair jumps (mode 3): pair slot table nblocks*27, per-pair ss/ms
+  const int* pair_slot;
+  unsigned long long* pair_jumps;
+};
+int launch_epoch(const EpochArgs& a, cudaStream_t s);
+
+// K5: dp = max_b change_b / max(1, ||P_b||_inf) and epoch bookkeeping.
+struct DpArgs {
+  int nblocks;
+  unsigned long long* change;
+  unsigned long long* linf_sh;
+  const unsigned long long* linf_int;
+  EpochAcc* acc;
+  double* epoch_out;  // 3 doubles: dp, jump_ss, jump_ms
+  double* host_mirror;  // optional pinned-mapped copy (nullable)
+};
+int launch_dp(const DpArgs& a, cudaStream_t s);
+
+// K6: assemble_owned (solver.cpp:281-294).
+struct AssembleArgs {
+  int D;
+  int B[3];
+  std::int64_t N[3];
+  const int* own_coord;  // per dim concatenated: owning block coordinate of each control index
+  std::int64_t oc_off[3];
+  const AxisProb* probs;
+  int axbase[3];
+  const std::int64_t* poff;
+  const double* P;
+  double* lattice;
+};
+int launch_assemble(const AssembleArgs& a, cudaStream_t s);
+
+// K7: decode the global lattice over the input grid (decode.cpp:83-97 as
+// called by block_error_slab, solver.cpp:298-328), error field, L2^2/Linf.
+struct DecodeArgs {
+  int D;
+  std::int64_t M[3];  // output (input-grid) extents, padded to 3 with leading 1s
+  std::int64_t N[3];  // lattice extents, padded
+  int T[3];           // tile extents
+  std::int64_t ntiles[3];
+  int W[3];           // smem control-box extents bound
+  const int* g0[3];   // global rows per (padded) dim
+  const double* vals[3];
+  int pk[3];          // per padded dim: degree (0 for padding dims)
+  const double* lattice;
+  const double* field;   // nullable -> pure decode (no error)
+  double* out;           // error field (field != null) or decoded values; nullable
+  double* partial;       // per tile {l2sq, linf}
+};
+int launch_decode(int degree, const DecodeArgs& a, cudaStream_t s);
+// K7b: deterministic reduction of the tile partials.
+int launch_reduce_partials(const double* partial, std::int64_t n, double* out2, cudaStream_t s);
+
+}  // namespace mfb

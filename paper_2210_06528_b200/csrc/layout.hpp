@@ -1,0 +1,75 @@
+// Host-side decomposition metadata for the B200 MFA encode path.
+//
+// Restates the reference's partition() (proj/core/src/layout.cpp:217-342),
+// plan_dim (:81-121), SharedDofMap (:125-203) and shared_dof_box (:205-215).
+// Every integer here is bit-exact with the reference; knots are generated with
+// the same floating-point expressions (knots.cpp:58-79, layout.cpp:94-101).
+// This is plan-time host work (the reference also runs partition() outside
+// solve()); everything inside solve() runs on the GPU.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace mfb {
+
+// BlockDim field order (layout.hpp:47-57)
+enum BlockDimField : int {
+  SPAN_LO, SPAN_HI, DELTA_LO, DELTA_HI, OVL_LO, OVL_HI, LSPAN_LO, LSPAN_HI,
+  DOF_LO, DOF_HI, OWN_LO, OWN_HI, IN_LO, IN_HI, OWNIN_LO, OWNIN_HI, BD_N
+};
+
+struct SingularFit : std::runtime_error {
+  int dim;
+  std::int64_t span;
+  SingularFit(int d, std::int64_t s, const std::string& w) : std::runtime_error(w), dim(d), span(s) {}
+};
+
+struct Decomp {
+  int rank = 0, degree = 0;
+  bool clamp = false;
+  std::int64_t overlap = 0;
+  std::array<std::int64_t, 3> grid{1, 1, 1};
+  std::array<int, 3> blocks{1, 1, 1};
+  std::array<std::int64_t, 3> n_ctrl{1, 1, 1};
+  std::array<std::int64_t, 3> spans{0, 0, 0};          // T: nonempty span count
+  std::vector<std::array<double, 2>> bounds;
+  std::array<std::vector<double>, 3> knots;
+  std::array<std::vector<int>, 3> span_knot;
+  int nblocks = 0;
+  std::vector<std::array<int, 3>> coords;               // per block
+  std::vector<std::int64_t> bd;                         // nblocks*rank*BD_N
+  std::array<std::vector<std::array<int, 2>>, 3> holder;  // per dim per ctrl index
+  std::vector<std::vector<int>> neighbors;
+  bool any_shared = false;
+
+  std::int64_t& at(int b, int k, int f) { return bd[(static_cast<std::size_t>(b) * rank + k) * BD_N + f]; }
+  std::int64_t at(int b, int k, int f) const { return bd[(static_cast<std::size_t>(b) * rank + k) * BD_N + f]; }
+  int block_id(const int* c) const {
+    int id = 0;
+    for (int k = 0; k < rank; ++k) id = id * blocks[k] + c[k];
+    return id;
+  }
+  // Per-dim block coordinate -> BlockDim of any block with that coordinate
+  // (ranges along dim k depend only on the coordinate along k).
+  std::int64_t dim_field(int k, int c, int f) const;
+  bool shared_box(int a, int b, std::array<std::array<std::int64_t, 2>, 3>& box) const;
+  std::int64_t total_inputs() const;
+  std::int64_t total_ctrl() const;
+};
+
+// layout.cpp:217-342.  Throws std::invalid_argument like the reference.
+Decomp partition(int rank, const std::int64_t* grid, const double* bounds, const int* blocks, int degree,
+                 const std::int64_t* nctrl_per_block, std::int64_t overlap, bool clamp_interfaces);
+
+// knots.cpp:48-81 (uniform clamped/floating knot vector)
+std::vector<double> make_knot_vector(int degree, int basis_count, double a, double b, bool clamp_left,
+                                     bool clamp_right);
+
+// runtime.cpp:160-171
+std::vector<std::int64_t> exchange_volume(const Decomp& d);
+
+}  // namespace mfb
