@@ -1,0 +1,347 @@
+#!/usr/bin/env python
+"""bench.py — converged domain-decomposed MFA encode throughput on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl reference]
+
+One step = one full solve() of the workload (setup: basis rows + Gram/
+Cholesky; decoupled local fits; exchange/averaging epochs until dp < 1e-10 or
+20 iterations; final jumps; owned-slab assembly; decode + error field +
+L2/Linf) — everything the reference's mfadd::solve does, nothing skipped.
+
+`value`: field already resident in HBM; device time per step (CUDA events on
+the launching stream, barrier + synchronize on both sides, max over ranks).
+`e2e`: the C-ABI host call mfadd_solve_host: pinned host field -> H2D ->
+solve -> D2H of the global lattice and the global_error field, every step.
+The input (8192^2 fp64 = 537 MB for C5) is larger than the 126 MB L2, so no
+explicit flush is needed between timed steps.
+
+--impl reference: the reference's own CPU implementation (oracle/_ref, built
+from the unmodified /root/reference sources) on all host threads, same config,
+each step one full solve.  Under torchrun only rank 0 runs it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "input pts encoded/s (converged Schwarz)"
+UNIT = "pts/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def workload_desc(cfg):
+    return (f"{cfg.name}: {cfg.generator} {'x'.join(map(str, cfg.grid))} fp64, {'x'.join(map(str, cfg.blocks))} "
+            f"blocks, p={cfg.degree}, {'x'.join(map(str, cfg.nctrl))} ctrl/block, overlap {cfg.overlap}, "
+            f"tol {cfg.tolerance:g}, max {cfg.max_iters} iters")
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.lines = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(kernel):
+    """Per-launch dram bytes of `kernel` from the committed ncu --set full summary, or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(kernel)
+    except Exception:
+        return None
+
+
+def kernel_bytes(cfg, dec, ab):
+    """Algorithmic bytes per launch of each kernel."""
+    import numpy as np
+    bd = dec.block_dims_array()
+    D = dec.rank
+    m = bd[:, :, 13] - bd[:, :, 12]
+    n = bd[:, :, 9] - bd[:, :, 8]
+    out = {}
+    if D >= 2:
+        t1 = int(sum(n[b, 0] * np.prod(m[b, 1:]) for b in range(dec.nblocks)))
+        out["fit_axis0"] = 8 * (ab["q_loc"] + t1)
+        if D == 3:
+            t2 = int(sum(n[b, 0] * n[b, 1] * m[b, 2] for b in range(dec.nblocks)))
+            out["fit_axis1"] = 8 * (t1 + t2)
+            out["fit_last"] = 8 * (t2 + ab["p_held"])
+        else:
+            out["fit_last"] = 8 * (t1 + ab["p_held"])
+    else:
+        out["fit_last"] = 8 * (ab["q_loc"] + ab["p_held"])
+    out["epoch"] = 16 * ab["ns_total"]
+    out["decode"] = 8 * (2 * ab["points"] + int(np.prod(dec.n_ctrl)))  # read Q + write error + read lattice
+    out["assemble"] = 16 * int(np.prod(dec.n_ctrl))
+    return out
+
+
+def run_reference(args, cfg, rank):
+    from oracle import ref
+    if rank != 0:
+        return
+    if not ref.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libmfadd_ref.so not built"}))
+        return
+    from paper_2210_06528_b200 import workloads as W
+    values = W.make_field_numpy(cfg)
+    dec = ref.RefDecomposition(cfg.grid, cfg.blocks, cfg.degree, cfg.nctrl, cfg.overlap,
+                               bounds=[list(b) for b in cfg.bounds])
+    cores = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        ref.solve(dec, values, cfg.max_iters, cfg.tolerance, workers=cores, log_errors=False, want_blocks=False)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        ref.solve(dec, values, cfg.max_iters, cfg.tolerance, workers=cores, log_errors=False, want_blocks=False)
+        times.append(time.perf_counter() - t0)
+    t = sum(times) / len(times)
+    v = cfg.points / t
+    sample = f"full {cfg.name} solve per step ({cfg.points} pts), log_errors=false, workers={cores}"
+    print(json.dumps({
+        "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, BASELINE shapes)", "impl": "reference",
+        "config": {"workload": workload_desc(cfg), "parallelism": f"{cores} host threads (reference thread pool)"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def cpu_baseline(cfg, values_host):
+    """The reference (oracle/_ref) on this host's cores, one bounded full solve."""
+    from oracle import ref
+    cores = os.cpu_count() or 1
+    if ref.available():
+        dec = ref.RefDecomposition(cfg.grid, cfg.blocks, cfg.degree, cfg.nctrl, cfg.overlap,
+                                   bounds=[list(b) for b in cfg.bounds])
+        t0 = time.perf_counter()
+        r = ref.solve(dec, values_host, cfg.max_iters, cfg.tolerance, workers=cores, log_errors=False,
+                      want_blocks=False)
+        t = time.perf_counter() - t0
+        return {"value": cfg.points / t, "unit": UNIT, "cores": cores, "kind": "reference",
+                "sample": f"1 full {cfg.name} solve ({cfg.points} pts) in {t:.2f} s, workers={cores}"}, r
+    from oracle import orc
+    dec = orc.Decomposition(cfg.grid, cfg.blocks, cfg.degree, cfg.nctrl, cfg.overlap)
+    t0 = time.perf_counter()
+    r = orc.solve(dec, values_host, cfg.max_iters, cfg.tolerance)
+    t = time.perf_counter() - t0
+    return {"value": cfg.points / t, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"1 full {cfg.name} solve ({cfg.points} pts) in {t:.2f} s, C restatement"}, r
+
+
+def main():
+    args = parse()
+    from paper_2210_06528_b200 import workloads as W
+    cfg = W.CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, cfg, rank)
+        return
+
+    import numpy as np
+    import torch
+    import paper_2210_06528_b200 as m
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    field = W.make_field_torch(cfg)
+    torch.cuda.synchronize()
+    dec = m.partition(cfg.grid, cfg.bounds, cfg.blocks, cfg.degree, cfg.nctrl, cfg.overlap)
+    stream = torch.cuda.current_stream()
+    ctx = m.Context(local, stream=stream.cuda_stream)
+    scfg = m.SolverConfig(max_outer_iterations=cfg.max_iters, tolerance=cfg.tolerance, log_errors=False,
+                          store_error=True)
+    solver = m.Solver(dec, scfg, ctx)
+    for _ in range(max(3, args.warmup)):
+        solver.run(field, on_device=True)
+    res = solver.result(want_blocks=False, want_error=False)
+    epochs_exchanged = len(res.epochs) - 1
+
+    # ---------------- timed region (device-resident input)
+    solver.set_profiling(True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    launches = 0
+    for _ in range(args.steps):
+        solver.run(field, on_device=True)
+        launches += solver.last_launches()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    ktimes = solver.kernel_times()
+    solver.set_profiling(False)
+    if dist:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = cfg.points * world / (ms * 1e-3)
+
+    # ---------------- e2e through the C-ABI host call
+    e2e = None
+    if not args.no_e2e:
+        host_field = torch.empty(cfg.grid, dtype=torch.float64, pin_memory=True)
+        host_field.copy_(field.cpu())
+        out_c = torch.empty(tuple(dec.n_ctrl), dtype=torch.float64, pin_memory=True)
+        out_e = torch.empty(cfg.grid, dtype=torch.float64, pin_memory=True)
+        solver.run_host(host_field, out_c, out_e)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(args.steps):
+            solver.run_host(host_field, out_c, out_e)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        ems = a0.elapsed_time(a1) / args.steps
+        if dist:
+            t = torch.tensor([ems], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": cfg.points * world / (ems * 1e-3), "unit": UNIT, "ms_per_step": ems,
+               "h2d_bytes_per_step": 8 * cfg.points,
+               "d2h_bytes_per_step": 8 * (int(np.prod(dec.n_ctrl)) + cfg.points)}
+
+    # ---------------- roofline of the dominant kernel (live CUDA events)
+    ab = W.algorithmic_bytes(cfg, dec, epochs_exchanged, store_error=True)
+    kb = kernel_bytes(cfg, dec, ab)
+    per = {}
+    for name, t in ktimes:
+        per.setdefault(name, []).append(t)
+    shares = {k: sum(v) for k, v in per.items()}
+    tot = sum(shares.values()) or 1.0
+    dom = max((k for k in shares if k in kb), key=lambda k: shares[k])
+    launches_dom = len(per[dom])
+    avg_ms = shares[dom] / launches_dom
+    peak, peak_src = measured_peaks()
+    achieved = kb[dom] / (avg_ms * 1e-3) / 1e9
+    roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": ncu_traffic(dom), "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": kb[dom], "avg_launch_ms": avg_ms,
+            "step_share": shares[dom] / tot,
+            "step_algorithmic_bytes": ab["bytes"],
+            "step_frac": ab["bytes"] / (ms * 1e-3) / 1e9 / peak}
+    kern = {k: {"ms_per_step": shares[k] / args.steps, "launches_per_step": len(per[k]) / args.steps,
+                **({"GBps": kb[k] * len(per[k]) / (shares[k] * 1e-3) / 1e9} if k in kb else {})}
+            for k in shares}
+
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator on device, BASELINE shapes)",
+        "config": {"workload": workload_desc(cfg), "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                   "l2_flush": "input 8*prod(M) bytes > 126 MB L2 (no explicit flush)",
+                   "constraint_iterations": res.constraint_iterations, "epochs": len(res.epochs),
+                   "store_error": True, "log_errors": False},
+        "gpu_launches": launches,
+        "clocks": clk,
+        "roofline": roof,
+        "kernels": kern,
+    }
+    if e2e:
+        out["e2e"] = e2e
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        host = field.cpu().numpy()
+        cb, r = cpu_baseline(cfg, host)
+        ours = solver.result(want_blocks=False, want_error=False)
+        scale = max(1.0, float(np.abs(r.controls).max()))
+        cb["parity_max_abs_dP_rel"] = float(np.abs(ours.model.controls - r.controls).max()) / scale
+        cb["parity_iters_equal"] = ours.constraint_iterations == r.constraint_iterations
+        out["cpu_baseline"] = cb
+    if rank == 0:
+        print(json.dumps(out))
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

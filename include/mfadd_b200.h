@@ -137,6 +137,12 @@ int mfadd_solver_block_errors(const mfadd_solver* s, int epoch, double* out2);
 const double* mfadd_solver_device_controls(const mfadd_solver* s);
 /* Kernel launches issued by the last mfadd_solve (launch accounting). */
 int mfadd_solver_last_launches(const mfadd_solver* s);
+/* Per-kernel CUDA-event timeline (on the launching stream); clears the record
+ * list, which then accumulates over every following solve. */
+int mfadd_solver_set_profiling(mfadd_solver* s, int on);
+/* (name, milliseconds) of every recorded kernel since set_profiling, in order;
+ * names: cap * name_len chars (nullable).  Returns the record count. */
+int mfadd_solver_kernel_times(const mfadd_solver* s, char* names, int name_len, double* ms, int cap);
 
 /* ---------------------------------------------------------- fine-grained
  * Unit-parity sub-boundaries.  All buffers are HOST memory;

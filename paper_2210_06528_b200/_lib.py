@@ -71,6 +71,8 @@ _SIGS = {
     "mfadd_solver_block_errors": (C.c_int, [C.c_void_p, C.c_int, c_dp]),
     "mfadd_solver_device_controls": (C.c_void_p, [C.c_void_p]),
     "mfadd_solver_last_launches": (C.c_int, [C.c_void_p]),
+    "mfadd_solver_set_profiling": (C.c_int, [C.c_void_p, C.c_int]),
+    "mfadd_solver_kernel_times": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int, c_dp, C.c_int]),
     "mfadd_collocation": (C.c_int, [C.c_void_p, c_dp, C.c_int, C.c_int, c_dp, C.c_int64, C.c_int64, C.c_int64,
                                     c_lp, c_ip, c_dp]),
     "mfadd_fit_unconstrained": (C.c_int, [C.c_void_p, C.c_int, C.c_int, c_dp, c_lp, c_dp, c_lp, c_lp, c_lp, c_dp,

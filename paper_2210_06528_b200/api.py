@@ -614,6 +614,18 @@ class Solver:
             C.byref(self.summary)))
         return self.summary
 
+    def set_profiling(self, on: bool = True):
+        _check(L.load().mfadd_solver_set_profiling(self._h, int(on)))
+
+    def kernel_times(self):
+        """[(name, ms)] per kernel launch of the last solve (CUDA events on the launching stream)."""
+        cap, nl = 4096, 32
+        names = C.create_string_buffer(cap * nl)
+        ms = np.zeros(cap)
+        n = L.load().mfadd_solver_kernel_times(self._h, names, nl, _dp(ms), cap)
+        raw = names.raw
+        return [(raw[i * nl:(i + 1) * nl].split(b"\0")[0].decode(), float(ms[i])) for i in range(min(n, cap))]
+
     def last_launches(self) -> int:
         return L.load().mfadd_solver_last_launches(self._h)
 

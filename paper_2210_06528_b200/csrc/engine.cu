@@ -158,6 +158,43 @@ struct ContextScope {  // make the context's device current for the call
   }
 };
 
+// Optional per-kernel CUDA-event timeline (bench roofline / phase evidence).
+struct Timeline {
+  struct Rec {
+    std::string name;
+    cudaEvent_t a = nullptr, b = nullptr;
+  };
+  bool on = false;
+  std::vector<Rec> recs;
+  std::size_t used = 0;
+  cudaStream_t st = nullptr;
+  ~Timeline() {
+    for (auto& r : recs) {
+      if (r.a) cudaEventDestroy(r.a);
+      if (r.b) cudaEventDestroy(r.b);
+    }
+  }
+  void reset(cudaStream_t s) {
+    used = 0;
+    st = s;
+  }
+  void begin(const char* name) {
+    if (!on) return;
+    if (used == recs.size()) {
+      recs.emplace_back();
+      CK(cudaEventCreate(&recs.back().a));
+      CK(cudaEventCreate(&recs.back().b));
+    }
+    recs[used].name = name;
+    CK(cudaEventRecord(recs[used].a, st));
+  }
+  void end() {
+    if (!on) return;
+    CK(cudaEventRecord(recs[used].b, st));
+    ++used;
+  }
+};
+
 // Device tables for a batch of local problems sharing one degree: the fit
 // machinery of both solve() and fit_unconstrained().
 struct Workload {
@@ -248,19 +285,27 @@ struct Workload {
   }
 
   // K1 + K2
-  int setup(mfadd_context* ctx) {
+  int setup(mfadd_context* ctx, Timeline* tl = nullptr) {
+    Timeline dummy;
+    if (!tl) tl = &dummy;
     mfb::RowsArgs ra{d_probs.p, static_cast<int>(probs.size()), max_m, knots.p, params.p, g0.p, first_col.p,
                      count.p, vals.p, ctx->d_status};
+    tl->begin("basis_rows");
     int l = mfb::launch_basis_rows(p, ra, ctx->stream);
+    tl->end();
     mfb::CholArgs ca{d_probs.p, d_factor.p, static_cast<int>(factor_ids.size()), max_n_factor, g0.p, vals.p, ltab.p,
                      ctx->d_status};
+    tl->begin("gram_chol");
     l += mfb::launch_gram_chol(p, ca, ctx->stream);
+    tl->end();
     CK(cudaGetLastError());
     return l;
   }
 
   // K3
-  int fit(mfadd_context* ctx, const double* field) {
+  int fit(mfadd_context* ctx, const double* field, Timeline* tl = nullptr) {
+    Timeline dummy;
+    if (!tl) tl = &dummy;
     CK(cudaMemsetAsync(linf_int.p, 0, blocks.size() * sizeof(unsigned long long), ctx->stream));
     mfb::FitArgs fa{};
     fa.D = D;
@@ -283,7 +328,16 @@ struct Workload {
       fa.max_lines_strided[k] = max_lines_strided[k];
     }
     fa.max_lines_last = max_lines_last;
-    const int l = mfb::launch_fit(p, fa, ctx->stream);
+    static const char* kNames[2] = {"fit_axis0", "fit_axis1"};
+    int l = 0;
+    for (int d = 0; d + 1 < D; ++d) {
+      tl->begin(kNames[d]);
+      l += mfb::launch_fit_strided(p, fa, d, ctx->stream);
+      tl->end();
+    }
+    tl->begin("fit_last");
+    l += mfb::launch_fit_last(p, fa, ctx->stream);
+    tl->end();
     CK(cudaGetLastError());
     return l;
   }
@@ -394,6 +448,7 @@ struct mfadd_solver {
   mfadd_solve_summary summary{};
   bool have_result = false;
   int last_launches = 0;
+  Timeline tl;
   cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
 
   ~mfadd_solver() {
@@ -736,10 +791,14 @@ mfb::EpochArgs epoch_args(mfadd_solver* s, int mode) {
 
 // One epoch: K4 + K5; returns launches.  Result lands in epoch_out[3*slot].
 int run_epoch(mfadd_solver* s, int mode, int slot) {
+  s->tl.begin("epoch");
   int l = mfb::launch_epoch(epoch_args(s, mode), s->ctx->stream);
+  s->tl.end();
   mfb::DpArgs da{s->dec.nblocks, s->change.p, s->linf_sh.p, s->wl.linf_int.p, s->acc.p, s->epoch_out.p + 3 * slot,
                  nullptr};
+  s->tl.begin("dp");
   l += mfb::launch_dp(da, s->ctx->stream);
+  s->tl.end();
   CK(cudaGetLastError());
   return l;
 }
@@ -758,12 +817,13 @@ void solve_impl(mfadd_solver* s, const double* dfield) {
   int launches = 0;
   s->have_result = false;
   s->epochs.clear();
+  s->tl.st = st;
   CK(cudaEventRecord(s->ev[0], st));
   // ---- setup: basis rows + Gram/Cholesky (solver.cpp:346 make_block_state)
-  launches += wl.setup(ctx);
+  launches += wl.setup(ctx, &s->tl);
   CK(cudaEventRecord(s->ev[1], st));
   // ---- decoupled local fits (solver.cpp:369-373)
-  launches += wl.fit(ctx, dfield);
+  launches += wl.fit(ctx, dfield, &s->tl);
   CK(cudaEventRecord(s->ev[2], st));
   // ---- record_epoch(0, 0.0)
   launches += run_epoch(s, 0, 0);
@@ -796,7 +856,9 @@ void solve_impl(mfadd_solver* s, const double* dfield) {
   // ---- final jumps per neighbour pair (solver.cpp:416)
   if (s->npairs > 0) {
     CK(cudaMemsetAsync(s->pair_jumps.p, 0, s->pair_jumps.n * sizeof(unsigned long long), st));
+    s->tl.begin("pair_jumps");
     launches += mfb::launch_epoch(epoch_args(s, 3), st);
+    s->tl.end();
   }
   // ---- assemble_owned (solver.cpp:418-423)
   mfb::AssembleArgs aa{};
@@ -812,7 +874,9 @@ void solve_impl(mfadd_solver* s, const double* dfield) {
   aa.poff = s->poff.p;
   aa.P = wl.P.p;
   aa.lattice = s->lattice.p;
+  s->tl.begin("assemble");
   launches += mfb::launch_assemble(aa, st);
+  s->tl.end();
   // ---- block_error_slab over every block == global decode (solver.cpp:425-438)
   mfb::DecodeArgs da{};
   const DecodePlan& dp = s->dp;
@@ -837,8 +901,12 @@ void solve_impl(mfadd_solver* s, const double* dfield) {
   da.field = dfield;
   da.out = s->cfg.store_error ? s->error.p : nullptr;
   da.partial = s->partial.p;
+  s->tl.begin("decode");
   launches += mfb::launch_decode(wl.p, da, st);
+  s->tl.end();
+  s->tl.begin("reduce");
   launches += mfb::launch_reduce_partials(s->partial.p, static_cast<std::int64_t>(s->partial.n / 2), s->red2.p, st);
+  s->tl.end();
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(hp + 4, s->red2.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
   std::vector<unsigned long long> pj(s->pair_jumps.n);
@@ -964,6 +1032,27 @@ MFB_API int mfadd_solver_block_errors(const mfadd_solver* s, int epoch, double* 
 }
 
 MFB_API const double* mfadd_solver_device_controls(const mfadd_solver* s) { return s->lattice.p; }
+
+MFB_API int mfadd_solver_set_profiling(mfadd_solver* s, int on) {
+  s->tl.on = on != 0;
+  s->tl.reset(s->ctx->stream);  // records accumulate across solves until the next call
+  return MFADD_OK;
+}
+
+MFB_API int mfadd_solver_kernel_times(const mfadd_solver* s, char* names, int name_len, double* ms, int cap) {
+  const int n = static_cast<int>(s->tl.used);
+  for (int i = 0; i < n && i < cap; ++i) {
+    const auto& r = s->tl.recs[static_cast<std::size_t>(i)];
+    float t = 0.f;
+    cudaEventElapsedTime(&t, r.a, r.b);
+    ms[i] = t;
+    if (names) {
+      std::strncpy(names + static_cast<std::size_t>(i) * name_len, r.name.c_str(), static_cast<std::size_t>(name_len) - 1);
+      names[static_cast<std::size_t>(i) * name_len + name_len - 1] = 0;
+    }
+  }
+  return n;
+}
 MFB_API int mfadd_solver_last_launches(const mfadd_solver* s) { return s->last_launches; }
 
 // ---------------------------------------------------------------- fine-grained

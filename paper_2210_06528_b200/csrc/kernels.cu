@@ -784,20 +784,23 @@ struct CholLaunch {
 };
 
 template <int P>
-struct FitLaunch {
+struct FitStridedLaunch {
+  static int run(const FitArgs& a, int d, cudaStream_t s) {
+    dim3 grid((a.max_lines_strided[d] + kStridedThreads - 1) / kStridedThreads, a.nblocks);
+    k_fit_strided<P><<<grid, kStridedThreads, 0, s>>>(a, d);
+    return 1;
+  }
+};
+
+template <int P>
+struct FitLastLaunch {
   static int run(const FitArgs& a, cudaStream_t s) {
-    int launches = 0;
-    for (int d = 0; d + 1 < a.D; ++d) {
-      dim3 grid((a.max_lines_strided[d] + kStridedThreads - 1) / kStridedThreads, a.nblocks);
-      k_fit_strided<P><<<grid, kStridedThreads, 0, s>>>(a, d);
-      ++launches;
-    }
     const size_t smem = (static_cast<size_t>(kLastThreads) * (kLastCols + 1) + kLastCols * (P + 1)) * sizeof(double) +
                         kLastCols * sizeof(int);
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_fit_last<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     dim3 grid((a.max_lines_last + kLastThreads - 1) / kLastThreads, a.nblocks);
     k_fit_last<P><<<grid, kLastThreads, smem, s>>>(a);
-    return launches + 1;
+    return 1;
   }
 };
 
@@ -821,7 +824,12 @@ int launch_basis_rows(int degree, const RowsArgs& a, cudaStream_t s) {
 int launch_gram_chol(int degree, const CholArgs& a, cudaStream_t s) {
   return dispatch_degree<CholLaunch>(degree, a, s);
 }
-int launch_fit(int degree, const FitArgs& a, cudaStream_t s) { return dispatch_degree<FitLaunch>(degree, a, s); }
+int launch_fit_strided(int degree, const FitArgs& a, int axis, cudaStream_t s) {
+  return dispatch_degree<FitStridedLaunch>(degree, a, axis, s);
+}
+int launch_fit_last(int degree, const FitArgs& a, cudaStream_t s) {
+  return dispatch_degree<FitLastLaunch>(degree, a, s);
+}
 int launch_decode(int degree, const DecodeArgs& a, cudaStream_t s) {
   return dispatch_degree<DecodeLaunch>(degree, a, s);
 }

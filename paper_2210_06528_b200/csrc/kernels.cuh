@@ -61,7 +61,8 @@ struct FitArgs {
   int max_lines_strided[3];          // per axis: max lines over blocks
   int max_lines_last;
 };
-int launch_fit(int degree, const FitArgs& a, cudaStream_t s);
+int launch_fit_strided(int degree, const FitArgs& a, int axis, cudaStream_t s);  // axis < D-1
+int launch_fit_last(int degree, const FitArgs& a, cudaStream_t s);
 
 // K4: one averaging epoch over every shared control (solver.cpp:112-164 with
 // the runtime.cpp:123-158 Jacobi snapshot), jump residuals (solver.cpp:

@@ -149,7 +149,7 @@ def test_fit_windowed_truncated(ctx):
     p = 3
     kv = m.make_knot_vector(p, 40)
     params = [np.arange(300, 700) / 999.0, np.arange(100, 420) / 999.0]
-    wins = [(9, 28), (1, 16)]
+    wins = [(12, 27), (4, 17)]
     q = np.random.default_rng(7).standard_normal((400, 320))
     g = m.fit_unconstrained(m.LocalProblem([kv, kv], params, wins, q), ctx)
     o = orc.fit_unconstrained([kv.knots, kv.knots], p, params, wins, q)
