@@ -898,9 +898,28 @@ int orc_solve(const orc_dec* d, const double* field, int max_iters, double tol, 
           do {
             const int ns = n_s_of(d, idx);
             if (ns < 2) continue;
-            if (iter < 2 && ns > 2) continue;
-            int ids[8];
+            int ids[27];
             holders_of(d, idx, ids);
+            /* solver.cpp:134-141: contributions arrive only from neighbors
+             * (coordinate distance <= 1, runtime.cpp:17-21); every other
+             * holder must have sent, else runtime_error. */
+            int received = 0;
+            for (int h = 0; h < ns; ++h) {
+              if (ids[h] == b) continue;
+              int near = 1;
+              for (int k = 0; k < D; ++k)
+                if (abs(d->coords[ids[h] * D + k] - d->coords[b * D + k]) > 1) near = 0;
+              received += near;
+            }
+            if (received != ns - 1) {
+              for (int b2 = 0; b2 < NB; ++b2) free(snap[b2].data);
+              free(snap);
+              free(change);
+              rc = fail(4, "enforce_constraints: block %d received %d contributions for a control shared by %d blocks",
+                        b, received, ns);
+              goto solve_failed;
+            }
+            if (iter < 2 && ns > 2) continue;
             double sum = 0.0;
             for (int h = 0; h < ns; ++h) sum += *bp_at(d, snap, ids[h], idx);
             const double avg = sum / (double)ns;
@@ -931,6 +950,8 @@ int orc_solve(const orc_dec* d, const double* field, int max_iters, double tol, 
       free(snap);
       free(change);
     }
+  solve_failed:
+    if (rc) goto cleanup;
     /* solver.cpp:416 final jumps */
     int np = 0;
     for (int a = 0; a < NB; ++a) np += d->nbr_off[a + 1] - d->nbr_off[a];
@@ -1003,6 +1024,7 @@ int orc_solve(const orc_dec* d, const double* field, int max_iters, double tol, 
     }
     res->l2 = sqrt(sq);
   }
+cleanup:
   for (int b = 0; b < NB; ++b) {
     for (int k = 0; k < D; ++k) banded_free(&R[b * D + k]);
     free(Q[b].data);

@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmfadd_b200.so")
+# MFADD_DEBUG=1 selects the bounds-checked build (libmfadd_b200_debug.so)
+LIB_PATH = os.path.join(HERE, "libmfadd_b200_debug.so" if os.environ.get("MFADD_DEBUG") else "libmfadd_b200.so")
 
 c_dp = C.POINTER(C.c_double)
 c_lp = C.POINTER(C.c_int64)

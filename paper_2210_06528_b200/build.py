@@ -17,6 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmfadd_b200.so")
+LIB_DEBUG = os.path.join(HERE, "libmfadd_b200_debug.so")  # -DMFB_DEBUG: device-side bounds checks
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -35,19 +36,21 @@ def _stale(out, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
     deps = sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.hpp")) + \
         [os.path.join(ROOT, "include", "mfadd_b200.h")]
-    if not force and not _stale(LIB, deps):
-        return LIB
-    objdir = os.path.join(HERE, "_build")
+    lib = LIB_DEBUG if debug else LIB
+    if not force and not _stale(lib, deps):
+        return lib
+    objdir = os.path.join(HERE, "_build_debug" if debug else "_build")
+    extra = ["-DMFB_DEBUG"] if debug else []
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         objs.append(obj)
-        cmd = [NVCC, *ARCH, *FLAGS, "-I", CSRC, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
+        cmd = [NVCC, *ARCH, *FLAGS, *extra, "-I", CSRC, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
         if src.endswith(".cpp"):
             cmd = [NVCC, "-Wno-deprecated-gpu-targets", *FLAGS, "-x", "c++", "-I", CSRC, "-c", src, "-o", obj]
         if verbose:
@@ -63,14 +66,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
             sys.stderr.write(out.decode(errors="replace"))
     if failed:
         raise RuntimeError("libmfadd_b200 build failed")
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     link = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
     if verbose:
         print(" ".join(link))
     subprocess.run(link, check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose=True, debug="--debug" in sys.argv))

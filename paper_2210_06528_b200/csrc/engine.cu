@@ -10,6 +10,7 @@
 #include <array>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -178,7 +179,11 @@ struct Timeline {
     used = 0;
     st = s;
   }
+  // MFADD_SYNC_CHECK=1: synchronise after every kernel and name the failing one.
+  const char* cur = "";
+  bool sync_check = std::getenv("MFADD_SYNC_CHECK") != nullptr;
   void begin(const char* name) {
+    cur = name;
     if (!on) return;
     if (used == recs.size()) {
       recs.emplace_back();
@@ -189,6 +194,12 @@ struct Timeline {
     CK(cudaEventRecord(recs[used].a, st));
   }
   void end() {
+    if (sync_check) {
+      const cudaError_t e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) throw ApiError(MFADD_ECUDA, std::string("kernel ") + cur + ": " + cudaGetErrorString(e));
+      if (const int line = mfb::debug_fail_line())
+        throw ApiError(MFADD_ECUDA, std::string("kernel ") + cur + ": bounds check failed at kernels.cu:" + std::to_string(line));
+    }
     if (!on) return;
     CK(cudaEventRecord(recs[used].b, st));
     ++used;
@@ -204,6 +215,7 @@ struct Workload {
   std::vector<int> factor_ids;
   std::int64_t total_rows = 0, total_cols = 0, total_p = 0, total_t1 = 0, total_t2 = 0;
   std::int64_t fs[3] = {0, 0, 0};
+  std::int64_t field_n = 0;  // elements of the field buffer the fit reads
   int max_m = 0, max_n_factor = 0;
   int max_lines_strided[3] = {0, 0, 0};
   int max_lines_last = 0;
@@ -287,6 +299,7 @@ struct Workload {
   // K1 + K2
   int setup(mfadd_context* ctx, Timeline* tl = nullptr) {
     Timeline dummy;
+    dummy.st = ctx->stream;
     if (!tl) tl = &dummy;
     mfb::RowsArgs ra{d_probs.p, static_cast<int>(probs.size()), max_m, knots.p, params.p, g0.p, first_col.p,
                      count.p, vals.p, ctx->d_status};
@@ -305,6 +318,7 @@ struct Workload {
   // K3
   int fit(mfadd_context* ctx, const double* field, Timeline* tl = nullptr) {
     Timeline dummy;
+    dummy.st = ctx->stream;
     if (!tl) tl = &dummy;
     CK(cudaMemsetAsync(linf_int.p, 0, blocks.size() * sizeof(unsigned long long), ctx->stream));
     mfb::FitArgs fa{};
@@ -328,6 +342,10 @@ struct Workload {
       fa.max_lines_strided[k] = max_lines_strided[k];
     }
     fa.max_lines_last = max_lines_last;
+    fa.n_field = field_n;
+    fa.n_t1 = total_t1;
+    fa.n_t2 = total_t2;
+    fa.n_P = total_p;
     static const char* kNames[2] = {"fit_axis0", "fit_axis1"};
     int l = 0;
     for (int d = 0; d + 1 < D; ++d) {
@@ -441,6 +459,11 @@ struct mfadd_solver {
   DBuf<double> epoch_out, lattice, error, partial, red2, field_buf;
   int npairs = 0;
   std::vector<std::array<int, 2>> pair_ids;
+  // Non-empty when some shared control has a holder that is not a neighbour of
+  // another holder: the reference throws this runtime_error from
+  // enforce_constraints in the first exchange epoch (solver.cpp:134-141).
+  std::string holder_fault;
+  int max_holders = 1;
 
   // results
   std::vector<mfadd_epoch_stats> epochs;
@@ -603,6 +626,7 @@ MFB_API int mfadd_solver_create(mfadd_context* ctx, const mfadd_decomposition* d
         wl.fs[k] = st;
         st *= d.grid[k];
       }
+      wl.field_n = st;
     }
     // axis problems: one per (dim, block coordinate) — solver.cpp:59-66,83-88
     for (int k = 0; k < D; ++k) {
@@ -684,6 +708,14 @@ MFB_API int mfadd_solver_create(mfadd_context* ctx, const mfadd_decomposition* d
       s->nS[k] = static_cast<std::int64_t>(sl.size()) - s->s_off[k];
       s->nC[k] = static_cast<std::int64_t>(cl.size()) - s->c_off[k];
     }
+    s->max_holders = 1;
+    for (int k = 0; k < D; ++k) {
+      int mx = 1;
+      for (const auto& r : d.holder[k]) mx = std::max(mx, r[1] - r[0] + 1);
+      s->max_holders *= mx;
+    }
+    if (s->max_holders > 27) throw std::logic_error("partition: a control has more than 3 holders along one axis");
+    if (s->max_holders > 8) s->max_holders = 27;
     s->total_shared = 0;
     for (int pc = 0; pc < D; ++pc) {
       std::int64_t cnt = 1;
@@ -713,6 +745,43 @@ MFB_API int mfadd_solver_create(mfadd_context* ctx, const mfadd_decomposition* d
         s->pair_ids.push_back({a, j});
       }
     s->npairs = static_cast<int>(s->pair_ids.size());
+    // solver.cpp:134-141 + runtime.cpp:17-21: a block only hears from its
+    // neighbours (coordinate distance <= 1).  Find, for the lowest block id,
+    // the first held control (row-major) with a holder two coordinates away.
+    for (int b = 0; b < d.nblocks && s->holder_fault.empty(); ++b) {
+      const auto& cb = d.coords[static_cast<std::size_t>(b)];
+      std::array<std::int64_t, 3> lo{0, 0, 0}, hi{1, 1, 1}, fmin{-1, -1, -1};
+      for (int k = 0; k < D; ++k) {
+        lo[k] = d.at(b, k, mfb::DOF_LO);
+        hi[k] = d.at(b, k, mfb::DOF_HI);
+        for (std::int64_t i = lo[k]; i < hi[k]; ++i) {
+          const auto r = d.holder[k][static_cast<std::size_t>(i)];
+          if (r[0] < cb[k] - 1 || r[1] > cb[k] + 1) {
+            fmin[k] = i;
+            break;
+          }
+        }
+      }
+      bool found = false;
+      std::array<std::int64_t, 3> best{0, 0, 0};
+      for (int k = 0; k < D; ++k) {
+        if (fmin[k] < 0) continue;
+        std::array<std::int64_t, 3> cand = lo;
+        cand[k] = fmin[k];
+        if (!found || std::lexicographical_compare(cand.begin(), cand.begin() + D, best.begin(), best.begin() + D))
+          best = cand;
+        found = true;
+      }
+      if (!found) continue;
+      int ns = 1, near = 1;
+      for (int k = 0; k < D; ++k) {
+        const auto r = d.holder[k][static_cast<std::size_t>(best[k])];
+        ns *= r[1] - r[0] + 1;
+        near *= std::min(r[1], cb[k] + 1) - std::max(r[0], cb[k] - 1) + 1;
+      }
+      s->holder_fault = "enforce_constraints: block " + std::to_string(b) + " received " + std::to_string(near - 1) +
+                        " contributions for a control shared by " + std::to_string(ns) + " blocks";
+    }
     s->pair_slot.upload(ps, st);
     s->pair_jumps.alloc(static_cast<std::size_t>(std::max(1, s->npairs)) * 2);
     s->change.alloc(static_cast<std::size_t>(d.nblocks));
@@ -786,6 +855,8 @@ mfb::EpochArgs epoch_args(mfadd_solver* s, int mode) {
   a.acc = s->acc.p;
   a.pair_slot = s->pair_slot.p;
   a.pair_jumps = s->pair_jumps.p;
+  a.n_P = s->wl.total_p;
+  a.max_holders = s->max_holders;
   return a;
 }
 
@@ -836,6 +907,7 @@ void solve_impl(mfadd_solver* s, const double* dfield) {
   sum = mfadd_solve_summary{};
   sum.converged = 1;
   if (s->cfg.enforce_continuity && d.any_shared) {
+    if (!s->holder_fault.empty()) throw std::runtime_error(s->holder_fault);
     sum.converged = 0;
     for (int iter = 1; iter <= s->cfg.max_outer_iterations; ++iter) {
       launches += run_epoch(s, iter >= 2 ? 2 : 1, iter);  // solver.cpp:397
@@ -1167,6 +1239,7 @@ MFB_API int mfadd_fit_unconstrained(mfadd_context* ctx, int rank, int degree, co
         wl.fs[k] = stv;
         stv *= wl.probs[static_cast<std::size_t>(k)].m;
       }
+      wl.field_n = stv;
     }
     wl.blocks.push_back(bd);
     wl.layout_tables();

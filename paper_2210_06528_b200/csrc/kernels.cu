@@ -26,6 +26,28 @@
 
 #include "kernels.cuh"
 
+#include <cstdio>
+
+// Debug builds (-DMFB_DEBUG, libmfadd_b200_debug.so) range-check every global
+// index and trap with a message instead of touching memory out of bounds.
+// Debug builds (-DMFB_DEBUG, libmfadd_b200_debug.so) range-check global
+// indices; a failed check records its source line in a device word and makes
+// the thread return (no trap, so the host can still read the record).
+#ifdef MFB_DEBUG
+__device__ int g_mfb_debug_line = 0;
+#define MFB_ASSERT(c, tag)                        \
+  do {                                            \
+    if (!(c)) {                                   \
+      atomicCAS(&g_mfb_debug_line, 0, __LINE__);  \
+      return;                                     \
+    }                                             \
+  } while (0)
+#else
+#define MFB_ASSERT(c, tag) \
+  do {                     \
+  } while (0)
+#endif
+
 namespace mfb {
 
 namespace {
@@ -270,6 +292,16 @@ __global__ void __launch_bounds__(kStridedThreads) k_fit_strided(FitArgs a, int 
   }
   double* dst = (d == 0 ? a.t1 + blk.t1off : a.t2 + blk.t2off) + (l * n) * Tr + t;
   const std::int64_t dstr = Tr;
+#ifdef MFB_DEBUG
+  if (active) {
+    const double* sb = d == 0 ? a.field : a.t1;
+    const std::int64_t sn = d == 0 ? a.n_field : a.n_t1;
+    MFB_ASSERT(src - sb >= 0 && (src - sb) + static_cast<std::int64_t>(m - 1) * sst < sn, "strided src");
+    const double* db = d == 0 ? a.t1 : a.t2;
+    const std::int64_t dn = d == 0 ? a.n_t1 : a.n_t2;
+    MFB_ASSERT(dst - db >= 0 && (dst - db) + static_cast<std::int64_t>(n - 1) * dstr < dn, "strided dst");
+  }
+#endif
   const int* g0g = a.g0 + pr.row_off;
   const double* vg = a.vals + pr.row_off * (P + 1);
   const double* lt = a.ltab + pr.col_off * (2 * P + 1);
@@ -352,6 +384,15 @@ __global__ void __launch_bounds__(kLastThreads) k_fit_last(FitArgs a) {
   const double* src = (a.D == 1 ? a.field + blk.fbase : (a.D == 2 ? a.t1 + blk.t1off : a.t2 + blk.t2off)) + l0 * m;
   double* Pb = a.P + blk.poff + l0 * n;
   double* Yb = a.Y + blk.poff + l0 + tid;  // transposed scratch: Y[c*L + l]
+#ifdef MFB_DEBUG
+  {
+    const double* sb = a.D == 1 ? a.field : (a.D == 2 ? a.t1 : a.t2);
+    const std::int64_t sn = a.D == 1 ? a.n_field : (a.D == 2 ? a.n_t1 : a.n_t2);
+    MFB_ASSERT(src - sb >= 0 && (src - sb) + static_cast<std::int64_t>(nl) * m <= sn, "last src");
+    MFB_ASSERT(blk.poff + l0 * n + static_cast<std::int64_t>(nl) * n <= a.n_P, "last P");
+    MFB_ASSERT(blk.poff + L * n <= a.n_P, "last Y");
+  }
+#endif
   const int* g0g = a.g0 + pr.row_off;
   const double* vg = a.vals + pr.row_off * (P + 1);
   const double* lt = a.ltab + pr.col_off * (2 * P + 1);
@@ -439,6 +480,12 @@ __device__ __forceinline__ bool piece_index(const EpochArgs& a, std::int64_t g, 
     const std::int64_t r = g % ext;
     g /= ext;
     idx[k] = k < pc ? a.clist[a.c_off[k] + r] : (k == pc ? a.slist[a.s_off[k] + r] : r);
+#ifdef MFB_DEBUG
+    if (idx[k] < 0 || idx[k] >= a.N[k]) {
+      atomicCAS(&g_mfb_debug_line, 0, __LINE__);
+      return false;
+    }
+#endif
   }
   return true;
 }
@@ -446,6 +493,28 @@ __device__ __forceinline__ bool piece_index(const EpochArgs& a, std::int64_t g, 
 constexpr int kEpochThreads = 256;
 constexpr int kEpochSmemBlocks = 1024;  // per-CTA smem reduction slots
 
+// True when two block ids are neighbours in the reference's sense (all
+// coordinate distances <= 1, layout.cpp:328-340; holders share the dof, so
+// their shared box is non-empty).  Writes the 3^D neighbour code.
+__device__ __forceinline__ bool neighbour_code(const EpochArgs& a, int ia, int ib, int* code) {
+  int c = 0, mul = 1;
+  for (int k = a.D - 1; k >= 0; --k) {
+    const int ca = ia % a.B[k], cb = ib % a.B[k];
+    ia /= a.B[k];
+    ib /= a.B[k];
+    const int df = cb - ca;
+    if (df < -1 || df > 1) return false;
+    c += (df + 1) * mul;
+    mul *= 3;
+  }
+  *code = c;
+  return true;
+}
+
+// MAXH = 8 when every control has at most 2 holders per axis (all holders are
+// then mutual neighbours); MAXH = 27 otherwise (only measurement modes run:
+// the reference throws before averaging, solver.cpp:134-141).
+template <int MAXH>
 __global__ void __launch_bounds__(kEpochThreads) k_epoch(EpochArgs a) {
   __shared__ unsigned long long s_change[kEpochSmemBlocks];
   __shared__ unsigned long long s_linf[kEpochSmemBlocks];
@@ -469,11 +538,13 @@ __global__ void __launch_bounds__(kEpochThreads) k_epoch(EpochArgs a) {
       f[k] = r.x;
       e[k] = r.y - r.x + 1;
       ns *= e[k];
+      MFB_ASSERT(r.x >= 0 && r.y < a.B[k] && r.y >= r.x, "epoch holder range");
     }
+    MFB_ASSERT(ns >= 1 && ns <= MAXH, "epoch ns");
     // holders in ascending block id (layout.cpp:177-195): lexicographic coords
-    std::int64_t off[8];
-    int ids[8];
-    double v[8];
+    std::int64_t off[MAXH];
+    int ids[MAXH];
+    double v[MAXH];
     for (int h = 0; h < ns; ++h) {
       int rr = h, c[3] = {0, 0, 0};
       for (int k = a.D - 1; k >= 0; --k) {
@@ -485,29 +556,26 @@ __global__ void __launch_bounds__(kEpochThreads) k_epoch(EpochArgs a) {
       for (int k = 0; k < a.D; ++k) {
         id = id * a.B[k] + c[k];
         const AxisProb& pk = a.probs[a.axbase[k] + c[k]];
+        MFB_ASSERT(idx[k] - pk.col_lo >= 0 && idx[k] - pk.col_lo < pk.n, "epoch local index");
         o = o * pk.n + (idx[k] - pk.col_lo);
       }
+      MFB_ASSERT(id >= 0 && id < a.nblocks, "epoch id");
       ids[h] = id;
       off[h] = a.poff[id] + o;
+      MFB_ASSERT(off[h] >= 0 && off[h] < a.n_P, "epoch off");
       v[h] = a.P[off[h]];
     }
     if (a.mode == 3) {  // final per-pair jumps (solver.cpp:416 -> :166-193)
       for (int h1 = 0; h1 < ns; ++h1)
         for (int h2 = h1 + 1; h2 < ns; ++h2) {
-          int code = 0, ra = ids[h1], rb = ids[h2], mul = 1;
-          for (int k = a.D - 1; k >= 0; --k) {
-            const int ca = ra % a.B[k], cb = rb % a.B[k];
-            ra /= a.B[k];
-            rb /= a.B[k];
-            code += (cb - ca + 1) * mul;
-            mul *= 3;
-          }
+          int code;
+          if (!neighbour_code(a, ids[h1], ids[h2], &code)) continue;
           const int slot = a.pair_slot[ids[h1] * 27 + code];
           if (slot >= 0) atomicMax(a.pair_jumps + 2 * slot + (ns > 2 ? 1 : 0), dbits(fabs(v[h1] - v[h2])));
         }
       continue;
     }
-    const bool update = (a.mode == 2) || (a.mode == 1 && ns == 2);
+    const bool update = MAXH == 8 && ((a.mode == 2) || (a.mode == 1 && ns == 2));
     if (update) {
       // solver.cpp:147-159: ordered sum in ascending holder id, divide once
       double sum = 0.0;
@@ -527,21 +595,32 @@ __global__ void __launch_bounds__(kEpochThreads) k_epoch(EpochArgs a) {
       }
       // all copies now bit-identical: post-update jumps are exactly zero
     } else {
-      double mn = v[0], mx = v[0];
+      double jd = 0.0;
+      if (MAXH == 8) {  // all holders are mutual neighbours: max |Pa-Pb| = max - min
+        double mn = v[0], mx = v[0];
+        for (int h = 1; h < ns; ++h) {
+          mn = fmin(mn, v[h]);
+          mx = fmax(mx, v[h]);
+        }
+        jd = mx - mn;
+      } else {
+        for (int h1 = 0; h1 < ns; ++h1)
+          for (int h2 = h1 + 1; h2 < ns; ++h2) {
+            int code;
+            if (neighbour_code(a, ids[h1], ids[h2], &code)) jd = fmax(jd, fabs(v[h1] - v[h2]));
+          }
+      }
       for (int h = 0; h < ns; ++h) {
-        mn = fmin(mn, v[h]);
-        mx = fmax(mx, v[h]);
         const unsigned long long lv = dbits(fabs(v[h]));
         if (use_smem)
           atomicMax(s_linf + ids[h], lv);
         else
           atomicMax(a.linf_sh + ids[h], lv);
       }
-      const unsigned long long jd = dbits(mx - mn);  // = max over holder pairs |Pa - Pb|
       if (ns == 2)
-        jss = umax(jss, jd);
+        jss = umax(jss, dbits(jd));
       else
-        jms = umax(jms, jd);
+        jms = umax(jms, dbits(jd));
     }
   }
   if (a.mode == 3) return;
@@ -818,6 +897,16 @@ struct DecodeLaunch {
 
 }  // namespace
 
+int debug_fail_line() {
+#ifdef MFB_DEBUG
+  int line = 0;
+  cudaMemcpyFromSymbol(&line, g_mfb_debug_line, sizeof(int));
+  return line;
+#else
+  return 0;
+#endif
+}
+
 int launch_basis_rows(int degree, const RowsArgs& a, cudaStream_t s) {
   return dispatch_degree<RowsLaunch>(degree, a, s);
 }
@@ -842,7 +931,10 @@ int launch_epoch(const EpochArgs& a, cudaStream_t s) {
   std::int64_t want = (a.total + kEpochThreads - 1) / kEpochThreads;
   const std::int64_t cap = static_cast<std::int64_t>(sms) * 4;
   const unsigned grid = static_cast<unsigned>(want < cap ? want : cap);
-  k_epoch<<<grid, kEpochThreads, 0, s>>>(a);
+  if (a.max_holders <= 8)
+    k_epoch<8><<<grid, kEpochThreads, 0, s>>>(a);
+  else
+    k_epoch<27><<<grid, kEpochThreads, 0, s>>>(a);
   return 1;
 }
 

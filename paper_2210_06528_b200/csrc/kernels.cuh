@@ -9,6 +9,9 @@
 
 namespace mfb {
 
+// Source line of the first failed device bounds check (debug builds), else 0.
+int debug_fail_line();
+
 // K1: per-row find_span + Cox-de Boor basis + window clip
 // (knots.cpp:83-129, collocation.cpp:83-111).
 struct RowsArgs {
@@ -60,6 +63,7 @@ struct FitArgs {
   std::int64_t sflag_off[3];
   int max_lines_strided[3];          // per axis: max lines over blocks
   int max_lines_last;
+  std::int64_t n_field, n_t1, n_t2, n_P;  // buffer sizes (debug bounds checks)
 };
 int launch_fit_strided(int degree, const FitArgs& a, int axis, cudaStream_t s);  // axis < D-1
 int launch_fit_last(int degree, const FitArgs& a, cudaStream_t s);
@@ -91,6 +95,8 @@ struct EpochArgs {
   // final per-pair jumps (mode 3): pair slot table nblocks*27, per-pair ss/ms
   const int* pair_slot;
   unsigned long long* pair_jumps;
+  std::int64_t n_P;  // debug bounds checks
+  int max_holders;   // max n_s over all controls (8: <= 2 holders per axis)
 };
 int launch_epoch(const EpochArgs& a, cudaStream_t s);
 

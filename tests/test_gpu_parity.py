@@ -224,11 +224,14 @@ def test_decode_windowed(ctx):
 # ------------------------------------------------------------------ solve
 
 
+# Scaled families keep every block at least 2(floor(p/2)+overlap) spans wide,
+# so each control has <= 2 holders per axis (the reference throws otherwise;
+# see test_three_holder_fault).
 SMALL = {
     "C1": W.CONFIGS["C1"],  # full size: 10,000 points
     "C2": W.CONFIGS["C2"],  # full size: 1024^2
-    "C3s": W.scaled(W.CONFIGS["C3"], (64, 72, 80), (8, 9, 10)),
-    "C4s": W.scaled(W.CONFIGS["C4"], (96, 90, 84), (8, 8, 8)),
+    "C3s": W.scaled(W.CONFIGS["C3"], (64, 72, 80), (12, 13, 14)),
+    "C4s": W.scaled(W.CONFIGS["C4"], (120, 116, 112), (14, 14, 13)),
     "C5s": W.scaled(W.CONFIGS["C5"], (1024, 960), (24, 22)),
 }
 
@@ -238,6 +241,25 @@ def test_solve_parity(ctx, name):
     cfg = SMALL[name]
     values = W.make_field_numpy(cfg)
     g, o, _ = run_both(cfg, values)
+    assert_solve_parity(g, o)
+
+
+def test_three_holder_fault(ctx):
+    """Blocks narrower than 2(floor(p/2)+overlap) spans: a control has a holder
+    two coordinates away, which never hears from it; the reference throws
+    runtime_error from enforce_constraints (solver.cpp:134-141)."""
+    cfg = W.scaled(W.CONFIGS["C3"], (64, 72, 80), (8, 9, 10))
+    values = W.make_field_numpy(cfg)
+    od = orc.Decomposition(cfg.grid, cfg.blocks, cfg.degree, cfg.nctrl, cfg.overlap)
+    with pytest.raises(orc.OracleError) as oe:
+        orc.solve(od, values, 20, 1e-10)
+    dec = m.partition(cfg.grid, cfg.bounds, cfg.blocks, cfg.degree, cfg.nctrl, cfg.overlap)
+    with pytest.raises(m.RuntimeFault) as ge:
+        m.Solver(dec, m.SolverConfig(max_outer_iterations=20, log_errors=False)).run(values.reshape(-1))
+    assert str(ge.value) == str(oe.value).split("] ", 1)[1]
+    # without continuity enforcement the reference completes: decoupled fits,
+    # epoch-0 jumps over neighbour pairs only, final per-pair jumps
+    g, o, _ = run_both(cfg, values, enforce=False)
     assert_solve_parity(g, o)
 
 
