@@ -226,13 +226,15 @@ def test_decode_windowed(ctx):
 
 # Scaled families keep every block at least 2(floor(p/2)+overlap) spans wide,
 # so each control has <= 2 holders per axis (the reference throws otherwise;
-# see test_three_holder_fault).
+# see test_three_holder_fault), and keep the parent's inputs-per-control
+# ratio (C3 2.0, C4 ~3.7, C5 4.0) so the local problems stay as well
+# conditioned as at full size.
 SMALL = {
     "C1": W.CONFIGS["C1"],  # full size: 10,000 points
     "C2": W.CONFIGS["C2"],  # full size: 1024^2
-    "C3s": W.scaled(W.CONFIGS["C3"], (64, 72, 80), (12, 13, 14)),
-    "C4s": W.scaled(W.CONFIGS["C4"], (120, 116, 112), (14, 14, 13)),
-    "C5s": W.scaled(W.CONFIGS["C5"], (1024, 960), (24, 22)),
+    "C3s": W.scaled(W.CONFIGS["C3"], (96, 100, 104), (12, 12, 13)),
+    "C4s": W.Config("C4s", (190, 186, 182), (4, 4, 4), 4, (13, 13, 13), 4, "combustion"),
+    "C5s": W.scaled(W.CONFIGS["C5"], (1536, 1408), (24, 22)),
 }
 
 
