@@ -4,6 +4,8 @@
 // kernels.cu.  No CPU fallback: every value of SolveResult is produced on the
 // GPU; the host only builds integer metadata tables at plan time and reads
 // back scalars.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -128,6 +130,42 @@ int host_find_span(const std::vector<double>& kn, int p, double u) {
   return mid;
 }
 
+constexpr int kRowPad = 64;  // rows of slack after every row table (bulk copies read whole chunks)
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !p)
+      throw ApiError(MFADD_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// Tiled fp64 tensor map over a row-major array; dims/box innermost first.
+CUtensorMap make_tmap(const double* base, int rank, const std::uint64_t* dims, const std::uint32_t* box) {
+  CUtensorMap m;
+  std::uint64_t strides[3] = {0, 0, 0};
+  std::uint64_t st = 8;
+  for (int i = 0; i + 1 < rank; ++i) {
+    st *= dims[i];
+    strides[i] = st;
+  }
+  const std::uint32_t estr[3] = {1, 1, 1};
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, static_cast<cuuint32_t>(rank),
+                                 const_cast<double*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw ApiError(MFADD_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+  return m;
+}
+
+int round_up(int x, int a) { return (x + a - 1) / a * a; }
+
 }  // namespace
 
 // ===================================================================== types
@@ -228,17 +266,48 @@ struct Workload {
   DBuf<unsigned long long> linf_int;
   DBuf<unsigned char> sflag;
   std::int64_t sflag_off[3] = {0, 0, 0};
+  // TMA axis-0 pass (field row strides must be 16-B multiples)
+  bool tma_axis0 = false;
+  mfb::TmaGeom axis0_geo{1, 1, 16, 4};
+  int axis0_tiles = 0;
+  std::array<std::int64_t, 3> field_dims{1, 1, 1};  // global field extents (solver) for the tensor map
+
+  void plan_tma(bool enable) {
+    tma_axis0 = false;
+    if (!enable || D < 2 || std::getenv("MFADD_NO_TMA")) return;
+    int mx1 = 0, mx2 = 0;
+    for (const auto& b : blocks) {
+      mx1 = std::max(mx1, probs[static_cast<std::size_t>(b.ax[1])].m);
+      if (D == 3) mx2 = std::max(mx2, probs[static_cast<std::size_t>(b.ax[2])].m);
+    }
+    if (field_dims[static_cast<std::size_t>(D - 1)] % 2 != 0) return;  // row stride not 16-B aligned
+    if (D == 2) {
+      const int nt = (mx1 + 255) / 256;
+      axis0_geo.B2 = round_up((mx1 + nt - 1) / nt, 2);
+      axis0_geo.B1 = 1;
+      axis0_tiles = (mx1 + axis0_geo.B2 - 1) / axis0_geo.B2;
+    } else {
+      if (mx2 > 256) return;
+      axis0_geo.B2 = round_up(mx2, 2);
+      axis0_geo.B1 = std::max(1, 256 / axis0_geo.B2);
+      axis0_tiles = (mx1 + axis0_geo.B1 - 1) / axis0_geo.B1;
+    }
+    axis0_geo.R = 16;
+    axis0_geo.S = 4;
+    tma_axis0 = true;
+  }
 
   // Derive offsets/sizes from probs + blocks (row/col offsets, intermediates).
   void layout_tables() {
     total_rows = 0;
     total_cols = 0;
     max_m = 0;
-    for (auto& pr : probs) {
+    for (auto& pr : probs) {  // 4-row aligned (16-B bulk copies of g0 / vals)
       pr.row_off = total_rows;
-      total_rows += pr.m;
+      total_rows = (total_rows + pr.m + 3) / 4 * 4;
       max_m = std::max(max_m, pr.m);
     }
+    total_rows += kRowPad;
     std::vector<char> is_factor(probs.size(), 0);
     for (int id : factor_ids) is_factor[static_cast<std::size_t>(id)] = 1;
     max_n_factor = 0;
@@ -350,7 +419,22 @@ struct Workload {
     int l = 0;
     for (int d = 0; d + 1 < D; ++d) {
       tl->begin(kNames[d]);
-      l += mfb::launch_fit_strided(p, fa, d, ctx->stream);
+      if (d == 0 && tma_axis0) {
+        std::uint64_t dims[3];
+        std::uint32_t box[3];
+        for (int k = 0; k < D; ++k) dims[k] = static_cast<std::uint64_t>(field_dims[static_cast<std::size_t>(D - 1 - k)]);
+        box[0] = static_cast<std::uint32_t>(axis0_geo.B2);
+        if (D == 2) {
+          box[1] = static_cast<std::uint32_t>(axis0_geo.R);
+        } else {
+          box[1] = static_cast<std::uint32_t>(axis0_geo.B1);
+          box[2] = static_cast<std::uint32_t>(axis0_geo.R);
+        }
+        const CUtensorMap map = make_tmap(field, D, dims, box);
+        l += mfb::launch_fit_axis0_tma(p, fa, map, axis0_geo, axis0_tiles, ctx->stream);
+      } else {
+        l += mfb::launch_fit_strided(p, fa, d, ctx->stream);
+      }
       tl->end();
     }
     tl->begin("fit_last");
@@ -447,6 +531,10 @@ struct mfadd_solver {
   int axbase[3] = {0, 0, 0};
   int dec_prob[3] = {-1, -1, -1};
   DecodePlan dp;
+  // TMA decode sweep (D >= 2, even last extent)
+  bool tma_decode = false;
+  mfb::TmaGeom dgeo{1, 1, 16, 4};
+  int dnt1 = 1, dnt2 = 1, dnrange = 1, dH = 1;
 
   DBuf<int2> hr;
   DBuf<int> slist, clist, own_coord, pair_slot, unit_g0;
@@ -680,6 +768,8 @@ MFB_API int mfadd_solver_create(mfadd_context* ctx, const mfadd_decomposition* d
       wl.blocks.push_back(bd);
     }
     wl.layout_tables();
+    for (int k = 0; k < D; ++k) wl.field_dims[static_cast<std::size_t>(k)] = d.grid[k];
+    wl.plan_tma(true);
     cudaStream_t st = ctx->stream;
     wl.allocate(st);
     wl.knots.upload(kn, st);
@@ -801,7 +891,28 @@ MFB_API int mfadd_solver_create(mfadd_context* ctx, const mfadd_decomposition* d
       s->dp.size_windows(k, d.knots[src], u, p, 0);
       s->dp.prob_of[k] = s->dec_prob[src];
     }
-    s->partial.alloc(static_cast<std::size_t>(s->dp.ntiles[0] * s->dp.ntiles[1] * s->dp.ntiles[2]) * 2);
+    std::size_t npart = static_cast<std::size_t>(s->dp.ntiles[0] * s->dp.ntiles[1] * s->dp.ntiles[2]);
+    if (D >= 2 && d.grid[D - 1] % 2 == 0 && !std::getenv("MFADD_NO_TMA")) {
+      const int M1 = static_cast<int>(d.grid[1]), M2 = D == 3 ? static_cast<int>(d.grid[2]) : 1;
+      const int inner = D == 2 ? M1 : M2;
+      const int nt = (inner + 255) / 256;
+      s->dgeo.B2 = round_up((inner + nt - 1) / nt, 2);
+      s->dgeo.B1 = D == 2 ? 1 : std::max(1, 256 / s->dgeo.B2);
+      s->dgeo.R = 16;
+      s->dgeo.S = 4;
+      s->dnt2 = (inner + s->dgeo.B2 - 1) / s->dgeo.B2;
+      s->dnt1 = D == 2 ? 1 : (M1 + s->dgeo.B1 - 1) / s->dgeo.B1;
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+      const int M0 = static_cast<int>(d.grid[0]);
+      const int want = std::max(1, (8 * sms + s->dnt1 * s->dnt2 - 1) / (s->dnt1 * s->dnt2));
+      const int nr = std::min(want, (M0 + s->dgeo.R - 1) / s->dgeo.R);
+      s->dH = round_up((M0 + nr - 1) / nr, s->dgeo.R);
+      s->dnrange = (M0 + s->dH - 1) / s->dH;
+      s->tma_decode = true;
+      npart = std::max(npart, static_cast<std::size_t>(s->dnt1) * s->dnt2 * s->dnrange);
+    }
+    s->partial.alloc(npart * 2);
     s->red2.alloc(2);
     s->unit_g0.upload(std::vector<int>{0}, st);
     s->unit_vals.upload(std::vector<double>{1.0}, st);
@@ -973,11 +1084,51 @@ void solve_impl(mfadd_solver* s, const double* dfield) {
   da.field = dfield;
   da.out = s->cfg.store_error ? s->error.p : nullptr;
   da.partial = s->partial.p;
+  std::int64_t nparts = static_cast<std::int64_t>(s->partial.n / 2);
   s->tl.begin("decode");
-  launches += mfb::launch_decode(wl.p, da, st);
+  if (s->tma_decode) {
+    mfb::DecodeSweepArgs ds{};
+    ds.D = d.rank;
+    ds.M0 = static_cast<int>(d.grid[0]);
+    ds.M1 = static_cast<int>(d.grid[1]);
+    ds.M2 = d.rank == 3 ? static_cast<int>(d.grid[2]) : 1;
+    ds.N1 = static_cast<int>(d.n_ctrl[1]);
+    ds.N2 = d.rank == 3 ? static_cast<int>(d.n_ctrl[2]) : 1;
+    ds.ntile1 = s->dnt1;
+    ds.ntile2 = s->dnt2;
+    ds.nrange = s->dnrange;
+    ds.H = s->dH;
+    auto rows = [&](int k, const int** g, const double** v) {
+      const AxisProb& pr = wl.probs[static_cast<std::size_t>(s->dec_prob[k])];
+      *g = wl.g0.p + pr.row_off;
+      *v = wl.vals.p + pr.row_off * (wl.p + 1);
+    };
+    rows(0, &ds.g0_0, &ds.v_0);
+    rows(1, &ds.g0_1, &ds.v_1);
+    if (d.rank == 3) rows(2, &ds.g0_2, &ds.v_2);
+    ds.lattice = s->lattice.p;
+    ds.err = s->cfg.store_error ? s->error.p : nullptr;
+    ds.partial = s->partial.p;
+    std::uint64_t dims[3];
+    std::uint32_t box[3];
+    for (int k = 0; k < d.rank; ++k) dims[k] = static_cast<std::uint64_t>(d.grid[d.rank - 1 - k]);
+    box[0] = static_cast<std::uint32_t>(s->dgeo.B2);
+    if (d.rank == 2) {
+      box[1] = static_cast<std::uint32_t>(s->dgeo.R);
+    } else {
+      box[1] = static_cast<std::uint32_t>(s->dgeo.B1);
+      box[2] = static_cast<std::uint32_t>(s->dgeo.R);
+    }
+    const CUtensorMap map = make_tmap(dfield, d.rank, dims, box);
+    launches += mfb::launch_decode_tma(wl.p, ds, map, s->dgeo, st);
+    nparts = static_cast<std::int64_t>(s->dnt1) * s->dnt2 * s->dnrange;
+  } else {
+    launches += mfb::launch_decode(wl.p, da, st);
+    nparts = s->dp.ntiles[0] * s->dp.ntiles[1] * s->dp.ntiles[2];
+  }
   s->tl.end();
   s->tl.begin("reduce");
-  launches += mfb::launch_reduce_partials(s->partial.p, static_cast<std::int64_t>(s->partial.n / 2), s->red2.p, st);
+  launches += mfb::launch_reduce_partials(s->partial.p, nparts, s->red2.p, st);
   s->tl.end();
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(hp + 4, s->red2.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "dev.cuh"
@@ -145,6 +146,33 @@ struct DecodeArgs {
   double* partial;       // per tile {l2sq, linf}
 };
 int launch_decode(int degree, const DecodeArgs& a, cudaStream_t s);
+// TMA pipeline geometry: box = (B2 inner, [B1], R rows) per stage, S stages.
+struct TmaGeom {
+  int B1, B2, R, S;
+};
+// TMA axis-0 fit pass (stream_tma.cu); needs 16-B aligned field row strides.
+int launch_fit_axis0_tma(int degree, const FitArgs& a, const CUtensorMap& map, const TmaGeom& g, int ntiles,
+                         cudaStream_t s);
+
+// TMA decode sweep over the whole input grid (D = 2, 3), stream_tma.cu.
+struct DecodeSweepArgs {
+  int D;
+  int M0, M1, M2;   // input grid extents (M2 = 1 for D = 2)
+  int N1, N2;       // lattice trailing extents (N2 = 1 for D = 2)
+  int ntile1, ntile2, nrange, H;
+  const int* g0_0;  // global decode rows per dim (row tables, 16-B aligned)
+  const double* v_0;
+  const int* g0_1;
+  const double* v_1;
+  const int* g0_2;
+  const double* v_2;
+  const double* lattice;
+  double* err;      // nullable
+  double* partial;  // per CTA {l2sq, linf}
+};
+int launch_decode_tma(int degree, const DecodeSweepArgs& a, const CUtensorMap& map, const TmaGeom& g,
+                      cudaStream_t s);
+
 // K7b: deterministic reduction of the tile partials.
 int launch_reduce_partials(const double* partial, std::int64_t n, double* out2, cudaStream_t s);
 

@@ -1,0 +1,409 @@
+// TMA-pipelined streaming passes of the B200 MFA encode path (sm_100a).
+//
+//  k_fit_axis0_tma   axis-0 fit pass (lsq.cpp:57-61 on axis 0): the HBM-bound
+//                    read of every block's input box Q_loc.
+//  k_decode_tma      decode of the global lattice over the whole input grid
+//                    + error field + L2^2/Linf partials (solver.cpp:298-328).
+//
+// Both sweep axis 0 with one thread per trailing grid point.  Input rows are
+// staged through an S-stage shared-memory ring filled by the Tensor Memory
+// Accelerator (one elected thread issues a tensor-map tile load of R rows
+// plus 1-D bulk copies of the matching basis rows; an mbarrier with expect_tx
+// completes each stage).  The per-thread arithmetic is the register-window
+// R^T contraction / decode of kernels.cu; see DESIGN.md §4.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.cuh"
+#include "tma.cuh"
+
+namespace mfb {
+
+namespace {
+
+constexpr unsigned kFullMask = 0xffffffffu;
+
+struct StageLayout {
+  int q_bytes;     // R * nthr * 8 (the full TMA box)
+  int v_off;       // offset of basis values in the stage
+  int g_off;       // offset of g0 ints
+  int stage_bytes;
+};
+
+__host__ __device__ inline StageLayout stage_layout(int R, int nthr, int P) {
+  StageLayout L;
+  L.q_bytes = R * nthr * 8;
+  L.v_off = (L.q_bytes + 127) / 128 * 128;
+  L.g_off = L.v_off + R * (P + 1) * 8;
+  L.stage_bytes = ((L.g_off + R * 4) + 127) / 128 * 128;
+  return L;
+}
+
+// ---------------------------------------------------------------- fit axis 0
+template <int P>
+__global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __grid_constant__ CUtensorMap map,
+                                                       const TmaGeom geo) {
+  extern __shared__ __align__(128) unsigned char sm_raw[];
+  const int b = blockIdx.y;
+  const BlockDev blk = a.blocks[b];
+  const AxisProb pr = a.probs[blk.ax[0]];
+  const int m = pr.m, n = pr.n;
+  const int D = a.D;
+  const int m1 = a.probs[blk.ax[1]].m;
+  const int m2 = D == 3 ? a.probs[blk.ax[2]].m : 1;
+  const int B1 = geo.B1, B2 = geo.B2, R = geo.R, S = geo.S;
+  const int nthr = B1 * B2;
+  const int tile = blockIdx.x;
+  const int tid = threadIdx.x;
+  int j1, j2;
+  if (D == 2) {
+    if (tile * B2 >= m1) return;
+    j1 = tile * B2 + tid;
+    j2 = 0;
+  } else {
+    if (tile * B1 >= m1) return;
+    j1 = tile * B1 + tid / B2;
+    j2 = tid % B2;
+  }
+  const bool active = (D == 2) ? (j1 < m1) : (j1 < m1 && j2 < m2);
+  const std::int64_t Tr = static_cast<std::int64_t>(m1) * m2;
+  const std::int64_t t = static_cast<std::int64_t>(j1) * m2 + j2;
+  double* dst = a.t1 + blk.t1off + t;  // T1[i0][Tr]
+  const int* g0g = a.g0 + pr.row_off;
+  const double* vg = a.vals + pr.row_off * (P + 1);
+  const double* lt = a.ltab + pr.col_off * (2 * P + 1);
+  // global coordinates of this CTA's box origin
+  const AxisProb p1 = a.probs[blk.ax[1]];
+  const int in0 = static_cast<int>(pr.in_lo);
+  const int c_inner = D == 2 ? static_cast<int>(p1.in_lo) + tile * B2 : static_cast<int>(a.probs[blk.ax[2]].in_lo);
+  const int c_mid = D == 2 ? 0 : static_cast<int>(p1.in_lo) + tile * B1;
+
+  const StageLayout SL = stage_layout(R, nthr, P);
+  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(sm_raw + S * SL.stage_bytes);
+  const int nchunks = (m + R - 1) / R;
+  const unsigned tx_bytes = static_cast<unsigned>(SL.q_bytes + R * (P + 1) * 8 + R * 4);
+  auto issue = [&](int c) {
+    const int st = c % S;
+    unsigned char* base = sm_raw + st * SL.stage_bytes;
+    mbar_arrive_expect_tx(&bars[st], tx_bytes);
+    if (D == 2)
+      tma_load_2d(base, &map, c_inner, in0 + c * R, &bars[st]);
+    else
+      tma_load_3d(base, &map, c_inner, c_mid, in0 + c * R, &bars[st]);
+    bulk_load_1d(base + SL.v_off, vg + static_cast<std::int64_t>(c) * R * (P + 1), R * (P + 1) * 8, &bars[st]);
+    bulk_load_1d(base + SL.g_off, g0g + static_cast<std::int64_t>(c) * R, R * 4, &bars[st]);
+  };
+  if (tid == 0) {
+    prefetch_tmap(&map);
+    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int c = 0; c < S && c < nchunks; ++c) issue(c);
+
+  double acc[P + 1], yw[P];
+#pragma unroll
+  for (int k = 0; k <= P; ++k) acc[k] = 0.0;
+#pragma unroll
+  for (int k = 0; k < P; ++k) yw[k] = 0.0;
+  int cbase = __ldg(g0g) < 0 ? __ldg(g0g) : 0;
+  const std::int64_t dstr = Tr;
+
+  for (int c = 0; c < nchunks; ++c) {
+    const int st = c % S;
+    const unsigned char* base = sm_raw + st * SL.stage_bytes;
+    const double* sq = reinterpret_cast<const double*>(base);
+    const double* sv = reinterpret_cast<const double*>(base + SL.v_off);
+    const int* sg = reinterpret_cast<const int*>(base + SL.g_off);
+    mbar_wait(&bars[st], (c / S) & 1);
+    const int jn = (m - c * R) < R ? (m - c * R) : R;
+    for (int jj = 0; jj < jn; ++jj) {
+      const int g = sg[jj];
+      while (cbase < g) {
+        const int cc = cbase;
+        if (cc >= 0 && cc < n) {  // forward substitution of column cc
+          const double* Lc = lt + static_cast<std::int64_t>(cc) * (2 * P + 1);
+          double s = acc[0];
+#pragma unroll
+          for (int k = 1; k <= P; ++k) s = fma(-__ldg(Lc + k), yw[k - 1], s);
+          const double y = s * __ldg(Lc);
+          if (active) dst[static_cast<std::int64_t>(cc) * dstr] = y;
+#pragma unroll
+          for (int k = P - 1; k >= 1; --k) yw[k] = yw[k - 1];
+          yw[0] = y;
+        }
+#pragma unroll
+        for (int k = 0; k < P; ++k) acc[k] = acc[k + 1];
+        acc[P] = 0.0;
+        ++cbase;
+      }
+      const double q = sq[jj * nthr + tid];
+      const double* vr = sv + jj * (P + 1);
+#pragma unroll
+      for (int k = 0; k <= P; ++k) acc[k] = fma(vr[k], q, acc[k]);
+    }
+    __syncthreads();
+    if (tid == 0 && c + S < nchunks) {
+      fence_proxy_async();
+      issue(c + S);
+    }
+  }
+  while (cbase < n) {
+    const int cc = cbase;
+    if (cc >= 0) {
+      const double* Lc = lt + static_cast<std::int64_t>(cc) * (2 * P + 1);
+      double s = acc[0];
+#pragma unroll
+      for (int k = 1; k <= P; ++k) s = fma(-__ldg(Lc + k), yw[k - 1], s);
+      const double y = s * __ldg(Lc);
+      if (active) dst[static_cast<std::int64_t>(cc) * dstr] = y;
+#pragma unroll
+      for (int k = P - 1; k >= 1; --k) yw[k] = yw[k - 1];
+      yw[0] = y;
+    }
+#pragma unroll
+    for (int k = 0; k < P; ++k) acc[k] = acc[k + 1];
+    acc[P] = 0.0;
+    ++cbase;
+  }
+  // Back substitution in place, y values prefetched 8 columns ahead.
+  if (!active) return;
+  constexpr int PF = 8;
+  double yr[PF];
+#pragma unroll
+  for (int u = 0; u < PF; ++u) yr[u] = (n - 1 - u >= 0) ? dst[static_cast<std::int64_t>(n - 1 - u) * dstr] : 0.0;
+  double xw[P];
+#pragma unroll
+  for (int k = 0; k < P; ++k) xw[k] = 0.0;
+  for (int c0 = n - 1; c0 >= 0; c0 -= PF) {
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+      const int c = c0 - u;
+      if (c >= 0) {
+        const double* Lc = lt + static_cast<std::int64_t>(c) * (2 * P + 1);
+        double s = yr[u];
+        const int cn = c - PF;
+        yr[u] = cn >= 0 ? dst[static_cast<std::int64_t>(cn) * dstr] : 0.0;
+#pragma unroll
+        for (int k = 1; k <= P; ++k) s = fma(-__ldg(Lc + P + k), xw[k - 1], s);
+        const double x = s * __ldg(Lc);
+        dst[static_cast<std::int64_t>(c) * dstr] = x;
+#pragma unroll
+        for (int k = P - 1; k >= 1; --k) xw[k] = xw[k - 1];
+        xw[0] = x;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- decode
+template <int P>
+__global__ void __launch_bounds__(256) k_decode_tma(const DecodeSweepArgs a, const __grid_constant__ CUtensorMap map,
+                                                    const TmaGeom geo) {
+  extern __shared__ __align__(128) unsigned char sm_raw[];
+  __shared__ double s_red[64];
+  const int D = a.D;
+  const int B1 = geo.B1, B2 = geo.B2, R = geo.R, S = geo.S;
+  const int nthr = B1 * B2;
+  const int tid = threadIdx.x;
+  // trailing tile
+  const int tx = blockIdx.x % a.ntile2, ty = blockIdx.x / a.ntile2;
+  int j1, j2;
+  if (D == 2) {
+    j1 = tx * B2 + tid;
+    j2 = 0;
+  } else {
+    j1 = ty * B1 + tid / B2;
+    j2 = tx * B2 + tid % B2;
+  }
+  const bool active = D == 2 ? j1 < a.M1 : (j1 < a.M1 && j2 < a.M2);
+  const int y0 = blockIdx.y * a.H;
+  const int y1 = (y0 + a.H) < a.M0 ? (y0 + a.H) : a.M0;
+  const std::int64_t Tr = static_cast<std::int64_t>(a.M1) * a.M2;
+  const std::int64_t t = static_cast<std::int64_t>(j1) * a.M2 + j2;
+  // trailing basis of this thread (fixed for the whole sweep)
+  double w1[P + 1], w2[P + 1];
+  int g1 = 0, g2 = 0;
+  const int j1c = active ? j1 : 0, j2c = active ? j2 : 0;
+  if (D == 2) {
+    g1 = __ldg(a.g0_1 + j1c);
+#pragma unroll
+    for (int k = 0; k <= P; ++k) w1[k] = __ldg(a.v_1 + static_cast<std::int64_t>(j1c) * (P + 1) + k);
+  } else {
+    g1 = __ldg(a.g0_1 + j1c);
+    g2 = __ldg(a.g0_2 + j2c);
+#pragma unroll
+    for (int k = 0; k <= P; ++k) {
+      w1[k] = __ldg(a.v_1 + static_cast<std::int64_t>(j1c) * (P + 1) + k);
+      w2[k] = __ldg(a.v_2 + static_cast<std::int64_t>(j2c) * (P + 1) + k);
+    }
+  }
+  const std::int64_t N12 = static_cast<std::int64_t>(a.N1) * a.N2;
+  auto plane = [&](int ai) -> double {  // trailing contraction of control plane ai
+    const double* L0 = a.lattice + static_cast<std::int64_t>(ai) * N12;
+    double s = 0.0;
+    if (D == 2) {
+#pragma unroll
+      for (int k = 0; k <= P; ++k) s = fma(w1[k], __ldg(L0 + g1 + k), s);
+    } else {
+#pragma unroll
+      for (int k1 = 0; k1 <= P; ++k1) {
+        const double* Lr = L0 + static_cast<std::int64_t>(g1 + k1) * a.N2 + g2;
+        double r = 0.0;
+#pragma unroll
+        for (int k2 = 0; k2 <= P; ++k2) r = fma(w2[k2], __ldg(Lr + k2), r);
+        s = fma(w1[k1], r, s);
+      }
+    }
+    return s;
+  };
+
+  const StageLayout SL = stage_layout(R, nthr, P);
+  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(sm_raw + S * SL.stage_bytes);
+  const int nchunks = (y1 - y0 + R - 1) / R;
+  const unsigned tx_bytes = static_cast<unsigned>(SL.q_bytes + R * (P + 1) * 8 + R * 4);
+  const int c_inner = D == 2 ? tx * B2 : tx * B2;
+  const int c_mid = D == 2 ? 0 : ty * B1;
+  auto issue = [&](int c) {
+    const int st = c % S;
+    unsigned char* base = sm_raw + st * SL.stage_bytes;
+    mbar_arrive_expect_tx(&bars[st], tx_bytes);
+    if (D == 2)
+      tma_load_2d(base, &map, c_inner, y0 + c * R, &bars[st]);
+    else
+      tma_load_3d(base, &map, c_inner, c_mid, y0 + c * R, &bars[st]);
+    bulk_load_1d(base + SL.v_off, a.v_0 + static_cast<std::int64_t>(y0 + c * R) * (P + 1), R * (P + 1) * 8,
+                 &bars[st]);
+    bulk_load_1d(base + SL.g_off, a.g0_0 + y0 + c * R, R * 4, &bars[st]);
+  };
+  if (tid == 0) {
+    prefetch_tmap(&map);
+    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int c = 0; c < S && c < nchunks; ++c) issue(c);
+
+  // control-plane window Tw[k] = plane(abase + k)
+  int abase = __ldg(a.g0_0 + y0);
+  double Tw[P + 1];
+#pragma unroll
+  for (int k = 0; k <= P; ++k) Tw[k] = active ? plane(abase + k) : 0.0;
+  double l2 = 0.0, li = 0.0;
+  for (int c = 0; c < nchunks; ++c) {
+    const int st = c % S;
+    const unsigned char* base = sm_raw + st * SL.stage_bytes;
+    const double* sq = reinterpret_cast<const double*>(base);
+    const double* sv = reinterpret_cast<const double*>(base + SL.v_off);
+    const int* sg = reinterpret_cast<const int*>(base + SL.g_off);
+    mbar_wait(&bars[st], (c / S) & 1);
+    const int yc = y0 + c * R;
+    const int jn = (y1 - yc) < R ? (y1 - yc) : R;
+    for (int jj = 0; jj < jn; ++jj) {
+      const int g = sg[jj];
+      while (abase < g) {
+#pragma unroll
+        for (int k = 0; k < P; ++k) Tw[k] = Tw[k + 1];
+        ++abase;
+        Tw[P] = active ? plane(abase + P) : 0.0;
+      }
+      const double* vr = sv + jj * (P + 1);
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k <= P; ++k) s = fma(vr[k], Tw[k], s);
+      if (active) {
+        const double q = sq[jj * nthr + tid];
+        const double e = q - s;
+        const std::int64_t gi = static_cast<std::int64_t>(yc + jj) * Tr + t;
+        if (a.err) a.err[gi] = e;
+        l2 = fma(e, e, l2);
+        li = fmax(li, fabs(e));
+      }
+    }
+    __syncthreads();
+    if (tid == 0 && c + S < nchunks) {
+      fence_proxy_async();
+      issue(c + S);
+    }
+  }
+  // CTA reduction -> partial[blockIdx]
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    l2 += __shfl_xor_sync(kFullMask, l2, off);
+    li = fmax(li, __shfl_xor_sync(kFullMask, li, off));
+  }
+  const int wid = tid >> 5;
+  if ((tid & 31) == 0) {
+    s_red[wid] = l2;
+    s_red[32 + wid] = li;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double sl = 0.0, sm2 = 0.0;
+    for (int w = 0; w < (nthr + 31) / 32; ++w) {
+      sl += s_red[w];
+      sm2 = fmax(sm2, s_red[32 + w]);
+    }
+    const std::int64_t cta = static_cast<std::int64_t>(blockIdx.y) * gridDim.x + blockIdx.x;
+    a.partial[2 * cta] = sl;
+    a.partial[2 * cta + 1] = sm2;
+  }
+}
+
+template <int P>
+struct Axis0Launch {
+  static int run(const FitArgs& a, const CUtensorMap& map, const TmaGeom& g, int ntiles, cudaStream_t s) {
+    const StageLayout SL = stage_layout(g.R, g.B1 * g.B2, P);
+    const size_t smem = static_cast<size_t>(g.S) * SL.stage_bytes + g.S * 8;
+    cudaFuncSetAttribute(k_fit_axis0_tma<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    dim3 grid(ntiles, a.nblocks);
+    k_fit_axis0_tma<P><<<grid, g.B1 * g.B2, smem, s>>>(a, map, g);
+    return 1;
+  }
+};
+
+template <int P>
+struct DecodeSweepLaunch {
+  static int run(const DecodeSweepArgs& a, const CUtensorMap& map, const TmaGeom& g, cudaStream_t s) {
+    const StageLayout SL = stage_layout(g.R, g.B1 * g.B2, P);
+    const size_t smem = static_cast<size_t>(g.S) * SL.stage_bytes + g.S * 8;
+    cudaFuncSetAttribute(k_decode_tma<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    dim3 grid(a.ntile1 * a.ntile2, a.nrange);
+    k_decode_tma<P><<<grid, g.B1 * g.B2, smem, s>>>(a, map, g);
+    return 1;
+  }
+};
+
+template <template <int> class F, class... Args>
+int dispatch_p(int p, Args&&... args) {
+  switch (p) {
+    case 1: return F<1>::run(args...);
+    case 2: return F<2>::run(args...);
+    case 3: return F<3>::run(args...);
+    case 4: return F<4>::run(args...);
+    case 5: return F<5>::run(args...);
+    case 6: return F<6>::run(args...);
+    case 7: return F<7>::run(args...);
+    case 8: return F<8>::run(args...);
+    case 9: return F<9>::run(args...);
+    default: return -1;
+  }
+}
+
+}  // namespace
+
+int launch_fit_axis0_tma(int degree, const FitArgs& a, const CUtensorMap& map, const TmaGeom& g, int ntiles,
+                         cudaStream_t s) {
+  return dispatch_p<Axis0Launch>(degree, a, map, g, ntiles, s);
+}
+
+int launch_decode_tma(int degree, const DecodeSweepArgs& a, const CUtensorMap& map, const TmaGeom& g,
+                      cudaStream_t s) {
+  return dispatch_p<DecodeSweepLaunch>(degree, a, map, g, s);
+}
+
+}  // namespace mfb

@@ -351,3 +351,28 @@ def test_solve_host_e2e(ctx):
     r = s.result()
     assert np.array_equal(out_c, r.model.controls)
     assert np.array_equal(out_e, r.global_error)
+
+
+@pytest.mark.parametrize("grid", [(200, 199), (41, 38, 37)])
+def test_odd_extent_fallback_path(ctx, grid):
+    """Odd last extent: field rows are not 16-B multiples, so the TMA passes
+    are not eligible and the generic register-prefetch kernels run."""
+    if len(grid) == 2:
+        cfg = W.Config("odd2", grid, (2, 3), 3, (20, 14), 3, "sinc_radial")
+    else:
+        cfg = W.Config("odd3", grid, (2, 2, 2), 2, (7, 7, 6), 2, "sinc_radial")
+    values = W.make_field_numpy(cfg)
+    g, o, _ = run_both(cfg, values)
+    assert_solve_parity(g, o)
+
+
+def test_tma_and_generic_paths_agree(ctx, monkeypatch):
+    cfg = SMALL["C5s"]
+    values = W.make_field_numpy(cfg)
+    g_tma, o, _ = run_both(cfg, values)
+    monkeypatch.setenv("MFADD_NO_TMA", "1")
+    g_gen, _, _ = run_both(cfg, values)
+    assert_solve_parity(g_tma, o)
+    assert_solve_parity(g_gen, o)
+    # identical arithmetic order in both paths for the fit: bitwise-equal lattices
+    assert np.array_equal(g_tma.blocks[0].p, g_gen.blocks[0].p)
