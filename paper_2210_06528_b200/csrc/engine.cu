@@ -281,14 +281,17 @@ struct Workload {
       if (D == 3) mx2 = std::max(mx2, probs[static_cast<std::size_t>(b.ax[2])].m);
     }
     if (field_dims[static_cast<std::size_t>(D - 1)] % 2 != 0) return;  // row stride not 16-B aligned
+    // B2 is the TMA box width W (even); it includes one spare column so the
+    // box can start on an even (16-B aligned) column (stream_tma.cu).
     if (D == 2) {
-      const int nt = (mx1 + 255) / 256;
-      axis0_geo.B2 = round_up((mx1 + nt - 1) / nt, 2);
+      const int nt = (mx1 + 253) / 254;
+      const int cols = round_up((mx1 + nt - 1) / nt, 2);
+      axis0_geo.B2 = cols + 2;
       axis0_geo.B1 = 1;
-      axis0_tiles = (mx1 + axis0_geo.B2 - 1) / axis0_geo.B2;
+      axis0_tiles = (mx1 + cols - 1) / cols;
     } else {
-      if (mx2 > 256) return;
-      axis0_geo.B2 = round_up(mx2, 2);
+      if (mx2 + 1 > 256) return;
+      axis0_geo.B2 = round_up(mx2 + 1, 2);
       axis0_geo.B1 = std::max(1, 256 / axis0_geo.B2);
       axis0_tiles = (mx1 + axis0_geo.B1 - 1) / axis0_geo.B1;
     }

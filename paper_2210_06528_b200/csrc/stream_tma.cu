@@ -53,32 +53,42 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
   const int D = a.D;
   const int m1 = a.probs[blk.ax[1]].m;
   const int m2 = D == 3 ? a.probs[blk.ax[2]].m : 1;
-  const int B1 = geo.B1, B2 = geo.B2, R = geo.R, S = geo.S;
-  const int nthr = B1 * B2;
+  // Box: W inner columns (even, 16-B multiple) x [B1] x R rows.  TMA tile
+  // loads need a 16-B aligned innermost start coordinate, so the box starts
+  // at the even column at or below the block's first column and the thread
+  // -> column map is shifted by that parity (geo.B2 = W, one spare column).
+  const int B1 = geo.B1, W = geo.B2, R = geo.R, S = geo.S;
+  const int nthr = B1 * W;
   const int tile = blockIdx.x;
   const int tid = threadIdx.x;
-  int j1, j2;
+  const AxisProb p1 = a.probs[blk.ax[1]];
+  const int in0 = static_cast<int>(pr.in_lo);
+  int j1, j2, c_inner, c_mid;
+  bool active;
   if (D == 2) {
-    if (tile * B2 >= m1) return;
-    j1 = tile * B2 + tid;
+    const int cols = W - 2;  // columns owned per tile
+    if (tile * cols >= m1) return;
+    const int first = static_cast<int>(p1.in_lo) + tile * cols;
+    c_inner = first & ~1;
+    c_mid = 0;
+    j1 = tile * cols + tid - (first - c_inner);
     j2 = 0;
+    active = j1 >= tile * cols && j1 < tile * cols + cols && j1 < m1;
   } else {
     if (tile * B1 >= m1) return;
-    j1 = tile * B1 + tid / B2;
-    j2 = tid % B2;
+    const int in2 = static_cast<int>(a.probs[blk.ax[2]].in_lo);
+    c_inner = in2 & ~1;
+    c_mid = static_cast<int>(p1.in_lo) + tile * B1;
+    j1 = tile * B1 + tid / W;
+    j2 = tid % W - (in2 - c_inner);
+    active = j1 < m1 && j2 >= 0 && j2 < m2;
   }
-  const bool active = (D == 2) ? (j1 < m1) : (j1 < m1 && j2 < m2);
   const std::int64_t Tr = static_cast<std::int64_t>(m1) * m2;
-  const std::int64_t t = static_cast<std::int64_t>(j1) * m2 + j2;
+  const std::int64_t t = active ? static_cast<std::int64_t>(j1) * m2 + j2 : 0;
   double* dst = a.t1 + blk.t1off + t;  // T1[i0][Tr]
   const int* g0g = a.g0 + pr.row_off;
   const double* vg = a.vals + pr.row_off * (P + 1);
   const double* lt = a.ltab + pr.col_off * (2 * P + 1);
-  // global coordinates of this CTA's box origin
-  const AxisProb p1 = a.probs[blk.ax[1]];
-  const int in0 = static_cast<int>(pr.in_lo);
-  const int c_inner = D == 2 ? static_cast<int>(p1.in_lo) + tile * B2 : static_cast<int>(a.probs[blk.ax[2]].in_lo);
-  const int c_mid = D == 2 ? 0 : static_cast<int>(p1.in_lo) + tile * B1;
 
   const StageLayout SL = stage_layout(R, nthr, P);
   std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(sm_raw + S * SL.stage_bytes);
