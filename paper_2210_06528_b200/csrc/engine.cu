@@ -295,7 +295,7 @@ struct Workload {
       axis0_geo.B1 = std::max(1, 256 / axis0_geo.B2);
       axis0_tiles = (mx1 + axis0_geo.B1 - 1) / axis0_geo.B1;
     }
-    axis0_geo.R = 16;
+    axis0_geo.R = 8;
     axis0_geo.S = 4;
     tma_axis0 = true;
   }
@@ -901,7 +901,7 @@ MFB_API int mfadd_solver_create(mfadd_context* ctx, const mfadd_decomposition* d
       const int nt = (inner + 255) / 256;
       s->dgeo.B2 = round_up((inner + nt - 1) / nt, 2);
       s->dgeo.B1 = D == 2 ? 1 : std::max(1, 256 / s->dgeo.B2);
-      s->dgeo.R = 16;
+      s->dgeo.R = 8;
       s->dgeo.S = 4;
       s->dnt2 = (inner + s->dgeo.B2 - 1) / s->dgeo.B2;
       s->dnt1 = D == 2 ? 1 : (M1 + s->dgeo.B1 - 1) / s->dgeo.B1;
@@ -1095,6 +1095,7 @@ void solve_impl(mfadd_solver* s, const double* dfield) {
     ds.M0 = static_cast<int>(d.grid[0]);
     ds.M1 = static_cast<int>(d.grid[1]);
     ds.M2 = d.rank == 3 ? static_cast<int>(d.grid[2]) : 1;
+    ds.N0 = static_cast<int>(d.n_ctrl[0]);
     ds.N1 = static_cast<int>(d.n_ctrl[1]);
     ds.N2 = d.rank == 3 ? static_cast<int>(d.n_ctrl[2]) : 1;
     ds.ntile1 = s->dnt1;

@@ -158,7 +158,7 @@ int launch_fit_axis0_tma(int degree, const FitArgs& a, const CUtensorMap& map, c
 struct DecodeSweepArgs {
   int D;
   int M0, M1, M2;   // input grid extents (M2 = 1 for D = 2)
-  int N1, N2;       // lattice trailing extents (N2 = 1 for D = 2)
+  int N0, N1, N2;   // lattice extents (N2 = 1 for D = 2)
   int ntile1, ntile2, nrange, H;
   const int* g0_0;  // global decode rows per dim (row tables, 16-B aligned)
   const double* v_0;

@@ -121,6 +121,34 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
   for (int k = 0; k < P; ++k) yw[k] = 0.0;
   int cbase = __ldg(g0g) < 0 ? __ldg(g0g) : 0;
   const std::int64_t dstr = Tr;
+  // Forward coefficients of the next column to flush, fetched one flush
+  // ahead so the L2 round trip overlaps the row loop.
+  double Lnx[P + 1];
+  auto fetch_fwd = [&](int cc, double* L) {
+    const int cl = cc < 0 ? 0 : (cc >= n ? n - 1 : cc);
+    const double* Lc = lt + static_cast<std::int64_t>(cl) * (2 * P + 1);
+#pragma unroll
+    for (int k = 0; k <= P; ++k) L[k] = __ldg(Lc + k);
+  };
+  fetch_fwd(cbase, Lnx);
+  auto flush = [&]() {
+    const int cc = cbase;
+    if (cc >= 0 && cc < n) {  // forward substitution of column cc
+      double s = acc[0];
+#pragma unroll
+      for (int k = 1; k <= P; ++k) s = fma(-Lnx[k], yw[k - 1], s);
+      const double y = s * Lnx[0];
+      if (active) dst[static_cast<std::int64_t>(cc) * dstr] = y;
+#pragma unroll
+      for (int k = P - 1; k >= 1; --k) yw[k] = yw[k - 1];
+      yw[0] = y;
+    }
+#pragma unroll
+    for (int k = 0; k < P; ++k) acc[k] = acc[k + 1];
+    acc[P] = 0.0;
+    ++cbase;
+    fetch_fwd(cbase, Lnx);
+  };
 
   for (int c = 0; c < nchunks; ++c) {
     const int st = c % S;
@@ -132,24 +160,7 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
     const int jn = (m - c * R) < R ? (m - c * R) : R;
     for (int jj = 0; jj < jn; ++jj) {
       const int g = sg[jj];
-      while (cbase < g) {
-        const int cc = cbase;
-        if (cc >= 0 && cc < n) {  // forward substitution of column cc
-          const double* Lc = lt + static_cast<std::int64_t>(cc) * (2 * P + 1);
-          double s = acc[0];
-#pragma unroll
-          for (int k = 1; k <= P; ++k) s = fma(-__ldg(Lc + k), yw[k - 1], s);
-          const double y = s * __ldg(Lc);
-          if (active) dst[static_cast<std::int64_t>(cc) * dstr] = y;
-#pragma unroll
-          for (int k = P - 1; k >= 1; --k) yw[k] = yw[k - 1];
-          yw[0] = y;
-        }
-#pragma unroll
-        for (int k = 0; k < P; ++k) acc[k] = acc[k + 1];
-        acc[P] = 0.0;
-        ++cbase;
-      }
+      while (cbase < g) flush();
       const double q = sq[jj * nthr + tid];
       const double* vr = sv + jj * (P + 1);
 #pragma unroll
@@ -161,24 +172,7 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
       issue(c + S);
     }
   }
-  while (cbase < n) {
-    const int cc = cbase;
-    if (cc >= 0) {
-      const double* Lc = lt + static_cast<std::int64_t>(cc) * (2 * P + 1);
-      double s = acc[0];
-#pragma unroll
-      for (int k = 1; k <= P; ++k) s = fma(-__ldg(Lc + k), yw[k - 1], s);
-      const double y = s * __ldg(Lc);
-      if (active) dst[static_cast<std::int64_t>(cc) * dstr] = y;
-#pragma unroll
-      for (int k = P - 1; k >= 1; --k) yw[k] = yw[k - 1];
-      yw[0] = y;
-    }
-#pragma unroll
-    for (int k = 0; k < P; ++k) acc[k] = acc[k + 1];
-    acc[P] = 0.0;
-    ++cbase;
-  }
+  while (cbase < n) flush();
   // Back substitution in place, y values prefetched 8 columns ahead.
   if (!active) return;
   constexpr int PF = 8;
@@ -188,18 +182,26 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
   double xw[P];
 #pragma unroll
   for (int k = 0; k < P; ++k) xw[k] = 0.0;
+  double Lb[P + 1];  // backward coefficients of the current column, fetched ahead
+  auto fetch_bwd = [&](int c, double* L) {
+    const double* Lc = lt + static_cast<std::int64_t>(c < 0 ? 0 : c) * (2 * P + 1);
+    L[0] = __ldg(Lc);
+#pragma unroll
+    for (int k = 1; k <= P; ++k) L[k] = __ldg(Lc + P + k);
+  };
+  fetch_bwd(n - 1, Lb);
   for (int c0 = n - 1; c0 >= 0; c0 -= PF) {
 #pragma unroll
     for (int u = 0; u < PF; ++u) {
       const int c = c0 - u;
       if (c >= 0) {
-        const double* Lc = lt + static_cast<std::int64_t>(c) * (2 * P + 1);
         double s = yr[u];
         const int cn = c - PF;
         yr[u] = cn >= 0 ? dst[static_cast<std::int64_t>(cn) * dstr] : 0.0;
 #pragma unroll
-        for (int k = 1; k <= P; ++k) s = fma(-__ldg(Lc + P + k), xw[k - 1], s);
-        const double x = s * __ldg(Lc);
+        for (int k = 1; k <= P; ++k) s = fma(-Lb[k], xw[k - 1], s);
+        const double x = s * Lb[0];
+        fetch_bwd(c - 1, Lb);
         dst[static_cast<std::int64_t>(c) * dstr] = x;
 #pragma unroll
         for (int k = P - 1; k >= 1; --k) xw[k] = xw[k - 1];
@@ -298,11 +300,45 @@ __global__ void __launch_bounds__(256) k_decode_tma(const DecodeSweepArgs a, con
   if (tid == 0)
     for (int c = 0; c < S && c < nchunks; ++c) issue(c);
 
-  // control-plane window Tw[k] = plane(abase + k)
+  // control-plane window Tw[k] = plane(abase + k); the lattice values of the
+  // next plane (abase + P + 1) are loaded one shift ahead (L2 latency hidden).
   int abase = __ldg(a.g0_0 + y0);
   double Tw[P + 1];
 #pragma unroll
   for (int k = 0; k <= P; ++k) Tw[k] = active ? plane(abase + k) : 0.0;
+  constexpr int NV = (P + 1) * (P + 1);
+  double nxt[NV];
+  auto fetch_plane = [&](int ai) {
+    const int a2 = ai < a.N0 ? ai : a.N0 - 1;
+    const double* L0 = a.lattice + static_cast<std::int64_t>(a2) * N12;
+    if (D == 2) {
+#pragma unroll
+      for (int k = 0; k <= P; ++k) nxt[k] = __ldg(L0 + g1 + k);
+    } else {
+#pragma unroll
+      for (int k1 = 0; k1 <= P; ++k1)
+#pragma unroll
+        for (int k2 = 0; k2 <= P; ++k2)
+          nxt[k1 * (P + 1) + k2] = __ldg(L0 + static_cast<std::int64_t>(g1 + k1) * a.N2 + g2 + k2);
+    }
+  };
+  auto reduce_plane = [&]() -> double {
+    double s = 0.0;
+    if (D == 2) {
+#pragma unroll
+      for (int k = 0; k <= P; ++k) s = fma(w1[k], nxt[k], s);
+    } else {
+#pragma unroll
+      for (int k1 = 0; k1 <= P; ++k1) {
+        double r = 0.0;
+#pragma unroll
+        for (int k2 = 0; k2 <= P; ++k2) r = fma(w2[k2], nxt[k1 * (P + 1) + k2], r);
+        s = fma(w1[k1], r, s);
+      }
+    }
+    return s;
+  };
+  if (active) fetch_plane(abase + P + 1);
   double l2 = 0.0, li = 0.0;
   for (int c = 0; c < nchunks; ++c) {
     const int st = c % S;
@@ -319,7 +355,8 @@ __global__ void __launch_bounds__(256) k_decode_tma(const DecodeSweepArgs a, con
 #pragma unroll
         for (int k = 0; k < P; ++k) Tw[k] = Tw[k + 1];
         ++abase;
-        Tw[P] = active ? plane(abase + P) : 0.0;
+        Tw[P] = active ? reduce_plane() : 0.0;
+        if (active) fetch_plane(abase + P + 1);
       }
       const double* vr = sv + jj * (P + 1);
       double s = 0.0;
