@@ -1039,8 +1039,13 @@ void solve_impl(mfadd_solver* s, const double* dfield) {
     }
   }
   CK(cudaEventRecord(s->ev[3], st));
-  // ---- final jumps per neighbour pair (solver.cpp:416)
-  if (s->npairs > 0) {
+  // ---- final jumps per neighbour pair (solver.cpp:416).  When the last
+  // epoch averaged every shared control (mode 2), all copies of each control
+  // are bit-identical, so every per-pair jump is exactly 0: skip the pass.
+  const bool last_all = !s->epochs.empty() && s->epochs.back().iteration >= 2;
+  if (s->npairs > 0 && last_all) {
+    CK(cudaMemsetAsync(s->pair_jumps.p, 0, s->pair_jumps.n * sizeof(unsigned long long), st));
+  } else if (s->npairs > 0) {
     CK(cudaMemsetAsync(s->pair_jumps.p, 0, s->pair_jumps.n * sizeof(unsigned long long), st));
     s->tl.begin("pair_jumps");
     launches += mfb::launch_epoch(epoch_args(s, 3), st);

@@ -192,26 +192,46 @@ __global__ void __launch_bounds__(256) k_gram_chol(CholArgs a) {
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    // Banded left-looking Cholesky, in place; sm[c*(P+1)] keeps 1/L(c,c)
-    // during the sweep and L(c,c) is recovered when the table is written.
+    // Banded left-looking Cholesky with the last P rows of L held in a
+    // register window: Lw[r] = row (c-1-r), Lw[r][0] = 1/L(row,row),
+    // Lw[r][k] = L(row, row-k).  Row c is written back over sm[c*(P+1)..].
+    double Lw[P][P + 1];
+#pragma unroll
+    for (int r = 0; r < P; ++r)
+#pragma unroll
+      for (int k = 0; k <= P; ++k) Lw[r][k] = 0.0;
     for (int c = 0; c < n; ++c) {
-      double* Lc = sm + c * (P + 1);
-      const int kmax = c < P ? c : P;
-      for (int k = kmax; k >= 1; --k) {
-        const int j = c - k;
-        const double* Lj = sm + j * (P + 1);
-        double s = Lc[k];
-        const int t0 = c - P > 0 ? c - P : 0;
-        for (int t = t0; t < j; ++t) s = fma(-Lc[c - t], Lj[j - t], s);
-        Lc[k] = s * Lj[0];  // * 1/L(j,j)
+      double* Gc = sm + c * (P + 1);
+      double Lc[P + 1];
+#pragma unroll
+      for (int k = 0; k <= P; ++k) Lc[k] = Gc[k];
+#pragma unroll
+      for (int k = P; k >= 1; --k) {
+        if (c - k < 0) {
+          Lc[k] = 0.0;
+          continue;
+        }
+        double sacc = Lc[k];
+#pragma unroll
+        for (int t = k + 1; t <= P; ++t) sacc = fma(-Lc[t], Lw[k - 1][t - k], sacc);
+        Lc[k] = sacc * Lw[k - 1][0];  // * 1/L(j,j), j = c-k
       }
       double dg = Lc[0];
-      for (int k = 1; k <= kmax; ++k) dg = fma(-Lc[k], Lc[k], dg);
+#pragma unroll
+      for (int k = 1; k <= P; ++k) dg = fma(-Lc[k], Lc[k], dg);
       if (!(dg > 0.0)) {  // Eigen LLT NumericalIssue -> SingularFitError
         set_status(a.status, 3, pid, c);
         dg = 1.0;
       }
       Lc[0] = 1.0 / sqrt(dg);
+#pragma unroll
+      for (int k = 0; k <= P; ++k) Gc[k] = Lc[k];
+#pragma unroll
+      for (int r = P - 1; r >= 1; --r)
+#pragma unroll
+        for (int k = 0; k <= P; ++k) Lw[r][k] = Lw[r - 1][k];
+#pragma unroll
+      for (int k = 0; k <= P; ++k) Lw[0][k] = Lc[k];
     }
   }
   __syncthreads();
@@ -639,6 +659,132 @@ __global__ void __launch_bounds__(kEpochThreads) k_epoch(EpochArgs a) {
   }
 }
 
+// Common case: every control has <= 2 holders per axis (n_s <= 8).  Holder
+// loops are fully unrolled (registers, no local memory) and the per-(dim,
+// coordinate) window tables and block offsets live in shared memory.
+constexpr int kMaxCoords = 128;
+
+__global__ void __launch_bounds__(kEpochThreads) k_epoch8(EpochArgs a) {
+  __shared__ unsigned long long s_change[kEpochSmemBlocks];
+  __shared__ unsigned long long s_linf[kEpochSmemBlocks];
+  __shared__ long long s_poff[kEpochSmemBlocks];
+  __shared__ int s_lo[3][kMaxCoords], s_n[3][kMaxCoords];
+  const int tid = threadIdx.x;
+  for (int i = tid; i < a.nblocks; i += blockDim.x) {
+    s_change[i] = 0ull;
+    s_linf[i] = 0ull;
+    s_poff[i] = a.poff[i];
+  }
+  for (int k = 0; k < a.D; ++k)
+    for (int c = tid; c < a.B[k]; c += blockDim.x) {
+      const AxisProb pk = a.probs[a.axbase[k] + c];
+      s_lo[k][c] = static_cast<int>(pk.col_lo);
+      s_n[k][c] = pk.n;
+    }
+  __syncthreads();
+  const bool measure = a.mode == 0, pairs = a.mode == 3;
+  unsigned long long jss = 0ull, jms = 0ull;
+  const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+  for (std::int64_t g = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + tid; g < a.total; g += stride) {
+    std::int64_t idx[3] = {0, 0, 0};
+    if (!piece_index(a, g, idx)) continue;
+    int f[3] = {0, 0, 0}, e[3] = {1, 1, 1};
+    int ns = 1;
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      if (k < a.D) {
+        const int2 r = a.hr[a.hr_off[k] + idx[k]];
+        f[k] = r.x;
+        e[k] = r.y - r.x + 1;
+        ns *= e[k];
+      }
+    double v[8];
+    int ids[8];
+    long long off[8];
+#pragma unroll
+    for (int h = 0; h < 8; ++h) {
+      ids[h] = 0;
+      off[h] = 0;
+      v[h] = 0.0;
+      if (h < ns) {
+        int c[3] = {0, 0, 0}, rr = h;
+#pragma unroll
+        for (int k = 2; k >= 0; --k)
+          if (k < a.D) {
+            c[k] = f[k] + (e[k] == 2 ? (rr & 1) : 0);
+            rr = e[k] == 2 ? (rr >> 1) : rr;
+          }
+        int id = 0;
+        long long o = 0;
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+          if (k < a.D) {
+            id = id * a.B[k] + c[k];
+            o = o * s_n[k][c[k]] + (idx[k] - s_lo[k][c[k]]);
+          }
+        ids[h] = id;
+        off[h] = s_poff[id] + o;
+        v[h] = a.P[off[h]];
+      }
+    }
+    if (pairs) {  // final per-pair jumps (solver.cpp:416 -> :166-193)
+#pragma unroll
+      for (int h1 = 0; h1 < 8; ++h1)
+#pragma unroll
+        for (int h2 = h1 + 1; h2 < 8; ++h2)
+          if (h2 < ns) {
+            int code;
+            if (!neighbour_code(a, ids[h1], ids[h2], &code)) continue;
+            const int slot = a.pair_slot[ids[h1] * 27 + code];
+            if (slot >= 0) atomicMax(a.pair_jumps + 2 * slot + (ns > 2 ? 1 : 0), dbits(fabs(v[h1] - v[h2])));
+          }
+      continue;
+    }
+    const bool update = !measure && (a.mode == 2 || ns == 2);
+    if (update) {
+      // solver.cpp:147-159: ordered sum in ascending holder id, divide once
+      double sum = 0.0;
+#pragma unroll
+      for (int h = 0; h < 8; ++h)
+        if (h < ns) sum = __dadd_rn(sum, v[h]);
+      const double avg = __ddiv_rn(sum, static_cast<double>(ns));
+      const unsigned long long la = dbits(fabs(avg));
+#pragma unroll
+      for (int h = 0; h < 8; ++h)
+        if (h < ns) {
+          a.P[off[h]] = avg;
+          atomicMax(s_change + ids[h], dbits(fabs(avg - v[h])));
+          atomicMax(s_linf + ids[h], la);
+        }
+    } else {
+      double mn = v[0], mx = v[0];
+#pragma unroll
+      for (int h = 0; h < 8; ++h)
+        if (h < ns) {
+          mn = fmin(mn, v[h]);
+          mx = fmax(mx, v[h]);
+          atomicMax(s_linf + ids[h], dbits(fabs(v[h])));
+        }
+      if (ns == 2)
+        jss = umax(jss, dbits(mx - mn));
+      else
+        jms = umax(jms, dbits(mx - mn));
+    }
+  }
+  if (pairs) return;
+  jss = warp_umax(jss);
+  jms = warp_umax(jms);
+  if ((tid & 31) == 0) {
+    if (jss) atomicMax(&a.acc->jump_ss, jss);
+    if (jms) atomicMax(&a.acc->jump_ms, jms);
+  }
+  __syncthreads();
+  for (int i = tid; i < a.nblocks; i += blockDim.x) {
+    if (s_change[i]) atomicMax(a.change + i, s_change[i]);
+    if (s_linf[i]) atomicMax(a.linf_sh + i, s_linf[i]);
+  }
+}
+
 // ------------------------------------------------------------------- K5
 __global__ void __launch_bounds__(1024) k_dp(DpArgs a) {
   __shared__ unsigned long long red[32];
@@ -931,7 +1077,11 @@ int launch_epoch(const EpochArgs& a, cudaStream_t s) {
   std::int64_t want = (a.total + kEpochThreads - 1) / kEpochThreads;
   const std::int64_t cap = static_cast<std::int64_t>(sms) * 4;
   const unsigned grid = static_cast<unsigned>(want < cap ? want : cap);
-  if (a.max_holders <= 8)
+  bool small = a.nblocks <= kEpochSmemBlocks;
+  for (int k = 0; k < a.D; ++k) small = small && a.B[k] <= kMaxCoords;
+  if (a.max_holders <= 8 && small)
+    k_epoch8<<<grid, kEpochThreads, 0, s>>>(a);
+  else if (a.max_holders <= 8)
     k_epoch<8><<<grid, kEpochThreads, 0, s>>>(a);
   else
     k_epoch<27><<<grid, kEpochThreads, 0, s>>>(a);

@@ -212,12 +212,11 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
 }
 
 // ---------------------------------------------------------------- decode
-template <int P>
+template <int P, int D>
 __global__ void __launch_bounds__(256) k_decode_tma(const DecodeSweepArgs a, const __grid_constant__ CUtensorMap map,
                                                     const TmaGeom geo) {
   extern __shared__ __align__(128) unsigned char sm_raw[];
   __shared__ double s_red[64];
-  const int D = a.D;
   const int B1 = geo.B1, B2 = geo.B2, R = geo.R, S = geo.S;
   const int nthr = B1 * B2;
   const int tid = threadIdx.x;
@@ -306,7 +305,7 @@ __global__ void __launch_bounds__(256) k_decode_tma(const DecodeSweepArgs a, con
   double Tw[P + 1];
 #pragma unroll
   for (int k = 0; k <= P; ++k) Tw[k] = active ? plane(abase + k) : 0.0;
-  constexpr int NV = (P + 1) * (P + 1);
+  constexpr int NV = D == 2 ? (P + 1) : (P + 1) * (P + 1);
   double nxt[NV];
   auto fetch_plane = [&](int ai) {
     const int a2 = ai < a.N0 ? ai : a.N0 - 1;
@@ -319,7 +318,7 @@ __global__ void __launch_bounds__(256) k_decode_tma(const DecodeSweepArgs a, con
       for (int k1 = 0; k1 <= P; ++k1)
 #pragma unroll
         for (int k2 = 0; k2 <= P; ++k2)
-          nxt[k1 * (P + 1) + k2] = __ldg(L0 + static_cast<std::int64_t>(g1 + k1) * a.N2 + g2 + k2);
+          nxt[(k1 * (P + 1) + k2) % NV] = __ldg(L0 + static_cast<std::int64_t>(g1 + k1) * a.N2 + g2 + k2);
     }
   };
   auto reduce_plane = [&]() -> double {
@@ -332,7 +331,7 @@ __global__ void __launch_bounds__(256) k_decode_tma(const DecodeSweepArgs a, con
       for (int k1 = 0; k1 <= P; ++k1) {
         double r = 0.0;
 #pragma unroll
-        for (int k2 = 0; k2 <= P; ++k2) r = fma(w2[k2], nxt[k1 * (P + 1) + k2], r);
+        for (int k2 = 0; k2 <= P; ++k2) r = fma(w2[k2], nxt[(k1 * (P + 1) + k2) % NV], r);
         s = fma(w1[k1], r, s);
       }
     }
@@ -418,9 +417,14 @@ struct DecodeSweepLaunch {
   static int run(const DecodeSweepArgs& a, const CUtensorMap& map, const TmaGeom& g, cudaStream_t s) {
     const StageLayout SL = stage_layout(g.R, g.B1 * g.B2, P);
     const size_t smem = static_cast<size_t>(g.S) * SL.stage_bytes + g.S * 8;
-    cudaFuncSetAttribute(k_decode_tma<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     dim3 grid(a.ntile1 * a.ntile2, a.nrange);
-    k_decode_tma<P><<<grid, g.B1 * g.B2, smem, s>>>(a, map, g);
+    if (a.D == 2) {
+      cudaFuncSetAttribute(k_decode_tma<P, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      k_decode_tma<P, 2><<<grid, g.B1 * g.B2, smem, s>>>(a, map, g);
+    } else {
+      cudaFuncSetAttribute(k_decode_tma<P, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      k_decode_tma<P, 3><<<grid, g.B1 * g.B2, smem, s>>>(a, map, g);
+    }
     return 1;
   }
 };
