@@ -664,6 +664,39 @@ __global__ void __launch_bounds__(kEpochThreads) k_epoch(EpochArgs a) {
 // coordinate) window tables and block offsets live in shared memory.
 constexpr int kMaxCoords = 128;
 
+// 32-bit piece decomposition (every extent and piece count < 2^31).
+__device__ __forceinline__ bool piece_index32(const EpochArgs& a, unsigned g, int* idx) {
+  int pc = 0;
+  while (pc < a.D && g >= static_cast<unsigned>(a.piece[pc])) {
+    g -= static_cast<unsigned>(a.piece[pc]);
+    ++pc;
+  }
+  if (pc >= a.D) return false;
+  for (int k = a.D - 1; k >= 0; --k) {
+    const unsigned ext = static_cast<unsigned>(k < pc ? a.nC[k] : (k == pc ? a.nS[k] : a.N[k]));
+    const unsigned q = g / ext, r = g - q * ext;
+    g = q;
+    idx[k] = k < pc ? a.clist[a.c_off[k] + r] : (k == pc ? a.slist[a.s_off[k] + r] : static_cast<int>(r));
+  }
+  return true;
+}
+
+// Max-reduce `val` into slot[key] for the whole warp: one shared atomic per
+// warp when all participating lanes share the key (the common case), else
+// one per lane.  key < 0 marks a non-participating lane.
+__device__ __forceinline__ void warp_atomic_max(unsigned long long* slot, int key, unsigned long long val) {
+  const unsigned part = __ballot_sync(kFull, key >= 0);
+  if (!part) return;
+  const int leader = __ffs(part) - 1;
+  const int keyL = __shfl_sync(kFull, key, leader);
+  if (__all_sync(kFull, key < 0 || key == keyL)) {
+    val = warp_umax(key < 0 ? 0ull : val);
+    if ((threadIdx.x & 31) == leader && val) atomicMax(slot + keyL, val);
+  } else if (key >= 0 && val) {
+    atomicMax(slot + key, val);
+  }
+}
+
 __global__ void __launch_bounds__(kEpochThreads) k_epoch8(EpochArgs a) {
   __shared__ unsigned long long s_change[kEpochSmemBlocks];
   __shared__ unsigned long long s_linf[kEpochSmemBlocks];
@@ -684,15 +717,18 @@ __global__ void __launch_bounds__(kEpochThreads) k_epoch8(EpochArgs a) {
   __syncthreads();
   const bool measure = a.mode == 0, pairs = a.mode == 3;
   unsigned long long jss = 0ull, jms = 0ull;
-  const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
-  for (std::int64_t g = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + tid; g < a.total; g += stride) {
-    std::int64_t idx[3] = {0, 0, 0};
-    if (!piece_index(a, g, idx)) continue;
+  const unsigned total = static_cast<unsigned>(a.total);
+  const unsigned stride = gridDim.x * blockDim.x;
+  // warp-uniform trip count so the warp collectives below see all lanes
+  for (unsigned g0 = blockIdx.x * blockDim.x + (tid & ~31u); g0 < total; g0 += stride) {
+    const unsigned g = g0 + (tid & 31);
+    int idx[3] = {0, 0, 0};
+    const bool valid = g < total && piece_index32(a, g, idx);
     int f[3] = {0, 0, 0}, e[3] = {1, 1, 1};
-    int ns = 1;
+    int ns = valid ? 1 : 0;
 #pragma unroll
     for (int k = 0; k < 3; ++k)
-      if (k < a.D) {
+      if (valid && k < a.D) {
         const int2 r = a.hr[a.hr_off[k] + idx[k]];
         f[k] = r.x;
         e[k] = r.y - r.x + 1;
@@ -703,7 +739,7 @@ __global__ void __launch_bounds__(kEpochThreads) k_epoch8(EpochArgs a) {
     long long off[8];
 #pragma unroll
     for (int h = 0; h < 8; ++h) {
-      ids[h] = 0;
+      ids[h] = -1;
       off[h] = 0;
       v[h] = 0.0;
       if (h < ns) {
@@ -740,7 +776,8 @@ __global__ void __launch_bounds__(kEpochThreads) k_epoch8(EpochArgs a) {
           }
       continue;
     }
-    const bool update = !measure && (a.mode == 2 || ns == 2);
+    const bool update = !measure && ns >= 2 && (a.mode == 2 || ns == 2);
+    unsigned long long ch[8], lv[8];
     if (update) {
       // solver.cpp:147-159: ordered sum in ascending holder id, divide once
       double sum = 0.0;
@@ -750,25 +787,32 @@ __global__ void __launch_bounds__(kEpochThreads) k_epoch8(EpochArgs a) {
       const double avg = __ddiv_rn(sum, static_cast<double>(ns));
       const unsigned long long la = dbits(fabs(avg));
 #pragma unroll
-      for (int h = 0; h < 8; ++h)
-        if (h < ns) {
-          a.P[off[h]] = avg;
-          atomicMax(s_change + ids[h], dbits(fabs(avg - v[h])));
-          atomicMax(s_linf + ids[h], la);
-        }
+      for (int h = 0; h < 8; ++h) {
+        ch[h] = h < ns ? dbits(fabs(avg - v[h])) : 0ull;
+        lv[h] = h < ns ? la : 0ull;
+        if (h < ns) a.P[off[h]] = avg;
+      }
     } else {
       double mn = v[0], mx = v[0];
 #pragma unroll
-      for (int h = 0; h < 8; ++h)
+      for (int h = 0; h < 8; ++h) {
         if (h < ns) {
           mn = fmin(mn, v[h]);
           mx = fmax(mx, v[h]);
-          atomicMax(s_linf + ids[h], dbits(fabs(v[h])));
         }
+        ch[h] = 0ull;
+        lv[h] = h < ns ? dbits(fabs(v[h])) : 0ull;
+      }
       if (ns == 2)
         jss = umax(jss, dbits(mx - mn));
-      else
+      else if (ns > 2)
         jms = umax(jms, dbits(mx - mn));
+    }
+#pragma unroll
+    for (int h = 0; h < 8; ++h) {
+      if (!__any_sync(kFull, h < ns)) break;
+      if (!measure) warp_atomic_max(s_change, ids[h], ch[h]);
+      warp_atomic_max(s_linf, ids[h], lv[h]);
     }
   }
   if (pairs) return;
