@@ -25,6 +25,11 @@ namespace {
 
 constexpr unsigned kFullMask = 0xffffffffu;
 
+template <int V>
+struct Int {
+  static constexpr int value = V;
+};
+
 struct StageLayout {
   int q_bytes;     // R * nthr * 8 (the full TMA box)
   int v_off;       // offset of basis values in the stage
@@ -121,50 +126,90 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
   for (int k = 0; k < P; ++k) yw[k] = 0.0;
   int cbase = __ldg(g0g) < 0 ? __ldg(g0g) : 0;
   const std::int64_t dstr = Tr;
-  // Forward coefficients of the next column to flush, fetched one flush
-  // ahead so the L2 round trip overlaps the row loop.
-  double Lnx[P + 1];
-  auto fetch_fwd = [&](int cc, double* L) {
+  // Sliding window without register rotation: slot (ph + k) % (P+1) holds
+  // column cbase + k.  `ph` is warp-uniform, so the two switch statements
+  // below pick fully static register indices (no per-row window moves).
+  int ph = 0;
+  double Lnx[P + 1];  // forward coefficients of column cbase, fetched one flush ahead
+  auto fetch_fwd = [&](int cc) {
     const int cl = cc < 0 ? 0 : (cc >= n ? n - 1 : cc);
     const double* Lc = lt + static_cast<std::int64_t>(cl) * (2 * P + 1);
 #pragma unroll
-    for (int k = 0; k <= P; ++k) L[k] = __ldg(Lc + k);
+    for (int k = 0; k <= P; ++k) Lnx[k] = __ldg(Lc + k);
   };
-  fetch_fwd(cbase, Lnx);
-  auto flush = [&]() {
+  fetch_fwd(cbase);
+  // Complete column cbase (slot PH): forward substitution, then recycle the
+  // slot for column cbase + P + 1.
+  auto flush_slot = [&](auto phc) {
+    constexpr int PH = decltype(phc)::value;
     const int cc = cbase;
-    if (cc >= 0 && cc < n) {  // forward substitution of column cc
-      double s = acc[0];
+    if (cc >= 0 && cc < n) {
+      double sacc = acc[PH];
 #pragma unroll
-      for (int k = 1; k <= P; ++k) s = fma(-Lnx[k], yw[k - 1], s);
-      const double y = s * Lnx[0];
+      for (int k = 1; k <= P; ++k) sacc = fma(-Lnx[k], yw[k - 1], sacc);
+      const double y = sacc * Lnx[0];
       if (active) dst[static_cast<std::int64_t>(cc) * dstr] = y;
 #pragma unroll
       for (int k = P - 1; k >= 1; --k) yw[k] = yw[k - 1];
       yw[0] = y;
     }
-#pragma unroll
-    for (int k = 0; k < P; ++k) acc[k] = acc[k + 1];
-    acc[P] = 0.0;
+    acc[PH] = 0.0;
     ++cbase;
-    fetch_fwd(cbase, Lnx);
+    fetch_fwd(cbase);
+  };
+  auto flush = [&]() {
+    switch (ph) {
+      case 0: flush_slot(Int<0>{}); break;
+      case 1: flush_slot(Int<1 % (P + 1)>{}); break;
+      case 2: flush_slot(Int<2 % (P + 1)>{}); break;
+      case 3: flush_slot(Int<3 % (P + 1)>{}); break;
+      case 4: flush_slot(Int<4 % (P + 1)>{}); break;
+      case 5: flush_slot(Int<5 % (P + 1)>{}); break;
+      case 6: flush_slot(Int<6 % (P + 1)>{}); break;
+      case 7: flush_slot(Int<7 % (P + 1)>{}); break;
+      case 8: flush_slot(Int<8 % (P + 1)>{}); break;
+      default: flush_slot(Int<9 % (P + 1)>{}); break;
+    }
+    ph = ph == P ? 0 : ph + 1;
+  };
+  // Accumulate the run of rows [jj, jn) that share span g (static slots).
+  auto run_rows = [&](auto phc, const double* sq, const double* sv, const int* sg, int& jj, int jn, int g) {
+    constexpr int PH = decltype(phc)::value;
+    do {
+      const double q = sq[jj * nthr];
+      const double* vr = sv + jj * (P + 1);
+#pragma unroll
+      for (int k = 0; k <= P; ++k) acc[(PH + k) % (P + 1)] = fma(vr[k], q, acc[(PH + k) % (P + 1)]);
+      ++jj;
+    } while (jj < jn && sg[jj] == g);
+  };
+  auto run_dyn = [&](const double* sq, const double* sv, const int* sg, int& jj, int jn, int g) {
+    switch (ph) {
+      case 0: run_rows(Int<0>{}, sq, sv, sg, jj, jn, g); break;
+      case 1: run_rows(Int<1 % (P + 1)>{}, sq, sv, sg, jj, jn, g); break;
+      case 2: run_rows(Int<2 % (P + 1)>{}, sq, sv, sg, jj, jn, g); break;
+      case 3: run_rows(Int<3 % (P + 1)>{}, sq, sv, sg, jj, jn, g); break;
+      case 4: run_rows(Int<4 % (P + 1)>{}, sq, sv, sg, jj, jn, g); break;
+      case 5: run_rows(Int<5 % (P + 1)>{}, sq, sv, sg, jj, jn, g); break;
+      case 6: run_rows(Int<6 % (P + 1)>{}, sq, sv, sg, jj, jn, g); break;
+      case 7: run_rows(Int<7 % (P + 1)>{}, sq, sv, sg, jj, jn, g); break;
+      case 8: run_rows(Int<8 % (P + 1)>{}, sq, sv, sg, jj, jn, g); break;
+      default: run_rows(Int<9 % (P + 1)>{}, sq, sv, sg, jj, jn, g); break;
+    }
   };
 
   for (int c = 0; c < nchunks; ++c) {
     const int st = c % S;
     const unsigned char* base = sm_raw + st * SL.stage_bytes;
-    const double* sq = reinterpret_cast<const double*>(base);
+    const double* sq = reinterpret_cast<const double*>(base) + tid;
     const double* sv = reinterpret_cast<const double*>(base + SL.v_off);
     const int* sg = reinterpret_cast<const int*>(base + SL.g_off);
     mbar_wait(&bars[st], (c / S) & 1);
     const int jn = (m - c * R) < R ? (m - c * R) : R;
-    for (int jj = 0; jj < jn; ++jj) {
+    for (int jj = 0; jj < jn;) {
       const int g = sg[jj];
       while (cbase < g) flush();
-      const double q = sq[jj * nthr + tid];
-      const double* vr = sv + jj * (P + 1);
-#pragma unroll
-      for (int k = 0; k <= P; ++k) acc[k] = fma(vr[k], q, acc[k]);
+      run_dyn(sq, sv, sg, jj, jn, g);
     }
     __syncthreads();
     if (tid == 0 && c + S < nchunks) {
