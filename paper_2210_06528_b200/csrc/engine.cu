@@ -268,7 +268,7 @@ struct Workload {
   std::int64_t sflag_off[3] = {0, 0, 0};
   // TMA axis-0 pass (field row strides must be 16-B multiples)
   bool tma_axis0 = false;
-  mfb::TmaGeom axis0_geo{1, 1, 16, 4};
+  mfb::TmaGeom axis0_geo{1, 1, 16, 4, 0};
   int axis0_tiles = 0;
   std::array<std::int64_t, 3> field_dims{1, 1, 1};  // global field extents (solver) for the tensor map
 
@@ -297,6 +297,10 @@ struct Workload {
     }
     axis0_geo.R = 8;
     axis0_geo.S = 4;
+    int mxn = 0;
+    for (const auto& b : blocks) mxn = std::max(mxn, probs[static_cast<std::size_t>(b.ax[0])].n);
+    const int need = mxn * (2 * p + 1);
+    axis0_geo.lt_cap = need <= 4096 ? need : 0;  // <= 32 KB of smem
     tma_axis0 = true;
   }
 
@@ -536,7 +540,7 @@ struct mfadd_solver {
   DecodePlan dp;
   // TMA decode sweep (D >= 2, even last extent)
   bool tma_decode = false;
-  mfb::TmaGeom dgeo{1, 1, 16, 4};
+  mfb::TmaGeom dgeo{1, 1, 16, 4, 0};
   int dnt1 = 1, dnt2 = 1, dnrange = 1, dH = 1;
 
   DBuf<int2> hr;

@@ -149,6 +149,7 @@ int launch_decode(int degree, const DecodeArgs& a, cudaStream_t s);
 // TMA pipeline geometry: box = (B2 inner, [B1], R rows) per stage, S stages.
 struct TmaGeom {
   int B1, B2, R, S;
+  int lt_cap;  // doubles of smem reserved for the Cholesky table (0 = use global)
 };
 // TMA axis-0 fit pass (stream_tma.cu); needs 16-B aligned field row strides.
 int launch_fit_axis0_tma(int degree, const FitArgs& a, const CUtensorMap& map, const TmaGeom& g, int ntiles,

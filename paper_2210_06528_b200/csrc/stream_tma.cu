@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
   double* dst = a.t1 + blk.t1off + t;  // T1[i0][Tr]
   const int* g0g = a.g0 + pr.row_off;
   const double* vg = a.vals + pr.row_off * (P + 1);
-  const double* lt = a.ltab + pr.col_off * (2 * P + 1);
+  const double* lt = a.ltab + pr.col_off * (2 * P + 1);  // may be redirected to smem
 
   const StageLayout SL = stage_layout(R, nthr, P);
   std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(sm_raw + S * SL.stage_bytes);
@@ -115,6 +115,14 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
     for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
   }
+  // Cholesky coefficients of this block's axis-0 problem, staged in smem
+  // (L1 is mostly carved out for the TMA ring).
+  double* s_lt = reinterpret_cast<double*>(sm_raw + S * SL.stage_bytes + 128);
+  const bool lt_in_smem = n * (2 * P + 1) <= geo.lt_cap;
+  if (lt_in_smem) {
+    for (int i = tid; i < n * (2 * P + 1); i += blockDim.x) s_lt[i] = __ldg(lt + i);
+    lt = s_lt;
+  }
   __syncthreads();
   if (tid == 0)
     for (int c = 0; c < S && c < nchunks; ++c) issue(c);
@@ -135,7 +143,7 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
     const int cl = cc < 0 ? 0 : (cc >= n ? n - 1 : cc);
     const double* Lc = lt + static_cast<std::int64_t>(cl) * (2 * P + 1);
 #pragma unroll
-    for (int k = 0; k <= P; ++k) Lnx[k] = __ldg(Lc + k);
+    for (int k = 0; k <= P; ++k) Lnx[k] = Lc[k];
   };
   fetch_fwd(cbase);
   // Complete column cbase (slot PH): forward substitution, then recycle the
@@ -220,7 +228,7 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
   while (cbase < n) flush();
   // Back substitution in place, y values prefetched 8 columns ahead.
   if (!active) return;
-  constexpr int PF = 8;
+  constexpr int PF = 16;
   double yr[PF];
 #pragma unroll
   for (int u = 0; u < PF; ++u) yr[u] = (n - 1 - u >= 0) ? dst[static_cast<std::int64_t>(n - 1 - u) * dstr] : 0.0;
@@ -230,9 +238,9 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
   double Lb[P + 1];  // backward coefficients of the current column, fetched ahead
   auto fetch_bwd = [&](int c, double* L) {
     const double* Lc = lt + static_cast<std::int64_t>(c < 0 ? 0 : c) * (2 * P + 1);
-    L[0] = __ldg(Lc);
+    L[0] = Lc[0];
 #pragma unroll
-    for (int k = 1; k <= P; ++k) L[k] = __ldg(Lc + P + k);
+    for (int k = 1; k <= P; ++k) L[k] = Lc[P + k];
   };
   fetch_bwd(n - 1, Lb);
   for (int c0 = n - 1; c0 >= 0; c0 -= PF) {
@@ -449,7 +457,7 @@ template <int P>
 struct Axis0Launch {
   static int run(const FitArgs& a, const CUtensorMap& map, const TmaGeom& g, int ntiles, cudaStream_t s) {
     const StageLayout SL = stage_layout(g.R, g.B1 * g.B2, P);
-    const size_t smem = static_cast<size_t>(g.S) * SL.stage_bytes + g.S * 8;
+    const size_t smem = static_cast<size_t>(g.S) * SL.stage_bytes + 128 + static_cast<size_t>(g.lt_cap) * 8;
     cudaFuncSetAttribute(k_fit_axis0_tma<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     dim3 grid(ntiles, a.nblocks);
     k_fit_axis0_tma<P><<<grid, g.B1 * g.B2, smem, s>>>(a, map, g);
