@@ -299,8 +299,9 @@ struct Workload {
     axis0_geo.S = 4;
     int mxn = 0;
     for (const auto& b : blocks) mxn = std::max(mxn, probs[static_cast<std::size_t>(b.ax[0])].n);
-    const int need = mxn * (2 * p + 1);
-    axis0_geo.lt_cap = need <= 4096 ? need : 0;  // <= 32 KB of smem
+    const int need = (mxn + 2 * (p + 1)) * (2 * p + 1);  // padded Cholesky table in smem
+    if (need > 6144) return;                             // > 48 KB: generic kernel
+    axis0_geo.lt_cap = need;
     tma_axis0 = true;
   }
 

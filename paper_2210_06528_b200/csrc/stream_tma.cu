@@ -47,9 +47,13 @@ __host__ __device__ inline StageLayout stage_layout(int R, int nthr, int P) {
 }
 
 // ---------------------------------------------------------------- fit axis 0
+constexpr int kFitR = 8;  // rows per TMA stage (fit axis 0)
+constexpr int kFitS = 4;  // stages
+
 template <int P>
 __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __grid_constant__ CUtensorMap map,
                                                        const TmaGeom geo) {
+  constexpr int R = kFitR, S = kFitS;
   extern __shared__ __align__(128) unsigned char sm_raw[];
   const int b = blockIdx.y;
   const BlockDev blk = a.blocks[b];
@@ -62,7 +66,7 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
   // loads need a 16-B aligned innermost start coordinate, so the box starts
   // at the even column at or below the block's first column and the thread
   // -> column map is shifted by that parity (geo.B2 = W, one spare column).
-  const int B1 = geo.B1, W = geo.B2, R = geo.R, S = geo.S;
+  const int B1 = geo.B1, W = geo.B2;
   const int nthr = B1 * W;
   const int tile = blockIdx.x;
   const int tid = threadIdx.x;
@@ -116,13 +120,15 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
     fence_mbar_init();
   }
   // Cholesky coefficients of this block's axis-0 problem, staged in smem
-  // (L1 is mostly carved out for the TMA ring).
+  // with P+1 zero columns on both sides (fetches need no clamping; L1 is
+  // mostly carved out for the TMA ring).
   double* s_lt = reinterpret_cast<double*>(sm_raw + S * SL.stage_bytes + 128);
-  const bool lt_in_smem = n * (2 * P + 1) <= geo.lt_cap;
-  if (lt_in_smem) {
-    for (int i = tid; i < n * (2 * P + 1); i += blockDim.x) s_lt[i] = __ldg(lt + i);
-    lt = s_lt;
+  constexpr int LW = 2 * P + 1;
+  for (int i = tid; i < (n + 2 * (P + 1)) * LW; i += blockDim.x) {
+    const int cc = i / LW - (P + 1);
+    s_lt[i] = (cc >= 0 && cc < n) ? __ldg(lt + static_cast<std::int64_t>(cc) * LW + (i - (i / LW) * LW)) : 0.0;
   }
+  const double* slt = s_lt + (P + 1) * LW;  // slt[cc * LW + k], cc in [-(P+1), n+P]
   __syncthreads();
   if (tid == 0)
     for (int c = 0; c < S && c < nchunks; ++c) issue(c);
@@ -140,8 +146,7 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
   int ph = 0;
   double Lnx[P + 1];  // forward coefficients of column cbase, fetched one flush ahead
   auto fetch_fwd = [&](int cc) {
-    const int cl = cc < 0 ? 0 : (cc >= n ? n - 1 : cc);
-    const double* Lc = lt + static_cast<std::int64_t>(cl) * (2 * P + 1);
+    const double* Lc = slt + (cc < -(P + 1) ? -(P + 1) : cc) * LW;
 #pragma unroll
     for (int k = 0; k <= P; ++k) Lnx[k] = Lc[k];
   };
@@ -237,7 +242,7 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
   for (int k = 0; k < P; ++k) xw[k] = 0.0;
   double Lb[P + 1];  // backward coefficients of the current column, fetched ahead
   auto fetch_bwd = [&](int c, double* L) {
-    const double* Lc = lt + static_cast<std::int64_t>(c < 0 ? 0 : c) * (2 * P + 1);
+    const double* Lc = slt + c * LW;  // c >= -1
     L[0] = Lc[0];
 #pragma unroll
     for (int k = 1; k <= P; ++k) L[k] = Lc[P + k];
@@ -270,7 +275,8 @@ __global__ void __launch_bounds__(256) k_decode_tma(const DecodeSweepArgs a, con
                                                     const TmaGeom geo) {
   extern __shared__ __align__(128) unsigned char sm_raw[];
   __shared__ double s_red[64];
-  const int B1 = geo.B1, B2 = geo.B2, R = geo.R, S = geo.S;
+  constexpr int R = kFitR, S = kFitS;  // same stage geometry as the fit pass
+  const int B1 = geo.B1, B2 = geo.B2;
   const int nthr = B1 * B2;
   const int tid = threadIdx.x;
   // trailing tile
@@ -456,8 +462,8 @@ __global__ void __launch_bounds__(256) k_decode_tma(const DecodeSweepArgs a, con
 template <int P>
 struct Axis0Launch {
   static int run(const FitArgs& a, const CUtensorMap& map, const TmaGeom& g, int ntiles, cudaStream_t s) {
-    const StageLayout SL = stage_layout(g.R, g.B1 * g.B2, P);
-    const size_t smem = static_cast<size_t>(g.S) * SL.stage_bytes + 128 + static_cast<size_t>(g.lt_cap) * 8;
+    const StageLayout SL = stage_layout(kFitR, g.B1 * g.B2, P);
+    const size_t smem = static_cast<size_t>(kFitS) * SL.stage_bytes + 128 + static_cast<size_t>(g.lt_cap) * 8;
     cudaFuncSetAttribute(k_fit_axis0_tma<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     dim3 grid(ntiles, a.nblocks);
     k_fit_axis0_tma<P><<<grid, g.B1 * g.B2, smem, s>>>(a, map, g);
@@ -468,8 +474,8 @@ struct Axis0Launch {
 template <int P>
 struct DecodeSweepLaunch {
   static int run(const DecodeSweepArgs& a, const CUtensorMap& map, const TmaGeom& g, cudaStream_t s) {
-    const StageLayout SL = stage_layout(g.R, g.B1 * g.B2, P);
-    const size_t smem = static_cast<size_t>(g.S) * SL.stage_bytes + g.S * 8;
+    const StageLayout SL = stage_layout(kFitR, g.B1 * g.B2, P);
+    const size_t smem = static_cast<size_t>(kFitS) * SL.stage_bytes + kFitS * 8;
     dim3 grid(a.ntile1 * a.ntile2, a.nrange);
     if (a.D == 2) {
       cudaFuncSetAttribute(k_decode_tma<P, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
