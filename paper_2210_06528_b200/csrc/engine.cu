@@ -147,7 +147,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // Tiled fp64 tensor map over a row-major array; dims/box innermost first.
-CUtensorMap make_tmap(const double* base, int rank, const std::uint64_t* dims, const std::uint32_t* box) {
+CUtensorMap make_tmap(const double* base, int rank, const std::uint64_t* dims, const std::uint32_t* box,
+                      CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_NONE) {
   CUtensorMap m;
   std::uint64_t strides[3] = {0, 0, 0};
   std::uint64_t st = 8;
@@ -158,7 +159,7 @@ CUtensorMap make_tmap(const double* base, int rank, const std::uint64_t* dims, c
   const std::uint32_t estr[3] = {1, 1, 1};
   const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, static_cast<cuuint32_t>(rank),
                                  const_cast<double*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                 CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw ApiError(MFADD_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
   return m;
@@ -257,6 +258,7 @@ struct Workload {
   int max_m = 0, max_n_factor = 0;
   int max_lines_strided[3] = {0, 0, 0};
   int max_lines_last = 0;
+  std::int64_t pitch_last = 1;
 
   DBuf<double> knots, params;
   DBuf<AxisProb> d_probs;
@@ -270,6 +272,9 @@ struct Workload {
   bool tma_axis0 = false;
   mfb::TmaGeom axis0_geo{1, 1, 16, 4, 0};
   int axis0_tiles = 0;
+  // TMA last-axis pass (D >= 2)
+  bool tma_last = false;
+  int last_LT = 128, last_ltcap = 0;
   std::array<std::int64_t, 3> field_dims{1, 1, 1};  // global field extents (solver) for the tensor map
 
   void plan_tma(bool enable) {
@@ -303,6 +308,16 @@ struct Workload {
     if (need > 6144) return;                             // > 48 KB: generic kernel
     axis0_geo.lt_cap = need;
     tma_axis0 = true;
+    // last axis: LT lines per CTA (<= 256, multiple of 8), padded L table in smem
+    int mxnl = 0;
+    for (const auto& b : blocks) mxnl = std::max(mxnl, probs[static_cast<std::size_t>(b.ax[D - 1])].n);
+    const int needl = (mxnl + 2 * (p + 1)) * (2 * p + 1);
+    if (needl <= 6144 && max_lines_last > 0) {
+      const int ncta = (max_lines_last + 255) / 256;
+      last_LT = round_up((max_lines_last + ncta - 1) / ncta, 8);
+      last_ltcap = needl;
+      tma_last = true;
+    }
   }
 
   // Derive offsets/sizes from probs + blocks (row/col offsets, intermediates).
@@ -329,6 +344,11 @@ struct Workload {
     total_p = total_t1 = total_t2 = 0;
     for (auto& mx : max_lines_strided) mx = 0;
     max_lines_last = 0;
+    pitch_last = 1;
+    if (D >= 2)
+      for (const auto& b : blocks)
+        pitch_last = std::max<std::int64_t>(pitch_last, probs[static_cast<std::size_t>(b.ax[D - 1])].m);
+    pitch_last = (pitch_last + 1) / 2 * 2;  // even: 16-B aligned rows (TMA)
     for (auto& b : blocks) {
       std::int64_t np = 1;
       std::array<std::int64_t, 3> m{1, 1, 1}, n{1, 1, 1};
@@ -341,8 +361,9 @@ struct Workload {
       total_p += np;
       b.t1off = total_t1;
       b.t2off = total_t2;
-      if (D >= 2) total_t1 += n[0] * m[1] * (D == 3 ? m[2] : 1);
-      if (D == 3) total_t2 += n[0] * n[1] * m[2];
+      if (D == 2) total_t1 += n[0] * pitch_last;
+      if (D == 3) total_t1 += n[0] * m[1] * m[2];
+      if (D == 3) total_t2 += n[0] * n[1] * pitch_last;
       for (int d = 0; d + 1 < D; ++d) {
         std::int64_t L = 1, Tr = 1;
         for (int k = 0; k < D; ++k) {
@@ -419,6 +440,7 @@ struct Workload {
       fa.max_lines_strided[k] = max_lines_strided[k];
     }
     fa.max_lines_last = max_lines_last;
+    fa.pitch_last = pitch_last;
     fa.n_field = field_n;
     fa.n_t1 = total_t1;
     fa.n_t2 = total_t2;
@@ -446,7 +468,16 @@ struct Workload {
       tl->end();
     }
     tl->begin("fit_last");
-    l += mfb::launch_fit_last(p, fa, ctx->stream);
+    if (tma_last) {
+      const double* src = D == 2 ? t1.p : t2.p;
+      const std::int64_t rows = (D == 2 ? total_t1 : total_t2) / pitch_last;
+      const std::uint64_t dims[2] = {static_cast<std::uint64_t>(pitch_last), static_cast<std::uint64_t>(rows)};
+      const std::uint32_t box[2] = {16u, static_cast<std::uint32_t>(last_LT)};
+      const CUtensorMap map = make_tmap(src, 2, dims, box, CU_TENSOR_MAP_SWIZZLE_128B);
+      l += mfb::launch_fit_last_tma(p, fa, map, last_LT, last_ltcap, ctx->stream);
+    } else {
+      l += mfb::launch_fit_last(p, fa, ctx->stream);
+    }
     tl->end();
     CK(cudaGetLastError());
     return l;

@@ -310,8 +310,10 @@ __global__ void __launch_bounds__(kStridedThreads) k_fit_strided(FitArgs a, int 
     src = a.t1 + blk.t1off + (l * m) * Tr + t;
     sst = Tr;
   }
-  double* dst = (d == 0 ? a.t1 + blk.t1off : a.t2 + blk.t2off) + (l * n) * Tr + t;
-  const std::int64_t dstr = Tr;
+  // rows of the last-axis input (written by pass D-2) use the common pitch
+  const std::int64_t Tro = (d == a.D - 2) ? a.pitch_last : Tr;
+  double* dst = (d == 0 ? a.t1 + blk.t1off : a.t2 + blk.t2off) + (l * n) * Tro + t;
+  const std::int64_t dstr = Tro;
 #ifdef MFB_DEBUG
   if (active) {
     const double* sb = d == 0 ? a.field : a.t1;
@@ -401,14 +403,15 @@ __global__ void __launch_bounds__(kLastThreads) k_fit_last(FitArgs a) {
   const int nl = static_cast<int>((L - l0) < kLastThreads ? (L - l0) : kLastThreads);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = kLastThreads / 32;
   const bool active = tid < nl;
-  const double* src = (a.D == 1 ? a.field + blk.fbase : (a.D == 2 ? a.t1 + blk.t1off : a.t2 + blk.t2off)) + l0 * m;
+  const std::int64_t lpitch = a.D == 1 ? m : a.pitch_last;
+  const double* src = (a.D == 1 ? a.field + blk.fbase : (a.D == 2 ? a.t1 + blk.t1off : a.t2 + blk.t2off)) + l0 * lpitch;
   double* Pb = a.P + blk.poff + l0 * n;
   double* Yb = a.Y + blk.poff + l0 + tid;  // transposed scratch: Y[c*L + l]
 #ifdef MFB_DEBUG
   {
     const double* sb = a.D == 1 ? a.field : (a.D == 2 ? a.t1 : a.t2);
     const std::int64_t sn = a.D == 1 ? a.n_field : (a.D == 2 ? a.n_t1 : a.n_t2);
-    MFB_ASSERT(src - sb >= 0 && (src - sb) + static_cast<std::int64_t>(nl) * m <= sn, "last src");
+    MFB_ASSERT(src - sb >= 0 && (src - sb) + static_cast<std::int64_t>(nl - 1) * lpitch + m <= sn, "last src");
     MFB_ASSERT(blk.poff + l0 * n + static_cast<std::int64_t>(nl) * n <= a.n_P, "last P");
     MFB_ASSERT(blk.poff + L * n <= a.n_P, "last Y");
   }
@@ -427,7 +430,7 @@ __global__ void __launch_bounds__(kLastThreads) k_fit_last(FitArgs a) {
     const int jn = (m - j0) < CW ? (m - j0) : CW;
     __syncthreads();
     for (int li = warp; li < nl; li += nwarps)
-      s_q[li * SP + lane] = lane < jn ? src[static_cast<std::int64_t>(li) * m + j0 + lane] : 0.0;
+      s_q[li * SP + lane] = lane < jn ? src[static_cast<std::int64_t>(li) * lpitch + j0 + lane] : 0.0;
     for (int e = tid; e < jn; e += kLastThreads) s_g0[e] = g0g[j0 + e];
     for (int e = tid; e < jn * (P + 1); e += kLastThreads) s_v[e] = vg[static_cast<std::int64_t>(j0) * (P + 1) + e];
     __syncthreads();

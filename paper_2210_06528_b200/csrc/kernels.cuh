@@ -64,6 +64,7 @@ struct FitArgs {
   std::int64_t sflag_off[3];
   int max_lines_strided[3];          // per axis: max lines over blocks
   int max_lines_last;
+  std::int64_t pitch_last;           // row pitch (even) of the last-axis input (T1 for D=2, T2 for D=3)
   std::int64_t n_field, n_t1, n_t2, n_P;  // buffer sizes (debug bounds checks)
 };
 int launch_fit_strided(int degree, const FitArgs& a, int axis, cudaStream_t s);  // axis < D-1
@@ -154,6 +155,10 @@ struct TmaGeom {
 // TMA axis-0 fit pass (stream_tma.cu); needs 16-B aligned field row strides.
 int launch_fit_axis0_tma(int degree, const FitArgs& a, const CUtensorMap& map, const TmaGeom& g, int ntiles,
                          cudaStream_t s);
+
+// TMA last-axis fit pass (D >= 2): 128-B swizzled 16-column boxes of the
+// last-axis input, LT lines per CTA.
+int launch_fit_last_tma(int degree, const FitArgs& a, const CUtensorMap& map, int LT, int lt_cap, cudaStream_t s);
 
 // TMA decode sweep over the whole input grid (D = 2, 3), stream_tma.cu.
 struct DecodeSweepArgs {

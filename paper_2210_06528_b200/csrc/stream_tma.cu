@@ -30,6 +30,10 @@ struct Int {
   static constexpr int value = V;
 };
 
+__device__ __forceinline__ unsigned long long dbits_s(double x) {
+  return static_cast<unsigned long long>(__double_as_longlong(x));
+}
+
 struct StageLayout {
   int q_bytes;     // R * nthr * 8 (the full TMA box)
   int v_off;       // offset of basis values in the stage
@@ -54,7 +58,7 @@ template <int P>
 __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __grid_constant__ CUtensorMap map,
                                                        const TmaGeom geo) {
   constexpr int R = kFitR, S = kFitS;
-  extern __shared__ __align__(128) unsigned char sm_raw[];
+  extern __shared__ __align__(1024) unsigned char sm_raw[];
   const int b = blockIdx.y;
   const BlockDev blk = a.blocks[b];
   const AxisProb pr = a.probs[blk.ax[0]];
@@ -139,7 +143,7 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
 #pragma unroll
   for (int k = 0; k < P; ++k) yw[k] = 0.0;
   int cbase = __ldg(g0g) < 0 ? __ldg(g0g) : 0;
-  const std::int64_t dstr = Tr;
+  const std::int64_t dstr = D == 2 ? a.pitch_last : Tr;  // T1 row stride
   // Sliding window without register rotation: slot (ph + k) % (P+1) holds
   // column cbase + k.  `ph` is warp-uniform, so the two switch statements
   // below pick fully static register indices (no per-row window moves).
@@ -269,11 +273,235 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
   }
 }
 
+// ---------------------------------------------------------------- fit last axis
+// One thread per line of the last-axis input (T1 rows for D = 2, T2 rows for
+// D = 3; common even pitch).  A stage is a 16-column x LT-line box (128 B per
+// line, SWIZZLE_128B: 16-B chunk k of line t sits at chunk k ^ (t & 7), so the
+// per-thread LDS.128 of two columns is bank-conflict free) plus the matching
+// basis rows.  Forward substitution goes to the transposed scratch Y[c][l]
+// (coalesced); back substitution is staged through smem to write P rows.
+constexpr int kLastCW = 16;
+constexpr int kLastS = 4;
+
+__host__ __device__ inline int last_stage_bytes(int LT, int P) {
+  return ((LT * 128 + kLastCW * (P + 1) * 8 + kLastCW * 4) + 1023) / 1024 * 1024;
+}
+
+template <int P>
+__global__ void __launch_bounds__(256) k_fit_last_tma(const FitArgs a, const __grid_constant__ CUtensorMap map,
+                                                      const int LT) {
+  extern __shared__ __align__(1024) unsigned char sm_raw[];
+  __shared__ unsigned long long s_red[32];
+  constexpr int S = kLastS, CW = kLastCW, LW = 2 * P + 1;
+  const int D = a.D, d = D - 1;
+  const int b = blockIdx.y;
+  const BlockDev blk = a.blocks[b];
+  const AxisProb pr = a.probs[blk.ax[d]];
+  const int m = pr.m, n = pr.n;
+  std::int64_t L = 1;
+  for (int k = 0; k < d; ++k) L *= a.probs[blk.ax[k]].n;
+  const std::int64_t l0 = static_cast<std::int64_t>(blockIdx.x) * LT;
+  if (l0 >= L) return;
+  const int nl = static_cast<int>((L - l0) < LT ? (L - l0) : LT);
+  const int tid = threadIdx.x;
+  const bool active = tid < nl;
+  const int row0 = static_cast<int>((D == 2 ? blk.t1off : blk.t2off) / a.pitch_last + l0);
+  const int* g0g = a.g0 + pr.row_off;
+  const double* vg = a.vals + pr.row_off * (P + 1);
+  const double* lt = a.ltab + pr.col_off * LW;
+  double* Pb = a.P + blk.poff + l0 * n;
+  double* Yb = a.Y + blk.poff + l0 + tid;  // transposed scratch: Y[c*L + l]
+
+  const int SB = last_stage_bytes(LT, P);
+  const int v_off = LT * 128, g_off = v_off + CW * (P + 1) * 8;
+  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(sm_raw + S * SB);
+  double* s_lt = reinterpret_cast<double*>(sm_raw + S * SB + 128);
+  const int nchunks = (m + CW - 1) / CW;
+  const unsigned tx_bytes = static_cast<unsigned>(LT * 128 + CW * (P + 1) * 8 + CW * 4);
+  auto issue = [&](int c) {
+    const int st = c % S;
+    unsigned char* base = sm_raw + st * SB;
+    mbar_arrive_expect_tx(&bars[st], tx_bytes);
+    tma_load_2d(base, &map, c * CW, row0, &bars[st]);
+    bulk_load_1d(base + v_off, vg + static_cast<std::int64_t>(c) * CW * (P + 1), CW * (P + 1) * 8, &bars[st]);
+    bulk_load_1d(base + g_off, g0g + static_cast<std::int64_t>(c) * CW, CW * 4, &bars[st]);
+  };
+  if (tid == 0) {
+    prefetch_tmap(&map);
+    for (int st = 0; st < S; ++st) mbar_init(&bars[st], 1);
+    fence_mbar_init();
+  }
+  for (int i = tid; i < (n + 2 * (P + 1)) * LW; i += blockDim.x) {
+    const int cc = i / LW - (P + 1);
+    s_lt[i] = (cc >= 0 && cc < n) ? __ldg(lt + static_cast<std::int64_t>(cc) * LW + (i - (i / LW) * LW)) : 0.0;
+  }
+  const double* slt = s_lt + (P + 1) * LW;
+  __syncthreads();
+  if (tid == 0)
+    for (int c = 0; c < S && c < nchunks; ++c) issue(c);
+
+  double acc[P + 1], yw[P], Lnx[P + 1];
+#pragma unroll
+  for (int k = 0; k <= P; ++k) acc[k] = 0.0;
+#pragma unroll
+  for (int k = 0; k < P; ++k) yw[k] = 0.0;
+  int cbase = __ldg(g0g) < 0 ? __ldg(g0g) : 0;
+  int ph = 0;
+  auto fetch_fwd = [&](int cc) {
+    const double* Lc = slt + (cc < -(P + 1) ? -(P + 1) : cc) * LW;
+#pragma unroll
+    for (int k = 0; k <= P; ++k) Lnx[k] = Lc[k];
+  };
+  fetch_fwd(cbase);
+  auto flush_slot = [&](auto phc) {
+    constexpr int PH = decltype(phc)::value;
+    const int cc = cbase;
+    if (cc >= 0 && cc < n) {
+      double sacc = acc[PH];
+#pragma unroll
+      for (int k = 1; k <= P; ++k) sacc = fma(-Lnx[k], yw[k - 1], sacc);
+      const double y = sacc * Lnx[0];
+      if (active) Yb[static_cast<std::int64_t>(cc) * L] = y;
+#pragma unroll
+      for (int k = P - 1; k >= 1; --k) yw[k] = yw[k - 1];
+      yw[0] = y;
+    }
+    acc[PH] = 0.0;
+    ++cbase;
+    fetch_fwd(cbase);
+  };
+  auto accum = [&](auto phc, const double* vr, double q) {
+    constexpr int PH = decltype(phc)::value;
+#pragma unroll
+    for (int k = 0; k <= P; ++k) acc[(PH + k) % (P + 1)] = fma(vr[k], q, acc[(PH + k) % (P + 1)]);
+  };
+#define MFB_PHASE_SWITCH(CALL)                  \
+  switch (ph) {                                 \
+    case 0: CALL(Int<0>{}); break;              \
+    case 1: CALL(Int<1 % (P + 1)>{}); break;    \
+    case 2: CALL(Int<2 % (P + 1)>{}); break;    \
+    case 3: CALL(Int<3 % (P + 1)>{}); break;    \
+    case 4: CALL(Int<4 % (P + 1)>{}); break;    \
+    case 5: CALL(Int<5 % (P + 1)>{}); break;    \
+    case 6: CALL(Int<6 % (P + 1)>{}); break;    \
+    case 7: CALL(Int<7 % (P + 1)>{}); break;    \
+    case 8: CALL(Int<8 % (P + 1)>{}); break;    \
+    default: CALL(Int<9 % (P + 1)>{}); break;   \
+  }
+  auto column = [&](int j, const int* sg, const double* sv, double q) {
+    const int g = sg[j];
+    while (cbase < g) {
+#define MFB_FLUSH_CALL(X) flush_slot(X)
+      MFB_PHASE_SWITCH(MFB_FLUSH_CALL)
+#undef MFB_FLUSH_CALL
+      ph = ph == P ? 0 : ph + 1;
+    }
+    const double* vr = sv + j * (P + 1);
+#define MFB_ACC_CALL(X) accum(X, vr, q)
+    MFB_PHASE_SWITCH(MFB_ACC_CALL)
+#undef MFB_ACC_CALL
+  };
+
+  const int swz = tid & 7;
+  for (int c = 0; c < nchunks; ++c) {
+    const int st = c % S;
+    const unsigned char* base = sm_raw + st * SB;
+    const int* sg = reinterpret_cast<const int*>(base + g_off);
+    const double* sv = reinterpret_cast<const double*>(base + v_off);
+    mbar_wait(&bars[st], (c / S) & 1);
+    const int jn = (m - c * CW) < CW ? (m - c * CW) : CW;
+    const double2* line = reinterpret_cast<const double2*>(base + tid * 128);
+#pragma unroll 1
+    for (int kk = 0; kk < CW / 2; ++kk) {
+      if (2 * kk >= jn) break;
+      const double2 q2 = line[kk ^ swz];
+      column(2 * kk, sg, sv, q2.x);
+      if (2 * kk + 1 < jn) column(2 * kk + 1, sg, sv, q2.y);
+    }
+    __syncthreads();
+    if (tid == 0 && c + S < nchunks) {
+      fence_proxy_async();
+      issue(c + S);
+    }
+  }
+  while (cbase < n) {
+#define MFB_FLUSH_CALL(X) flush_slot(X)
+    MFB_PHASE_SWITCH(MFB_FLUSH_CALL)
+#undef MFB_FLUSH_CALL
+    ph = ph == P ? 0 : ph + 1;
+  }
+#undef MFB_PHASE_SWITCH
+
+  // Is this line's lead index shared along any leading dim?
+  bool lead_shared = false;
+  {
+    std::int64_t r = l0 + tid;
+    for (int k = d - 1; k >= 0; --k) {
+      const AxisProb pk = a.probs[blk.ax[k]];
+      const std::int64_t ik = r % pk.n;
+      r /= pk.n;
+      if (active && a.shared_flag[a.sflag_off[k] + pk.col_lo + ik]) lead_shared = true;
+    }
+  }
+  const unsigned char* sf_last = a.shared_flag + a.sflag_off[d] + pr.col_lo;
+  // Back substitution; x staged through smem (stage buffers are free now).
+  __syncthreads();
+  constexpr int XP = 33;
+  double* s_x = reinterpret_cast<double*>(sm_raw);
+  const int lane = tid & 31, warp = tid >> 5, nwarps = (blockDim.x + 31) >> 5;
+  double xw[P], Lb[P + 1];
+#pragma unroll
+  for (int k = 0; k < P; ++k) xw[k] = 0.0;
+  auto fetch_bwd = [&](int cc) {
+    const double* Lc = slt + cc * LW;  // cc >= -1
+    Lb[0] = Lc[0];
+#pragma unroll
+    for (int k = 1; k <= P; ++k) Lb[k] = Lc[P + k];
+  };
+  fetch_bwd(n - 1);
+  unsigned long long lmax = 0ull;
+  for (int chi = n - 1; chi >= 0; chi -= 32) {
+    const int clo = chi - 31 > 0 ? chi - 31 : 0;
+    const int cn = chi - clo + 1;
+    double ynext = active ? Yb[static_cast<std::int64_t>(chi) * L] : 0.0;
+    for (int cc = chi; cc >= clo; --cc) {
+      double sacc = ynext;
+      if (cc > clo && active) ynext = Yb[static_cast<std::int64_t>(cc - 1) * L];
+#pragma unroll
+      for (int k = 1; k <= P; ++k) sacc = fma(-Lb[k], xw[k - 1], sacc);
+      const double x = sacc * Lb[0];
+      fetch_bwd(cc - 1);
+#pragma unroll
+      for (int k = P - 1; k >= 1; --k) xw[k] = xw[k - 1];
+      xw[0] = x;
+      s_x[tid * XP + (cc - clo)] = x;
+      if (active && !lead_shared && !sf_last[cc]) lmax = lmax > dbits_s(fabs(x)) ? lmax : dbits_s(fabs(x));
+    }
+    __syncthreads();
+    for (int li = warp; li < nl; li += nwarps)
+      if (lane < cn) Pb[static_cast<std::int64_t>(li) * n + clo + lane] = s_x[li * XP + lane];
+    __syncthreads();
+  }
+  // block-wide max of lmax -> linf_int[b]
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long t2 = __shfl_xor_sync(kFullMask, lmax, o);
+    lmax = lmax > t2 ? lmax : t2;
+  }
+  if (lane == 0) s_red[warp] = lmax;
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long mx = 0ull;
+    for (int w = 0; w < nwarps; ++w) mx = mx > s_red[w] ? mx : s_red[w];
+    if (mx) atomicMax(a.linf_int + b, mx);
+  }
+}
+
 // ---------------------------------------------------------------- decode
 template <int P, int D>
 __global__ void __launch_bounds__(256) k_decode_tma(const DecodeSweepArgs a, const __grid_constant__ CUtensorMap map,
                                                     const TmaGeom geo) {
-  extern __shared__ __align__(128) unsigned char sm_raw[];
+  extern __shared__ __align__(1024) unsigned char sm_raw[];
   __shared__ double s_red[64];
   constexpr int R = kFitR, S = kFitS;  // same stage geometry as the fit pass
   const int B1 = geo.B1, B2 = geo.B2;
@@ -504,7 +732,22 @@ int dispatch_p(int p, Args&&... args) {
   }
 }
 
+template <int P>
+struct LastLaunch {
+  static int run(const FitArgs& a, const CUtensorMap& map, int LT, int lt_cap, cudaStream_t s) {
+    const size_t smem = static_cast<size_t>(kLastS) * last_stage_bytes(LT, P) + 128 + static_cast<size_t>(lt_cap) * 8;
+    cudaFuncSetAttribute(k_fit_last_tma<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    dim3 grid((a.max_lines_last + LT - 1) / LT, a.nblocks);
+    k_fit_last_tma<P><<<grid, LT, smem, s>>>(a, map, LT);
+    return 1;
+  }
+};
+
 }  // namespace
+
+int launch_fit_last_tma(int degree, const FitArgs& a, const CUtensorMap& map, int LT, int lt_cap, cudaStream_t s) {
+  return dispatch_p<LastLaunch>(degree, a, map, LT, lt_cap, s);
+}
 
 int launch_fit_axis0_tma(int degree, const FitArgs& a, const CUtensorMap& map, const TmaGeom& g, int ntiles,
                          cudaStream_t s) {
