@@ -238,6 +238,8 @@ struct Timeline {
       if (e != cudaSuccess) throw ApiError(MFADD_ECUDA, std::string("kernel ") + cur + ": " + cudaGetErrorString(e));
       if (const int line = mfb::debug_fail_line())
         throw ApiError(MFADD_ECUDA, std::string("kernel ") + cur + ": bounds check failed at kernels.cu:" + std::to_string(line));
+      if (const int line = mfb::debug_fail_line_tma())
+        throw ApiError(MFADD_ECUDA, std::string("kernel ") + cur + ": check failed at stream_tma.cu:" + std::to_string(line));
     }
     if (!on) return;
     CK(cudaEventRecord(recs[used].b, st));
@@ -308,13 +310,13 @@ struct Workload {
     if (need > 6144) return;                             // > 48 KB: generic kernel
     axis0_geo.lt_cap = need;
     tma_axis0 = true;
-    // last axis: LT lines per CTA (<= 256, multiple of 8), padded L table in smem
+    // last axis: LT lines per CTA (<= 256, multiple of 32), padded L table in smem
     int mxnl = 0;
     for (const auto& b : blocks) mxnl = std::max(mxnl, probs[static_cast<std::size_t>(b.ax[D - 1])].n);
     const int needl = (mxnl + 2 * (p + 1)) * (2 * p + 1);
-    if (needl <= 6144 && max_lines_last > 0) {
+    if (needl <= 6144 && max_lines_last > 0 && !std::getenv("MFADD_NO_TMA_LAST")) {
       const int ncta = (max_lines_last + 255) / 256;
-      last_LT = round_up((max_lines_last + ncta - 1) / ncta, 8);
+      last_LT = round_up((max_lines_last + ncta - 1) / ncta, 32);  // whole warps
       last_ltcap = needl;
       tma_last = true;
     }

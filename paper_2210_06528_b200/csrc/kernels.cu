@@ -28,8 +28,6 @@
 
 #include <cstdio>
 
-// Debug builds (-DMFB_DEBUG, libmfadd_b200_debug.so) range-check every global
-// index and trap with a message instead of touching memory out of bounds.
 // Debug builds (-DMFB_DEBUG, libmfadd_b200_debug.so) range-check global
 // indices; a failed check records its source line in a device word and makes
 // the thread return (no trap, so the host can still read the record).

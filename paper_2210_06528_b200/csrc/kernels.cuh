@@ -12,6 +12,7 @@ namespace mfb {
 
 // Source line of the first failed device bounds check (debug builds), else 0.
 int debug_fail_line();
+int debug_fail_line_tma();  // stream_tma.cu lines (debug builds)
 
 // K1: per-row find_span + Cox-de Boor basis + window clip
 // (knots.cpp:83-129, collocation.cpp:83-111).

@@ -19,6 +19,26 @@
 #include "kernels.cuh"
 #include "tma.cuh"
 
+#ifdef MFB_DEBUG
+__device__ int g_tma_debug_line = 0;
+#define MFB_ASSERT(c, tag)                       \
+  do {                                           \
+    if (!(c)) {                                  \
+      atomicCAS(&g_tma_debug_line, 0, __LINE__); \
+      return;                                    \
+    }                                            \
+  } while (0)
+// record-only variant for checks between barriers (no early return)
+#define MFB_CHECK(c) \
+  do {               \
+    if (!(c)) atomicCAS(&g_tma_debug_line, 0, __LINE__); \
+  } while (0)
+#else
+#define MFB_ASSERT(c, tag) \
+  do {                     \
+  } while (0)
+#endif
+
 namespace mfb {
 
 namespace {
@@ -411,6 +431,20 @@ __global__ void __launch_bounds__(256) k_fit_last_tma(const FitArgs a, const __g
     mbar_wait(&bars[st], (c / S) & 1);
     const int jn = (m - c * CW) < CW ? (m - c * CW) : CW;
     const double2* line = reinterpret_cast<const double2*>(base + tid * 128);
+#ifdef MFB_DEBUG
+    {
+      const double* srcd = (D == 2 ? a.t1 : a.t2) + static_cast<std::int64_t>(row0 + tid) * a.pitch_last;
+      for (int kk = 0; 2 * kk < jn && active; ++kk) {
+        const double2 q2 = line[kk ^ swz];
+        MFB_CHECK(q2.x == srcd[c * CW + 2 * kk]);
+        if (2 * kk + 1 < jn) MFB_CHECK(q2.y == srcd[c * CW + 2 * kk + 1]);
+      }
+      for (int j = 0; j < jn && tid == 0; ++j) {
+        MFB_CHECK(sg[j] == g0g[c * CW + j]);
+        for (int k = 0; k <= P; ++k) MFB_CHECK(sv[j * (P + 1) + k] == vg[(c * CW + j) * (P + 1) + k]);
+      }
+    }
+#endif
 #pragma unroll 1
     for (int kk = 0; kk < CW / 2; ++kk) {
       if (2 * kk >= jn) break;
@@ -478,8 +512,11 @@ __global__ void __launch_bounds__(256) k_fit_last_tma(const FitArgs a, const __g
       if (active && !lead_shared && !sf_last[cc]) lmax = lmax > dbits_s(fabs(x)) ? lmax : dbits_s(fabs(x));
     }
     __syncthreads();
-    for (int li = warp; li < nl; li += nwarps)
-      if (lane < cn) Pb[static_cast<std::int64_t>(li) * n + clo + lane] = s_x[li * XP + lane];
+    // LT need not be a multiple of 32: stride (line, column) pairs over all threads
+    for (int e = tid; e < nl * 32; e += blockDim.x) {
+      const int li = e >> 5, cl = e & 31;
+      if (cl < cn) Pb[static_cast<std::int64_t>(li) * n + clo + cl] = s_x[li * XP + cl];
+    }
     __syncthreads();
   }
   // block-wide max of lmax -> linf_int[b]
@@ -744,6 +781,14 @@ struct LastLaunch {
 };
 
 }  // namespace
+
+int debug_fail_line_tma() {
+  int line = 0;
+#ifdef MFB_DEBUG
+  cudaMemcpyFromSymbol(&line, g_tma_debug_line, sizeof(int));
+#endif
+  return line;
+}
 
 int launch_fit_last_tma(int degree, const FitArgs& a, const CUtensorMap& map, int LT, int lt_cap, cudaStream_t s) {
   return dispatch_p<LastLaunch>(degree, a, map, LT, lt_cap, s);
