@@ -54,4 +54,32 @@ struct EpochAcc {
   unsigned long long jump_ss, jump_ms;
 };
 
+// A region of shared controls: a box of global control indices over which the
+// holder set is constant (the product of one constant-holder interval per
+// dim).  Holders are listed in ascending block id (layout.cpp:177-195);
+// holder h's copy of control lo + r sits at P[base[h] + sum_k r[k]*str[h][k]].
+constexpr int kRegionMaxHolders = 8;
+struct RegionDev {
+  int ns;      // holders (2, 4 or 8)
+  int ext[3];  // box extents (1 for unused dims)
+  int ids[kRegionMaxHolders];
+  long long base[kRegionMaxHolders];
+  int str[kRegionMaxHolders][3];
+  int pslot[kRegionMaxHolders * (kRegionMaxHolders - 1) / 2];  // final-jump slot per holder pair, -1 if none
+};
+
+// A CTA's slice [start, start + count) of one region's row-major box.
+struct TileDev {
+  int region, start, count, pad_;
+};
+
+// Device-side epoch loop state (the loop runs without host round trips).
+struct EpochState {
+  int iter;          // last loop iteration that ran (0 before the loop)
+  int done;          // CTA tickets of the running epoch (last-CTA pattern)
+  int last_iter;     // last iteration that ran
+  int converged;     // dp < tol at last_iter
+  unsigned long long jump_ss, jump_ms;
+};
+
 }  // namespace mfb

@@ -593,6 +593,13 @@ struct mfadd_solver {
   // enforce_constraints in the first exchange epoch (solver.cpp:134-141).
   std::string holder_fault;
   int max_holders = 1;
+  // region-form epochs (max_holders <= 8): tables + the epoch-loop graph
+  DBuf<mfb::RegionDev> regions;
+  DBuf<mfb::TileDev> tiles;
+  int ntiles = 0;
+  DBuf<mfb::EpochState> est;
+  cudaGraph_t loop_graph = nullptr;
+  cudaGraphExec_t loop_exec = nullptr;
 
   // results
   std::vector<mfadd_epoch_stats> epochs;
@@ -606,6 +613,8 @@ struct mfadd_solver {
   ~mfadd_solver() {
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
+    if (loop_exec) cudaGraphExecDestroy(loop_exec);
+    if (loop_graph) cudaGraphDestroy(loop_graph);
   }
 };
 
@@ -721,6 +730,134 @@ double bits_to_double(unsigned long long u) {
   double d;
   std::memcpy(&d, &u, sizeof d);
   return d;
+}
+
+mfb::EpochRegionArgs region_args(mfadd_solver* s, int mode) {
+  mfb::EpochRegionArgs a{};
+  a.regions = s->regions.p;
+  a.tiles = s->tiles.p;
+  a.ntiles = s->ntiles;
+  a.nblocks = s->dec.nblocks;
+  a.P = s->wl.P.p;
+  a.mode = mode;
+  a.change = s->change.p;
+  a.linf_sh = s->linf_sh.p;
+  a.linf_int = s->wl.linf_int.p;
+  a.st = s->est.p;
+  a.epoch_out = s->epoch_out.p;
+  a.pair_jumps = s->pair_jumps.p;
+  a.max_iter = s->cfg.max_outer_iterations;
+  a.tol = s->cfg.tolerance;
+  a.max_ns = s->max_holders;
+  return a;
+}
+
+// Shared controls as regions: products of one constant-holder interval per
+// dim (SharedDofMap::holder_span, layout.cpp:125-203) with n_s >= 2, each cut
+// into tiles of at most kTile controls.  Holder h follows the reference's
+// ascending block-id order (last dim least significant).
+void build_regions(mfadd_solver* s, const std::vector<int>& pair_slot) {
+  constexpr int kTile = 512;  // kRegionThreads x 2 (one pass for n_s = 2, two for n_s >= 4)
+  const Decomp& d = s->dec;
+  const int D = d.rank;
+  struct Iv {
+    std::int64_t lo, hi;
+    int f, e;
+  };
+  std::vector<Iv> iv[3];
+  for (int k = 0; k < D; ++k)
+    for (std::int64_t i = 0; i < d.n_ctrl[k]; ++i) {
+      const auto r = d.holder[k][static_cast<std::size_t>(i)];
+      if (!iv[k].empty() && iv[k].back().f == r[0] && iv[k].back().e == r[1] - r[0] + 1 && iv[k].back().hi == i)
+        ++iv[k].back().hi;
+      else
+        iv[k].push_back({i, i + 1, r[0], r[1] - r[0] + 1});
+    }
+  std::vector<mfb::RegionDev> regs;
+  std::vector<mfb::TileDev> tls;
+  std::size_t cnt[3] = {1, 1, 1};
+  for (int k = 0; k < D; ++k) cnt[k] = iv[k].size();
+  for (std::size_t i0 = 0; i0 < cnt[0]; ++i0)
+    for (std::size_t i1 = 0; i1 < cnt[1]; ++i1)
+      for (std::size_t i2 = 0; i2 < cnt[2]; ++i2) {
+        const std::size_t ii[3] = {i0, i1, i2};
+        const Iv* v[3];
+        int ns = 1;
+        for (int k = 0; k < D; ++k) {
+          v[k] = &iv[k][ii[k]];
+          ns *= v[k]->e;
+        }
+        if (ns < 2) continue;
+        mfb::RegionDev R{};
+        R.ns = ns;
+        const int sh = 3 - D;  // box dims are right-aligned in the kernel's 3-D view
+        for (int k = 0; k < 3; ++k) R.ext[k] = 1;
+        for (int k = 0; k < D; ++k) R.ext[sh + k] = static_cast<int>(v[k]->hi - v[k]->lo);
+        int cs[8][3];
+        for (int h = 0; h < ns; ++h) {
+          int rr = h, c[3] = {0, 0, 0};
+          for (int k = D - 1; k >= 0; --k) {
+            c[k] = v[k]->f + (v[k]->e == 2 ? (rr & 1) : 0);
+            rr = v[k]->e == 2 ? (rr >> 1) : rr;
+          }
+          int id = 0;
+          for (int k = 0; k < D; ++k) id = id * d.blocks[k] + c[k];
+          std::int64_t stride = 1, base = 0;
+          for (int k = D - 1; k >= 0; --k) {
+            const AxisProb& pk = s->wl.probs[static_cast<std::size_t>(s->axbase[k] + c[k])];
+            base += (v[k]->lo - pk.col_lo) * stride;
+            R.str[h][sh + k] = static_cast<int>(stride);
+            stride *= pk.n;
+          }
+          R.ids[h] = id;
+          R.base[h] = s->wl.blocks[static_cast<std::size_t>(id)].poff + base;
+          for (int k = 0; k < 3; ++k) cs[h][k] = c[k];
+        }
+        int q = 0;
+        for (int h1 = 0; h1 < ns; ++h1)
+          for (int h2 = h1 + 1; h2 < ns; ++h2, ++q) {
+            int code = 0, mul = 1;
+            for (int k = D - 1; k >= 0; --k) {
+              code += (cs[h2][k] - cs[h1][k] + 1) * mul;
+              mul *= 3;
+            }
+            R.pslot[q] = pair_slot[static_cast<std::size_t>(R.ids[h1]) * 27 + code];
+          }
+        const int total = R.ext[0] * R.ext[1] * R.ext[2];
+        for (int st0 = 0; st0 < total; st0 += kTile)
+          tls.push_back({static_cast<int>(regs.size()), st0, std::min(kTile, total - st0), 0});
+        regs.push_back(R);
+      }
+  s->ntiles = static_cast<int>(tls.size());
+  if (s->ntiles == 0) return;
+  s->regions.upload(regs, s->ctx->stream);
+  s->tiles.upload(tls, s->ctx->stream);
+}
+
+// The epoch loop (solver.cpp:394-413) as a CUDA graph: a conditional WHILE
+// node whose body is one region-form epoch; the epoch's last CTA computes dp
+// and sets the condition, so the loop runs with no host round trips.
+void build_loop_graph(mfadd_solver* s) {
+  CK(cudaGraphCreate(&s->loop_graph, 0));
+  cudaGraphConditionalHandle h;
+  CK(cudaGraphConditionalHandleCreate(&h, s->loop_graph, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams np = {};
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = h;
+  np.conditional.type = cudaGraphCondTypeWhile;
+  np.conditional.size = 1;
+  cudaGraphNode_t node;
+  CK(cudaGraphAddNode(&node, s->loop_graph, nullptr, 0, &np));
+  cudaGraph_t body = np.conditional.phGraph_out[0];
+  cudaStream_t cs;
+  CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  CK(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  mfb::EpochRegionArgs a = region_args(s, -1);
+  a.cond = static_cast<unsigned long long>(h);
+  mfb::launch_epoch_regions(a, cs);
+  CK(cudaStreamEndCapture(cs, &body));
+  CK(cudaStreamDestroy(cs));
+  CK(cudaGraphInstantiate(&s->loop_exec, s->loop_graph, 0));
 }
 
 }  // namespace
@@ -914,10 +1051,12 @@ MFB_API int mfadd_solver_create(mfadd_context* ctx, const mfadd_decomposition* d
                         " contributions for a control shared by " + std::to_string(ns) + " blocks";
     }
     s->pair_slot.upload(ps, st);
+    if (s->max_holders <= 8 && d.any_shared) build_regions(s.get(), ps);
     s->pair_jumps.alloc(static_cast<std::size_t>(std::max(1, s->npairs)) * 2);
     s->change.alloc(static_cast<std::size_t>(d.nblocks));
     s->linf_sh.alloc(static_cast<std::size_t>(d.nblocks));
     s->acc.alloc(1);
+    s->est.alloc(1);
     s->epoch_out.alloc(static_cast<std::size_t>(cfg->max_outer_iterations + 1) * 3 + 3);
     s->lattice.alloc(static_cast<std::size_t>(d.total_ctrl()));
     if (cfg->store_error) s->error.alloc(static_cast<std::size_t>(d.total_inputs()));
@@ -961,6 +1100,8 @@ MFB_API int mfadd_solver_create(mfadd_context* ctx, const mfadd_decomposition* d
     CK(cudaMemsetAsync(s->change.p, 0, s->change.n * sizeof(unsigned long long), st));
     CK(cudaMemsetAsync(s->linf_sh.p, 0, s->linf_sh.n * sizeof(unsigned long long), st));
     CK(cudaMemsetAsync(s->acc.p, 0, sizeof(mfb::EpochAcc), st));
+    CK(cudaMemsetAsync(s->est.p, 0, sizeof(mfb::EpochState), st));
+    if (s->ntiles > 0 && cfg->enforce_continuity) build_loop_graph(s.get());
     CK(cudaStreamSynchronize(st));
     *out = s.release();
   });
@@ -1049,44 +1190,37 @@ void solve_impl(mfadd_solver* s, const double* dfield) {
   launches += wl.fit(ctx, dfield, &s->tl);
   CK(cudaEventRecord(s->ev[2], st));
   // ---- record_epoch(0, 0.0)
-  launches += run_epoch(s, 0, 0);
-  double* hp = ctx->h_pinned;
-  CK(cudaMemcpyAsync(hp, s->epoch_out.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
-  const mfb::DevStatus stt = read_status(ctx);  // synchronises
-  wl.raise_status(stt, "");
-  s->epochs.push_back({0, 0.0, hp[1], hp[2]});
-  mfadd_solve_summary& sum = s->summary;
-  sum = mfadd_solve_summary{};
-  sum.converged = 1;
-  if (s->cfg.enforce_continuity && d.any_shared) {
-    if (!s->holder_fault.empty()) throw std::runtime_error(s->holder_fault);
-    sum.converged = 0;
-    for (int iter = 1; iter <= s->cfg.max_outer_iterations; ++iter) {
-      launches += run_epoch(s, iter >= 2 ? 2 : 1, iter);  // solver.cpp:397
-      CK(cudaMemcpyAsync(hp, s->epoch_out.p + 3 * iter, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      const double dpv = hp[0];
-      s->epochs.push_back({iter, dpv, hp[1], hp[2]});
-      sum.final_dp = dpv;
-      if (dpv < s->cfg.tolerance) {  // solver.cpp:406-412
-        sum.converged = 1;
-        sum.constraint_iterations = iter - 1;
-        break;
-      }
-      sum.constraint_iterations = iter;
-    }
+  const bool regions = s->ntiles > 0;
+  const bool loop = s->cfg.enforce_continuity && d.any_shared;
+  if (loop && !s->holder_fault.empty()) {
+    // the reference fails in the fit first if it is singular, then in the
+    // first exchange epoch (solver.cpp:134-141)
+    wl.raise_status(read_status(ctx), "");
+    throw std::runtime_error(s->holder_fault);
+  }
+  CK(cudaMemsetAsync(s->est.p, 0, sizeof(mfb::EpochState), st));
+  if (regions) {
+    s->tl.begin("epoch");
+    launches += mfb::launch_epoch_regions(region_args(s, 0), st);
+    s->tl.end();
+  } else {
+    launches += run_epoch(s, 0, 0);
+  }
+  // ---- outer iterations (solver.cpp:394-413), entirely on the device
+  if (loop) {
+    s->tl.begin("epoch");
+    CK(cudaGraphLaunch(s->loop_exec, st));
+    s->tl.end();
   }
   CK(cudaEventRecord(s->ev[3], st));
-  // ---- final jumps per neighbour pair (solver.cpp:416).  When the last
-  // epoch averaged every shared control (mode 2), all copies of each control
-  // are bit-identical, so every per-pair jump is exactly 0: skip the pass.
-  const bool last_all = !s->epochs.empty() && s->epochs.back().iteration >= 2;
-  if (s->npairs > 0 && last_all) {
-    CK(cudaMemsetAsync(s->pair_jumps.p, 0, s->pair_jumps.n * sizeof(unsigned long long), st));
-  } else if (s->npairs > 0) {
+  // ---- final jumps per neighbour pair (solver.cpp:416).  After a mode-2
+  // epoch all copies of each control are bit-identical and every per-pair
+  // jump is exactly 0 (the kernel checks the last iteration on the device).
+  if (s->npairs > 0) {
     CK(cudaMemsetAsync(s->pair_jumps.p, 0, s->pair_jumps.n * sizeof(unsigned long long), st));
     s->tl.begin("pair_jumps");
-    launches += mfb::launch_epoch(epoch_args(s, 3), st);
+    launches += regions ? mfb::launch_epoch_regions(region_args(s, 3), st)
+                        : mfb::launch_epoch(epoch_args(s, 3), st);
     s->tl.end();
   }
   // ---- assemble_owned (solver.cpp:418-423)
@@ -1178,13 +1312,37 @@ void solve_impl(mfadd_solver* s, const double* dfield) {
   launches += mfb::launch_reduce_partials(s->partial.p, nparts, s->red2.p, st);
   s->tl.end();
   CK(cudaGetLastError());
+  double* hp = ctx->h_pinned;
   CK(cudaMemcpyAsync(hp + 4, s->red2.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  std::vector<double> eo(s->epoch_out.n);
+  CK(cudaMemcpyAsync(eo.data(), s->epoch_out.p, eo.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+  mfb::EpochState es{};
+  CK(cudaMemcpyAsync(&es, s->est.p, sizeof es, cudaMemcpyDeviceToHost, st));
+  mfb::DevStatus stt{};
+  CK(cudaMemcpyAsync(&stt, ctx->d_status, sizeof stt, cudaMemcpyDeviceToHost, st));
   std::vector<unsigned long long> pj(s->pair_jumps.n);
   if (s->npairs > 0)
     CK(cudaMemcpyAsync(pj.data(), s->pair_jumps.p, pj.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                        st));
   CK(cudaEventRecord(s->ev[4], st));
   CK(cudaStreamSynchronize(st));
+  if (stt.code) {
+    CK(cudaMemsetAsync(ctx->d_status, 0, sizeof(mfb::DevStatus), st));
+    wl.raise_status(stt, "");
+  }
+  mfadd_solve_summary& sum = s->summary;
+  sum = mfadd_solve_summary{};
+  s->epochs.push_back({0, 0.0, eo[1], eo[2]});
+  sum.converged = 1;
+  if (loop) {
+    const int last = es.iter;
+    for (int it = 1; it <= last; ++it)
+      s->epochs.push_back({it, eo[3 * it], eo[3 * it + 1], eo[3 * it + 2]});
+    sum.final_dp = eo[3 * last];
+    sum.converged = es.converged;
+    sum.constraint_iterations = es.converged ? last - 1 : last;  // solver.cpp:406-412
+    launches += last;  // one epoch kernel per loop iteration
+  }
   sum.global_l2 = std::sqrt(hp[4]);
   sum.global_linf = hp[5];
   s->final_jumps.assign(static_cast<std::size_t>(s->npairs) * 4, 0.0);

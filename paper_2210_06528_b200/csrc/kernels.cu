@@ -830,6 +830,233 @@ __global__ void __launch_bounds__(kEpochThreads) k_epoch8(EpochArgs a) {
   }
 }
 
+// ------------------------------------------------------- K4 (region form)
+// enforce_constraints (solver.cpp:112-164) + record_epoch jumps (:166-193)
+// over one tile of a region.  Every control of the region has the same NS
+// holders, so holder ids, offsets and the per-holder reductions are uniform
+// across the CTA: one atomic per holder per CTA instead of per control.
+constexpr int kRegionThreads = 256;
+constexpr int kRegionWarps = kRegionThreads / 32;
+constexpr int kRegionPerThread = 2;  // controls per thread per tile (n_s == 2: loads issued together)
+
+__device__ __forceinline__ double warp_dmax(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(kFull, v, o));
+  return v;
+}
+
+// CTA max of K non-negative doubles with one barrier; thread j < K receives
+// value j's CTA max (as a bit pattern, ordered like the value).
+template <int K>
+__device__ __forceinline__ unsigned long long cta_dmax_multi(double (&v)[K], double (*s_w)[kRegionWarps]) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const double r = warp_dmax(v[j]);
+    if (lane == 0) s_w[j][w] = r;
+  }
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x < K)
+    for (int i = 0; i < kRegionWarps; ++i) r = fmax(r, s_w[threadIdx.x][i]);
+  return dbits(r);
+}
+
+struct RegionRegs {
+  long long base;
+  int s0, s1, s2;
+};
+
+// R is the CTA's shared-memory copy of the region descriptor.  PT controls
+// per thread per pass (PT loads per holder in flight); the n_s = 8 form keeps
+// offsets in shared memory to stay within the register budget.
+template <int NS>
+__device__ __forceinline__ void region_tile(const EpochRegionArgs& a, const RegionDev& R, const TileDev& t, int mode,
+                                            double (*s_w)[kRegionWarps]) {
+  constexpr int PT = NS == 2 ? kRegionPerThread : 1;
+  const bool update = mode == 2 || (mode == 1 && NS == 2);
+  RegionRegs hr[NS <= 4 ? NS : 1];
+#pragma unroll
+  for (int h = 0; h < (NS <= 4 ? NS : 1); ++h) hr[h] = RegionRegs{R.base[h], R.str[h][0], R.str[h][1], R.str[h][2]};
+  auto offset = [&](int h, int r0, int r1, int r2) -> long long {
+    if (NS <= 4) return hr[h].base + static_cast<long long>(r0) * hr[h].s0 + r1 * hr[h].s1 + r2 * hr[h].s2;
+    return R.base[h] + static_cast<long long>(r0) * R.str[h][0] + r1 * R.str[h][1] + r2 * R.str[h][2];
+  };
+  const int e1 = R.ext[1], e2 = R.ext[2];
+  // update: red[h] = change of holder h, red[NS] = max |avg| (every copy);
+  // measure: red[h] = max |copy of holder h|, red[NS] = jump
+  double red[NS + 1];
+#pragma unroll
+  for (int j = 0; j <= NS; ++j) red[j] = 0.0;
+  const int end = t.start + t.count;
+  for (int i0 = t.start + threadIdx.x; i0 < end; i0 += kRegionThreads * PT) {
+    long long off[PT][NS];
+    double v[PT][NS];
+#pragma unroll
+    for (int u = 0; u < PT; ++u) {
+      const int i = i0 + u * kRegionThreads;
+      const int r2 = i % e2, q = i / e2;
+      const int r1 = q % e1, r0 = q / e1;
+#pragma unroll
+      for (int h = 0; h < NS; ++h) {
+        off[u][h] = offset(h, r0, r1, r2);
+        v[u][h] = i < end ? a.P[off[u][h]] : 0.0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < PT; ++u) {
+      if (i0 + u * kRegionThreads >= end) break;
+      if (update) {
+        double sum = 0.0;  // solver.cpp:147-159: ascending holder id, divide once
+#pragma unroll
+        for (int h = 0; h < NS; ++h) sum = __dadd_rn(sum, v[u][h]);
+        const double avg = __ddiv_rn(sum, static_cast<double>(NS));
+#pragma unroll
+        for (int h = 0; h < NS; ++h) {
+          red[h] = fmax(red[h], fabs(avg - v[u][h]));
+          a.P[off[u][h]] = avg;
+        }
+        red[NS] = fmax(red[NS], fabs(avg));  // every holder's copy is now avg
+      } else {
+        double mn = v[u][0], mx = v[u][0];
+#pragma unroll
+        for (int h = 0; h < NS; ++h) {
+          mn = fmin(mn, v[u][h]);
+          mx = fmax(mx, v[u][h]);
+          red[h] = fmax(red[h], fabs(v[u][h]));
+        }
+        red[NS] = fmax(red[NS], mx - mn);  // all holders are mutual neighbours
+      }
+    }
+  }
+  const unsigned long long b = cta_dmax_multi<NS + 1>(red, s_w);
+  const int j = threadIdx.x;
+  if (b && j < NS) {
+    atomicMax((update ? a.change : a.linf_sh) + R.ids[j], b);
+  } else if (b && j == NS) {
+    if (update) {
+#pragma unroll
+      for (int h = 0; h < NS; ++h) atomicMax(a.linf_sh + R.ids[h], b);
+    } else {
+      atomicMax(NS == 2 ? &a.st->jump_ss : &a.st->jump_ms, b);
+    }
+  }
+  __syncthreads();  // s_w and s_R are reused by the next tile
+}
+
+// MAXNS = 4 for 1-D/2-D decompositions (tighter register budget, 3 CTAs/SM),
+// 8 for 3-D.
+template <int MAXNS>
+__global__ void __launch_bounds__(kRegionThreads, MAXNS == 8 ? 2 : 3) k_epoch_regions(EpochRegionArgs a) {
+  __shared__ double s_w[2 * kRegionMaxHolders + 1][kRegionWarps];
+  __shared__ unsigned long long s_red[32];
+  __shared__ int s_last;
+  __shared__ RegionDev s_R;
+  const int iter = a.mode < 0 ? a.st->iter + 1 : 0;
+  const int mode = a.mode < 0 ? (iter >= 2 ? 2 : 1) : a.mode;  // solver.cpp:397
+  for (int tb = blockIdx.x; tb < a.ntiles; tb += gridDim.x) {
+    const TileDev t = a.tiles[tb];
+    {
+      const int* src = reinterpret_cast<const int*>(a.regions + t.region);
+      int* dst = reinterpret_cast<int*>(&s_R);
+      for (int w = threadIdx.x; w < static_cast<int>(sizeof(RegionDev) / 4); w += blockDim.x) dst[w] = src[w];
+    }
+    __syncthreads();
+    const RegionDev& R = s_R;
+    switch (R.ns) {
+      case 2: region_tile<2>(a, R, t, mode, s_w); break;
+      case 4: region_tile<4>(a, R, t, mode, s_w); break;
+      default: region_tile<MAXNS>(a, R, t, mode, s_w); break;
+    }
+  }
+  // last CTA: dp = max_b change_b / max(1, ||P_b||_inf) (solver.cpp:398-405)
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&a.st->done, 1) == static_cast<int>(gridDim.x) - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  unsigned long long dp = 0ull;
+  for (int b = threadIdx.x; b < a.nblocks; b += blockDim.x) {
+    const unsigned long long li = umax(a.linf_int[b], __ldcg(a.linf_sh + b));
+    const double lin = __longlong_as_double(static_cast<long long>(li));
+    const double chv = __longlong_as_double(static_cast<long long>(__ldcg(a.change + b)));
+    dp = umax(dp, dbits(chv / (lin > 1.0 ? lin : 1.0)));
+    a.change[b] = 0ull;
+    a.linf_sh[b] = 0ull;
+  }
+  dp = block_umax(dp, s_red);
+  if (threadIdx.x == 0) {
+    const double dpv = mode == 0 ? 0.0 : __longlong_as_double(static_cast<long long>(dp));  // record_epoch(0, 0.0)
+    const unsigned long long js = atomicExch(&a.st->jump_ss, 0ull), jm = atomicExch(&a.st->jump_ms, 0ull);
+    double* out = a.epoch_out + 3 * iter;
+    out[0] = dpv;
+    out[1] = __longlong_as_double(static_cast<long long>(js));
+    out[2] = __longlong_as_double(static_cast<long long>(jm));
+    a.st->done = 0;
+    if (a.mode < 0) {  // loop bookkeeping (solver.cpp:406-412)
+      const bool conv = dpv < a.tol;
+      a.st->last_iter = iter;
+      a.st->converged = conv ? 1 : 0;
+      a.st->iter = iter;
+      cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(a.cond),
+                              (!conv && iter < a.max_iter) ? 1u : 0u);
+    }
+  }
+}
+
+// Final per-pair jumps (solver.cpp:416 -> :166-193): L-inf of |P_a - P_b| per
+// holder pair of each region, split SS/MS by the region's n_s.  Only needed
+// when the last epoch did not average every shared control.
+template <int NS>
+__device__ __forceinline__ void region_pairs(const EpochRegionArgs& a, const RegionDev& R, const TileDev& t,
+                                             double (*s_w)[kRegionWarps]) {
+  constexpr int NP = NS * (NS - 1) / 2;
+  double pj[NP];
+#pragma unroll
+  for (int q = 0; q < NP; ++q) pj[q] = 0.0;
+  const int e1 = R.ext[1], e2 = R.ext[2];
+  for (int i = t.start + threadIdx.x; i < t.start + t.count; i += kRegionThreads) {
+    const int r2 = i % e2, q = i / e2;
+    const int r1 = q % e1, r0 = q / e1;
+    double v[NS];
+#pragma unroll
+    for (int h = 0; h < NS; ++h)
+      v[h] = a.P[R.base[h] + static_cast<long long>(r0) * R.str[h][0] + r1 * R.str[h][1] + r2 * R.str[h][2]];
+    int q2 = 0;
+#pragma unroll
+    for (int h1 = 0; h1 < NS; ++h1)
+#pragma unroll
+      for (int h2 = h1 + 1; h2 < NS; ++h2, ++q2) pj[q2] = fmax(pj[q2], fabs(v[h1] - v[h2]));
+  }
+  // NP <= 28 > 2*kRegionMaxHolders+1 slots: reduce in chunks of 16
+#pragma unroll
+  for (int c0 = 0; c0 < NP; c0 += 16) {
+    double part[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) part[j] = c0 + j < NP ? pj[c0 + j] : 0.0;
+    const unsigned long long b = cta_dmax_multi<16>(part, s_w);
+    const int q = c0 + static_cast<int>(threadIdx.x);
+    if (threadIdx.x < 16 && q < NP && R.pslot[q] >= 0 && b)
+      atomicMax(a.pair_jumps + 2 * R.pslot[q] + (NS > 2 ? 1 : 0), b);
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kRegionThreads) k_pair_jumps_regions(EpochRegionArgs a) {
+  __shared__ double s_w[2 * kRegionMaxHolders + 1][kRegionWarps];
+  if (a.st->last_iter >= 2) return;  // after a mode-2 epoch all copies agree bitwise
+  for (int tb = blockIdx.x; tb < a.ntiles; tb += gridDim.x) {
+    const TileDev t = a.tiles[tb];
+    const RegionDev& R = a.regions[t.region];
+    switch (R.ns) {
+      case 2: region_pairs<2>(a, R, t, s_w); break;
+      case 4: region_pairs<4>(a, R, t, s_w); break;
+      default: region_pairs<8>(a, R, t, s_w); break;
+    }
+  }
+}
+
 // ------------------------------------------------------------------- K5
 __global__ void __launch_bounds__(1024) k_dp(DpArgs a) {
   __shared__ unsigned long long red[32];
@@ -1130,6 +1357,17 @@ int launch_epoch(const EpochArgs& a, cudaStream_t s) {
     k_epoch<8><<<grid, kEpochThreads, 0, s>>>(a);
   else
     k_epoch<27><<<grid, kEpochThreads, 0, s>>>(a);
+  return 1;
+}
+
+int launch_epoch_regions(const EpochRegionArgs& a, cudaStream_t s) {
+  if (a.ntiles <= 0) return 0;
+  if (a.mode == 3)
+    k_pair_jumps_regions<<<a.ntiles, kRegionThreads, 0, s>>>(a);
+  else if (a.max_ns > 4)
+    k_epoch_regions<8><<<a.ntiles, kRegionThreads, 0, s>>>(a);
+  else
+    k_epoch_regions<4><<<a.ntiles, kRegionThreads, 0, s>>>(a);
   return 1;
 }
 

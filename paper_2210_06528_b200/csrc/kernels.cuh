@@ -103,6 +103,29 @@ struct EpochArgs {
 };
 int launch_epoch(const EpochArgs& a, cudaStream_t s);
 
+// K4 (region form, n_s <= 8): one CTA per tile of a region's box; holder ids
+// and offsets are CTA-uniform.  The last CTA to finish computes dp (K5 fused)
+// and, inside the epoch-loop graph, sets the WHILE condition.
+struct EpochRegionArgs {
+  const RegionDev* regions;
+  const TileDev* tiles;
+  int ntiles;
+  int nblocks;
+  double* P;
+  int mode;  // 0 measure, 3 final pair jumps, -1 loop (1 on iteration 1, 2 after)
+  unsigned long long* change;
+  unsigned long long* linf_sh;
+  const unsigned long long* linf_int;
+  EpochState* st;
+  double* epoch_out;  // 3 doubles per epoch slot: dp, jump_ss, jump_ms
+  unsigned long long* pair_jumps;
+  int max_iter;
+  double tol;
+  unsigned long long cond;  // cudaGraphConditionalHandle (loop mode only)
+  int max_ns;               // largest region n_s (selects the kernel form)
+};
+int launch_epoch_regions(const EpochRegionArgs& a, cudaStream_t s);
+
 // K5: dp = max_b change_b / max(1, ||P_b||_inf) and epoch bookkeeping.
 struct DpArgs {
   int nblocks;
