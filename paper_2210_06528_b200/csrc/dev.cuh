@@ -38,7 +38,13 @@ struct BlockDev {
   std::int64_t poff;   // offset of the held lattice P_b
   std::int64_t t1off;  // axis-0 intermediate   [n0][m1][m2]
   std::int64_t t2off;  // axis-1 intermediate   [n0][n1][m2]
+  std::int64_t coff;   // last-axis segment carries [K-1][P+1][lines]
 };
+
+// Last-axis row segments (k_last_contract_tma): per axis problem
+// {K, js[0..K]} padded to kSegStride ints.
+constexpr int kMaxSeg = 8;
+constexpr int kSegStride = kMaxSeg + 2;
 
 // Status word written by kernels when the reference would throw.
 struct DevStatus {

@@ -276,7 +276,11 @@ struct Workload {
   int axis0_tiles = 0;
   // TMA last-axis pass (D >= 2)
   bool tma_last = false;
-  int last_LT = 128, last_ltcap = 0;
+  int last_LT = 128, last_ltcap = 0, last_kseg = 1;
+  std::vector<int> segtab;  // kSegStride ints per axis problem (last-axis problems filled)
+  DBuf<int> d_segtab;
+  DBuf<double> carry;
+  std::int64_t total_carry = 0;
   std::array<std::int64_t, 3> field_dims{1, 1, 1};  // global field extents (solver) for the tensor map
 
   void plan_tma(bool enable) {
@@ -319,6 +323,43 @@ struct Workload {
       last_LT = round_up((max_lines_last + ncta - 1) / ncta, 32);  // whole warps
       last_ltcap = needl;
       tma_last = true;
+      plan_segments();
+    }
+  }
+
+  // Row segments of the last-axis problems: about 4 contraction threads per
+  // SM thread slot over all lines, segments of >= 64 rows on 16-row chunk
+  // boundaries; carries sized per block.
+  void plan_segments() {
+    std::int64_t lines = 0;
+    for (const auto& b : blocks) {
+      std::int64_t Ll = 1;
+      for (int k = 0; k + 1 < D; ++k) Ll *= probs[static_cast<std::size_t>(b.ax[k])].n;
+      lines += round_up(static_cast<int>(Ll), last_LT);
+    }
+    const int want = static_cast<int>(std::lround(4.0 * 148 * 256 / static_cast<double>(std::max<std::int64_t>(lines, 1))));
+    segtab.assign(probs.size() * mfb::kSegStride, 0);
+    last_kseg = 1;
+    for (const auto& b : blocks) {
+      const int pid = b.ax[D - 1];
+      const AxisProb& pr = probs[static_cast<std::size_t>(pid)];
+      int K = std::max(1, std::min({want, mfb::kMaxSeg, pr.m / 64}));
+      // a segment must span more than P+1 columns so that carry ranges of
+      // consecutive boundaries never overlap
+      while (K > 1 && static_cast<std::int64_t>(pr.n) < static_cast<std::int64_t>(K) * 4 * (p + 1)) --K;
+      int* t = segtab.data() + static_cast<std::size_t>(pid) * mfb::kSegStride;
+      t[0] = K;
+      for (int sgi = 0; sgi <= K; ++sgi)
+        t[1 + sgi] = sgi == K ? pr.m : std::min(pr.m, (static_cast<int>(static_cast<std::int64_t>(pr.m) * sgi / K) + 8) / 16 * 16);
+      last_kseg = std::max(last_kseg, K);
+    }
+    total_carry = 0;
+    for (auto& b : blocks) {
+      std::int64_t Ll = 1;
+      for (int k = 0; k + 1 < D; ++k) Ll *= probs[static_cast<std::size_t>(b.ax[k])].n;
+      const int K = segtab[static_cast<std::size_t>(b.ax[D - 1]) * mfb::kSegStride];
+      b.coff = total_carry;
+      total_carry += static_cast<std::int64_t>(K - 1) * (p + 1) * Ll;
     }
   }
 
@@ -394,6 +435,10 @@ struct Workload {
     P.alloc(static_cast<std::size_t>(total_p));
     Y.alloc(static_cast<std::size_t>(total_p));
     linf_int.alloc(blocks.size());
+    if (tma_last) {
+      d_segtab.upload(segtab, s);
+      carry.alloc(static_cast<std::size_t>(std::max<std::int64_t>(total_carry, 1)));
+    }
   }
 
   // K1 + K2
@@ -443,6 +488,8 @@ struct Workload {
     }
     fa.max_lines_last = max_lines_last;
     fa.pitch_last = pitch_last;
+    fa.segtab = d_segtab.p;
+    fa.carry = carry.p;
     fa.n_field = field_n;
     fa.n_t1 = total_t1;
     fa.n_t2 = total_t2;
@@ -476,7 +523,7 @@ struct Workload {
       const std::uint64_t dims[2] = {static_cast<std::uint64_t>(pitch_last), static_cast<std::uint64_t>(rows)};
       const std::uint32_t box[2] = {16u, static_cast<std::uint32_t>(last_LT)};
       const CUtensorMap map = make_tmap(src, 2, dims, box, CU_TENSOR_MAP_SWIZZLE_128B);
-      l += mfb::launch_fit_last_tma(p, fa, map, last_LT, last_ltcap, ctx->stream);
+      l += mfb::launch_fit_last_tma(p, fa, map, last_LT, last_ltcap, last_kseg, ctx->stream);
     } else {
       l += mfb::launch_fit_last(p, fa, ctx->stream);
     }

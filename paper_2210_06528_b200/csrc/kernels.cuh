@@ -67,6 +67,8 @@ struct FitArgs {
   int max_lines_last;
   std::int64_t pitch_last;           // row pitch (even) of the last-axis input (T1 for D=2, T2 for D=3)
   std::int64_t n_field, n_t1, n_t2, n_P;  // buffer sizes (debug bounds checks)
+  const int* segtab;                 // last-axis row segments per axis problem (kSegStride ints)
+  double* carry;                     // last-axis segment carries (BlockDev::coff)
 };
 int launch_fit_strided(int degree, const FitArgs& a, int axis, cudaStream_t s);  // axis < D-1
 int launch_fit_last(int degree, const FitArgs& a, cudaStream_t s);
@@ -182,7 +184,8 @@ int launch_fit_axis0_tma(int degree, const FitArgs& a, const CUtensorMap& map, c
 
 // TMA last-axis fit pass (D >= 2): 128-B swizzled 16-column boxes of the
 // last-axis input, LT lines per CTA.
-int launch_fit_last_tma(int degree, const FitArgs& a, const CUtensorMap& map, int LT, int lt_cap, cudaStream_t s);
+int launch_fit_last_tma(int degree, const FitArgs& a, const CUtensorMap& map, int LT, int lt_cap, int kseg,
+                        cudaStream_t s);
 
 // TMA decode sweep over the whole input grid (D = 2, 3), stream_tma.cu.
 struct DecodeSweepArgs {

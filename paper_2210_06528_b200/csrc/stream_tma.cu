@@ -294,163 +294,124 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
 }
 
 // ---------------------------------------------------------------- fit last axis
-// One thread per line of the last-axis input (T1 rows for D = 2, T2 rows for
-// D = 3; common even pitch).  A stage is a 16-column x LT-line box (128 B per
-// line, SWIZZLE_128B: 16-B chunk k of line t sits at chunk k ^ (t & 7), so the
-// per-thread LDS.128 of two columns is bank-conflict free) plus the matching
-// basis rows.  Forward substitution goes to the transposed scratch Y[c][l]
-// (coalesced); back substitution is staged through smem to write P rows.
+// The last-axis pass (lsq.cpp:57-61 on axis D-1) in two kernels:
+//
+//  k_last_contract_tma  Z = R^T y per line (collocation.cpp:46-54), each line
+//                       split into up to kMaxSeg row segments so that
+//                       lines x segments threads stream the input (4x the
+//                       parallelism of one thread per line).  Segment s owns
+//                       the columns below the next segment's first column
+//                       cs_{s+1} = g0(js_{s+1}); its partial sums for columns
+//                       cs_{s+1} .. cs_{s+1}+P go to a carry buffer.
+//  k_last_solve         per line: add the carries, forward and back
+//                       substitution with the banded Cholesky factor
+//                       (lsq.cpp:59-60), write P, per-block max |P| over
+//                       non-shared controls.
+//
+// Input boxes: 16 columns x LT lines, SWIZZLE_128B (16-B chunk k of line t at
+// chunk k ^ (t & 7): the per-thread LDS.128 of two columns is conflict-free),
+// plus the chunk's basis rows by 1-D bulk copies, in an S-stage TMA ring.
 constexpr int kLastCW = 16;
-constexpr int kLastS = 4;
+constexpr int kLastS = 2;
 
 __host__ __device__ inline int last_stage_bytes(int LT, int P) {
   return ((LT * 128 + kLastCW * (P + 1) * 8 + kLastCW * 4) + 1023) / 1024 * 1024;
 }
 
 template <int P>
-__global__ void __launch_bounds__(256) k_fit_last_tma(const FitArgs a, const __grid_constant__ CUtensorMap map,
-                                                      const int LT) {
+__global__ void __launch_bounds__(256) k_last_contract_tma(const FitArgs a, const __grid_constant__ CUtensorMap map,
+                                                           const int LT) {
   extern __shared__ __align__(1024) unsigned char sm_raw[];
-  __shared__ unsigned long long s_red[32];
-  constexpr int S = kLastS, CW = kLastCW, LW = 2 * P + 1;
+  constexpr int S = kLastS, CW = kLastCW;
   const int D = a.D, d = D - 1;
-  const int b = blockIdx.y;
-  const BlockDev blk = a.blocks[b];
-  const AxisProb pr = a.probs[blk.ax[d]];
-  const int m = pr.m, n = pr.n;
+  const int b = blockIdx.y, sgi = blockIdx.z;
+  const BlockDev& blk = a.blocks[b];  // by reference: ax[] is indexed at run time
+  const int pid = blk.ax[d];
+  const int* seg = a.segtab + pid * kSegStride;
+  const int K = seg[0];
+  if (sgi >= K) return;
+  const AxisProb pr = a.probs[pid];
+  const int n = pr.n;
   std::int64_t L = 1;
   for (int k = 0; k < d; ++k) L *= a.probs[blk.ax[k]].n;
   const std::int64_t l0 = static_cast<std::int64_t>(blockIdx.x) * LT;
   if (l0 >= L) return;
-  const int nl = static_cast<int>((L - l0) < LT ? (L - l0) : LT);
   const int tid = threadIdx.x;
-  const bool active = tid < nl;
-  const int row0 = static_cast<int>((D == 2 ? blk.t1off : blk.t2off) / a.pitch_last + l0);
+  const bool active = l0 + tid < L;
+  const int js = seg[1 + sgi], je = seg[2 + sgi];
   const int* g0g = a.g0 + pr.row_off;
   const double* vg = a.vals + pr.row_off * (P + 1);
-  const double* lt = a.ltab + pr.col_off * LW;
-  double* Pb = a.P + blk.poff + l0 * n;
-  double* Yb = a.Y + blk.poff + l0 + tid;  // transposed scratch: Y[c*L + l]
+  const int cs_next = sgi + 1 < K ? __ldg(g0g + je) : 0x7fffffff;  // first column of the next segment
+  const int row0 = static_cast<int>((D == 2 ? blk.t1off : blk.t2off) / a.pitch_last + l0);
+  double* Zb = a.Y + blk.poff + l0 + tid;                                        // Z[c*L + l]
+  double* Cb = a.carry + blk.coff + static_cast<std::int64_t>(sgi) * (P + 1) * L + l0 + tid;  // carry[s][k][l]
 
   const int SB = last_stage_bytes(LT, P);
   const int v_off = LT * 128, g_off = v_off + CW * (P + 1) * 8;
   std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(sm_raw + S * SB);
-  double* s_lt = reinterpret_cast<double*>(sm_raw + S * SB + 128);
-  const int nchunks = (m + CW - 1) / CW;
+  const int c_first = js / CW, nchunks = (je + CW - 1) / CW - c_first;
   const unsigned tx_bytes = static_cast<unsigned>(LT * 128 + CW * (P + 1) * 8 + CW * 4);
-  auto issue = [&](int c) {
+  auto issue = [&](int c) {  // c: chunk index within the segment
     const int st = c % S;
     unsigned char* base = sm_raw + st * SB;
+    const int col = (c_first + c) * CW;
     mbar_arrive_expect_tx(&bars[st], tx_bytes);
-    tma_load_2d(base, &map, c * CW, row0, &bars[st]);
-    bulk_load_1d(base + v_off, vg + static_cast<std::int64_t>(c) * CW * (P + 1), CW * (P + 1) * 8, &bars[st]);
-    bulk_load_1d(base + g_off, g0g + static_cast<std::int64_t>(c) * CW, CW * 4, &bars[st]);
+    tma_load_2d(base, &map, col, row0, &bars[st]);
+    bulk_load_1d(base + v_off, vg + static_cast<std::int64_t>(col) * (P + 1), CW * (P + 1) * 8, &bars[st]);
+    bulk_load_1d(base + g_off, g0g + col, CW * 4, &bars[st]);
   };
   if (tid == 0) {
     prefetch_tmap(&map);
     for (int st = 0; st < S; ++st) mbar_init(&bars[st], 1);
     fence_mbar_init();
-  }
-  for (int i = tid; i < (n + 2 * (P + 1)) * LW; i += blockDim.x) {
-    const int cc = i / LW - (P + 1);
-    s_lt[i] = (cc >= 0 && cc < n) ? __ldg(lt + static_cast<std::int64_t>(cc) * LW + (i - (i / LW) * LW)) : 0.0;
-  }
-  const double* slt = s_lt + (P + 1) * LW;
-  __syncthreads();
-  if (tid == 0)
     for (int c = 0; c < S && c < nchunks; ++c) issue(c);
+  }
+  __syncthreads();
 
-  double acc[P + 1], yw[P], Lnx[P + 1];
+  // sliding window: acc[k] accumulates column cbase + k
+  double acc[P + 1];
 #pragma unroll
   for (int k = 0; k <= P; ++k) acc[k] = 0.0;
-#pragma unroll
-  for (int k = 0; k < P; ++k) yw[k] = 0.0;
-  int cbase = __ldg(g0g) < 0 ? __ldg(g0g) : 0;
-  int ph = 0;
-  auto fetch_fwd = [&](int cc) {
-    const double* Lc = slt + (cc < -(P + 1) ? -(P + 1) : cc) * LW;
-#pragma unroll
-    for (int k = 0; k <= P; ++k) Lnx[k] = Lc[k];
-  };
-  fetch_fwd(cbase);
-  auto flush_slot = [&](auto phc) {
-    constexpr int PH = decltype(phc)::value;
-    const int cc = cbase;
-    if (cc >= 0 && cc < n) {
-      double sacc = acc[PH];
-#pragma unroll
-      for (int k = 1; k <= P; ++k) sacc = fma(-Lnx[k], yw[k - 1], sacc);
-      const double y = sacc * Lnx[0];
-      if (active) Yb[static_cast<std::int64_t>(cc) * L] = y;
-#pragma unroll
-      for (int k = P - 1; k >= 1; --k) yw[k] = yw[k - 1];
-      yw[0] = y;
-    }
-    acc[PH] = 0.0;
-    ++cbase;
-    fetch_fwd(cbase);
-  };
-  auto accum = [&](auto phc, const double* vr, double q) {
-    constexpr int PH = decltype(phc)::value;
-#pragma unroll
-    for (int k = 0; k <= P; ++k) acc[(PH + k) % (P + 1)] = fma(vr[k], q, acc[(PH + k) % (P + 1)]);
-  };
-#define MFB_PHASE_SWITCH(CALL)                  \
-  switch (ph) {                                 \
-    case 0: CALL(Int<0>{}); break;              \
-    case 1: CALL(Int<1 % (P + 1)>{}); break;    \
-    case 2: CALL(Int<2 % (P + 1)>{}); break;    \
-    case 3: CALL(Int<3 % (P + 1)>{}); break;    \
-    case 4: CALL(Int<4 % (P + 1)>{}); break;    \
-    case 5: CALL(Int<5 % (P + 1)>{}); break;    \
-    case 6: CALL(Int<6 % (P + 1)>{}); break;    \
-    case 7: CALL(Int<7 % (P + 1)>{}); break;    \
-    case 8: CALL(Int<8 % (P + 1)>{}); break;    \
-    default: CALL(Int<9 % (P + 1)>{}); break;   \
-  }
-  auto column = [&](int j, const int* sg, const double* sv, double q) {
-    const int g = sg[j];
-    while (cbase < g) {
-#define MFB_FLUSH_CALL(X) flush_slot(X)
-      MFB_PHASE_SWITCH(MFB_FLUSH_CALL)
-#undef MFB_FLUSH_CALL
-      ph = ph == P ? 0 : ph + 1;
-    }
-    const double* vr = sv + j * (P + 1);
-#define MFB_ACC_CALL(X) accum(X, vr, q)
-    MFB_PHASE_SWITCH(MFB_ACC_CALL)
-#undef MFB_ACC_CALL
-  };
-
+  int cbase = __ldg(g0g + js);
+  if (sgi == 0 && cbase > 0) cbase = 0;
+#define MFB_LAST_FLUSH()                                                       \
+  do {                                                                         \
+    const int cc = cbase;                                                      \
+    if (cc >= 0 && cc < n && active) {                                        \
+      if (cc >= cs_next)                                                       \
+        Cb[static_cast<std::int64_t>(cc - cs_next) * L] = acc[0];              \
+      else                                                                     \
+        Zb[static_cast<std::int64_t>(cc) * L] = acc[0];                        \
+    }                                                                          \
+    _Pragma("unroll") for (int k = 0; k < P; ++k) acc[k] = acc[k + 1];         \
+    acc[P] = 0.0;                                                              \
+    ++cbase;                                                                   \
+  } while (0)
   const int swz = tid & 7;
   for (int c = 0; c < nchunks; ++c) {
     const int st = c % S;
     const unsigned char* base = sm_raw + st * SB;
     const int* sg = reinterpret_cast<const int*>(base + g_off);
     const double* sv = reinterpret_cast<const double*>(base + v_off);
-    mbar_wait(&bars[st], (c / S) & 1);
-    const int jn = (m - c * CW) < CW ? (m - c * CW) : CW;
     const double2* line = reinterpret_cast<const double2*>(base + tid * 128);
-#ifdef MFB_DEBUG
-    {
-      const double* srcd = (D == 2 ? a.t1 : a.t2) + static_cast<std::int64_t>(row0 + tid) * a.pitch_last;
-      for (int kk = 0; 2 * kk < jn && active; ++kk) {
-        const double2 q2 = line[kk ^ swz];
-        MFB_CHECK(q2.x == srcd[c * CW + 2 * kk]);
-        if (2 * kk + 1 < jn) MFB_CHECK(q2.y == srcd[c * CW + 2 * kk + 1]);
-      }
-      for (int j = 0; j < jn && tid == 0; ++j) {
-        MFB_CHECK(sg[j] == g0g[c * CW + j]);
-        for (int k = 0; k <= P; ++k) MFB_CHECK(sv[j * (P + 1) + k] == vg[(c * CW + j) * (P + 1) + k]);
-      }
-    }
-#endif
-#pragma unroll 1
+    const int jb = (c_first + c) * CW;
+    const int jlo = (js > jb ? js : jb) - jb, jhi = (je < jb + CW ? je : jb + CW) - jb;
+    mbar_wait(&bars[st], (c / S) & 1);
+#pragma unroll
     for (int kk = 0; kk < CW / 2; ++kk) {
-      if (2 * kk >= jn) break;
       const double2 q2 = line[kk ^ swz];
-      column(2 * kk, sg, sv, q2.x);
-      if (2 * kk + 1 < jn) column(2 * kk + 1, sg, sv, q2.y);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int jj = 2 * kk + e;
+        if (jj >= jlo && jj < jhi) {  // CTA-uniform
+          const int g = sg[jj];
+          while (cbase < g) MFB_LAST_FLUSH();
+          const double q = e ? q2.y : q2.x;
+          const double* vr = sv + jj * (P + 1);
+#pragma unroll
+          for (int k = 0; k <= P; ++k) acc[k] = fma(vr[k], q, acc[k]);
+        }
+      }
     }
     __syncthreads();
     if (tid == 0 && c + S < nchunks) {
@@ -458,14 +419,84 @@ __global__ void __launch_bounds__(256) k_fit_last_tma(const FitArgs a, const __g
       issue(c + S);
     }
   }
-  while (cbase < n) {
-#define MFB_FLUSH_CALL(X) flush_slot(X)
-    MFB_PHASE_SWITCH(MFB_FLUSH_CALL)
-#undef MFB_FLUSH_CALL
-    ph = ph == P ? 0 : ph + 1;
-  }
-#undef MFB_PHASE_SWITCH
+  // complete the segment's columns: up to the end of the line, or through the
+  // carry range cs_next .. cs_next+P of the next segment
+  const int cend = sgi + 1 < K ? cs_next + P + 1 : n;
+  while (cbase < cend) MFB_LAST_FLUSH();
+#undef MFB_LAST_FLUSH
+}
 
+template <int P>
+__global__ void __launch_bounds__(128) k_last_solve(const FitArgs a) {
+  extern __shared__ __align__(1024) unsigned char sm_raw[];
+  __shared__ unsigned long long s_red[32];
+  constexpr int LW = 2 * P + 1, XP = 33, U = 8;
+  const int D = a.D, d = D - 1;
+  const int b = blockIdx.y;
+  const BlockDev& blk = a.blocks[b];  // by reference: ax[] is indexed at run time
+  const int pid = blk.ax[d];
+  const AxisProb pr = a.probs[pid];
+  const int n = pr.n;
+  std::int64_t L = 1;
+  for (int k = 0; k < d; ++k) L *= a.probs[blk.ax[k]].n;
+  const std::int64_t l0 = static_cast<std::int64_t>(blockIdx.x) * blockDim.x;
+  if (l0 >= L) return;
+  const int nl = static_cast<int>((L - l0) < blockDim.x ? (L - l0) : blockDim.x);
+  const int tid = threadIdx.x;
+  const bool active = tid < nl;
+  double* s_x = reinterpret_cast<double*>(sm_raw);                 // blockDim x XP staging
+  double* s_lt = s_x + blockDim.x * XP;                            // (n + 2(P+1)) x LW, zero padded
+  const double* lt = a.ltab + pr.col_off * LW;
+  for (int i = tid; i < (n + 2 * (P + 1)) * LW; i += blockDim.x) {
+    const int cc = i / LW - (P + 1);
+    s_lt[i] = (cc >= 0 && cc < n) ? __ldg(lt + static_cast<std::int64_t>(cc) * LW + (i - (i / LW) * LW)) : 0.0;
+  }
+  const double* slt = s_lt + (P + 1) * LW;
+  __syncthreads();
+  double* Zb = a.Y + blk.poff + l0 + tid;
+  // add the segment carries (k_last_contract_tma) into Z
+  const int* seg = a.segtab + pid * kSegStride;
+  const int K = seg[0];
+  const int* g0g = a.g0 + pr.row_off;
+  if (active)
+    for (int s2 = 0; s2 + 1 < K; ++s2) {
+      const int cs = __ldg(g0g + seg[2 + s2]);
+      const double* Cb = a.carry + blk.coff + static_cast<std::int64_t>(s2) * (P + 1) * L + l0 + tid;
+#pragma unroll
+      for (int k = 0; k <= P; ++k)
+        if (cs + k >= 0 && cs + k < n) Zb[static_cast<std::int64_t>(cs + k) * L] += Cb[static_cast<std::int64_t>(k) * L];
+    }
+  // forward substitution in place (Z -> y), U columns of Z in flight
+  double yw[P];
+#pragma unroll
+  for (int k = 0; k < P; ++k) yw[k] = 0.0;
+  double zn[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) zn[u] = (active && u < n) ? Zb[static_cast<std::int64_t>(u) * L] : 0.0;
+  for (int c0 = 0; c0 < n; c0 += U) {
+    double z[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      z[u] = zn[u];
+      const int cn = c0 + U + u;
+      zn[u] = (active && cn < n) ? Zb[static_cast<std::int64_t>(cn) * L] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int c = c0 + u;
+      if (c < n) {
+        const double* Lc = slt + c * LW;
+        double sacc = z[u];
+#pragma unroll
+        for (int k = P; k >= 1; --k) sacc = fma(-Lc[k], yw[k - 1], sacc);
+        const double y = sacc * Lc[0];
+        if (active) Zb[static_cast<std::int64_t>(c) * L] = y;
+#pragma unroll
+        for (int k = P - 1; k >= 1; --k) yw[k] = yw[k - 1];
+        yw[0] = y;
+      }
+    }
+  }
   // Is this line's lead index shared along any leading dim?
   bool lead_shared = false;
   {
@@ -478,41 +509,40 @@ __global__ void __launch_bounds__(256) k_fit_last_tma(const FitArgs a, const __g
     }
   }
   const unsigned char* sf_last = a.shared_flag + a.sflag_off[d] + pr.col_lo;
-  // Back substitution; x staged through smem (stage buffers are free now).
-  __syncthreads();
-  constexpr int XP = 33;
-  double* s_x = reinterpret_cast<double*>(sm_raw);
-  const int lane = tid & 31, warp = tid >> 5, nwarps = (blockDim.x + 31) >> 5;
-  double xw[P], Lb[P + 1];
+  // back substitution; x staged through smem for coalesced P rows
+  double* Pb = a.P + blk.poff + l0 * n;
+  double xw[P];
 #pragma unroll
   for (int k = 0; k < P; ++k) xw[k] = 0.0;
-  auto fetch_bwd = [&](int cc) {
-    const double* Lc = slt + cc * LW;  // cc >= -1
-    Lb[0] = Lc[0];
-#pragma unroll
-    for (int k = 1; k <= P; ++k) Lb[k] = Lc[P + k];
-  };
-  fetch_bwd(n - 1);
   unsigned long long lmax = 0ull;
   for (int chi = n - 1; chi >= 0; chi -= 32) {
     const int clo = chi - 31 > 0 ? chi - 31 : 0;
     const int cn = chi - clo + 1;
-    double ynext = active ? Yb[static_cast<std::int64_t>(chi) * L] : 0.0;
-    for (int cc = chi; cc >= clo; --cc) {
-      double sacc = ynext;
-      if (cc > clo && active) ynext = Yb[static_cast<std::int64_t>(cc - 1) * L];
+    for (int c1 = chi; c1 >= clo; c1 -= U) {
+      double y[U];
 #pragma unroll
-      for (int k = 1; k <= P; ++k) sacc = fma(-Lb[k], xw[k - 1], sacc);
-      const double x = sacc * Lb[0];
-      fetch_bwd(cc - 1);
+      for (int u = 0; u < U; ++u) {
+        const int c = c1 - u;
+        y[u] = (active && c >= clo) ? Zb[static_cast<std::int64_t>(c) * L] : 0.0;
+      }
 #pragma unroll
-      for (int k = P - 1; k >= 1; --k) xw[k] = xw[k - 1];
-      xw[0] = x;
-      s_x[tid * XP + (cc - clo)] = x;
-      if (active && !lead_shared && !sf_last[cc]) lmax = lmax > dbits_s(fabs(x)) ? lmax : dbits_s(fabs(x));
+      for (int u = 0; u < U; ++u) {
+        const int c = c1 - u;
+        if (c >= clo) {
+          const double* Lc = slt + c * LW;
+          double sacc = y[u];
+#pragma unroll
+          for (int k = P; k >= 1; --k) sacc = fma(-Lc[P + k], xw[k - 1], sacc);
+          const double x = sacc * Lc[0];
+#pragma unroll
+          for (int k = P - 1; k >= 1; --k) xw[k] = xw[k - 1];
+          xw[0] = x;
+          s_x[tid * XP + (c - clo)] = x;
+          if (active && !lead_shared && !sf_last[c]) lmax = lmax > dbits_s(fabs(x)) ? lmax : dbits_s(fabs(x));
+        }
+      }
     }
     __syncthreads();
-    // LT need not be a multiple of 32: stride (line, column) pairs over all threads
     for (int e = tid; e < nl * 32; e += blockDim.x) {
       const int li = e >> 5, cl = e & 31;
       if (cl < cn) Pb[static_cast<std::int64_t>(li) * n + clo + cl] = s_x[li * XP + cl];
@@ -520,6 +550,7 @@ __global__ void __launch_bounds__(256) k_fit_last_tma(const FitArgs a, const __g
     __syncthreads();
   }
   // block-wide max of lmax -> linf_int[b]
+  const int lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     const unsigned long long t2 = __shfl_xor_sync(kFullMask, lmax, o);
@@ -771,12 +802,17 @@ int dispatch_p(int p, Args&&... args) {
 
 template <int P>
 struct LastLaunch {
-  static int run(const FitArgs& a, const CUtensorMap& map, int LT, int lt_cap, cudaStream_t s) {
-    const size_t smem = static_cast<size_t>(kLastS) * last_stage_bytes(LT, P) + 128 + static_cast<size_t>(lt_cap) * 8;
-    cudaFuncSetAttribute(k_fit_last_tma<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    dim3 grid((a.max_lines_last + LT - 1) / LT, a.nblocks);
-    k_fit_last_tma<P><<<grid, LT, smem, s>>>(a, map, LT);
-    return 1;
+  static int run(const FitArgs& a, const CUtensorMap& map, int LT, int lt_cap, int kseg, cudaStream_t s) {
+    const size_t smem = static_cast<size_t>(kLastS) * last_stage_bytes(LT, P) + 128;
+    cudaFuncSetAttribute(k_last_contract_tma<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    dim3 grid((a.max_lines_last + LT - 1) / LT, a.nblocks, kseg);
+    k_last_contract_tma<P><<<grid, LT, smem, s>>>(a, map, LT);
+    constexpr int T2 = 64;
+    const size_t smem2 = static_cast<size_t>(T2) * 33 * 8 + static_cast<size_t>(lt_cap) * 8;
+    cudaFuncSetAttribute(k_last_solve<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem2));
+    dim3 grid2((a.max_lines_last + T2 - 1) / T2, a.nblocks);
+    k_last_solve<P><<<grid2, T2, smem2, s>>>(a);
+    return 2;
   }
 };
 
@@ -790,8 +826,9 @@ int debug_fail_line_tma() {
   return line;
 }
 
-int launch_fit_last_tma(int degree, const FitArgs& a, const CUtensorMap& map, int LT, int lt_cap, cudaStream_t s) {
-  return dispatch_p<LastLaunch>(degree, a, map, LT, lt_cap, s);
+int launch_fit_last_tma(int degree, const FitArgs& a, const CUtensorMap& map, int LT, int lt_cap, int kseg,
+                        cudaStream_t s) {
+  return dispatch_p<LastLaunch>(degree, a, map, LT, lt_cap, kseg, s);
 }
 
 int launch_fit_axis0_tma(int degree, const FitArgs& a, const CUtensorMap& map, const TmaGeom& g, int ntiles,

@@ -374,5 +374,7 @@ def test_tma_and_generic_paths_agree(ctx, monkeypatch):
     g_gen, _, _ = run_both(cfg, values)
     assert_solve_parity(g_tma, o)
     assert_solve_parity(g_gen, o)
-    # identical arithmetic order in both paths for the fit: bitwise-equal lattices
-    assert np.array_equal(g_tma.blocks[0].p, g_gen.blocks[0].p)
+    # the TMA last-axis pass sums row segments then adds their carries, the
+    # generic one sums rows in order: equal to rounding
+    for bt, bg in zip(g_tma.blocks, g_gen.blocks):
+        assert np.max(np.abs(bt.p - bg.p)) <= 1e-12 * max(1.0, np.max(np.abs(bg.p)))
