@@ -74,9 +74,11 @@ struct RegionDev {
   int pslot[kRegionMaxHolders * (kRegionMaxHolders - 1) / 2];  // final-jump slot per holder pair, -1 if none
 };
 
-// A CTA's slice [start, start + count) of one region's row-major box.
+// A CTA's slice [start, start + count) of one region's row-major box, with
+// the region's descriptor inlined (one dependent load per tile).
 struct TileDev {
-  int region, start, count, pad_;
+  RegionDev r;
+  int start, count;
 };
 
 // Device-side epoch loop state (the loop runs without host round trips).

@@ -451,8 +451,10 @@ struct Workload {
     tl->begin("basis_rows");
     int l = mfb::launch_basis_rows(p, ra, ctx->stream);
     tl->end();
-    mfb::CholArgs ca{d_probs.p, d_factor.p, static_cast<int>(factor_ids.size()), max_n_factor, g0.p, vals.p, ltab.p,
-                     ctx->d_status};
+    int max_m_factor = 0;
+    for (int id : factor_ids) max_m_factor = std::max(max_m_factor, probs[static_cast<std::size_t>(id)].m);
+    mfb::CholArgs ca{d_probs.p, d_factor.p, static_cast<int>(factor_ids.size()), max_n_factor, max_m_factor, 0, g0.p,
+                     vals.p, ltab.p, ctx->d_status};
     tl->begin("gram_chol");
     l += mfb::launch_gram_chol(p, ca, ctx->stream);
     tl->end();
@@ -641,7 +643,6 @@ struct mfadd_solver {
   std::string holder_fault;
   int max_holders = 1;
   // region-form epochs (max_holders <= 8): tables + the epoch-loop graph
-  DBuf<mfb::RegionDev> regions;
   DBuf<mfb::TileDev> tiles;
   int ntiles = 0;
   DBuf<mfb::EpochState> est;
@@ -781,7 +782,6 @@ double bits_to_double(unsigned long long u) {
 
 mfb::EpochRegionArgs region_args(mfadd_solver* s, int mode) {
   mfb::EpochRegionArgs a{};
-  a.regions = s->regions.p;
   a.tiles = s->tiles.p;
   a.ntiles = s->ntiles;
   a.nblocks = s->dec.nblocks;
@@ -804,7 +804,7 @@ mfb::EpochRegionArgs region_args(mfadd_solver* s, int mode) {
 // into tiles of at most kTile controls.  Holder h follows the reference's
 // ascending block-id order (last dim least significant).
 void build_regions(mfadd_solver* s, const std::vector<int>& pair_slot) {
-  constexpr int kTile = 512;  // kRegionThreads x 2 (one pass for n_s = 2, two for n_s >= 4)
+  constexpr int kTile = 1024;  // 256 threads x 4 controls (n_s = 2: one pass)
   const Decomp& d = s->dec;
   const int D = d.rank;
   struct Iv {
@@ -820,7 +820,6 @@ void build_regions(mfadd_solver* s, const std::vector<int>& pair_slot) {
       else
         iv[k].push_back({i, i + 1, r[0], r[1] - r[0] + 1});
     }
-  std::vector<mfb::RegionDev> regs;
   std::vector<mfb::TileDev> tls;
   std::size_t cnt[3] = {1, 1, 1};
   for (int k = 0; k < D; ++k) cnt[k] = iv[k].size();
@@ -870,14 +869,14 @@ void build_regions(mfadd_solver* s, const std::vector<int>& pair_slot) {
             }
             R.pslot[q] = pair_slot[static_cast<std::size_t>(R.ids[h1]) * 27 + code];
           }
-        const int total = R.ext[0] * R.ext[1] * R.ext[2];
-        for (int st0 = 0; st0 < total; st0 += kTile)
-          tls.push_back({static_cast<int>(regs.size()), st0, std::min(kTile, total - st0), 0});
-        regs.push_back(R);
+        const std::int64_t total64 = static_cast<std::int64_t>(R.ext[0]) * R.ext[1] * R.ext[2];
+        if (total64 >= (std::int64_t{1} << 24))  // fast_divmod range (kernels.cu)
+          throw std::invalid_argument("mfadd_b200: a shared-control region exceeds 2^24 controls");
+        const int total = static_cast<int>(total64);
+        for (int st0 = 0; st0 < total; st0 += kTile) tls.push_back({R, st0, std::min(kTile, total - st0)});
       }
   s->ntiles = static_cast<int>(tls.size());
   if (s->ntiles == 0) return;
-  s->regions.upload(regs, s->ctx->stream);
   s->tiles.upload(tls, s->ctx->stream);
 }
 
@@ -923,6 +922,10 @@ MFB_API int mfadd_solver_create(mfadd_context* ctx, const mfadd_decomposition* d
     if (p > mfb::kMaxDegree)
       throw std::invalid_argument("mfadd_b200: degree " + std::to_string(p) + " exceeds the compiled maximum " +
                                   std::to_string(mfb::kMaxDegree));
+    for (int k = 0; k < D; ++k)
+      if (d.blocks[k] > 256)
+        throw std::invalid_argument("mfadd_b200: at most 256 blocks per dimension are supported (dimension " +
+                                    std::to_string(k) + " has " + std::to_string(d.blocks[k]) + ")");
     Workload& wl = s->wl;
     wl.D = D;
     wl.p = p;

@@ -167,6 +167,15 @@ __global__ void __launch_bounds__(256) k_gram_chol(CholArgs a) {
   const int n = pr.n, m = pr.m;
   const int* g0 = a.g0 + pr.row_off;
   const double* v = a.vals + pr.row_off * (P + 1);
+  if (a.stage_rows) {  // row table -> smem (coalesced), then the Gram reads are smem hits
+    double* sv = sm + a.max_n * (P + 1);
+    int* sg = reinterpret_cast<int*>(sv + a.max_m * (P + 1));
+    for (int i = threadIdx.x; i < m * (P + 1); i += blockDim.x) sv[i] = v[i];
+    for (int i = threadIdx.x; i < m; i += blockDim.x) sg[i] = g0[i];
+    __syncthreads();
+    v = sv;
+    g0 = sg;
+  }
   // collocation.cpp:56-67: each entry accumulated over rows in row order
   for (int e = threadIdx.x; e < n * (P + 1); e += blockDim.x) {
     const int c = e / (P + 1), k = e - c * (P + 1);
@@ -190,14 +199,10 @@ __global__ void __launch_bounds__(256) k_gram_chol(CholArgs a) {
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    // Banded left-looking Cholesky with the last P rows of L held in a
-    // register window: Lw[r] = row (c-1-r), Lw[r][0] = 1/L(row,row),
-    // Lw[r][k] = L(row, row-k).  Row c is written back over sm[c*(P+1)..].
-    double Lw[P][P + 1];
-#pragma unroll
-    for (int r = 0; r < P; ++r)
-#pragma unroll
-      for (int k = 0; k <= P; ++k) Lw[r][k] = 0.0;
+    // Banded left-looking Cholesky (the Eigen LLT of lsq.cpp:46-49 restricted
+    // to the band: L has no fill outside it).  Row c is written back over
+    // sm[c*(P+1)..]: [1/L(c,c), L(c,c-1), .., L(c,c-P)]; rows c-1..c-P are
+    // read back from shared memory (loads independent of row c's chain).
     for (int c = 0; c < n; ++c) {
       double* Gc = sm + c * (P + 1);
       double Lc[P + 1];
@@ -209,10 +214,11 @@ __global__ void __launch_bounds__(256) k_gram_chol(CholArgs a) {
           Lc[k] = 0.0;
           continue;
         }
+        const double* Lj = sm + (c - k) * (P + 1);  // row j = c-k
         double sacc = Lc[k];
 #pragma unroll
-        for (int t = k + 1; t <= P; ++t) sacc = fma(-Lc[t], Lw[k - 1][t - k], sacc);
-        Lc[k] = sacc * Lw[k - 1][0];  // * 1/L(j,j), j = c-k
+        for (int t = k + 1; t <= P; ++t) sacc = fma(-Lc[t], Lj[t - k], sacc);  // L(c,c-t) L(j,c-t)
+        Lc[k] = sacc * Lj[0];                                                   // * 1/L(j,j)
       }
       double dg = Lc[0];
 #pragma unroll
@@ -221,15 +227,9 @@ __global__ void __launch_bounds__(256) k_gram_chol(CholArgs a) {
         set_status(a.status, 3, pid, c);
         dg = 1.0;
       }
-      Lc[0] = 1.0 / sqrt(dg);
+      Lc[0] = rsqrt(dg);
 #pragma unroll
       for (int k = 0; k <= P; ++k) Gc[k] = Lc[k];
-#pragma unroll
-      for (int r = P - 1; r >= 1; --r)
-#pragma unroll
-        for (int k = 0; k <= P; ++k) Lw[r][k] = Lw[r - 1][k];
-#pragma unroll
-      for (int k = 0; k <= P; ++k) Lw[0][k] = Lc[k];
     }
   }
   __syncthreads();
@@ -837,7 +837,6 @@ __global__ void __launch_bounds__(kEpochThreads) k_epoch8(EpochArgs a) {
 // across the CTA: one atomic per holder per CTA instead of per control.
 constexpr int kRegionThreads = 256;
 constexpr int kRegionWarps = kRegionThreads / 32;
-constexpr int kRegionPerThread = 2;  // controls per thread per tile (n_s == 2: loads issued together)
 
 __device__ __forceinline__ double warp_dmax(double v) {
 #pragma unroll
@@ -867,13 +866,28 @@ struct RegionRegs {
   int s0, s1, s2;
 };
 
+// q = n / d, r = n % d for 0 <= n < 2^24, 1 <= d: fp32 reciprocal estimate
+// (off by at most one) plus one correction step, instead of the ~20-instruction
+// integer division by a run-time divisor.
+__device__ __forceinline__ void fast_divmod(int n, int d, float rcp, int& q, int& r) {
+  q = __float2int_rz(__int2float_rz(n) * rcp);
+  r = n - q * d;
+  if (r < 0) {
+    --q;
+    r += d;
+  } else if (r >= d) {
+    ++q;
+    r -= d;
+  }
+}
+
 // R is the CTA's shared-memory copy of the region descriptor.  PT controls
 // per thread per pass (PT loads per holder in flight); the n_s = 8 form keeps
 // offsets in shared memory to stay within the register budget.
 template <int NS>
 __device__ __forceinline__ void region_tile(const EpochRegionArgs& a, const RegionDev& R, const TileDev& t, int mode,
                                             double (*s_w)[kRegionWarps]) {
-  constexpr int PT = NS == 2 ? kRegionPerThread : 1;
+  constexpr int PT = NS == 2 ? 4 : (NS == 4 ? 2 : 1);  // controls per thread per pass: 8 loads in flight
   const bool update = mode == 2 || (mode == 1 && NS == 2);
   RegionRegs hr[NS <= 4 ? NS : 1];
 #pragma unroll
@@ -883,6 +897,7 @@ __device__ __forceinline__ void region_tile(const EpochRegionArgs& a, const Regi
     return R.base[h] + static_cast<long long>(r0) * R.str[h][0] + r1 * R.str[h][1] + r2 * R.str[h][2];
   };
   const int e1 = R.ext[1], e2 = R.ext[2];
+  const float rc1 = 1.0f / static_cast<float>(e1), rc2 = 1.0f / static_cast<float>(e2);
   // update: red[h] = change of holder h, red[NS] = max |avg| (every copy);
   // measure: red[h] = max |copy of holder h|, red[NS] = jump
   double red[NS + 1];
@@ -895,8 +910,9 @@ __device__ __forceinline__ void region_tile(const EpochRegionArgs& a, const Regi
 #pragma unroll
     for (int u = 0; u < PT; ++u) {
       const int i = i0 + u * kRegionThreads;
-      const int r2 = i % e2, q = i / e2;
-      const int r1 = q % e1, r0 = q / e1;
+      int q, r2, r0, r1;
+      fast_divmod(i, e2, rc2, q, r2);
+      fast_divmod(q, e1, rc1, r0, r1);
 #pragma unroll
       for (int h = 0; h < NS; ++h) {
         off[u][h] = offset(h, r0, r1, r2);
@@ -910,7 +926,7 @@ __device__ __forceinline__ void region_tile(const EpochRegionArgs& a, const Regi
         double sum = 0.0;  // solver.cpp:147-159: ascending holder id, divide once
 #pragma unroll
         for (int h = 0; h < NS; ++h) sum = __dadd_rn(sum, v[u][h]);
-        const double avg = __ddiv_rn(sum, static_cast<double>(NS));
+        const double avg = sum * (1.0 / NS);  // NS is a power of two: bitwise equal to sum / NS
 #pragma unroll
         for (int h = 0; h < NS; ++h) {
           red[h] = fmax(red[h], fabs(avg - v[u][h]));
@@ -941,7 +957,7 @@ __device__ __forceinline__ void region_tile(const EpochRegionArgs& a, const Regi
       atomicMax(NS == 2 ? &a.st->jump_ss : &a.st->jump_ms, b);
     }
   }
-  __syncthreads();  // s_w and s_R are reused by the next tile
+  __syncthreads();  // s_w and the tile descriptor are reused by the next tile
 }
 
 // MAXNS = 4 for 1-D/2-D decompositions (tighter register budget, 3 CTAs/SM),
@@ -951,22 +967,26 @@ __global__ void __launch_bounds__(kRegionThreads, MAXNS == 8 ? 2 : 3) k_epoch_re
   __shared__ double s_w[2 * kRegionMaxHolders + 1][kRegionWarps];
   __shared__ unsigned long long s_red[32];
   __shared__ int s_last;
-  __shared__ RegionDev s_R;
+  __shared__ TileDev s_T;
+  constexpr int kWords = static_cast<int>(sizeof(TileDev) / 4);
+  static_assert(kWords <= kRegionThreads, "one descriptor word per thread");
   const int iter = a.mode < 0 ? a.st->iter + 1 : 0;
   const int mode = a.mode < 0 ? (iter >= 2 ? 2 : 1) : a.mode;  // solver.cpp:397
+  // persistent CTAs: the next tile's descriptor is fetched while this one runs
+  const int tid = threadIdx.x;
+  int w = 0;
+  if (tid < kWords && static_cast<int>(blockIdx.x) < a.ntiles)
+    w = __ldg(reinterpret_cast<const int*>(a.tiles + blockIdx.x) + tid);
   for (int tb = blockIdx.x; tb < a.ntiles; tb += gridDim.x) {
-    const TileDev t = a.tiles[tb];
-    {
-      const int* src = reinterpret_cast<const int*>(a.regions + t.region);
-      int* dst = reinterpret_cast<int*>(&s_R);
-      for (int w = threadIdx.x; w < static_cast<int>(sizeof(RegionDev) / 4); w += blockDim.x) dst[w] = src[w];
-    }
+    if (tid < kWords) reinterpret_cast<int*>(&s_T)[tid] = w;
     __syncthreads();
-    const RegionDev& R = s_R;
-    switch (R.ns) {
-      case 2: region_tile<2>(a, R, t, mode, s_w); break;
-      case 4: region_tile<4>(a, R, t, mode, s_w); break;
-      default: region_tile<MAXNS>(a, R, t, mode, s_w); break;
+    const int tn = tb + gridDim.x;
+    if (tid < kWords && tn < a.ntiles) w = __ldg(reinterpret_cast<const int*>(a.tiles + tn) + tid);
+    const TileDev& t = s_T;
+    switch (t.r.ns) {
+      case 2: region_tile<2>(a, t.r, t, mode, s_w); break;
+      case 4: region_tile<4>(a, t.r, t, mode, s_w); break;
+      default: region_tile<MAXNS>(a, t.r, t, mode, s_w); break;
     }
   }
   // last CTA: dp = max_b change_b / max(1, ||P_b||_inf) (solver.cpp:398-405)
@@ -1047,12 +1067,11 @@ __global__ void __launch_bounds__(kRegionThreads) k_pair_jumps_regions(EpochRegi
   __shared__ double s_w[2 * kRegionMaxHolders + 1][kRegionWarps];
   if (a.st->last_iter >= 2) return;  // after a mode-2 epoch all copies agree bitwise
   for (int tb = blockIdx.x; tb < a.ntiles; tb += gridDim.x) {
-    const TileDev t = a.tiles[tb];
-    const RegionDev& R = a.regions[t.region];
-    switch (R.ns) {
-      case 2: region_pairs<2>(a, R, t, s_w); break;
-      case 4: region_pairs<4>(a, R, t, s_w); break;
-      default: region_pairs<8>(a, R, t, s_w); break;
+    const TileDev& t = a.tiles[tb];
+    switch (t.r.ns) {
+      case 2: region_pairs<2>(a, t.r, t, s_w); break;
+      case 4: region_pairs<4>(a, t.r, t, s_w); break;
+      default: region_pairs<8>(a, t.r, t, s_w); break;
     }
   }
 }
@@ -1089,25 +1108,47 @@ __global__ void __launch_bounds__(1024) k_dp(DpArgs a) {
 }
 
 // ------------------------------------------------------------------- K6
+// One CTA per lattice row (all dims but the last): the lead-dim owner
+// coordinates and local indices are CTA-uniform; the last dim's owner table and
+// per-owner window origins sit in shared memory.
+constexpr int kAsmMaxLast = 4096;  // last-dim extent handled by the smem owner table
+constexpr int kAsmMaxB = 256;
+
 __global__ void __launch_bounds__(256) k_assemble(AssembleArgs a) {
-  std::int64_t total = 1;
-  for (int k = 0; k < a.D; ++k) total *= a.N[k];
-  const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
-  for (std::int64_t g = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < total; g += stride) {
-    std::int64_t r = g, idx[3] = {0, 0, 0};
-    for (int k = a.D - 1; k >= 0; --k) {
-      idx[k] = r % a.N[k];
-      r /= a.N[k];
-    }
-    int id = 0;
+  __shared__ short s_own[kAsmMaxLast];
+  __shared__ long long s_base[kAsmMaxB];  // P offset of the row in block (lead, c) minus col_lo
+  const int D = a.D, dl = D - 1;
+  const int Nl = static_cast<int>(a.N[dl]), Bl = a.B[dl];
+  const bool own_smem = Nl <= kAsmMaxLast;
+  if (own_smem)
+    for (int i = threadIdx.x; i < Nl; i += blockDim.x) s_own[i] = static_cast<short>(a.own_coord[a.oc_off[dl] + i]);
+  // lead coordinates of this row
+  std::int64_t row = blockIdx.x;
+  int cl[3] = {0, 0, 0};
+  std::int64_t il[3] = {0, 0, 0};
+  for (int k = dl - 1; k >= 0; --k) {
+    il[k] = row % a.N[k];
+    row /= a.N[k];
+    cl[k] = a.own_coord[a.oc_off[k] + il[k]];
+  }
+  int lead_id = 0;
+  for (int k = 0; k < dl; ++k) lead_id = lead_id * a.B[k] + cl[k];
+  for (int c = threadIdx.x; c < Bl; c += blockDim.x) {
+    const int id = lead_id * Bl + c;
+    // local row index within block id: row-major over the lead dims, then x n_last
     std::int64_t o = 0;
-    for (int k = 0; k < a.D; ++k) {
-      const int c = a.own_coord[a.oc_off[k] + idx[k]];
-      id = id * a.B[k] + c;
-      const AxisProb& pk = a.probs[a.axbase[k] + c];
-      o = o * pk.n + (idx[k] - pk.col_lo);
+    for (int k = 0; k < dl; ++k) {
+      const AxisProb& pk = a.probs[a.axbase[k] + cl[k]];
+      o = o * pk.n + (il[k] - pk.col_lo);
     }
-    a.lattice[g] = a.P[a.poff[id] + o];
+    const AxisProb& pl = a.probs[a.axbase[dl] + c];
+    s_base[c] = a.poff[id] + o * pl.n - pl.col_lo;
+  }
+  __syncthreads();
+  double* out = a.lattice + static_cast<std::int64_t>(blockIdx.x) * Nl;
+  for (int i = threadIdx.x; i < Nl; i += blockDim.x) {
+    const int c = own_smem ? s_own[i] : a.own_coord[a.oc_off[dl] + i];
+    out[i] = a.P[s_base[c] + i];
   }
 }
 
@@ -1273,9 +1314,13 @@ template <int P>
 struct CholLaunch {
   static int run(const CholArgs& a, cudaStream_t s) {
     if (a.nfactor == 0) return 0;
-    const size_t smem = static_cast<size_t>(a.max_n) * (P + 1) * sizeof(double);
+    CholArgs b = a;
+    size_t smem = static_cast<size_t>(a.max_n) * (P + 1) * sizeof(double);
+    const size_t staged = smem + static_cast<size_t>(a.max_m) * ((P + 1) * sizeof(double) + sizeof(int));
+    b.stage_rows = staged <= 200 * 1024;
+    if (b.stage_rows) smem = staged;
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_gram_chol<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    k_gram_chol<P><<<a.nfactor, 256, smem, s>>>(a);
+    k_gram_chol<P><<<a.nfactor, 256, smem, s>>>(b);
     return 1;
   }
 };
@@ -1364,10 +1409,20 @@ int launch_epoch_regions(const EpochRegionArgs& a, cudaStream_t s) {
   if (a.ntiles <= 0) return 0;
   if (a.mode == 3)
     k_pair_jumps_regions<<<a.ntiles, kRegionThreads, 0, s>>>(a);
-  else if (a.max_ns > 4)
-    k_epoch_regions<8><<<a.ntiles, kRegionThreads, 0, s>>>(a);
-  else
-    k_epoch_regions<4><<<a.ntiles, kRegionThreads, 0, s>>>(a);
+  else {
+    static int sms = 0;
+    if (!sms) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int per_sm = a.max_ns > 4 ? 2 : 3;  // __launch_bounds__ residency
+    const int grid = a.ntiles < sms * per_sm ? a.ntiles : sms * per_sm;
+    if (a.max_ns > 4)
+      k_epoch_regions<8><<<grid, kRegionThreads, 0, s>>>(a);
+    else
+      k_epoch_regions<4><<<grid, kRegionThreads, 0, s>>>(a);
+  }
   return 1;
 }
 
@@ -1377,14 +1432,10 @@ int launch_dp(const DpArgs& a, cudaStream_t s) {
 }
 
 int launch_assemble(const AssembleArgs& a, cudaStream_t s) {
-  std::int64_t total = 1;
-  for (int k = 0; k < a.D; ++k) total *= a.N[k];
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  std::int64_t want = (total + 255) / 256;
-  const std::int64_t cap = static_cast<std::int64_t>(sms) * 8;
-  k_assemble<<<static_cast<unsigned>(want < cap ? want : cap), 256, 0, s>>>(a);
+  std::int64_t rows = 1;
+  for (int k = 0; k + 1 < a.D; ++k) rows *= a.N[k];
+  if (a.B[a.D - 1] > kAsmMaxB) return -1;  // host validates blocks_per_dim first
+  k_assemble<<<static_cast<unsigned>(rows), 256, 0, s>>>(a);
   return 1;
 }
 

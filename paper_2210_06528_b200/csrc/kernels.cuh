@@ -37,6 +37,8 @@ struct CholArgs {
   const int* prob_ids;  // problems to factor
   int nfactor;
   int max_n;
+  int max_m;      // rows of the largest factored problem
+  int stage_rows; // 1: the row table is staged in shared memory
   const int* g0;
   const double* vals;
   double* ltab;
@@ -109,7 +111,6 @@ int launch_epoch(const EpochArgs& a, cudaStream_t s);
 // and offsets are CTA-uniform.  The last CTA to finish computes dp (K5 fused)
 // and, inside the epoch-loop graph, sets the WHILE condition.
 struct EpochRegionArgs {
-  const RegionDev* regions;
   const TileDev* tiles;
   int ntiles;
   int nblocks;
