@@ -38,7 +38,7 @@ struct BlockDev {
   std::int64_t poff;   // offset of the held lattice P_b
   std::int64_t t1off;  // axis-0 intermediate   [n0][m1][m2]
   std::int64_t t2off;  // axis-1 intermediate   [n0][n1][m2]
-  std::int64_t coff;   // last-axis segment carries [K-1][P+1][lines]
+  std::int64_t zoff;   // last-axis contraction buffer: [n + 2(P+1)][lines] per parity half
 };
 
 // Last-axis row segments (k_last_contract_tma): per axis problem

@@ -279,8 +279,7 @@ struct Workload {
   int last_LT = 128, last_ltcap = 0, last_kseg = 1;
   std::vector<int> segtab;  // kSegStride ints per axis problem (last-axis problems filled)
   DBuf<int> d_segtab;
-  DBuf<double> carry;
-  std::int64_t total_carry = 0;
+  std::int64_t zhalf = 0;  // one parity half of the last-axis contraction buffer
   std::array<std::int64_t, 3> field_dims{1, 1, 1};  // global field extents (solver) for the tensor map
 
   void plan_tma(bool enable) {
@@ -353,13 +352,12 @@ struct Workload {
         t[1 + sgi] = sgi == K ? pr.m : std::min(pr.m, (static_cast<int>(static_cast<std::int64_t>(pr.m) * sgi / K) + 8) / 16 * 16);
       last_kseg = std::max(last_kseg, K);
     }
-    total_carry = 0;
+    zhalf = 0;
     for (auto& b : blocks) {
       std::int64_t Ll = 1;
       for (int k = 0; k + 1 < D; ++k) Ll *= probs[static_cast<std::size_t>(b.ax[k])].n;
-      const int K = segtab[static_cast<std::size_t>(b.ax[D - 1]) * mfb::kSegStride];
-      b.coff = total_carry;
-      total_carry += static_cast<std::int64_t>(K - 1) * (p + 1) * Ll;
+      b.zoff = zhalf;
+      zhalf += (probs[static_cast<std::size_t>(b.ax[D - 1])].n + 2 * (p + 1)) * Ll;
     }
   }
 
@@ -433,12 +431,9 @@ struct Workload {
     t1.alloc(static_cast<std::size_t>(total_t1));
     t2.alloc(static_cast<std::size_t>(total_t2));
     P.alloc(static_cast<std::size_t>(total_p));
-    Y.alloc(static_cast<std::size_t>(total_p));
+    Y.alloc(static_cast<std::size_t>(tma_last ? 2 * zhalf + total_p : total_p));
     linf_int.alloc(blocks.size());
-    if (tma_last) {
-      d_segtab.upload(segtab, s);
-      carry.alloc(static_cast<std::size_t>(std::max<std::int64_t>(total_carry, 1)));
-    }
+    if (tma_last) d_segtab.upload(segtab, s);
   }
 
   // K1 + K2
@@ -491,7 +486,7 @@ struct Workload {
     fa.max_lines_last = max_lines_last;
     fa.pitch_last = pitch_last;
     fa.segtab = d_segtab.p;
-    fa.carry = carry.p;
+    fa.zhalf = zhalf;
     fa.n_field = field_n;
     fa.n_t1 = total_t1;
     fa.n_t2 = total_t2;

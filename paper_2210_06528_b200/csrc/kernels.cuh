@@ -70,7 +70,7 @@ struct FitArgs {
   std::int64_t pitch_last;           // row pitch (even) of the last-axis input (T1 for D=2, T2 for D=3)
   std::int64_t n_field, n_t1, n_t2, n_P;  // buffer sizes (debug bounds checks)
   const int* segtab;                 // last-axis row segments per axis problem (kSegStride ints)
-  double* carry;                     // last-axis segment carries (BlockDev::coff)
+  std::int64_t zhalf;                // last-axis contraction: Y = [parity 0 | parity 1 | y scratch]
 };
 int launch_fit_strided(int degree, const FitArgs& a, int axis, cudaStream_t s);  // axis < D-1
 int launch_fit_last(int degree, const FitArgs& a, cudaStream_t s);

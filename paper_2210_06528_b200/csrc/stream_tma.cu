@@ -322,7 +322,7 @@ template <int P>
 __global__ void __launch_bounds__(256) k_last_contract_tma(const FitArgs a, const __grid_constant__ CUtensorMap map,
                                                            const int LT) {
   extern __shared__ __align__(1024) unsigned char sm_raw[];
-  constexpr int S = kLastS, CW = kLastCW;
+  constexpr int S = kLastS, CW = kLastCW, PADC = P + 1;
   const int D = a.D, d = D - 1;
   const int b = blockIdx.y, sgi = blockIdx.z;
   const BlockDev& blk = a.blocks[b];  // by reference: ax[] is indexed at run time
@@ -331,7 +331,6 @@ __global__ void __launch_bounds__(256) k_last_contract_tma(const FitArgs a, cons
   const int K = seg[0];
   if (sgi >= K) return;
   const AxisProb pr = a.probs[pid];
-  const int n = pr.n;
   std::int64_t L = 1;
   for (int k = 0; k < d; ++k) L *= a.probs[blk.ax[k]].n;
   const std::int64_t l0 = static_cast<std::int64_t>(blockIdx.x) * LT;
@@ -341,10 +340,7 @@ __global__ void __launch_bounds__(256) k_last_contract_tma(const FitArgs a, cons
   const int js = seg[1 + sgi], je = seg[2 + sgi];
   const int* g0g = a.g0 + pr.row_off;
   const double* vg = a.vals + pr.row_off * (P + 1);
-  const int cs_next = sgi + 1 < K ? __ldg(g0g + je) : 0x7fffffff;  // first column of the next segment
   const int row0 = static_cast<int>((D == 2 ? blk.t1off : blk.t2off) / a.pitch_last + l0);
-  double* Zb = a.Y + blk.poff + l0 + tid;                                        // Z[c*L + l]
-  double* Cb = a.carry + blk.coff + static_cast<std::int64_t>(sgi) * (P + 1) * L + l0 + tid;  // carry[s][k][l]
 
   const int SB = last_stage_bytes(LT, P);
   const int v_off = LT * 128, g_off = v_off + CW * (P + 1) * 8;
@@ -368,72 +364,81 @@ __global__ void __launch_bounds__(256) k_last_contract_tma(const FitArgs a, cons
   }
   __syncthreads();
 
-  // sliding window: acc[k] accumulates column cbase + k
+  // Column-ordered accumulation with static register slots: columns are
+  // visited in groups of P+1 (slot u = column mod P+1, the unrolled loop
+  // index), and before column c is flushed the run of rows whose span starts
+  // at c (g0 == c) is accumulated into slots (u + k) mod (P+1).  All register
+  // indices are compile-time constants.  Columns go to this segment's parity
+  // buffer at padded index c + P + 1 (a store through an incrementing pointer).
   double acc[P + 1];
 #pragma unroll
   for (int k = 0; k <= P; ++k) acc[k] = 0.0;
   int cbase = __ldg(g0g + js);
   if (sgi == 0 && cbase > 0) cbase = 0;
-#define MFB_LAST_FLUSH()                                                       \
-  do {                                                                         \
-    const int cc = cbase;                                                      \
-    if (cc >= 0 && cc < n && active) {                                        \
-      if (cc >= cs_next)                                                       \
-        Cb[static_cast<std::int64_t>(cc - cs_next) * L] = acc[0];              \
-      else                                                                     \
-        Zb[static_cast<std::int64_t>(cc) * L] = acc[0];                        \
-    }                                                                          \
-    _Pragma("unroll") for (int k = 0; k < P; ++k) acc[k] = acc[k + 1];         \
-    acc[P] = 0.0;                                                              \
-    ++cbase;                                                                   \
-  } while (0)
+  double* zp = a.Y + (sgi & 1) * a.zhalf + blk.zoff + static_cast<std::int64_t>(cbase + PADC) * L + l0 + tid;
+  const int cend = sgi + 1 < K ? __ldg(g0g + je) + P + 1 : pr.n;
   const int swz = tid & 7;
-  for (int c = 0; c < nchunks; ++c) {
+  // row cursor over the TMA stages: chunk c, local row jl in [.., jhi)
+  int c = 0, jl = 0, jhi = 0, gnext = 0x7fffffff;
+  const unsigned char* lineb = nullptr;
+  const int* sg = nullptr;
+  const double* sv = nullptr;
+  auto open_chunk = [&]() {
     const int st = c % S;
     const unsigned char* base = sm_raw + st * SB;
-    const int* sg = reinterpret_cast<const int*>(base + g_off);
-    const double* sv = reinterpret_cast<const double*>(base + v_off);
-    const double2* line = reinterpret_cast<const double2*>(base + tid * 128);
+    sg = reinterpret_cast<const int*>(base + g_off);
+    sv = reinterpret_cast<const double*>(base + v_off);
+    lineb = base + tid * 128;
     const int jb = (c_first + c) * CW;
-    const int jlo = (js > jb ? js : jb) - jb, jhi = (je < jb + CW ? je : jb + CW) - jb;
+    jl = (js > jb ? js : jb) - jb;
+    jhi = (je < jb + CW ? je : jb + CW) - jb;
     mbar_wait(&bars[st], (c / S) & 1);
-#pragma unroll
-    for (int kk = 0; kk < CW / 2; ++kk) {
-      const double2 q2 = line[kk ^ swz];
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int jj = 2 * kk + e;
-        if (jj >= jlo && jj < jhi) {  // CTA-uniform
-          const int g = sg[jj];
-          while (cbase < g) MFB_LAST_FLUSH();
-          const double q = e ? q2.y : q2.x;
-          const double* vr = sv + jj * (P + 1);
-#pragma unroll
-          for (int k = 0; k <= P; ++k) acc[k] = fma(vr[k], q, acc[k]);
-        }
-      }
+    gnext = sg[jl];
+  };
+  auto advance = [&]() {
+    if (++jl < jhi) {
+      gnext = sg[jl];
+      return;
     }
-    __syncthreads();
+    __syncthreads();  // every line is done with chunk c: refill its stage
     if (tid == 0 && c + S < nchunks) {
       fence_proxy_async();
       issue(c + S);
     }
+    if (++c < nchunks)
+      open_chunk();
+    else
+      gnext = 0x7fffffff;
+  };
+  if (nchunks > 0) open_chunk();
+  while (cbase < cend) {
+#pragma unroll
+    for (int u = 0; u <= P; ++u) {
+      while (gnext == cbase) {  // CTA-uniform
+        const double q = *reinterpret_cast<const double*>(lineb + ((((jl >> 1) ^ swz) << 4) | ((jl & 1) << 3)));
+        const double* vr = sv + jl * (P + 1);
+#pragma unroll
+        for (int k = 0; k <= P; ++k) acc[(u + k) % (P + 1)] = fma(vr[k], q, acc[(u + k) % (P + 1)]);
+        advance();
+      }
+      if (active) *zp = acc[u];
+      zp += L;
+      acc[u] = 0.0;
+      if (++cbase >= cend) break;
+    }
   }
-  // complete the segment's columns: up to the end of the line, or through the
-  // carry range cs_next .. cs_next+P of the next segment
-  const int cend = sgi + 1 < K ? cs_next + P + 1 : n;
-  while (cbase < cend) MFB_LAST_FLUSH();
-#undef MFB_LAST_FLUSH
 }
 
 template <int P>
 __global__ void __launch_bounds__(128) k_last_solve(const FitArgs a) {
   extern __shared__ __align__(1024) unsigned char sm_raw[];
   __shared__ unsigned long long s_red[32];
-  constexpr int LW = 2 * P + 1, XP = 33, U = 8;
+  constexpr int LW = 2 * P + 1, XP = 33, PADC = P + 1;
+  constexpr int U = P * ((8 + P - 1) / P);  // batch of columns, a multiple of P (static window slots)
+  constexpr int F = (P + 2) & ~1;  // coefficients per column, padded to 16 B
   const int D = a.D, d = D - 1;
   const int b = blockIdx.y;
-  const BlockDev& blk = a.blocks[b];  // by reference: ax[] is indexed at run time
+  const BlockDev& blk = a.blocks[b];
   const int pid = blk.ax[d];
   const AxisProb pr = a.probs[pid];
   const int n = pr.n;
@@ -444,62 +449,35 @@ __global__ void __launch_bounds__(128) k_last_solve(const FitArgs a) {
   const int nl = static_cast<int>((L - l0) < blockDim.x ? (L - l0) : blockDim.x);
   const int tid = threadIdx.x;
   const bool active = tid < nl;
-  double* s_x = reinterpret_cast<double*>(sm_raw);                 // blockDim x XP staging
-  double* s_lt = s_x + blockDim.x * XP;                            // (n + 2(P+1)) x LW, zero padded
+  // smem: x staging | fwd coefficients | bwd coefficients | column codes | line flags
+  double* s_x = reinterpret_cast<double*>(sm_raw);
+  double* s_f = s_x + blockDim.x * XP;          // (n + 1) x F: [1/L(c,c), L(c,c-1) .. L(c,c-P)]
+  double* s_b = s_f + (n + 1) * F;              // (n + 1) x F: [1/L(c,c), L(c+1,c) .. L(c+P,c)]
+  unsigned char* s_code = reinterpret_cast<unsigned char*>(s_b + (n + 1) * F);  // n: owner parity | 2*(carry)
+  unsigned char* s_sf = s_code + n;             // n: column shared along the last dim
+  unsigned char* s_lead = s_sf + n;             // blockDim: line's lead index shared
   const double* lt = a.ltab + pr.col_off * LW;
-  for (int i = tid; i < (n + 2 * (P + 1)) * LW; i += blockDim.x) {
-    const int cc = i / LW - (P + 1);
-    s_lt[i] = (cc >= 0 && cc < n) ? __ldg(lt + static_cast<std::int64_t>(cc) * LW + (i - (i / LW) * LW)) : 0.0;
+  for (int i = tid; i < n * F; i += blockDim.x) {
+    const int c = i / F, k = i - c * F;
+    const double* Lc = lt + static_cast<std::int64_t>(c) * LW;
+    s_f[i] = k == 0 ? Lc[0] : (k <= P ? Lc[k] : 0.0);
+    s_b[i] = k == 0 ? Lc[0] : (k <= P ? Lc[P + k] : 0.0);
   }
-  const double* slt = s_lt + (P + 1) * LW;
-  __syncthreads();
-  double* Zb = a.Y + blk.poff + l0 + tid;
-  // add the segment carries (k_last_contract_tma) into Z
   const int* seg = a.segtab + pid * kSegStride;
   const int K = seg[0];
   const int* g0g = a.g0 + pr.row_off;
-  if (active)
-    for (int s2 = 0; s2 + 1 < K; ++s2) {
-      const int cs = __ldg(g0g + seg[2 + s2]);
-      const double* Cb = a.carry + blk.coff + static_cast<std::int64_t>(s2) * (P + 1) * L + l0 + tid;
-#pragma unroll
-      for (int k = 0; k <= P; ++k)
-        if (cs + k >= 0 && cs + k < n) Zb[static_cast<std::int64_t>(cs + k) * L] += Cb[static_cast<std::int64_t>(k) * L];
+  for (int c = tid; c < n; c += blockDim.x) {
+    int own = 0, carry = 0;
+    for (int s2 = 1; s2 < K; ++s2) {
+      const int cs = __ldg(g0g + seg[1 + s2]);
+      if (c >= cs) own = s2;
+      if (c >= cs && c <= cs + P) carry = 1;
     }
-  // forward substitution in place (Z -> y), U columns of Z in flight
-  double yw[P];
-#pragma unroll
-  for (int k = 0; k < P; ++k) yw[k] = 0.0;
-  double zn[U];
-#pragma unroll
-  for (int u = 0; u < U; ++u) zn[u] = (active && u < n) ? Zb[static_cast<std::int64_t>(u) * L] : 0.0;
-  for (int c0 = 0; c0 < n; c0 += U) {
-    double z[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      z[u] = zn[u];
-      const int cn = c0 + U + u;
-      zn[u] = (active && cn < n) ? Zb[static_cast<std::int64_t>(cn) * L] : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int c = c0 + u;
-      if (c < n) {
-        const double* Lc = slt + c * LW;
-        double sacc = z[u];
-#pragma unroll
-        for (int k = P; k >= 1; --k) sacc = fma(-Lc[k], yw[k - 1], sacc);
-        const double y = sacc * Lc[0];
-        if (active) Zb[static_cast<std::int64_t>(c) * L] = y;
-#pragma unroll
-        for (int k = P - 1; k >= 1; --k) yw[k] = yw[k - 1];
-        yw[0] = y;
-      }
-    }
+    s_code[c] = static_cast<unsigned char>((own & 1) | (carry << 1));
+    s_sf[c] = a.shared_flag[a.sflag_off[d] + pr.col_lo + c];
   }
-  // Is this line's lead index shared along any leading dim?
-  bool lead_shared = false;
   {
+    bool lead_shared = false;
     std::int64_t r = l0 + tid;
     for (int k = d - 1; k >= 0; --k) {
       const AxisProb pk = a.probs[blk.ax[k]];
@@ -507,45 +485,115 @@ __global__ void __launch_bounds__(128) k_last_solve(const FitArgs a) {
       r /= pk.n;
       if (active && a.shared_flag[a.sflag_off[k] + pk.col_lo + ik]) lead_shared = true;
     }
+    s_lead[tid] = lead_shared ? 1 : 0;
   }
-  const unsigned char* sf_last = a.shared_flag + a.sflag_off[d] + pr.col_lo;
+  __syncthreads();
+  // the two parity buffers of this line, padded column 0
+  const std::int64_t zbase = blk.zoff + static_cast<std::int64_t>(PADC) * L + l0 + tid;
+  const double* z0 = a.Y + zbase;
+  const double* z1 = a.Y + a.zhalf + zbase;
+  double* yb = a.Y + a.zhalf * 2 + blk.poff + l0 + tid;  // y scratch Y2[c*L + l]
+  auto zload = [&](int c) -> double {
+    if (!active || c >= n) return 0.0;
+    const unsigned code = s_code[c];
+    const std::int64_t o = static_cast<std::int64_t>(c) * L;
+    double z = (code & 1) ? z1[o] : z0[o];
+    if (code & 2) z += (code & 1) ? z0[o] : z1[o];  // carry of the previous segment
+    return z;
+  };
+  // forward substitution, U columns of Z in flight.  U is a multiple of P, so
+  // y_{c-k} lives in the static slot (c - k) mod P of yw (no window moves).
+  double yw[P];
+#pragma unroll
+  for (int k = 0; k < P; ++k) yw[k] = 0.0;
+  double zn[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) zn[u] = zload(u);
+  double* yp = yb;
+  for (int c0 = 0; c0 < n; c0 += U) {
+    double z[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      z[u] = zn[u];
+      zn[u] = zload(c0 + U + u);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int c = c0 + u;
+      if (c < n) {
+        const double2* Lc = reinterpret_cast<const double2*>(s_f + c * F);
+        double cf[F];
+#pragma unroll
+        for (int h = 0; h < F / 2; ++h) {
+          const double2 t = Lc[h];
+          cf[2 * h] = t.x;
+          cf[2 * h + 1] = t.y;
+        }
+        double sacc = z[u];
+#pragma unroll
+        for (int k = P; k >= 1; --k) sacc = fma(-cf[k], yw[(u - k + U) % P], sacc);
+        const double y = sacc * cf[0];
+        if (active) *yp = y;
+        yp += L;
+        yw[u % P] = y;
+      }
+    }
+  }
   // back substitution; x staged through smem for coalesced P rows
   double* Pb = a.P + blk.poff + l0 * n;
+  // back substitution from the last column down, U columns per batch (x_{c+k}
+  // in static slot (n - 1 - c - k) mod P counted from the top); x staged
+  // through smem in 32-column chunks for coalesced P rows.
   double xw[P];
 #pragma unroll
   for (int k = 0; k < P; ++k) xw[k] = 0.0;
   unsigned long long lmax = 0ull;
-  for (int chi = n - 1; chi >= 0; chi -= 32) {
-    const int clo = chi - 31 > 0 ? chi - 31 : 0;
-    const int cn = chi - clo + 1;
-    for (int c1 = chi; c1 >= clo; c1 -= U) {
+  const double* ybp = yb + static_cast<std::int64_t>(n - 1) * L;  // y of column n-1-t at ybp - t*L
+  double yn[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) yn[u] = (active && u < n) ? *(ybp - static_cast<std::int64_t>(u) * L) : 0.0;
+  constexpr int XC = 32 / U * U;  // columns per staging chunk (multiple of U)
+  for (int t0 = 0; t0 < n; t0 += XC) {  // t = n - 1 - c counts columns from the top
+    for (int t1 = t0; t1 < t0 + XC && t1 < n; t1 += U) {
       double y[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int c = c1 - u;
-        y[u] = (active && c >= clo) ? Zb[static_cast<std::int64_t>(c) * L] : 0.0;
+        y[u] = yn[u];
+        const int tn = t1 + U + u;
+        yn[u] = (active && tn < n) ? *(ybp - static_cast<std::int64_t>(tn) * L) : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int c = c1 - u;
-        if (c >= clo) {
-          const double* Lc = slt + c * LW;
+        const int t = t1 + u, c = n - 1 - t;
+        if (t < n) {
+          const double2* Lc = reinterpret_cast<const double2*>(s_b + c * F);
+          double cf[F];
+#pragma unroll
+          for (int h = 0; h < F / 2; ++h) {
+            const double2 v2 = Lc[h];
+            cf[2 * h] = v2.x;
+            cf[2 * h + 1] = v2.y;
+          }
           double sacc = y[u];
 #pragma unroll
-          for (int k = P; k >= 1; --k) sacc = fma(-Lc[P + k], xw[k - 1], sacc);
-          const double x = sacc * Lc[0];
-#pragma unroll
-          for (int k = P - 1; k >= 1; --k) xw[k] = xw[k - 1];
-          xw[0] = x;
-          s_x[tid * XP + (c - clo)] = x;
-          if (active && !lead_shared && !sf_last[c]) lmax = lmax > dbits_s(fabs(x)) ? lmax : dbits_s(fabs(x));
+          for (int k = P; k >= 1; --k) sacc = fma(-cf[k], xw[(u - k + U) % P], sacc);
+          const double x = sacc * cf[0];
+          xw[u % P] = x;
+          s_x[tid * XP + (t - t0)] = x;
         }
       }
     }
+    const int cn = (n - t0) < XC ? (n - t0) : XC;  // columns c = n-1-t0 down to n-t0-cn
+    const int clo = n - t0 - cn;
     __syncthreads();
+    // coalesced P rows; L-inf over non-shared controls (dp denominator)
     for (int e = tid; e < nl * 32; e += blockDim.x) {
       const int li = e >> 5, cl = e & 31;
-      if (cl < cn) Pb[static_cast<std::int64_t>(li) * n + clo + cl] = s_x[li * XP + cl];
+      if (cl < cn) {  // column clo + cl was staged at t - t0 = cn - 1 - cl
+        const double x = s_x[li * XP + (cn - 1 - cl)];
+        Pb[static_cast<std::int64_t>(li) * n + clo + cl] = x;
+        if (!s_lead[li] && !s_sf[clo + cl]) lmax = lmax > dbits_s(fabs(x)) ? lmax : dbits_s(fabs(x));
+      }
     }
     __syncthreads();
   }
@@ -807,8 +855,10 @@ struct LastLaunch {
     cudaFuncSetAttribute(k_last_contract_tma<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     dim3 grid((a.max_lines_last + LT - 1) / LT, a.nblocks, kseg);
     k_last_contract_tma<P><<<grid, LT, smem, s>>>(a, map, LT);
-    constexpr int T2 = 64;
-    const size_t smem2 = static_cast<size_t>(T2) * 33 * 8 + static_cast<size_t>(lt_cap) * 8;
+    constexpr int T2 = 64, F = (P + 2) & ~1;
+    const int nmax = lt_cap / (2 * P + 1);  // max last-axis n (+ padding) from the L-table capacity
+    const size_t smem2 = static_cast<size_t>(T2) * 33 * 8 + 2 * static_cast<size_t>(nmax + 1) * F * 8 +
+                         2 * static_cast<size_t>(nmax) + T2;
     cudaFuncSetAttribute(k_last_solve<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem2));
     dim3 grid2((a.max_lines_last + T2 - 1) / T2, a.nblocks);
     k_last_solve<P><<<grid2, T2, smem2, s>>>(a);
