@@ -643,6 +643,15 @@ struct mfadd_solver {
   DBuf<mfb::EpochState> est;
   cudaGraph_t loop_graph = nullptr;
   cudaGraphExec_t loop_exec = nullptr;
+  // whole-solve graph (profiling off), keyed by the field pointer
+  cudaGraphExec_t solve_exec = nullptr;
+  cudaStream_t aux_stream = nullptr;  // captures conditional-node bodies
+  const double* solve_field = nullptr;
+  const double* direct_field = nullptr;
+  int solve_launches = 0;
+  // pinned result block: red2[2] | DevStatus | epoch_out | EpochState | pair_jumps
+  double* hres = nullptr;
+  std::size_t hres_eo = 0, hres_es = 0, hres_pj = 0, hres_n = 0;
 
   // results
   std::vector<mfadd_epoch_stats> epochs;
@@ -654,10 +663,14 @@ struct mfadd_solver {
   cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
 
   ~mfadd_solver() {
-    for (auto& e : ev)
-      if (e) cudaEventDestroy(e);
+    // graphs first: the solve graph holds event-record nodes on ev[]
+    if (solve_exec) cudaGraphExecDestroy(solve_exec);
     if (loop_exec) cudaGraphExecDestroy(loop_exec);
     if (loop_graph) cudaGraphDestroy(loop_graph);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    if (aux_stream) cudaStreamDestroy(aux_stream);
+    if (hres) cudaFreeHost(hres);
   }
 };
 
@@ -890,15 +903,40 @@ void build_loop_graph(mfadd_solver* s) {
   cudaGraphNode_t node;
   CK(cudaGraphAddNode(&node, s->loop_graph, nullptr, 0, &np));
   cudaGraph_t body = np.conditional.phGraph_out[0];
-  cudaStream_t cs;
-  CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  cudaStream_t cs = s->aux_stream;
   CK(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
   mfb::EpochRegionArgs a = region_args(s, -1);
   a.cond = static_cast<unsigned long long>(h);
   mfb::launch_epoch_regions(a, cs);
   CK(cudaStreamEndCapture(cs, &body));
-  CK(cudaStreamDestroy(cs));
   CK(cudaGraphInstantiate(&s->loop_exec, s->loop_graph, 0));
+}
+
+// The epoch loop as a conditional WHILE node appended to the graph being
+// captured on `st` (whole-solve graph).
+void add_loop_node(mfadd_solver* s, cudaStream_t st) {
+  cudaStreamCaptureStatus cs;
+  cudaGraph_t g = nullptr;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  CK(cudaStreamGetCaptureInfo(st, &cs, nullptr, &g, &deps, &ndeps));
+  cudaGraphConditionalHandle h;
+  CK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams np = {};
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = h;
+  np.conditional.type = cudaGraphCondTypeWhile;
+  np.conditional.size = 1;
+  cudaGraphNode_t node;
+  CK(cudaGraphAddNode(&node, g, deps, ndeps, &np));
+  cudaGraph_t body = np.conditional.phGraph_out[0];
+  cudaStream_t bs = s->aux_stream;
+  CK(cudaStreamBeginCaptureToGraph(bs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  mfb::EpochRegionArgs a = region_args(s, -1);
+  a.cond = static_cast<unsigned long long>(h);
+  mfb::launch_epoch_regions(a, bs);
+  CK(cudaStreamEndCapture(bs, &body));
+  CK(cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies));
 }
 
 }  // namespace
@@ -1146,7 +1184,13 @@ MFB_API int mfadd_solver_create(mfadd_context* ctx, const mfadd_decomposition* d
     CK(cudaMemsetAsync(s->linf_sh.p, 0, s->linf_sh.n * sizeof(unsigned long long), st));
     CK(cudaMemsetAsync(s->acc.p, 0, sizeof(mfb::EpochAcc), st));
     CK(cudaMemsetAsync(s->est.p, 0, sizeof(mfb::EpochState), st));
+    CK(cudaStreamCreateWithFlags(&s->aux_stream, cudaStreamNonBlocking));
     if (s->ntiles > 0 && cfg->enforce_continuity) build_loop_graph(s.get());
+    s->hres_eo = 4;
+    s->hres_es = s->hres_eo + s->epoch_out.n;
+    s->hres_pj = s->hres_es + (sizeof(mfb::EpochState) + 7) / 8;
+    s->hres_n = s->hres_pj + s->pair_jumps.n;
+    CK(cudaMallocHost(&s->hres, s->hres_n * sizeof(double)));
     CK(cudaStreamSynchronize(st));
     *out = s.release();
   });
@@ -1159,6 +1203,7 @@ MFB_API void mfadd_solver_free(mfadd_solver* s) {
   cudaSetDevice(s->ctx->device);
   cudaStreamSynchronize(s->ctx->stream);
   delete s;
+  (void)cudaGetLastError();  // teardown errors must not surface in a later call
   if (prev >= 0) cudaSetDevice(prev);
 }
 
@@ -1218,15 +1263,17 @@ float ev_ms(cudaEvent_t a, cudaEvent_t b) {
   return ms;
 }
 
-void solve_impl(mfadd_solver* s, const double* dfield) {
+// Issue every device operation of one solve on the context stream (kernels,
+// the epoch-loop conditional node, result copies into pinned memory); no
+// host synchronisation, so the sequence can be captured into a graph.
+int enqueue_solve(mfadd_solver* s, const double* dfield) {
   mfadd_context* ctx = s->ctx;
   cudaStream_t st = ctx->stream;
   const Decomp& d = s->dec;
   Workload& wl = s->wl;
   int launches = 0;
-  s->have_result = false;
-  s->epochs.clear();
   s->tl.st = st;
+  (void)cudaGetLastError();  // report only this solve's launch errors
   CK(cudaEventRecord(s->ev[0], st));
   // ---- setup: basis rows + Gram/Cholesky (solver.cpp:346 make_block_state)
   launches += wl.setup(ctx, &s->tl);
@@ -1254,7 +1301,12 @@ void solve_impl(mfadd_solver* s, const double* dfield) {
   // ---- outer iterations (solver.cpp:394-413), entirely on the device
   if (loop) {
     s->tl.begin("epoch");
-    CK(cudaGraphLaunch(s->loop_exec, st));
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CK(cudaStreamIsCapturing(st, &cs));
+    if (cs == cudaStreamCaptureStatusActive)
+      add_loop_node(s, st);
+    else
+      CK(cudaGraphLaunch(s->loop_exec, st));
     s->tl.end();
   }
   CK(cudaEventRecord(s->ev[3], st));
@@ -1357,29 +1409,41 @@ void solve_impl(mfadd_solver* s, const double* dfield) {
   launches += mfb::launch_reduce_partials(s->partial.p, nparts, s->red2.p, st);
   s->tl.end();
   CK(cudaGetLastError());
-  double* hp = ctx->h_pinned;
-  CK(cudaMemcpyAsync(hp + 4, s->red2.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
-  std::vector<double> eo(s->epoch_out.n);
-  CK(cudaMemcpyAsync(eo.data(), s->epoch_out.p, eo.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
-  mfb::EpochState es{};
-  CK(cudaMemcpyAsync(&es, s->est.p, sizeof es, cudaMemcpyDeviceToHost, st));
-  mfb::DevStatus stt{};
-  CK(cudaMemcpyAsync(&stt, ctx->d_status, sizeof stt, cudaMemcpyDeviceToHost, st));
-  std::vector<unsigned long long> pj(s->pair_jumps.n);
+  double* hr = s->hres;
+  CK(cudaMemcpyAsync(hr, s->red2.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(hr + 2, ctx->d_status, sizeof(mfb::DevStatus), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(hr + s->hres_eo, s->epoch_out.p, s->epoch_out.n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(hr + s->hres_es, s->est.p, sizeof(mfb::EpochState), cudaMemcpyDeviceToHost, st));
   if (s->npairs > 0)
-    CK(cudaMemcpyAsync(pj.data(), s->pair_jumps.p, pj.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                       st));
+    CK(cudaMemcpyAsync(hr + s->hres_pj, s->pair_jumps.p, s->pair_jumps.n * sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, st));
   CK(cudaEventRecord(s->ev[4], st));
+  return launches;
+}
+
+// Wait for an enqueued solve and unpack its results (the only host sync).
+void finish_solve(mfadd_solver* s, int launches) {
+  mfadd_context* ctx = s->ctx;
+  cudaStream_t st = ctx->stream;
+  const Decomp& d = s->dec;
   CK(cudaStreamSynchronize(st));
+  const double* hr = s->hres;
+  mfb::DevStatus stt{};
+  std::memcpy(&stt, hr + 2, sizeof stt);
   if (stt.code) {
     CK(cudaMemsetAsync(ctx->d_status, 0, sizeof(mfb::DevStatus), st));
-    wl.raise_status(stt, "");
+    CK(cudaStreamSynchronize(st));
+    s->wl.raise_status(stt, "");
   }
+  const double* eo = hr + s->hres_eo;
+  mfb::EpochState es{};
+  std::memcpy(&es, hr + s->hres_es, sizeof es);
+  s->epochs.clear();
   mfadd_solve_summary& sum = s->summary;
   sum = mfadd_solve_summary{};
   s->epochs.push_back({0, 0.0, eo[1], eo[2]});
   sum.converged = 1;
-  if (loop) {
+  if (s->cfg.enforce_continuity && d.any_shared) {
     const int last = es.iter;
     for (int it = 1; it <= last; ++it)
       s->epochs.push_back({it, eo[3 * it], eo[3 * it + 1], eo[3 * it + 2]});
@@ -1388,8 +1452,9 @@ void solve_impl(mfadd_solver* s, const double* dfield) {
     sum.constraint_iterations = es.converged ? last - 1 : last;  // solver.cpp:406-412
     launches += last;  // one epoch kernel per loop iteration
   }
-  sum.global_l2 = std::sqrt(hp[4]);
-  sum.global_linf = hp[5];
+  sum.global_l2 = std::sqrt(hr[0]);
+  sum.global_linf = hr[1];
+  const auto* pj = reinterpret_cast<const unsigned long long*>(hr + s->hres_pj);
   s->final_jumps.assign(static_cast<std::size_t>(s->npairs) * 4, 0.0);
   for (int i = 0; i < s->npairs; ++i) {
     s->final_jumps[4 * static_cast<std::size_t>(i)] = s->pair_ids[static_cast<std::size_t>(i)][0];
@@ -1407,6 +1472,49 @@ void solve_impl(mfadd_solver* s, const double* dfield) {
   s->last_launches = launches;
   ctx->launches += launches;
   s->have_result = true;
+}
+
+// solve(): replay the cached whole-solve graph when possible (no per-kernel
+// profiling, no debug sync checks, no holder fault), else launch directly.
+void solve_impl(mfadd_solver* s, const double* dfield) {
+  s->have_result = false;
+  const bool graphable = !s->tl.on && !s->tl.sync_check && s->holder_fault.empty() && !std::getenv("MFADD_NO_GRAPH");
+  if (!graphable) {
+    finish_solve(s, enqueue_solve(s, dfield));
+    return;
+  }
+  cudaStream_t st = s->ctx->stream;
+  if (!s->solve_exec || s->solve_field != dfield) {
+    if (s->solve_exec) {
+      CK(cudaGraphExecDestroy(s->solve_exec));
+      s->solve_exec = nullptr;
+    }
+    if (s->direct_field != dfield) {
+      // first solve on this field pointer: direct launches (also performs every
+      // one-time function attribute setup outside of capture)
+      s->direct_field = dfield;
+      finish_solve(s, enqueue_solve(s, dfield));
+      return;
+    }
+    cudaGraph_t g = nullptr;
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+    int launches = 0;
+    try {
+      launches = enqueue_solve(s, dfield);
+    } catch (...) {
+      cudaStreamEndCapture(st, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    CK(cudaStreamEndCapture(st, &g));
+    const cudaError_t e = cudaGraphInstantiate(&s->solve_exec, g, 0);
+    cudaGraphDestroy(g);
+    CK(e);
+    s->solve_field = dfield;
+    s->solve_launches = launches;
+  }
+  CK(cudaGraphLaunch(s->solve_exec, st));
+  finish_solve(s, s->solve_launches);
 }
 
 }  // namespace

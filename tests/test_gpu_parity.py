@@ -378,3 +378,25 @@ def test_tma_and_generic_paths_agree(ctx, monkeypatch):
     # generic one sums rows in order: equal to rounding
     for bt, bg in zip(g_tma.blocks, g_gen.blocks):
         assert np.max(np.abs(bt.p - bg.p)) <= 1e-12 * max(1.0, np.max(np.abs(bg.p)))
+
+
+def test_graph_replay_matches_direct(ctx, monkeypatch):
+    """The first solve on a field pointer runs direct launches, the second
+    captures the whole solve into a CUDA graph, later ones replay it: all must
+    be bitwise identical (and identical to the never-graphed path)."""
+    cfg = SMALL["C2"]
+    values = W.make_field_numpy(cfg)
+    dec = m.partition(cfg.grid, cfg.bounds, cfg.blocks, cfg.degree, cfg.nctrl, cfg.overlap)
+    s = m.Solver(dec, m.SolverConfig(max_outer_iterations=20, log_errors=False))
+    res = []
+    for _ in range(4):
+        s.run(values.reshape(-1))
+        res.append(s.result())
+    monkeypatch.setenv("MFADD_NO_GRAPH", "1")
+    s.run(values.reshape(-1))
+    res.append(s.result())
+    for r in res[1:]:
+        assert np.array_equal(r.model.controls, res[0].model.controls)
+        assert np.array_equal(r.global_error, res[0].global_error)
+        assert [e.dp_max for e in r.epochs] == [e.dp_max for e in res[0].epochs]
+        assert r.global_l2 == res[0].global_l2 and r.constraint_iterations == res[0].constraint_iterations
