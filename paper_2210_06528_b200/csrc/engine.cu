@@ -247,6 +247,11 @@ struct Timeline {
   }
 };
 
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+
 // Device tables for a batch of local problems sharing one degree: the fit
 // machinery of both solve() and fit_unconstrained().
 struct Workload {
@@ -306,7 +311,7 @@ struct Workload {
       axis0_tiles = (mx1 + axis0_geo.B1 - 1) / axis0_geo.B1;
     }
     axis0_geo.R = 8;
-    axis0_geo.S = 4;
+    axis0_geo.S = env_int("MFADD_FIT_S", 4);
     int mxn = 0;
     for (const auto& b : blocks) mxn = std::max(mxn, probs[static_cast<std::size_t>(b.ax[0])].n);
     const int need = (mxn + 2 * (p + 1)) * (2 * p + 1);  // padded Cholesky table in smem
@@ -1162,7 +1167,7 @@ MFB_API int mfadd_solver_create(mfadd_context* ctx, const mfadd_decomposition* d
       s->dgeo.B2 = round_up((inner + nt - 1) / nt, 2);
       s->dgeo.B1 = D == 2 ? 1 : std::max(1, 256 / s->dgeo.B2);
       s->dgeo.R = 8;
-      s->dgeo.S = 4;
+      s->dgeo.S = env_int("MFADD_DEC_S", 3);
       s->dnt2 = (inner + s->dgeo.B2 - 1) / s->dgeo.B2;
       s->dnt1 = D == 2 ? 1 : (M1 + s->dgeo.B1 - 1) / s->dgeo.B1;
       int sms = 148;

@@ -72,12 +72,11 @@ __host__ __device__ inline StageLayout stage_layout(int R, int nthr, int P) {
 
 // ---------------------------------------------------------------- fit axis 0
 constexpr int kFitR = 8;  // rows per TMA stage (fit axis 0)
-constexpr int kFitS = 4;  // stages
 
-template <int P>
+template <int P, int S>
 __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __grid_constant__ CUtensorMap map,
                                                        const TmaGeom geo) {
-  constexpr int R = kFitR, S = kFitS;
+  constexpr int R = kFitR;
   extern __shared__ __align__(1024) unsigned char sm_raw[];
   const int b = blockIdx.y;
   const BlockDev blk = a.blocks[b];
@@ -164,97 +163,77 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
   for (int k = 0; k < P; ++k) yw[k] = 0.0;
   int cbase = __ldg(g0g) < 0 ? __ldg(g0g) : 0;
   const std::int64_t dstr = D == 2 ? a.pitch_last : Tr;  // T1 row stride
-  // Sliding window without register rotation: slot (ph + k) % (P+1) holds
-  // column cbase + k.  `ph` is warp-uniform, so the two switch statements
-  // below pick fully static register indices (no per-row window moves).
-  int ph = 0;
-  double Lnx[P + 1];  // forward coefficients of column cbase, fetched one flush ahead
+  // Column-ordered accumulation with static register slots (as in
+  // k_last_contract_tma): columns are visited in groups of P+1, slot u = the
+  // unrolled loop index; before column c is completed, the run of rows whose
+  // span starts at c is accumulated into slots (u + k) mod (P+1).  Completing
+  // a column is one step of forward substitution (y window shifted).
+  double Lnx[P + 1];  // forward coefficients of column cbase, fetched one column ahead
   auto fetch_fwd = [&](int cc) {
     const double* Lc = slt + (cc < -(P + 1) ? -(P + 1) : cc) * LW;
 #pragma unroll
     for (int k = 0; k <= P; ++k) Lnx[k] = Lc[k];
   };
   fetch_fwd(cbase);
-  // Complete column cbase (slot PH): forward substitution, then recycle the
-  // slot for column cbase + P + 1.
-  auto flush_slot = [&](auto phc) {
-    constexpr int PH = decltype(phc)::value;
-    const int cc = cbase;
-    if (cc >= 0 && cc < n) {
-      double sacc = acc[PH];
-#pragma unroll
-      for (int k = 1; k <= P; ++k) sacc = fma(-Lnx[k], yw[k - 1], sacc);
-      const double y = sacc * Lnx[0];
-      if (active) dst[static_cast<std::int64_t>(cc) * dstr] = y;
-#pragma unroll
-      for (int k = P - 1; k >= 1; --k) yw[k] = yw[k - 1];
-      yw[0] = y;
-    }
-    acc[PH] = 0.0;
-    ++cbase;
-    fetch_fwd(cbase);
-  };
-  auto flush = [&]() {
-    switch (ph) {
-      case 0: flush_slot(Int<0>{}); break;
-      case 1: flush_slot(Int<1 % (P + 1)>{}); break;
-      case 2: flush_slot(Int<2 % (P + 1)>{}); break;
-      case 3: flush_slot(Int<3 % (P + 1)>{}); break;
-      case 4: flush_slot(Int<4 % (P + 1)>{}); break;
-      case 5: flush_slot(Int<5 % (P + 1)>{}); break;
-      case 6: flush_slot(Int<6 % (P + 1)>{}); break;
-      case 7: flush_slot(Int<7 % (P + 1)>{}); break;
-      case 8: flush_slot(Int<8 % (P + 1)>{}); break;
-      default: flush_slot(Int<9 % (P + 1)>{}); break;
-    }
-    ph = ph == P ? 0 : ph + 1;
-  };
-  // Accumulate the run of rows [jj, jn) that share span g (static slots).
-  auto run_rows = [&](auto phc, const double* sq, const double* sv, const int* sg, int& jj, int jn, int g) {
-    constexpr int PH = decltype(phc)::value;
-    do {
-      const double q = sq[jj * nthr];
-      const double* vr = sv + jj * (P + 1);
-#pragma unroll
-      for (int k = 0; k <= P; ++k) acc[(PH + k) % (P + 1)] = fma(vr[k], q, acc[(PH + k) % (P + 1)]);
-      ++jj;
-    } while (jj < jn && sg[jj] == g);
-  };
-  auto run_dyn = [&](const double* sq, const double* sv, const int* sg, int& jj, int jn, int g) {
-    switch (ph) {
-      case 0: run_rows(Int<0>{}, sq, sv, sg, jj, jn, g); break;
-      case 1: run_rows(Int<1 % (P + 1)>{}, sq, sv, sg, jj, jn, g); break;
-      case 2: run_rows(Int<2 % (P + 1)>{}, sq, sv, sg, jj, jn, g); break;
-      case 3: run_rows(Int<3 % (P + 1)>{}, sq, sv, sg, jj, jn, g); break;
-      case 4: run_rows(Int<4 % (P + 1)>{}, sq, sv, sg, jj, jn, g); break;
-      case 5: run_rows(Int<5 % (P + 1)>{}, sq, sv, sg, jj, jn, g); break;
-      case 6: run_rows(Int<6 % (P + 1)>{}, sq, sv, sg, jj, jn, g); break;
-      case 7: run_rows(Int<7 % (P + 1)>{}, sq, sv, sg, jj, jn, g); break;
-      case 8: run_rows(Int<8 % (P + 1)>{}, sq, sv, sg, jj, jn, g); break;
-      default: run_rows(Int<9 % (P + 1)>{}, sq, sv, sg, jj, jn, g); break;
-    }
-  };
-
-  for (int c = 0; c < nchunks; ++c) {
+  double* yp = dst + static_cast<std::int64_t>(cbase) * dstr;
+  // row cursor over the TMA stages
+  int c = 0, jl = 0, jn = 0, gnext = 0x7fffffff;
+  const double* sq = nullptr;
+  const double* sv = nullptr;
+  const int* sg = nullptr;
+  auto open_chunk = [&]() {
     const int st = c % S;
     const unsigned char* base = sm_raw + st * SL.stage_bytes;
-    const double* sq = reinterpret_cast<const double*>(base) + tid;
-    const double* sv = reinterpret_cast<const double*>(base + SL.v_off);
-    const int* sg = reinterpret_cast<const int*>(base + SL.g_off);
+    sq = reinterpret_cast<const double*>(base) + tid;
+    sv = reinterpret_cast<const double*>(base + SL.v_off);
+    sg = reinterpret_cast<const int*>(base + SL.g_off);
+    jn = (m - c * R) < R ? (m - c * R) : R;
+    jl = 0;
     mbar_wait(&bars[st], (c / S) & 1);
-    const int jn = (m - c * R) < R ? (m - c * R) : R;
-    for (int jj = 0; jj < jn;) {
-      const int g = sg[jj];
-      while (cbase < g) flush();
-      run_dyn(sq, sv, sg, jj, jn, g);
+    gnext = sg[0];
+  };
+  auto advance = [&]() {
+    if (++jl < jn) {
+      gnext = sg[jl];
+      return;
     }
-    __syncthreads();
+    __syncthreads();  // every column is done with chunk c: refill its stage
     if (tid == 0 && c + S < nchunks) {
       fence_proxy_async();
       issue(c + S);
     }
+    if (++c < nchunks)
+      open_chunk();
+    else
+      gnext = 0x7fffffff;
+  };
+  if (nchunks > 0) open_chunk();
+  while (cbase < n) {
+#pragma unroll
+    for (int u = 0; u <= P; ++u) {
+      while (gnext == cbase) {  // CTA-uniform
+        const double q = sq[jl * nthr];
+        const double* vr = sv + jl * (P + 1);
+#pragma unroll
+        for (int k = 0; k <= P; ++k) acc[(u + k) % (P + 1)] = fma(vr[k], q, acc[(u + k) % (P + 1)]);
+        advance();
+      }
+      if (cbase >= 0) {  // forward substitution of column cbase (< n)
+        double sacc = acc[u];
+#pragma unroll
+        for (int k = 1; k <= P; ++k) sacc = fma(-Lnx[k], yw[k - 1], sacc);
+        const double y = sacc * Lnx[0];
+        if (active) *yp = y;
+#pragma unroll
+        for (int k = P - 1; k >= 1; --k) yw[k] = yw[k - 1];
+        yw[0] = y;
+      }
+      yp += dstr;
+      acc[u] = 0.0;
+      fetch_fwd(++cbase);
+      if (cbase >= n) break;
+    }
   }
-  while (cbase < n) flush();
   // Back substitution in place, y values prefetched 8 columns ahead.
   if (!active) return;
   constexpr int PF = 16;
@@ -614,12 +593,12 @@ __global__ void __launch_bounds__(128) k_last_solve(const FitArgs a) {
 }
 
 // ---------------------------------------------------------------- decode
-template <int P, int D>
+template <int P, int D, int S>
 __global__ void __launch_bounds__(256) k_decode_tma(const DecodeSweepArgs a, const __grid_constant__ CUtensorMap map,
                                                     const TmaGeom geo) {
   extern __shared__ __align__(1024) unsigned char sm_raw[];
   __shared__ double s_red[64];
-  constexpr int R = kFitR, S = kFitS;  // same stage geometry as the fit pass
+  constexpr int R = kFitR;  // same row stages as the fit pass
   const int B1 = geo.B1, B2 = geo.B2;
   const int nthr = B1 * B2;
   const int tid = threadIdx.x;
@@ -805,29 +784,38 @@ __global__ void __launch_bounds__(256) k_decode_tma(const DecodeSweepArgs a, con
 
 template <int P>
 struct Axis0Launch {
-  static int run(const FitArgs& a, const CUtensorMap& map, const TmaGeom& g, int ntiles, cudaStream_t s) {
+  template <int S>
+  static void go(const FitArgs& a, const CUtensorMap& map, const TmaGeom& g, int ntiles, cudaStream_t s) {
     const StageLayout SL = stage_layout(kFitR, g.B1 * g.B2, P);
-    const size_t smem = static_cast<size_t>(kFitS) * SL.stage_bytes + 128 + static_cast<size_t>(g.lt_cap) * 8;
-    cudaFuncSetAttribute(k_fit_axis0_tma<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    const size_t smem = static_cast<size_t>(S) * SL.stage_bytes + 128 + static_cast<size_t>(g.lt_cap) * 8;
+    cudaFuncSetAttribute(k_fit_axis0_tma<P, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     dim3 grid(ntiles, a.nblocks);
-    k_fit_axis0_tma<P><<<grid, g.B1 * g.B2, smem, s>>>(a, map, g);
+    k_fit_axis0_tma<P, S><<<grid, g.B1 * g.B2, smem, s>>>(a, map, g);
+  }
+  static int run(const FitArgs& a, const CUtensorMap& map, const TmaGeom& g, int ntiles, cudaStream_t s) {
+    if (g.S == 3)
+      go<3>(a, map, g, ntiles, s);
+    else
+      go<4>(a, map, g, ntiles, s);
     return 1;
   }
 };
 
 template <int P>
 struct DecodeSweepLaunch {
-  static int run(const DecodeSweepArgs& a, const CUtensorMap& map, const TmaGeom& g, cudaStream_t s) {
+  template <int D, int S>
+  static void go(const DecodeSweepArgs& a, const CUtensorMap& map, const TmaGeom& g, cudaStream_t s) {
     const StageLayout SL = stage_layout(kFitR, g.B1 * g.B2, P);
-    const size_t smem = static_cast<size_t>(kFitS) * SL.stage_bytes + kFitS * 8;
+    const size_t smem = static_cast<size_t>(S) * SL.stage_bytes + S * 8;
     dim3 grid(a.ntile1 * a.ntile2, a.nrange);
-    if (a.D == 2) {
-      cudaFuncSetAttribute(k_decode_tma<P, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      k_decode_tma<P, 2><<<grid, g.B1 * g.B2, smem, s>>>(a, map, g);
-    } else {
-      cudaFuncSetAttribute(k_decode_tma<P, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      k_decode_tma<P, 3><<<grid, g.B1 * g.B2, smem, s>>>(a, map, g);
-    }
+    cudaFuncSetAttribute(k_decode_tma<P, D, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k_decode_tma<P, D, S><<<grid, g.B1 * g.B2, smem, s>>>(a, map, g);
+  }
+  static int run(const DecodeSweepArgs& a, const CUtensorMap& map, const TmaGeom& g, cudaStream_t s) {
+    if (a.D == 2)
+      g.S == 3 ? go<2, 3>(a, map, g, s) : go<2, 4>(a, map, g, s);
+    else
+      g.S == 3 ? go<3, 3>(a, map, g, s) : go<3, 4>(a, map, g, s);
     return 1;
   }
 };
