@@ -681,8 +681,11 @@ __global__ void __launch_bounds__(256) k_decode_tma(const DecodeSweepArgs a, con
   if (tid == 0)
     for (int c = 0; c < S && c < nchunks; ++c) issue(c);
 
-  // control-plane window Tw[k] = plane(abase + k); the lattice values of the
-  // next plane (abase + P + 1) are loaded one shift ahead (L2 latency hidden).
+  // Control-plane window in static register slots: plane a lives in slot
+  // a mod (P+1).  Walking the planes in order (unrolled step u = slot of
+  // plane abase), the run of rows whose window starts at abase is decoded
+  // from slots (u + k) mod (P+1); advancing the window replaces slot u by
+  // plane abase + P + 1, whose lattice values were fetched one step ahead.
   int abase = __ldg(a.g0_0 + y0);
   double Tw[P + 1];
 #pragma unroll
@@ -721,41 +724,61 @@ __global__ void __launch_bounds__(256) k_decode_tma(const DecodeSweepArgs a, con
   };
   if (active) fetch_plane(abase + P + 1);
   double l2 = 0.0, li = 0.0;
-  for (int c = 0; c < nchunks; ++c) {
+  double* errp = a.err ? a.err + static_cast<std::int64_t>(y0) * Tr + t : nullptr;  // error of the current row
+  // row cursor over the TMA stages
+  int c = 0, jl = 0, jn = 0, gnext = 0x7fffffff;
+  const double* sq = nullptr;
+  const double* sv = nullptr;
+  const int* sg = nullptr;
+  auto open_chunk = [&]() {
     const int st = c % S;
     const unsigned char* base = sm_raw + st * SL.stage_bytes;
-    const double* sq = reinterpret_cast<const double*>(base);
-    const double* sv = reinterpret_cast<const double*>(base + SL.v_off);
-    const int* sg = reinterpret_cast<const int*>(base + SL.g_off);
-    mbar_wait(&bars[st], (c / S) & 1);
+    sq = reinterpret_cast<const double*>(base) + tid;
+    sv = reinterpret_cast<const double*>(base + SL.v_off);
+    sg = reinterpret_cast<const int*>(base + SL.g_off);
     const int yc = y0 + c * R;
-    const int jn = (y1 - yc) < R ? (y1 - yc) : R;
-    for (int jj = 0; jj < jn; ++jj) {
-      const int g = sg[jj];
-      while (abase < g) {
-#pragma unroll
-        for (int k = 0; k < P; ++k) Tw[k] = Tw[k + 1];
-        ++abase;
-        Tw[P] = active ? reduce_plane() : 0.0;
-        if (active) fetch_plane(abase + P + 1);
-      }
-      const double* vr = sv + jj * (P + 1);
-      double s = 0.0;
-#pragma unroll
-      for (int k = 0; k <= P; ++k) s = fma(vr[k], Tw[k], s);
-      if (active) {
-        const double q = sq[jj * nthr + tid];
-        const double e = q - s;
-        const std::int64_t gi = static_cast<std::int64_t>(yc + jj) * Tr + t;
-        if (a.err) a.err[gi] = e;
-        l2 = fma(e, e, l2);
-        li = fmax(li, fabs(e));
-      }
+    jn = (y1 - yc) < R ? (y1 - yc) : R;
+    jl = 0;
+    mbar_wait(&bars[st], (c / S) & 1);
+    gnext = sg[0];
+  };
+  auto advance = [&]() {
+    if (++jl < jn) {
+      gnext = sg[jl];
+      return;
     }
-    __syncthreads();
+    __syncthreads();  // every thread is done with chunk c: refill its stage
     if (tid == 0 && c + S < nchunks) {
       fence_proxy_async();
       issue(c + S);
+    }
+    if (++c < nchunks)
+      open_chunk();
+    else
+      gnext = 0x7fffffff;
+  };
+  if (nchunks > 0) open_chunk();
+  while (gnext != 0x7fffffff) {
+#pragma unroll
+    for (int u = 0; u <= P; ++u) {
+      while (gnext == abase) {  // CTA-uniform
+        const double* vr = sv + jl * (P + 1);
+        double sd = 0.0;
+#pragma unroll
+        for (int k = 0; k <= P; ++k) sd = fma(vr[k], Tw[(u + k) % (P + 1)], sd);
+        if (active) {
+          const double e = sq[jl * nthr] - sd;
+          if (errp) *errp = e;
+          l2 = fma(e, e, l2);
+          li = fmax(li, fabs(e));
+        }
+        if (errp) errp += Tr;
+        advance();
+      }
+      if (gnext == 0x7fffffff) break;
+      Tw[u] = active ? reduce_plane() : 0.0;  // plane abase + P + 1 replaces plane abase
+      ++abase;
+      if (active) fetch_plane(abase + P + 1);
     }
   }
   // CTA reduction -> partial[blockIdx]
