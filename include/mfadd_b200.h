@@ -144,6 +144,37 @@ int mfadd_solver_set_profiling(mfadd_solver* s, int on);
  * names: cap * name_len chars (nullable).  Returns the record count. */
 int mfadd_solver_kernel_times(const mfadd_solver* s, char* names, int name_len, double* ms, int cap);
 
+/* ------------------------------------------------------------- multi-GPU
+ * The path shards by blocks: rank r of n owns the block rows
+ * [r*B0/n, (r+1)*B0/n) along axis 0.  Each epoch exchanges the copies of the
+ * controls shared across ranks (ncclSend/ncclRecv with the adjacent ranks, the
+ * runtime.cpp:123-158 exchange) and max-reduces dp; the lattice rows are
+ * all-gathered and every rank decodes its own input rows.  Results equal the
+ * single-device solve (bitwise for the lattice). */
+typedef struct mfadd_comm mfadd_comm;
+/* ncclGetUniqueId on one rank; the 128 bytes are then broadcast by the caller. */
+int mfadd_nccl_unique_id(unsigned char* out128);
+int mfadd_comm_create(mfadd_context* ctx, const unsigned char* id128, int rank, int nranks, mfadd_comm** out);
+void mfadd_comm_free(mfadd_comm* comm);
+/* A solver for the calling rank's shard; mfadd_solve()/mfadd_solve_host() then
+ * take the full global field and run collectively on every rank. */
+int mfadd_solver_create_sharded(mfadd_context* ctx, const mfadd_decomposition* dec, const mfadd_solver_config* cfg,
+                                mfadd_comm* comm, mfadd_solver** out);
+/* Host-side shard plan: block ids [blo, bhi) and own input rows [in_lo, in_hi). */
+int mfadd_shard_range(const mfadd_decomposition* dec, int rank, int nranks, int* blo, int* bhi, int64_t* in_lo,
+                      int64_t* in_hi);
+/* Per-epoch exchange layout with one peer (recv=0: what `rank` sends, 1: what it
+ * receives): entries (holder block, i0, i1, i2) in buffer order.  Returns the
+ * entry count (out may be NULL), or -status on error. */
+int mfadd_shard_exchange(const mfadd_decomposition* dec, int rank, int nranks, int peer, int recv, int64_t* out,
+                         int64_t cap);
+/* All n ranks' shard solvers in one process on the context's device, driven in
+ * lockstep with device-to-device copies in place of NCCL (tests). */
+int mfadd_solve_loopback(mfadd_context* ctx, const mfadd_decomposition* dec, const mfadd_solver_config* cfg,
+                         int nranks, const double* field_host, double* out_controls, double* out_error,
+                         mfadd_solve_summary* out, mfadd_epoch_stats* epochs, int epochs_cap, double* final_jumps4,
+                         int jumps_cap);
+
 /* ---------------------------------------------------------- fine-grained
  * Unit-parity sub-boundaries.  All buffers are HOST memory;
  * the work runs on the context's GPU. */

@@ -8,6 +8,7 @@ from .api import (BandedCollocation, BlockDim, BlockLayout, BlockState, Context,
                   EpochStats, Field, InterfaceJump, InvalidArgument, KnotVector, LocalProblem, LogicError, MfaModel,
                   MfaddError, OutOfRange, PhaseTimings, RuntimeFault, SharedDofMap, SingularFitError, SolveResult,
                   Solver, SolverConfig, collocation_matrix, compression_ratio, decode, default_context, delta_width,
-                  exchange_volume, find_span, fit_unconstrained, make_knot_vector, partition, solve)
+                  exchange_volume, find_span, fit_unconstrained, make_knot_vector, partition, solve, Comm,
+                  shard_range, shard_exchange, solve_loopback)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -79,6 +79,16 @@ _SIGS = {
     "mfadd_fit_unconstrained": (C.c_int, [C.c_void_p, C.c_int, C.c_int, c_dp, c_lp, c_dp, c_lp, c_lp, c_lp, c_dp,
                                           c_dp]),
     "mfadd_decode": (C.c_int, [C.c_void_p, C.c_int, C.c_int, c_dp, c_lp, c_dp, c_lp, c_lp, c_lp, c_dp, c_dp]),
+    "mfadd_nccl_unique_id": (C.c_int, [C.c_void_p]),
+    "mfadd_comm_create": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "mfadd_comm_free": (None, [C.c_void_p]),
+    "mfadd_solver_create_sharded": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(SolverConfigC), C.c_void_p,
+                                              C.POINTER(C.c_void_p)]),
+    "mfadd_shard_range": (C.c_int, [C.c_void_p, C.c_int, C.c_int, c_ip, c_ip, c_lp, c_lp]),
+    "mfadd_shard_exchange": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, c_lp, C.c_int64]),
+    "mfadd_solve_loopback": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(SolverConfigC), C.c_int, C.c_void_p,
+                                       C.c_void_p, C.c_void_p, C.POINTER(SolveSummaryC), C.POINTER(EpochStatsC),
+                                       C.c_int, c_dp, C.c_int]),
 }
 
 # Symbols include/mfadd_b200.h declares (checked by the CPU test suite).

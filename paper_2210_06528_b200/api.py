@@ -568,16 +568,98 @@ class SolveResult:
     global_error: Optional[np.ndarray]
 
 
-class Solver:
-    """A solve() plan: the decomposition's device tables + work buffers."""
+class Comm:
+    """An NCCL communicator for sharded solves (one rank per GPU process)."""
 
-    def __init__(self, dec: Decomposition, config: SolverConfig = None, ctx: Optional[Context] = None):
+    def __init__(self, unique_id: bytes, rank: int, nranks: int, ctx: Optional["Context"] = None):
+        self.ctx = ctx or default_context()
+        self.rank, self.nranks = rank, nranks
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        h = C.c_void_p()
+        _check(L.load().mfadd_comm_create(self.ctx._h, buf, rank, nranks, C.byref(h)))
+        self._h = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(L.load().mfadd_nccl_unique_id(buf))
+        return buf.raw
+
+    def close(self):
+        if getattr(self, "_h", None):
+            L.load().mfadd_comm_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def shard_range(dec: "Decomposition", rank: int, nranks: int):
+    """(block_lo, block_hi, input_row_lo, input_row_hi) of `rank` (host-side plan)."""
+    blo, bhi, ilo, ihi = C.c_int(), C.c_int(), C.c_int64(), C.c_int64()
+    _check(L.load().mfadd_shard_range(dec._h, rank, nranks, C.byref(blo), C.byref(bhi), C.byref(ilo), C.byref(ihi)))
+    return blo.value, bhi.value, ilo.value, ihi.value
+
+
+def shard_exchange(dec: "Decomposition", rank: int, nranks: int, peer: int, recv: bool) -> np.ndarray:
+    """Per-epoch exchange layout of `rank` with `peer`: rows (holder block, i0, i1, i2) in buffer order."""
+    lib = L.load()
+    n = lib.mfadd_shard_exchange(dec._h, rank, nranks, peer, int(recv), None, 0)
+    if n < 0:
+        _check(-n)
+    out = np.zeros((n, 4), np.int64)
+    if n:
+        lib.mfadd_shard_exchange(dec._h, rank, nranks, peer, int(recv), out.ctypes.data_as(C.POINTER(C.c_int64)), n)
+    return out
+
+
+def solve_loopback(field_: "Field", dec: "Decomposition", nranks: int, config: "SolverConfig" = None,
+                   ctx: Optional["Context"] = None) -> "SolveResult":
+    """The sharded solve with all `nranks` shard solvers in this process on one
+    device (device-to-device copies stand in for NCCL): checks the multi-GPU
+    path against the single-device solve."""
+    ctx = ctx or default_context()
+    config = config or SolverConfig()
+    cfg = config.to_c()
+    v = np.ascontiguousarray(field_.values, np.float64).reshape(-1)
+    ctrl = np.zeros(tuple(dec.n_ctrl), np.float64)
+    err = np.zeros(dec.grid_dims, np.float64)
+    sm = L.SolveSummaryC()
+    ep = (L.EpochStatsC * (config.max_outer_iterations + 2))()
+    npairs = sum(len([j for j in b.neighbors if j > b.id]) for b in dec.blocks)
+    fj = np.zeros((max(1, npairs), 4))
+    _check(L.load().mfadd_solve_loopback(ctx._h, dec._h, C.byref(cfg), nranks, v.ctypes.data_as(C.c_void_p),
+                                         ctrl.ctypes.data_as(C.c_void_p), err.ctypes.data_as(C.c_void_p),
+                                         C.byref(sm), ep, len(ep), _dp(fj), len(fj)))
+    epochs = [EpochStats(e.iteration, e.dp_max, e.jump_ss, e.jump_ms) for e in ep[:sm.n_epochs]]
+    jumps = [InterfaceJump(int(r[0]), int(r[1]), float(r[2]), float(r[3])) for r in fj[:sm.n_final_jumps]]
+    model = MfaModel([dec.degree] * dec.rank, dec.kvs, ctrl, dec.bounds)
+    t = PhaseTimings(sm.t_setup, sm.t_local_solve, sm.t_exchange, sm.t_constraint, sm.t_decode)
+    return SolveResult(model, bool(sm.converged), sm.constraint_iterations, sm.final_dp, epochs, jumps, t, [],
+                       sm.global_l2, sm.global_linf, err)
+
+
+class Solver:
+    """A solve() plan: the decomposition's device tables + work buffers.  With
+    `comm`, the plan of this rank's shard (mfadd_solver_create_sharded); run()
+    is then collective over the communicator's ranks."""
+
+    def __init__(self, dec: Decomposition, config: SolverConfig = None, ctx: Optional[Context] = None,
+                 comm: Optional[Comm] = None):
         self.ctx = ctx or default_context()
         self.dec = dec
         self.config = config or SolverConfig()
+        self.comm = comm
         self._cfg = self.config.to_c()
         h = C.c_void_p()
-        _check(L.load().mfadd_solver_create(self.ctx._h, dec._h, C.byref(self._cfg), C.byref(h)))
+        if comm is None:
+            _check(L.load().mfadd_solver_create(self.ctx._h, dec._h, C.byref(self._cfg), C.byref(h)))
+        else:
+            _check(L.load().mfadd_solver_create_sharded(self.ctx._h, dec._h, C.byref(self._cfg), comm._h,
+                                                        C.byref(h)))
         self._h = h
         self.summary = L.SolveSummaryC()
 

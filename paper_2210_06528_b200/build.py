@@ -67,7 +67,7 @@ def build(force: bool = False, verbose: bool = False, debug: bool = False) -> st
     if failed:
         raise RuntimeError("libmfadd_b200 build failed")
     tmp = lib + ".tmp"
-    link = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
+    link = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart_static", "-lnccl", "-lrt", "-ldl", "-lpthread"]
     if verbose:
         print(" ".join(link))
     subprocess.run(link, check=True)

@@ -67,6 +67,7 @@ struct EpochAcc {
 constexpr int kRegionMaxHolders = 8;
 struct RegionDev {
   int ns;      // holders (2, 4 or 8)
+  int rmask;   // bit h: holder h lives on another rank (value read from the receive buffer, not written)
   int ext[3];  // box extents (1 for unused dims)
   int ids[kRegionMaxHolders];
   long long base[kRegionMaxHolders];
@@ -78,6 +79,15 @@ struct RegionDev {
 // the region's descriptor inlined (one dependent load per tile).
 struct TileDev {
   RegionDev r;
+  int start, count;
+};
+
+// Sharded solve: copy [start, start+count) of one holder's copy of a region
+// box (P offset base + r.str) into the send buffer at dst + i.
+struct PackTile {
+  long long base, dst;
+  int str[3];
+  int ext1, ext2;
   int start, count;
 };
 

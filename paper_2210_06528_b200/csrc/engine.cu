@@ -12,12 +12,15 @@
 #include <array>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
+
+#include <nccl.h>
 
 #include "../../include/mfadd_b200.h"
 #include "dev.cuh"
@@ -45,6 +48,11 @@ void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw ApiError(MFADD_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 #define CK(x) cuda_check((x), #x)
+#define NCK(x)                                                                                   \
+  do {                                                                                           \
+    const ncclResult_t r_ = (x);                                                                 \
+    if (r_ != ncclSuccess) throw ApiError(MFADD_ECUDA, std::string(#x) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
 
 template <class Fn>
 int guarded(Fn&& fn) {
@@ -613,6 +621,16 @@ struct DecodePlan {
 
 }  // namespace
 
+struct mfadd_comm {
+  ncclComm_t comm = nullptr;
+  int rank = 0, nranks = 1;
+};
+
+struct ShardPeer {
+  int rank = -1;
+  std::int64_t send_off = 0, send_count = 0, recv_off = 0, recv_count = 0;
+};
+
 struct mfadd_solver {
   mfadd_context* ctx = nullptr;
   Decomp dec;
@@ -642,6 +660,18 @@ struct mfadd_solver {
   // enforce_constraints in the first exchange epoch (solver.cpp:134-141).
   std::string holder_fault;
   int max_holders = 1;
+  // shard: rank of nranks owns blocks [srange.blo, srange.bhi)
+  int rank = 0, nranks = 1;
+  mfb::ShardRange srange;
+  std::vector<int> local_of;  // global block id -> local index (-1: other rank)
+  mfadd_comm* comm = nullptr;
+  std::vector<ShardPeer> peers;
+  std::int64_t send_total = 0, recv_total = 0;
+  DBuf<double> sendbuf, recvbuf;
+  DBuf<mfb::PackTile> pack_tiles;
+  int npack = 0;
+  DBuf<mfb::TileDev> xtiles;  // cross-rank region tiles
+  int nxtiles = 0;
   // region-form epochs (max_holders <= 8): tables + the epoch-loop graph
   DBuf<mfb::TileDev> tiles;
   int ntiles = 0;
@@ -797,7 +827,7 @@ mfb::EpochRegionArgs region_args(mfadd_solver* s, int mode) {
   mfb::EpochRegionArgs a{};
   a.tiles = s->tiles.p;
   a.ntiles = s->ntiles;
-  a.nblocks = s->dec.nblocks;
+  a.nblocks = static_cast<int>(s->wl.blocks.size());  // local blocks
   a.P = s->wl.P.p;
   a.mode = mode;
   a.change = s->change.p;
@@ -809,88 +839,127 @@ mfb::EpochRegionArgs region_args(mfadd_solver* s, int mode) {
   a.max_iter = s->cfg.max_outer_iterations;
   a.tol = s->cfg.tolerance;
   a.max_ns = s->max_holders;
+  a.finalize = 1;  // the last CTA computes dp (and ends the graph loop)
   return a;
 }
 
-// Shared controls as regions: products of one constant-holder interval per
-// dim (SharedDofMap::holder_span, layout.cpp:125-203) with n_s >= 2, each cut
-// into tiles of at most kTile controls.  Holder h follows the reference's
-// ascending block-id order (last dim least significant).
+// Shared controls as regions (mfb::enumerate_regions), each cut into tiles of
+// at most kTile controls.  Regions whose holders are all local become local
+// tiles; on a sharded solver, regions that also have holders on other ranks
+// become cross tiles whose remote holders read the receive buffer (rmask),
+// plus pack tiles that gather this rank's copies for each peer.
 void build_regions(mfadd_solver* s, const std::vector<int>& pair_slot) {
   constexpr int kTile = 1024;  // 256 threads x 4 controls (n_s = 2: one pass)
   const Decomp& d = s->dec;
-  const int D = d.rank;
-  struct Iv {
-    std::int64_t lo, hi;
-    int f, e;
-  };
-  std::vector<Iv> iv[3];
-  for (int k = 0; k < D; ++k)
-    for (std::int64_t i = 0; i < d.n_ctrl[k]; ++i) {
-      const auto r = d.holder[k][static_cast<std::size_t>(i)];
-      if (!iv[k].empty() && iv[k].back().f == r[0] && iv[k].back().e == r[1] - r[0] + 1 && iv[k].back().hi == i)
-        ++iv[k].back().hi;
-      else
-        iv[k].push_back({i, i + 1, r[0], r[1] - r[0] + 1});
+  const int D = d.rank, sh = 3 - D;  // box dims are right-aligned in the kernel's 3-D view
+  const std::vector<mfb::Region> regs = mfb::enumerate_regions(d);
+  const std::vector<mfb::PeerLayout> peers = mfb::shard_peers(d, regs, s->rank, s->nranks);
+  // receive-buffer offset of (region, holder) and the peer segments
+  std::vector<std::int64_t> rbase(regs.size() * 8, -1);
+  s->peers.clear();
+  std::int64_t soff = 0, roff = 0;
+  std::vector<mfb::PackTile> packs;
+  for (const auto& pl : peers) {
+    ShardPeer sp;
+    sp.rank = pl.peer;
+    sp.send_off = soff;
+    sp.send_count = pl.send_count;
+    sp.recv_off = roff;
+    sp.recv_count = pl.recv_count;
+    for (const auto& e : pl.recv) {
+      rbase[static_cast<std::size_t>(e.first) * 8 + e.second] = roff;
+      roff += regs[static_cast<std::size_t>(e.first)].size();
     }
-  std::vector<mfb::TileDev> tls;
-  std::size_t cnt[3] = {1, 1, 1};
-  for (int k = 0; k < D; ++k) cnt[k] = iv[k].size();
-  for (std::size_t i0 = 0; i0 < cnt[0]; ++i0)
-    for (std::size_t i1 = 0; i1 < cnt[1]; ++i1)
-      for (std::size_t i2 = 0; i2 < cnt[2]; ++i2) {
-        const std::size_t ii[3] = {i0, i1, i2};
-        const Iv* v[3];
-        int ns = 1;
-        for (int k = 0; k < D; ++k) {
-          v[k] = &iv[k][ii[k]];
-          ns *= v[k]->e;
-        }
-        if (ns < 2) continue;
-        mfb::RegionDev R{};
-        R.ns = ns;
-        const int sh = 3 - D;  // box dims are right-aligned in the kernel's 3-D view
-        for (int k = 0; k < 3; ++k) R.ext[k] = 1;
-        for (int k = 0; k < D; ++k) R.ext[sh + k] = static_cast<int>(v[k]->hi - v[k]->lo);
-        int cs[8][3];
-        for (int h = 0; h < ns; ++h) {
-          int rr = h, c[3] = {0, 0, 0};
-          for (int k = D - 1; k >= 0; --k) {
-            c[k] = v[k]->f + (v[k]->e == 2 ? (rr & 1) : 0);
-            rr = v[k]->e == 2 ? (rr >> 1) : rr;
-          }
-          int id = 0;
-          for (int k = 0; k < D; ++k) id = id * d.blocks[k] + c[k];
-          std::int64_t stride = 1, base = 0;
-          for (int k = D - 1; k >= 0; --k) {
-            const AxisProb& pk = s->wl.probs[static_cast<std::size_t>(s->axbase[k] + c[k])];
-            base += (v[k]->lo - pk.col_lo) * stride;
-            R.str[h][sh + k] = static_cast<int>(stride);
-            stride *= pk.n;
-          }
-          R.ids[h] = id;
-          R.base[h] = s->wl.blocks[static_cast<std::size_t>(id)].poff + base;
-          for (int k = 0; k < 3; ++k) cs[h][k] = c[k];
-        }
-        int q = 0;
-        for (int h1 = 0; h1 < ns; ++h1)
-          for (int h2 = h1 + 1; h2 < ns; ++h2, ++q) {
-            int code = 0, mul = 1;
-            for (int k = D - 1; k >= 0; --k) {
-              code += (cs[h2][k] - cs[h1][k] + 1) * mul;
-              mul *= 3;
-            }
-            R.pslot[q] = pair_slot[static_cast<std::size_t>(R.ids[h1]) * 27 + code];
-          }
-        const std::int64_t total64 = static_cast<std::int64_t>(R.ext[0]) * R.ext[1] * R.ext[2];
-        if (total64 >= (std::int64_t{1} << 24))  // fast_divmod range (kernels.cu)
-          throw std::invalid_argument("mfadd_b200: a shared-control region exceeds 2^24 controls");
-        const int total = static_cast<int>(total64);
-        for (int st0 = 0; st0 < total; st0 += kTile) tls.push_back({R, st0, std::min(kTile, total - st0)});
+    for (const auto& e : pl.send) {  // pack this rank's copy of (region, holder) at soff
+      const mfb::Region& R = regs[static_cast<std::size_t>(e.first)];
+      const int b = R.ids[static_cast<std::size_t>(e.second)];
+      const int lb = s->local_of[static_cast<std::size_t>(b)];
+      std::int64_t stride = 1, base = 0;
+      mfb::PackTile pt{};
+      for (int k = D - 1; k >= 0; --k) {
+        const AxisProb& pk = s->wl.probs[static_cast<std::size_t>(s->axbase[k] + R.coords[static_cast<std::size_t>(e.second)][static_cast<std::size_t>(k)])];
+        base += (R.lo[static_cast<std::size_t>(k)] - pk.col_lo) * stride;
+        pt.str[sh + k] = static_cast<int>(stride);
+        stride *= pk.n;
       }
-  s->ntiles = static_cast<int>(tls.size());
-  if (s->ntiles == 0) return;
-  s->tiles.upload(tls, s->ctx->stream);
+      pt.base = s->wl.blocks[static_cast<std::size_t>(lb)].poff + base;
+      int ext[3] = {1, 1, 1};
+      for (int k = 0; k < D; ++k) ext[sh + k] = static_cast<int>(R.ext[static_cast<std::size_t>(k)]);
+      pt.ext1 = ext[1];
+      pt.ext2 = ext[2];
+      const int total = static_cast<int>(R.size());
+      for (int st0 = 0; st0 < total; st0 += kTile) {
+        mfb::PackTile t = pt;
+        t.dst = soff;
+        t.start = st0;
+        t.count = std::min(kTile, total - st0);
+        packs.push_back(t);
+      }
+      soff += R.size();
+    }
+    s->peers.push_back(sp);
+  }
+  s->send_total = soff;
+  s->recv_total = roff;
+  std::vector<mfb::TileDev> local_tiles, cross_tiles;
+  for (std::size_t ri = 0; ri < regs.size(); ++ri) {
+    const mfb::Region& G = regs[ri];
+    bool any_local = false;
+    for (int h = 0; h < G.ns; ++h) any_local = any_local || s->local_of[static_cast<std::size_t>(G.ids[static_cast<std::size_t>(h)])] >= 0;
+    if (!any_local) continue;
+    const std::int64_t total64 = G.size();
+    if (total64 >= (std::int64_t{1} << 24))  // fast_divmod range (kernels.cu)
+      throw std::invalid_argument("mfadd_b200: a shared-control region exceeds 2^24 controls");
+    mfb::RegionDev R{};
+    R.ns = G.ns;
+    for (int k = 0; k < 3; ++k) R.ext[k] = 1;
+    for (int k = 0; k < D; ++k) R.ext[sh + k] = static_cast<int>(G.ext[static_cast<std::size_t>(k)]);
+    for (int h = 0; h < G.ns; ++h) {
+      const int id = G.ids[static_cast<std::size_t>(h)];
+      const int lb = s->local_of[static_cast<std::size_t>(id)];
+      if (lb >= 0) {
+        std::int64_t stride = 1, base = 0;
+        for (int k = D - 1; k >= 0; --k) {
+          const AxisProb& pk = s->wl.probs[static_cast<std::size_t>(s->axbase[k] + G.coords[static_cast<std::size_t>(h)][static_cast<std::size_t>(k)])];
+          base += (G.lo[static_cast<std::size_t>(k)] - pk.col_lo) * stride;
+          R.str[h][sh + k] = static_cast<int>(stride);
+          stride *= pk.n;
+        }
+        R.ids[h] = lb;
+        R.base[h] = s->wl.blocks[static_cast<std::size_t>(lb)].poff + base;
+      } else {  // remote holder: linear index into its receive-buffer copy
+        R.rmask |= 1 << h;
+        R.ids[h] = -1;
+        R.base[h] = rbase[ri * 8 + static_cast<std::size_t>(h)];
+        if (R.base[h] < 0) throw std::logic_error("build_regions: remote holder without a receive slot");
+        R.str[h][0] = R.ext[1] * R.ext[2];
+        R.str[h][1] = R.ext[2];
+        R.str[h][2] = 1;
+      }
+    }
+    int q = 0;
+    for (int h1 = 0; h1 < G.ns; ++h1)
+      for (int h2 = h1 + 1; h2 < G.ns; ++h2, ++q) {
+        int code = 0, mul = 1;
+        for (int k = D - 1; k >= 0; --k) {
+          code += (G.coords[static_cast<std::size_t>(h2)][static_cast<std::size_t>(k)] -
+                   G.coords[static_cast<std::size_t>(h1)][static_cast<std::size_t>(k)] + 1) * mul;
+          mul *= 3;
+        }
+        R.pslot[q] = pair_slot[static_cast<std::size_t>(G.ids[static_cast<std::size_t>(h1)]) * 27 + code];
+      }
+    const int total = static_cast<int>(total64);
+    auto& dst = R.rmask ? cross_tiles : local_tiles;
+    for (int st0 = 0; st0 < total; st0 += kTile) dst.push_back({R, st0, std::min(kTile, total - st0)});
+  }
+  s->ntiles = static_cast<int>(local_tiles.size());
+  s->nxtiles = static_cast<int>(cross_tiles.size());
+  s->npack = static_cast<int>(packs.size());
+  if (s->ntiles > 0) s->tiles.upload(local_tiles, s->ctx->stream);
+  if (s->nxtiles > 0) s->xtiles.upload(cross_tiles, s->ctx->stream);
+  if (s->npack > 0) s->pack_tiles.upload(packs, s->ctx->stream);
+  s->sendbuf.alloc(static_cast<std::size_t>(std::max<std::int64_t>(s->send_total, 1)));
+  s->recvbuf.alloc(static_cast<std::size_t>(std::max<std::int64_t>(s->recv_total, 1)));
 }
 
 // The epoch loop (solver.cpp:394-413) as a CUDA graph: a conditional WHILE
@@ -947,9 +1016,11 @@ void add_loop_node(mfadd_solver* s, cudaStream_t st) {
 }  // namespace
 
 // ---------------------------------------------------------------- solver
-MFB_API int mfadd_solver_create(mfadd_context* ctx, const mfadd_decomposition* dech, const mfadd_solver_config* cfg,
-                                mfadd_solver** out) {
-  return guarded([&] {
+namespace {
+
+// Solver construction for rank `rank` of `nranks` (1: the whole decomposition).
+std::unique_ptr<mfadd_solver> create_solver(mfadd_context* ctx, const mfadd_decomposition* dech,
+                                            const mfadd_solver_config* cfg, int rank, int nranks, mfadd_comm* comm) {
     ContextScope scope(ctx);
     auto s = std::make_unique<mfadd_solver>();
     s->ctx = ctx;
@@ -957,6 +1028,12 @@ MFB_API int mfadd_solver_create(mfadd_context* ctx, const mfadd_decomposition* d
     s->cfg = *cfg;
     const Decomp& d = s->dec;
     const int D = d.rank, p = d.degree;
+    s->rank = rank;
+    s->nranks = nranks;
+    s->comm = comm;
+    s->srange = mfb::shard_range(d, rank, nranks);
+    s->local_of.assign(static_cast<std::size_t>(d.nblocks), -1);
+    for (int b = s->srange.blo; b < s->srange.bhi; ++b) s->local_of[static_cast<std::size_t>(b)] = b - s->srange.blo;
     if (p > mfb::kMaxDegree)
       throw std::invalid_argument("mfadd_b200: degree " + std::to_string(p) + " exceeds the compiled maximum " +
                                   std::to_string(mfb::kMaxDegree));
@@ -1022,8 +1099,8 @@ MFB_API int mfadd_solver_create(mfadd_context* ctx, const mfadd_decomposition* d
       s->dec_prob[k] = static_cast<int>(wl.probs.size());
       wl.probs.push_back(pr);
     }
-    // blocks
-    for (int b = 0; b < d.nblocks; ++b) {
+    // blocks (this rank's)
+    for (int b = s->srange.blo; b < s->srange.bhi; ++b) {
       BlockDev bd{};
       std::int64_t fb = 0;
       for (int k = 0; k < D; ++k) {
@@ -1084,8 +1161,9 @@ MFB_API int mfadd_solver_create(mfadd_context* ctx, const mfadd_decomposition* d
     s->slist.upload(sl.empty() ? std::vector<int>{0} : sl, st);
     s->clist.upload(cl.empty() ? std::vector<int>{0} : cl, st);
     s->own_coord.upload(oc, st);
-    std::vector<std::int64_t> po;
-    for (const auto& b : wl.blocks) po.push_back(b.poff);
+    std::vector<std::int64_t> po(static_cast<std::size_t>(d.nblocks), 0);  // by global id (local blocks only)
+    for (int b = s->srange.blo; b < s->srange.bhi; ++b)
+      po[static_cast<std::size_t>(b)] = wl.blocks[static_cast<std::size_t>(b - s->srange.blo)].poff;
     s->poff.upload(po, st);
     // final-jump pair slots in the reference's order (solver.cpp:170-174)
     std::vector<int> ps(static_cast<std::size_t>(d.nblocks) * 27, -1);
@@ -1141,8 +1219,8 @@ MFB_API int mfadd_solver_create(mfadd_context* ctx, const mfadd_decomposition* d
     s->pair_slot.upload(ps, st);
     if (s->max_holders <= 8 && d.any_shared) build_regions(s.get(), ps);
     s->pair_jumps.alloc(static_cast<std::size_t>(std::max(1, s->npairs)) * 2);
-    s->change.alloc(static_cast<std::size_t>(d.nblocks));
-    s->linf_sh.alloc(static_cast<std::size_t>(d.nblocks));
+    s->change.alloc(wl.blocks.size());  // by local block index
+    s->linf_sh.alloc(wl.blocks.size());
     s->acc.alloc(1);
     s->est.alloc(1);
     s->epoch_out.alloc(static_cast<std::size_t>(cfg->max_outer_iterations + 1) * 3 + 3);
@@ -1172,9 +1250,9 @@ MFB_API int mfadd_solver_create(mfadd_context* ctx, const mfadd_decomposition* d
       s->dnt1 = D == 2 ? 1 : (M1 + s->dgeo.B1 - 1) / s->dgeo.B1;
       int sms = 148;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
-      const int M0 = static_cast<int>(d.grid[0]);
+      const int M0 = static_cast<int>(s->srange.in_hi - s->srange.in_lo);  // this rank's input rows
       const int want = std::max(1, (8 * sms + s->dnt1 * s->dnt2 - 1) / (s->dnt1 * s->dnt2));
-      const int nr = std::min(want, (M0 + s->dgeo.R - 1) / s->dgeo.R);
+      const int nr = std::max(1, std::min(want, (M0 + s->dgeo.R - 1) / s->dgeo.R));
       s->dH = round_up((M0 + nr - 1) / nr, s->dgeo.R);
       s->dnrange = (M0 + s->dH - 1) / s->dH;
       s->tma_decode = true;
@@ -1190,14 +1268,32 @@ MFB_API int mfadd_solver_create(mfadd_context* ctx, const mfadd_decomposition* d
     CK(cudaMemsetAsync(s->acc.p, 0, sizeof(mfb::EpochAcc), st));
     CK(cudaMemsetAsync(s->est.p, 0, sizeof(mfb::EpochState), st));
     CK(cudaStreamCreateWithFlags(&s->aux_stream, cudaStreamNonBlocking));
-    if (s->ntiles > 0 && cfg->enforce_continuity) build_loop_graph(s.get());
+    if (nranks > 1) {
+      if (s->max_holders > 8)
+        throw std::invalid_argument("mfadd_b200: a sharded solve needs at most two holders per axis");
+    }
+    if (nranks == 1 && s->ntiles > 0 && cfg->enforce_continuity) build_loop_graph(s.get());
     s->hres_eo = 4;
     s->hres_es = s->hres_eo + s->epoch_out.n;
     s->hres_pj = s->hres_es + (sizeof(mfb::EpochState) + 7) / 8;
     s->hres_n = s->hres_pj + s->pair_jumps.n;
     CK(cudaMallocHost(&s->hres, s->hres_n * sizeof(double)));
     CK(cudaStreamSynchronize(st));
-    *out = s.release();
+    return s;
+}
+
+}  // namespace
+
+MFB_API int mfadd_solver_create(mfadd_context* ctx, const mfadd_decomposition* dech, const mfadd_solver_config* cfg,
+                                mfadd_solver** out) {
+  return guarded([&] { *out = create_solver(ctx, dech, cfg, 0, 1, nullptr).release(); });
+}
+
+MFB_API int mfadd_solver_create_sharded(mfadd_context* ctx, const mfadd_decomposition* dech,
+                                        const mfadd_solver_config* cfg, mfadd_comm* comm, mfadd_solver** out) {
+  return guarded([&] {
+    if (!comm) throw std::invalid_argument("mfadd_solver_create_sharded: null communicator");
+    *out = create_solver(ctx, dech, cfg, comm->rank, comm->nranks, comm).release();
   });
 }
 
@@ -1266,6 +1362,109 @@ float ev_ms(cudaEvent_t a, cudaEvent_t b) {
   float ms = 0.f;
   cudaEventElapsedTime(&ms, a, b);
   return ms;
+}
+
+// The lattice part this rank assembles: its owned control rows along axis 0
+// (for D == 1 the single lattice row, restricted to the owned columns).
+void set_assemble_range(const mfadd_solver* s, mfb::AssembleArgs& aa) {
+  const Decomp& d = s->dec;
+  if (d.rank == 1) {
+    aa.row0 = 0;
+    aa.nrows = 1;
+    aa.col0 = s->srange.own_lo;
+    aa.ncols = s->srange.own_hi - s->srange.own_lo;
+    return;
+  }
+  std::int64_t rest = 1;
+  for (int k = 1; k + 1 < d.rank; ++k) rest *= d.n_ctrl[k];
+  aa.row0 = s->srange.own_lo * rest;
+  aa.nrows = (s->srange.own_hi - s->srange.own_lo) * rest;
+  aa.col0 = 0;
+  aa.ncols = d.n_ctrl[d.rank - 1];
+}
+
+// Decode of the lattice at this rank's own input rows (all rows on one rank) +
+// the deterministic partial reduction into red2 (solver.cpp:425-438).
+int enqueue_decode(mfadd_solver* s, const double* dfield) {
+  mfadd_context* ctx = s->ctx;
+  cudaStream_t st = ctx->stream;
+  const Decomp& d = s->dec;
+  Workload& wl = s->wl;
+  int launches = 0;
+  // ---- block_error_slab over every block == global decode (solver.cpp:425-438)
+  mfb::DecodeArgs da{};
+  const DecodePlan& dp = s->dp;
+  da.D = d.rank;
+  for (int k = 0; k < 3; ++k) {
+    da.M[k] = dp.M[k];
+    da.N[k] = dp.N[k];
+    da.T[k] = dp.T[k];
+    da.ntiles[k] = dp.ntiles[k];
+    da.W[k] = dp.W[k];
+    da.pk[k] = dp.pk[k];
+    if (dp.prob_of[k] >= 0) {
+      const AxisProb& pr = wl.probs[static_cast<std::size_t>(dp.prob_of[k])];
+      da.g0[k] = wl.g0.p + pr.row_off;
+      da.vals[k] = wl.vals.p + pr.row_off * (wl.p + 1);
+    } else {
+      da.g0[k] = s->unit_g0.p;
+      da.vals[k] = s->unit_vals.p;
+    }
+  }
+  da.lattice = s->lattice.p;
+  da.field = dfield;
+  da.out = s->cfg.store_error ? s->error.p : nullptr;
+  da.partial = s->partial.p;
+  std::int64_t nparts = static_cast<std::int64_t>(s->partial.n / 2);
+  s->tl.begin("decode");
+  if (s->tma_decode) {
+    mfb::DecodeSweepArgs ds{};
+    ds.D = d.rank;
+    ds.M0 = static_cast<int>(d.grid[0]);
+    ds.M1 = static_cast<int>(d.grid[1]);
+    ds.M2 = d.rank == 3 ? static_cast<int>(d.grid[2]) : 1;
+    ds.N0 = static_cast<int>(d.n_ctrl[0]);
+    ds.N1 = static_cast<int>(d.n_ctrl[1]);
+    ds.N2 = d.rank == 3 ? static_cast<int>(d.n_ctrl[2]) : 1;
+    ds.ntile1 = s->dnt1;
+    ds.ntile2 = s->dnt2;
+    ds.nrange = s->dnrange;
+    ds.H = s->dH;
+    ds.ybeg = static_cast<int>(s->srange.in_lo);
+    ds.yend = static_cast<int>(s->srange.in_hi);
+    auto rows = [&](int k, const int** g, const double** v) {
+      const AxisProb& pr = wl.probs[static_cast<std::size_t>(s->dec_prob[k])];
+      *g = wl.g0.p + pr.row_off;
+      *v = wl.vals.p + pr.row_off * (wl.p + 1);
+    };
+    rows(0, &ds.g0_0, &ds.v_0);
+    rows(1, &ds.g0_1, &ds.v_1);
+    if (d.rank == 3) rows(2, &ds.g0_2, &ds.v_2);
+    ds.lattice = s->lattice.p;
+    ds.err = s->cfg.store_error ? s->error.p : nullptr;
+    ds.partial = s->partial.p;
+    std::uint64_t dims[3];
+    std::uint32_t box[3];
+    for (int k = 0; k < d.rank; ++k) dims[k] = static_cast<std::uint64_t>(d.grid[d.rank - 1 - k]);
+    box[0] = static_cast<std::uint32_t>(s->dgeo.B2);
+    if (d.rank == 2) {
+      box[1] = static_cast<std::uint32_t>(s->dgeo.R);
+    } else {
+      box[1] = static_cast<std::uint32_t>(s->dgeo.B1);
+      box[2] = static_cast<std::uint32_t>(s->dgeo.R);
+    }
+    const CUtensorMap map = make_tmap(dfield, d.rank, dims, box);
+    launches += mfb::launch_decode_tma(wl.p, ds, map, s->dgeo, st);
+    nparts = static_cast<std::int64_t>(s->dnt1) * s->dnt2 * s->dnrange;
+  } else {
+    launches += mfb::launch_decode(wl.p, da, st);
+    nparts = s->dp.ntiles[0] * s->dp.ntiles[1] * s->dp.ntiles[2];
+  }
+  s->tl.end();
+  s->tl.begin("reduce");
+  launches += mfb::launch_reduce_partials(s->partial.p, nparts, s->red2.p, st);
+  s->tl.end();
+  return launches;
 }
 
 // Issue every device operation of one solve on the context stream (kernels,
@@ -1339,80 +1538,12 @@ int enqueue_solve(mfadd_solver* s, const double* dfield) {
   aa.poff = s->poff.p;
   aa.P = wl.P.p;
   aa.lattice = s->lattice.p;
+  set_assemble_range(s, aa);
   s->tl.begin("assemble");
   launches += mfb::launch_assemble(aa, st);
   s->tl.end();
   // ---- block_error_slab over every block == global decode (solver.cpp:425-438)
-  mfb::DecodeArgs da{};
-  const DecodePlan& dp = s->dp;
-  da.D = d.rank;
-  for (int k = 0; k < 3; ++k) {
-    da.M[k] = dp.M[k];
-    da.N[k] = dp.N[k];
-    da.T[k] = dp.T[k];
-    da.ntiles[k] = dp.ntiles[k];
-    da.W[k] = dp.W[k];
-    da.pk[k] = dp.pk[k];
-    if (dp.prob_of[k] >= 0) {
-      const AxisProb& pr = wl.probs[static_cast<std::size_t>(dp.prob_of[k])];
-      da.g0[k] = wl.g0.p + pr.row_off;
-      da.vals[k] = wl.vals.p + pr.row_off * (wl.p + 1);
-    } else {
-      da.g0[k] = s->unit_g0.p;
-      da.vals[k] = s->unit_vals.p;
-    }
-  }
-  da.lattice = s->lattice.p;
-  da.field = dfield;
-  da.out = s->cfg.store_error ? s->error.p : nullptr;
-  da.partial = s->partial.p;
-  std::int64_t nparts = static_cast<std::int64_t>(s->partial.n / 2);
-  s->tl.begin("decode");
-  if (s->tma_decode) {
-    mfb::DecodeSweepArgs ds{};
-    ds.D = d.rank;
-    ds.M0 = static_cast<int>(d.grid[0]);
-    ds.M1 = static_cast<int>(d.grid[1]);
-    ds.M2 = d.rank == 3 ? static_cast<int>(d.grid[2]) : 1;
-    ds.N0 = static_cast<int>(d.n_ctrl[0]);
-    ds.N1 = static_cast<int>(d.n_ctrl[1]);
-    ds.N2 = d.rank == 3 ? static_cast<int>(d.n_ctrl[2]) : 1;
-    ds.ntile1 = s->dnt1;
-    ds.ntile2 = s->dnt2;
-    ds.nrange = s->dnrange;
-    ds.H = s->dH;
-    auto rows = [&](int k, const int** g, const double** v) {
-      const AxisProb& pr = wl.probs[static_cast<std::size_t>(s->dec_prob[k])];
-      *g = wl.g0.p + pr.row_off;
-      *v = wl.vals.p + pr.row_off * (wl.p + 1);
-    };
-    rows(0, &ds.g0_0, &ds.v_0);
-    rows(1, &ds.g0_1, &ds.v_1);
-    if (d.rank == 3) rows(2, &ds.g0_2, &ds.v_2);
-    ds.lattice = s->lattice.p;
-    ds.err = s->cfg.store_error ? s->error.p : nullptr;
-    ds.partial = s->partial.p;
-    std::uint64_t dims[3];
-    std::uint32_t box[3];
-    for (int k = 0; k < d.rank; ++k) dims[k] = static_cast<std::uint64_t>(d.grid[d.rank - 1 - k]);
-    box[0] = static_cast<std::uint32_t>(s->dgeo.B2);
-    if (d.rank == 2) {
-      box[1] = static_cast<std::uint32_t>(s->dgeo.R);
-    } else {
-      box[1] = static_cast<std::uint32_t>(s->dgeo.B1);
-      box[2] = static_cast<std::uint32_t>(s->dgeo.R);
-    }
-    const CUtensorMap map = make_tmap(dfield, d.rank, dims, box);
-    launches += mfb::launch_decode_tma(wl.p, ds, map, s->dgeo, st);
-    nparts = static_cast<std::int64_t>(s->dnt1) * s->dnt2 * s->dnrange;
-  } else {
-    launches += mfb::launch_decode(wl.p, da, st);
-    nparts = s->dp.ntiles[0] * s->dp.ntiles[1] * s->dp.ntiles[2];
-  }
-  s->tl.end();
-  s->tl.begin("reduce");
-  launches += mfb::launch_reduce_partials(s->partial.p, nparts, s->red2.p, st);
-  s->tl.end();
+  launches += enqueue_decode(s, dfield);
   CK(cudaGetLastError());
   double* hr = s->hres;
   CK(cudaMemcpyAsync(hr, s->red2.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -1479,10 +1610,284 @@ void finish_solve(mfadd_solver* s, int launches) {
   s->have_result = true;
 }
 
+// ---------------------------------------------------------------- sharded
+// A group of shard solvers driven in lockstep (one per process with NCCL, or
+// all ranks in one process with the loopback transport).  Per epoch: pack the
+// cross-rank holder copies, exchange, average (local tiles + cross tiles; both
+// ranks of a cross region form the identical ascending-holder sum, so every
+// copy stays bitwise equal to the single-device solve), dp/jumps max-reduced
+// across ranks (solver.cpp:394-413 with the runtime.cpp exchange over NCCL).
+struct Transport {
+  virtual ~Transport() = default;
+  virtual void exchange(std::vector<mfadd_solver*>& g) = 0;               // send -> recv buffers
+  virtual void max_u64(std::vector<mfadd_solver*>& g, std::size_t off, std::size_t n, bool pairs) = 0;
+  virtual void gather_lattice(std::vector<mfadd_solver*>& g) = 0;         // owned rows to every rank
+  // red2: sum l2^2 over ranks (each decoded its own rows), or max when every
+  // rank decoded all rows (generic decode path: identical values), max linf
+  virtual void reduce_err(std::vector<mfadd_solver*>& g, bool sum_l2) = 0;
+};
+
+std::int64_t lattice_row_elems(const Decomp& d) {
+  std::int64_t r = 1;
+  for (int k = 1; k < d.rank; ++k) r *= d.n_ctrl[k];
+  return r;
+}
+
+struct NcclTransport : Transport {
+  void exchange(std::vector<mfadd_solver*>& g) override {
+    mfadd_solver* s = g[0];
+    if (s->peers.empty()) return;
+    cudaStream_t st = s->ctx->stream;
+    NCK(ncclGroupStart());
+    for (const auto& pr : s->peers) {
+      if (pr.send_count) NCK(ncclSend(s->sendbuf.p + pr.send_off, pr.send_count, ncclFloat64, pr.rank, s->comm->comm, st));
+      if (pr.recv_count) NCK(ncclRecv(s->recvbuf.p + pr.recv_off, pr.recv_count, ncclFloat64, pr.rank, s->comm->comm, st));
+    }
+    NCK(ncclGroupEnd());
+  }
+  void max_u64(std::vector<mfadd_solver*>& g, std::size_t off, std::size_t n, bool pairs) override {
+    mfadd_solver* s = g[0];
+    auto* p = pairs ? s->pair_jumps.p + off : reinterpret_cast<unsigned long long*>(s->epoch_out.p + off);
+    NCK(ncclAllReduce(p, p, n, ncclUint64, ncclMax, s->comm->comm, s->ctx->stream));
+  }
+  void gather_lattice(std::vector<mfadd_solver*>& g) override {
+    mfadd_solver* s = g[0];
+    const Decomp& d = s->dec;
+    const std::int64_t row = lattice_row_elems(d);
+    NCK(ncclGroupStart());
+    for (int q = 0; q < s->nranks; ++q) {
+      if (q == s->rank) continue;
+      const mfb::ShardRange mine = s->srange, theirs = mfb::shard_range(d, q, s->nranks);
+      NCK(ncclSend(s->lattice.p + mine.own_lo * row, (mine.own_hi - mine.own_lo) * row, ncclFloat64, q, s->comm->comm,
+                   s->ctx->stream));
+      NCK(ncclRecv(s->lattice.p + theirs.own_lo * row, (theirs.own_hi - theirs.own_lo) * row, ncclFloat64, q,
+                   s->comm->comm, s->ctx->stream));
+    }
+    NCK(ncclGroupEnd());
+  }
+  void reduce_err(std::vector<mfadd_solver*>& g, bool sum_l2) override {
+    mfadd_solver* s = g[0];
+    NCK(ncclAllReduce(s->red2.p, s->red2.p, 1, ncclFloat64, sum_l2 ? ncclSum : ncclMax, s->comm->comm,
+                      s->ctx->stream));
+    NCK(ncclAllReduce(s->red2.p + 1, s->red2.p + 1, 1, ncclFloat64, ncclMax, s->comm->comm, s->ctx->stream));
+  }
+};
+
+// All ranks' shard solvers in one process on one device (tests): the host
+// orders every step, so no kernel waits on another.
+struct LoopbackTransport : Transport {
+  void exchange(std::vector<mfadd_solver*>& g) override {
+    for (mfadd_solver* r : g)
+      for (const auto& pr : r->peers) {
+        mfadd_solver* q = g[static_cast<std::size_t>(pr.rank)];
+        const ShardPeer* back = nullptr;
+        for (const auto& pq : q->peers)
+          if (pq.rank == r->rank) back = &pq;
+        if (!back || back->send_count != pr.recv_count) throw std::logic_error("loopback: asymmetric exchange plan");
+        if (pr.recv_count)
+          CK(cudaMemcpyAsync(r->recvbuf.p + pr.recv_off, q->sendbuf.p + back->send_off, pr.recv_count * sizeof(double),
+                             cudaMemcpyDeviceToDevice, r->ctx->stream));
+      }
+  }
+  void max_u64(std::vector<mfadd_solver*>& g, std::size_t off, std::size_t n, bool pairs) override {
+    std::vector<unsigned long long> acc(n, 0ull), v(n);
+    for (mfadd_solver* s : g) {
+      const void* p = pairs ? static_cast<const void*>(s->pair_jumps.p + off) : static_cast<const void*>(s->epoch_out.p + off);
+      CK(cudaMemcpyAsync(v.data(), p, n * 8, cudaMemcpyDeviceToHost, s->ctx->stream));
+      CK(cudaStreamSynchronize(s->ctx->stream));
+      for (std::size_t i = 0; i < n; ++i) acc[i] = std::max(acc[i], v[i]);
+    }
+    for (mfadd_solver* s : g) {
+      void* p = pairs ? static_cast<void*>(s->pair_jumps.p + off) : static_cast<void*>(s->epoch_out.p + off);
+      CK(cudaMemcpyAsync(p, acc.data(), n * 8, cudaMemcpyHostToDevice, s->ctx->stream));
+      CK(cudaStreamSynchronize(s->ctx->stream));
+    }
+  }
+  void gather_lattice(std::vector<mfadd_solver*>& g) override {
+    const Decomp& d = g[0]->dec;
+    const std::int64_t row = lattice_row_elems(d);
+    for (mfadd_solver* q : g)
+      for (mfadd_solver* r : g)
+        if (q != r)
+          CK(cudaMemcpyAsync(r->lattice.p + q->srange.own_lo * row, q->lattice.p + q->srange.own_lo * row,
+                             (q->srange.own_hi - q->srange.own_lo) * row * sizeof(double), cudaMemcpyDeviceToDevice,
+                             r->ctx->stream));
+  }
+  void reduce_err(std::vector<mfadd_solver*>& g, bool sum_l2) override {
+    double l2 = 0.0, li = 0.0, v[2];
+    for (mfadd_solver* s : g) {  // rank order
+      CK(cudaMemcpyAsync(v, s->red2.p, sizeof v, cudaMemcpyDeviceToHost, s->ctx->stream));
+      CK(cudaStreamSynchronize(s->ctx->stream));
+      l2 = sum_l2 ? l2 + v[0] : std::max(l2, v[0]);
+      li = std::max(li, v[1]);
+    }
+    v[0] = l2;
+    v[1] = li;
+    for (mfadd_solver* s : g) {
+      CK(cudaMemcpyAsync(s->red2.p, v, sizeof v, cudaMemcpyHostToDevice, s->ctx->stream));
+      CK(cudaStreamSynchronize(s->ctx->stream));
+    }
+  }
+};
+
+int shard_pack(mfadd_solver* s) {
+  return mfb::launch_pack(s->pack_tiles.p, s->npack, s->wl.P.p, s->sendbuf.p, s->ctx->stream);
+}
+
+// One epoch's averaging/measurement on this rank after the exchange.
+int shard_compute(mfadd_solver* s, int mode, int slot) {
+  cudaStream_t st = s->ctx->stream;
+  int l = 0;
+  mfb::EpochRegionArgs a = region_args(s, mode);
+  a.finalize = 0;
+  a.recv = s->recvbuf.p;
+  a.slot = slot;
+  l += mfb::launch_epoch_regions(a, st);
+  a.tiles = s->xtiles.p;
+  a.ntiles = s->nxtiles;
+  l += mfb::launch_epoch_regions(a, st);
+  if (mode != 3) {
+    a.tiles = s->tiles.p;
+    a.ntiles = s->ntiles;
+    l += mfb::launch_epoch_finalize(a, st);
+  }
+  return l;
+}
+
+double read_epoch_dp(mfadd_solver* s, int slot) {
+  double v = 0.0;
+  CK(cudaMemcpyAsync(&v, s->epoch_out.p + 3 * slot, sizeof v, cudaMemcpyDeviceToHost, s->ctx->stream));
+  CK(cudaStreamSynchronize(s->ctx->stream));
+  return v;
+}
+
+int shard_assemble_decode(mfadd_solver* s, const double* dfield) {
+  const Decomp& d = s->dec;
+  Workload& wl = s->wl;
+  cudaStream_t st = s->ctx->stream;
+  int l = 0;
+  mfb::AssembleArgs aa{};
+  aa.D = d.rank;
+  for (int k = 0; k < 3; ++k) {
+    aa.B[k] = d.blocks[k];
+    aa.N[k] = d.n_ctrl[k];
+    aa.oc_off[k] = s->oc_off[k];
+    aa.axbase[k] = s->axbase[k];
+  }
+  aa.own_coord = s->own_coord.p;
+  aa.probs = wl.d_probs.p;
+  aa.poff = s->poff.p;
+  aa.P = wl.P.p;
+  aa.lattice = s->lattice.p;
+  set_assemble_range(s, aa);
+  l += mfb::launch_assemble(aa, st);
+  return l;
+}
+
+int shard_decode(mfadd_solver* s, const double* dfield) { return enqueue_decode(s, dfield); }
+
+void solve_group(std::vector<mfadd_solver*>& g, const std::vector<const double*>& fields, Transport& tr) {
+  static const bool trace = std::getenv("MFADD_TRACE") != nullptr;
+  auto tmark = [&](const char* what, int it) {
+    if (!trace) return;
+    for (mfadd_solver* s : g) CK(cudaStreamSynchronize(s->ctx->stream));
+    std::fprintf(stderr, "[mfadd shard] %s %d\n", what, it);
+  };
+  mfadd_solver* s0 = g[0];
+  const Decomp& d = s0->dec;
+  const bool loop = s0->cfg.enforce_continuity && d.any_shared;
+  std::vector<int> launches(g.size(), 0);
+  for (std::size_t r = 0; r < g.size(); ++r) {
+    mfadd_solver* s = g[r];
+    s->have_result = false;
+    s->tl.st = s->ctx->stream;
+    (void)cudaGetLastError();
+    if (loop && !s->holder_fault.empty()) {
+      s->wl.setup(s->ctx, &s->tl);
+      s->wl.fit(s->ctx, fields[r], &s->tl);
+      s->wl.raise_status(read_status(s->ctx), "");
+      throw std::runtime_error(s->holder_fault);
+    }
+    CK(cudaEventRecord(s->ev[0], s->ctx->stream));
+    launches[r] += s->wl.setup(s->ctx, &s->tl);
+    CK(cudaEventRecord(s->ev[1], s->ctx->stream));
+    launches[r] += s->wl.fit(s->ctx, fields[r], &s->tl);
+    CK(cudaEventRecord(s->ev[2], s->ctx->stream));
+    CK(cudaMemsetAsync(s->est.p, 0, sizeof(mfb::EpochState), s->ctx->stream));
+  }
+  auto epoch = [&](int mode, int slot) {
+    for (std::size_t r = 0; r < g.size(); ++r) launches[r] += shard_pack(g[r]);
+    tr.exchange(g);
+    for (std::size_t r = 0; r < g.size(); ++r) launches[r] += shard_compute(g[r], mode, slot);
+    tr.max_u64(g, static_cast<std::size_t>(3 * slot), 3, false);
+  };
+  tmark("fit done", 0);
+  epoch(0, 0);  // record_epoch(0, 0.0)
+  tmark("epoch", 0);
+  int last = 0;
+  bool converged = true;
+  if (loop) {
+    converged = false;
+    for (int it = 1; it <= s0->cfg.max_outer_iterations; ++it) {
+      epoch(it >= 2 ? 2 : 1, it);
+      tmark("epoch", it);
+      last = it;
+      if (read_epoch_dp(s0, it) < s0->cfg.tolerance) {  // identical on every rank after the max
+        converged = true;
+        break;
+      }
+    }
+  }
+  for (mfadd_solver* s : g) CK(cudaEventRecord(s->ev[3], s->ctx->stream));
+  if (s0->npairs > 0) {  // final jumps (solver.cpp:416); exactly zero after a mode-2 epoch
+    for (mfadd_solver* s : g)
+      CK(cudaMemsetAsync(s->pair_jumps.p, 0, s->pair_jumps.n * sizeof(unsigned long long), s->ctx->stream));
+    if (last < 2) {
+      for (std::size_t r = 0; r < g.size(); ++r) launches[r] += shard_pack(g[r]);
+      tr.exchange(g);
+      for (std::size_t r = 0; r < g.size(); ++r) launches[r] += shard_compute(g[r], 3, 0);
+      tr.max_u64(g, 0, s0->pair_jumps.n, true);
+    }
+  }
+  tmark("jumps", 0);
+  for (std::size_t r = 0; r < g.size(); ++r) launches[r] += shard_assemble_decode(g[r], fields[r]);
+  tr.gather_lattice(g);
+  tmark("assembled", 0);
+  for (std::size_t r = 0; r < g.size(); ++r) launches[r] += shard_decode(g[r], fields[r]);
+  tr.reduce_err(g, s0->tma_decode);
+  tmark("decoded", 0);
+  // results (identical on every rank after the reductions)
+  for (std::size_t r = 0; r < g.size(); ++r) {
+    mfadd_solver* s = g[r];
+    cudaStream_t st = s->ctx->stream;
+    double* hr = s->hres;
+    CK(cudaMemcpyAsync(hr, s->red2.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hr + 2, s->ctx->d_status, sizeof(mfb::DevStatus), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hr + s->hres_eo, s->epoch_out.p, s->epoch_out.n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (s->npairs > 0)
+      CK(cudaMemcpyAsync(hr + s->hres_pj, s->pair_jumps.p, s->pair_jumps.n * sizeof(unsigned long long),
+                         cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(s->ev[4], st));
+    mfb::EpochState es{};
+    es.iter = last;
+    es.last_iter = last;
+    es.converged = converged ? 1 : 0;
+    CK(cudaStreamSynchronize(st));
+    std::memcpy(hr + s->hres_es, &es, sizeof es);
+    finish_solve(s, launches[r] - (loop ? last : 0));  // finish_solve adds one launch per iteration
+  }
+}
+
 // solve(): replay the cached whole-solve graph when possible (no per-kernel
 // profiling, no debug sync checks, no holder fault), else launch directly.
 void solve_impl(mfadd_solver* s, const double* dfield) {
   s->have_result = false;
+  if (s->nranks > 1) {  // sharded: host-driven epochs with NCCL exchanges
+    std::vector<mfadd_solver*> g{s};
+    NcclTransport tr;
+    solve_group(g, {dfield}, tr);
+    return;
+  }
   const bool graphable = !s->tl.on && !s->tl.sync_check && s->holder_fault.empty() && !std::getenv("MFADD_NO_GRAPH");
   if (!graphable) {
     finish_solve(s, enqueue_solve(s, dfield));
@@ -1599,8 +2004,11 @@ MFB_API int mfadd_solver_block_controls(const mfadd_solver* s, int block, double
   return guarded([&] {
     if (!s->have_result) throw std::logic_error("mfadd_solver_block_controls: no solve result");
     if (block < 0 || block >= s->dec.nblocks) throw std::out_of_range("mfadd_solver_block_controls: block id");
+    const int lb = s->local_of[static_cast<std::size_t>(block)];
+    if (lb < 0) throw std::out_of_range("mfadd_solver_block_controls: block " + std::to_string(block) + " is on rank " +
+                                        std::to_string(mfb::shard_of_block(s->dec, s->nranks, block)));
     ContextScope scope(s->ctx);
-    const BlockDev& b = s->wl.blocks[static_cast<std::size_t>(block)];
+    const BlockDev& b = s->wl.blocks[static_cast<std::size_t>(lb)];
     std::int64_t np = 1;
     for (int k = 0; k < s->dec.rank; ++k) np *= s->wl.probs[static_cast<std::size_t>(b.ax[k])].n;
     CK(cudaMemcpyAsync(out, s->wl.P.p + b.poff, static_cast<std::size_t>(np) * sizeof(double),
@@ -1869,5 +2277,110 @@ MFB_API int mfadd_decode(mfadd_context* ctx, int rank, int degree, const double*
     wl.raise_status(stt, "");
     CK(cudaMemcpyAsync(out, dout.p, static_cast<std::size_t>(nout) * sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+  });
+}
+
+// ---------------------------------------------------------------- multi-GPU
+MFB_API int mfadd_nccl_unique_id(unsigned char* out128) {
+  return guarded([&] {
+    ncclUniqueId id;
+    NCK(ncclGetUniqueId(&id));
+    static_assert(sizeof(id) == 128, "ncclUniqueId size");
+    std::memcpy(out128, &id, sizeof id);
+  });
+}
+
+MFB_API int mfadd_comm_create(mfadd_context* ctx, const unsigned char* id128, int rank, int nranks, mfadd_comm** out) {
+  return guarded([&] {
+    ContextScope scope(ctx);
+    auto c = std::make_unique<mfadd_comm>();
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof id);
+    NCK(ncclCommInitRank(&c->comm, nranks, id, rank));
+    c->rank = rank;
+    c->nranks = nranks;
+    *out = c.release();
+  });
+}
+
+MFB_API void mfadd_comm_free(mfadd_comm* c) {
+  if (!c) return;
+  if (c->comm) ncclCommDestroy(c->comm);
+  delete c;
+}
+
+MFB_API int mfadd_shard_range(const mfadd_decomposition* dec, int rank, int nranks, int* blo, int* bhi,
+                              int64_t* in_lo, int64_t* in_hi) {
+  return guarded([&] {
+    const mfb::ShardRange r = mfb::shard_range(dec->d, rank, nranks);
+    *blo = r.blo;
+    *bhi = r.bhi;
+    if (in_lo) *in_lo = r.in_lo;
+    if (in_hi) *in_hi = r.in_hi;
+  });
+}
+
+MFB_API int mfadd_shard_exchange(const mfadd_decomposition* dec, int rank, int nranks, int peer, int recv,
+                                 int64_t* out, int64_t cap) {
+  int64_t count = -1;
+  const int rc = guarded([&] {
+    const mfb::Decomp& d = dec->d;
+    const auto regs = mfb::enumerate_regions(d);
+    count = 0;
+    for (const auto& pl : mfb::shard_peers(d, regs, rank, nranks)) {
+      if (pl.peer != peer) continue;
+      for (const auto& e : recv ? pl.recv : pl.send) {
+        const mfb::Region& R = regs[static_cast<std::size_t>(e.first)];
+        for (std::int64_t i0 = 0; i0 < R.ext[0]; ++i0)
+          for (std::int64_t i1 = 0; i1 < R.ext[1]; ++i1)
+            for (std::int64_t i2 = 0; i2 < R.ext[2]; ++i2) {
+              if (out && count < cap) {  // (holder block, global control indices)
+                out[4 * count] = R.ids[static_cast<std::size_t>(e.second)];
+                out[4 * count + 1] = R.lo[0] + i0;
+                out[4 * count + 2] = R.lo[1] + i1;
+                out[4 * count + 3] = R.lo[2] + i2;
+              }
+              ++count;
+            }
+      }
+    }
+  });
+  return rc == MFADD_OK ? static_cast<int>(count) : -rc;
+}
+
+MFB_API int mfadd_solve_loopback(mfadd_context* ctx, const mfadd_decomposition* dec, const mfadd_solver_config* cfg,
+                                 int nranks, const double* field_host, double* out_controls, double* out_error,
+                                 mfadd_solve_summary* out, mfadd_epoch_stats* epochs, int epochs_cap,
+                                 double* final_jumps4, int jumps_cap) {
+  return guarded([&] {
+    ContextScope scope(ctx);
+    std::vector<std::unique_ptr<mfadd_solver>> own;
+    std::vector<mfadd_solver*> g;
+    for (int r = 0; r < nranks; ++r) {
+      own.push_back(create_solver(ctx, dec, cfg, r, nranks, nullptr));
+      g.push_back(own.back().get());
+    }
+    const std::size_t n = static_cast<std::size_t>(dec->d.total_inputs());
+    DBuf<double> f;
+    f.alloc(n);
+    CK(cudaMemcpyAsync(f.p, field_host, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    std::vector<const double*> fields(g.size(), f.p);
+    LoopbackTransport tr;
+    solve_group(g, fields, tr);
+    mfadd_solver* s0 = g[0];
+    if (out_controls)
+      CK(cudaMemcpy(out_controls, s0->lattice.p, s0->lattice.n * sizeof(double), cudaMemcpyDeviceToHost));
+    if (out_error) {  // each rank's own input rows
+      const mfb::Decomp& d = dec->d;
+      std::int64_t row = 1;
+      for (int k = 1; k < d.rank; ++k) row *= d.grid[k];
+      for (mfadd_solver* s : g)
+        CK(cudaMemcpy(out_error + s->srange.in_lo * row, s->error.p + s->srange.in_lo * row,
+                      (s->srange.in_hi - s->srange.in_lo) * row * sizeof(double), cudaMemcpyDeviceToHost));
+    }
+    if (out) *out = s0->summary;
+    for (int i = 0; i < static_cast<int>(s0->epochs.size()) && i < epochs_cap; ++i) epochs[i] = s0->epochs[static_cast<std::size_t>(i)];
+    for (int i = 0; i < s0->npairs && i < jumps_cap; ++i)
+      for (int k = 0; k < 4; ++k) final_jumps4[4 * i + k] = s0->final_jumps[4 * static_cast<std::size_t>(i) + k];
   });
 }

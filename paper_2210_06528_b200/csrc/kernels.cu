@@ -897,6 +897,7 @@ __device__ __forceinline__ void region_tile(const EpochRegionArgs& a, const Regi
     return R.base[h] + static_cast<long long>(r0) * R.str[h][0] + r1 * R.str[h][1] + r2 * R.str[h][2];
   };
   const int e1 = R.ext[1], e2 = R.ext[2];
+  const int rmask = R.rmask;  // remote holders: read from the receive buffer, never written
   const float rc1 = 1.0f / static_cast<float>(e1), rc2 = 1.0f / static_cast<float>(e2);
   // update: red[h] = change of holder h, red[NS] = max |avg| (every copy);
   // measure: red[h] = max |copy of holder h|, red[NS] = jump
@@ -916,7 +917,7 @@ __device__ __forceinline__ void region_tile(const EpochRegionArgs& a, const Regi
 #pragma unroll
       for (int h = 0; h < NS; ++h) {
         off[u][h] = offset(h, r0, r1, r2);
-        v[u][h] = i < end ? a.P[off[u][h]] : 0.0;
+        v[u][h] = i < end ? ((rmask >> h) & 1 ? a.recv[off[u][h]] : a.P[off[u][h]]) : 0.0;
       }
     }
 #pragma unroll
@@ -930,7 +931,7 @@ __device__ __forceinline__ void region_tile(const EpochRegionArgs& a, const Regi
 #pragma unroll
         for (int h = 0; h < NS; ++h) {
           red[h] = fmax(red[h], fabs(avg - v[u][h]));
-          a.P[off[u][h]] = avg;
+          if (!((rmask >> h) & 1)) a.P[off[u][h]] = avg;
         }
         red[NS] = fmax(red[NS], fabs(avg));  // every holder's copy is now avg
       } else {
@@ -948,16 +949,49 @@ __device__ __forceinline__ void region_tile(const EpochRegionArgs& a, const Regi
   const unsigned long long b = cta_dmax_multi<NS + 1>(red, s_w);
   const int j = threadIdx.x;
   if (b && j < NS) {
-    atomicMax((update ? a.change : a.linf_sh) + R.ids[j], b);
+    if (!((rmask >> j) & 1)) atomicMax((update ? a.change : a.linf_sh) + R.ids[j], b);
   } else if (b && j == NS) {
     if (update) {
 #pragma unroll
-      for (int h = 0; h < NS; ++h) atomicMax(a.linf_sh + R.ids[h], b);
+      for (int h = 0; h < NS; ++h)
+        if (!((rmask >> h) & 1)) atomicMax(a.linf_sh + R.ids[h], b);
     } else {
       atomicMax(NS == 2 ? &a.st->jump_ss : &a.st->jump_ms, b);
     }
   }
   __syncthreads();  // s_w and the tile descriptor are reused by the next tile
+}
+
+// dp = max_b change_b / max(1, ||P_b||_inf) (solver.cpp:398-405) into
+// epoch_out[3*slot], jumps, accumulator reset; loop bookkeeping in loop mode.
+__device__ void epoch_finalize(const EpochRegionArgs& a, int mode, int slot, unsigned long long* s_red) {
+  unsigned long long dp = 0ull;
+  for (int b = threadIdx.x; b < a.nblocks; b += blockDim.x) {
+    const unsigned long long li = umax(a.linf_int[b], __ldcg(a.linf_sh + b));
+    const double lin = __longlong_as_double(static_cast<long long>(li));
+    const double chv = __longlong_as_double(static_cast<long long>(__ldcg(a.change + b)));
+    dp = umax(dp, dbits(chv / (lin > 1.0 ? lin : 1.0)));
+    a.change[b] = 0ull;
+    a.linf_sh[b] = 0ull;
+  }
+  dp = block_umax(dp, s_red);
+  if (threadIdx.x == 0) {
+    const double dpv = mode == 0 ? 0.0 : __longlong_as_double(static_cast<long long>(dp));  // record_epoch(0, 0.0)
+    const unsigned long long js = atomicExch(&a.st->jump_ss, 0ull), jm = atomicExch(&a.st->jump_ms, 0ull);
+    double* out = a.epoch_out + 3 * slot;
+    out[0] = dpv;
+    out[1] = __longlong_as_double(static_cast<long long>(js));
+    out[2] = __longlong_as_double(static_cast<long long>(jm));
+    a.st->done = 0;
+    if (a.mode < 0) {  // loop bookkeeping (solver.cpp:406-412)
+      const bool conv = dpv < a.tol;
+      a.st->last_iter = slot;
+      a.st->converged = conv ? 1 : 0;
+      a.st->iter = slot;
+      cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(a.cond),
+                              (!conv && slot < a.max_iter) ? 1u : 0u);
+    }
+  }
 }
 
 // MAXNS = 4 for 1-D/2-D decompositions (tighter register budget, 3 CTAs/SM),
@@ -989,6 +1023,7 @@ __global__ void __launch_bounds__(kRegionThreads, MAXNS == 8 ? 2 : 3) k_epoch_re
       default: region_tile<MAXNS>(a, t.r, t, mode, s_w); break;
     }
   }
+  if (!a.finalize) return;
   // last CTA: dp = max_b change_b / max(1, ||P_b||_inf) (solver.cpp:398-405)
   __threadfence();
   __syncthreads();
@@ -996,33 +1031,14 @@ __global__ void __launch_bounds__(kRegionThreads, MAXNS == 8 ? 2 : 3) k_epoch_re
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  unsigned long long dp = 0ull;
-  for (int b = threadIdx.x; b < a.nblocks; b += blockDim.x) {
-    const unsigned long long li = umax(a.linf_int[b], __ldcg(a.linf_sh + b));
-    const double lin = __longlong_as_double(static_cast<long long>(li));
-    const double chv = __longlong_as_double(static_cast<long long>(__ldcg(a.change + b)));
-    dp = umax(dp, dbits(chv / (lin > 1.0 ? lin : 1.0)));
-    a.change[b] = 0ull;
-    a.linf_sh[b] = 0ull;
-  }
-  dp = block_umax(dp, s_red);
-  if (threadIdx.x == 0) {
-    const double dpv = mode == 0 ? 0.0 : __longlong_as_double(static_cast<long long>(dp));  // record_epoch(0, 0.0)
-    const unsigned long long js = atomicExch(&a.st->jump_ss, 0ull), jm = atomicExch(&a.st->jump_ms, 0ull);
-    double* out = a.epoch_out + 3 * iter;
-    out[0] = dpv;
-    out[1] = __longlong_as_double(static_cast<long long>(js));
-    out[2] = __longlong_as_double(static_cast<long long>(jm));
-    a.st->done = 0;
-    if (a.mode < 0) {  // loop bookkeeping (solver.cpp:406-412)
-      const bool conv = dpv < a.tol;
-      a.st->last_iter = iter;
-      a.st->converged = conv ? 1 : 0;
-      a.st->iter = iter;
-      cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(a.cond),
-                              (!conv && iter < a.max_iter) ? 1u : 0u);
-    }
-  }
+  epoch_finalize(a, mode, iter, s_red);
+}
+
+// One-CTA epoch bookkeeping after separately launched region kernels (the
+// sharded path, where dp is then max-reduced across ranks).
+__global__ void __launch_bounds__(kRegionThreads) k_epoch_finalize(EpochRegionArgs a) {
+  __shared__ unsigned long long s_red[32];
+  epoch_finalize(a, a.mode, a.slot, s_red);
 }
 
 // Final per-pair jumps (solver.cpp:416 -> :166-193): L-inf of |P_a - P_b| per
@@ -1041,8 +1057,10 @@ __device__ __forceinline__ void region_pairs(const EpochRegionArgs& a, const Reg
     const int r1 = q % e1, r0 = q / e1;
     double v[NS];
 #pragma unroll
-    for (int h = 0; h < NS; ++h)
-      v[h] = a.P[R.base[h] + static_cast<long long>(r0) * R.str[h][0] + r1 * R.str[h][1] + r2 * R.str[h][2]];
+    for (int h = 0; h < NS; ++h) {
+      const long long o = R.base[h] + static_cast<long long>(r0) * R.str[h][0] + r1 * R.str[h][1] + r2 * R.str[h][2];
+      v[h] = (R.rmask >> h) & 1 ? a.recv[o] : a.P[o];  // remote holder: its copy from the exchange
+    }
     int q2 = 0;
 #pragma unroll
     for (int h1 = 0; h1 < NS; ++h1)
@@ -1123,7 +1141,8 @@ __global__ void __launch_bounds__(256) k_assemble(AssembleArgs a) {
   if (own_smem)
     for (int i = threadIdx.x; i < Nl; i += blockDim.x) s_own[i] = static_cast<short>(a.own_coord[a.oc_off[dl] + i]);
   // lead coordinates of this row
-  std::int64_t row = blockIdx.x;
+  const std::int64_t grow = a.row0 + blockIdx.x;
+  std::int64_t row = grow;
   int cl[3] = {0, 0, 0};
   std::int64_t il[3] = {0, 0, 0};
   for (int k = dl - 1; k >= 0; --k) {
@@ -1145,8 +1164,9 @@ __global__ void __launch_bounds__(256) k_assemble(AssembleArgs a) {
     s_base[c] = a.poff[id] + o * pl.n - pl.col_lo;
   }
   __syncthreads();
-  double* out = a.lattice + static_cast<std::int64_t>(blockIdx.x) * Nl;
-  for (int i = threadIdx.x; i < Nl; i += blockDim.x) {
+  double* out = a.lattice + grow * Nl;
+  const int i0 = static_cast<int>(a.col0), i1 = static_cast<int>(a.col0 + a.ncols);
+  for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
     const int c = own_smem ? s_own[i] : a.own_coord[a.oc_off[dl] + i];
     out[i] = a.P[s_base[c] + i];
   }
@@ -1405,6 +1425,28 @@ int launch_epoch(const EpochArgs& a, cudaStream_t s) {
   return 1;
 }
 
+__global__ void __launch_bounds__(256) k_pack(const PackTile* tiles, const double* P, double* send) {
+  const PackTile t = tiles[blockIdx.x];
+  const float rc1 = 1.0f / static_cast<float>(t.ext1), rc2 = 1.0f / static_cast<float>(t.ext2);
+  for (int i = t.start + threadIdx.x; i < t.start + t.count; i += blockDim.x) {
+    int q, r2, r0, r1;
+    fast_divmod(i, t.ext2, rc2, q, r2);
+    fast_divmod(q, t.ext1, rc1, r0, r1);
+    send[t.dst + i] = P[t.base + static_cast<long long>(r0) * t.str[0] + r1 * t.str[1] + r2 * t.str[2]];
+  }
+}
+
+int launch_pack(const PackTile* tiles, int ntiles, const double* P, double* send, cudaStream_t s) {
+  if (ntiles <= 0) return 0;
+  k_pack<<<ntiles, 256, 0, s>>>(tiles, P, send);
+  return 1;
+}
+
+int launch_epoch_finalize(const EpochRegionArgs& a, cudaStream_t s) {
+  k_epoch_finalize<<<1, kRegionThreads, 0, s>>>(a);
+  return 1;
+}
+
 int launch_epoch_regions(const EpochRegionArgs& a, cudaStream_t s) {
   if (a.ntiles <= 0) return 0;
   if (a.mode == 3)
@@ -1432,10 +1474,9 @@ int launch_dp(const DpArgs& a, cudaStream_t s) {
 }
 
 int launch_assemble(const AssembleArgs& a, cudaStream_t s) {
-  std::int64_t rows = 1;
-  for (int k = 0; k + 1 < a.D; ++k) rows *= a.N[k];
   if (a.B[a.D - 1] > kAsmMaxB) return -1;  // host validates blocks_per_dim first
-  k_assemble<<<static_cast<unsigned>(rows), 256, 0, s>>>(a);
+  if (a.nrows <= 0) return 0;
+  k_assemble<<<static_cast<unsigned>(a.nrows), 256, 0, s>>>(a);
   return 1;
 }
 

@@ -126,8 +126,15 @@ struct EpochRegionArgs {
   double tol;
   unsigned long long cond;  // cudaGraphConditionalHandle (loop mode only)
   int max_ns;               // largest region n_s (selects the kernel form)
+  const double* recv;       // sharded: remote holders' copies (RegionDev::rmask)
+  int finalize;             // 1: the last CTA computes dp and writes epoch_out (else k_epoch_finalize)
+  int slot;                 // epoch_out slot when finalize is done separately
 };
 int launch_epoch_regions(const EpochRegionArgs& a, cudaStream_t s);
+// dp / jumps of the epoch into epoch_out[3*slot] and accumulator reset (one CTA).
+int launch_epoch_finalize(const EpochRegionArgs& a, cudaStream_t s);
+// Sharded solve: gather holder copies into the send buffer.
+int launch_pack(const PackTile* tiles, int ntiles, const double* P, double* send, cudaStream_t s);
 
 // K5: dp = max_b change_b / max(1, ||P_b||_inf) and epoch bookkeeping.
 struct DpArgs {
@@ -153,6 +160,8 @@ struct AssembleArgs {
   const std::int64_t* poff;
   const double* P;
   double* lattice;
+  std::int64_t row0, nrows;  // lattice rows (all dims but the last) to assemble
+  std::int64_t col0, ncols;  // last-dim range (a shard's own range when D == 1)
 };
 int launch_assemble(const AssembleArgs& a, cudaStream_t s);
 
@@ -194,6 +203,7 @@ struct DecodeSweepArgs {
   int M0, M1, M2;   // input grid extents (M2 = 1 for D = 2)
   int N0, N1, N2;   // lattice extents (N2 = 1 for D = 2)
   int ntile1, ntile2, nrange, H;
+  int ybeg, yend;   // input rows [ybeg, yend) along axis 0 decoded by this launch
   const int* g0_0;  // global decode rows per dim (row tables, 16-B aligned)
   const double* v_0;
   const int* g0_1;

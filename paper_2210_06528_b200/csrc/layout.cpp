@@ -242,4 +242,114 @@ std::vector<std::int64_t> exchange_volume(const Decomp& d) {
   return vol;
 }
 
+// ---------------------------------------------------------------- regions
+std::vector<Region> enumerate_regions(const Decomp& d) {
+  const int D = d.rank;
+  struct Iv {
+    std::int64_t lo, hi;
+    int f, e;
+  };
+  std::vector<Iv> iv[3];
+  for (int k = 0; k < D; ++k)
+    for (std::int64_t i = 0; i < d.n_ctrl[k]; ++i) {
+      const auto r = d.holder[k][static_cast<std::size_t>(i)];
+      if (r[1] - r[0] > 1) throw std::logic_error("enumerate_regions: more than two holders along one axis");
+      if (!iv[k].empty() && iv[k].back().f == r[0] && iv[k].back().e == r[1] - r[0] + 1 && iv[k].back().hi == i)
+        ++iv[k].back().hi;
+      else
+        iv[k].push_back({i, i + 1, r[0], r[1] - r[0] + 1});
+    }
+  std::vector<Region> out;
+  std::size_t cnt[3] = {1, 1, 1};
+  for (int k = 0; k < D; ++k) cnt[k] = iv[k].size();
+  for (std::size_t i0 = 0; i0 < cnt[0]; ++i0)
+    for (std::size_t i1 = 0; i1 < cnt[1]; ++i1)
+      for (std::size_t i2 = 0; i2 < cnt[2]; ++i2) {
+        const std::size_t ii[3] = {i0, i1, i2};
+        int ns = 1;
+        for (int k = 0; k < D; ++k) ns *= iv[k][ii[k]].e;
+        if (ns < 2) continue;
+        Region R;
+        R.ns = ns;
+        for (int k = 0; k < D; ++k) {
+          R.lo[static_cast<std::size_t>(k)] = iv[k][ii[k]].lo;
+          R.ext[static_cast<std::size_t>(k)] = iv[k][ii[k]].hi - iv[k][ii[k]].lo;
+        }
+        for (int h = 0; h < ns; ++h) {
+          int rr = h, c[3] = {0, 0, 0};
+          for (int k = D - 1; k >= 0; --k) {
+            const Iv& v = iv[k][ii[k]];
+            c[k] = v.f + (v.e == 2 ? (rr & 1) : 0);
+            rr = v.e == 2 ? (rr >> 1) : rr;
+          }
+          R.ids[static_cast<std::size_t>(h)] = d.block_id(c);
+          for (int k = 0; k < 3; ++k) R.coords[static_cast<std::size_t>(h)][static_cast<std::size_t>(k)] = c[k];
+        }
+        out.push_back(R);
+      }
+  return out;
+}
+
+// ---------------------------------------------------------------- sharding
+ShardRange shard_range(const Decomp& d, int rank, int nranks) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) throw std::invalid_argument("shard_range: bad rank");
+  const int B0 = d.blocks[0];
+  if (nranks > B0)
+    throw std::invalid_argument("shard_range: " + std::to_string(nranks) + " ranks for " + std::to_string(B0) +
+                                " block rows along axis 0");
+  ShardRange s;
+  s.row_lo = static_cast<int>(static_cast<std::int64_t>(rank) * B0 / nranks);
+  s.row_hi = static_cast<int>(static_cast<std::int64_t>(rank + 1) * B0 / nranks);
+  const int per_row = d.nblocks / B0;
+  s.blo = s.row_lo * per_row;
+  s.bhi = s.row_hi * per_row;
+  s.in_lo = d.dim_field(0, s.row_lo, OWNIN_LO);
+  s.in_hi = d.dim_field(0, s.row_hi - 1, OWNIN_HI);
+  s.own_lo = d.dim_field(0, s.row_lo, OWN_LO);
+  s.own_hi = d.dim_field(0, s.row_hi - 1, OWN_HI);
+  s.box_lo = d.dim_field(0, s.row_lo, IN_LO);
+  s.box_hi = d.dim_field(0, s.row_hi - 1, IN_HI);
+  return s;
+}
+
+int shard_of_block(const Decomp& d, int nranks, int block) {
+  const int B0 = d.blocks[0], row = d.coords[static_cast<std::size_t>(block)][0];
+  // inverse of row_lo(r) = r*B0/n: the largest r with row_lo(r) <= row
+  int r = static_cast<int>((static_cast<std::int64_t>(row) * nranks + nranks - 1) / B0);
+  while (r > 0 && static_cast<std::int64_t>(r) * B0 / nranks > row) --r;
+  while (r + 1 < nranks && static_cast<std::int64_t>(r + 1) * B0 / nranks <= row) ++r;
+  return r;
+}
+
+std::vector<PeerLayout> shard_peers(const Decomp& d, const std::vector<Region>& regions, int rank, int nranks) {
+  std::vector<PeerLayout> out;
+  for (int q = 0; q < nranks; ++q) {
+    if (q == rank) continue;
+    PeerLayout pl;
+    pl.peer = q;
+    for (std::size_t ri = 0; ri < regions.size(); ++ri) {
+      const Region& R = regions[ri];
+      bool mine = false, theirs = false;
+      for (int h = 0; h < R.ns; ++h) {
+        const int s = shard_of_block(d, nranks, R.ids[static_cast<std::size_t>(h)]);
+        mine = mine || s == rank;
+        theirs = theirs || s == q;
+      }
+      if (!mine || !theirs) continue;
+      for (int h = 0; h < R.ns; ++h) {
+        const int s = shard_of_block(d, nranks, R.ids[static_cast<std::size_t>(h)]);
+        if (s == rank) {
+          pl.send.emplace_back(static_cast<int>(ri), h);
+          pl.send_count += R.size();
+        } else if (s == q) {
+          pl.recv.emplace_back(static_cast<int>(ri), h);
+          pl.recv_count += R.size();
+        }
+      }
+    }
+    if (!pl.send.empty() || !pl.recv.empty()) out.push_back(pl);
+  }
+  return out;
+}
+
 }  // namespace mfb

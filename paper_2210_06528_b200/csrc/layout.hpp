@@ -72,4 +72,45 @@ std::vector<double> make_knot_vector(int degree, int basis_count, double a, doub
 // runtime.cpp:160-171
 std::vector<std::int64_t> exchange_volume(const Decomp& d);
 
+// ------------------------------------------------------------ shared regions
+// A box of shared controls with one holder set: the product of one
+// constant-holder-range interval per dim (SharedDofMap::holder_span,
+// layout.cpp:125-203) with n_s >= 2.  Holders in ascending block id
+// (layout.cpp:177-195; last dim least significant).  Requires at most two
+// holders per dim (n_s <= 8); enumeration order is deterministic.
+struct Region {
+  std::array<std::int64_t, 3> lo{0, 0, 0}, ext{1, 1, 1};
+  int ns = 0;
+  std::array<int, 8> ids{};
+  std::array<std::array<int, 3>, 8> coords{};
+  std::int64_t size() const { return ext[0] * ext[1] * ext[2]; }
+};
+std::vector<Region> enumerate_regions(const Decomp& d);
+
+// ------------------------------------------------------------ sharding
+// Rank r of n owns block rows [row_lo, row_hi) along axis 0 (block ids are
+// lexicographic with axis 0 slowest, layout.cpp:320-323), i.e. the contiguous
+// block ids [blo, bhi).  A shared control then has holders on at most two
+// adjacent ranks.
+struct ShardRange {
+  int row_lo = 0, row_hi = 0, blo = 0, bhi = 0;
+  std::int64_t in_lo = 0, in_hi = 0;    // own input rows along axis 0 (decode)
+  std::int64_t own_lo = 0, own_hi = 0;  // owned control indices along axis 0 (assembly)
+  std::int64_t box_lo = 0, box_hi = 0;  // input rows touched by the local blocks' fits
+};
+ShardRange shard_range(const Decomp& d, int rank, int nranks);
+int shard_of_block(const Decomp& d, int nranks, int block);
+
+// Per-epoch exchange with one peer rank: the buffer is the concatenation, over
+// the regions holding controls on both ranks (ascending region index), of the
+// sending rank's holders' copies (ascending holder slot), each region box in
+// row-major order.  `send` lists (region, holder slot) of this rank's copies,
+// `recv` those of the peer, in buffer order.
+struct PeerLayout {
+  int peer = -1;
+  std::vector<std::pair<int, int>> send, recv;
+  std::int64_t send_count = 0, recv_count = 0;
+};
+std::vector<PeerLayout> shard_peers(const Decomp& d, const std::vector<Region>& regions, int rank, int nranks);
+
 }  // namespace mfb

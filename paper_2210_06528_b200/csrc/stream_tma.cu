@@ -613,8 +613,8 @@ __global__ void __launch_bounds__(256) k_decode_tma(const DecodeSweepArgs a, con
     j2 = tx * B2 + tid % B2;
   }
   const bool active = D == 2 ? j1 < a.M1 : (j1 < a.M1 && j2 < a.M2);
-  const int y0 = blockIdx.y * a.H;
-  const int y1 = (y0 + a.H) < a.M0 ? (y0 + a.H) : a.M0;
+  const int y0 = a.ybeg + blockIdx.y * a.H;
+  const int y1 = (y0 + a.H) < a.yend ? (y0 + a.H) : a.yend;
   const std::int64_t Tr = static_cast<std::int64_t>(a.M1) * a.M2;
   const std::int64_t t = static_cast<std::int64_t>(j1) * a.M2 + j2;
   // trailing basis of this thread (fixed for the whole sweep)
@@ -656,7 +656,10 @@ __global__ void __launch_bounds__(256) k_decode_tma(const DecodeSweepArgs a, con
 
   const StageLayout SL = stage_layout(R, nthr, P);
   std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(sm_raw + S * SL.stage_bytes);
-  const int nchunks = (y1 - y0 + R - 1) / R;
+  // chunks start at a 4-row boundary (16-B aligned bulk copies of the int row
+  // table); rows before y0 in the first chunk are skipped
+  const int ya = y0 & ~3;
+  const int nchunks = y1 > y0 ? (y1 - ya + R - 1) / R : 0;
   const unsigned tx_bytes = static_cast<unsigned>(SL.q_bytes + R * (P + 1) * 8 + R * 4);
   const int c_inner = D == 2 ? tx * B2 : tx * B2;
   const int c_mid = D == 2 ? 0 : ty * B1;
@@ -665,12 +668,12 @@ __global__ void __launch_bounds__(256) k_decode_tma(const DecodeSweepArgs a, con
     unsigned char* base = sm_raw + st * SL.stage_bytes;
     mbar_arrive_expect_tx(&bars[st], tx_bytes);
     if (D == 2)
-      tma_load_2d(base, &map, c_inner, y0 + c * R, &bars[st]);
+      tma_load_2d(base, &map, c_inner, ya + c * R, &bars[st]);
     else
-      tma_load_3d(base, &map, c_inner, c_mid, y0 + c * R, &bars[st]);
-    bulk_load_1d(base + SL.v_off, a.v_0 + static_cast<std::int64_t>(y0 + c * R) * (P + 1), R * (P + 1) * 8,
+      tma_load_3d(base, &map, c_inner, c_mid, ya + c * R, &bars[st]);
+    bulk_load_1d(base + SL.v_off, a.v_0 + static_cast<std::int64_t>(ya + c * R) * (P + 1), R * (P + 1) * 8,
                  &bars[st]);
-    bulk_load_1d(base + SL.g_off, a.g0_0 + y0 + c * R, R * 4, &bars[st]);
+    bulk_load_1d(base + SL.g_off, a.g0_0 + ya + c * R, R * 4, &bars[st]);
   };
   if (tid == 0) {
     prefetch_tmap(&map);
@@ -736,11 +739,11 @@ __global__ void __launch_bounds__(256) k_decode_tma(const DecodeSweepArgs a, con
     sq = reinterpret_cast<const double*>(base) + tid;
     sv = reinterpret_cast<const double*>(base + SL.v_off);
     sg = reinterpret_cast<const int*>(base + SL.g_off);
-    const int yc = y0 + c * R;
+    const int yc = ya + c * R;
     jn = (y1 - yc) < R ? (y1 - yc) : R;
-    jl = 0;
+    jl = y0 > yc ? y0 - yc : 0;
     mbar_wait(&bars[st], (c / S) & 1);
-    gnext = sg[0];
+    gnext = sg[jl];
   };
   auto advance = [&]() {
     if (++jl < jn) {

@@ -1,0 +1,65 @@
+"""Sharded (multi-GPU) solve, all ranks in one process on one device with the
+loopback transport (device copies in place of NCCL, host-ordered steps): the
+per-epoch cross-rank exchange and the dp max-reduction must reproduce the
+single-device solve."""
+import numpy as np
+import pytest
+
+import paper_2210_06528_b200 as m
+from paper_2210_06528_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+CASES = [
+    ("C2s", W.scaled(W.CONFIGS["C2"], (400, 380), (20, 18)), (2, 4)),
+    ("C3s", W.scaled(W.CONFIGS["C3"], (96, 100, 104), (12, 12, 13)), (2,)),
+    ("C5s", W.scaled(W.CONFIGS["C5"], (1536, 1408), (24, 22)), (2, 3, 8)),
+]
+
+
+@pytest.mark.parametrize("name,cfg,ranks", CASES, ids=[c[0] for c in CASES])
+def test_loopback_matches_single_device(ctx, name, cfg, ranks):
+    values = W.make_field_numpy(cfg)
+    dec = m.partition(cfg.grid, cfg.bounds, cfg.blocks, cfg.degree, cfg.nctrl, cfg.overlap)
+    scfg = m.SolverConfig(max_outer_iterations=cfg.max_iters, tolerance=cfg.tolerance, log_errors=False)
+    f = m.Field(list(cfg.grid), list(cfg.bounds), values)
+    ref = m.solve(f, dec, scfg)
+    for n in ranks:
+        if n > cfg.blocks[0]:
+            continue
+        r = m.solve_loopback(f, dec, n, scfg)
+        # identical ordered sums on both ranks of every cross-rank region
+        assert np.array_equal(r.model.controls, ref.model.controls), (name, n)
+        assert r.converged == ref.converged and r.constraint_iterations == ref.constraint_iterations
+        assert [e.dp_max for e in r.epochs] == [e.dp_max for e in ref.epochs]
+        assert [(e.jump_ss, e.jump_ms) for e in r.epochs] == [(e.jump_ss, e.jump_ms) for e in ref.epochs]
+        assert [(j.block_a, j.block_b, j.linf_ss, j.linf_ms) for j in r.final_jumps] == \
+               [(j.block_a, j.block_b, j.linf_ss, j.linf_ms) for j in ref.final_jumps]
+        assert np.array_equal(r.global_error, ref.global_error)
+        # L2: per-rank partial sums combined in rank order
+        assert abs(r.global_l2 - ref.global_l2) <= 1e-12 * ref.global_l2
+        assert r.global_linf == ref.global_linf
+
+
+def test_loopback_enforce_off_and_1d(ctx):
+    # decoupled fits (no exchange epochs) still need the final cross-rank jumps
+    cfg = W.scaled(W.CONFIGS["C2"], (400, 380), (20, 18))
+    values = W.make_field_numpy(cfg)
+    dec = m.partition(cfg.grid, cfg.bounds, cfg.blocks, cfg.degree, cfg.nctrl, cfg.overlap)
+    f = m.Field(list(cfg.grid), list(cfg.bounds), values)
+    scfg = m.SolverConfig(max_outer_iterations=20, log_errors=False, enforce_continuity=False)
+    ref = m.solve(f, dec, scfg)
+    r = m.solve_loopback(f, dec, 2, scfg)
+    assert np.array_equal(r.model.controls, ref.model.controls)
+    assert [(j.linf_ss, j.linf_ms) for j in r.final_jumps] == [(j.linf_ss, j.linf_ms) for j in ref.final_jumps]
+    # 1-D, converges after one constraint iteration: final jumps from the exchange
+    cfg1 = W.CONFIGS["C1"]
+    v1 = W.make_field_numpy(cfg1)
+    dec1 = m.partition(cfg1.grid, cfg1.bounds, cfg1.blocks, cfg1.degree, cfg1.nctrl, cfg1.overlap)
+    f1 = m.Field(list(cfg1.grid), list(cfg1.bounds), v1)
+    s1 = m.SolverConfig(max_outer_iterations=20, log_errors=False)
+    ref1 = m.solve(f1, dec1, s1)
+    for n in (2, 4):
+        r1 = m.solve_loopback(f1, dec1, n, s1)
+        assert np.array_equal(r1.model.controls, ref1.model.controls)
+        assert [(j.linf_ss, j.linf_ms) for j in r1.final_jumps] == [(j.linf_ss, j.linf_ms) for j in ref1.final_jumps]
