@@ -61,6 +61,15 @@ def scaled(cfg: Config, grid, nctrl, name=None) -> Config:
                   cfg.generator, cfg.tolerance, cfg.max_iters)
 
 
+def weak(cfg: Config, n: int) -> Config:
+    """Weak scaling over n GPUs: n times the grid and the block rows along
+    axis 0 (same per-block shape), so each rank's block slab is one `cfg`."""
+    if n == 1:
+        return cfg
+    return Config(f"{cfg.name}x{n}", (cfg.grid[0] * n,) + tuple(cfg.grid[1:]), (cfg.blocks[0] * n,) + tuple(cfg.blocks[1:]),
+                  cfg.degree, cfg.nctrl, cfg.overlap, cfg.generator, cfg.tolerance, cfg.max_iters)
+
+
 def _axes(cfg: Config, xp):
     return [xp.linspace(a, b, n, dtype=xp.float64) if xp is np else
             xp.linspace(a, b, n, dtype=xp.float64, device="cuda") for (a, b), n in zip(cfg.bounds, cfg.grid)]

@@ -63,3 +63,22 @@ def test_loopback_enforce_off_and_1d(ctx):
         r1 = m.solve_loopback(f1, dec1, n, s1)
         assert np.array_equal(r1.model.controls, ref1.model.controls)
         assert [(j.linf_ss, j.linf_ms) for j in r1.final_jumps] == [(j.linf_ss, j.linf_ms) for j in ref1.final_jumps]
+
+
+def test_nccl_comm_single_rank(ctx):
+    """NCCL initialisation and the sharded constructor through the C ABI; with
+    one rank the solve must equal the plain solver."""
+    cfg = W.scaled(W.CONFIGS["C2"], (400, 380), (20, 18))
+    values = W.make_field_numpy(cfg)
+    dec = m.partition(cfg.grid, cfg.bounds, cfg.blocks, cfg.degree, cfg.nctrl, cfg.overlap)
+    scfg = m.SolverConfig(max_outer_iterations=20, log_errors=False)
+    comm = m.Comm(m.Comm.unique_id(), 0, 1, ctx)
+    try:
+        s = m.Solver(dec, scfg, ctx, comm=comm)
+        s.run(values.reshape(-1))
+        r = s.result()
+        ref = m.solve(m.Field(list(cfg.grid), list(cfg.bounds), values), dec, scfg)
+        assert np.array_equal(r.model.controls, ref.model.controls)
+        s.close()
+    finally:
+        comm.close()
