@@ -660,6 +660,10 @@ struct mfadd_solver {
   // enforce_constraints in the first exchange epoch (solver.cpp:134-141).
   std::string holder_fault;
   int max_holders = 1;
+  // log_errors: per-epoch block residuals
+  DBuf<double> res_partial, block_errs;
+  int res_ntile = 0;
+  std::vector<double> h_block_errs;
   // shard: rank of nranks owns blocks [srange.blo, srange.bhi)
   int rank = 0, nranks = 1;
   mfb::ShardRange srange;
@@ -678,6 +682,7 @@ struct mfadd_solver {
   DBuf<mfb::EpochState> est;
   cudaGraph_t loop_graph = nullptr;
   cudaGraphExec_t loop_exec = nullptr;
+  const double* loop_field = nullptr;  // field the loop graph's residual kernels read (log_errors)
   // whole-solve graph (profiling off), keyed by the field pointer
   cudaGraphExec_t solve_exec = nullptr;
   cudaStream_t aux_stream = nullptr;  // captures conditional-node bodies
@@ -843,6 +848,36 @@ mfb::EpochRegionArgs region_args(mfadd_solver* s, int mode) {
   return a;
 }
 
+mfb::BlockResArgs res_args(mfadd_solver* s, const double* dfield, const mfb::EpochState* st, int slot) {
+  mfb::BlockResArgs a{};
+  a.D = s->dec.rank;
+  a.nblocks = static_cast<int>(s->wl.blocks.size());
+  a.blocks = s->wl.d_blocks.p;
+  a.probs = s->wl.d_probs.p;
+  a.g0 = s->wl.g0.p;
+  a.vals = s->wl.vals.p;
+  a.P = s->wl.P.p;
+  a.field = dfield;
+  for (int k = 0; k < 3; ++k) a.fs[k] = s->wl.fs[k];
+  a.ntile = s->res_ntile;
+  a.partial = s->res_partial.p;
+  a.errs = s->block_errs.p;
+  a.st = st;
+  a.slot = slot;
+  a.nglobal = s->dec.nblocks;
+  a.boff = s->srange.blo;
+  return a;
+}
+
+// record_epoch's block residuals (solver.cpp:357-364) when log_errors.
+int launch_residuals(mfadd_solver* s, const double* dfield, const mfb::EpochState* st, int slot, cudaStream_t cs) {
+  if (!s->cfg.log_errors) return 0;
+  s->tl.begin("residual");
+  const int l = mfb::launch_block_residual(s->wl.p, res_args(s, dfield, st, slot), cs);
+  s->tl.end();
+  return l;
+}
+
 // Shared controls as regions (mfb::enumerate_regions), each cut into tiles of
 // at most kTile controls.  Regions whose holders are all local become local
 // tiles; on a sharded solver, regions that also have holders on other ranks
@@ -965,7 +1000,16 @@ void build_regions(mfadd_solver* s, const std::vector<int>& pair_slot) {
 // The epoch loop (solver.cpp:394-413) as a CUDA graph: a conditional WHILE
 // node whose body is one region-form epoch; the epoch's last CTA computes dp
 // and sets the condition, so the loop runs with no host round trips.
-void build_loop_graph(mfadd_solver* s) {
+void build_loop_graph(mfadd_solver* s, const double* dfield) {
+  if (s->loop_exec) {
+    CK(cudaGraphExecDestroy(s->loop_exec));
+    s->loop_exec = nullptr;
+  }
+  if (s->loop_graph) {
+    CK(cudaGraphDestroy(s->loop_graph));
+    s->loop_graph = nullptr;
+  }
+  s->loop_field = dfield;
   CK(cudaGraphCreate(&s->loop_graph, 0));
   cudaGraphConditionalHandle h;
   CK(cudaGraphConditionalHandleCreate(&h, s->loop_graph, 1, cudaGraphCondAssignDefault));
@@ -982,13 +1026,14 @@ void build_loop_graph(mfadd_solver* s) {
   mfb::EpochRegionArgs a = region_args(s, -1);
   a.cond = static_cast<unsigned long long>(h);
   mfb::launch_epoch_regions(a, cs);
+  if (s->cfg.log_errors) mfb::launch_block_residual(s->wl.p, res_args(s, dfield, s->est.p, 0), cs);
   CK(cudaStreamEndCapture(cs, &body));
   CK(cudaGraphInstantiate(&s->loop_exec, s->loop_graph, 0));
 }
 
 // The epoch loop as a conditional WHILE node appended to the graph being
 // captured on `st` (whole-solve graph).
-void add_loop_node(mfadd_solver* s, cudaStream_t st) {
+void add_loop_node(mfadd_solver* s, cudaStream_t st, const double* dfield) {
   cudaStreamCaptureStatus cs;
   cudaGraph_t g = nullptr;
   const cudaGraphNode_t* deps = nullptr;
@@ -1009,6 +1054,7 @@ void add_loop_node(mfadd_solver* s, cudaStream_t st) {
   mfb::EpochRegionArgs a = region_args(s, -1);
   a.cond = static_cast<unsigned long long>(h);
   mfb::launch_epoch_regions(a, bs);
+  if (s->cfg.log_errors) mfb::launch_block_residual(s->wl.p, res_args(s, dfield, s->est.p, 0), bs);
   CK(cudaStreamEndCapture(bs, &body));
   CK(cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies));
 }
@@ -1272,12 +1318,24 @@ std::unique_ptr<mfadd_solver> create_solver(mfadd_context* ctx, const mfadd_deco
       if (s->max_holders > 8)
         throw std::invalid_argument("mfadd_b200: a sharded solve needs at most two holders per axis");
     }
-    if (nranks == 1 && s->ntiles > 0 && cfg->enforce_continuity) build_loop_graph(s.get());
+    if (nranks == 1 && s->ntiles > 0 && cfg->enforce_continuity) build_loop_graph(s.get(), nullptr);
     s->hres_eo = 4;
     s->hres_es = s->hres_eo + s->epoch_out.n;
     s->hres_pj = s->hres_es + (sizeof(mfb::EpochState) + 7) / 8;
     s->hres_n = s->hres_pj + s->pair_jumps.n;
     CK(cudaMallocHost(&s->hres, s->hres_n * sizeof(double)));
+    if (cfg->log_errors) {
+      int mx = 1;
+      for (const auto& b : wl.blocks) {
+        const int m0 = wl.probs[static_cast<std::size_t>(b.ax[0])].m;
+        int tr = 1;
+        for (int k = 1; k < D; ++k) tr *= wl.probs[static_cast<std::size_t>(b.ax[k])].m;
+        mx = std::max(mx, D == 1 ? m0 : tr);
+      }
+      s->res_ntile = std::min(4096, (mx + 127) / 128);
+      s->res_partial.alloc(wl.blocks.size() * static_cast<std::size_t>(s->res_ntile) * 2);
+      s->block_errs.alloc(static_cast<std::size_t>(cfg->max_outer_iterations + 1) * d.nblocks * 2);
+    }
     CK(cudaStreamSynchronize(st));
     return s;
 }
@@ -1502,15 +1560,18 @@ int enqueue_solve(mfadd_solver* s, const double* dfield) {
   } else {
     launches += run_epoch(s, 0, 0);
   }
+  launches += launch_residuals(s, dfield, nullptr, 0, st);  // record_epoch(0, ...) block errors
   // ---- outer iterations (solver.cpp:394-413), entirely on the device
   if (loop) {
     s->tl.begin("epoch");
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     CK(cudaStreamIsCapturing(st, &cs));
     if (cs == cudaStreamCaptureStatusActive)
-      add_loop_node(s, st);
-    else
+      add_loop_node(s, st, dfield);
+    else {
+      if (!s->loop_exec || (s->cfg.log_errors && s->loop_field != dfield)) build_loop_graph(s, dfield);
       CK(cudaGraphLaunch(s->loop_exec, st));
+    }
     s->tl.end();
   }
   CK(cudaEventRecord(s->ev[3], st));
@@ -1600,6 +1661,11 @@ void finish_solve(mfadd_solver* s, int launches) {
   }
   sum.n_epochs = static_cast<int>(s->epochs.size());
   sum.n_final_jumps = s->npairs;
+  if (s->cfg.log_errors) {
+    s->h_block_errs.resize(static_cast<std::size_t>(sum.n_epochs) * d.nblocks * 2);
+    CK(cudaMemcpy(s->h_block_errs.data(), s->block_errs.p, s->h_block_errs.size() * sizeof(double),
+                  cudaMemcpyDeviceToHost));
+  }
   sum.t_setup = ev_ms(s->ev[0], s->ev[1]) * 1e-3;
   sum.t_local_solve = ev_ms(s->ev[1], s->ev[2]) * 1e-3;
   sum.t_exchange = 0.0;  // single device: the exchange is fused into K4
@@ -1622,6 +1688,9 @@ struct Transport {
   virtual void exchange(std::vector<mfadd_solver*>& g) = 0;               // send -> recv buffers
   virtual void max_u64(std::vector<mfadd_solver*>& g, std::size_t off, std::size_t n, bool pairs) = 0;
   virtual void gather_lattice(std::vector<mfadd_solver*>& g) = 0;         // owned rows to every rank
+  // elementwise sum of a device array that every rank filled at its own entries
+  using ArrayOf = std::pair<double*, std::size_t> (*)(mfadd_solver*);
+  virtual void sum_f64(std::vector<mfadd_solver*>& g, ArrayOf arr) = 0;
   // red2: sum l2^2 over ranks (each decoded its own rows), or max when every
   // rank decoded all rows (generic decode path: identical values), max linf
   virtual void reduce_err(std::vector<mfadd_solver*>& g, bool sum_l2) = 0;
@@ -1649,6 +1718,10 @@ struct NcclTransport : Transport {
     mfadd_solver* s = g[0];
     auto* p = pairs ? s->pair_jumps.p + off : reinterpret_cast<unsigned long long*>(s->epoch_out.p + off);
     NCK(ncclAllReduce(p, p, n, ncclUint64, ncclMax, s->comm->comm, s->ctx->stream));
+  }
+  void sum_f64(std::vector<mfadd_solver*>& g, ArrayOf arr) override {
+    const auto a = arr(g[0]);
+    NCK(ncclAllReduce(a.first, a.first, a.second, ncclFloat64, ncclSum, g[0]->comm->comm, g[0]->ctx->stream));
   }
   void gather_lattice(std::vector<mfadd_solver*>& g) override {
     mfadd_solver* s = g[0];
@@ -1702,6 +1775,15 @@ struct LoopbackTransport : Transport {
       CK(cudaMemcpyAsync(p, acc.data(), n * 8, cudaMemcpyHostToDevice, s->ctx->stream));
       CK(cudaStreamSynchronize(s->ctx->stream));
     }
+  }
+  void sum_f64(std::vector<mfadd_solver*>& g, ArrayOf arr) override {
+    const std::size_t n = arr(g[0]).second;
+    std::vector<double> acc(n, 0.0), v(n);
+    for (mfadd_solver* s : g) {  // rank order
+      CK(cudaMemcpy(v.data(), arr(s).first, n * sizeof(double), cudaMemcpyDeviceToHost));
+      for (std::size_t i = 0; i < n; ++i) acc[i] += v[i];
+    }
+    for (mfadd_solver* s : g) CK(cudaMemcpy(arr(s).first, acc.data(), n * sizeof(double), cudaMemcpyHostToDevice));
   }
   void gather_lattice(std::vector<mfadd_solver*>& g) override {
     const Decomp& d = g[0]->dec;
@@ -1818,9 +1900,15 @@ void solve_group(std::vector<mfadd_solver*>& g, const std::vector<const double*>
   auto epoch = [&](int mode, int slot) {
     for (std::size_t r = 0; r < g.size(); ++r) launches[r] += shard_pack(g[r]);
     tr.exchange(g);
-    for (std::size_t r = 0; r < g.size(); ++r) launches[r] += shard_compute(g[r], mode, slot);
+    for (std::size_t r = 0; r < g.size(); ++r) {
+      launches[r] += shard_compute(g[r], mode, slot);
+      launches[r] += launch_residuals(g[r], fields[r], nullptr, slot, g[r]->ctx->stream);
+    }
     tr.max_u64(g, static_cast<std::size_t>(3 * slot), 3, false);
   };
+  if (s0->cfg.log_errors)
+    for (mfadd_solver* s : g)
+      CK(cudaMemsetAsync(s->block_errs.p, 0, s->block_errs.n * sizeof(double), s->ctx->stream));
   tmark("fit done", 0);
   epoch(0, 0);  // record_epoch(0, 0.0)
   tmark("epoch", 0);
@@ -1855,6 +1943,7 @@ void solve_group(std::vector<mfadd_solver*>& g, const std::vector<const double*>
   tmark("assembled", 0);
   for (std::size_t r = 0; r < g.size(); ++r) launches[r] += shard_decode(g[r], fields[r]);
   tr.reduce_err(g, s0->tma_decode);
+  if (s0->cfg.log_errors) tr.sum_f64(g, [](mfadd_solver* s) { return std::make_pair(s->block_errs.p, s->block_errs.n); });
   tmark("decoded", 0);
   // results (identical on every rank after the reductions)
   for (std::size_t r = 0; r < g.size(); ++r) {
@@ -2018,11 +2107,14 @@ MFB_API int mfadd_solver_block_controls(const mfadd_solver* s, int block, double
 }
 
 MFB_API int mfadd_solver_block_errors(const mfadd_solver* s, int epoch, double* out2) {
-  (void)s;
-  (void)epoch;
-  (void)out2;
-  g_err = "mfadd_solver_block_errors: log_errors is not implemented in this build";
-  return MFADD_EINVAL;
+  return guarded([&] {
+    if (!s->have_result) throw std::logic_error("mfadd_solver_block_errors: no solve result");
+    if (!s->cfg.log_errors) throw std::invalid_argument("mfadd_solver_block_errors: solver built without log_errors");
+    const int nb = s->dec.nblocks;
+    if (epoch < 0 || static_cast<std::size_t>(epoch + 1) * nb * 2 > s->h_block_errs.size())
+      throw std::out_of_range("mfadd_solver_block_errors: epoch");
+    std::memcpy(out2, s->h_block_errs.data() + static_cast<std::size_t>(epoch) * nb * 2, nb * 2 * sizeof(double));
+  });
 }
 
 MFB_API const double* mfadd_solver_device_controls(const mfadd_solver* s) { return s->lattice.p; }

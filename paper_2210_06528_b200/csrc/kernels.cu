@@ -1094,6 +1094,140 @@ __global__ void __launch_bounds__(kRegionThreads) k_pair_jumps_regions(EpochRegi
   }
 }
 
+// ------------------------------------------------------------------- K9
+// residual_error (lsq.cpp:66-85) per local block: decode the block's held
+// lattice P_b with its own (window-clipped) collocation rows at every point of
+// its input box.  One thread per trailing point (j1[, j2]) sweeps axis 0 with a
+// window of P+1 trailing-contracted control planes (D = 1: thread per row).
+// Out-of-window basis values are zero in the row tables; their column indices
+// are clamped so every lattice read stays inside P_b.
+constexpr int kResThreads = 128;
+
+template <int P>
+__global__ void __launch_bounds__(kResThreads) k_block_residual(BlockResArgs a) {
+  __shared__ double s_red[2][kResThreads / 32];
+  const int b = blockIdx.y;
+  const BlockDev& blk = a.blocks[b];
+  const int D = a.D;
+  const AxisProb p0 = a.probs[blk.ax[0]];
+  const int m0 = p0.m, n0 = p0.n;
+  const int* g00 = a.g0 + p0.row_off;
+  const double* v00 = a.vals + p0.row_off * (P + 1);
+  const double* Pb = a.P + blk.poff;
+  double l2 = 0.0, li = 0.0;
+  auto clampi = [](int i, int n) { return i < 0 ? 0 : (i >= n ? n - 1 : i); };
+  if (D == 1) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m0; j += gridDim.x * blockDim.x) {
+      const int g = __ldg(g00 + j);
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k <= P; ++k) s = fma(__ldg(v00 + j * (P + 1) + k), Pb[clampi(g + k, n0)], s);
+      const double e = a.field[blk.fbase + j * a.fs[0]] - s;
+      l2 = fma(e, e, l2);
+      li = fmax(li, fabs(e));
+    }
+  } else {
+    const AxisProb p1 = a.probs[blk.ax[1]];
+    const AxisProb p2 = D == 3 ? a.probs[blk.ax[2]] : p1;
+    const int m1 = p1.m, n1 = p1.n, m2 = D == 3 ? p2.m : 1, n2 = D == 3 ? p2.n : 1;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < m1 * m2) {
+      const int j1 = D == 3 ? t / m2 : t, j2 = D == 3 ? t - (t / m2) * m2 : 0;
+      double w1[P + 1], w2[P + 1];
+      const int g1 = __ldg(a.g0 + p1.row_off + j1);
+      const int g2 = D == 3 ? __ldg(a.g0 + p2.row_off + j2) : 0;
+#pragma unroll
+      for (int k = 0; k <= P; ++k) {
+        w1[k] = __ldg(a.vals + (p1.row_off + j1) * (P + 1) + k);
+        w2[k] = D == 3 ? __ldg(a.vals + (p2.row_off + j2) * (P + 1) + k) : 0.0;
+      }
+      const std::int64_t plane_sz = static_cast<std::int64_t>(n1) * n2;
+      auto plane = [&](int ai) -> double {  // trailing contraction of held plane ai
+        const double* L0 = Pb + static_cast<std::int64_t>(clampi(ai, n0)) * plane_sz;
+        double s = 0.0;
+#pragma unroll
+        for (int k1 = 0; k1 <= P; ++k1) {
+          const std::int64_t r1 = static_cast<std::int64_t>(clampi(g1 + k1, n1)) * n2;
+          if (D == 2) {
+            s = fma(w1[k1], L0[r1], s);
+          } else {
+            double r = 0.0;
+#pragma unroll
+            for (int k2 = 0; k2 <= P; ++k2) r = fma(w2[k2], L0[r1 + clampi(g2 + k2, n2)], r);
+            s = fma(w1[k1], r, s);
+          }
+        }
+        return s;
+      };
+      int abase = __ldg(g00);
+      double Tw[P + 1];
+#pragma unroll
+      for (int k = 0; k <= P; ++k) Tw[k] = plane(abase + k);
+      const double* q = a.field + blk.fbase + j1 * a.fs[1] + (D == 3 ? j2 * a.fs[2] : 0);
+      for (int j = 0; j < m0; ++j) {
+        const int g = __ldg(g00 + j);
+        while (abase < g) {
+#pragma unroll
+          for (int k = 0; k < P; ++k) Tw[k] = Tw[k + 1];
+          ++abase;
+          Tw[P] = plane(abase + P);
+        }
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k <= P; ++k) s = fma(__ldg(v00 + j * (P + 1) + k), Tw[k], s);
+        const double e = q[static_cast<std::int64_t>(j) * a.fs[0]] - s;
+        l2 = fma(e, e, l2);
+        li = fmax(li, fabs(e));
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    l2 += __shfl_xor_sync(kFull, l2, o);
+    li = fmax(li, __shfl_xor_sync(kFull, li, o));
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    s_red[0][w] = l2;
+    s_red[1][w] = li;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sl = 0.0, sm = 0.0;
+    for (int i = 0; i < kResThreads / 32; ++i) {
+      sl += s_red[0][i];
+      sm = fmax(sm, s_red[1][i]);
+    }
+    a.partial[2 * (static_cast<std::int64_t>(b) * a.ntile + blockIdx.x)] = sl;
+    a.partial[2 * (static_cast<std::int64_t>(b) * a.ntile + blockIdx.x) + 1] = sm;
+  }
+}
+
+// Fixed-order reduction of the per-tile partials: errs[slot][b] = {sqrt(sum), max}.
+__global__ void k_block_residual_reduce(BlockResArgs a) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= a.nblocks) return;
+  const int slot = a.st ? a.st->iter : a.slot;
+  double sl = 0.0, sm = 0.0;
+  for (int t = 0; t < a.ntile; ++t) {
+    sl += a.partial[2 * (static_cast<std::int64_t>(b) * a.ntile + t)];
+    sm = fmax(sm, a.partial[2 * (static_cast<std::int64_t>(b) * a.ntile + t) + 1]);
+  }
+  const std::int64_t o = 2 * (static_cast<std::int64_t>(slot) * a.nglobal + a.boff + b);
+  a.errs[o] = sqrt(sl);
+  a.errs[o + 1] = sm;
+}
+
+template <int P>
+struct BlockResLaunch {
+  static int run(const BlockResArgs& a, cudaStream_t s) {
+    dim3 grid(a.ntile, a.nblocks);
+    k_block_residual<P><<<grid, kResThreads, 0, s>>>(a);
+    k_block_residual_reduce<<<(a.nblocks + 127) / 128, 128, 0, s>>>(a);
+    return 2;
+  }
+};
+
 // ------------------------------------------------------------------- K5
 __global__ void __launch_bounds__(1024) k_dp(DpArgs a) {
   __shared__ unsigned long long red[32];
@@ -1392,6 +1526,10 @@ int debug_fail_line() {
 
 int launch_basis_rows(int degree, const RowsArgs& a, cudaStream_t s) {
   return dispatch_degree<RowsLaunch>(degree, a, s);
+}
+int launch_block_residual(int degree, const BlockResArgs& a, cudaStream_t s) {
+  if (a.nblocks <= 0) return 0;
+  return dispatch_degree<BlockResLaunch>(degree, a, s);
 }
 int launch_gram_chol(int degree, const CholArgs& a, cudaStream_t s) {
   return dispatch_degree<CholLaunch>(degree, a, s);

@@ -136,6 +136,27 @@ int launch_epoch_finalize(const EpochRegionArgs& a, cudaStream_t s);
 // Sharded solve: gather holder copies into the send buffer.
 int launch_pack(const PackTile* tiles, int ntiles, const double* P, double* send, cudaStream_t s);
 
+// K9 (log_errors): residual_error (lsq.cpp:66-85) of every local block's held
+// lattice over its input box, per epoch (record_epoch, solver.cpp:357-364).
+struct BlockResArgs {
+  int D;
+  int nblocks;                 // local blocks (grid.y)
+  const BlockDev* blocks;
+  const AxisProb* probs;
+  const int* g0;
+  const double* vals;
+  const double* P;
+  const double* field;
+  std::int64_t fs[3];
+  int ntile;                   // CTAs per block (grid.x)
+  double* partial;             // [nblocks][ntile] x {l2^2, linf}
+  double* errs;                // [(max_iter + 1)][nglobal] x {l2, linf}
+  const EpochState* st;        // slot = st->iter (the epoch just recorded), or `slot` when null
+  int slot;
+  int nglobal, boff;           // all blocks; global id of local block 0
+};
+int launch_block_residual(int degree, const BlockResArgs& a, cudaStream_t s);
+
 // K5: dp = max_b change_b / max(1, ||P_b||_inf) and epoch bookkeeping.
 struct DpArgs {
   int nblocks;

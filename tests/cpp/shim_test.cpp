@@ -80,6 +80,11 @@ static void gpu_cases() {
   }
   EXPECT(r.global_linf > 0.0 && li == r.global_linf);
   EXPECT(std::fabs(std::sqrt(l2) - r.global_l2) <= 1e-12 * r.global_l2);
+  // the reference defaults (log_errors = true): per-epoch block residuals
+  const auto rl = mfadd::solve(f, dec, mfadd::SolverConfig{});
+  EXPECT(rl.epochs.size() == r.epochs.size() && rl.epochs[0].block_errors.size() == 4);
+  EXPECT(rl.epochs.back().block_errors[0][0] > 0.0 && rl.epochs.back().block_errors[0][1] > 0.0);
+  EXPECT(rl.model.controls.values() == r.model.controls.values());
   // the error field is q - decode(controls) at the grid params
   std::vector<std::vector<double>> u(2);
   for (int d = 0; d < 2; ++d)

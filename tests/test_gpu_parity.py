@@ -400,3 +400,26 @@ def test_graph_replay_matches_direct(ctx, monkeypatch):
         assert np.array_equal(r.global_error, res[0].global_error)
         assert [e.dp_max for e in r.epochs] == [e.dp_max for e in res[0].epochs]
         assert r.global_l2 == res[0].global_l2 and r.constraint_iterations == res[0].constraint_iterations
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3s"])
+def test_log_errors_block_residuals(ctx, name):
+    """record_epoch with log_errors (solver.cpp:357-364): residual_error
+    (lsq.cpp:66-85) of every block's held lattice over its input box, each
+    epoch, vs the reference."""
+    cfg = SMALL[name]
+    values = W.make_field_numpy(cfg)
+    dec = m.partition(cfg.grid, cfg.bounds, cfg.blocks, cfg.degree, cfg.nctrl, cfg.overlap)
+    scfg = m.SolverConfig(max_outer_iterations=20, log_errors=True)
+    r = m.solve(m.Field(list(cfg.grid), list(cfg.bounds), values), dec, scfg)
+    o = orc.solve(orc.Decomposition(cfg.grid, cfg.blocks, cfg.degree, cfg.nctrl, cfg.overlap), values, 20, 1e-10,
+                  log_errors=True)
+    assert len(r.epochs) == len(o.block_errors)
+    for e, ob in zip(r.epochs, o.block_errors):
+        got = np.array(e.block_errors)
+        ref = np.asarray(ob).reshape(got.shape)
+        assert np.all(np.abs(got - ref) <= 1e-10 * np.maximum(1.0, np.abs(ref))), (name, e.iteration)
+    # the solve itself is unchanged by logging
+    r2 = m.solve(m.Field(list(cfg.grid), list(cfg.bounds), values), dec,
+                 m.SolverConfig(max_outer_iterations=20, log_errors=False))
+    assert np.array_equal(r.model.controls, r2.model.controls)
