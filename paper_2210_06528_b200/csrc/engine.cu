@@ -1977,6 +1977,14 @@ void solve_impl(mfadd_solver* s, const double* dfield) {
     solve_group(g, {dfield}, tr);
     return;
   }
+  static const bool host_loop = std::getenv("MFADD_HOST_LOOP") != nullptr;
+  if (host_loop && s->holder_fault.empty() && (s->ntiles > 0 || !s->dec.any_shared)) {
+    // profiling aid: every kernel as a direct launch (host-driven epoch loop)
+    std::vector<mfadd_solver*> g{s};
+    LoopbackTransport tr;
+    solve_group(g, {dfield}, tr);
+    return;
+  }
   const bool graphable = !s->tl.on && !s->tl.sync_check && s->holder_fault.empty() && !std::getenv("MFADD_NO_GRAPH");
   if (!graphable) {
     finish_solve(s, enqueue_solve(s, dfield));
