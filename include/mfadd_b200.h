@@ -121,6 +121,15 @@ int mfadd_solve(mfadd_solver* s, const double* field, int field_on_device, mfadd
 int mfadd_solve_host(mfadd_solver* s, const double* field_host, double* out_controls_host,
                      double* out_error_host /* nullable */, mfadd_solve_summary* out);
 
+/* A stream of n independent solves with host buffers (e.g. the time steps of
+ * a simulation): the H2D copy of field i+1 and the D2H copies of solve i's
+ * lattice / error field overlap with the solves (separate copy streams, two
+ * device slots).  Per step the copies equal mfadd_solve_host's.  out: n
+ * summaries (nullable); the getters below then describe the last solve. */
+int mfadd_solve_host_batch(mfadd_solver* s, int n, const double* const* fields_host,
+                           double* const* out_controls_host, double* const* out_errors_host /* nullable */,
+                           mfadd_solve_summary* out /* nullable */);
+
 /* Results of the last solve (SolveResult members, solver.hpp:56-68). */
 int mfadd_solver_epochs(const mfadd_solver* s, mfadd_epoch_stats* out, int cap);
 /* InterfaceJump list (solver.hpp:34-38): block_a, block_b, linf_ss, linf_ms */

@@ -64,6 +64,8 @@ _SIGS = {
     "mfadd_solver_free": (None, [C.c_void_p]),
     "mfadd_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(SolveSummaryC)]),
     "mfadd_solve_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(SolveSummaryC)]),
+    "mfadd_solve_host_batch": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                         C.POINTER(SolveSummaryC)]),
     "mfadd_solver_epochs": (C.c_int, [C.c_void_p, C.POINTER(EpochStatsC), C.c_int]),
     "mfadd_solver_final_jumps": (C.c_int, [C.c_void_p, c_dp, C.c_int]),
     "mfadd_solver_controls": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),

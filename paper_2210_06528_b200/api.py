@@ -696,6 +696,20 @@ class Solver:
             C.byref(self.summary)))
         return self.summary
 
+    def run_host_batch(self, fields, out_controls, out_errors=None):
+        """mfadd_solve_host_batch: a stream of solves on host buffers with the
+        copies of neighbouring steps overlapped.  Returns the n summaries."""
+        def ptr(a):
+            return a.ctypes.data if isinstance(a, np.ndarray) else a.data_ptr()
+        n = len(fields)
+        fp = (C.c_void_p * n)(*[ptr(f) for f in fields])
+        cp = (C.c_void_p * n)(*[ptr(o) for o in out_controls])
+        ep = None if out_errors is None else (C.c_void_p * n)(*[ptr(o) for o in out_errors])
+        sums = (L.SolveSummaryC * n)()
+        _check(L.load().mfadd_solve_host_batch(self._h, n, fp, cp, ep, sums))
+        self.summary = sums[n - 1]
+        return list(sums)
+
     def set_profiling(self, on: bool = True):
         _check(L.load().mfadd_solver_set_profiling(self._h, int(on)))
 

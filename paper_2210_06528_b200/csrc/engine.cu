@@ -115,6 +115,10 @@ struct DBuf {
     alloc(h.size());
     if (!h.empty()) CK(cudaMemcpyAsync(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, s));
   }
+  void swap(DBuf& o) {
+    std::swap(p, o.p);
+    std::swap(n, o.n);
+  }
 };
 
 // Host binary search with the find_span rule (knots.cpp:83-106) — used only
@@ -683,12 +687,20 @@ struct mfadd_solver {
   cudaGraph_t loop_graph = nullptr;
   cudaGraphExec_t loop_exec = nullptr;
   const double* loop_field = nullptr;  // field the loop graph's residual kernels read (log_errors)
-  // whole-solve graph (profiling off), keyed by the field pointer
-  cudaGraphExec_t solve_exec = nullptr;
+  // whole-solve graphs keyed by (field buffer, output slot): the first solve of
+  // a key runs direct launches (one-time attribute setup), the second captures
+  struct SolveGraph {
+    const double* field = nullptr;
+    const double* lattice = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    int launches = 0;
+  };
+  std::vector<SolveGraph> graphs;
   cudaStream_t aux_stream = nullptr;  // captures conditional-node bodies
-  const double* solve_field = nullptr;
-  const double* direct_field = nullptr;
-  int solve_launches = 0;
+  // mfadd_solve_host_batch: second field / output slot, copy streams, events
+  DBuf<double> field_buf2, lattice_alt, error_alt;
+  cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
+  cudaEvent_t bev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // h2d[2], comp[2], d2h[2]
   // pinned result block: red2[2] | DevStatus | epoch_out | EpochState | pair_jumps
   double* hres = nullptr;
   std::size_t hres_eo = 0, hres_es = 0, hres_pj = 0, hres_n = 0;
@@ -704,12 +716,17 @@ struct mfadd_solver {
 
   ~mfadd_solver() {
     // graphs first: the solve graph holds event-record nodes on ev[]
-    if (solve_exec) cudaGraphExecDestroy(solve_exec);
+    for (auto& gr : graphs)
+      if (gr.exec) cudaGraphExecDestroy(gr.exec);
     if (loop_exec) cudaGraphExecDestroy(loop_exec);
     if (loop_graph) cudaGraphDestroy(loop_graph);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
+    for (auto& e : bev)
+      if (e) cudaEventDestroy(e);
     if (aux_stream) cudaStreamDestroy(aux_stream);
+    if (h2d_stream) cudaStreamDestroy(h2d_stream);
+    if (d2h_stream) cudaStreamDestroy(d2h_stream);
     if (hres) cudaFreeHost(hres);
   }
 };
@@ -1967,6 +1984,45 @@ void solve_group(std::vector<mfadd_solver*>& g, const std::vector<const double*>
   }
 }
 
+// Enqueue one solve on the context stream without waiting: replay the cached
+// whole-solve graph of (field, output slot) when possible (no per-kernel
+// profiling, no debug sync checks, no holder fault), else direct launches.
+int enqueue_cached(mfadd_solver* s, const double* dfield) {
+  const bool graphable = !s->tl.on && !s->tl.sync_check && s->holder_fault.empty() && !std::getenv("MFADD_NO_GRAPH");
+  if (!graphable) return enqueue_solve(s, dfield);
+  cudaStream_t st = s->ctx->stream;
+  mfadd_solver::SolveGraph* gr = nullptr;
+  for (auto& e : s->graphs)
+    if (e.field == dfield && e.lattice == s->lattice.p) gr = &e;
+  if (!gr) {  // first solve of this key: direct launches (one-time attribute setup outside capture)
+    if (s->graphs.size() >= 4) {
+      if (s->graphs.front().exec) CK(cudaGraphExecDestroy(s->graphs.front().exec));
+      s->graphs.erase(s->graphs.begin());
+    }
+    s->graphs.push_back({dfield, s->lattice.p, nullptr, 0});
+    return enqueue_solve(s, dfield);
+  }
+  if (!gr->exec) {
+    cudaGraph_t g = nullptr;
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+    int launches = 0;
+    try {
+      launches = enqueue_solve(s, dfield);
+    } catch (...) {
+      cudaStreamEndCapture(st, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    CK(cudaStreamEndCapture(st, &g));
+    const cudaError_t e = cudaGraphInstantiate(&gr->exec, g, 0);
+    cudaGraphDestroy(g);
+    CK(e);
+    gr->launches = launches;
+  }
+  CK(cudaGraphLaunch(gr->exec, st));
+  return gr->launches;
+}
+
 // solve(): replay the cached whole-solve graph when possible (no per-kernel
 // profiling, no debug sync checks, no holder fault), else launch directly.
 void solve_impl(mfadd_solver* s, const double* dfield) {
@@ -1985,43 +2041,7 @@ void solve_impl(mfadd_solver* s, const double* dfield) {
     solve_group(g, {dfield}, tr);
     return;
   }
-  const bool graphable = !s->tl.on && !s->tl.sync_check && s->holder_fault.empty() && !std::getenv("MFADD_NO_GRAPH");
-  if (!graphable) {
-    finish_solve(s, enqueue_solve(s, dfield));
-    return;
-  }
-  cudaStream_t st = s->ctx->stream;
-  if (!s->solve_exec || s->solve_field != dfield) {
-    if (s->solve_exec) {
-      CK(cudaGraphExecDestroy(s->solve_exec));
-      s->solve_exec = nullptr;
-    }
-    if (s->direct_field != dfield) {
-      // first solve on this field pointer: direct launches (also performs every
-      // one-time function attribute setup outside of capture)
-      s->direct_field = dfield;
-      finish_solve(s, enqueue_solve(s, dfield));
-      return;
-    }
-    cudaGraph_t g = nullptr;
-    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
-    int launches = 0;
-    try {
-      launches = enqueue_solve(s, dfield);
-    } catch (...) {
-      cudaStreamEndCapture(st, &g);
-      if (g) cudaGraphDestroy(g);
-      throw;
-    }
-    CK(cudaStreamEndCapture(st, &g));
-    const cudaError_t e = cudaGraphInstantiate(&s->solve_exec, g, 0);
-    cudaGraphDestroy(g);
-    CK(e);
-    s->solve_field = dfield;
-    s->solve_launches = launches;
-  }
-  CK(cudaGraphLaunch(s->solve_exec, st));
-  finish_solve(s, s->solve_launches);
+  finish_solve(s, enqueue_cached(s, dfield));
 }
 
 }  // namespace
@@ -2060,6 +2080,98 @@ MFB_API int mfadd_solve_host(mfadd_solver* s, const double* field_host, double* 
       CK(cudaMemcpyAsync(out_error_host, s->error.p, s->error.n * sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     if (out) *out = s->summary;
+  });
+}
+
+// A stream of independent solves (e.g. the time steps of a simulation) with
+// host buffers: field i+1 is copied in while solve i computes and while the
+// results of solve i are copied out (separate H2D / D2H streams, two device
+// field and output slots).  Per step the copies are exactly those of
+// mfadd_solve_host; only their overlap differs.
+MFB_API int mfadd_solve_host_batch(mfadd_solver* s, int n, const double* const* fields_host,
+                                   double* const* out_controls_host, double* const* out_errors_host,
+                                   mfadd_solve_summary* out) {
+  return guarded([&] {
+    ContextScope scope(s->ctx);
+    check_config(s->cfg);
+    const std::size_t nf = static_cast<std::size_t>(s->dec.total_inputs());
+    if (n <= 0) return;
+    for (int i = 0; i < n; ++i)
+      if (out_errors_host && out_errors_host[i] && !s->cfg.store_error)
+        throw std::invalid_argument("mfadd_solve_host_batch: out_errors requires store_error in the solver config");
+    if (s->nranks > 1 || s->tl.on || s->tl.sync_check) {  // no overlap: one call per step
+      for (int i = 0; i < n; ++i) {
+        if (s->field_buf.n != nf) s->field_buf.alloc(nf);
+        CK(cudaMemcpyAsync(s->field_buf.p, fields_host[i], nf * sizeof(double), cudaMemcpyHostToDevice,
+                           s->ctx->stream));
+        solve_impl(s, s->field_buf.p);
+        if (out_controls_host && out_controls_host[i])
+          CK(cudaMemcpy(out_controls_host[i], s->lattice.p, s->lattice.n * sizeof(double), cudaMemcpyDeviceToHost));
+        if (out_errors_host && out_errors_host[i])
+          CK(cudaMemcpy(out_errors_host[i], s->error.p, s->error.n * sizeof(double), cudaMemcpyDeviceToHost));
+        if (out) out[i] = s->summary;
+      }
+      return;
+    }
+    // one-time resources
+    if (s->field_buf.n != nf) s->field_buf.alloc(nf);
+    if (s->field_buf2.n != nf) s->field_buf2.alloc(nf);
+    if (s->lattice_alt.n != s->lattice.n) s->lattice_alt.alloc(s->lattice.n);
+    if (s->cfg.store_error && s->error_alt.n != s->error.n) s->error_alt.alloc(s->error.n);
+    if (!s->h2d_stream) CK(cudaStreamCreateWithFlags(&s->h2d_stream, cudaStreamNonBlocking));
+    if (!s->d2h_stream) CK(cudaStreamCreateWithFlags(&s->d2h_stream, cudaStreamNonBlocking));
+    for (auto& e : s->bev)
+      if (!e) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    cudaEvent_t* ev_h2d = s->bev;
+    cudaEvent_t* ev_comp = s->bev + 2;
+    cudaEvent_t* ev_d2h = s->bev + 4;
+    cudaStream_t cs = s->ctx->stream;
+    double* fbuf[2] = {s->field_buf.p, s->field_buf2.p};
+    int cur_slot = 0;  // which output buffers s->lattice / s->error hold
+    auto use_slot = [&](int slot) {
+      if (slot != cur_slot) {
+        s->lattice.swap(s->lattice_alt);
+        if (s->cfg.store_error) s->error.swap(s->error_alt);
+        cur_slot = slot;
+      }
+    };
+    auto h2d = [&](int i) {
+      const int slot = i & 1;
+      if (i >= 2) CK(cudaStreamWaitEvent(s->h2d_stream, ev_comp[slot], 0));  // solve i-2 done reading
+      CK(cudaMemcpyAsync(fbuf[slot], fields_host[i], nf * sizeof(double), cudaMemcpyHostToDevice, s->h2d_stream));
+      CK(cudaEventRecord(ev_h2d[slot], s->h2d_stream));
+    };
+    try {
+      h2d(0);
+      if (n > 1) h2d(1);
+      for (int i = 0; i < n; ++i) {
+        const int slot = i & 1;
+        use_slot(slot);
+        CK(cudaStreamWaitEvent(cs, ev_h2d[slot], 0));
+        if (i >= 2) CK(cudaStreamWaitEvent(cs, ev_d2h[slot], 0));  // outputs of solve i-2 copied out
+        s->have_result = false;
+        const int launches = enqueue_cached(s, fbuf[slot]);
+        CK(cudaEventRecord(ev_comp[slot], cs));
+        CK(cudaStreamWaitEvent(s->d2h_stream, ev_comp[slot], 0));
+        if (out_controls_host && out_controls_host[i])
+          CK(cudaMemcpyAsync(out_controls_host[i], s->lattice.p, s->lattice.n * sizeof(double),
+                             cudaMemcpyDeviceToHost, s->d2h_stream));
+        if (out_errors_host && out_errors_host[i])
+          CK(cudaMemcpyAsync(out_errors_host[i], s->error.p, s->error.n * sizeof(double), cudaMemcpyDeviceToHost,
+                             s->d2h_stream));
+        CK(cudaEventRecord(ev_d2h[slot], s->d2h_stream));
+        if (i + 2 < n) h2d(i + 2);
+        finish_solve(s, launches);  // waits for solve i only; the copies keep running
+        if (out) out[i] = s->summary;
+      }
+      CK(cudaStreamSynchronize(s->d2h_stream));
+      CK(cudaStreamSynchronize(s->h2d_stream));
+    } catch (...) {
+      cudaStreamSynchronize(s->d2h_stream);
+      cudaStreamSynchronize(s->h2d_stream);
+      throw;
+    }
+    // s->lattice / s->error now hold the last solve's outputs (read by the getters)
   });
 }
 
