@@ -156,11 +156,11 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
   if (tid == 0)
     for (int c = 0; c < S && c < nchunks; ++c) issue(c);
 
-  double acc[P + 1], yw[P];
+  // acc[u]: R^T q of the column in slot u; yv[u]: its forward-substitution
+  // value once completed (y_{c-k} sits in slot (u - k) mod (P+1): no moves)
+  double acc[P + 1], yv[P + 1];
 #pragma unroll
-  for (int k = 0; k <= P; ++k) acc[k] = 0.0;
-#pragma unroll
-  for (int k = 0; k < P; ++k) yw[k] = 0.0;
+  for (int k = 0; k <= P; ++k) acc[k] = yv[k] = 0.0;
   int cbase = __ldg(g0g) < 0 ? __ldg(g0g) : 0;
   const std::int64_t dstr = D == 2 ? a.pitch_last : Tr;  // T1 row stride
   // Column-ordered accumulation with static register slots (as in
@@ -221,12 +221,10 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
       if (cbase >= 0) {  // forward substitution of column cbase (< n)
         double sacc = acc[u];
 #pragma unroll
-        for (int k = 1; k <= P; ++k) sacc = fma(-Lnx[k], yw[k - 1], sacc);
+        for (int k = P; k >= 1; --k) sacc = fma(-Lnx[k], yv[(u + P + 1 - k) % (P + 1)], sacc);
         const double y = sacc * Lnx[0];
         if (active) *yp = y;
-#pragma unroll
-        for (int k = P - 1; k >= 1; --k) yw[k] = yw[k - 1];
-        yw[0] = y;
+        yv[u] = y;
       }
       yp += dstr;
       acc[u] = 0.0;
@@ -234,9 +232,10 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
       if (cbase >= n) break;
     }
   }
-  // Back substitution in place, y values prefetched 8 columns ahead.
+  // Back substitution in place, y values prefetched PF columns ahead.  PF is a
+  // multiple of P: x_{c+k} sits in the static slot (u - k) mod P of xw.
   if (!active) return;
-  constexpr int PF = 16;
+  constexpr int PF = P * ((16 + P - 1) / P);
   double yr[PF];
 #pragma unroll
   for (int u = 0; u < PF; ++u) yr[u] = (n - 1 - u >= 0) ? dst[static_cast<std::int64_t>(n - 1 - u) * dstr] : 0.0;
@@ -260,13 +259,11 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
         const int cn = c - PF;
         yr[u] = cn >= 0 ? dst[static_cast<std::int64_t>(cn) * dstr] : 0.0;
 #pragma unroll
-        for (int k = 1; k <= P; ++k) s = fma(-Lb[k], xw[k - 1], s);
+        for (int k = P; k >= 1; --k) s = fma(-Lb[k], xw[(u - k + PF) % P], s);
         const double x = s * Lb[0];
         fetch_bwd(c - 1, Lb);
         dst[static_cast<std::int64_t>(c) * dstr] = x;
-#pragma unroll
-        for (int k = P - 1; k >= 1; --k) xw[k] = xw[k - 1];
-        xw[0] = x;
+        xw[u % P] = x;
       }
     }
   }
