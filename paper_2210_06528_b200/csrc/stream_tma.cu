@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.cuh"
 #include "tma.cuh"
@@ -73,13 +74,13 @@ __host__ __device__ inline StageLayout stage_layout(int R, int nthr, int P) {
 // ---------------------------------------------------------------- fit axis 0
 constexpr int kFitR = 8;  // rows per TMA stage (fit axis 0)
 
-template <int P, int S>
+template <int P, int S, int NC>
 __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __grid_constant__ CUtensorMap map,
                                                        const TmaGeom geo) {
   constexpr int R = kFitR;
   extern __shared__ __align__(1024) unsigned char sm_raw[];
   const int b = blockIdx.y;
-  const BlockDev blk = a.blocks[b];
+  const BlockDev& blk = a.blocks[b];
   const AxisProb pr = a.probs[blk.ax[0]];
   const int m = pr.m, n = pr.n;
   const int D = a.D;
@@ -87,42 +88,57 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
   const int m2 = D == 3 ? a.probs[blk.ax[2]].m : 1;
   // Box: W inner columns (even, 16-B multiple) x [B1] x R rows.  TMA tile
   // loads need a 16-B aligned innermost start coordinate, so the box starts
-  // at the even column at or below the block's first column and the thread
-  // -> column map is shifted by that parity (geo.B2 = W, one spare column).
+  // at the even column at or below the block's first column and the column
+  // map is shifted by that parity (geo.B2 = W, one spare column).  Each
+  // thread owns NC adjacent box columns (NC = 2: one LDS.128 per row, the
+  // broadcast basis values and loop bookkeeping shared by two columns).
   const int B1 = geo.B1, W = geo.B2;
-  const int nthr = B1 * W;
+  const int nbox = B1 * W;  // doubles per box row
   const int tile = blockIdx.x;
   const int tid = threadIdx.x;
   const AxisProb p1 = a.probs[blk.ax[1]];
   const int in0 = static_cast<int>(pr.in_lo);
-  int j1, j2, c_inner, c_mid;
-  bool active;
+  int c_inner, c_mid, bcol;  // bcol: first box column of this thread (row-major over [B1][W])
+  int j1[NC], j2[NC];
+  bool act[NC];
   if (D == 2) {
     const int cols = W - 2;  // columns owned per tile
     if (tile * cols >= m1) return;
     const int first = static_cast<int>(p1.in_lo) + tile * cols;
     c_inner = first & ~1;
     c_mid = 0;
-    j1 = tile * cols + tid - (first - c_inner);
-    j2 = 0;
-    active = j1 >= tile * cols && j1 < tile * cols + cols && j1 < m1;
+    bcol = NC * tid;
+#pragma unroll
+    for (int e = 0; e < NC; ++e) {
+      j1[e] = tile * cols + bcol + e - (first - c_inner);
+      j2[e] = 0;
+      act[e] = bcol + e < W && j1[e] >= tile * cols && j1[e] < tile * cols + cols && j1[e] < m1;
+    }
   } else {
     if (tile * B1 >= m1) return;
     const int in2 = static_cast<int>(a.probs[blk.ax[2]].in_lo);
     c_inner = in2 & ~1;
     c_mid = static_cast<int>(p1.in_lo) + tile * B1;
-    j1 = tile * B1 + tid / W;
-    j2 = tid % W - (in2 - c_inner);
-    active = j1 < m1 && j2 >= 0 && j2 < m2;
+    const int tpr = W / NC;  // threads per box row
+    const int row = tid / tpr;
+    bcol = row * W + NC * (tid - row * tpr);
+#pragma unroll
+    for (int e = 0; e < NC; ++e) {
+      j1[e] = tile * B1 + row;
+      j2[e] = NC * (tid - row * tpr) + e - (in2 - c_inner);
+      act[e] = row < B1 && j1[e] < m1 && j2[e] >= 0 && j2[e] < m2;
+    }
   }
   const std::int64_t Tr = static_cast<std::int64_t>(m1) * m2;
-  const std::int64_t t = active ? static_cast<std::int64_t>(j1) * m2 + j2 : 0;
-  double* dst = a.t1 + blk.t1off + t;  // T1[i0][Tr]
+  double* dst[NC];  // T1[i0][Tr] column of each owned input column
+#pragma unroll
+  for (int e = 0; e < NC; ++e)
+    dst[e] = a.t1 + blk.t1off + (act[e] ? static_cast<std::int64_t>(j1[e]) * m2 + j2[e] : 0);
   const int* g0g = a.g0 + pr.row_off;
   const double* vg = a.vals + pr.row_off * (P + 1);
-  const double* lt = a.ltab + pr.col_off * (2 * P + 1);  // may be redirected to smem
+  const double* lt = a.ltab + pr.col_off * (2 * P + 1);
 
-  const StageLayout SL = stage_layout(R, nthr, P);
+  const StageLayout SL = stage_layout(R, nbox, P);
   std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(sm_raw + S * SL.stage_bytes);
   const int nchunks = (m + R - 1) / R;
   const unsigned tx_bytes = static_cast<unsigned>(SL.q_bytes + R * (P + 1) * 8 + R * 4);
@@ -156,18 +172,19 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
   if (tid == 0)
     for (int c = 0; c < S && c < nchunks; ++c) issue(c);
 
-  // acc[u]: R^T q of the column in slot u; yv[u]: its forward-substitution
-  // value once completed (y_{c-k} sits in slot (u - k) mod (P+1): no moves)
-  double acc[P + 1], yv[P + 1];
+  // acc[e][u]: R^T q of column e's output column in slot u; yv[e][u]: its
+  // forward-substitution value (y_{c-k} in slot (u - k) mod (P+1): no moves)
+  double acc[NC][P + 1], yv[NC][P + 1];
 #pragma unroll
-  for (int k = 0; k <= P; ++k) acc[k] = yv[k] = 0.0;
+  for (int e = 0; e < NC; ++e)
+#pragma unroll
+    for (int k = 0; k <= P; ++k) acc[e][k] = yv[e][k] = 0.0;
   int cbase = __ldg(g0g) < 0 ? __ldg(g0g) : 0;
   const std::int64_t dstr = D == 2 ? a.pitch_last : Tr;  // T1 row stride
   // Column-ordered accumulation with static register slots (as in
-  // k_last_contract_tma): columns are visited in groups of P+1, slot u = the
-  // unrolled loop index; before column c is completed, the run of rows whose
-  // span starts at c is accumulated into slots (u + k) mod (P+1).  Completing
-  // a column is one step of forward substitution (y window shifted).
+  // k_last_contract_tma): output columns are visited in groups of P+1, slot
+  // u = the unrolled loop index; before column c is completed, the run of
+  // rows whose span starts at c is accumulated into slots (u + k) mod (P+1).
   double Lnx[P + 1];  // forward coefficients of column cbase, fetched one column ahead
   auto fetch_fwd = [&](int cc) {
     const double* Lc = slt + (cc < -(P + 1) ? -(P + 1) : cc) * LW;
@@ -175,7 +192,7 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
     for (int k = 0; k <= P; ++k) Lnx[k] = Lc[k];
   };
   fetch_fwd(cbase);
-  double* yp = dst + static_cast<std::int64_t>(cbase) * dstr;
+  std::int64_t yoff = static_cast<std::int64_t>(cbase) * dstr;  // T1 offset of output column cbase
   // row cursor over the TMA stages
   int c = 0, jl = 0, jn = 0, gnext = 0x7fffffff;
   const double* sq = nullptr;
@@ -184,7 +201,7 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
   auto open_chunk = [&]() {
     const int st = c % S;
     const unsigned char* base = sm_raw + st * SL.stage_bytes;
-    sq = reinterpret_cast<const double*>(base) + tid;
+    sq = reinterpret_cast<const double*>(base) + bcol;
     sv = reinterpret_cast<const double*>(base + SL.v_off);
     sg = reinterpret_cast<const int*>(base + SL.g_off);
     jn = (m - c * R) < R ? (m - c * R) : R;
@@ -212,58 +229,88 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
 #pragma unroll
     for (int u = 0; u <= P; ++u) {
       while (gnext == cbase) {  // CTA-uniform
-        const double q = sq[jl * nthr];
+        double q[NC];
+        if (NC == 2) {
+          const double2 q2 = *reinterpret_cast<const double2*>(sq + jl * nbox);
+          q[0] = q2.x;
+          q[NC - 1] = q2.y;
+        } else {
+          q[0] = sq[jl * nbox];
+        }
         const double* vr = sv + jl * (P + 1);
 #pragma unroll
-        for (int k = 0; k <= P; ++k) acc[(u + k) % (P + 1)] = fma(vr[k], q, acc[(u + k) % (P + 1)]);
+        for (int k = 0; k <= P; ++k) {
+          const double v = vr[k];
+#pragma unroll
+          for (int e = 0; e < NC; ++e) acc[e][(u + k) % (P + 1)] = fma(v, q[e], acc[e][(u + k) % (P + 1)]);
+        }
         advance();
       }
       if (cbase >= 0) {  // forward substitution of column cbase (< n)
-        double sacc = acc[u];
 #pragma unroll
-        for (int k = P; k >= 1; --k) sacc = fma(-Lnx[k], yv[(u + P + 1 - k) % (P + 1)], sacc);
-        const double y = sacc * Lnx[0];
-        if (active) *yp = y;
-        yv[u] = y;
+        for (int e = 0; e < NC; ++e) {
+          double sacc = acc[e][u];
+#pragma unroll
+          for (int k = P; k >= 1; --k) sacc = fma(-Lnx[k], yv[e][(u + P + 1 - k) % (P + 1)], sacc);
+          const double y = sacc * Lnx[0];
+          if (act[e]) dst[e][yoff] = y;
+          yv[e][u] = y;
+        }
       }
-      yp += dstr;
-      acc[u] = 0.0;
+      yoff += dstr;
+#pragma unroll
+      for (int e = 0; e < NC; ++e) acc[e][u] = 0.0;
       fetch_fwd(++cbase);
       if (cbase >= n) break;
     }
   }
   // Back substitution in place, y values prefetched PF columns ahead.  PF is a
   // multiple of P: x_{c+k} sits in the static slot (u - k) mod P of xw.
-  if (!active) return;
-  constexpr int PF = P * ((16 + P - 1) / P);
-  double yr[PF];
+  bool any = false;
 #pragma unroll
-  for (int u = 0; u < PF; ++u) yr[u] = (n - 1 - u >= 0) ? dst[static_cast<std::int64_t>(n - 1 - u) * dstr] : 0.0;
-  double xw[P];
+  for (int e = 0; e < NC; ++e) any = any || act[e];
+  if (!any) return;
+  constexpr int PF = P * ((16 / NC + P - 1) / P);
+  double yr[NC][PF];
 #pragma unroll
-  for (int k = 0; k < P; ++k) xw[k] = 0.0;
+  for (int u = 0; u < PF; ++u)
+#pragma unroll
+    for (int e = 0; e < NC; ++e)
+      yr[e][u] = (act[e] && n - 1 - u >= 0) ? dst[e][static_cast<std::int64_t>(n - 1 - u) * dstr] : 0.0;
+  double xw[NC][P];
+#pragma unroll
+  for (int e = 0; e < NC; ++e)
+#pragma unroll
+    for (int k = 0; k < P; ++k) xw[e][k] = 0.0;
   double Lb[P + 1];  // backward coefficients of the current column, fetched ahead
-  auto fetch_bwd = [&](int c, double* L) {
-    const double* Lc = slt + c * LW;  // c >= -1
-    L[0] = Lc[0];
+  auto fetch_bwd = [&](int cc) {
+    const double* Lc = slt + cc * LW;  // cc >= -1
+    Lb[0] = Lc[0];
 #pragma unroll
-    for (int k = 1; k <= P; ++k) L[k] = Lc[P + k];
+    for (int k = 1; k <= P; ++k) Lb[k] = Lc[P + k];
   };
-  fetch_bwd(n - 1, Lb);
+  fetch_bwd(n - 1);
   for (int c0 = n - 1; c0 >= 0; c0 -= PF) {
 #pragma unroll
     for (int u = 0; u < PF; ++u) {
-      const int c = c0 - u;
-      if (c >= 0) {
-        double s = yr[u];
-        const int cn = c - PF;
-        yr[u] = cn >= 0 ? dst[static_cast<std::int64_t>(cn) * dstr] : 0.0;
+      const int cc = c0 - u;
+      if (cc >= 0) {
+        const int cn = cc - PF;
+        const double Lb0 = Lb[0];
+        double Lk[P + 1];
 #pragma unroll
-        for (int k = P; k >= 1; --k) s = fma(-Lb[k], xw[(u - k + PF) % P], s);
-        const double x = s * Lb[0];
-        fetch_bwd(c - 1, Lb);
-        dst[static_cast<std::int64_t>(c) * dstr] = x;
-        xw[u % P] = x;
+        for (int k = 1; k <= P; ++k) Lk[k] = Lb[k];
+        fetch_bwd(cc - 1);
+#pragma unroll
+        for (int e = 0; e < NC; ++e) {
+          double sacc = yr[e][u];
+          yr[e][u] = (act[e] && cn >= 0) ? dst[e][static_cast<std::int64_t>(cn) * dstr] : 0.0;
+#pragma unroll
+          for (int k = P; k >= 1; --k) sacc = fma(-Lk[k], xw[e][(u - k + PF) % P], sacc);
+          const double x = sacc * Lb0;
+          if (act[e]) dst[e][static_cast<std::int64_t>(cc) * dstr] = x;
+          xw[e][u % P] = x;
+        }
       }
     }
   }
@@ -807,19 +854,22 @@ __global__ void __launch_bounds__(256) k_decode_tma(const DecodeSweepArgs a, con
 
 template <int P>
 struct Axis0Launch {
-  template <int S>
+  template <int S, int NC>
   static void go(const FitArgs& a, const CUtensorMap& map, const TmaGeom& g, int ntiles, cudaStream_t s) {
     const StageLayout SL = stage_layout(kFitR, g.B1 * g.B2, P);
     const size_t smem = static_cast<size_t>(S) * SL.stage_bytes + 128 + static_cast<size_t>(g.lt_cap) * 8;
-    cudaFuncSetAttribute(k_fit_axis0_tma<P, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(k_fit_axis0_tma<P, S, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
     dim3 grid(ntiles, a.nblocks);
-    k_fit_axis0_tma<P, S><<<grid, g.B1 * g.B2, smem, s>>>(a, map, g);
+    k_fit_axis0_tma<P, S, NC><<<grid, g.B1 * g.B2 / NC, smem, s>>>(a, map, g);
   }
   static int run(const FitArgs& a, const CUtensorMap& map, const TmaGeom& g, int ntiles, cudaStream_t s) {
-    if (g.S == 3)
-      go<3>(a, map, g, ntiles, s);
+    // NC = 2 (two columns per thread) measured slower on C5 (331 vs 233 us): fewer resident warps
+    static const int nc = std::getenv("MFADD_FIT_NC") ? std::atoi(std::getenv("MFADD_FIT_NC")) : 1;
+    if (nc == 1)
+      g.S == 3 ? go<3, 1>(a, map, g, ntiles, s) : go<4, 1>(a, map, g, ntiles, s);
     else
-      go<4>(a, map, g, ntiles, s);
+      g.S == 3 ? go<3, 2>(a, map, g, ntiles, s) : go<4, 2>(a, map, g, ntiles, s);
     return 1;
   }
 };
