@@ -657,6 +657,7 @@ struct mfadd_solver {
   DBuf<unsigned long long> change, linf_sh, pair_jumps;
   DBuf<mfb::EpochAcc> acc;
   DBuf<double> epoch_out, lattice, error, partial, red2, field_buf;
+  DBuf<unsigned> ticket;  // decode CTA completion counter
   int npairs = 0;
   std::vector<std::array<int, 2>> pair_ids;
   // Non-empty when some shared control has a holder that is not a neighbour of
@@ -1323,6 +1324,8 @@ std::unique_ptr<mfadd_solver> create_solver(mfadd_context* ctx, const mfadd_deco
     }
     s->partial.alloc(npart * 2);
     s->red2.alloc(2);
+    s->ticket.alloc(1);
+    CK(cudaMemsetAsync(s->ticket.p, 0, sizeof(unsigned), st));
     s->unit_g0.upload(std::vector<int>{0}, st);
     s->unit_vals.upload(std::vector<double>{1.0}, st);
     for (auto& e : s->ev) CK(cudaEventCreate(&e));
@@ -1528,17 +1531,21 @@ int enqueue_decode(mfadd_solver* s, const double* dfield) {
       box[1] = static_cast<std::uint32_t>(s->dgeo.B1);
       box[2] = static_cast<std::uint32_t>(s->dgeo.R);
     }
+    ds.ticket = s->ticket.p;
+    ds.red2 = s->red2.p;
     const CUtensorMap map = make_tmap(dfield, d.rank, dims, box);
     launches += mfb::launch_decode_tma(wl.p, ds, map, s->dgeo, st);
-    nparts = static_cast<std::int64_t>(s->dnt1) * s->dnt2 * s->dnrange;
+    nparts = 0;  // reduced by the decode's last CTA
   } else {
     launches += mfb::launch_decode(wl.p, da, st);
     nparts = s->dp.ntiles[0] * s->dp.ntiles[1] * s->dp.ntiles[2];
   }
   s->tl.end();
-  s->tl.begin("reduce");
-  launches += mfb::launch_reduce_partials(s->partial.p, nparts, s->red2.p, st);
-  s->tl.end();
+  if (nparts > 0) {
+    s->tl.begin("reduce");
+    launches += mfb::launch_reduce_partials(s->partial.p, nparts, s->red2.p, st);
+    s->tl.end();
+  }
   return launches;
 }
 

@@ -201,8 +201,14 @@ __global__ void __launch_bounds__(256) k_gram_chol(CholArgs a) {
   if (threadIdx.x == 0) {
     // Banded left-looking Cholesky (the Eigen LLT of lsq.cpp:46-49 restricted
     // to the band: L has no fill outside it).  Row c is written back over
-    // sm[c*(P+1)..]: [1/L(c,c), L(c,c-1), .., L(c,c-P)]; rows c-1..c-P are
-    // read back from shared memory (loads independent of row c's chain).
+    // sm[c*(P+1)..]: [1/L(c,c), L(c,c-1), .., L(c,c-P)].  The last P rows stay
+    // in a register window (Lw[r] = row c-1-r), so the dependent chain from
+    // one row to the next never waits on a shared-memory store/load.
+    double Lw[P][P + 1];
+#pragma unroll
+    for (int r = 0; r < P; ++r)
+#pragma unroll
+      for (int k = 0; k <= P; ++k) Lw[r][k] = 0.0;
     for (int c = 0; c < n; ++c) {
       double* Gc = sm + c * (P + 1);
       double Lc[P + 1];
@@ -214,11 +220,11 @@ __global__ void __launch_bounds__(256) k_gram_chol(CholArgs a) {
           Lc[k] = 0.0;
           continue;
         }
-        const double* Lj = sm + (c - k) * (P + 1);  // row j = c-k
+        // row j = c-k is Lw[k-1]: L(c,c-k) = (G(c,c-k) - sum_t L(c,c-t) L(j,c-t)) / L(j,j)
         double sacc = Lc[k];
 #pragma unroll
-        for (int t = k + 1; t <= P; ++t) sacc = fma(-Lc[t], Lj[t - k], sacc);  // L(c,c-t) L(j,c-t)
-        Lc[k] = sacc * Lj[0];                                                   // * 1/L(j,j)
+        for (int t = k + 1; t <= P; ++t) sacc = fma(-Lc[t], Lw[k - 1][t - k], sacc);
+        Lc[k] = sacc * Lw[k - 1][0];
       }
       double dg = Lc[0];
 #pragma unroll
@@ -230,6 +236,12 @@ __global__ void __launch_bounds__(256) k_gram_chol(CholArgs a) {
       Lc[0] = rsqrt(dg);
 #pragma unroll
       for (int k = 0; k <= P; ++k) Gc[k] = Lc[k];
+#pragma unroll
+      for (int r = P - 1; r >= 1; --r)
+#pragma unroll
+        for (int k = 0; k <= P; ++k) Lw[r][k] = Lw[r - 1][k];
+#pragma unroll
+      for (int k = 0; k <= P; ++k) Lw[0][k] = Lc[k];
     }
   }
   __syncthreads();

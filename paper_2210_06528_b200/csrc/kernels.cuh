@@ -234,6 +234,8 @@ struct DecodeSweepArgs {
   const double* lattice;
   double* err;      // nullable
   double* partial;  // per CTA {l2sq, linf}
+  unsigned* ticket; // CTA completion counter (zero between launches)
+  double* red2;     // {sum l2sq, max linf}, written by the last CTA
 };
 int launch_decode_tma(int degree, const DecodeSweepArgs& a, const CUtensorMap& map, const TmaGeom& g,
                       cudaStream_t s);

@@ -850,6 +850,41 @@ __global__ void __launch_bounds__(256) k_decode_tma(const DecodeSweepArgs a, con
     a.partial[2 * cta] = sl;
     a.partial[2 * cta + 1] = sm2;
   }
+  // last CTA: fixed-order reduction of all partials into red2 (L2^2, L-inf)
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = atomicAdd(a.ticket, 1u) == gridDim.x * gridDim.y - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const std::int64_t nparts = static_cast<std::int64_t>(gridDim.x) * gridDim.y;
+  double pl = 0.0, pm = 0.0;
+  for (std::int64_t i = tid; i < nparts; i += nthr) {
+    pl += __ldcg(a.partial + 2 * i);
+    pm = fmax(pm, __ldcg(a.partial + 2 * i + 1));
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    pl += __shfl_xor_sync(kFullMask, pl, off);
+    pm = fmax(pm, __shfl_xor_sync(kFullMask, pm, off));
+  }
+  __syncthreads();
+  if ((tid & 31) == 0) {
+    s_red[wid] = pl;
+    s_red[32 + wid] = pm;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double sl = 0.0, sm2 = 0.0;
+    for (int w = 0; w < (nthr + 31) / 32; ++w) {
+      sl += s_red[w];
+      sm2 = fmax(sm2, s_red[32 + w]);
+    }
+    a.red2[0] = sl;
+    a.red2[1] = sm2;
+    *a.ticket = 0u;
+  }
 }
 
 template <int P>
