@@ -221,14 +221,15 @@ __global__ void __launch_bounds__(256) k_gram_chol(CholArgs a) {
           continue;
         }
         // row j = c-k is Lw[k-1]: L(c,c-k) = (G(c,c-k) - sum_t L(c,c-t) L(j,c-t)) / L(j,j)
+        // newest value (Lc[k+1]) enters last: the older terms overlap its computation
         double sacc = Lc[k];
 #pragma unroll
-        for (int t = k + 1; t <= P; ++t) sacc = fma(-Lc[t], Lw[k - 1][t - k], sacc);
+        for (int t = P; t >= k + 1; --t) sacc = fma(-Lc[t], Lw[k - 1][t - k], sacc);
         Lc[k] = sacc * Lw[k - 1][0];
       }
       double dg = Lc[0];
 #pragma unroll
-      for (int k = 1; k <= P; ++k) dg = fma(-Lc[k], Lc[k], dg);
+      for (int k = P; k >= 1; --k) dg = fma(-Lc[k], Lc[k], dg);
       if (!(dg > 0.0)) {  // Eigen LLT NumericalIssue -> SingularFitError
         set_status(a.status, 3, pid, c);
         dg = 1.0;
