@@ -538,6 +538,8 @@ struct Workload {
       const std::uint32_t box[2] = {16u, static_cast<std::uint32_t>(last_LT)};
       const CUtensorMap map = make_tmap(src, 2, dims, box, CU_TENSOR_MAP_SWIZZLE_128B);
       l += mfb::launch_fit_last_tma(p, fa, map, last_LT, last_ltcap, last_kseg, ctx->stream);
+    } else if (D == 1 && max_n_factor * (2 * p + 2) <= 24576) {  // z + factor in <= 192 KB smem
+      l += mfb::launch_fit_1d(p, fa, max_n_factor, ctx->stream);
     } else {
       l += mfb::launch_fit_last(p, fa, ctx->stream);
     }

@@ -1501,6 +1501,87 @@ struct FitStridedLaunch {
   }
 };
 
+// 1-D fit (lsq.cpp:39-64 with D = 1): one CTA per block.  Thread per output
+// column c accumulates R^T q over the contiguous run of rows whose basis
+// covers c (g0 in [c-P, c]), in row order; one thread then runs the banded
+// forward / back substitution (n steps each) and the L-inf of the non-shared
+// controls.
+template <int P>
+__global__ void __launch_bounds__(256) k_fit_1d(FitArgs a) {
+  extern __shared__ double s_z[];  // n, then the factor table n x (2P+1)
+  const int b = blockIdx.x;
+  const BlockDev& blk = a.blocks[b];
+  const AxisProb pr = a.probs[blk.ax[0]];
+  const int m = pr.m, n = pr.n;
+  const int* g0 = a.g0 + pr.row_off;
+  const double* v = a.vals + pr.row_off * (P + 1);
+  const double* q = a.field + blk.fbase;
+  for (int c = threadIdx.x; c < n; c += blockDim.x) {
+    int lo = 0, hi = m;  // first row with g0 >= c - P
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (__ldg(g0 + mid) < c - P)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    double z = 0.0;
+    for (int j = lo; j < m; ++j) {
+      const int g = __ldg(g0 + j);
+      if (g > c) break;
+      z = fma(__ldg(v + static_cast<std::int64_t>(j) * (P + 1) + (c - g)), q[static_cast<std::int64_t>(j) * a.fs[0]], z);
+    }
+    s_z[c] = z;
+  }
+  double* s_lt = s_z + n;  // factor staged in smem: the serial solve never waits on L2
+  for (int i = threadIdx.x; i < n * (2 * P + 1); i += blockDim.x) s_lt[i] = a.ltab[pr.col_off * (2 * P + 1) + i];
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  const double* lt = s_lt;
+  double w[P];
+#pragma unroll
+  for (int k = 0; k < P; ++k) w[k] = 0.0;
+  for (int c = 0; c < n; ++c) {  // forward: y_c = (z_c - sum_k L(c,c-k) y_{c-k}) / L(c,c)
+    const double* Lc = lt + static_cast<std::int64_t>(c) * (2 * P + 1);
+    double sacc = s_z[c];
+#pragma unroll
+    for (int k = P; k >= 1; --k) sacc = fma(-Lc[k], w[k - 1], sacc);
+    const double y = sacc * Lc[0];
+#pragma unroll
+    for (int k = P - 1; k >= 1; --k) w[k] = w[k - 1];
+    w[0] = y;
+    s_z[c] = y;
+  }
+#pragma unroll
+  for (int k = 0; k < P; ++k) w[k] = 0.0;
+  double* Pb = a.P + blk.poff;
+  const unsigned char* sf = a.shared_flag + a.sflag_off[0] + pr.col_lo;
+  unsigned long long lmax = 0ull;
+  for (int c = n - 1; c >= 0; --c) {  // back: x_c = (y_c - sum_k L(c+k,c) x_{c+k}) / L(c,c)
+    const double* Lc = lt + static_cast<std::int64_t>(c) * (2 * P + 1);
+    double sacc = s_z[c];
+#pragma unroll
+    for (int k = P; k >= 1; --k) sacc = fma(-Lc[P + k], w[k - 1], sacc);
+    const double x = sacc * Lc[0];
+#pragma unroll
+    for (int k = P - 1; k >= 1; --k) w[k] = w[k - 1];
+    w[0] = x;
+    Pb[c] = x;
+    if (!sf[c]) lmax = umax(lmax, dbits(fabs(x)));
+  }
+  if (lmax) atomicMax(a.linf_int + b, lmax);
+}
+
+template <int P>
+struct Fit1DLaunch {
+  static int run(const FitArgs& a, int max_n, cudaStream_t s) {
+    const size_t smem = static_cast<size_t>(max_n) * (2 * P + 2) * sizeof(double);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_fit_1d<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k_fit_1d<P><<<a.nblocks, 256, smem, s>>>(a);
+    return 1;
+  }
+};
+
 template <int P>
 struct FitLastLaunch {
   static int run(const FitArgs& a, cudaStream_t s) {
@@ -1552,6 +1633,9 @@ int launch_fit_strided(int degree, const FitArgs& a, int axis, cudaStream_t s) {
 }
 int launch_fit_last(int degree, const FitArgs& a, cudaStream_t s) {
   return dispatch_degree<FitLastLaunch>(degree, a, s);
+}
+int launch_fit_1d(int degree, const FitArgs& a, int max_n, cudaStream_t s) {
+  return dispatch_degree<Fit1DLaunch>(degree, a, max_n, s);
 }
 int launch_decode(int degree, const DecodeArgs& a, cudaStream_t s) {
   return dispatch_degree<DecodeLaunch>(degree, a, s);

@@ -74,6 +74,8 @@ struct FitArgs {
 };
 int launch_fit_strided(int degree, const FitArgs& a, int axis, cudaStream_t s);  // axis < D-1
 int launch_fit_last(int degree, const FitArgs& a, cudaStream_t s);
+// D = 1: CTA per block, column-parallel R^T q + serial banded solve (smem: max_n x (2P+2) doubles).
+int launch_fit_1d(int degree, const FitArgs& a, int max_n, cudaStream_t s);
 
 // K4: one averaging epoch over every shared control (solver.cpp:112-164 with
 // the runtime.cpp:123-158 Jacobi snapshot), jump residuals (solver.cpp:
