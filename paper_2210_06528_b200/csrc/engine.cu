@@ -292,6 +292,9 @@ struct Workload {
   mfb::TmaGeom axis0_geo{1, 1, 16, 4, 0};
   int axis0_tiles = 0;
   // TMA last-axis pass (D >= 2)
+  bool tma_mid = false;  // D = 3 middle axis through a T1 tensor map
+  mfb::TmaGeom mid_geo{1, 1, 8, 4, 0};
+  int mid_tiles = 0, mid_n0 = 0;
   bool tma_last = false;
   int last_LT = 128, last_ltcap = 0, last_kseg = 1;
   std::vector<int> segtab;  // kSegStride ints per axis problem (last-axis problems filled)
@@ -340,6 +343,24 @@ struct Workload {
       last_ltcap = needl;
       tma_last = true;
       plan_segments();
+    }
+    // D = 3 middle axis: per (block, c0) slice of T1 = [m1 rows][pitch]
+    if (D == 3 && !std::getenv("MFADD_NO_TMA_MID")) {
+      int mx = 0, mxn1 = 0, mxn0 = 0;
+      for (const auto& b : blocks) {
+        mx = std::max(mx, probs[static_cast<std::size_t>(b.ax[2])].m);
+        mxn1 = std::max(mxn1, probs[static_cast<std::size_t>(b.ax[1])].n);
+        mxn0 = std::max(mxn0, probs[static_cast<std::size_t>(b.ax[0])].n);
+      }
+      const int needm = (mxn1 + 2 * (p + 1)) * (2 * p + 1);
+      if (needm <= 6144) {
+        const int nt = (mx + 253) / 254;
+        const int cols = round_up((mx + nt - 1) / nt, 2);
+        mid_geo = mfb::TmaGeom{1, cols + 2, 8, 4, needm};
+        mid_tiles = (mx + cols - 1) / cols;
+        mid_n0 = mxn0;
+        tma_mid = true;
+      }
     }
   }
 
@@ -420,7 +441,7 @@ struct Workload {
       b.t1off = total_t1;
       b.t2off = total_t2;
       if (D == 2) total_t1 += n[0] * pitch_last;
-      if (D == 3) total_t1 += n[0] * m[1] * m[2];
+      if (D == 3) total_t1 += n[0] * m[1] * pitch_last;  // [n0][m1][pitch]
       if (D == 3) total_t2 += n[0] * n[1] * pitch_last;
       for (int d = 0; d + 1 < D; ++d) {
         std::int64_t L = 1, Tr = 1;
@@ -525,6 +546,12 @@ struct Workload {
         }
         const CUtensorMap map = make_tmap(field, D, dims, box);
         l += mfb::launch_fit_axis0_tma(p, fa, map, axis0_geo, axis0_tiles, ctx->stream);
+      } else if (d == 1 && tma_mid) {
+        const std::uint64_t dims[2] = {static_cast<std::uint64_t>(pitch_last),
+                                       static_cast<std::uint64_t>(total_t1 / pitch_last)};
+        const std::uint32_t box[2] = {static_cast<std::uint32_t>(mid_geo.B2), static_cast<std::uint32_t>(mid_geo.R)};
+        const CUtensorMap map = make_tmap(t1.p, 2, dims, box);
+        l += mfb::launch_fit_mid_tma(p, fa, map, mid_geo, mid_tiles, mid_n0, ctx->stream);
       } else {
         l += mfb::launch_fit_strided(p, fa, d, ctx->stream);
       }

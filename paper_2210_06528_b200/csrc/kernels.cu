@@ -317,13 +317,21 @@ __global__ void __launch_bounds__(kStridedThreads) k_fit_strided(FitArgs a, int 
     }
     src = a.field + off;
     sst = a.fs[0];
-  } else {
-    src = a.t1 + blk.t1off + (l * m) * Tr + t;
-    sst = Tr;
+  } else {  // d == 1 of D = 3: T1[c0][j1][pitch]
+    src = a.t1 + blk.t1off + l * (static_cast<std::int64_t>(m) * a.pitch_last) + t;
+    sst = a.pitch_last;
   }
-  // rows of the last-axis input (written by pass D-2) use the common pitch
-  const std::int64_t Tro = (d == a.D - 2) ? a.pitch_last : Tr;
-  double* dst = (d == 0 ? a.t1 + blk.t1off : a.t2 + blk.t2off) + (l * n) * Tro + t;
+  // Outputs use the common even pitch on their last axis: T1 (D = 3) is
+  // [n0][m1][pitch], the last-axis input (pass D-2) is [..][pitch].
+  std::int64_t Tro = Tr, tpos = t;
+  if (d == a.D - 2) {
+    Tro = a.pitch_last;
+  } else if (a.D == 3 && d == 0) {
+    const std::int64_t m2 = a.probs[blk.ax[2]].m;
+    Tro = a.probs[blk.ax[1]].m * a.pitch_last;
+    tpos = (t / m2) * a.pitch_last + (t - (t / m2) * m2);
+  }
+  double* dst = (d == 0 ? a.t1 + blk.t1off : a.t2 + blk.t2off) + (l * n) * Tro + tpos;
   const std::int64_t dstr = Tro;
 #ifdef MFB_DEBUG
   if (active) {

@@ -214,6 +214,9 @@ struct TmaGeom {
 // TMA axis-0 fit pass (stream_tma.cu); needs 16-B aligned field row strides.
 int launch_fit_axis0_tma(int degree, const FitArgs& a, const CUtensorMap& map, const TmaGeom& g, int ntiles,
                          cudaStream_t s);
+// D = 3 middle axis through the T1 tensor map ([rows][pitch]): grid.z = c0.
+int launch_fit_mid_tma(int degree, const FitArgs& a, const CUtensorMap& map, const TmaGeom& g, int ntiles, int max_n0,
+                       cudaStream_t s);
 
 // TMA last-axis fit pass (D >= 2): 128-B swizzled 16-column boxes of the
 // last-axis input, LT lines per CTA.

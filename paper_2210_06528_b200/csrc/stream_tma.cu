@@ -74,17 +74,23 @@ __host__ __device__ inline StageLayout stage_layout(int R, int nthr, int P) {
 // ---------------------------------------------------------------- fit axis 0
 constexpr int kFitR = 8;  // rows per TMA stage (fit axis 0)
 
-template <int P, int S, int NC>
+// MID: the middle axis of D = 3 (lsq.cpp:57-61 on axis 1).  Each (block, c0)
+// slice of T1 = [n0][m1][pitch] is a 2-D box of m1 rows x m2 columns read
+// through the same kind of tensor map; the sweep runs over j1 and writes
+// T2[c0][c1][j2] (row pitch = the common last-axis pitch).
+template <int P, int S, int NC, bool MID>
 __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __grid_constant__ CUtensorMap map,
                                                        const TmaGeom geo) {
   constexpr int R = kFitR;
   extern __shared__ __align__(1024) unsigned char sm_raw[];
   const int b = blockIdx.y;
   const BlockDev& blk = a.blocks[b];
-  const AxisProb pr = a.probs[blk.ax[0]];
+  const AxisProb pr = a.probs[blk.ax[MID ? 1 : 0]];
   const int m = pr.m, n = pr.n;
-  const int D = a.D;
-  const int m1 = a.probs[blk.ax[1]].m;
+  const int D = MID ? 2 : a.D;  // MID sweeps a 2-D slice
+  const int c0s = MID ? static_cast<int>(blockIdx.z) : 0;
+  if (MID && c0s >= a.probs[blk.ax[0]].n) return;
+  const int m1 = MID ? a.probs[blk.ax[2]].m : a.probs[blk.ax[1]].m;  // columns of the swept box
   const int m2 = D == 3 ? a.probs[blk.ax[2]].m : 1;
   // Box: W inner columns (even, 16-B multiple) x [B1] x R rows.  TMA tile
   // loads need a 16-B aligned innermost start coordinate, so the box starts
@@ -96,15 +102,17 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
   const int nbox = B1 * W;  // doubles per box row
   const int tile = blockIdx.x;
   const int tid = threadIdx.x;
-  const AxisProb p1 = a.probs[blk.ax[1]];
-  const int in0 = static_cast<int>(pr.in_lo);
+  const AxisProb p1 = a.probs[blk.ax[MID ? 2 : 1]];
+  // first box row: the block's first input row (field), or the slice's first
+  // T1 row (T1 rows are [block][c0][j1], all of width pitch)
+  const int in0 = MID ? static_cast<int>(blk.t1off / a.pitch_last) + c0s * m : static_cast<int>(pr.in_lo);
   int c_inner, c_mid, bcol;  // bcol: first box column of this thread (row-major over [B1][W])
   int j1[NC], j2[NC];
   bool act[NC];
   if (D == 2) {
     const int cols = W - 2;  // columns owned per tile
     if (tile * cols >= m1) return;
-    const int first = static_cast<int>(p1.in_lo) + tile * cols;
+    const int first = (MID ? 0 : static_cast<int>(p1.in_lo)) + tile * cols;
     c_inner = first & ~1;
     c_mid = 0;
     bcol = NC * tid;
@@ -129,11 +137,15 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
       act[e] = row < B1 && j1[e] < m1 && j2[e] >= 0 && j2[e] < m2;
     }
   }
-  const std::int64_t Tr = static_cast<std::int64_t>(m1) * m2;
-  double* dst[NC];  // T1[i0][Tr] column of each owned input column
+  // output: T1[i0][m1][pitch] (D = 3), T1[i0][pitch] (D = 2), or for MID
+  // T2[c0][c1][pitch]; dstr = the stride between consecutive output rows
+  const std::int64_t pitch = a.pitch_last;
+  double* dst[NC];
 #pragma unroll
-  for (int e = 0; e < NC; ++e)
-    dst[e] = a.t1 + blk.t1off + (act[e] ? static_cast<std::int64_t>(j1[e]) * m2 + j2[e] : 0);
+  for (int e = 0; e < NC; ++e) {
+    const std::int64_t col = act[e] ? (D == 3 ? static_cast<std::int64_t>(j1[e]) * pitch + j2[e] : j1[e]) : 0;
+    dst[e] = MID ? a.t2 + blk.t2off + static_cast<std::int64_t>(c0s) * n * pitch + col : a.t1 + blk.t1off + col;
+  }
   const int* g0g = a.g0 + pr.row_off;
   const double* vg = a.vals + pr.row_off * (P + 1);
   const double* lt = a.ltab + pr.col_off * (2 * P + 1);
@@ -180,7 +192,7 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
 #pragma unroll
     for (int k = 0; k <= P; ++k) acc[e][k] = yv[e][k] = 0.0;
   int cbase = __ldg(g0g) < 0 ? __ldg(g0g) : 0;
-  const std::int64_t dstr = D == 2 ? a.pitch_last : Tr;  // T1 row stride
+  const std::int64_t dstr = D == 2 ? pitch : static_cast<std::int64_t>(m1) * pitch;  // output row stride
   // Column-ordered accumulation with static register slots (as in
   // k_last_contract_tma): output columns are visited in groups of P+1, slot
   // u = the unrolled loop index; before column c is completed, the run of
@@ -889,14 +901,15 @@ __global__ void __launch_bounds__(256) k_decode_tma(const DecodeSweepArgs a, con
 
 template <int P>
 struct Axis0Launch {
-  template <int S, int NC>
-  static void go(const FitArgs& a, const CUtensorMap& map, const TmaGeom& g, int ntiles, cudaStream_t s) {
+  template <int S, int NC, bool MID = false>
+  static void go(const FitArgs& a, const CUtensorMap& map, const TmaGeom& g, int ntiles, cudaStream_t s,
+                 int zdim = 1) {
     const StageLayout SL = stage_layout(kFitR, g.B1 * g.B2, P);
     const size_t smem = static_cast<size_t>(S) * SL.stage_bytes + 128 + static_cast<size_t>(g.lt_cap) * 8;
-    cudaFuncSetAttribute(k_fit_axis0_tma<P, S, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_fit_axis0_tma<P, S, NC, MID>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
-    dim3 grid(ntiles, a.nblocks);
-    k_fit_axis0_tma<P, S, NC><<<grid, g.B1 * g.B2 / NC, smem, s>>>(a, map, g);
+    dim3 grid(ntiles, a.nblocks, zdim);
+    k_fit_axis0_tma<P, S, NC, MID><<<grid, g.B1 * g.B2 / NC, smem, s>>>(a, map, g);
   }
   static int run(const FitArgs& a, const CUtensorMap& map, const TmaGeom& g, int ntiles, cudaStream_t s) {
     // NC = 2 (two columns per thread) measured slower on C5 (331 vs 233 us): fewer resident warps
@@ -980,6 +993,21 @@ int launch_fit_last_tma(int degree, const FitArgs& a, const CUtensorMap& map, in
 int launch_fit_axis0_tma(int degree, const FitArgs& a, const CUtensorMap& map, const TmaGeom& g, int ntiles,
                          cudaStream_t s) {
   return dispatch_p<Axis0Launch>(degree, a, map, g, ntiles, s);
+}
+
+namespace {
+template <int P>
+struct MidLaunch {
+  static int run(const FitArgs& a, const CUtensorMap& map, const TmaGeom& g, int ntiles, int max_n0, cudaStream_t s) {
+    Axis0Launch<P>::template go<4, 1, true>(a, map, g, ntiles, s, max_n0);
+    return 1;
+  }
+};
+}  // namespace
+
+int launch_fit_mid_tma(int degree, const FitArgs& a, const CUtensorMap& map, const TmaGeom& g, int ntiles, int max_n0,
+                       cudaStream_t s) {
+  return dispatch_p<MidLaunch>(degree, a, map, g, ntiles, max_n0, s);
 }
 
 int launch_decode_tma(int degree, const DecodeSweepArgs& a, const CUtensorMap& map, const TmaGeom& g,
