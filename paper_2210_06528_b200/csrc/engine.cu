@@ -525,6 +525,9 @@ struct Workload {
     fa.pitch_last = pitch_last;
     fa.segtab = d_segtab.p;
     fa.zhalf = zhalf;
+    // axis 0 forward-only, L0^-T on the held lattices at the end (stream_tma.cu)
+    static const bool no_defer = std::getenv("MFADD_NO_DEFER") != nullptr;
+    fa.defer_back = (tma_axis0 && tma_last && !no_defer) ? 1 : 0;
     fa.n_field = field_n;
     fa.n_t1 = total_t1;
     fa.n_t2 = total_t2;
@@ -571,6 +574,19 @@ struct Workload {
       l += mfb::launch_fit_last(p, fa, ctx->stream);
     }
     tl->end();
+    if (fa.defer_back) {
+      int mxn0 = 0;
+      std::int64_t mxr = 1;
+      for (const auto& b : blocks) {
+        mxn0 = std::max(mxn0, probs[static_cast<std::size_t>(b.ax[0])].n);
+        std::int64_t r = 1;
+        for (int k = 1; k < D; ++k) r *= probs[static_cast<std::size_t>(b.ax[k])].n;
+        mxr = std::max(mxr, r);
+      }
+      tl->begin("fit_backsub0");
+      l += mfb::launch_axis0_backsub(p, fa, mxn0, mxr, ctx->stream);
+      tl->end();
+    }
     CK(cudaGetLastError());
     return l;
   }

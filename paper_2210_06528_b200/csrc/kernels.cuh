@@ -71,6 +71,7 @@ struct FitArgs {
   std::int64_t n_field, n_t1, n_t2, n_P;  // buffer sizes (debug bounds checks)
   const int* segtab;                 // last-axis row segments per axis problem (kSegStride ints)
   std::int64_t zhalf;                // last-axis contraction: Y = [parity 0 | parity 1 | y scratch]
+  int defer_back;                    // axis 0 forward-only; L0^-T applied to P by k_axis0_backsub
 };
 int launch_fit_strided(int degree, const FitArgs& a, int axis, cudaStream_t s);  // axis < D-1
 int launch_fit_last(int degree, const FitArgs& a, cudaStream_t s);
@@ -214,6 +215,8 @@ struct TmaGeom {
 // TMA axis-0 fit pass (stream_tma.cu); needs 16-B aligned field row strides.
 int launch_fit_axis0_tma(int degree, const FitArgs& a, const CUtensorMap& map, const TmaGeom& g, int ntiles,
                          cudaStream_t s);
+// Deferred axis-0 back substitution on the held lattices (+ per-block L-inf).
+int launch_axis0_backsub(int degree, const FitArgs& a, int max_n0, std::int64_t max_rest, cudaStream_t s);
 // D = 3 middle axis through the T1 tensor map ([rows][pitch]): grid.z = c0.
 int launch_fit_mid_tma(int degree, const FitArgs& a, const CUtensorMap& map, const TmaGeom& g, int ntiles, int max_n0,
                        cudaStream_t s);

@@ -78,7 +78,11 @@ constexpr int kFitR = 8;  // rows per TMA stage (fit axis 0)
 // slice of T1 = [n0][m1][pitch] is a 2-D box of m1 rows x m2 columns read
 // through the same kind of tensor map; the sweep runs over j1 and writes
 // T2[c0][c1][j2] (row pitch = the common last-axis pitch).
-template <int P, int S, int NC, bool MID>
+// BACK = false (axis 0 when FitArgs::defer_back): forward substitution only;
+// the L^-T half of the axis-0 solve then runs on the held lattice at the end
+// (k_axis0_backsub): the axis operators commute, so the result is the same up
+// to rounding while T1 is written once instead of written, re-read, rewritten.
+template <int P, int S, int NC, bool MID, bool BACK = true>
 __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __grid_constant__ CUtensorMap map,
                                                        const TmaGeom geo) {
   constexpr int R = kFitR;
@@ -276,6 +280,7 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
       if (cbase >= n) break;
     }
   }
+  if (!BACK) return;
   // Back substitution in place, y values prefetched PF columns ahead.  PF is a
   // multiple of P: x_{c+k} sits in the static slot (u - k) mod P of xw.
   bool any = false;
@@ -627,7 +632,7 @@ __global__ void __launch_bounds__(128) k_last_solve(const FitArgs a) {
       if (cl < cn) {  // column clo + cl was staged at t - t0 = cn - 1 - cl
         const double x = s_x[li * XP + (cn - 1 - cl)];
         Pb[static_cast<std::int64_t>(li) * n + clo + cl] = x;
-        if (!s_lead[li] && !s_sf[clo + cl]) lmax = lmax > dbits_s(fabs(x)) ? lmax : dbits_s(fabs(x));
+        if (!a.defer_back && !s_lead[li] && !s_sf[clo + cl]) lmax = lmax > dbits_s(fabs(x)) ? lmax : dbits_s(fabs(x));
       }
     }
     __syncthreads();
@@ -647,6 +652,100 @@ __global__ void __launch_bounds__(128) k_last_solve(const FitArgs a) {
     if (mx) atomicMax(a.linf_int + b, mx);
   }
 }
+
+
+// ------------------------------------------------------- deferred axis-0 L^-T
+// x = L0^-T y along axis 0 of every held lattice P_b = [n0][rest] (rest =
+// n1 [x n2]): thread per trailing index, in place, y values prefetched PF
+// rows ahead, static window slots; then the per-block L-inf over non-shared
+// controls (the dp denominator, solver.cpp:402-405).
+constexpr int kBacksubThreads = 64;
+
+template <int P>
+__global__ void __launch_bounds__(kBacksubThreads) k_axis0_backsub(const FitArgs a) {
+  extern __shared__ __align__(16) double s_lt0[];  // (n0 + 1) x (P+1): [1/L(c,c), L(c+1,c) .. L(c+P,c)]
+  __shared__ unsigned long long s_red[32];
+  constexpr int PF = P * ((32 + P - 1) / P);  // rows of y in flight per thread (latency-bound chain)
+  const int b = blockIdx.y;
+  const BlockDev& blk = a.blocks[b];
+  const AxisProb p0 = a.probs[blk.ax[0]];
+  const int n0 = p0.n, D = a.D;
+  std::int64_t rest = 1;
+  for (int k = 1; k < D; ++k) rest *= a.probs[blk.ax[k]].n;
+  const std::int64_t t = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (static_cast<std::int64_t>(blockIdx.x) * blockDim.x >= rest) return;
+  const bool active = t < rest;
+  const double* lt = a.ltab + p0.col_off * (2 * P + 1);
+  for (int i = threadIdx.x; i < (n0 + 1) * (P + 1); i += blockDim.x) {
+    const int c = i / (P + 1), k = i - c * (P + 1);
+    s_lt0[i] = c < n0 ? lt[static_cast<std::int64_t>(c) * (2 * P + 1) + (k == 0 ? 0 : P + k)] : 0.0;
+  }
+  __syncthreads();
+  // is this trailing index shared along dims >= 1?
+  bool trail_shared = false;
+  {
+    std::int64_t r = active ? t : 0;
+    for (int k = D - 1; k >= 1; --k) {
+      const AxisProb pk = a.probs[blk.ax[k]];
+      const std::int64_t ik = r % pk.n;
+      r /= pk.n;
+      if (a.shared_flag[a.sflag_off[k] + pk.col_lo + ik]) trail_shared = true;
+    }
+  }
+  const unsigned char* sf0 = a.shared_flag + a.sflag_off[0] + p0.col_lo;
+  double* col = a.P + blk.poff + (active ? t : 0);
+  double yr[PF];
+#pragma unroll
+  for (int u = 0; u < PF; ++u) yr[u] = (active && n0 - 1 - u >= 0) ? col[static_cast<std::int64_t>(n0 - 1 - u) * rest] : 0.0;
+  double xw[P];
+#pragma unroll
+  for (int k = 0; k < P; ++k) xw[k] = 0.0;
+  unsigned long long lmax = 0ull;
+  for (int c0 = n0 - 1; c0 >= 0; c0 -= PF) {
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+      const int c = c0 - u;
+      if (c >= 0) {
+        const double* Lc = s_lt0 + c * (P + 1);
+        double sacc = yr[u];
+        const int cn = c - PF;
+        yr[u] = (active && cn >= 0) ? col[static_cast<std::int64_t>(cn) * rest] : 0.0;
+#pragma unroll
+        for (int k = P; k >= 1; --k) sacc = fma(-Lc[k], xw[(u - k + PF) % P], sacc);
+        const double x = sacc * Lc[0];
+        xw[u % P] = x;
+        if (active) {
+          col[static_cast<std::int64_t>(c) * rest] = x;
+          if (!trail_shared && !sf0[c]) lmax = lmax > dbits_s(fabs(x)) ? lmax : dbits_s(fabs(x));
+        }
+      }
+    }
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long t2 = __shfl_xor_sync(kFullMask, lmax, o);
+    lmax = lmax > t2 ? lmax : t2;
+  }
+  if (lane == 0) s_red[warp] = lmax;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long mx = 0ull;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) mx = mx > s_red[w] ? mx : s_red[w];
+    if (mx) atomicMax(a.linf_int + b, mx);
+  }
+}
+
+template <int P>
+struct BacksubLaunch {
+  static int run(const FitArgs& a, int max_n0, std::int64_t max_rest, cudaStream_t s) {
+    const size_t smem = static_cast<size_t>(max_n0 + 1) * (P + 1) * sizeof(double);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_axis0_backsub<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    dim3 grid(static_cast<unsigned>((max_rest + kBacksubThreads - 1) / kBacksubThreads), a.nblocks);
+    k_axis0_backsub<P><<<grid, kBacksubThreads, smem, s>>>(a);
+    return 1;
+  }
+};
 
 // ---------------------------------------------------------------- decode
 template <int P, int D, int S>
@@ -906,10 +1005,16 @@ struct Axis0Launch {
                  int zdim = 1) {
     const StageLayout SL = stage_layout(kFitR, g.B1 * g.B2, P);
     const size_t smem = static_cast<size_t>(S) * SL.stage_bytes + 128 + static_cast<size_t>(g.lt_cap) * 8;
-    cudaFuncSetAttribute(k_fit_axis0_tma<P, S, NC, MID>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
     dim3 grid(ntiles, a.nblocks, zdim);
-    k_fit_axis0_tma<P, S, NC, MID><<<grid, g.B1 * g.B2 / NC, smem, s>>>(a, map, g);
+    if (!MID && a.defer_back) {
+      cudaFuncSetAttribute(k_fit_axis0_tma<P, S, NC, MID, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem));
+      k_fit_axis0_tma<P, S, NC, MID, false><<<grid, g.B1 * g.B2 / NC, smem, s>>>(a, map, g);
+    } else {
+      cudaFuncSetAttribute(k_fit_axis0_tma<P, S, NC, MID>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem));
+      k_fit_axis0_tma<P, S, NC, MID><<<grid, g.B1 * g.B2 / NC, smem, s>>>(a, map, g);
+    }
   }
   static int run(const FitArgs& a, const CUtensorMap& map, const TmaGeom& g, int ntiles, cudaStream_t s) {
     // NC = 2 (two columns per thread) measured slower on C5 (331 vs 233 us): fewer resident warps
@@ -983,6 +1088,10 @@ int debug_fail_line_tma() {
   cudaMemcpyFromSymbol(&line, g_tma_debug_line, sizeof(int));
 #endif
   return line;
+}
+
+int launch_axis0_backsub(int degree, const FitArgs& a, int max_n0, std::int64_t max_rest, cudaStream_t s) {
+  return dispatch_p<BacksubLaunch>(degree, a, max_n0, max_rest, s);
 }
 
 int launch_fit_last_tma(int degree, const FitArgs& a, const CUtensorMap& map, int LT, int lt_cap, int kseg,
