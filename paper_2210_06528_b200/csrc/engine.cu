@@ -292,6 +292,17 @@ struct Workload {
   mfb::TmaGeom axis0_geo{1, 1, 16, 4, 0};
   int axis0_tiles = 0;
   // TMA last-axis pass (D >= 2)
+  // axis-0 sweep as a pure contraction (defer 2): Gram/Cholesky on a side
+  // stream, overlapping the sweep (fork after the basis rows, join before the
+  // first pass that needs a factor)
+  int defer_mode = 0;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_rows = nullptr, ev_chol = nullptr;
+  ~Workload() {
+    if (ev_rows) cudaEventDestroy(ev_rows);
+    if (ev_chol) cudaEventDestroy(ev_chol);
+    if (side) cudaStreamDestroy(side);
+  }
   bool tma_mid = false;  // D = 3 middle axis through a T1 tensor map
   mfb::TmaGeom mid_geo{1, 1, 8, 4, 0};
   int mid_tiles = 0, mid_n0 = 0;
@@ -344,6 +355,10 @@ struct Workload {
       tma_last = true;
       plan_segments();
     }
+    // Axis-0 solve deferred to the held lattices (stream_tma.cu k_axis0_backsub):
+    // 2 = the sweep only contracts (Gram/Cholesky overlap it), 1 = only the
+    // back substitution is deferred, 0 = fused (MFADD_DEFER overrides).
+    if (tma_last) defer_mode = std::getenv("MFADD_DEFER") ? std::atoi(std::getenv("MFADD_DEFER")) : 2;
     // D = 3 middle axis: per (block, c0) slice of T1 = [m1 rows][pitch]
     if (D == 3 && !std::getenv("MFADD_NO_TMA_MID")) {
       int mx = 0, mxn1 = 0, mxn0 = 0;
@@ -488,9 +503,26 @@ struct Workload {
     for (int id : factor_ids) max_m_factor = std::max(max_m_factor, probs[static_cast<std::size_t>(id)].m);
     mfb::CholArgs ca{d_probs.p, d_factor.p, static_cast<int>(factor_ids.size()), max_n_factor, max_m_factor, 0, g0.p,
                      vals.p, ltab.p, ctx->d_status};
-    tl->begin("gram_chol");
-    l += mfb::launch_gram_chol(p, ca, ctx->stream);
-    tl->end();
+    if (defer_mode == 2) {  // fork: the factorizations run beside the axis-0 contraction
+      if (!side) {
+        CK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&ev_rows, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ev_chol, cudaEventDisableTiming));
+      }
+      CK(cudaEventRecord(ev_rows, ctx->stream));
+      CK(cudaStreamWaitEvent(side, ev_rows, 0));
+      cudaStream_t main_st = tl->st;
+      tl->st = side;
+      tl->begin("gram_chol");
+      l += mfb::launch_gram_chol(p, ca, side);
+      tl->end();
+      tl->st = main_st;
+      CK(cudaEventRecord(ev_chol, side));
+    } else {
+      tl->begin("gram_chol");
+      l += mfb::launch_gram_chol(p, ca, ctx->stream);
+      tl->end();
+    }
     CK(cudaGetLastError());
     return l;
   }
@@ -526,8 +558,7 @@ struct Workload {
     fa.segtab = d_segtab.p;
     fa.zhalf = zhalf;
     // axis 0 forward-only, L0^-T on the held lattices at the end (stream_tma.cu)
-    static const bool no_defer = std::getenv("MFADD_NO_DEFER") != nullptr;
-    fa.defer_back = (tma_axis0 && tma_last && !no_defer) ? 1 : 0;
+    fa.defer_back = defer_mode;
     fa.n_field = field_n;
     fa.n_t1 = total_t1;
     fa.n_t2 = total_t2;
@@ -559,7 +590,9 @@ struct Workload {
         l += mfb::launch_fit_strided(p, fa, d, ctx->stream);
       }
       tl->end();
+      if (d == 0 && defer_mode == 2) CK(cudaStreamWaitEvent(ctx->stream, ev_chol, 0));  // join the factorizations
     }
+    if (D == 1 && defer_mode == 2) CK(cudaStreamWaitEvent(ctx->stream, ev_chol, 0));
     tl->begin("fit_last");
     if (tma_last) {
       const double* src = D == 2 ? t1.p : t2.p;
@@ -577,7 +610,9 @@ struct Workload {
     if (fa.defer_back) {
       int mxn0 = 0;
       std::int64_t mxr = 1;
+      fa.min_n0 = 1 << 30;
       for (const auto& b : blocks) {
+        fa.min_n0 = std::min(fa.min_n0, probs[static_cast<std::size_t>(b.ax[0])].n);
         mxn0 = std::max(mxn0, probs[static_cast<std::size_t>(b.ax[0])].n);
         std::int64_t r = 1;
         for (int k = 1; k < D; ++k) r *= probs[static_cast<std::size_t>(b.ax[k])].n;

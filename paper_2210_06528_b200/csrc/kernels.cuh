@@ -71,7 +71,8 @@ struct FitArgs {
   std::int64_t n_field, n_t1, n_t2, n_P;  // buffer sizes (debug bounds checks)
   const int* segtab;                 // last-axis row segments per axis problem (kSegStride ints)
   std::int64_t zhalf;                // last-axis contraction: Y = [parity 0 | parity 1 | y scratch]
-  int defer_back;                    // axis 0 forward-only; L0^-T applied to P by k_axis0_backsub
+  int defer_back;                    // 1: axis 0 forward-only, 2: contraction only; the rest on P at the end
+  int min_n0;                        // smallest axis-0 held extent (partitioned final solve eligibility)
 };
 int launch_fit_strided(int degree, const FitArgs& a, int axis, cudaStream_t s);  // axis < D-1
 int launch_fit_last(int degree, const FitArgs& a, cudaStream_t s);

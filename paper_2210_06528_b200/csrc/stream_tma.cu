@@ -82,7 +82,10 @@ constexpr int kFitR = 8;  // rows per TMA stage (fit axis 0)
 // the L^-T half of the axis-0 solve then runs on the held lattice at the end
 // (k_axis0_backsub): the axis operators commute, so the result is the same up
 // to rounding while T1 is written once instead of written, re-read, rewritten.
-template <int P, int S, int NC, bool MID, bool BACK = true>
+// FWD = false (axis 0 when FitArgs::defer_back == 2): contraction only, the
+// whole G0^-1 solve runs on the held lattices at the end (no factor needed
+// during the sweep, so the Gram/Cholesky setup overlaps it).
+template <int P, int S, int NC, bool MID, bool BACK = true, bool FWD = true>
 __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __grid_constant__ CUtensorMap map,
                                                        const TmaGeom geo) {
   constexpr int R = kFitR;
@@ -179,10 +182,11 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
   // mostly carved out for the TMA ring).
   double* s_lt = reinterpret_cast<double*>(sm_raw + S * SL.stage_bytes + 128);
   constexpr int LW = 2 * P + 1;
-  for (int i = tid; i < (n + 2 * (P + 1)) * LW; i += blockDim.x) {
-    const int cc = i / LW - (P + 1);
-    s_lt[i] = (cc >= 0 && cc < n) ? __ldg(lt + static_cast<std::int64_t>(cc) * LW + (i - (i / LW) * LW)) : 0.0;
-  }
+  if (FWD)
+    for (int i = tid; i < (n + 2 * (P + 1)) * LW; i += blockDim.x) {
+      const int cc = i / LW - (P + 1);
+      s_lt[i] = (cc >= 0 && cc < n) ? __ldg(lt + static_cast<std::int64_t>(cc) * LW + (i - (i / LW) * LW)) : 0.0;
+    }
   const double* slt = s_lt + (P + 1) * LW;  // slt[cc * LW + k], cc in [-(P+1), n+P]
   __syncthreads();
   if (tid == 0)
@@ -203,6 +207,7 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
   // rows whose span starts at c is accumulated into slots (u + k) mod (P+1).
   double Lnx[P + 1];  // forward coefficients of column cbase, fetched one column ahead
   auto fetch_fwd = [&](int cc) {
+    if (!FWD) return;
     const double* Lc = slt + (cc < -(P + 1) ? -(P + 1) : cc) * LW;
 #pragma unroll
     for (int k = 0; k <= P; ++k) Lnx[k] = Lc[k];
@@ -262,15 +267,19 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
         }
         advance();
       }
-      if (cbase >= 0) {  // forward substitution of column cbase (< n)
+      if (cbase >= 0) {  // forward substitution of column cbase (< n), or just R^T q
 #pragma unroll
         for (int e = 0; e < NC; ++e) {
-          double sacc = acc[e][u];
+          if (FWD) {
+            double sacc = acc[e][u];
 #pragma unroll
-          for (int k = P; k >= 1; --k) sacc = fma(-Lnx[k], yv[e][(u + P + 1 - k) % (P + 1)], sacc);
-          const double y = sacc * Lnx[0];
-          if (act[e]) dst[e][yoff] = y;
-          yv[e][u] = y;
+            for (int k = P; k >= 1; --k) sacc = fma(-Lnx[k], yv[e][(u + P + 1 - k) % (P + 1)], sacc);
+            const double y = sacc * Lnx[0];
+            if (act[e]) dst[e][yoff] = y;
+            yv[e][u] = y;
+          } else if (act[e]) {
+            dst[e][yoff] = acc[e][u];
+          }
         }
       }
       yoff += dstr;
@@ -663,7 +672,7 @@ constexpr int kBacksubThreads = 64;
 
 template <int P>
 __global__ void __launch_bounds__(kBacksubThreads) k_axis0_backsub(const FitArgs a) {
-  extern __shared__ __align__(16) double s_lt0[];  // (n0 + 1) x (P+1): [1/L(c,c), L(c+1,c) .. L(c+P,c)]
+  extern __shared__ __align__(16) double s_lt0[];  // (n0 + 1) x (P+1) backward, then (n0 + 1) x (P+1) forward
   __shared__ unsigned long long s_red[32];
   constexpr int PF = P * ((32 + P - 1) / P);  // rows of y in flight per thread (latency-bound chain)
   const int b = blockIdx.y;
@@ -676,9 +685,12 @@ __global__ void __launch_bounds__(kBacksubThreads) k_axis0_backsub(const FitArgs
   if (static_cast<std::int64_t>(blockIdx.x) * blockDim.x >= rest) return;
   const bool active = t < rest;
   const double* lt = a.ltab + p0.col_off * (2 * P + 1);
+  const bool fwd = a.defer_back == 2;  // full G0^-1 (forward then back), else L0^-T only
+  double* s_f0 = s_lt0 + (n0 + 1) * (P + 1);  // [1/L(c,c), L(c,c-1) .. L(c,c-P)]
   for (int i = threadIdx.x; i < (n0 + 1) * (P + 1); i += blockDim.x) {
     const int c = i / (P + 1), k = i - c * (P + 1);
     s_lt0[i] = c < n0 ? lt[static_cast<std::int64_t>(c) * (2 * P + 1) + (k == 0 ? 0 : P + k)] : 0.0;
+    if (fwd) s_f0[i] = c < n0 ? lt[static_cast<std::int64_t>(c) * (2 * P + 1) + k] : 0.0;
   }
   __syncthreads();
   // is this trailing index shared along dims >= 1?
@@ -694,6 +706,30 @@ __global__ void __launch_bounds__(kBacksubThreads) k_axis0_backsub(const FitArgs
   }
   const unsigned char* sf0 = a.shared_flag + a.sflag_off[0] + p0.col_lo;
   double* col = a.P + blk.poff + (active ? t : 0);
+  if (fwd) {  // y = L0^-1 w in place, w values prefetched PF rows ahead
+    double wr[PF], yw[P];
+#pragma unroll
+    for (int u = 0; u < PF; ++u) wr[u] = (active && u < n0) ? col[static_cast<std::int64_t>(u) * rest] : 0.0;
+#pragma unroll
+    for (int k = 0; k < P; ++k) yw[k] = 0.0;
+    for (int c0 = 0; c0 < n0; c0 += PF) {
+#pragma unroll
+      for (int u = 0; u < PF; ++u) {
+        const int c = c0 + u;
+        if (c < n0) {
+          const double* Lc = s_f0 + c * (P + 1);
+          double sacc = wr[u];
+          const int cn = c + PF;
+          wr[u] = (active && cn < n0) ? col[static_cast<std::int64_t>(cn) * rest] : 0.0;
+#pragma unroll
+          for (int k = P; k >= 1; --k) sacc = fma(-Lc[k], yw[(u - k + PF) % P], sacc);
+          const double y = sacc * Lc[0];
+          yw[u % P] = y;
+          if (active) col[static_cast<std::int64_t>(c) * rest] = y;
+        }
+      }
+    }
+  }
   double yr[PF];
 #pragma unroll
   for (int u = 0; u < PF; ++u) yr[u] = (active && n0 - 1 - u >= 0) ? col[static_cast<std::int64_t>(n0 - 1 - u) * rest] : 0.0;
@@ -736,10 +772,265 @@ __global__ void __launch_bounds__(kBacksubThreads) k_axis0_backsub(const FitArgs
   }
 }
 
+// Partitioned form of the same solve (FitArgs::defer_back == 2: forward then
+// back substitution with the axis-0 factor) for more parallelism per column:
+// each column is cut into K segments, one thread each.  A segment is first
+// solved with zero carry-in (y0); the true solution is y0 + F_k c_k where c_k
+// holds the P values just before the segment and F_k (len x P) is the
+// segment's response to unit carries, a property of the factor alone (built
+// per CTA in smem).  Carries are propagated segment to segment with the last
+// P rows of F_k (P x P), then every segment is corrected.  The back
+// substitution runs the same scheme from the bottom.  P is L2-resident here,
+// so the extra passes over it are cheap next to the latency they hide.
+constexpr int kPartSeg = 4;
+constexpr int kPartCols = 32;
+
+template <int P>
+__global__ void __launch_bounds__(kPartSeg * kPartCols) k_axis0_solve_part(const FitArgs a) {
+  extern __shared__ __align__(16) double s_part[];
+  __shared__ unsigned long long s_red[32];
+  constexpr int K = kPartSeg, NCOL = kPartCols, LW = 2 * P + 1;
+  const int b = blockIdx.y;
+  const BlockDev& blk = a.blocks[b];
+  const AxisProb p0 = a.probs[blk.ax[0]];
+  const int n0 = p0.n, D = a.D;
+  std::int64_t rest = 1;
+  for (int k = 1; k < D; ++k) rest *= a.probs[blk.ax[k]].n;
+  const std::int64_t col0 = static_cast<std::int64_t>(blockIdx.x) * NCOL;
+  if (col0 >= rest) return;
+  const int tid = threadIdx.x, cl = tid % NCOL, sg = tid / NCOL;
+  const std::int64_t t = col0 + cl;
+  const bool active = t < rest;
+  // smem: factor (n0 x LW) | F responses (n0 x P) | B responses (n0 x P) | carries K x NCOL x P (x2)
+  double* s_l = s_part;
+  double* s_F = s_l + n0 * LW;
+  double* s_B = s_F + n0 * P;
+  double* s_tail = s_B + n0 * P;         // [K][NCOL][P]: last P values of each segment's zero-carry solve
+  double* s_car = s_tail + K * NCOL * P;  // [K][NCOL][P]: carry into each segment
+  double* s_x = s_car + K * NCOL * P;     // [n0][NCOL]: the CTA's column tile of P_b
+  const double* lt = a.ltab + p0.col_off * LW;
+  // global -> smem with 8 independent loads in flight per thread (the copies
+  // are otherwise serialised on each load's latency)
+  auto stage = [&](double* dst, auto src_of, int count) {
+    constexpr int B = 8;
+    for (int i0 = tid; i0 < count; i0 += B * static_cast<int>(blockDim.x)) {
+      double v[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const int i = i0 + u * static_cast<int>(blockDim.x);
+        v[u] = i < count ? src_of(i) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const int i = i0 + u * static_cast<int>(blockDim.x);
+        if (i < count) dst[i] = v[u];
+      }
+    }
+  };
+  stage(s_l, [&](int i) { return __ldg(lt + i); }, n0 * LW);
+  __syncthreads();
+  auto seg_lo = [&](int k) { return static_cast<int>(static_cast<std::int64_t>(k) * n0 / K); };
+  // response matrices: thread (k, j) for k = 1..K-1, j < P
+  if (tid < (K - 1) * P) {
+    const int k = 1 + tid / P, j = tid % P, lo = seg_lo(k), hi = seg_lo(k + 1);
+    double w[P];  // w[m-1] = value at row c-m (carry unit vector e_j: row lo-1-j)
+#pragma unroll
+    for (int m = 0; m < P; ++m) w[m] = m == j ? 1.0 : 0.0;
+    for (int c = lo; c < hi; ++c) {  // forward: y_c = -(sum_m L(c,c-m) y_{c-m}) / L(c,c)
+      const double* Lc = s_l + c * LW;
+      double sacc = 0.0;
+#pragma unroll
+      for (int m = P; m >= 1; --m) sacc = fma(-Lc[m], w[m - 1], sacc);
+      const double y = sacc * Lc[0];
+#pragma unroll
+      for (int m = P - 1; m >= 1; --m) w[m] = w[m - 1];
+      w[0] = y;
+      s_F[c * P + j] = y;
+    }
+  } else if (tid >= 64 && tid < 64 + (K - 1) * P) {
+    const int q = tid - 64, k = q / P, j = q % P, lo = seg_lo(k), hi = seg_lo(k + 1);  // k = 0..K-2
+    double w[P];  // w[m-1] = value at row c+m (carry unit vector e_j: row hi+j)
+#pragma unroll
+    for (int m = 0; m < P; ++m) w[m] = m == j ? 1.0 : 0.0;
+    for (int c = hi - 1; c >= lo; --c) {  // back: x_c = -(sum_m L(c+m,c) x_{c+m}) / L(c,c)
+      const double* Lc = s_l + c * LW;
+      double sacc = 0.0;
+#pragma unroll
+      for (int m = P; m >= 1; --m) sacc = fma(-Lc[P + m], w[m - 1], sacc);
+      const double x = sacc * Lc[0];
+#pragma unroll
+      for (int m = P - 1; m >= 1; --m) w[m] = w[m - 1];
+      w[0] = x;
+      s_B[c * P + j] = x;
+    }
+  }
+  // the column tile -> smem (independent coalesced loads), solved there, written back once
+  double* Pt = a.P + blk.poff + col0;
+  const int ncl = static_cast<int>(rest - col0 < NCOL ? rest - col0 : NCOL);
+  stage(s_x, [&](int i) {
+    const int c = i / NCOL, j = i - c * NCOL;
+    return j < ncl ? Pt[static_cast<std::int64_t>(c) * rest + j] : 0.0;
+  }, n0 * NCOL);
+  __syncthreads();
+  double* xs = s_x + cl;  // this thread's column: xs[c * NCOL]
+  const int lo = seg_lo(sg), hi = seg_lo(sg + 1);
+  // (1) forward, zero carry-in
+  {
+    double w[P];
+#pragma unroll
+    for (int m = 0; m < P; ++m) w[m] = 0.0;
+    for (int c = lo; c < hi; ++c) {
+      const double* Lc = s_l + c * LW;
+      double sacc = xs[c * NCOL];
+#pragma unroll
+      for (int m = P; m >= 1; --m) sacc = fma(-Lc[m], w[m - 1], sacc);
+      const double y = sacc * Lc[0];
+#pragma unroll
+      for (int m = P - 1; m >= 1; --m) w[m] = w[m - 1];
+      w[0] = y;
+      xs[c * NCOL] = y;
+    }
+#pragma unroll
+    for (int m = 0; m < P; ++m) s_tail[(sg * NCOL + cl) * P + m] = w[m];  // w[m] = y at row hi-1-m
+  }
+  __syncthreads();
+  // (2) carries: c_0 = 0, c_{k+1}[m] = y0_k(hi-1-m) + sum_j F_k(hi-1-m, j) c_k[j]
+  if (sg == 0) {
+    double c[P];
+#pragma unroll
+    for (int m = 0; m < P; ++m) c[m] = 0.0;
+    for (int k = 0; k + 1 < K; ++k) {
+      const int hk = seg_lo(k + 1);
+      double nc[P];
+#pragma unroll
+      for (int m = 0; m < P; ++m) {
+        double v = s_tail[(k * NCOL + cl) * P + m];
+        if (k > 0)
+#pragma unroll
+          for (int j = 0; j < P; ++j) v = fma(s_F[(hk - 1 - m) * P + j], c[j], v);
+        nc[m] = v;
+      }
+#pragma unroll
+      for (int m = 0; m < P; ++m) {
+        c[m] = nc[m];
+        s_car[((k + 1) * NCOL + cl) * P + m] = nc[m];
+      }
+    }
+  }
+  __syncthreads();
+  // (3) correct segments k >= 1 (y = y0 + F c), then (4) back, zero carry-in
+  {
+    double cf[P];
+#pragma unroll
+    for (int j = 0; j < P; ++j) cf[j] = sg > 0 ? s_car[(sg * NCOL + cl) * P + j] : 0.0;
+    double w[P];
+#pragma unroll
+    for (int m = 0; m < P; ++m) w[m] = 0.0;
+    // a segment's back pass needs its own corrected y: fuse (3) into (4) bottom-up
+    for (int c = hi - 1; c >= lo; --c) {
+      double y = xs[c * NCOL];
+      if (sg > 0)
+#pragma unroll
+        for (int j = 0; j < P; ++j) y = fma(s_F[c * P + j], cf[j], y);
+      const double* Lc = s_l + c * LW;
+      double sacc = y;
+#pragma unroll
+      for (int m = P; m >= 1; --m) sacc = fma(-Lc[P + m], w[m - 1], sacc);
+      const double x = sacc * Lc[0];
+#pragma unroll
+      for (int m = P - 1; m >= 1; --m) w[m] = w[m - 1];
+      w[0] = x;
+      xs[c * NCOL] = x;
+    }
+#pragma unroll
+    for (int m = 0; m < P; ++m) s_tail[(sg * NCOL + cl) * P + m] = w[m];  // w[m] = x0 at row lo+m
+  }
+  __syncthreads();
+  // (5) back carries from the bottom: d_{K-1} = 0, d_{k-1}[m] = x0_k(lo_k+m) + sum_j B_k(lo_k+m, j) d_k[j]
+  if (sg == 0) {
+    double d[P];
+#pragma unroll
+    for (int m = 0; m < P; ++m) d[m] = 0.0;
+    for (int k = K - 1; k >= 1; --k) {
+      const int lk = seg_lo(k);
+      double nd[P];
+#pragma unroll
+      for (int m = 0; m < P; ++m) {
+        double v = s_tail[(k * NCOL + cl) * P + m];
+        if (k < K - 1)
+#pragma unroll
+          for (int j = 0; j < P; ++j) v = fma(s_B[(lk + m) * P + j], d[j], v);
+        nd[m] = v;
+      }
+#pragma unroll
+      for (int m = 0; m < P; ++m) {
+        d[m] = nd[m];
+        s_car[((k - 1) * NCOL + cl) * P + m] = nd[m];
+      }
+    }
+  }
+  __syncthreads();
+  // (6) correct segments k < K-1 (x = x0 + B d) and the L-inf of non-shared controls
+  bool trail_shared = false;
+  {
+    std::int64_t r = active ? t : 0;
+    for (int k = D - 1; k >= 1; --k) {
+      const AxisProb pk = a.probs[blk.ax[k]];
+      const std::int64_t ik = r % pk.n;
+      r /= pk.n;
+      if (a.shared_flag[a.sflag_off[k] + pk.col_lo + ik]) trail_shared = true;
+    }
+  }
+  const unsigned char* sf0 = a.shared_flag + a.sflag_off[0] + p0.col_lo;
+  unsigned long long lmax = 0ull;
+  {
+    double df[P];
+#pragma unroll
+    for (int j = 0; j < P; ++j) df[j] = sg < K - 1 ? s_car[(sg * NCOL + cl) * P + j] : 0.0;
+    for (int c = lo; c < hi; ++c) {
+      double x = xs[c * NCOL];
+      if (sg < K - 1) {
+#pragma unroll
+        for (int j = 0; j < P; ++j) x = fma(s_B[c * P + j], df[j], x);
+        xs[c * NCOL] = x;
+      }
+      if (active && !trail_shared && !sf0[c]) lmax = lmax > dbits_s(fabs(x)) ? lmax : dbits_s(fabs(x));
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < n0 * NCOL; i += blockDim.x) {
+    const int c = i / NCOL, j = i - c * NCOL;
+    if (j < ncl) Pt[static_cast<std::int64_t>(c) * rest + j] = s_x[i];
+  }
+  const int lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long t2 = __shfl_xor_sync(kFullMask, lmax, o);
+    lmax = lmax > t2 ? lmax : t2;
+  }
+  if (lane == 0) s_red[warp] = lmax;
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long mx = 0ull;
+    for (int w2 = 0; w2 < static_cast<int>(blockDim.x >> 5); ++w2) mx = mx > s_red[w2] ? mx : s_red[w2];
+    if (mx) atomicMax(a.linf_int + b, mx);
+  }
+}
+
 template <int P>
 struct BacksubLaunch {
   static int run(const FitArgs& a, int max_n0, std::int64_t max_rest, cudaStream_t s) {
-    const size_t smem = static_cast<size_t>(max_n0 + 1) * (P + 1) * sizeof(double);
+    static const bool no_part = std::getenv("MFADD_NO_PART") != nullptr;
+    if (a.defer_back == 2 && !no_part && a.min_n0 >= kPartSeg * 2 * (P + 1)) {
+      const size_t smem = (static_cast<size_t>(max_n0) * (2 * P + 1) + 2 * static_cast<size_t>(max_n0) * P +
+                           2 * static_cast<size_t>(kPartSeg) * kPartCols * P + static_cast<size_t>(max_n0) * kPartCols) *
+                          sizeof(double);
+      cudaFuncSetAttribute(k_axis0_solve_part<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      dim3 grid(static_cast<unsigned>((max_rest + kPartCols - 1) / kPartCols), a.nblocks);
+      k_axis0_solve_part<P><<<grid, kPartSeg * kPartCols, smem, s>>>(a);
+      return 1;
+    }
+    const size_t smem = 2 * static_cast<size_t>(max_n0 + 1) * (P + 1) * sizeof(double);
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_axis0_backsub<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     dim3 grid(static_cast<unsigned>((max_rest + kBacksubThreads - 1) / kBacksubThreads), a.nblocks);
     k_axis0_backsub<P><<<grid, kBacksubThreads, smem, s>>>(a);
@@ -1006,7 +1297,12 @@ struct Axis0Launch {
     const StageLayout SL = stage_layout(kFitR, g.B1 * g.B2, P);
     const size_t smem = static_cast<size_t>(S) * SL.stage_bytes + 128 + static_cast<size_t>(g.lt_cap) * 8;
     dim3 grid(ntiles, a.nblocks, zdim);
-    if (!MID && a.defer_back) {
+    if (!MID && a.defer_back == 2) {  // contraction only: no factor table in smem
+      const size_t smem_c = static_cast<size_t>(S) * SL.stage_bytes + 128;
+      cudaFuncSetAttribute(k_fit_axis0_tma<P, S, NC, MID, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem_c));
+      k_fit_axis0_tma<P, S, NC, MID, false, false><<<grid, g.B1 * g.B2 / NC, smem_c, s>>>(a, map, g);
+    } else if (!MID && a.defer_back) {
       cudaFuncSetAttribute(k_fit_axis0_tma<P, S, NC, MID, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(smem));
       k_fit_axis0_tma<P, S, NC, MID, false><<<grid, g.B1 * g.B2 / NC, smem, s>>>(a, map, g);
