@@ -33,7 +33,7 @@ struct AxisProb {
 // One block of the decomposition as the fit kernels see it.
 struct BlockDev {
   int ax[3];           // AxisProb id per dim
-  int pad_;
+  int zl;              // last-axis contraction buffer: column pitch in lines (even, = 2 mod 4)
   std::int64_t fbase;  // field offset of the input box origin (input_lo per dim)
   std::int64_t poff;   // offset of the held lattice P_b
   std::int64_t t1off;  // axis-0 intermediate   [n0][m1][m2]

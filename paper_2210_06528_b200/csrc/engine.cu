@@ -409,8 +409,11 @@ struct Workload {
     for (auto& b : blocks) {
       std::int64_t Ll = 1;
       for (int k = 0; k + 1 < D; ++k) Ll *= probs[static_cast<std::size_t>(b.ax[k])].n;
+      // column pitch: even (16-B aligned bulk copies of columns) and = 2 mod 4
+      // (k_solve2d's column-parallel phase then has at most 2-way conflicts)
+      b.zl = static_cast<int>((Ll + 1) / 4 * 4 + 2);
       b.zoff = zhalf;
-      zhalf += (probs[static_cast<std::size_t>(b.ax[D - 1])].n + 2 * (p + 1)) * Ll;
+      zhalf += (probs[static_cast<std::size_t>(b.ax[D - 1])].n + 2 * (p + 1)) * b.zl;
     }
   }
 
@@ -593,6 +596,14 @@ struct Workload {
       if (d == 0 && defer_mode == 2) CK(cudaStreamWaitEvent(ctx->stream, ev_chol, 0));  // join the factorizations
     }
     if (D == 1 && defer_mode == 2) CK(cudaStreamWaitEvent(ctx->stream, ev_chol, 0));
+    if (D == 2 && defer_mode == 2 && tma_last && !std::getenv("MFADD_NO_FUSE2D")) {
+      for (const auto& b : blocks) {
+        fa.max_n0 = std::max(fa.max_n0, probs[static_cast<std::size_t>(b.ax[0])].n);
+        fa.max_n1 = std::max(fa.max_n1, probs[static_cast<std::size_t>(b.ax[1])].n);
+        fa.max_zl = std::max(fa.max_zl, b.zl);
+      }
+      fa.fuse2d = mfb::solve2d_smem(p, fa.max_n0, fa.max_n1, fa.max_zl, last_kseg) > 0 ? 1 : 0;
+    }
     tl->begin("fit_last");
     if (tma_last) {
       const double* src = D == 2 ? t1.p : t2.p;
@@ -607,7 +618,7 @@ struct Workload {
       l += mfb::launch_fit_last(p, fa, ctx->stream);
     }
     tl->end();
-    if (fa.defer_back) {
+    if (fa.defer_back && !fa.fuse2d) {
       int mxn0 = 0;
       std::int64_t mxr = 1;
       fa.min_n0 = 1 << 30;

@@ -73,9 +73,13 @@ struct FitArgs {
   std::int64_t zhalf;                // last-axis contraction: Y = [parity 0 | parity 1 | y scratch]
   int defer_back;                    // 1: axis 0 forward-only, 2: contraction only; the rest on P at the end
   int min_n0;                        // smallest axis-0 held extent (partitioned final solve eligibility)
+  int fuse2d;                        // D = 2: k_solve2d (CTA per block) replaces k_last_solve + the axis-0 solve
+  int max_n0, max_n1, max_zl;        // largest held extents / Z pitch (k_solve2d shared-memory size)
 };
 int launch_fit_strided(int degree, const FitArgs& a, int axis, cudaStream_t s);  // axis < D-1
 int launch_fit_last(int degree, const FitArgs& a, cudaStream_t s);
+// Shared-memory bytes of k_solve2d for held extents n0 x n1 (0 if it does not fit one CTA).
+size_t solve2d_smem(int degree, int n0, int n1, int zl, int kseg);
 // D = 1: CTA per block, column-parallel R^T q + serial banded solve (smem: max_n x (2P+2) doubles).
 int launch_fit_1d(int degree, const FitArgs& a, int max_n, cudaStream_t s);
 

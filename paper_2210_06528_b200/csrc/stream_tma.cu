@@ -424,7 +424,8 @@ __global__ void __launch_bounds__(256) k_last_contract_tma(const FitArgs a, cons
   for (int k = 0; k <= P; ++k) acc[k] = 0.0;
   int cbase = __ldg(g0g + js);
   if (sgi == 0 && cbase > 0) cbase = 0;
-  double* zp = a.Y + (sgi & 1) * a.zhalf + blk.zoff + static_cast<std::int64_t>(cbase + PADC) * L + l0 + tid;
+  const int zl = blk.zl;
+  double* zp = a.Y + (sgi & 1) * a.zhalf + blk.zoff + static_cast<std::int64_t>(cbase + PADC) * zl + l0 + tid;
   const int cend = sgi + 1 < K ? __ldg(g0g + je) + P + 1 : pr.n;
   const int swz = tid & 7;
   // row cursor over the TMA stages: chunk c, local row jl in [.., jhi)
@@ -471,7 +472,7 @@ __global__ void __launch_bounds__(256) k_last_contract_tma(const FitArgs a, cons
         advance();
       }
       if (active) *zp = acc[u];
-      zp += L;
+      zp += zl;
       acc[u] = 0.0;
       if (++cbase >= cend) break;
     }
@@ -538,14 +539,14 @@ __global__ void __launch_bounds__(128) k_last_solve(const FitArgs a) {
   }
   __syncthreads();
   // the two parity buffers of this line, padded column 0
-  const std::int64_t zbase = blk.zoff + static_cast<std::int64_t>(PADC) * L + l0 + tid;
+  const std::int64_t zbase = blk.zoff + static_cast<std::int64_t>(PADC) * blk.zl + l0 + tid;
   const double* z0 = a.Y + zbase;
   const double* z1 = a.Y + a.zhalf + zbase;
   double* yb = a.Y + a.zhalf * 2 + blk.poff + l0 + tid;  // y scratch Y2[c*L + l]
   auto zload = [&](int c) -> double {
     if (!active || c >= n) return 0.0;
     const unsigned code = s_code[c];
-    const std::int64_t o = static_cast<std::int64_t>(c) * L;
+    const std::int64_t o = static_cast<std::int64_t>(c) * blk.zl;
     double z = (code & 1) ? z1[o] : z0[o];
     if (code & 2) z += (code & 1) ? z0[o] : z1[o];  // carry of the previous segment
     return z;
@@ -1017,6 +1018,237 @@ __global__ void __launch_bounds__(kPartSeg * kPartCols) k_axis0_solve_part(const
   }
 }
 
+// ------------------------------------------- fused 2-D solve (CTA per block)
+// D = 2 with the axis-0 sweep as a pure contraction (defer_back == 2): after
+// k_last_contract_tma the block's whole right-hand side Z = R0^T Q_b R1 is
+// n0 x n1 values, which fit in one CTA's shared memory.  One CTA per block
+// pulls Z in with 1-D bulk copies (one per contraction segment, plus the
+// segment carries), runs the banded G1 solve along every row (thread per
+// row, lsq.cpp:59-60 on axis 1), then the banded G0 solve along every column
+// (thread per column, lsq.cpp:59-60 on axis 0), and writes P_b once plus the
+// per-block L-inf over non-shared controls (solver.cpp:97-101).  Replaces
+// k_last_solve + k_axis0_solve_part: no y scratch round trip through HBM,
+// one launch, no per-element index arithmetic on the load path.
+//
+// Shared-memory tile: X[c][i] in Z's own column-major layout (pitch zl lines,
+// even so every column is 16-B aligned for the bulk copies, = 2 mod 4 so the
+// column-parallel phase has at most 2-way bank conflicts).
+constexpr int kSolve2dThreads = 256;
+
+// Right-looking banded substitution passes on one line of a shared-memory
+// tile.  A pass walks steps t = 0..n-1 over x0[t*ds] (ds < 0 walks a line
+// backwards) with a step table of W doubles per step:
+//   forward  (L y = z,   column c = t):      [L(c+k,c)/L(c+k,c+k) k=1..P, 1/L(c+P,c+P)]
+//   backward (L^T x = y, column c = n-1-t):  [L(c,c-k)/L(c-k,c-k) k=1..P, 1/L(c-P,c-P)]
+// Rows -P..-1 carry only the last entry (the scale of the first P values);
+// rows past the line are zero.  The P pending sums of the next steps sit in
+// static register slots (slot = step mod P; U is a multiple of P).  A
+// finished value updates the pending sums at once, the next step's first,
+// so the dependent chain per step is one FMA; the value P steps ahead enters
+// scaled by its 1/L(c,c).  The arithmetic is the reference's solve
+// (lsq.cpp:59-60) up to rounding order (1e-10 contract).  Full batches run
+// without bounds tests; the last < 2U+P steps run guarded.
+template <int P>
+struct RL {
+  static constexpr int W = (P + 2) & ~1;  // table row (16-B multiple)
+  static constexpr int U = P * ((8 + P - 1) / P);
+};
+
+__host__ __device__ inline int rl_rows(int n, int P) {  // table rows incl. the P leading ones
+  const int U = P * ((8 + P - 1) / P);
+  return P + n + 2 * U + P;
+}
+
+struct RLFinal {  // last pass of a tile: results also go to HBM (+ L-inf)
+  double* dst;            // global base of this line's outputs
+  std::int64_t dstride;   // global stride per step (signed)
+  const unsigned char* sfl;  // per-step shared flag (indexed by column)
+  int sf_dir;             // column of step t = sf_base + sf_dir * t
+  int sf_base;
+  bool line_shared;
+  unsigned long long lmax;
+};
+
+template <int P, bool TAIL, bool FINAL>
+__device__ __forceinline__ void rl_batch(double* x0, const int ds, const int n, const int t0, const double* tab,
+                                         double (&acc)[P], double (&zin)[RL<P>::U], RLFinal& fin) {
+  constexpr int U = RL<P>::U, W = RL<P>::W;
+  double znx[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int te = t0 + U + P + u;
+    znx[u] = (!TAIL || te < n) ? x0[te * ds] : 0.0;
+  }
+  const double* tb = tab + t0 * W;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    double cf[W];
+#pragma unroll
+    for (int h = 0; h < W / 2; ++h) {
+      const double2 v = reinterpret_cast<const double2*>(tb + u * W)[h];
+      cf[2 * h] = v.x;
+      cf[2 * h + 1] = v.y;
+    }
+    const double y = acc[u % P];
+#pragma unroll
+    for (int k = 1; k < P; ++k) acc[(u + k) % P] = fma(-cf[k - 1], y, acc[(u + k) % P]);
+    acc[u % P] = fma(-cf[P - 1], y, zin[u] * cf[P]);
+    const int t = t0 + u;
+    if (!TAIL || t < n) {
+      x0[t * ds] = y;
+      if (FINAL) {
+        fin.dst[t * fin.dstride] = y;
+        if (!fin.line_shared && !fin.sfl[fin.sf_base + fin.sf_dir * t]) {
+          const unsigned long long bits = dbits_s(fabs(y));
+          fin.lmax = fin.lmax > bits ? fin.lmax : bits;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) zin[u] = znx[u];
+}
+
+template <int P, bool FINAL>
+__device__ __forceinline__ void rl_pass(double* x0, const int ds, const int n, const double* tab, RLFinal& fin) {
+  constexpr int U = RL<P>::U, W = RL<P>::W;
+  double acc[P], zin[U];
+#pragma unroll
+  for (int k = 0; k < P; ++k) acc[k] = (k < n ? x0[k * ds] : 0.0) * tab[(k - P) * W + P];
+#pragma unroll
+  for (int u = 0; u < U; ++u) zin[u] = P + u < n ? x0[(P + u) * ds] : 0.0;
+  int t0 = 0;
+  for (; t0 + 2 * U + P <= n; t0 += U) rl_batch<P, false, FINAL>(x0, ds, n, t0, tab, acc, zin, fin);
+  for (; t0 < n; t0 += U) rl_batch<P, true, FINAL>(x0, ds, n, t0, tab, acc, zin, fin);
+}
+
+__host__ __device__ inline size_t solve2d_smem_bytes(int n0, int n1, int zl, int P, int kseg) {
+  const int W = (P + 2) & ~1;
+  return 128 + (static_cast<size_t>(n1) * zl + static_cast<size_t>(kseg > 1 ? kseg - 1 : 0) * (P + 1) * zl +
+                2 * static_cast<size_t>(rl_rows(n0, P) + rl_rows(n1, P)) * W) *
+                   8 +
+         static_cast<size_t>(n0 + n1 + 16);
+}
+
+// Forward / backward step tables of one axis problem (layout above) from the
+// Cholesky table (2P+1 per column: [1/L(c,c), L(c,c-k), L(c+k,c)]).  f and b
+// point at row -P of their rl_rows(n) rows.
+template <int P>
+__device__ __forceinline__ void build_rl_tables(const double* lt, int n, double* f, double* b, int tid, int nthr) {
+  constexpr int LW = 2 * P + 1, W = RL<P>::W;
+  const int rows = rl_rows(n, P);
+  for (int e = tid; e < rows * W; e += nthr) {
+    const int t = e / W - P, k = e - (t + P) * W;
+    double fv = 0.0, bv = 0.0;
+    if (k < P) {
+      if (t >= 0 && t < n) {
+        const int c = t, cb = n - 1 - t, j = k + 1;
+        fv = c + j < n ? __ldg(lt + c * LW + P + j) * __ldg(lt + (c + j) * LW) : 0.0;
+        bv = cb - j >= 0 ? __ldg(lt + cb * LW + j) * __ldg(lt + (cb - j) * LW) : 0.0;
+      }
+    } else if (k == P) {
+      const int te = t + P;  // the step whose value enters here
+      if (te >= 0 && te < n) {
+        fv = __ldg(lt + te * LW);
+        bv = __ldg(lt + (n - 1 - te) * LW);
+      }
+    }
+    f[e] = fv;
+    b[e] = bv;
+  }
+}
+
+template <int P>
+__global__ void __launch_bounds__(kSolve2dThreads) k_solve2d(const FitArgs a) {
+  extern __shared__ __align__(128) double s2d[];
+  __shared__ unsigned long long s_red[32];
+  constexpr int PADC = P + 1, W = RL<P>::W;
+  const int bid = blockIdx.x;
+  const BlockDev& blk = a.blocks[bid];
+  const AxisProb p0 = a.probs[blk.ax[0]], p1 = a.probs[blk.ax[1]];
+  const int n0 = p0.n, n1 = p1.n, zl = blk.zl;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int* seg = a.segtab + blk.ax[1] * kSegStride;
+  const int K = seg[0];
+  const int* g0g = a.g0 + p1.row_off;
+  std::uint64_t* bar = reinterpret_cast<std::uint64_t*>(s2d);
+  double* X = s2d + 16;                                   // [n1][zl]
+  double* C = X + static_cast<std::int64_t>(n1) * zl;     // [(K-1)(P+1)][zl] carries
+  double* f0 = C + static_cast<std::int64_t>(K - 1) * PADC * zl;
+  double* b0 = f0 + rl_rows(n0, P) * W;
+  double* f1 = b0 + rl_rows(n0, P) * W;
+  double* b1 = f1 + rl_rows(n1, P) * W;
+  unsigned char* sf0 = reinterpret_cast<unsigned char*>(b1 + rl_rows(n1, P) * W);  // n0: axis-0 index shared
+  unsigned char* sf1 = sf0 + n0;                                                   // n1: axis-1 index shared
+  const double* zb = a.Y + blk.zoff + static_cast<std::int64_t>(PADC) * zl;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    unsigned bytes = static_cast<unsigned>(n1) * zl * 8 + static_cast<unsigned>(K - 1) * PADC * zl * 8;
+    mbar_arrive_expect_tx(bar, bytes);
+    int cs = 0;
+    for (int sg = 0; sg < K; ++sg) {  // segment sg owns columns [cs_sg, cs_sg+1) in parity sg & 1
+      const int ce = sg + 1 < K ? __ldg(g0g + seg[2 + sg]) : n1;
+      const double* src = zb + (sg & 1) * a.zhalf + static_cast<std::int64_t>(cs) * zl;
+      if (ce > cs) bulk_load_1d(X + static_cast<std::int64_t>(cs) * zl, src, static_cast<unsigned>(ce - cs) * zl * 8, bar);
+      if (sg + 1 < K)  // its partial sums of the next segment's first P+1 columns
+        bulk_load_1d(C + static_cast<std::int64_t>(sg) * PADC * zl, zb + (sg & 1) * a.zhalf + static_cast<std::int64_t>(ce) * zl,
+                     static_cast<unsigned>(PADC) * zl * 8, bar);
+      cs = ce;
+    }
+  }
+  build_rl_tables<P>(a.ltab + p0.col_off * (2 * P + 1), n0, f0, b0, tid, nthr);
+  build_rl_tables<P>(a.ltab + p1.col_off * (2 * P + 1), n1, f1, b1, tid, nthr);
+  for (int c = tid; c < n1; c += nthr) sf1[c] = a.shared_flag[a.sflag_off[1] + p1.col_lo + c];
+  for (int i = tid; i < n0; i += nthr) sf0[i] = a.shared_flag[a.sflag_off[0] + p0.col_lo + i];
+  __syncthreads();  // barrier init visible before any wait
+  mbar_wait(bar, 0);
+  // carries: X[cs_s + k] += C[s-1][k] for boundaries s = 1..K-1
+  for (int e = tid; e < (K - 1) * PADC * n0; e += nthr) {
+    const int r = e / n0, i = e - r * n0;  // r = (s-1)*(P+1) + k
+    const int sb = r / PADC + 1, k = r - (sb - 1) * PADC;
+    const int c = __ldg(g0g + seg[1 + sb]) + k;
+    X[static_cast<std::int64_t>(c) * zl + i] += C[static_cast<std::int64_t>(r) * zl + i];
+  }
+  __syncthreads();
+  RLFinal fin{};
+  // G1^-1 along the rows (thread per row; stride zl)
+  for (int i = tid; i < n0; i += nthr) {
+    rl_pass<P, false>(X + i, zl, n1, f1 + P * W, fin);
+    rl_pass<P, false>(X + i + (n1 - 1) * zl, -zl, n1, b1 + P * W, fin);
+  }
+  __syncthreads();
+  // G0^-1 along the columns (thread per column); the backward pass writes
+  // P_b[i][c] (coalesced over the warp's columns) and the L-inf over
+  // non-shared controls.
+  double* Pb = a.P + blk.poff;
+  for (int c = tid; c < n1; c += nthr) {
+    double* xc = X + static_cast<std::int64_t>(c) * zl;
+    rl_pass<P, false>(xc, 1, n0, f0 + P * W, fin);
+    fin.dst = Pb + static_cast<std::int64_t>(n0 - 1) * n1 + c;
+    fin.dstride = -n1;
+    fin.sfl = sf0;
+    fin.sf_base = n0 - 1;
+    fin.sf_dir = -1;
+    fin.line_shared = sf1[c] != 0;
+    rl_pass<P, true>(xc + (n0 - 1), -1, n0, b0 + P * W, fin);
+  }
+  unsigned long long lmax = fin.lmax;
+  const int lane = tid & 31, warp = tid >> 5, nw = nthr >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long t2 = __shfl_xor_sync(kFullMask, lmax, o);
+    lmax = lmax > t2 ? lmax : t2;
+  }
+  if (lane == 0) s_red[warp] = lmax;
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long mx = 0ull;
+    for (int w2 = 0; w2 < nw; ++w2) mx = mx > s_red[w2] ? mx : s_red[w2];
+    if (mx) atomicMax(a.linf_int + bid, mx);
+  }
+}
+
 template <int P>
 struct BacksubLaunch {
   static int run(const FitArgs& a, int max_n0, std::int64_t max_rest, cudaStream_t s) {
@@ -1365,6 +1597,12 @@ struct LastLaunch {
     cudaFuncSetAttribute(k_last_contract_tma<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     dim3 grid((a.max_lines_last + LT - 1) / LT, a.nblocks, kseg);
     k_last_contract_tma<P><<<grid, LT, smem, s>>>(a, map, LT);
+    if (a.fuse2d) {
+      const size_t sm2 = solve2d_smem_bytes(a.max_n0, a.max_n1, a.max_zl, P, kseg);
+      cudaFuncSetAttribute(k_solve2d<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm2));
+      k_solve2d<P><<<a.nblocks, kSolve2dThreads, sm2, s>>>(a);
+      return 2;
+    }
     constexpr int T2 = 64, F = (P + 2) & ~1;
     const int nmax = lt_cap / (2 * P + 1);  // max last-axis n (+ padding) from the L-table capacity
     const size_t smem2 = static_cast<size_t>(T2) * 33 * 8 + 2 * static_cast<size_t>(nmax + 1) * F * 8 +
@@ -1384,6 +1622,11 @@ int debug_fail_line_tma() {
   cudaMemcpyFromSymbol(&line, g_tma_debug_line, sizeof(int));
 #endif
   return line;
+}
+
+size_t solve2d_smem(int degree, int n0, int n1, int zl, int kseg) {
+  const size_t b = solve2d_smem_bytes(n0, n1, zl, degree, kseg);
+  return b <= 227 * 1024 - 512 ? b : 0;
 }
 
 int launch_axis0_backsub(int degree, const FitArgs& a, int max_n0, std::int64_t max_rest, cudaStream_t s) {
