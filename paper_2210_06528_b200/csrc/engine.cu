@@ -993,7 +993,9 @@ int launch_residuals(mfadd_solver* s, const double* dfield, const mfb::EpochStat
 // become cross tiles whose remote holders read the receive buffer (rmask),
 // plus pack tiles that gather this rank's copies for each peer.
 void build_regions(mfadd_solver* s, const std::vector<int>& pair_slot) {
-  constexpr int kTile = 1024;  // 256 threads x 4 controls (n_s = 2: one pass)
+  // 256 threads x 4 controls per pass (n_s = 2); several passes per tile
+  // amortise the per-tile reduction
+  static const int kTile = std::getenv("MFADD_EPOCH_TILE") ? std::atoi(std::getenv("MFADD_EPOCH_TILE")) : 4096;
   const Decomp& d = s->dec;
   const int D = d.rank, sh = 3 - D;  // box dims are right-aligned in the kernel's 3-D view
   const std::vector<mfb::Region> regs = mfb::enumerate_regions(d);
@@ -1096,6 +1098,9 @@ void build_regions(mfadd_solver* s, const std::vector<int>& pair_slot) {
     auto& dst = R.rmask ? cross_tiles : local_tiles;
     for (int st0 = 0; st0 < total; st0 += kTile) dst.push_back({R, st0, std::min(kTile, total - st0)});
   }
+  // region_tile_local (kernels.cu) addresses the held lattices with 32-bit offsets
+  if (s->wl.total_p >= (std::int64_t{1} << 31))
+    throw std::invalid_argument("mfadd_b200: held lattices exceed 2^31 controls on one device");
   s->ntiles = static_cast<int>(local_tiles.size());
   s->nxtiles = static_cast<int>(cross_tiles.size());
   s->npack = static_cast<int>(packs.size());

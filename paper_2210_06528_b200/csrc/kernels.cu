@@ -882,6 +882,34 @@ __device__ __forceinline__ unsigned long long cta_dmax_multi(double (&v)[K], dou
   return dbits(r);
 }
 
+// u64 max over the warp in two 32-bit REDUX steps (high words, then the low
+// words of the lanes holding the maximal high word).
+__device__ __forceinline__ unsigned long long warp_umax64(unsigned long long v) {
+  const unsigned hi = static_cast<unsigned>(v >> 32);
+  const unsigned mhi = __reduce_max_sync(kFull, hi);
+  const unsigned mlo = __reduce_max_sync(kFull, hi == mhi ? static_cast<unsigned>(v) : 0u);
+  return (static_cast<unsigned long long>(mhi) << 32) | mlo;
+}
+
+// CTA max of K u64 bit patterns (non-negative doubles) with one barrier;
+// thread j < K receives value j's CTA max.
+template <int K>
+__device__ __forceinline__ unsigned long long cta_umax_multi(unsigned long long (&v)[K], double (*s_w)[kRegionWarps]) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned long long(*s_u)[kRegionWarps] = reinterpret_cast<unsigned long long(*)[kRegionWarps]>(s_w);
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const unsigned long long r = warp_umax64(v[j]);
+    if (lane == 0) s_u[j][w] = r;
+  }
+  __syncthreads();
+  unsigned long long r = 0ull;
+  if (threadIdx.x < K)
+#pragma unroll
+    for (int i = 0; i < kRegionWarps; ++i) r = umax(r, s_u[threadIdx.x][i]);
+  return r;
+}
+
 struct RegionRegs {
   long long base;
   int s0, s1, s2;
@@ -900,6 +928,100 @@ __device__ __forceinline__ void fast_divmod(int n, int d, float rcp, int& q, int
     ++q;
     r -= d;
   }
+}
+
+// fast_divmod without branches (the correction as selects).
+__device__ __forceinline__ void divmod_nb(int n, int d, float rcp, int& q, int& r) {
+  q = __float2int_rz(__int2float_rz(n) * rcp);
+  r = n - q * d;
+  const int lo = r < 0 ? 1 : 0, hi = r >= d ? 1 : 0;
+  q += hi - lo;
+  r += (lo - hi) * d;
+}
+
+// region_tile for a tile whose holders are all local (rmask == 0): 32-bit
+// element offsets (the engine keeps the held lattices below 2^31 doubles),
+// the last box dim contiguous in every copy (stride 1), branch-free index
+// arithmetic, and for FLAT boxes (ext[0] == 1: every 1-D/2-D region) a single
+// division.  Elements past the tile are loaded at a clamped index and not
+// used.  Same arithmetic and reduction as region_tile.
+template <int NS, bool FLAT>
+__device__ __forceinline__ void region_tile_local(const EpochRegionArgs& a, const RegionDev& R, const TileDev& t,
+                                                  int mode, double (*s_w)[kRegionWarps]) {
+  constexpr int PT = NS == 2 ? 4 : (NS == 4 ? 2 : 1);
+  const bool update = mode == 2 || (mode == 1 && NS == 2);
+  int base[NS], s0[NS], s1[NS];
+#pragma unroll
+  for (int h = 0; h < NS; ++h) {
+    base[h] = static_cast<int>(R.base[h]);
+    s0[h] = R.str[h][0];
+    s1[h] = R.str[h][1];
+  }
+  const int e1 = R.ext[1], e2 = R.ext[2];
+  const float rc1 = 1.0f / static_cast<float>(e1), rc2 = 1.0f / static_cast<float>(e2);
+  double* __restrict__ P = a.P;
+  unsigned long long red[NS + 1];
+#pragma unroll
+  for (int j = 0; j <= NS; ++j) red[j] = 0ull;
+  const int end = t.start + t.count;
+  for (int i0 = t.start + threadIdx.x; i0 < end; i0 += kRegionThreads * PT) {
+    int off[PT][NS];
+    double v[PT][NS];
+#pragma unroll
+    for (int u = 0; u < PT; ++u) {
+      const int i = min(i0 + u * kRegionThreads, end - 1);
+      int q, r2, r0 = 0, r1;
+      divmod_nb(i, e2, rc2, q, r2);
+      if (FLAT)
+        r1 = q;
+      else
+        divmod_nb(q, e1, rc1, r0, r1);
+#pragma unroll
+      for (int h = 0; h < NS; ++h) {
+        off[u][h] = base[h] + r0 * s0[h] + r1 * s1[h] + r2;
+        v[u][h] = P[off[u][h]];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < PT; ++u) {
+      if (i0 + u * kRegionThreads < end) {
+        if (update) {
+          double sum = 0.0;  // solver.cpp:147-159: ascending holder id, divide once
+#pragma unroll
+          for (int h = 0; h < NS; ++h) sum = __dadd_rn(sum, v[u][h]);
+          const double avg = sum * (1.0 / NS);  // NS is a power of two: bitwise equal to sum / NS
+#pragma unroll
+          for (int h = 0; h < NS; ++h) {
+            red[h] = umax(red[h], dbits(fabs(avg - v[u][h])));
+            P[off[u][h]] = avg;
+          }
+          red[NS] = umax(red[NS], dbits(fabs(avg)));
+        } else {
+          double mn = v[u][0], mx = v[u][0];
+#pragma unroll
+          for (int h = 0; h < NS; ++h) {
+            mn = fmin(mn, v[u][h]);
+            mx = fmax(mx, v[u][h]);
+            red[h] = umax(red[h], dbits(fabs(v[u][h])));
+          }
+          red[NS] = umax(red[NS], dbits(mx - mn));
+        }
+      }
+    }
+  }
+  const unsigned long long b = cta_umax_multi<NS + 1>(red, s_w);
+  const int j = threadIdx.x;
+  if (b && j < NS) {
+    atomicMax((update ? a.change : a.linf_sh) + R.ids[j], b);
+  } else if (b && j == NS) {
+    if (update) {
+#pragma unroll
+      for (int h = 0; h < NS; ++h) atomicMax(a.linf_sh + R.ids[h], b);
+    } else {
+      atomicMax(NS == 2 ? &a.st->jump_ss : &a.st->jump_ms, b);
+    }
+  }
+  __syncthreads();  // s_w and the tile descriptor are reused by the next tile
 }
 
 // R is the CTA's shared-memory copy of the region descriptor.  PT controls
@@ -922,9 +1044,9 @@ __device__ __forceinline__ void region_tile(const EpochRegionArgs& a, const Regi
   const float rc1 = 1.0f / static_cast<float>(e1), rc2 = 1.0f / static_cast<float>(e2);
   // update: red[h] = change of holder h, red[NS] = max |avg| (every copy);
   // measure: red[h] = max |copy of holder h|, red[NS] = jump
-  double red[NS + 1];
+  unsigned long long red[NS + 1];  // bit patterns of non-negative doubles (ordered like the values)
 #pragma unroll
-  for (int j = 0; j <= NS; ++j) red[j] = 0.0;
+  for (int j = 0; j <= NS; ++j) red[j] = 0ull;
   const int end = t.start + t.count;
   for (int i0 = t.start + threadIdx.x; i0 < end; i0 += kRegionThreads * PT) {
     long long off[PT][NS];
@@ -951,23 +1073,23 @@ __device__ __forceinline__ void region_tile(const EpochRegionArgs& a, const Regi
         const double avg = sum * (1.0 / NS);  // NS is a power of two: bitwise equal to sum / NS
 #pragma unroll
         for (int h = 0; h < NS; ++h) {
-          red[h] = fmax(red[h], fabs(avg - v[u][h]));
+          red[h] = umax(red[h], dbits(fabs(avg - v[u][h])));
           if (!((rmask >> h) & 1)) a.P[off[u][h]] = avg;
         }
-        red[NS] = fmax(red[NS], fabs(avg));  // every holder's copy is now avg
+        red[NS] = umax(red[NS], dbits(fabs(avg)));  // every holder's copy is now avg
       } else {
         double mn = v[u][0], mx = v[u][0];
 #pragma unroll
         for (int h = 0; h < NS; ++h) {
           mn = fmin(mn, v[u][h]);
           mx = fmax(mx, v[u][h]);
-          red[h] = fmax(red[h], fabs(v[u][h]));
+          red[h] = umax(red[h], dbits(fabs(v[u][h])));
         }
-        red[NS] = fmax(red[NS], mx - mn);  // all holders are mutual neighbours
+        red[NS] = umax(red[NS], dbits(mx - mn));  // all holders are mutual neighbours
       }
     }
   }
-  const unsigned long long b = cta_dmax_multi<NS + 1>(red, s_w);
+  const unsigned long long b = cta_umax_multi<NS + 1>(red, s_w);
   const int j = threadIdx.x;
   if (b && j < NS) {
     if (!((rmask >> j) & 1)) atomicMax((update ? a.change : a.linf_sh) + R.ids[j], b);
@@ -981,6 +1103,17 @@ __device__ __forceinline__ void region_tile(const EpochRegionArgs& a, const Regi
     }
   }
   __syncthreads();  // s_w and the tile descriptor are reused by the next tile
+}
+
+template <int NS>
+__device__ __forceinline__ void region_tile_any(const EpochRegionArgs& a, const TileDev& t, int mode,
+                                                double (*s_w)[kRegionWarps]) {
+  if (t.r.rmask != 0)
+    region_tile<NS>(a, t.r, t, mode, s_w);
+  else if (t.r.ext[0] == 1)
+    region_tile_local<NS, true>(a, t.r, t, mode, s_w);
+  else
+    region_tile_local<NS, false>(a, t.r, t, mode, s_w);
 }
 
 // dp = max_b change_b / max(1, ||P_b||_inf) (solver.cpp:398-405) into
@@ -1039,9 +1172,9 @@ __global__ void __launch_bounds__(kRegionThreads, MAXNS == 8 ? 2 : 3) k_epoch_re
     if (tid < kWords && tn < a.ntiles) w = __ldg(reinterpret_cast<const int*>(a.tiles + tn) + tid);
     const TileDev& t = s_T;
     switch (t.r.ns) {
-      case 2: region_tile<2>(a, t.r, t, mode, s_w); break;
-      case 4: region_tile<4>(a, t.r, t, mode, s_w); break;
-      default: region_tile<MAXNS>(a, t.r, t, mode, s_w); break;
+      case 2: region_tile_any<2>(a, t, mode, s_w); break;
+      case 4: region_tile_any<4>(a, t, mode, s_w); break;
+      default: region_tile_any<MAXNS>(a, t, mode, s_w); break;
     }
   }
   if (!a.finalize) return;
