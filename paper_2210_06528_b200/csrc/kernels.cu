@@ -1420,27 +1420,31 @@ __global__ void __launch_bounds__(1024) k_dp(DpArgs a) {
 constexpr int kAsmMaxLast = 4096;  // last-dim extent handled by the smem owner table
 constexpr int kAsmMaxB = 256;
 
+constexpr int kAsmRows = 4;  // lattice rows per CTA (owner table loaded once)
+
 __global__ void __launch_bounds__(256) k_assemble(AssembleArgs a) {
   __shared__ short s_own[kAsmMaxLast];
-  __shared__ long long s_base[kAsmMaxB];  // P offset of the row in block (lead, c) minus col_lo
+  __shared__ long long s_base[kAsmRows][kAsmMaxB];  // P offset of the row in block (lead, c) minus col_lo
   const int D = a.D, dl = D - 1;
   const int Nl = static_cast<int>(a.N[dl]), Bl = a.B[dl];
   const bool own_smem = Nl <= kAsmMaxLast;
   if (own_smem)
-    for (int i = threadIdx.x; i < Nl; i += blockDim.x) s_own[i] = static_cast<short>(a.own_coord[a.oc_off[dl] + i]);
-  // lead coordinates of this row
-  const std::int64_t grow = a.row0 + blockIdx.x;
-  std::int64_t row = grow;
-  int cl[3] = {0, 0, 0};
-  std::int64_t il[3] = {0, 0, 0};
-  for (int k = dl - 1; k >= 0; --k) {
-    il[k] = row % a.N[k];
-    row /= a.N[k];
-    cl[k] = a.own_coord[a.oc_off[k] + il[k]];
-  }
-  int lead_id = 0;
-  for (int k = 0; k < dl; ++k) lead_id = lead_id * a.B[k] + cl[k];
-  for (int c = threadIdx.x; c < Bl; c += blockDim.x) {
+    for (int i = threadIdx.x; i < Nl; i += blockDim.x) s_own[i] = static_cast<short>(__ldg(a.own_coord + a.oc_off[dl] + i));
+  const std::int64_t r0 = static_cast<std::int64_t>(blockIdx.x) * kAsmRows;
+  const int nr = static_cast<int>(a.nrows - r0 < kAsmRows ? a.nrows - r0 : kAsmRows);
+  // lead coordinates of each row; s_base per (row, last-dim block coordinate)
+  for (int e = threadIdx.x; e < nr * Bl; e += blockDim.x) {
+    const int r = e / Bl, c = e - r * Bl;
+    std::int64_t row = a.row0 + r0 + r;
+    int cl[3] = {0, 0, 0};
+    std::int64_t il[3] = {0, 0, 0};
+    for (int k = dl - 1; k >= 0; --k) {
+      il[k] = row % a.N[k];
+      row /= a.N[k];
+      cl[k] = a.own_coord[a.oc_off[k] + il[k]];
+    }
+    int lead_id = 0;
+    for (int k = 0; k < dl; ++k) lead_id = lead_id * a.B[k] + cl[k];
     const int id = lead_id * Bl + c;
     // local row index within block id: row-major over the lead dims, then x n_last
     std::int64_t o = 0;
@@ -1449,14 +1453,20 @@ __global__ void __launch_bounds__(256) k_assemble(AssembleArgs a) {
       o = o * pk.n + (il[k] - pk.col_lo);
     }
     const AxisProb& pl = a.probs[a.axbase[dl] + c];
-    s_base[c] = a.poff[id] + o * pl.n - pl.col_lo;
+    s_base[r][c] = a.poff[id] + o * pl.n - pl.col_lo;
   }
   __syncthreads();
-  double* out = a.lattice + grow * Nl;
   const int i0 = static_cast<int>(a.col0), i1 = static_cast<int>(a.col0 + a.ncols);
+  double* out = a.lattice + (a.row0 + r0) * Nl;
+  // all rows' loads of one column sweep in flight before the stores
   for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
     const int c = own_smem ? s_own[i] : a.own_coord[a.oc_off[dl] + i];
-    out[i] = a.P[s_base[c] + i];
+    double v[kAsmRows];
+#pragma unroll
+    for (int r = 0; r < kAsmRows; ++r) v[r] = r < nr ? a.P[s_base[r][c] + i] : 0.0;
+#pragma unroll
+    for (int r = 0; r < kAsmRows; ++r)
+      if (r < nr) out[static_cast<std::int64_t>(r) * Nl + i] = v[r];
   }
 }
 
@@ -1852,7 +1862,7 @@ int launch_dp(const DpArgs& a, cudaStream_t s) {
 int launch_assemble(const AssembleArgs& a, cudaStream_t s) {
   if (a.B[a.D - 1] > kAsmMaxB) return -1;  // host validates blocks_per_dim first
   if (a.nrows <= 0) return 0;
-  k_assemble<<<static_cast<unsigned>(a.nrows), 256, 0, s>>>(a);
+  k_assemble<<<static_cast<unsigned>((a.nrows + kAsmRows - 1) / kAsmRows), 256, 0, s>>>(a);
   return 1;
 }
 
