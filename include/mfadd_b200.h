@@ -209,6 +209,80 @@ int mfadd_decode(mfadd_context* ctx, int rank, int degree, const double* knots, 
                  const double* params, const int64_t* pm_off, const int64_t* ctrl_ext,
                  const int64_t* col_offset /* nullable */, const double* controls, double* out);
 
+/* ------------------------------------------- MfaModel output path (§8(f))
+ * eval_deriv / eval_deriv_sided (decode.hpp:28-40; MfaModel::eval /
+ * eval_deriv, model.hpp:29-31) at npts points [npts][rank] on the GPU (one
+ * thread per point, bitwise equal to the reference).  degrees[rank]; knots of
+ * dim d at knots[kn_off[d] .. kn_off[d+1]); controls row-major with extents
+ * ctrl_ext; col_offset (nullable) as in decode(); orders (nullable) the
+ * derivative order per dim; side_dim < 0 evaluates unsided, else side 0 =
+ * Side::Below, 1 = Side::Above along side_dim.  Errors as the reference:
+ * EINVAL (order > degree), ERANGE (find_span, lattice window), for the first
+ * failing point. */
+#define MFADD_SIDE_BELOW 0
+#define MFADD_SIDE_ABOVE 1
+int mfadd_eval_points(mfadd_context* ctx, int rank, const int* degrees, const double* knots, const int64_t* kn_off,
+                      const int64_t* ctrl_ext, const int64_t* col_offset, const double* controls, int64_t npts,
+                      const double* points, const int* orders, int side_dim, int side, double* out);
+
+/* std::vector<double> continuity_jumps(const MfaModel&, int dim, double u,
+ * int max_order, int cross_samples)                      solver.hpp:96
+ * out: max_order + 1 jumps (probe points evaluated on the GPU). */
+int mfadd_continuity_jumps(mfadd_context* ctx, int rank, const int* degrees, const double* knots,
+                           const int64_t* kn_off, const int64_t* ctrl_ext, const double* controls, int dim, double u,
+                           int max_order, int cross_samples, double* out);
+
+/* The pipeline's continuity probe over every interior interface of a solved
+ * decomposition (pipeline.cpp:210-228 over continuity_jumps(BlockState,
+ * BlockState, ...), solver.hpp:98), evaluated on the device-resident held
+ * lattices of the last solve.  probe_order < 0: degree - 1.  out: probe_order
+ * + 1 jumps (max over interfaces); *out_order receives the order used. */
+int mfadd_solver_continuity_probe(mfadd_solver* s, int probe_order, int cross_samples, double* out, int* out_order);
+
+/* Tensor MfaModel::decode_grid(const std::vector<int64_t>& res)   model.hpp:34
+ * out: prod(res) doubles (GPU decode at u_j = j / (res - 1)). */
+int mfadd_decode_grid(mfadd_context* ctx, int rank, int degree, const double* knots, const int64_t* kn_off,
+                      const int64_t* ctrl_ext, const double* controls, const int64_t* res, double* out);
+
+/* MfaModel as plain arrays (model.hpp:18-35).  Provenance is nprov key/value
+ * strings, written in ascending key order (std::map).  clamp flags and
+ * bounds are nullable on write (clamped, [0, 1]). */
+typedef struct mfadd_model_view {
+  int rank;
+  const int* degrees;
+  const unsigned char* clamp_left;
+  const unsigned char* clamp_right;
+  const double* knots;
+  const int64_t* kn_off;
+  const int64_t* ctrl_ext;
+  const double* bounds; /* [rank][2] */
+  int nprov;
+  const char* const* prov_keys;
+  const char* const* prov_values;
+  const double* controls;
+} mfadd_model_view;
+
+typedef struct mfadd_model mfadd_model; /* a model read from disk; owns its arrays */
+
+/* void write_mfa(const MfaModel&, const std::filesystem::path&)   model.hpp:40
+ * MFDD v1 container, bit-exact with the reference writer. */
+int mfadd_write_mfa(const char* path, const mfadd_model_view* model);
+/* MfaModel read_mfa(const std::filesystem::path&)                 model.hpp:41 */
+int mfadd_read_mfa(const char* path, mfadd_model** out);
+int mfadd_model_view_of(const mfadd_model* m, mfadd_model_view* out); /* pointers owned by m */
+void mfadd_model_free(mfadd_model* m);
+
+/* Field read_raw_grid(path, dims, RawScalar, RawByteOrder)        field.hpp:48-50
+ * Raw row-major grid, no header; file size must equal prod(dims) x width.
+ * The bytes go to the device and are byte-swapped / widened there; out is
+ * prod(dims) doubles in device memory (out_on_device) or host memory. */
+#define MFADD_RAW_F32 0
+#define MFADD_RAW_F64 1
+#define MFADD_RAW_LITTLE 0
+#define MFADD_RAW_BIG 1
+int mfadd_read_raw_grid(mfadd_context* ctx, const char* path, int rank, const int64_t* dims, int type, int byte_order,
+                        double* out, int out_on_device);
+
 #ifdef __cplusplus
 }
 #endif

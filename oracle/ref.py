@@ -309,3 +309,115 @@ def solve(dec: RefDecomposition, values, max_outer_iterations=10, tolerance=1e-1
                                    decode=dbl[7]), berr)
     finally:
         L.ref_result_free(h)
+
+
+# ---------------------------------------------------------------- §8(f): model path, probe, raw grid
+def _model_arrays(knots_list, degrees, controls):
+    kn = np.ascontiguousarray(np.concatenate([np.asarray(k, np.float64) for k in knots_list]))
+    ko = np.cumsum([0] + [len(k) for k in knots_list]).astype(np.int64)
+    deg = np.array(degrees, np.int32)
+    c = np.ascontiguousarray(controls, np.float64)
+    ext = np.array(c.shape, np.int64)
+    return kn, ko, deg, c, ext
+
+
+def eval_points(controls, knots_list, degrees, points, orders=None, side_dim=-1, side=1, col_offset=None):
+    """eval_deriv / eval_deriv_sided (decode.hpp:28-40), one reference call per point."""
+    kn, ko, deg, c, ext = _model_arrays(knots_list, degrees, controls)
+    pts = np.ascontiguousarray(np.atleast_2d(np.asarray(points, np.float64)))
+    ords = None if orders is None else np.array(orders, np.int32)
+    off = None if col_offset is None else np.array(col_offset, np.int64)
+    out = np.zeros(pts.shape[0], np.float64)
+    L = lib()
+    L.ref_eval_points.argtypes = None
+    _check(L.ref_eval_points(len(knots_list), _ptr(deg, _ip), _ptr(kn, _dp), _ptr(ko, _lp), _ptr(ext, _lp),
+                             None if off is None else _ptr(off, _lp), _ptr(c, _dp), C.c_longlong(pts.shape[0]),
+                             _ptr(pts, _dp), None if ords is None else _ptr(ords, _ip), side_dim, side,
+                             _ptr(out, _dp)))
+    return out
+
+
+def decode_grid(controls, knots_list, degrees, res):
+    """MfaModel::decode_grid (model.cpp:39-49)."""
+    kn, ko, deg, c, ext = _model_arrays(knots_list, degrees, controls)
+    r = np.array(res, np.int64)
+    out = np.zeros(tuple(int(x) for x in res), np.float64)
+    _check(lib().ref_decode_grid(len(knots_list), _ptr(deg, _ip), _ptr(kn, _dp), _ptr(ko, _lp), _ptr(ext, _lp),
+                                 _ptr(c, _dp), _ptr(r, _lp), _ptr(out, _dp)))
+    return out
+
+
+def write_mfa(path, knots_list, degrees, controls, clamp_left, clamp_right, bounds, provenance):
+    """write_mfa (model.cpp:93-118)."""
+    kn, ko, deg, c, ext = _model_arrays(knots_list, degrees, controls)
+    cl = np.array([int(x) for x in clamp_left], np.int32)
+    cr = np.array([int(x) for x in clamp_right], np.int32)
+    b = np.ascontiguousarray(np.array(bounds, np.float64).reshape(-1))
+    keys = [str(k).encode() for k in provenance]
+    vals = [str(provenance[k]).encode() for k in provenance]
+    karr = (C.c_char_p * max(len(keys), 1))(*keys)
+    varr = (C.c_char_p * max(len(vals), 1))(*vals)
+    _check(lib().ref_write_mfa(str(path).encode(), len(knots_list), _ptr(deg, _ip), _ptr(cl, _ip), _ptr(cr, _ip),
+                               _ptr(kn, _dp), _ptr(ko, _lp), _ptr(ext, _lp), _ptr(b, _dp), len(keys), karr, varr,
+                               _ptr(c, _dp)))
+
+
+def read_mfa_status(path):
+    """(code, message) of read_mfa (model.cpp:120-167) on `path`; code 0 = ok."""
+    L = lib()
+    rc = L.ref_read_mfa_check(str(path).encode())
+    return rc, (L.ref_last_error().decode() if rc else "")
+
+
+def read_raw_grid(path, dims, type_, order):
+    """read_raw_grid (field.cpp:149-191): type_ 0 f32 / 1 f64, order 0 little / 1 big."""
+    d = np.array(dims, np.int64)
+    out = np.zeros(tuple(int(x) for x in dims), np.float64)
+    _check(lib().ref_read_raw_grid(str(path).encode(), len(dims), _ptr(d, _lp), type_, order, _ptr(out, _dp)))
+    return out
+
+
+def continuity_jumps_model(controls, knots_list, degrees, dim, u, max_order, cross_samples=5):
+    """continuity_jumps(const MfaModel&, ...) (solver.cpp:244-261)."""
+    kn, ko, deg, c, ext = _model_arrays(knots_list, degrees, controls)
+    out = np.zeros(max_order + 1, np.float64)
+    _check(lib().ref_continuity_jumps_model(len(knots_list), _ptr(deg, _ip), _ptr(kn, _dp), _ptr(ko, _lp),
+                                            _ptr(ext, _lp), _ptr(c, _dp), dim, C.c_double(u), max_order,
+                                            cross_samples, _ptr(out, _dp)))
+    return out
+
+
+def solve_and_probe(dec: "RefDecomposition", values, max_outer_iterations=20, tolerance=1e-10, probe_order=-1,
+                    cross_samples=5):
+    """solve() then the pipeline's continuity probe (pipeline.cpp:210-228,
+    restated loop over continuity_jumps(BlockState, BlockState, ...))."""
+    v = np.ascontiguousarray(values, np.float64)
+    h = C.c_void_p()
+    L = lib()
+    L.ref_dec_span_param.restype = C.c_double
+    L.ref_dec_span_param.argtypes = [C.c_void_p, C.c_int, C.c_longlong]
+    _check(L.ref_solve(dec._h, _ptr(v, _dp), None, max_outer_iterations, C.c_double(tolerance), 1, 0, 1,
+                       C.byref(h)))
+    try:
+        order = probe_order if probe_order >= 0 else dec.degree - 1
+        jumps = np.zeros(order + 1, np.float64)
+        coords = dec.coords()
+        bdims = dec.blockdims()
+        bpd = [int(coords[:, k].max()) + 1 for k in range(dec.rank)]
+        buf = np.zeros(order + 1, np.float64)
+        for b in range(dec.nblocks):
+            for dim in range(dec.rank):
+                if coords[b, dim] + 1 >= bpd[dim]:
+                    continue
+                ac = list(coords[b])
+                ac[dim] += 1
+                above = 0
+                for k in range(dec.rank):
+                    above = above * bpd[k] + int(ac[k])
+                u = L.ref_dec_span_param(dec._h, dim, int(bdims[b, dim, 1]))
+                _check(L.ref_continuity_jumps_blocks(dec._h, h, b, above, dim, C.c_double(u), order, cross_samples,
+                                                     _ptr(buf, _dp)))
+                jumps = np.maximum(jumps, buf)
+        return order, jumps
+    finally:
+        L.ref_result_free(h)

@@ -23,6 +23,7 @@
 #include "mfadd/knots.hpp"
 #include "mfadd/layout.hpp"
 #include "mfadd/lsq.hpp"
+#include "mfadd/model.hpp"
 #include "mfadd/runtime.hpp"
 #include "mfadd/solver.hpp"
 
@@ -397,5 +398,110 @@ void ref_result_block_p(void* h, int block, double* out) {
   const Tensor& t = static_cast<RefResult*>(h)->res.blocks[static_cast<std::size_t>(block)].p;
   std::memcpy(out, t.data(), static_cast<std::size_t>(t.size()) * sizeof(double));
 }
+
+// ---- model.hpp / decode.hpp: §8(f) rows (MfaModel output path, probe) ----
+namespace {
+// A model from flat arrays: per-dim degree and clamp flags, knots of dim d at
+// knots[kn_off[d] .. kn_off[d+1]), bounds [rank][2] (NULL: [0,1]).
+MfaModel make_model(int rank, const int* degrees, const int* clamp_l, const int* clamp_r, const double* knots,
+                    const long long* kn_off, const long long* ctrl_ext, const double* bounds, const double* controls) {
+  MfaModel m;
+  std::vector<std::int64_t> ext;
+  for (int d = 0; d < rank; ++d) {
+    m.degrees.push_back(degrees[d]);
+    m.kvs.push_back(make_kv(knots + kn_off[d], static_cast<int>(kn_off[d + 1] - kn_off[d]), degrees[d],
+                            clamp_l ? clamp_l[d] : 1, clamp_r ? clamp_r[d] : 1));
+    m.bounds.push_back({bounds ? bounds[2 * d] : 0.0, bounds ? bounds[2 * d + 1] : 1.0});
+    ext.push_back(ctrl_ext[d]);
+  }
+  m.controls = Tensor(ext);
+  std::memcpy(m.controls.data(), controls, static_cast<std::size_t>(m.controls.size()) * sizeof(double));
+  return m;
+}
+}  // namespace
+
+// eval_deriv / eval_deriv_sided (decode.hpp:28-40) at npts points [npts][rank];
+// orders may be NULL (values); side_dim < 0: unsided; side 0 Below, 1 Above.
+int ref_eval_points(int rank, const int* degrees, const double* knots, const long long* kn_off,
+                    const long long* ctrl_ext, const long long* col_offset, const double* controls, long long npts,
+                    const double* points, const int* orders, int side_dim, int side, double* out) {
+  return guarded([&] {
+    const MfaModel m = make_model(rank, degrees, nullptr, nullptr, knots, kn_off, ctrl_ext, nullptr, controls);
+    std::vector<std::int64_t> off;
+    if (col_offset)
+      for (int d = 0; d < rank; ++d) off.push_back(col_offset[d]);
+    std::vector<int> ord;
+    if (orders)
+      for (int d = 0; d < rank; ++d) ord.push_back(orders[d]);
+    for (long long i = 0; i < npts; ++i) {
+      std::span<const double> pt(points + i * rank, static_cast<std::size_t>(rank));
+      out[i] = side_dim < 0 ? eval_deriv(m.controls, m.kvs, pt, ord, off)
+                            : eval_deriv_sided(m.controls, m.kvs, pt, ord, side_dim, side ? Side::Above : Side::Below, off);
+    }
+  });
+}
+
+// MfaModel::decode_grid (model.cpp:39-49)
+int ref_decode_grid(int rank, const int* degrees, const double* knots, const long long* kn_off,
+                    const long long* ctrl_ext, const double* controls, const long long* res, double* out) {
+  return guarded([&] {
+    const MfaModel m = make_model(rank, degrees, nullptr, nullptr, knots, kn_off, ctrl_ext, nullptr, controls);
+    const Tensor t = m.decode_grid(std::vector<std::int64_t>(res, res + rank));
+    std::memcpy(out, t.data(), static_cast<std::size_t>(t.size()) * sizeof(double));
+  });
+}
+
+// write_mfa (model.cpp:93-118); provenance as nprov key/value C strings.
+int ref_write_mfa(const char* path, int rank, const int* degrees, const int* clamp_l, const int* clamp_r,
+                  const double* knots, const long long* kn_off, const long long* ctrl_ext, const double* bounds,
+                  int nprov, const char* const* keys, const char* const* values, const double* controls) {
+  return guarded([&] {
+    MfaModel m = make_model(rank, degrees, clamp_l, clamp_r, knots, kn_off, ctrl_ext, bounds, controls);
+    for (int i = 0; i < nprov; ++i) m.provenance[keys[i]] = values[i];
+    write_mfa(m, path);
+  });
+}
+
+// read_mfa (model.cpp:120-167): status only (used for the error-path checks)
+int ref_read_mfa_check(const char* path) {
+  return guarded([&] { (void)read_mfa(path); });
+}
+
+// read_raw_grid (field.cpp:149-191): type 0 f32 / 1 f64, order 0 little / 1 big
+int ref_read_raw_grid(const char* path, int rank, const long long* dims, int type, int order, double* out) {
+  return guarded([&] {
+    const Field f = read_raw_grid(path, std::vector<std::int64_t>(dims, dims + rank),
+                                  type ? RawScalar::Float64 : RawScalar::Float32,
+                                  order ? RawByteOrder::Big : RawByteOrder::Little, {});
+    std::memcpy(out, f.values.data(), static_cast<std::size_t>(f.values.size()) * sizeof(double));
+  });
+}
+
+// continuity_jumps on an assembled model (solver.hpp:96)
+int ref_continuity_jumps_model(int rank, const int* degrees, const double* knots, const long long* kn_off,
+                               const long long* ctrl_ext, const double* controls, int dim, double u, int max_order,
+                               int cross_samples, double* out) {
+  return guarded([&] {
+    const MfaModel m = make_model(rank, degrees, nullptr, nullptr, knots, kn_off, ctrl_ext, nullptr, controls);
+    const auto j = continuity_jumps(m, dim, u, max_order, cross_samples);
+    std::memcpy(out, j.data(), j.size() * sizeof(double));
+  });
+}
+
+// continuity_jumps between two solved blocks (solver.hpp:98), as used by the
+// pipeline's probe (pipeline.cpp:210-228)
+int ref_continuity_jumps_blocks(void* dec_handle, void* result, int below, int above, int dim, double u,
+                                int max_order, int cross_samples, double* out) {
+  return guarded([&] {
+    const Decomposition& dec = static_cast<RefDec*>(dec_handle)->dec;
+    const SolveResult& r = static_cast<RefResult*>(result)->res;
+    const auto j = continuity_jumps(r.blocks[static_cast<std::size_t>(below)], r.blocks[static_cast<std::size_t>(above)],
+                                    dec, dim, u, max_order, cross_samples);
+    std::memcpy(out, j.data(), j.size() * sizeof(double));
+  });
+}
+
+// GlobalLayout::span_param (layout.cpp:22-27)
+double ref_dec_span_param(void* h, int dim, long long t) { return static_cast<RefDec*>(h)->dec.global.span_param(dim, t); }
 
 }  // extern "C"

@@ -33,6 +33,13 @@ class SolveSummaryC(C.Structure):
                 ("t_exchange", C.c_double), ("t_constraint", C.c_double), ("t_decode", C.c_double)]
 
 
+class ModelViewC(C.Structure):
+    _fields_ = [("rank", C.c_int), ("degrees", c_ip), ("clamp_left", C.POINTER(C.c_ubyte)),
+                ("clamp_right", C.POINTER(C.c_ubyte)), ("knots", c_dp), ("kn_off", c_lp), ("ctrl_ext", c_lp),
+                ("bounds", c_dp), ("nprov", C.c_int), ("prov_keys", C.POINTER(C.c_char_p)),
+                ("prov_values", C.POINTER(C.c_char_p)), ("controls", c_dp)]
+
+
 class EpochStatsC(C.Structure):
     _fields_ = [("iteration", C.c_int), ("dp_max", C.c_double), ("jump_ss", C.c_double), ("jump_ms", C.c_double)]
 
@@ -81,6 +88,17 @@ _SIGS = {
     "mfadd_fit_unconstrained": (C.c_int, [C.c_void_p, C.c_int, C.c_int, c_dp, c_lp, c_dp, c_lp, c_lp, c_lp, c_dp,
                                           c_dp]),
     "mfadd_decode": (C.c_int, [C.c_void_p, C.c_int, C.c_int, c_dp, c_lp, c_dp, c_lp, c_lp, c_lp, c_dp, c_dp]),
+    "mfadd_eval_points": (C.c_int, [C.c_void_p, C.c_int, c_ip, c_dp, c_lp, c_lp, c_lp, c_dp, C.c_int64, c_dp, c_ip,
+                                    C.c_int, C.c_int, c_dp]),
+    "mfadd_continuity_jumps": (C.c_int, [C.c_void_p, C.c_int, c_ip, c_dp, c_lp, c_lp, c_dp, C.c_int, C.c_double,
+                                         C.c_int, C.c_int, c_dp]),
+    "mfadd_solver_continuity_probe": (C.c_int, [C.c_void_p, C.c_int, C.c_int, c_dp, c_ip]),
+    "mfadd_decode_grid": (C.c_int, [C.c_void_p, C.c_int, C.c_int, c_dp, c_lp, c_lp, c_dp, c_lp, c_dp]),
+    "mfadd_write_mfa": (C.c_int, [C.c_char_p, C.POINTER(ModelViewC)]),
+    "mfadd_read_mfa": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p)]),
+    "mfadd_model_view_of": (C.c_int, [C.c_void_p, C.POINTER(ModelViewC)]),
+    "mfadd_model_free": (None, [C.c_void_p]),
+    "mfadd_read_raw_grid": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int, c_lp, C.c_int, C.c_int, C.c_void_p, C.c_int]),
     "mfadd_nccl_unique_id": (C.c_int, [C.c_void_p]),
     "mfadd_comm_create": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
     "mfadd_comm_free": (None, [C.c_void_p]),

@@ -540,10 +540,208 @@ class PhaseTimings:
 
 @dataclass
 class MfaModel:
+    """model.hpp:18-35: global knot vectors, the converged control lattice,
+    domain bounds and run provenance.  eval / eval_deriv / decode_grid run on
+    the GPU (model.cu)."""
     degrees: List[int]
     kvs: List[KnotVector]
     controls: np.ndarray
     bounds: List[tuple]
+    provenance: dict = field(default_factory=dict)
+
+    def rank(self) -> int:
+        return len(self.kvs)
+
+    def validate(self):
+        """model.cpp:11-24."""
+        if not self.kvs or len(self.kvs) != len(self.degrees) or len(self.kvs) != len(self.bounds):
+            raise InvalidArgument("MfaModel: inconsistent dimension counts")
+        if np.asarray(self.controls).ndim != self.rank():
+            raise InvalidArgument("MfaModel: control lattice rank mismatch")
+        for d, kv in enumerate(self.kvs):
+            if kv.degree != self.degrees[d]:
+                raise InvalidArgument(f"MfaModel: degree mismatch in dimension {d}")
+            if kv.basis_count() != np.asarray(self.controls).shape[d]:
+                raise InvalidArgument(f"MfaModel: control extent must equal #knots - p - 1 in dimension {d}")
+
+    def param_of(self, dim, x) -> float:
+        """model.cpp:26-29."""
+        a, b = self.bounds[dim]
+        return (x - a) / (b - a)
+
+    def eval(self, params, ctx: Optional[Context] = None) -> float:
+        """model.cpp:31-33."""
+        return float(eval_points(self.controls, self.kvs, np.asarray(params, np.float64)[None, :], ctx=ctx)[0])
+
+    def eval_deriv(self, params, orders, ctx: Optional[Context] = None) -> float:
+        """model.cpp:35-37."""
+        return float(eval_points(self.controls, self.kvs, np.asarray(params, np.float64)[None, :], orders,
+                                 ctx=ctx)[0])
+
+    def decode_grid(self, res, ctx: Optional[Context] = None) -> np.ndarray:
+        """model.cpp:39-49 (GPU decode at u_j = j / (res - 1))."""
+        ctx = ctx or default_context()
+        if len(res) != self.rank():
+            raise InvalidArgument("decode_grid: resolution rank mismatch")
+        if len(set(self.degrees)) != 1:
+            raise InvalidArgument("decode_grid: mixed per-dimension degrees are not supported")
+        c = np.ascontiguousarray(self.controls, np.float64)
+        kn, ko = _pack_knots(self.kvs)
+        r = np.array(res, np.int64)
+        out = np.zeros(tuple(int(x) for x in res) if all(x >= 2 for x in res) else (1,), np.float64)
+        _check(L.load().mfadd_decode_grid(ctx._h, self.rank(), self.degrees[0], _dp(kn), _lp(ko),
+                                          _lp(np.array(c.shape, np.int64)), _dp(c), _lp(r), _dp(out)))
+        return out
+
+
+class Side:
+    """decode.hpp:24."""
+    Below = 0
+    Above = 1
+
+
+def _pack_knots(kvs):
+    kn = np.ascontiguousarray(np.concatenate([np.asarray(k.knots, np.float64) for k in kvs]))
+    ko = np.zeros(len(kvs) + 1, np.int64)
+    for i, k in enumerate(kvs):
+        ko[i + 1] = ko[i] + len(k.knots)
+    return kn, ko
+
+
+def eval_points(controls, kvs: Sequence[KnotVector], points, orders=None, side_dim: int = -1, side: int = Side.Above,
+                col_offset=None, ctx: Optional[Context] = None) -> np.ndarray:
+    """Batched eval_deriv / eval_deriv_sided (decode.hpp:28-40) on the GPU:
+    points [npts][rank] -> values [npts], bitwise equal to the reference."""
+    ctx = ctx or default_context()
+    c = np.ascontiguousarray(controls, np.float64)
+    pts = np.ascontiguousarray(np.atleast_2d(np.asarray(points, np.float64)))
+    if c.ndim != len(kvs) or pts.shape[1] != len(kvs):
+        raise InvalidArgument("decode: dimension mismatch between lattice, knot vectors and parameters")
+    kn, ko = _pack_knots(kvs)
+    deg = np.array([k.degree for k in kvs], np.int32)
+    ords = None if orders is None or len(orders) == 0 else np.array(orders, np.int32)
+    off = None if col_offset is None or len(col_offset) == 0 else np.array(col_offset, np.int64)
+    out = np.zeros(pts.shape[0], np.float64)
+    _check(L.load().mfadd_eval_points(ctx._h, len(kvs), _ip(deg), _dp(kn), _lp(ko), _lp(np.array(c.shape, np.int64)),
+                                      None if off is None else _lp(off), _dp(c), pts.shape[0], _dp(pts),
+                                      None if ords is None else _ip(ords), side_dim, side, _dp(out)))
+    return out
+
+
+def eval_deriv(controls, kvs, point, orders=None, col_offset=None, ctx: Optional[Context] = None) -> float:
+    """decode.hpp:28-30."""
+    return float(eval_points(controls, kvs, np.asarray(point, np.float64)[None, :], orders, -1, Side.Above,
+                             col_offset, ctx)[0])
+
+
+def eval_deriv_sided(controls, kvs, point, orders, side_dim, side, col_offset=None,
+                     ctx: Optional[Context] = None) -> float:
+    """decode.hpp:35-38."""
+    return float(eval_points(controls, kvs, np.asarray(point, np.float64)[None, :], orders, side_dim, side,
+                             col_offset, ctx)[0])
+
+
+def continuity_jumps(model: MfaModel, dim: int, u_interface: float, max_order: int, cross_samples: int = 5,
+                     ctx: Optional[Context] = None) -> List[float]:
+    """solver.hpp:96 (assembled-model variant); probe points evaluated on the GPU."""
+    ctx = ctx or default_context()
+    c = np.ascontiguousarray(model.controls, np.float64)
+    kn, ko = _pack_knots(model.kvs)
+    deg = np.array(model.degrees, np.int32)
+    out = np.zeros(max(max_order, 0) + 1, np.float64)
+    _check(L.load().mfadd_continuity_jumps(ctx._h, model.rank(), _ip(deg), _dp(kn), _lp(ko),
+                                           _lp(np.array(c.shape, np.int64)), _dp(c), dim, float(u_interface),
+                                           max_order, cross_samples, _dp(out)))
+    return [float(x) for x in out]
+
+
+def write_mfa(model: MfaModel, path) -> None:
+    """model.hpp:40: MFDD v1 container, bit-exact with the reference writer."""
+    c = np.ascontiguousarray(model.controls, np.float64)
+    kn, ko = _pack_knots(model.kvs)
+    deg = np.array(model.degrees, np.int32)
+    cl = np.array([1 if k.clamp_left else 0 for k in model.kvs], np.uint8)
+    cr = np.array([1 if k.clamp_right else 0 for k in model.kvs], np.uint8)
+    bnd = np.ascontiguousarray(np.array(model.bounds, np.float64).reshape(-1))
+    keys = [str(k).encode() for k in model.provenance]
+    vals = [str(model.provenance[k]).encode() for k in model.provenance]
+    v = L.ModelViewC()
+    v.rank = len(model.kvs)
+    v.degrees = _ip(deg)
+    v.clamp_left = cl.ctypes.data_as(C.POINTER(C.c_ubyte))
+    v.clamp_right = cr.ctypes.data_as(C.POINTER(C.c_ubyte))
+    v.knots = _dp(kn)
+    v.kn_off = _lp(ko)
+    ext = np.array(c.shape, np.int64)
+    v.ctrl_ext = _lp(ext)
+    v.bounds = _dp(bnd)
+    v.nprov = len(keys)
+    karr = (C.c_char_p * max(len(keys), 1))(*keys)
+    varr = (C.c_char_p * max(len(vals), 1))(*vals)
+    v.prov_keys = C.cast(karr, C.POINTER(C.c_char_p))
+    v.prov_values = C.cast(varr, C.POINTER(C.c_char_p))
+    v.controls = _dp(c)
+    _check(L.load().mfadd_write_mfa(str(path).encode(), C.byref(v)))
+
+
+def read_mfa(path) -> MfaModel:
+    """model.hpp:41."""
+    lib = L.load()
+    h = C.c_void_p()
+    _check(lib.mfadd_read_mfa(str(path).encode(), C.byref(h)))
+    try:
+        v = L.ModelViewC()
+        _check(lib.mfadd_model_view_of(h, C.byref(v)))
+        r = v.rank
+        ko = [int(v.kn_off[i]) for i in range(r + 1)]
+        ext = [int(v.ctrl_ext[i]) for i in range(r)]
+        kvs = []
+        for d in range(r):
+            kn = np.array([v.knots[i] for i in range(ko[d], ko[d + 1])], np.float64)
+            kvs.append(KnotVector(int(v.degrees[d]), kn, bool(v.clamp_left[d]), bool(v.clamp_right[d])))
+        n = int(np.prod(ext))
+        ctrl = np.ctypeslib.as_array(v.controls, shape=(n,)).copy().reshape(ext)
+        bounds = [(float(v.bounds[2 * d]), float(v.bounds[2 * d + 1])) for d in range(r)]
+        prov = {v.prov_keys[i].decode(): v.prov_values[i].decode() for i in range(v.nprov)}
+        return MfaModel([int(v.degrees[d]) for d in range(r)], kvs, ctrl, bounds, prov)
+    finally:
+        lib.mfadd_model_free(h)
+
+
+class RawScalar:
+    """field.hpp:43."""
+    Float32 = 0
+    Float64 = 1
+
+
+class RawByteOrder:
+    """field.hpp:44."""
+    Little = 0
+    Big = 1
+
+
+def read_raw_grid(path, dims, type: int, order: int = RawByteOrder.Little, bounds=None, device_out=None,
+                  ctx: Optional[Context] = None):
+    """field.hpp:48-50: the bytes are copied to the device and byte-swapped /
+    widened to fp64 there (model.cu k_raw_to_f64).  With `device_out` (a CUDA
+    pointer of prod(dims) doubles, e.g. torch tensor.data_ptr()) the field
+    stays in HBM and only the Field metadata is returned."""
+    ctx = ctx or default_context()
+    import os
+    dims = [int(d) for d in dims]
+    d_arr = np.array(dims, np.int64)
+    values = None
+    if device_out is None:
+        values = np.zeros(int(np.prod(dims)) if dims else 0, np.float64)
+        ptr, on_dev = values.ctypes.data_as(C.c_void_p), 0
+    else:
+        ptr, on_dev = C.c_void_p(int(device_out)), 1
+    _check(L.load().mfadd_read_raw_grid(ctx._h, str(path).encode(), len(dims), _lp(d_arr), int(type), int(order), ptr,
+                                        on_dev))
+    b = list(bounds) if bounds else [(0.0, 1.0)] * len(dims)
+    if len(b) != len(dims):
+        raise InvalidArgument("read_raw_grid: bounds/dims mismatch")
+    return Field(dims, b, None if values is None else values.reshape(dims), os.path.basename(str(path)))
 
 
 @dataclass
@@ -721,6 +919,15 @@ class Solver:
         n = L.load().mfadd_solver_kernel_times(self._h, names, nl, _dp(ms), cap)
         raw = names.raw
         return [(raw[i * nl:(i + 1) * nl].split(b"\0")[0].decode(), float(ms[i])) for i in range(min(n, cap))]
+
+    def continuity_probe(self, probe_order: int = -1, cross_samples: int = 5):
+        """The pipeline's continuity probe (pipeline.cpp:210-228) over every
+        interior interface of the last solve, on the device-resident block
+        lattices: returns (order, jumps[0..order])."""
+        out = np.zeros(max(probe_order, self.dec.degree - 1, 0) + 1, np.float64)
+        o = C.c_int()
+        _check(L.load().mfadd_solver_continuity_probe(self._h, probe_order, cross_samples, _dp(out), C.byref(o)))
+        return o.value, [float(x) for x in out[:o.value + 1]]
 
     def last_launches(self) -> int:
         return L.load().mfadd_solver_last_launches(self._h)

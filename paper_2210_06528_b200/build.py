@@ -21,6 +21,19 @@ LIB_DEBUG = os.path.join(HERE, "libmfadd_b200_debug.so")  # -DMFB_DEBUG: device-
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _nccl_dir():
+    """The NCCL torch itself loads (site-packages/nvidia/nccl).  Linking the
+    same library (by path + rpath) keeps one libnccl.so.2 per process whatever
+    the import order; the system copy is older and would satisfy the SONAME
+    first if this library were loaded before torch."""
+    try:
+        import nvidia.nccl as nn  # noqa: F401
+        base = os.path.dirname(nn.__file__) if getattr(nn, "__file__", None) else list(nn.__path__)[0]
+    except Exception:
+        return None
+    return base if os.path.exists(os.path.join(base, "lib", "libnccl.so.2")) else None
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC,-fvisibility=hidden",
          "-Xptxas", "-O3"]
 
@@ -50,7 +63,9 @@ def build(force: bool = False, verbose: bool = False, debug: bool = False) -> st
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         objs.append(obj)
-        cmd = [NVCC, *ARCH, *FLAGS, *extra, "-I", CSRC, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
+        ncl = _nccl_dir()
+        inc = ["-I", os.path.join(ncl, "include")] if ncl else []
+        cmd = [NVCC, *ARCH, *FLAGS, *extra, *inc, "-I", CSRC, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
         if src.endswith(".cpp"):
             cmd = [NVCC, "-Wno-deprecated-gpu-targets", *FLAGS, "-x", "c++", "-I", CSRC, "-c", src, "-o", obj]
         if verbose:
@@ -67,7 +82,10 @@ def build(force: bool = False, verbose: bool = False, debug: bool = False) -> st
     if failed:
         raise RuntimeError("libmfadd_b200 build failed")
     tmp = lib + ".tmp"
-    link = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart_static", "-lnccl", "-lrt", "-ldl", "-lpthread"]
+    ncl = _nccl_dir()
+    nccl = ["-L", os.path.join(ncl, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath=" + os.path.join(ncl, "lib")] \
+        if ncl else ["-lnccl"]
+    link = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart_static", *nccl, "-lrt", "-ldl", "-lpthread"]
     if verbose:
         print(" ".join(link))
     subprocess.run(link, check=True)

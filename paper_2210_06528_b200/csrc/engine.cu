@@ -31,62 +31,24 @@ using mfb::AxisProb;
 using mfb::BlockDev;
 using mfb::Decomp;
 
-#define MFB_API extern "C" __attribute__((visibility("default")))
+#include "abi.hpp"
 
-namespace {
+using namespace mfb_abi;
 
+namespace mfb_abi {
 thread_local std::string g_err;
 thread_local int g_err_dim = -1;
 thread_local std::int64_t g_err_span = -1;
+}  // namespace mfb_abi
 
-struct ApiError : std::runtime_error {
-  int code;
-  ApiError(int c, const std::string& w) : std::runtime_error(w), code(c) {}
-};
+namespace {
 
-void cuda_check(cudaError_t e, const char* what) {
-  if (e != cudaSuccess) throw ApiError(MFADD_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
-}
 #define CK(x) cuda_check((x), #x)
 #define NCK(x)                                                                                   \
   do {                                                                                           \
     const ncclResult_t r_ = (x);                                                                 \
     if (r_ != ncclSuccess) throw ApiError(MFADD_ECUDA, std::string(#x) + ": " + ncclGetErrorString(r_)); \
   } while (0)
-
-template <class Fn>
-int guarded(Fn&& fn) {
-  try {
-    fn();
-    return MFADD_OK;
-  } catch (const ApiError& e) {
-    g_err = e.what();
-    return e.code;
-  } catch (const mfb::SingularFit& e) {
-    g_err = e.what();
-    g_err_dim = e.dim;
-    g_err_span = e.span;
-    return MFADD_ESINGULAR;
-  } catch (const std::invalid_argument& e) {
-    g_err = e.what();
-    return MFADD_EINVAL;
-  } catch (const std::out_of_range& e) {
-    g_err = e.what();
-    return MFADD_ERANGE;
-  } catch (const std::logic_error& e) {
-    g_err = e.what();
-    return MFADD_ELOGIC;
-  } catch (const std::bad_alloc& e) {
-    g_err = "host allocation failed";
-    return MFADD_ENOMEM;
-  } catch (const std::runtime_error& e) {
-    g_err = e.what();
-    return MFADD_ERUNTIME;
-  } catch (...) {
-    g_err = "unknown error";
-    return MFADD_ERUNTIME;
-  }
-}
 
 // Owning device buffer.
 template <class T>
@@ -186,29 +148,9 @@ struct mfadd_decomposition {
   Decomp d;
 };
 
-struct mfadd_context {
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  bool own_stream = false;
-  std::int64_t launches = 0;
-  mfb::DevStatus* d_status = nullptr;
-  double* h_pinned = nullptr;  // 16 doubles of pinned host scratch
-};
 
 namespace {
 
-struct ContextScope {  // make the context's device current for the call
-  int prev = -1;
-  explicit ContextScope(const mfadd_context* c) {
-    cudaGetDevice(&prev);
-    if (prev != c->device) CK(cudaSetDevice(c->device));
-  }
-  ~ContextScope() {
-    int cur = -1;
-    cudaGetDevice(&cur);
-    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
-  }
-};
 
 // Optional per-kernel CUDA-event timeline (bench roofline / phase evidence).
 struct Timeline {
@@ -2326,6 +2268,80 @@ MFB_API int mfadd_solver_block_controls(const mfadd_solver* s, int block, double
     CK(cudaMemcpyAsync(out, s->wl.P.p + b.poff, static_cast<std::size_t>(np) * sizeof(double),
                        out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s->ctx->stream));
     CK(cudaStreamSynchronize(s->ctx->stream));
+  });
+}
+
+// The pipeline's continuity probe (pipeline.cpp:210-228): for every block and
+// every dim with an upper neighbour, continuity_jumps(below, above, dec, dim,
+// u = span_param(dim, span_hi), order) (solver.cpp:263-277) on the held
+// lattices of the last solve, all probe points of all interfaces in one
+// batched GPU evaluation (model.cu); max over interfaces per order.
+MFB_API int mfadd_solver_continuity_probe(mfadd_solver* s, int probe_order, int cross_samples, double* out,
+                                          int* out_order) {
+  return guarded([&] {
+    if (!s->have_result) throw std::logic_error("mfadd_solver_continuity_probe: no solve result");
+    if (s->nranks != 1) throw std::logic_error("mfadd_solver_continuity_probe: needs every block on this rank");
+    ContextScope scope(s->ctx);
+    const Decomp& d = s->dec;
+    const int rank = d.rank;
+    const int order = probe_order >= 0 ? probe_order : d.degree - 1;
+    auto span_param = [&](int k, std::int64_t t) {  // layout.cpp:22-27
+      const auto& sk = d.span_knot[static_cast<std::size_t>(k)];
+      const auto& kn = d.knots[static_cast<std::size_t>(k)];
+      if (t == static_cast<std::int64_t>(sk.size())) return kn[kn.size() - static_cast<std::size_t>(d.degree) - 1];
+      return kn[static_cast<std::size_t>(sk[static_cast<std::size_t>(t)])];
+    };
+    std::vector<mfb::EvalLattice> lats(static_cast<std::size_t>(d.nblocks));
+    for (int b = 0; b < d.nblocks; ++b) {
+      const BlockDev& bd = s->wl.blocks[static_cast<std::size_t>(b)];
+      mfb::EvalLattice& L = lats[static_cast<std::size_t>(b)];
+      L.base = bd.poff;
+      for (int k = 0; k < rank; ++k) {
+        L.ext[k] = s->wl.probs[static_cast<std::size_t>(bd.ax[k])].n;
+        L.coff[k] = s->wl.probs[static_cast<std::size_t>(bd.ax[k])].col_lo;
+      }
+    }
+    std::vector<mfb::EvalItem> items;
+    std::vector<std::size_t> firsts;
+    for (int b = 0; b < d.nblocks; ++b)
+      for (int dim = 0; dim < rank; ++dim) {
+        const auto& c = d.coords[static_cast<std::size_t>(b)];
+        if (c[static_cast<std::size_t>(dim)] + 1 >= d.blocks[static_cast<std::size_t>(dim)]) continue;
+        int ac[3] = {c[0], c[1], c[2]};
+        ++ac[dim];
+        const int above = d.block_id(ac);
+        const double u = span_param(dim, d.at(b, dim, mfb::SPAN_HI));
+        std::vector<std::vector<double>> cross;  // probe_cross_params, solver.cpp:197-209
+        for (int k = 0; k < rank; ++k) {
+          if (k == dim) continue;
+          const double lo = span_param(k, d.at(b, k, mfb::SPAN_LO)), hi = span_param(k, d.at(b, k, mfb::SPAN_HI));
+          std::vector<double> pts;
+          for (int q = 0; q < cross_samples; ++q) {
+            const double t = cross_samples == 1
+                                 ? 0.5
+                                 : 0.1 + 0.8 * static_cast<double>(q) / static_cast<double>(cross_samples - 1);
+            pts.push_back(lo + t * (hi - lo));
+          }
+          cross.push_back(std::move(pts));
+        }
+        firsts.push_back(items.size());
+        mfb::probe_items(rank, dim, u, order, cross, b, above, items);
+      }
+    firsts.push_back(items.size());
+    std::vector<int> degs(static_cast<std::size_t>(rank), d.degree);
+    std::vector<double> kn;
+    std::vector<std::int64_t> ko(1, 0);
+    for (int k = 0; k < rank; ++k) {
+      kn.insert(kn.end(), d.knots[static_cast<std::size_t>(k)].begin(), d.knots[static_cast<std::size_t>(k)].end());
+      ko.push_back(static_cast<std::int64_t>(kn.size()));
+    }
+    std::vector<double> vals;
+    mfb::eval_items_device(s->ctx, rank, degs.data(), kn.data(), ko.data(), s->wl.P.p, lats, items, vals);
+    std::vector<double> jumps(static_cast<std::size_t>(order) + 1, 0.0);
+    for (std::size_t f = 0; f + 1 < firsts.size(); ++f)
+      mfb::probe_reduce(vals, firsts[f], firsts[f + 1] - firsts[f], order, jumps);
+    std::memcpy(out, jumps.data(), jumps.size() * sizeof(double));
+    if (out_order) *out_order = order;
   });
 }
 

@@ -256,4 +256,51 @@ int launch_decode_tma(int degree, const DecodeSweepArgs& a, const CUtensorMap& m
 // K7b: deterministic reduction of the tile partials.
 int launch_reduce_partials(const double* partial, std::int64_t n, double* out2, cudaStream_t s);
 
+
+// Point evaluation (model.cu): eval_deriv / eval_deriv_sided (decode.cpp:14-80)
+// of items against one or more control lattices resident on the device.
+struct EvalLattice {
+  std::int64_t base;     // offset of the lattice in EvalArgs::ctrl
+  std::int64_t ext[3];   // extents
+  std::int64_t coff[3];  // col_offset (global index of local column 0)
+};
+struct EvalItem {
+  int lat;       // EvalLattice index
+  int side_dim;  // -1: unsided
+  int side;      // 0 Below, 1 Above (decode.hpp:24)
+  int pad_;
+  int ord[3];    // derivative order per dim
+  int pad2_;
+  double pt[3];  // parameters
+};
+struct EvalArgs {
+  int rank;
+  int deg[3];
+  const double* knots;
+  std::int64_t kn_off[4];
+  const double* ctrl;
+  const EvalLattice* lats;
+  const EvalItem* items;
+  std::int64_t n;
+  double* out;
+  int* err;  // per item: 0, or (code << 8) | dim (1 order > degree, 2 find_span range, 3 lattice window)
+};
+int launch_eval_points(const EvalArgs& a, cudaStream_t s);
+// field.cpp:170-185 on the device: n raw scalars (width 4 or 8, optional byte swap) -> fp64
+int launch_raw_to_f64(const unsigned char* raw, std::int64_t n, int width, int swap, double* out, cudaStream_t s);
+
+}  // namespace mfb
+
+#include <vector>
+struct mfadd_context;
+namespace mfb {
+// Host helpers over launch_eval_points (model.cu), shared with engine.cu.
+void eval_items_device(mfadd_context* ctx, int rank, const int* degrees, const double* knots,
+                       const std::int64_t* kn_off, const double* d_ctrl, const std::vector<EvalLattice>& lats,
+                       const std::vector<EvalItem>& items, std::vector<double>& out);
+void probe_items(int rank, int dim, double u, int max_order, const std::vector<std::vector<double>>& cross,
+                 int lat_below, int lat_above, std::vector<EvalItem>& items);
+void probe_reduce(const std::vector<double>& vals, std::size_t first, std::size_t count, int max_order,
+                  std::vector<double>& jumps);
+
 }  // namespace mfb
