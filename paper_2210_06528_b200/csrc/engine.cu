@@ -267,7 +267,10 @@ struct Workload {
     // B2 is the TMA box width W (even); it includes one spare column so the
     // box can start on an even (16-B aligned) column (stream_tma.cu).
     if (D == 2) {
-      const int nt = (mx1 + 253) / 254;
+      // columns per CTA (threads = cols + 2): 144 -> four tiles of a C5 block,
+      // seven CTAs per SM with a 3-stage ring (one wave for 256 blocks)
+      const int wmax = env_int("MFADD_AX0_COLS", 144);
+      const int nt = (mx1 + wmax - 1) / wmax;
       const int cols = round_up((mx1 + nt - 1) / nt, 2);
       axis0_geo.B2 = cols + 2;
       axis0_geo.B1 = 1;
@@ -279,7 +282,7 @@ struct Workload {
       axis0_tiles = (mx1 + axis0_geo.B1 - 1) / axis0_geo.B1;
     }
     axis0_geo.R = 8;
-    axis0_geo.S = env_int("MFADD_FIT_S", 4);
+    axis0_geo.S = env_int("MFADD_FIT_S", 3);
     int mxn = 0;
     for (const auto& b : blocks) mxn = std::max(mxn, probs[static_cast<std::size_t>(b.ax[0])].n);
     const int need = (mxn + 2 * (p + 1)) * (2 * p + 1);  // padded Cholesky table in smem
@@ -446,9 +449,10 @@ struct Workload {
     tl->end();
     int max_m_factor = 0;
     for (int id : factor_ids) max_m_factor = std::max(max_m_factor, probs[static_cast<std::size_t>(id)].m);
-    mfb::CholArgs ca{d_probs.p, d_factor.p, static_cast<int>(factor_ids.size()), max_n_factor, max_m_factor, 0, g0.p,
-                     vals.p, ltab.p, ctx->d_status};
-    if (defer_mode == 2) {  // fork: the factorizations run beside the axis-0 contraction
+    mfb::CholArgs ca{d_probs.p, d_factor.p, static_cast<int>(factor_ids.size()), max_n_factor, max_m_factor, 0, 0,
+                     g0.p, vals.p, ltab.p, ctx->d_status};
+    static const bool chol_inline = std::getenv("MFADD_CHOL_INLINE") != nullptr;  // measurement aid
+    if (defer_mode == 2 && !chol_inline) {  // fork: the factorizations run beside the axis-0 contraction
       if (!side) {
         CK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&ev_rows, cudaEventDisableTiming));
@@ -458,6 +462,8 @@ struct Workload {
       CK(cudaStreamWaitEvent(side, ev_rows, 0));
       cudaStream_t main_st = tl->st;
       tl->st = side;
+      static const bool heavy = std::getenv("MFADD_CHOL_HEAVY") != nullptr;  // measurement aid
+      ca.light = heavy ? 0 : 1;
       tl->begin("gram_chol");
       l += mfb::launch_gram_chol(p, ca, side);
       tl->end();
@@ -535,7 +541,9 @@ struct Workload {
         l += mfb::launch_fit_strided(p, fa, d, ctx->stream);
       }
       tl->end();
-      if (d == 0 && defer_mode == 2) CK(cudaStreamWaitEvent(ctx->stream, ev_chol, 0));  // join the factorizations
+      // join the factorizations (D = 2 with the TMA last axis: inside the
+      // last-axis launch, after its contraction, which needs no factor)
+      if (d == 0 && defer_mode == 2 && !(D == 2 && tma_last)) CK(cudaStreamWaitEvent(ctx->stream, ev_chol, 0));
     }
     if (D == 1 && defer_mode == 2) CK(cudaStreamWaitEvent(ctx->stream, ev_chol, 0));
     if (D == 2 && defer_mode == 2 && tma_last && !std::getenv("MFADD_NO_FUSE2D")) {
@@ -546,6 +554,7 @@ struct Workload {
       }
       fa.fuse2d = mfb::solve2d_smem(p, fa.max_n0, fa.max_n1, fa.max_zl, last_kseg) > 0 ? 1 : 0;
     }
+    if (D == 2 && defer_mode == 2 && tma_last) fa.join_event = ev_chol;
     tl->begin("fit_last");
     if (tma_last) {
       const double* src = D == 2 ? t1.p : t2.p;
@@ -1353,7 +1362,8 @@ std::unique_ptr<mfadd_solver> create_solver(mfadd_context* ctx, const mfadd_deco
       int sms = 148;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
       const int M0 = static_cast<int>(s->srange.in_hi - s->srange.in_lo);  // this rank's input rows
-      const int want = std::max(1, (8 * sms + s->dnt1 * s->dnt2 - 1) / (s->dnt1 * s->dnt2));
+      const int per_sm = env_int("MFADD_DEC_CTAS", 8);  // CTAs per SM the row ranges aim at
+      const int want = std::max(1, (per_sm * sms + s->dnt1 * s->dnt2 - 1) / (s->dnt1 * s->dnt2));
       const int nr = std::max(1, std::min(want, (M0 + s->dgeo.R - 1) / s->dgeo.R));
       s->dH = round_up((M0 + nr - 1) / nr, s->dgeo.R);
       s->dnrange = (M0 + s->dH - 1) / s->dH;

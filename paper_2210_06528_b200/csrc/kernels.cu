@@ -167,11 +167,34 @@ __global__ void __launch_bounds__(256) k_gram_chol(CholArgs a) {
   const int n = pr.n, m = pr.m;
   const int* g0 = a.g0 + pr.row_off;
   const double* v = a.vals + pr.row_off * (P + 1);
+  double* band = a.ltab + pr.col_off * (2 * P + 1);  // light mode: the Gram band between the two launches
+  if (a.light == 2) {  // Cholesky-only launch: the band written by the Gram-only launch
+    for (int e = threadIdx.x; e < n * (P + 1); e += blockDim.x) sm[e] = band[e];
+    __syncthreads();
+  } else {
   if (a.stage_rows) {  // row table -> smem (coalesced), then the Gram reads are smem hits
     double* sv = sm + a.max_n * (P + 1);
     int* sg = reinterpret_cast<int*>(sv + a.max_m * (P + 1));
-    for (int i = threadIdx.x; i < m * (P + 1); i += blockDim.x) sv[i] = v[i];
-    for (int i = threadIdx.x; i < m; i += blockDim.x) sg[i] = g0[i];
+    {  // 8 independent loads in flight per thread (the copy is latency-bound otherwise)
+      constexpr int B = 8;
+      const int nv = m * (P + 1), nt = static_cast<int>(blockDim.x);
+      for (int i0 = threadIdx.x; i0 < nv; i0 += B * nt) {
+        double t[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) t[u] = i0 + u * nt < nv ? __ldg(v + i0 + u * nt) : 0.0;
+#pragma unroll
+        for (int u = 0; u < B; ++u)
+          if (i0 + u * nt < nv) sv[i0 + u * nt] = t[u];
+      }
+      for (int i0 = threadIdx.x; i0 < m; i0 += B * nt) {
+        int t[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) t[u] = i0 + u * nt < m ? __ldg(g0 + i0 + u * nt) : 0;
+#pragma unroll
+        for (int u = 0; u < B; ++u)
+          if (i0 + u * nt < m) sg[i0 + u * nt] = t[u];
+      }
+    }
     __syncthreads();
     v = sv;
     g0 = sg;
@@ -197,53 +220,66 @@ __global__ void __launch_bounds__(256) k_gram_chol(CholArgs a) {
     }
     sm[e] = s;
   }
+  if (a.light == 1) {  // Gram-only launch
+    for (int e = threadIdx.x; e < n * (P + 1); e += blockDim.x) band[e] = sm[e];
+    return;
+  }
   __syncthreads();
+  }
   if (threadIdx.x == 0) {
-    // Banded left-looking Cholesky (the Eigen LLT of lsq.cpp:46-49 restricted
-    // to the band: L has no fill outside it).  Row c is written back over
-    // sm[c*(P+1)..]: [1/L(c,c), L(c,c-1), .., L(c,c-P)].  The last P rows stay
-    // in a register window (Lw[r] = row c-1-r), so the dependent chain from
-    // one row to the next never waits on a shared-memory store/load.
-    double Lw[P][P + 1];
+    // Banded Cholesky (the Eigen LLT of lsq.cpp:46-49 restricted to the band:
+    // L has no fill outside it), right-looking within each row: as soon as
+    // L(c,c-k) is known it is applied to the pending sums of the entries
+    // left of it and to the diagonal, so the dependent chain per entry is one
+    // multiply and one FMA.  The last P rows sit in a register ring with
+    // compile-time slots (row j in slot j mod P; the column loop is unrolled
+    // by P), so the next row's first entries overlap this row's rsqrt.  Row c
+    // is written back over sm[c*(P+1)..]: [1/L(c,c), L(c,c-1), .., L(c,c-P)].
+    double R[P][P + 1];  // R[j mod P] = [1/L(j,j), L(j,j-1), .., L(j,j-P)]
 #pragma unroll
     for (int r = 0; r < P; ++r)
 #pragma unroll
-      for (int k = 0; k <= P; ++k) Lw[r][k] = 0.0;
-    for (int c = 0; c < n; ++c) {
-      double* Gc = sm + c * (P + 1);
-      double Lc[P + 1];
+      for (int k = 0; k <= P; ++k) R[r][k] = 0.0;
+    // Branch-free body (the tail past n reads the zero-padded Gram rows and is
+    // not stored), so the compiler can overlap a row's first entries with the
+    // previous row's reciprocal square root.
+    int bad = -1;
+    for (int c0 = 0; c0 < n; c0 += P) {
 #pragma unroll
-      for (int k = 0; k <= P; ++k) Lc[k] = Gc[k];
+      for (int u = 0; u < P; ++u) {
+        const int c = c0 + u;
+        const bool in = c < n;
+        double* Gc = sm + (in ? c : 0) * (P + 1);
+        double g[P + 1];
 #pragma unroll
-      for (int k = P; k >= 1; --k) {
-        if (c - k < 0) {
-          Lc[k] = 0.0;
-          continue;
+        for (int k = 0; k <= P; ++k) g[k] = in ? Gc[k] : 1.0;  // G(c,c), G(c,c-k); zero where c-k < 0
+        double Lc[P + 1];
+#pragma unroll
+        for (int k = P; k >= 1; --k) {
+          const int sj = (u - k + P) % P;  // row c-k
+          const double lk = g[k] * R[sj][0];
+          Lc[k] = lk;
+#pragma unroll
+          for (int k2 = k - 1; k2 >= 1; --k2) g[k2] = fma(-lk, R[(u - k2 + P) % P][k - k2], g[k2]);
+          g[0] = fma(-lk, lk, g[0]);
         }
-        // row j = c-k is Lw[k-1]: L(c,c-k) = (G(c,c-k) - sum_t L(c,c-t) L(j,c-t)) / L(j,j)
-        // newest value (Lc[k+1]) enters last: the older terms overlap its computation
-        double sacc = Lc[k];
+        double dg = g[0];
+        const bool sing = !(dg > 0.0);  // Eigen LLT NumericalIssue -> SingularFitError
+        bad = (sing && in && bad < 0) ? c : bad;
+        dg = sing ? 1.0 : dg;
+        // 1/sqrt(dg): fp32 estimate + two Newton steps (no slow-path branch)
+        double y = static_cast<double>(rsqrtf(static_cast<float>(dg)));
+        y = y * fma(-0.5 * dg, y * y, 1.5);
+        y = y * fma(-0.5 * dg, y * y, 1.5);
+        Lc[0] = y;
 #pragma unroll
-        for (int t = P; t >= k + 1; --t) sacc = fma(-Lc[t], Lw[k - 1][t - k], sacc);
-        Lc[k] = sacc * Lw[k - 1][0];
+        for (int k = 0; k <= P; ++k) {
+          if (in) Gc[k] = Lc[k];
+          R[u % P][k] = Lc[k];
+        }
       }
-      double dg = Lc[0];
-#pragma unroll
-      for (int k = P; k >= 1; --k) dg = fma(-Lc[k], Lc[k], dg);
-      if (!(dg > 0.0)) {  // Eigen LLT NumericalIssue -> SingularFitError
-        set_status(a.status, 3, pid, c);
-        dg = 1.0;
-      }
-      Lc[0] = rsqrt(dg);
-#pragma unroll
-      for (int k = 0; k <= P; ++k) Gc[k] = Lc[k];
-#pragma unroll
-      for (int r = P - 1; r >= 1; --r)
-#pragma unroll
-        for (int k = 0; k <= P; ++k) Lw[r][k] = Lw[r - 1][k];
-#pragma unroll
-      for (int k = 0; k <= P; ++k) Lw[0][k] = Lc[k];
     }
+    if (bad >= 0) set_status(a.status, 3, pid, bad);
   }
   __syncthreads();
   // table per column: [1/L(c,c), L(c,c-k) k=1..P, L(c+k,c) k=1..P]
@@ -1635,10 +1671,24 @@ struct CholLaunch {
     CholArgs b = a;
     size_t smem = static_cast<size_t>(a.max_n) * (P + 1) * sizeof(double);
     const size_t staged = smem + static_cast<size_t>(a.max_m) * ((P + 1) * sizeof(double) + sizeof(int));
-    b.stage_rows = staged <= 200 * 1024;
+    b.stage_rows = !a.light && staged <= 200 * 1024;
     if (b.stage_rows) smem = staged;
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_gram_chol<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    k_gram_chol<P><<<a.nfactor, 256, smem, s>>>(b);
+    if (!a.light) {
+      k_gram_chol<P><<<a.nfactor, 256, smem, s>>>(b);
+      return 1;
+    }
+    // light (beside the axis-0 sweep): the parallel Gram phase, then the
+    // serial Cholesky as one warp per problem with only the band in shared
+    // memory, so its CTAs co-reside with the sweep's instead of holding a
+    // full CTA's resources for the length of the dependent chain
+    b.light = 1;
+    b.stage_rows = 0;  // rows through L1: no shared-memory footprint beyond the band
+    k_gram_chol<P><<<a.nfactor, 256, static_cast<size_t>(a.max_n) * (P + 1) * sizeof(double), s>>>(b);
+    b.light = 2;
+    b.stage_rows = 0;
+    k_gram_chol<P><<<a.nfactor, 32, static_cast<size_t>(a.max_n) * (P + 1) * sizeof(double), s>>>(b);
+    return 2;
     return 1;
   }
 };

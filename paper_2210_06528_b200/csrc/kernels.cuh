@@ -39,6 +39,7 @@ struct CholArgs {
   int max_n;
   int max_m;      // rows of the largest factored problem
   int stage_rows; // 1: the row table is staged in shared memory
+  int light;      // 1: one warp per problem, rows read through L1 (runs beside the axis-0 sweep)
   const int* g0;
   const double* vals;
   double* ltab;
@@ -75,6 +76,7 @@ struct FitArgs {
   int min_n0;                        // smallest axis-0 held extent (partitioned final solve eligibility)
   int fuse2d;                        // D = 2: k_solve2d (CTA per block) replaces k_last_solve + the axis-0 solve
   int max_n0, max_n1, max_zl;        // largest held extents / Z pitch (k_solve2d shared-memory size)
+  void* join_event;                  // cudaEvent_t the last-axis solve waits for (factorizations on a side stream)
 };
 int launch_fit_strided(int degree, const FitArgs& a, int axis, cudaStream_t s);  // axis < D-1
 int launch_fit_last(int degree, const FitArgs& a, cudaStream_t s);

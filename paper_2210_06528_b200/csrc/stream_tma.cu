@@ -1271,8 +1271,8 @@ struct BacksubLaunch {
 };
 
 // ---------------------------------------------------------------- decode
-template <int P, int D, int S>
-__global__ void __launch_bounds__(256) k_decode_tma(const DecodeSweepArgs a, const __grid_constant__ CUtensorMap map,
+template <int P, int D, int S, int MB = 1>
+__global__ void __launch_bounds__(256, MB) k_decode_tma(const DecodeSweepArgs a, const __grid_constant__ CUtensorMap map,
                                                     const TmaGeom geo) {
   extern __shared__ __align__(1024) unsigned char sm_raw[];
   __shared__ double s_red[64];
@@ -1562,6 +1562,12 @@ struct DecodeSweepLaunch {
     const StageLayout SL = stage_layout(kFitR, g.B1 * g.B2, P);
     const size_t smem = static_cast<size_t>(S) * SL.stage_bytes + S * 8;
     dim3 grid(a.ntile1 * a.ntile2, a.nrange);
+    static const int mb = std::getenv("MFADD_DEC_MINB") ? std::atoi(std::getenv("MFADD_DEC_MINB")) : 1;
+    if (mb >= 4) {
+      cudaFuncSetAttribute(k_decode_tma<P, D, S, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      k_decode_tma<P, D, S, 4><<<grid, g.B1 * g.B2, smem, s>>>(a, map, g);
+      return;
+    }
     cudaFuncSetAttribute(k_decode_tma<P, D, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     k_decode_tma<P, D, S><<<grid, g.B1 * g.B2, smem, s>>>(a, map, g);
   }
@@ -1597,6 +1603,8 @@ struct LastLaunch {
     cudaFuncSetAttribute(k_last_contract_tma<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     dim3 grid((a.max_lines_last + LT - 1) / LT, a.nblocks, kseg);
     k_last_contract_tma<P><<<grid, LT, smem, s>>>(a, map, LT);
+    // the contraction needs no factor: the Gram/Cholesky side stream joins here
+    if (a.join_event) cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(a.join_event), 0);
     if (a.fuse2d) {
       const size_t sm2 = solve2d_smem_bytes(a.max_n0, a.max_n1, a.max_zl, P, kseg);
       cudaFuncSetAttribute(k_solve2d<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm2));
