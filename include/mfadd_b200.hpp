@@ -20,6 +20,7 @@
 
 #include <array>
 #include <cstdint>
+#include <map>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -251,6 +252,25 @@ struct Field {
   int rank() const { return static_cast<int>(dims.size()); }
 };
 
+// read_raw_grid (field.hpp:43-50): the bytes are converted on the GPU
+enum class RawScalar { Float32, Float64 };
+enum class RawByteOrder { Little, Big };
+inline Field read_raw_grid(const std::string& path, const std::vector<std::int64_t>& dims, RawScalar type,
+                           RawByteOrder order = RawByteOrder::Little,
+                           const std::vector<std::array<double, 2>>& bounds = {}, Context& ctx = default_context()) {
+  Field f;
+  f.dims = dims;
+  f.bounds = bounds.empty() ? std::vector<std::array<double, 2>>(dims.size(), {0.0, 1.0}) : bounds;
+  if (f.bounds.size() != dims.size()) throw std::invalid_argument("read_raw_grid: bounds/dims mismatch");
+  f.values = Tensor(dims);
+  check(mfadd_read_raw_grid(ctx.get(), path.c_str(), static_cast<int>(dims.size()), dims.data(),
+                            type == RawScalar::Float32 ? MFADD_RAW_F32 : MFADD_RAW_F64,
+                            order == RawByteOrder::Big ? MFADD_RAW_BIG : MFADD_RAW_LITTLE, f.values.data(), 0));
+  const auto slash = path.find_last_of('/');
+  f.name = slash == std::string::npos ? path : path.substr(slash + 1);
+  return f;
+}
+
 // ------------------------------------------------------------------- solve
 // SolverConfig (solver.hpp:16-22), same defaults.
 struct SolverConfig {
@@ -278,14 +298,148 @@ struct PhaseTimings {
   double setup = 0.0, local_solve = 0.0, exchange = 0.0, constraint = 0.0, decode = 0.0;
 };
 
-// MfaModel (model.hpp:19-37): the fields solve() fills.
+// decode.hpp:24
+enum class Side { Below, Above };
+
+namespace detail {
+inline void pack_knots(const std::vector<KnotVector>& kvs, std::vector<double>& kn, std::vector<std::int64_t>& ko,
+                       std::vector<int>& deg) {
+  ko.assign(1, 0);
+  for (const auto& kv : kvs) {
+    kn.insert(kn.end(), kv.knots.begin(), kv.knots.end());
+    ko.push_back(static_cast<std::int64_t>(kn.size()));
+    deg.push_back(kv.degree);
+  }
+}
+}  // namespace detail
+
+// eval_deriv_sided (decode.hpp:35-38); side_dim < 0: eval_deriv (decode.hpp:28-30)
+inline double eval_deriv_sided(const Tensor& controls, const std::vector<KnotVector>& kvs,
+                               const std::vector<double>& point, const std::vector<int>& orders, int side_dim,
+                               Side side, const std::vector<std::int64_t>& col_offset = {},
+                               Context& ctx = default_context()) {
+  std::vector<double> kn;
+  std::vector<std::int64_t> ko;
+  std::vector<int> deg;
+  detail::pack_knots(kvs, kn, ko, deg);
+  if (point.size() != kvs.size() || controls.rank() != static_cast<int>(kvs.size()))
+    throw std::invalid_argument("decode: dimension mismatch between lattice, knot vectors and parameters");
+  double out = 0.0;
+  check(mfadd_eval_points(ctx.get(), controls.rank(), deg.data(), kn.data(), ko.data(), controls.extents().data(),
+                          col_offset.empty() ? nullptr : col_offset.data(), controls.data(), 1, point.data(),
+                          orders.empty() ? nullptr : orders.data(), side_dim, side == Side::Above ? 1 : 0, &out));
+  return out;
+}
+inline double eval_deriv(const Tensor& controls, const std::vector<KnotVector>& kvs, const std::vector<double>& point,
+                         const std::vector<int>& orders, const std::vector<std::int64_t>& col_offset = {},
+                         Context& ctx = default_context()) {
+  return eval_deriv_sided(controls, kvs, point, orders, -1, Side::Above, col_offset, ctx);
+}
+
+// MfaModel (model.hpp:18-35)
 struct MfaModel {
   std::vector<int> degrees;
   std::vector<KnotVector> kvs;
   Tensor controls;
   std::vector<std::array<double, 2>> bounds;
+  std::map<std::string, std::string> provenance;
   int rank() const { return static_cast<int>(kvs.size()); }
+  double param_of(int dim, double x) const {
+    const auto& b = bounds[static_cast<std::size_t>(dim)];
+    return (x - b[0]) / (b[1] - b[0]);
+  }
+  double eval(const std::vector<double>& params) const { return mfadd_b200::eval_deriv(controls, kvs, params, {}); }
+  double eval_deriv(const std::vector<double>& params, const std::vector<int>& orders) const {
+    return mfadd_b200::eval_deriv(controls, kvs, params, orders);
+  }
+  // model.cpp:39-49 (GPU decode at u_j = j / (res - 1))
+  Tensor decode_grid(const std::vector<std::int64_t>& res, Context& ctx = default_context()) const {
+    if (static_cast<int>(res.size()) != rank()) throw std::invalid_argument("decode_grid: resolution rank mismatch");
+    std::vector<double> kn;
+    std::vector<std::int64_t> ko;
+    std::vector<int> deg;
+    detail::pack_knots(kvs, kn, ko, deg);
+    std::vector<std::int64_t> ext;
+    for (auto r : res) ext.push_back(r < 1 ? 1 : r);
+    Tensor out(ext);
+    check(mfadd_decode_grid(ctx.get(), rank(), deg[0], kn.data(), ko.data(), controls.extents().data(),
+                            controls.data(), res.data(), out.data()));
+    return out;
+  }
 };
+
+// continuity_jumps(const MfaModel&, ...) (solver.hpp:96)
+inline std::vector<double> continuity_jumps(const MfaModel& model, int dim, double u_interface, int max_order,
+                                            int cross_samples = 5, Context& ctx = default_context()) {
+  std::vector<double> kn;
+  std::vector<std::int64_t> ko;
+  std::vector<int> deg;
+  detail::pack_knots(model.kvs, kn, ko, deg);
+  std::vector<double> out(static_cast<std::size_t>(max_order < 0 ? 1 : max_order + 1), 0.0);
+  check(mfadd_continuity_jumps(ctx.get(), model.rank(), deg.data(), kn.data(), ko.data(),
+                               model.controls.extents().data(), model.controls.data(), dim, u_interface, max_order,
+                               cross_samples, out.data()));
+  return out;
+}
+
+// write_mfa / read_mfa (model.hpp:40-41): MFDD v1, byte-identical with the reference
+inline void write_mfa(const MfaModel& model, const std::string& path) {
+  std::vector<double> kn, bnd;
+  std::vector<std::int64_t> ko;
+  std::vector<int> deg;
+  detail::pack_knots(model.kvs, kn, ko, deg);
+  std::vector<unsigned char> cl, cr;
+  for (const auto& kv : model.kvs) {
+    cl.push_back(kv.clamp_left ? 1 : 0);
+    cr.push_back(kv.clamp_right ? 1 : 0);
+  }
+  for (const auto& b : model.bounds) {
+    bnd.push_back(b[0]);
+    bnd.push_back(b[1]);
+  }
+  std::vector<const char*> keys, vals;
+  for (const auto& [k, v] : model.provenance) {
+    keys.push_back(k.c_str());
+    vals.push_back(v.c_str());
+  }
+  mfadd_model_view v{};
+  v.rank = model.rank();
+  v.degrees = model.degrees.data();
+  v.clamp_left = cl.data();
+  v.clamp_right = cr.data();
+  v.knots = kn.data();
+  v.kn_off = ko.data();
+  v.ctrl_ext = model.controls.extents().data();
+  v.bounds = bnd.data();
+  v.nprov = static_cast<int>(keys.size());
+  v.prov_keys = keys.data();
+  v.prov_values = vals.data();
+  v.controls = model.controls.data();
+  check(mfadd_write_mfa(path.c_str(), &v));
+}
+
+inline MfaModel read_mfa(const std::string& path) {
+  mfadd_model* h = nullptr;
+  check(mfadd_read_mfa(path.c_str(), &h));
+  std::unique_ptr<mfadd_model, void (*)(mfadd_model*)> hold(h, mfadd_model_free);
+  mfadd_model_view v{};
+  check(mfadd_model_view_of(h, &v));
+  MfaModel m;
+  std::vector<std::int64_t> ext(v.ctrl_ext, v.ctrl_ext + v.rank);
+  for (int d = 0; d < v.rank; ++d) {
+    KnotVector kv;
+    kv.degree = v.degrees[d];
+    kv.knots.assign(v.knots + v.kn_off[d], v.knots + v.kn_off[d + 1]);
+    kv.clamp_left = v.clamp_left[d] != 0;
+    kv.clamp_right = v.clamp_right[d] != 0;
+    m.degrees.push_back(kv.degree);
+    m.kvs.push_back(std::move(kv));
+    m.bounds.push_back({v.bounds[2 * d], v.bounds[2 * d + 1]});
+  }
+  for (int i = 0; i < v.nprov; ++i) m.provenance[v.prov_keys[i]] = v.prov_values[i];
+  m.controls = Tensor(ext, std::vector<double>(v.controls, v.controls + Tensor::count(ext)));
+  return m;
+}
 
 // BlockState (solver.hpp:26-32): the held lattice of one block.
 struct BlockState {

@@ -324,7 +324,7 @@ struct Workload {
     }
   }
 
-  // Row segments of the last-axis problems: about 4 contraction threads per
+  // Row segments of the last-axis problems: about 2 contraction threads per
   // SM thread slot over all lines, segments of >= 64 rows on 16-row chunk
   // boundaries; carries sized per block.
   void plan_segments() {
@@ -334,13 +334,16 @@ struct Workload {
       for (int k = 0; k + 1 < D; ++k) Ll *= probs[static_cast<std::size_t>(b.ax[k])].n;
       lines += round_up(static_cast<int>(Ll), last_LT);
     }
-    const int want = static_cast<int>(std::lround(4.0 * 148 * 256 / static_cast<double>(std::max<std::int64_t>(lines, 1))));
+    // ~2 contraction threads per SM thread slot over all lines (C5: two
+    // segments; more segments add carries and a partial second wave)
+    const int want = static_cast<int>(std::lround(2.0 * 148 * 256 / static_cast<double>(std::max<std::int64_t>(lines, 1))));
     segtab.assign(probs.size() * mfb::kSegStride, 0);
     last_kseg = 1;
     for (const auto& b : blocks) {
       const int pid = b.ax[D - 1];
       const AxisProb& pr = probs[static_cast<std::size_t>(pid)];
-      int K = std::max(1, std::min({want, mfb::kMaxSeg, pr.m / 64}));
+      static const int kforce = env_int("MFADD_LAST_SEGS", 0);  // measurement aid
+      int K = std::max(1, std::min({kforce > 0 ? kforce : want, mfb::kMaxSeg, pr.m / 64}));
       // a segment must span more than P+1 columns so that carry ranges of
       // consecutive boundaries never overlap
       while (K > 1 && static_cast<std::int64_t>(pr.n) < static_cast<std::int64_t>(K) * 4 * (p + 1)) --K;

@@ -122,6 +122,24 @@ static void gpu_cases() {
     singular = ex.dim == 0 && ex.span >= 0;
   }
   EXPECT(singular);
+  // MfaModel output path (model.hpp): MFDD round trip, decode_grid, eval and
+  // the continuity probe on the converged model (floating interfaces: the
+  // value and first p-1 derivatives agree across an interior knot).
+  mfadd::MfaModel mm = r.model;
+  mm.provenance["source"] = "sinc";
+  const std::string path = "/tmp/mfadd_shim_model.mfa";
+  mfadd::write_mfa(mm, path);
+  const auto back_m = mfadd::read_mfa(path);
+  EXPECT(back_m.controls.values() == mm.controls.values() && back_m.provenance == mm.provenance);
+  EXPECT(back_m.kvs[1].knots == mm.kvs[1].knots && back_m.bounds == mm.bounds);
+  const auto grid = mm.decode_grid({64, 64});
+  double gmx = 0.0;
+  for (std::int64_t i = 0; i < grid.size(); ++i) gmx = std::fmax(gmx, std::fabs(grid[i] - dec_vals[i]));
+  EXPECT(gmx < 1e-12);
+  EXPECT(std::fabs(mm.eval({u[0][5], u[1][7]}) - dec_vals[5 * 64 + 7]) < 1e-12);
+  const auto jumps = mfadd::continuity_jumps(mm, 0, mm.kvs[0].knots[3 + 5], 2);
+  EXPECT(jumps.size() == 3 && jumps[0] < 1e-12 && jumps[1] < 1e-9);
+  std::remove(path.c_str());
 }
 
 int main(int argc, char** argv) {
