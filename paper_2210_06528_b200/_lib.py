@@ -12,6 +12,8 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 # MFADD_DEBUG=1 selects the bounds-checked build (libmfadd_b200_debug.so)
 LIB_PATH = os.path.join(HERE, "libmfadd_b200_debug.so" if os.environ.get("MFADD_DEBUG") else "libmfadd_b200.so")
+if os.environ.get("MFADD_LIB_VARIANT"):  # measurement aid: an in-tree build variant (libmfadd_b200_<v>.so)
+    LIB_PATH = os.path.join(HERE, f"libmfadd_b200_{os.environ['MFADD_LIB_VARIANT']}.so")
 
 c_dp = C.POINTER(C.c_double)
 c_lp = C.POINTER(C.c_int64)

@@ -1048,14 +1048,17 @@ constexpr int kSolve2dThreads = 256;
 // scaled by its 1/L(c,c).  The arithmetic is the reference's solve
 // (lsq.cpp:59-60) up to rounding order (1e-10 contract).  Full batches run
 // without bounds tests; the last < 2U+P steps run guarded.
+#ifndef MFB_RL_U
+#define MFB_RL_U 8  // unrolled steps per batch of the right-looking passes (rounded up to a multiple of P)
+#endif
 template <int P>
 struct RL {
   static constexpr int W = (P + 2) & ~1;  // table row (16-B multiple)
-  static constexpr int U = P * ((8 + P - 1) / P);
+  static constexpr int U = P * ((MFB_RL_U + P - 1) / P);
 };
 
 __host__ __device__ inline int rl_rows(int n, int P) {  // table rows incl. the P leading ones
-  const int U = P * ((8 + P - 1) / P);
+  const int U = P * ((MFB_RL_U + P - 1) / P);
   return P + n + 2 * U + P;
 }
 
