@@ -1274,7 +1274,7 @@ struct BacksubLaunch {
 };
 
 // ---------------------------------------------------------------- decode
-template <int P, int D, int S, int MB = 1>
+template <int P, int D, int S, int MB = 1, bool ERR = true>
 __global__ void __launch_bounds__(256, MB) k_decode_tma(const DecodeSweepArgs a, const __grid_constant__ CUtensorMap map,
                                                     const TmaGeom geo) {
   extern __shared__ __align__(1024) unsigned char sm_raw[];
@@ -1407,8 +1407,11 @@ __global__ void __launch_bounds__(256, MB) k_decode_tma(const DecodeSweepArgs a,
     return s;
   };
   if (active) fetch_plane(abase + P + 1);
-  double l2 = 0.0, li = 0.0;
-  double* errp = a.err ? a.err + static_cast<std::int64_t>(y0) * Tr + t : nullptr;  // error of the current row
+  double l2 = 0.0;
+  unsigned long long li = 0ull;  // L-inf as the bit pattern of |e| (ordered like the value)
+  // error of the current row (ERR: the error field is stored); inactive
+  // threads point at their clamped column and never store
+  double* errp = ERR ? a.err + static_cast<std::int64_t>(y0) * Tr + (active ? t : 0) : nullptr;
   // row cursor over the TMA stages
   int c = 0, jl = 0, jn = 0, gnext = 0x7fffffff;
   const double* sq = nullptr;
@@ -1450,13 +1453,16 @@ __global__ void __launch_bounds__(256, MB) k_decode_tma(const DecodeSweepArgs a,
         double sd = 0.0;
 #pragma unroll
         for (int k = 0; k <= P; ++k) sd = fma(vr[k], Tw[(u + k) % (P + 1)], sd);
-        if (active) {
-          const double e = sq[jl * nthr] - sd;
-          if (errp) *errp = e;
-          l2 = fma(e, e, l2);
-          li = fmax(li, fabs(e));
+        // no branches in the per-row body: inactive threads (box padding)
+        // compute on their staged column, store nothing and count zero
+        const double e = active ? sq[jl * nthr] - sd : 0.0;
+        if (ERR) {
+          if (active) *errp = e;
+          errp += Tr;
         }
-        if (errp) errp += Tr;
+        l2 = fma(e, e, l2);
+        const unsigned long long eb = dbits_s(e) & 0x7fffffffffffffffull;
+        li = li > eb ? li : eb;
         advance();
       }
       if (gnext == 0x7fffffff) break;
@@ -1466,15 +1472,16 @@ __global__ void __launch_bounds__(256, MB) k_decode_tma(const DecodeSweepArgs a,
     }
   }
   // CTA reduction -> partial[blockIdx]
+  double lid = __longlong_as_double(static_cast<long long>(li));
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
     l2 += __shfl_xor_sync(kFullMask, l2, off);
-    li = fmax(li, __shfl_xor_sync(kFullMask, li, off));
+    lid = fmax(lid, __shfl_xor_sync(kFullMask, lid, off));
   }
   const int wid = tid >> 5;
   if ((tid & 31) == 0) {
     s_red[wid] = l2;
-    s_red[32 + wid] = li;
+    s_red[32 + wid] = lid;
   }
   __syncthreads();
   if (tid == 0) {
@@ -1569,6 +1576,12 @@ struct DecodeSweepLaunch {
     if (mb >= 4) {
       cudaFuncSetAttribute(k_decode_tma<P, D, S, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
       k_decode_tma<P, D, S, 4><<<grid, g.B1 * g.B2, smem, s>>>(a, map, g);
+      return;
+    }
+    if (!a.err) {  // no error field: L2 / L-inf only
+      cudaFuncSetAttribute(k_decode_tma<P, D, S, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem));
+      k_decode_tma<P, D, S, 1, false><<<grid, g.B1 * g.B2, smem, s>>>(a, map, g);
       return;
     }
     cudaFuncSetAttribute(k_decode_tma<P, D, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
