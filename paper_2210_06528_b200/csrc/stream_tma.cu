@@ -233,6 +233,7 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
   auto advance = [&]() {
     if (++jl < jn) {
       gnext = sg[jl];
+      sq += nbox;  // this thread's column in the next staged row
       return;
     }
     __syncthreads();  // every column is done with chunk c: refill its stage
@@ -252,11 +253,11 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
       while (gnext == cbase) {  // CTA-uniform
         double q[NC];
         if (NC == 2) {
-          const double2 q2 = *reinterpret_cast<const double2*>(sq + jl * nbox);
+          const double2 q2 = *reinterpret_cast<const double2*>(sq);
           q[0] = q2.x;
           q[NC - 1] = q2.y;
         } else {
-          q[0] = sq[jl * nbox];
+          q[0] = *sq;
         }
         const double* vr = sv + jl * (P + 1);
 #pragma unroll
