@@ -239,10 +239,12 @@ struct Workload {
   // first pass that needs a factor)
   int defer_mode = 0;
   cudaStream_t side = nullptr;
-  cudaEvent_t ev_rows = nullptr, ev_chol = nullptr;
+  cudaEvent_t ev_rows = nullptr, ev_rows2 = nullptr, ev_chol = nullptr;
+  bool rows_split = false;  // the non-axis-0 rows are built on the side stream (joined before the last axis)
   ~Workload() {
     if (ev_rows) cudaEventDestroy(ev_rows);
     if (ev_chol) cudaEventDestroy(ev_chol);
+    if (ev_rows2) cudaEventDestroy(ev_rows2);
     if (side) cudaStreamDestroy(side);
   }
   bool tma_mid = false;  // D = 3 middle axis through a T1 tensor map
@@ -445,20 +447,41 @@ struct Workload {
     Timeline dummy;
     dummy.st = ctx->stream;
     if (!tl) tl = &dummy;
-    mfb::RowsArgs ra{d_probs.p, static_cast<int>(probs.size()), max_m, knots.p, params.p, g0.p, first_col.p,
-                     count.p, vals.p, ctx->d_status};
+    static const bool chol_inline = std::getenv("MFADD_CHOL_INLINE") != nullptr;  // measurement aid
+    const bool fork = defer_mode == 2 && !chol_inline;
+    // With the side stream, only the axis-0 problems' rows (the first ones:
+    // what the axis-0 sweep reads) are built before the sweep; the rest are
+    // built on the side stream ahead of the factorizations and joined before
+    // the last-axis contraction.
+    int n0p = 0;
+    rows_split = false;
+    if (fork && D >= 2) {
+      int lo_other = 1 << 30;
+      for (const auto& b : blocks) {
+        n0p = std::max(n0p, b.ax[0] + 1);
+        for (int k = 1; k < D; ++k) lo_other = std::min(lo_other, b.ax[k]);
+      }
+      rows_split = n0p < static_cast<int>(probs.size()) && lo_other >= n0p;
+    }
+    auto rows_args = [&](int lo, int hi) {
+      int mm = 0;
+      for (int i = lo; i < hi; ++i) mm = std::max(mm, probs[static_cast<std::size_t>(i)].m);
+      return mfb::RowsArgs{d_probs.p, hi - lo, mm, knots.p, params.p, g0.p, first_col.p, count.p, vals.p,
+                           ctx->d_status, lo};
+    };
     tl->begin("basis_rows");
-    int l = mfb::launch_basis_rows(p, ra, ctx->stream);
+    int l = mfb::launch_basis_rows(p, rows_split ? rows_args(0, n0p) : rows_args(0, static_cast<int>(probs.size())),
+                                   ctx->stream);
     tl->end();
     int max_m_factor = 0;
     for (int id : factor_ids) max_m_factor = std::max(max_m_factor, probs[static_cast<std::size_t>(id)].m);
     mfb::CholArgs ca{d_probs.p, d_factor.p, static_cast<int>(factor_ids.size()), max_n_factor, max_m_factor, 0, 0,
                      g0.p, vals.p, ltab.p, ctx->d_status};
-    static const bool chol_inline = std::getenv("MFADD_CHOL_INLINE") != nullptr;  // measurement aid
-    if (defer_mode == 2 && !chol_inline) {  // fork: the factorizations run beside the axis-0 contraction
+    if (fork) {  // the factorizations run beside the axis-0 sweep
       if (!side) {
         CK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&ev_rows, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ev_rows2, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&ev_chol, cudaEventDisableTiming));
       }
       CK(cudaEventRecord(ev_rows, ctx->stream));
@@ -468,6 +491,10 @@ struct Workload {
       static const bool heavy = std::getenv("MFADD_CHOL_HEAVY") != nullptr;  // measurement aid
       ca.light = heavy ? 0 : 1;
       tl->begin("gram_chol");
+      if (rows_split) {
+        l += mfb::launch_basis_rows(p, rows_args(n0p, static_cast<int>(probs.size())), side);
+        CK(cudaEventRecord(ev_rows2, side));
+      }
       l += mfb::launch_gram_chol(p, ca, side);
       tl->end();
       tl->st = main_st;
@@ -557,6 +584,7 @@ struct Workload {
       }
       fa.fuse2d = mfb::solve2d_smem(p, fa.max_n0, fa.max_n1, fa.max_zl, last_kseg) > 0 ? 1 : 0;
     }
+    if (rows_split && D == 2) CK(cudaStreamWaitEvent(ctx->stream, ev_rows2, 0));  // last-axis + decode rows
     if (D == 2 && defer_mode == 2 && tma_last) fa.join_event = ev_chol;
     tl->begin("fit_last");
     if (tma_last) {

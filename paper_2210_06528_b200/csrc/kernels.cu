@@ -89,7 +89,7 @@ __device__ __forceinline__ unsigned long long block_umax(unsigned long long v, u
 // ------------------------------------------------------------------- K1
 template <int P>
 __global__ void __launch_bounds__(256) k_basis_rows(RowsArgs a) {
-  const int pid = blockIdx.y;
+  const int pid = a.prob0 + static_cast<int>(blockIdx.y);
   const AxisProb pr = a.probs[pid];
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= pr.m) return;

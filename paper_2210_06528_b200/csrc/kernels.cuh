@@ -27,6 +27,7 @@ struct RowsArgs {
   int* count;            // BandedCollocation::count
   double* vals;          // (p+1) per row, clipped entries zero, unclipped positions
   DevStatus* status;
+  int prob0;             // the launch covers problems [prob0, prob0 + nprobs)
 };
 int launch_basis_rows(int degree, const RowsArgs& a, cudaStream_t s);
 
