@@ -98,6 +98,7 @@ struct EpochState {
   int last_iter;     // last iteration that ran
   int converged;     // dp < tol at last_iter
   unsigned long long jump_ss, jump_ms;
+  unsigned long long jump0_ss;  // fused epoch 0 + iteration 1 (mode 4): the SS jump before the averaging
 };
 
 }  // namespace mfb

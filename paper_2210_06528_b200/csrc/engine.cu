@@ -1127,16 +1127,25 @@ void build_loop_graph(mfadd_solver* s, const double* dfield) {
   CK(cudaGraphInstantiate(&s->loop_exec, s->loop_graph, 0));
 }
 
+// The WHILE condition of the epoch loop in the graph being captured on `st`
+// (default 1 at every launch of the graph; the epochs set it).
+cudaGraphConditionalHandle make_loop_handle(cudaStream_t st) {
+  cudaStreamCaptureStatus cs;
+  cudaGraph_t g = nullptr;
+  CK(cudaStreamGetCaptureInfo(st, &cs, nullptr, &g, nullptr, nullptr));
+  cudaGraphConditionalHandle h;
+  CK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+  return h;
+}
+
 // The epoch loop as a conditional WHILE node appended to the graph being
-// captured on `st` (whole-solve graph).
-void add_loop_node(mfadd_solver* s, cudaStream_t st, const double* dfield) {
+// captured on `st` (whole-solve graph), on condition `h`.
+void add_loop_node(mfadd_solver* s, cudaStream_t st, const double* dfield, cudaGraphConditionalHandle h) {
   cudaStreamCaptureStatus cs;
   cudaGraph_t g = nullptr;
   const cudaGraphNode_t* deps = nullptr;
   size_t ndeps = 0;
   CK(cudaStreamGetCaptureInfo(st, &cs, nullptr, &g, &deps, &ndeps));
-  cudaGraphConditionalHandle h;
-  CK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
   cudaGraphNodeParams np = {};
   np.type = cudaGraphNodeTypeConditional;
   np.conditional.handle = h;
@@ -1656,6 +1665,26 @@ int enqueue_solve(mfadd_solver* s, const double* dfield) {
     throw std::runtime_error(s->holder_fault);
   }
   CK(cudaMemsetAsync(s->est.p, 0, sizeof(mfb::EpochState), st));
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  CK(cudaStreamIsCapturing(st, &cs));
+  const bool captured = cs == cudaStreamCaptureStatusActive;
+  // In the whole-solve graph, record_epoch(0) and iteration 1 share one pass
+  // over the shared controls (mode 4): iteration 1 reads exactly the state
+  // epoch 0 measures, and its update leaves the n_s > 2 copies untouched.
+  const bool fuse01 = captured && loop && regions && s->nranks == 1;
+  if (fuse01) {
+    launches += launch_residuals(s, dfield, nullptr, 0, st);  // record_epoch(0) block errors, before the update
+    const cudaGraphConditionalHandle h = make_loop_handle(st);
+    mfb::EpochRegionArgs a = region_args(s, 4);
+    a.cond = static_cast<unsigned long long>(h);
+    s->tl.begin("epoch");
+    launches += mfb::launch_epoch_regions(a, st);
+    s->tl.end();
+    launches += launch_residuals(s, dfield, s->est.p, 0, st);  // record_epoch(1) block errors
+    s->tl.begin("epoch");
+    add_loop_node(s, st, dfield, h);
+    s->tl.end();
+  } else {
   if (regions) {
     s->tl.begin("epoch");
     launches += mfb::launch_epoch_regions(region_args(s, 0), st);
@@ -1664,13 +1693,12 @@ int enqueue_solve(mfadd_solver* s, const double* dfield) {
     launches += run_epoch(s, 0, 0);
   }
   launches += launch_residuals(s, dfield, nullptr, 0, st);  // record_epoch(0, ...) block errors
+  }
   // ---- outer iterations (solver.cpp:394-413), entirely on the device
-  if (loop) {
+  if (loop && !fuse01) {
     s->tl.begin("epoch");
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    CK(cudaStreamIsCapturing(st, &cs));
-    if (cs == cudaStreamCaptureStatusActive)
-      add_loop_node(s, st, dfield);
+    if (captured)
+      add_loop_node(s, st, dfield, make_loop_handle(st));
     else {
       if (!s->loop_exec || (s->cfg.log_errors && s->loop_field != dfield)) build_loop_graph(s, dfield);
       CK(cudaGraphLaunch(s->loop_exec, st));

@@ -985,7 +985,10 @@ template <int NS, bool FLAT>
 __device__ __forceinline__ void region_tile_local(const EpochRegionArgs& a, const RegionDev& R, const TileDev& t,
                                                   int mode, double (*s_w)[kRegionWarps]) {
   constexpr int PT = NS == 2 ? 4 : (NS == 4 ? 2 : 1);
-  const bool update = mode == 2 || (mode == 1 && NS == 2);
+  // mode 4 = epoch 0 fused with iteration 1: as mode 1, plus the pre-average
+  // SS jump of the n_s == 2 controls (epoch 0's measurement)
+  const bool update = mode == 2 || ((mode == 1 || mode == 4) && NS == 2);
+  const bool pre = mode == 4 && NS == 2;
   int base[NS], s0[NS], s1[NS];
 #pragma unroll
   for (int h = 0; h < NS; ++h) {
@@ -996,9 +999,9 @@ __device__ __forceinline__ void region_tile_local(const EpochRegionArgs& a, cons
   const int e1 = R.ext[1], e2 = R.ext[2];
   const float rc1 = 1.0f / static_cast<float>(e1), rc2 = 1.0f / static_cast<float>(e2);
   double* __restrict__ P = a.P;
-  unsigned long long red[NS + 1];
+  unsigned long long red[NS + 2];  // [NS + 1]: mode 4's pre-average jump
 #pragma unroll
-  for (int j = 0; j <= NS; ++j) red[j] = 0ull;
+  for (int j = 0; j <= NS + 1; ++j) red[j] = 0ull;
   const int end = t.start + t.count;
   for (int i0 = t.start + threadIdx.x; i0 < end; i0 += kRegionThreads * PT) {
     int off[PT][NS];
@@ -1022,6 +1025,15 @@ __device__ __forceinline__ void region_tile_local(const EpochRegionArgs& a, cons
     for (int u = 0; u < PT; ++u) {
       if (i0 + u * kRegionThreads < end) {
         if (update) {
+          if (pre) {
+            double mn = v[u][0], mx = v[u][0];
+#pragma unroll
+            for (int h = 1; h < NS; ++h) {
+              mn = fmin(mn, v[u][h]);
+              mx = fmax(mx, v[u][h]);
+            }
+            red[NS + 1] = umax(red[NS + 1], dbits(mx - mn));
+          }
           double sum = 0.0;  // solver.cpp:147-159: ascending holder id, divide once
 #pragma unroll
           for (int h = 0; h < NS; ++h) sum = __dadd_rn(sum, v[u][h]);
@@ -1045,7 +1057,7 @@ __device__ __forceinline__ void region_tile_local(const EpochRegionArgs& a, cons
       }
     }
   }
-  const unsigned long long b = cta_umax_multi<NS + 1>(red, s_w);
+  const unsigned long long b = cta_umax_multi<NS + 2>(red, s_w);
   const int j = threadIdx.x;
   if (b && j < NS) {
     atomicMax((update ? a.change : a.linf_sh) + R.ids[j], b);
@@ -1056,6 +1068,8 @@ __device__ __forceinline__ void region_tile_local(const EpochRegionArgs& a, cons
     } else {
       atomicMax(NS == 2 ? &a.st->jump_ss : &a.st->jump_ms, b);
     }
+  } else if (b && j == NS + 1) {
+    atomicMax(&a.st->jump0_ss, b);
   }
   __syncthreads();  // s_w and the tile descriptor are reused by the next tile
 }
@@ -1067,7 +1081,7 @@ template <int NS>
 __device__ __forceinline__ void region_tile(const EpochRegionArgs& a, const RegionDev& R, const TileDev& t, int mode,
                                             double (*s_w)[kRegionWarps]) {
   constexpr int PT = NS == 2 ? 4 : (NS == 4 ? 2 : 1);  // controls per thread per pass: 8 loads in flight
-  const bool update = mode == 2 || (mode == 1 && NS == 2);
+  const bool update = mode == 2 || (mode == 1 && NS == 2);  // (mode 4 runs on local tiles only)
   RegionRegs hr[NS <= 4 ? NS : 1];
 #pragma unroll
   for (int h = 0; h < (NS <= 4 ? NS : 1); ++h) hr[h] = RegionRegs{R.base[h], R.str[h][0], R.str[h][1], R.str[h][2]};
@@ -1168,12 +1182,19 @@ __device__ void epoch_finalize(const EpochRegionArgs& a, int mode, int slot, uns
   if (threadIdx.x == 0) {
     const double dpv = mode == 0 ? 0.0 : __longlong_as_double(static_cast<long long>(dp));  // record_epoch(0, 0.0)
     const unsigned long long js = atomicExch(&a.st->jump_ss, 0ull), jm = atomicExch(&a.st->jump_ms, 0ull);
+    if (mode == 4) {  // epoch 0: jumps of the fit (the n_s > 2 ones are untouched by iteration 1)
+      const unsigned long long j0 = atomicExch(&a.st->jump0_ss, 0ull);
+      double* o0 = a.epoch_out;
+      o0[0] = 0.0;
+      o0[1] = __longlong_as_double(static_cast<long long>(j0));
+      o0[2] = __longlong_as_double(static_cast<long long>(jm));
+    }
     double* out = a.epoch_out + 3 * slot;
     out[0] = dpv;
     out[1] = __longlong_as_double(static_cast<long long>(js));
     out[2] = __longlong_as_double(static_cast<long long>(jm));
     a.st->done = 0;
-    if (a.mode < 0) {  // loop bookkeeping (solver.cpp:406-412)
+    if (a.mode < 0 || a.mode == 4) {  // loop bookkeeping (solver.cpp:406-412)
       const bool conv = dpv < a.tol;
       a.st->last_iter = slot;
       a.st->converged = conv ? 1 : 0;
@@ -1194,7 +1215,7 @@ __global__ void __launch_bounds__(kRegionThreads, MAXNS == 8 ? 2 : 3) k_epoch_re
   __shared__ TileDev s_T;
   constexpr int kWords = static_cast<int>(sizeof(TileDev) / 4);
   static_assert(kWords <= kRegionThreads, "one descriptor word per thread");
-  const int iter = a.mode < 0 ? a.st->iter + 1 : 0;
+  const int iter = a.mode < 0 ? a.st->iter + 1 : (a.mode == 4 ? 1 : 0);
   const int mode = a.mode < 0 ? (iter >= 2 ? 2 : 1) : a.mode;  // solver.cpp:397
   // persistent CTAs: the next tile's descriptor is fetched while this one runs
   const int tid = threadIdx.x;

@@ -126,7 +126,7 @@ struct EpochRegionArgs {
   int ntiles;
   int nblocks;
   double* P;
-  int mode;  // 0 measure, 3 final pair jumps, -1 loop (1 on iteration 1, 2 after)
+  int mode;  // 0 measure, 3 final pair jumps, -1 loop (1 on iteration 1, 2 after), 4 epoch 0 + iteration 1
   unsigned long long* change;
   unsigned long long* linf_sh;
   const unsigned long long* linf_int;
