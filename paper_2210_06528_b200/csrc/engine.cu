@@ -1681,6 +1681,18 @@ int enqueue_solve(mfadd_solver* s, const double* dfield) {
     launches += mfb::launch_epoch_regions(a, st);
     s->tl.end();
     launches += launch_residuals(s, dfield, s->est.p, 0, st);  // record_epoch(1) block errors
+    // the next iterations as plain (predicated) kernel nodes: a conditional
+    // node costs more than a kernel that exits at once
+    static const int unroll = env_int("MFADD_UNROLL_EPOCHS", 3);
+    for (int u = 0; u < unroll; ++u) {
+      mfb::EpochRegionArgs b = region_args(s, -1);
+      b.cond = static_cast<unsigned long long>(h);
+      b.predicated = 1;
+      s->tl.begin("epoch");
+      launches += mfb::launch_epoch_regions(b, st);
+      s->tl.end();
+      if (s->cfg.log_errors) launches += mfb::launch_block_residual(s->wl.p, res_args(s, dfield, s->est.p, 0), st);
+    }
     s->tl.begin("epoch");
     add_loop_node(s, st, dfield, h);
     s->tl.end();

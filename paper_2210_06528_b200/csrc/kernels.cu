@@ -1217,6 +1217,10 @@ __global__ void __launch_bounds__(kRegionThreads, MAXNS == 8 ? 2 : 3) k_epoch_re
   static_assert(kWords <= kRegionThreads, "one descriptor word per thread");
   const int iter = a.mode < 0 ? a.st->iter + 1 : (a.mode == 4 ? 1 : 0);
   const int mode = a.mode < 0 ? (iter >= 2 ? 2 : 1) : a.mode;  // solver.cpp:397
+  // an unrolled loop iteration ahead of the WHILE node: nothing to do once the
+  // previous epoch converged or the iteration budget is spent (its finalize
+  // then already cleared the WHILE condition)
+  if (a.predicated && (a.st->converged || iter > a.max_iter)) return;
   // persistent CTAs: the next tile's descriptor is fetched while this one runs
   const int tid = threadIdx.x;
   int w = 0;

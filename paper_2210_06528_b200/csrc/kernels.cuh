@@ -136,6 +136,7 @@ struct EpochRegionArgs {
   int max_iter;
   double tol;
   unsigned long long cond;  // cudaGraphConditionalHandle (loop mode only)
+  int predicated;           // loop mode outside the WHILE node: no-op once converged or past max_iter
   int max_ns;               // largest region n_s (selects the kernel form)
   const double* recv;       // sharded: remote holders' copies (RegionDev::rmask)
   int finalize;             // 1: the last CTA computes dp and writes epoch_out (else k_epoch_finalize)
