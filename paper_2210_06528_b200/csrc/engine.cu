@@ -957,6 +957,7 @@ mfb::BlockResArgs res_args(mfadd_solver* s, const double* dfield, const mfb::Epo
   a.slot = slot;
   a.nglobal = s->dec.nblocks;
   a.boff = s->srange.blo;
+  a.expect_iter = -1;
   return a;
 }
 
@@ -1691,7 +1692,11 @@ int enqueue_solve(mfadd_solver* s, const double* dfield) {
       s->tl.begin("epoch");
       launches += mfb::launch_epoch_regions(b, st);
       s->tl.end();
-      if (s->cfg.log_errors) launches += mfb::launch_block_residual(s->wl.p, res_args(s, dfield, s->est.p, 0), st);
+      if (s->cfg.log_errors) {
+        mfb::BlockResArgs ra = res_args(s, dfield, s->est.p, 0);
+        ra.expect_iter = 2 + u;  // skipped with its epoch
+        launches += mfb::launch_block_residual(s->wl.p, ra, st);
+      }
     }
     s->tl.begin("epoch");
     add_loop_node(s, st, dfield, h);

@@ -1321,6 +1321,7 @@ constexpr int kResThreads = 128;
 template <int P>
 __global__ void __launch_bounds__(kResThreads) k_block_residual(BlockResArgs a) {
   __shared__ double s_red[2][kResThreads / 32];
+  if (a.expect_iter >= 0 && a.st->iter != a.expect_iter) return;  // its epoch did not run
   const int b = blockIdx.y;
   const BlockDev& blk = a.blocks[b];
   const int D = a.D;
@@ -1422,6 +1423,7 @@ __global__ void __launch_bounds__(kResThreads) k_block_residual(BlockResArgs a) 
 __global__ void k_block_residual_reduce(BlockResArgs a) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= a.nblocks) return;
+  if (a.expect_iter >= 0 && a.st->iter != a.expect_iter) return;
   const int slot = a.st ? a.st->iter : a.slot;
   double sl = 0.0, sm = 0.0;
   for (int t = 0; t < a.ntile; ++t) {

@@ -165,6 +165,7 @@ struct BlockResArgs {
   double* errs;                // [(max_iter + 1)][nglobal] x {l2, linf}
   const EpochState* st;        // slot = st->iter (the epoch just recorded), or `slot` when null
   int slot;
+  int expect_iter;             // >= 0: no-op unless st->iter == expect_iter (after a predicated epoch)
   int nglobal, boff;           // all blocks; global id of local block 0
 };
 int launch_block_residual(int degree, const BlockResArgs& a, cudaStream_t s);
