@@ -225,7 +225,8 @@ struct Workload {
   DBuf<AxisProb> d_probs;
   DBuf<BlockDev> d_blocks;
   DBuf<int> d_factor, g0, first_col, count;
-  DBuf<double> vals, ltab, t1, t2, P, Y;
+  DBuf<double> vals, ltab, t1, t2, P, Y, rlt;
+  std::int64_t rlt_stride = 0;
   DBuf<unsigned long long> linf_int;
   DBuf<unsigned char> sflag;
   std::int64_t sflag_off[3] = {0, 0, 0};
@@ -434,6 +435,8 @@ struct Workload {
     count.alloc(static_cast<std::size_t>(total_rows));
     vals.alloc(static_cast<std::size_t>(total_rows * (p + 1)));
     ltab.alloc(static_cast<std::size_t>(std::max<std::int64_t>(total_cols, 1) * (2 * p + 1)));
+    rlt_stride = (mfb::rl_table_doubles(p, max_n_factor) + 1) / 2 * 2;  // even: 16-B aligned per problem
+    rlt.alloc(static_cast<std::size_t>(probs.size() * rlt_stride));
     t1.alloc(static_cast<std::size_t>(total_t1));
     t2.alloc(static_cast<std::size_t>(total_t2));
     P.alloc(static_cast<std::size_t>(total_p));
@@ -496,12 +499,14 @@ struct Workload {
         CK(cudaEventRecord(ev_rows2, side));
       }
       l += mfb::launch_gram_chol(p, ca, side);
+      if (D == 2 && tma_last) l += mfb::launch_rl_tables(p, ca, rlt.p, rlt_stride, side);
       tl->end();
       tl->st = main_st;
       CK(cudaEventRecord(ev_chol, side));
     } else {
       tl->begin("gram_chol");
       l += mfb::launch_gram_chol(p, ca, ctx->stream);
+      if (D == 2 && tma_last) l += mfb::launch_rl_tables(p, ca, rlt.p, rlt_stride, ctx->stream);
       tl->end();
     }
     CK(cudaGetLastError());
@@ -586,6 +591,10 @@ struct Workload {
     }
     if (rows_split && D == 2) CK(cudaStreamWaitEvent(ctx->stream, ev_rows2, 0));  // last-axis + decode rows
     if (D == 2 && defer_mode == 2 && tma_last) fa.join_event = ev_chol;
+    if (D == 2 && tma_last) {
+      fa.rlt = rlt.p;
+      fa.rlt_stride = rlt_stride;
+    }
     tl->begin("fit_last");
     if (tma_last) {
       const double* src = D == 2 ? t1.p : t2.p;

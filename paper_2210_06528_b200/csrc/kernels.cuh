@@ -47,6 +47,10 @@ struct CholArgs {
   DevStatus* status;
 };
 int launch_gram_chol(int degree, const CholArgs& a, cudaStream_t s);
+// The solve kernels' right-looking step tables of every factored problem,
+// once per solve after the factorizations: rlt + problem id * stride.
+int launch_rl_tables(int degree, const CholArgs& a, double* rlt, std::int64_t stride, cudaStream_t s);
+std::int64_t rl_table_doubles(int degree, int n);  // forward + backward table of an extent-n problem
 
 // K3: per-axis fit passes (lsq.cpp:57-61 fused: R^T contraction in row order
 // + forward substitution + back substitution).
@@ -76,6 +80,8 @@ struct FitArgs {
   int defer_back;                    // 1: axis 0 forward-only, 2: contraction only; the rest on P at the end
   int min_n0;                        // smallest axis-0 held extent (partitioned final solve eligibility)
   int fuse2d;                        // D = 2: k_solve2d (CTA per block) replaces k_last_solve + the axis-0 solve
+  const double* rlt;                 // right-looking step tables per axis problem (k_rl_tables), or null
+  std::int64_t rlt_stride;           // doubles per axis problem in rlt (forward then backward table)
   int max_n0, max_n1, max_zl;        // largest held extents / Z pitch (k_solve2d shared-memory size)
   void* join_event;                  // cudaEvent_t the last-axis solve waits for (factorizations on a side stream)
 };
@@ -83,6 +89,7 @@ int launch_fit_strided(int degree, const FitArgs& a, int axis, cudaStream_t s); 
 int launch_fit_last(int degree, const FitArgs& a, cudaStream_t s);
 // Shared-memory bytes of k_solve2d for held extents n0 x n1 (0 if it does not fit one CTA).
 size_t solve2d_smem(int degree, int n0, int n1, int zl, int kseg);
+
 // D = 1: CTA per block, column-parallel R^T q + serial banded solve (smem: max_n x (2P+2) doubles).
 int launch_fit_1d(int degree, const FitArgs& a, int max_n, cudaStream_t s);
 

@@ -1074,8 +1074,9 @@ struct RLFinal {  // last pass of a tile: results also go to HBM (+ L-inf)
 };
 
 template <int P, bool TAIL, bool FINAL>
-__device__ __forceinline__ void rl_batch(double* x0, const int ds, const int n, const int t0, const double* tab,
-                                         double (&acc)[P], double (&zin)[RL<P>::U], RLFinal& fin) {
+__device__ __forceinline__ void rl_batch(double* __restrict__ x0, const int ds, const int n, const int t0,
+                                         const double* __restrict__ tab, double (&acc)[P], double (&zin)[RL<P>::U],
+                                         RLFinal& fin) {
   constexpr int U = RL<P>::U, W = RL<P>::W;
   double znx[U];
 #pragma unroll
@@ -1114,7 +1115,8 @@ __device__ __forceinline__ void rl_batch(double* x0, const int ds, const int n, 
 }
 
 template <int P, bool FINAL>
-__device__ __forceinline__ void rl_pass(double* x0, const int ds, const int n, const double* tab, RLFinal& fin) {
+__device__ __forceinline__ void rl_pass(double* __restrict__ x0, const int ds, const int n,
+                                        const double* __restrict__ tab, RLFinal& fin) {
   constexpr int U = RL<P>::U, W = RL<P>::W;
   double acc[P], zin[U];
 #pragma unroll
@@ -1162,6 +1164,37 @@ __device__ __forceinline__ void build_rl_tables(const double* lt, int n, double*
   }
 }
 
+// The right-looking step tables of every factored axis problem, once per
+// solve after the factorizations (the solve kernels bulk-copy them instead of
+// deriving them from the Cholesky table in every CTA).
+template <int P>
+__global__ void __launch_bounds__(256) k_rl_tables(const CholArgs a, double* rlt, std::int64_t stride) {
+  constexpr int W = RL<P>::W;
+  const int pid = a.prob_ids[blockIdx.x];
+  const AxisProb pr = a.probs[pid];
+  double* f = rlt + static_cast<std::int64_t>(pid) * stride;
+  build_rl_tables<P>(a.ltab + pr.col_off * (2 * P + 1), pr.n, f, f + rl_rows(pr.n, P) * W, threadIdx.x, blockDim.x);
+}
+
+// A problem's tables into shared memory: bulk copies (rlt) on `bar`, or
+// built from the Cholesky table by the CTA.  Returns the bytes the copies add.
+template <int P>
+__device__ __forceinline__ unsigned stage_rl_tables(const FitArgs& a, const AxisProb& pr, int pid, double* f, double* b,
+                                                    std::uint64_t* bar, int tid, int nthr) {
+  constexpr int W = RL<P>::W;
+  const unsigned bytes = static_cast<unsigned>(rl_rows(pr.n, P) * W) * 8;
+  if (a.rlt) {
+    if (tid == 0) {
+      const double* src = a.rlt + static_cast<std::int64_t>(pid) * a.rlt_stride;
+      bulk_load_1d(f, src, bytes, bar);
+      bulk_load_1d(b, src + rl_rows(pr.n, P) * W, bytes, bar);
+    }
+    return 2 * bytes;
+  }
+  build_rl_tables<P>(a.ltab + pr.col_off * (2 * P + 1), pr.n, f, b, tid, nthr);
+  return 0;
+}
+
 template <int P>
 __global__ void __launch_bounds__(kSolve2dThreads) k_solve2d(const FitArgs a) {
   extern __shared__ __align__(128) double s2d[];
@@ -1189,6 +1222,7 @@ __global__ void __launch_bounds__(kSolve2dThreads) k_solve2d(const FitArgs a) {
     mbar_init(bar, 1);
     fence_mbar_init();
     unsigned bytes = static_cast<unsigned>(n1) * zl * 8 + static_cast<unsigned>(K - 1) * PADC * zl * 8;
+    if (a.rlt) bytes += 2 * static_cast<unsigned>((rl_rows(n0, P) + rl_rows(n1, P)) * W) * 8;
     mbar_arrive_expect_tx(bar, bytes);
     int cs = 0;
     for (int sg = 0; sg < K; ++sg) {  // segment sg owns columns [cs_sg, cs_sg+1) in parity sg & 1
@@ -1201,8 +1235,8 @@ __global__ void __launch_bounds__(kSolve2dThreads) k_solve2d(const FitArgs a) {
       cs = ce;
     }
   }
-  build_rl_tables<P>(a.ltab + p0.col_off * (2 * P + 1), n0, f0, b0, tid, nthr);
-  build_rl_tables<P>(a.ltab + p1.col_off * (2 * P + 1), n1, f1, b1, tid, nthr);
+  stage_rl_tables<P>(a, p0, blk.ax[0], f0, b0, bar, tid, nthr);
+  stage_rl_tables<P>(a, p1, blk.ax[1], f1, b1, bar, tid, nthr);
   for (int c = tid; c < n1; c += nthr) sf1[c] = a.shared_flag[a.sflag_off[1] + p1.col_lo + c];
   for (int i = tid; i < n0; i += nthr) sf0[i] = a.shared_flag[a.sflag_off[0] + p0.col_lo + i];
   __syncthreads();  // barrier init visible before any wait
@@ -1647,6 +1681,39 @@ int debug_fail_line_tma() {
   cudaMemcpyFromSymbol(&line, g_tma_debug_line, sizeof(int));
 #endif
   return line;
+}
+
+namespace {
+template <int P>
+struct RlTablesLaunch {
+  static int run(const CholArgs& a, double* rlt, std::int64_t stride, cudaStream_t s) {
+    if (a.nfactor == 0) return 0;
+    k_rl_tables<P><<<a.nfactor, 256, 0, s>>>(a, rlt, stride);
+    return 1;
+  }
+};
+template <int P>
+struct RlDoubles {
+  static std::int64_t run(int n) { return 2 * static_cast<std::int64_t>(rl_rows(n, P)) * RL<P>::W; }
+};
+}  // namespace
+
+int launch_rl_tables(int degree, const CholArgs& a, double* rlt, std::int64_t stride, cudaStream_t s) {
+  return dispatch_p<RlTablesLaunch>(degree, a, rlt, stride, s);
+}
+std::int64_t rl_table_doubles(int degree, int n) {
+  switch (degree) {
+    case 1: return RlDoubles<1>::run(n);
+    case 2: return RlDoubles<2>::run(n);
+    case 3: return RlDoubles<3>::run(n);
+    case 4: return RlDoubles<4>::run(n);
+    case 5: return RlDoubles<5>::run(n);
+    case 6: return RlDoubles<6>::run(n);
+    case 7: return RlDoubles<7>::run(n);
+    case 8: return RlDoubles<8>::run(n);
+    case 9: return RlDoubles<9>::run(n);
+    default: return 0;
+  }
 }
 
 size_t solve2d_smem(int degree, int n0, int n1, int zl, int kseg) {
