@@ -1066,9 +1066,7 @@ __host__ __device__ inline int rl_rows(int n, int P) {  // table rows incl. the 
 struct RLFinal {  // last pass of a tile: results also go to HBM (+ L-inf)
   double* dst;            // global base of this line's outputs
   std::int64_t dstride;   // global stride per step (signed)
-  const unsigned char* sfl;  // per-step shared flag (indexed by column)
-  int sf_dir;             // column of step t = sf_base + sf_dir * t
-  int sf_base;
+  int t_lo, t_hi;         // steps [t_lo, t_hi) hold non-shared entries (shared ones sit at both ends of a line)
   bool line_shared;
   unsigned long long lmax;
 };
@@ -1103,7 +1101,7 @@ __device__ __forceinline__ void rl_batch(double* __restrict__ x0, const int ds, 
       x0[t * ds] = y;
       if (FINAL) {
         fin.dst[t * fin.dstride] = y;
-        if (!fin.line_shared && !fin.sfl[fin.sf_base + fin.sf_dir * t]) {
+        if (!fin.line_shared && t >= fin.t_lo && t < fin.t_hi) {  // no shared-memory flag on the chain
           const unsigned long long bits = dbits_s(fabs(y));
           fin.lmax = fin.lmax > bits ? fin.lmax : bits;
         }
@@ -1238,7 +1236,20 @@ __global__ void __launch_bounds__(kSolve2dThreads) k_solve2d(const FitArgs a) {
   stage_rl_tables<P>(a, p0, blk.ax[0], f0, b0, bar, tid, nthr);
   stage_rl_tables<P>(a, p1, blk.ax[1], f1, b1, bar, tid, nthr);
   for (int c = tid; c < n1; c += nthr) sf1[c] = a.shared_flag[a.sflag_off[1] + p1.col_lo + c];
-  for (int i = tid; i < n0; i += nthr) sf0[i] = a.shared_flag[a.sflag_off[0] + p0.col_lo + i];
+  __shared__ int s_ns[2];  // non-shared axis-0 indices: [s_ns[0], s_ns[1])
+  if (tid == 0) {
+    s_ns[0] = n0;
+    s_ns[1] = 0;
+  }
+  __syncthreads();
+  for (int i = tid; i < n0; i += nthr) {
+    const unsigned char f = a.shared_flag[a.sflag_off[0] + p0.col_lo + i];
+    sf0[i] = f;
+    if (!f) {
+      atomicMin(&s_ns[0], i);
+      atomicMax(&s_ns[1], i + 1);
+    }
+  }
   __syncthreads();  // barrier init visible before any wait
   mbar_wait(bar, 0);
   // carries: X[cs_s + k] += C[s-1][k] for boundaries s = 1..K-1
@@ -1265,9 +1276,8 @@ __global__ void __launch_bounds__(kSolve2dThreads) k_solve2d(const FitArgs a) {
     rl_pass<P, false>(xc, 1, n0, f0 + P * W, fin);
     fin.dst = Pb + static_cast<std::int64_t>(n0 - 1) * n1 + c;
     fin.dstride = -n1;
-    fin.sfl = sf0;
-    fin.sf_base = n0 - 1;
-    fin.sf_dir = -1;
+    fin.t_lo = n0 - s_ns[1];  // step t is axis-0 index n0 - 1 - t
+    fin.t_hi = n0 - s_ns[0];
     fin.line_shared = sf1[c] != 0;
     rl_pass<P, true>(xc + (n0 - 1), -1, n0, b0 + P * W, fin);
   }
