@@ -362,7 +362,10 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
 // chunk k ^ (t & 7): the per-thread LDS.128 of two columns is conflict-free),
 // plus the chunk's basis rows by 1-D bulk copies, in an S-stage TMA ring.
 constexpr int kLastCW = 16;
-constexpr int kLastS = 2;
+#ifndef MFB_LAST_S
+#define MFB_LAST_S 2
+#endif
+constexpr int kLastS = MFB_LAST_S;  // TMA ring stages of the last-axis contraction
 
 __host__ __device__ inline int last_stage_bytes(int LT, int P) {
   return ((LT * 128 + kLastCW * (P + 1) * 8 + kLastCW * 4) + 1023) / 1024 * 1024;
