@@ -297,7 +297,7 @@ struct Workload {
     for (const auto& b : blocks) mxnl = std::max(mxnl, probs[static_cast<std::size_t>(b.ax[D - 1])].n);
     const int needl = (mxnl + 2 * (p + 1)) * (2 * p + 1);
     if (needl <= 6144 && max_lines_last > 0 && !std::getenv("MFADD_NO_TMA_LAST")) {
-      const int ncta = (max_lines_last + 255) / 256;
+      const int ncta = std::max((max_lines_last + 255) / 256, env_int("MFADD_LAST_LSPLIT", 1));  // CTAs per block-segment
       last_LT = round_up((max_lines_last + ncta - 1) / ncta, 32);  // whole warps
       last_ltcap = needl;
       tma_last = true;
