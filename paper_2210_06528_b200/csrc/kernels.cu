@@ -114,16 +114,28 @@ __global__ void __launch_bounds__(256) k_basis_rows(RowsArgs a) {
     int s = nb - 1;
     while (s > P && kn[s] == kn[s + 1]) --s;
     span = s;
-  } else {  // knots.cpp:96-105: binary search, half-open spans
-    int low = P, high = nb, mid = (low + high) / 2;
-    while (u < kn[mid] || u >= kn[mid + 1]) {
-      if (u < kn[mid])
-        high = mid;
-      else
-        low = mid;
-      mid = (low + high) / 2;
+  } else {  // knots.cpp:96-105: the unique s in [P, nb) with kn[s] <= u < kn[s+1]
+    // a guess from uniform spacing plus a short walk (the decomposition's
+    // knots are uniform: two loads instead of the ~11 of the binary search);
+    // the binary search of the reference when the walk does not settle
+    int g = P + static_cast<int>((u - lo) / (hi - lo) * static_cast<double>(nb - P));
+    g = g < P ? P : (g > nb - 1 ? nb - 1 : g);
+    int steps = 0;
+    while (steps < 4 && u < kn[g]) --g, ++steps;
+    while (steps < 4 && u >= kn[g + 1]) ++g, ++steps;
+    if (kn[g] <= u && u < kn[g + 1]) {
+      span = g;
+    } else {
+      int low = P, high = nb, mid = (low + high) / 2;
+      while (u < kn[mid] || u >= kn[mid + 1]) {
+        if (u < kn[mid])
+          high = mid;
+        else
+          low = mid;
+        mid = (low + high) / 2;
+      }
+      span = mid;
     }
-    span = mid;
   }
   // knots.cpp:108-129 Cox-de Boor, explicit RN ops (no contraction)
   double N[P + 1], left[P + 1], right[P + 1];
@@ -1912,15 +1924,15 @@ int launch_epoch_finalize(const EpochRegionArgs& a, cudaStream_t s) {
 
 int launch_epoch_regions(const EpochRegionArgs& a, cudaStream_t s) {
   if (a.ntiles <= 0) return 0;
-  if (a.mode == 3)
-    k_pair_jumps_regions<<<a.ntiles, kRegionThreads, 0, s>>>(a);
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  if (a.mode == 3)  // persistent over the tiles: one wave (usually it exits at once)
+    k_pair_jumps_regions<<<a.ntiles < 2 * sms ? a.ntiles : 2 * sms, kRegionThreads, 0, s>>>(a);
   else {
-    static int sms = 0;
-    if (!sms) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
     const int per_sm = a.max_ns > 4 ? 2 : 3;  // __launch_bounds__ residency
     const int grid = a.ntiles < sms * per_sm ? a.ntiles : sms * per_sm;
     if (a.max_ns > 4)
