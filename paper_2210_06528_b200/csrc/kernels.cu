@@ -181,7 +181,16 @@ __global__ void __launch_bounds__(256) k_gram_chol(CholArgs a) {
   const double* v = a.vals + pr.row_off * (P + 1);
   double* band = a.ltab + pr.col_off * (2 * P + 1);  // light mode: the Gram band between the two launches
   if (a.light == 2) {  // Cholesky-only launch: the band written by the Gram-only launch
-    for (int e = threadIdx.x; e < n * (P + 1); e += blockDim.x) sm[e] = band[e];
+    constexpr int B = 8;  // independent loads in flight per thread (one warp)
+    const int nv = n * (P + 1), nt = static_cast<int>(blockDim.x);
+    for (int e0 = threadIdx.x; e0 < nv; e0 += B * nt) {
+      double t[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) t[u] = e0 + u * nt < nv ? band[e0 + u * nt] : 0.0;
+#pragma unroll
+      for (int u = 0; u < B; ++u)
+        if (e0 + u * nt < nv) sm[e0 + u * nt] = t[u];
+    }
     __syncthreads();
   } else {
   if (a.stage_rows) {  // row table -> smem (coalesced), then the Gram reads are smem hits
