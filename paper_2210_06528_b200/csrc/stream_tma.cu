@@ -1074,10 +1074,22 @@ struct RLFinal {  // last pass of a tile: results also go to HBM (+ L-inf)
   unsigned long long lmax;
 };
 
+template <int P>
+__device__ __forceinline__ void rl_load_step(const double* row, double (&cf)[RL<P>::W]) {
+#pragma unroll
+  for (int h = 0; h < RL<P>::W / 2; ++h) {
+    const double2 v = reinterpret_cast<const double2*>(row)[h];
+    cf[2 * h] = v.x;
+    cf[2 * h + 1] = v.y;
+  }
+}
+
+// cf holds step t0's table row on entry and step t0 + U's on exit: each
+// step's coefficients are loaded one step ahead, off the dependent chain.
 template <int P, bool TAIL, bool FINAL>
 __device__ __forceinline__ void rl_batch(double* __restrict__ x0, const int ds, const int n, const int t0,
                                          const double* __restrict__ tab, double (&acc)[P], double (&zin)[RL<P>::U],
-                                         RLFinal& fin) {
+                                         double (&cf)[RL<P>::W], RLFinal& fin) {
   constexpr int U = RL<P>::U, W = RL<P>::W;
   double znx[U];
 #pragma unroll
@@ -1088,13 +1100,8 @@ __device__ __forceinline__ void rl_batch(double* __restrict__ x0, const int ds, 
   const double* tb = tab + t0 * W;
 #pragma unroll
   for (int u = 0; u < U; ++u) {
-    double cf[W];
-#pragma unroll
-    for (int h = 0; h < W / 2; ++h) {
-      const double2 v = reinterpret_cast<const double2*>(tb + u * W)[h];
-      cf[2 * h] = v.x;
-      cf[2 * h + 1] = v.y;
-    }
+    double cfn[W];
+    rl_load_step<P>(tb + (u + 1) * W, cfn);  // the next step's row (tables are padded past the line)
     const double y = acc[u % P];
 #pragma unroll
     for (int k = 1; k < P; ++k) acc[(u + k) % P] = fma(-cf[k - 1], y, acc[(u + k) % P]);
@@ -1110,6 +1117,8 @@ __device__ __forceinline__ void rl_batch(double* __restrict__ x0, const int ds, 
         }
       }
     }
+#pragma unroll
+    for (int k = 0; k < W; ++k) cf[k] = cfn[k];
   }
 #pragma unroll
   for (int u = 0; u < U; ++u) zin[u] = znx[u];
@@ -1124,9 +1133,11 @@ __device__ __forceinline__ void rl_pass(double* __restrict__ x0, const int ds, c
   for (int k = 0; k < P; ++k) acc[k] = (k < n ? x0[k * ds] : 0.0) * tab[(k - P) * W + P];
 #pragma unroll
   for (int u = 0; u < U; ++u) zin[u] = P + u < n ? x0[(P + u) * ds] : 0.0;
+  double cf[W];
+  rl_load_step<P>(tab, cf);
   int t0 = 0;
-  for (; t0 + 2 * U + P <= n; t0 += U) rl_batch<P, false, FINAL>(x0, ds, n, t0, tab, acc, zin, fin);
-  for (; t0 < n; t0 += U) rl_batch<P, true, FINAL>(x0, ds, n, t0, tab, acc, zin, fin);
+  for (; t0 + 2 * U + P <= n; t0 += U) rl_batch<P, false, FINAL>(x0, ds, n, t0, tab, acc, zin, cf, fin);
+  for (; t0 < n; t0 += U) rl_batch<P, true, FINAL>(x0, ds, n, t0, tab, acc, zin, cf, fin);
 }
 
 __host__ __device__ inline size_t solve2d_smem_bytes(int n0, int n1, int zl, int P, int kseg) {
