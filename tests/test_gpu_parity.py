@@ -90,6 +90,26 @@ def test_collocation_rows_bit_exact(ctx, p):
         assert np.array_equal(g.values, ovals)  # bit-exact (explicit RN Cox-de Boor)
 
 
+@pytest.mark.parametrize("p", [2, 3, 5])
+def test_collocation_nonuniform_knots_bit_exact(ctx, p):
+    """Spans on strongly non-uniform knots with repeated interior knots: the
+    device's uniform-spacing guess must hand over to the binary search and
+    land on the reference's span (knots.cpp:83-106) every time."""
+    rng = np.random.default_rng(7 + p)
+    for trial in range(4):
+        inner = np.sort(rng.uniform(0.0, 1.0, 30) ** (1 + 3 * trial))  # clustered toward 0
+        inner = np.concatenate([inner, inner[5:8]])                     # repeated knots
+        inner.sort()
+        kn = np.concatenate([[0.0] * (p + 1), inner, [1.0] * (p + 1)])
+        kv = m.KnotVector(p, kn)
+        params = np.sort(np.concatenate([rng.uniform(0.0, 1.0, 400), inner, [0.0, 1.0]]))
+        g = m.collocation_matrix(kv, params, ctx=ctx)
+        ofc, ocnt, ovals = orc.collocation(kn, p, params)
+        assert np.array_equal(g.first_col, ofc)
+        assert np.array_equal(g.count, ocnt)
+        assert np.array_equal(g.values, ovals)
+
+
 def test_collocation_known_answers(ctx):
     # test_collocation.cpp:13-21
     kv = m.make_knot_vector(2, 3, 0.0, 1.0)
