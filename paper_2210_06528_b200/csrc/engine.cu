@@ -1407,6 +1407,8 @@ std::unique_ptr<mfadd_solver> create_solver(mfadd_context* ctx, const mfadd_deco
       s->dgeo.B1 = D == 2 ? 1 : std::max(1, 256 / s->dgeo.B2);
       s->dgeo.R = 8;
       s->dgeo.S = env_int("MFADD_DEC_S", 3);
+      // D = 3: shared axis-2 window of each control plane (k_decode_tma), up to B2 + p + 2 columns
+      s->dgeo.lt_cap = (D == 3 && !std::getenv("MFADD_NO_DEC_WINDOW")) ? s->dgeo.B2 + p + 2 : 0;
       s->dnt2 = (inner + s->dgeo.B2 - 1) / s->dgeo.B2;
       s->dnt1 = D == 2 ? 1 : (M1 + s->dgeo.B1 - 1) / s->dgeo.B1;
       int sms = 148;

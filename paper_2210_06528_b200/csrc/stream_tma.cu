@@ -1465,7 +1465,34 @@ __global__ void __launch_bounds__(256, MB) k_decode_tma(const DecodeSweepArgs a,
     }
     return s;
   };
-  if (active) fetch_plane(abase + P + 1);
+  // D = 3 with one row j1 per CTA (B1 == 1, C3/C4): every thread shares g1
+  // and w1, so each control plane's axis-1 contraction is done once per CTA
+  // for the tile's window of axis-2 columns (thread q of the window loads
+  // P+1 values, coalesced), staged in shared memory (double-buffered by
+  // plane), and each thread finishes with P+1 products: P+1 loads per plane
+  // per thread instead of (P+1)^2.
+  int g2base = 0, rw = 0;
+  double* sR = reinterpret_cast<double*>(sm_raw + S * SL.stage_bytes + S * 8);
+  if (D == 3 && B1 == 1) {
+    const int jf = tx * B2, jl = (tx * B2 + B2 - 1) < a.M2 - 1 ? (tx * B2 + B2 - 1) : a.M2 - 1;
+    g2base = __ldg(a.g0_2 + jf);
+    rw = __ldg(a.g0_2 + jl) - g2base + P + 1;
+  }
+  const bool win = D == 3 && B1 == 1 && rw <= geo.lt_cap && rw <= nthr;  // CTA-uniform
+  double lv[P + 1];  // this thread's window column of the plane after next (raw lattice values)
+  int rbuf = 0;
+  auto fetch_window = [&](int ai) {
+    const int a2 = ai < a.N0 ? ai : a.N0 - 1;
+    if (tid < rw) {
+      const double* L0 = a.lattice + static_cast<std::int64_t>(a2) * N12 + g2base + tid;
+#pragma unroll
+      for (int k1 = 0; k1 <= P; ++k1) lv[k1] = __ldg(L0 + static_cast<std::int64_t>(g1 + k1) * a.N2);
+    }
+  };
+  if (win)
+    fetch_window(abase + P + 1);
+  else if (active)
+    fetch_plane(abase + P + 1);
   double l2 = 0.0;
   unsigned long long li = 0ull;  // L-inf as the bit pattern of |e| (ordered like the value)
   // error of the current row (ERR: the error field is stored); inactive
@@ -1525,9 +1552,28 @@ __global__ void __launch_bounds__(256, MB) k_decode_tma(const DecodeSweepArgs a,
         advance();
       }
       if (gnext == 0x7fffffff) break;
-      Tw[u] = active ? reduce_plane() : 0.0;  // plane abase + P + 1 replaces plane abase
-      ++abase;
-      if (active) fetch_plane(abase + P + 1);
+      if (win) {  // plane abase + P + 1 replaces plane abase, through the shared window
+        double* R = sR + rbuf * geo.lt_cap;
+        if (tid < rw) {
+          double r = 0.0;
+#pragma unroll
+          for (int k1 = 0; k1 <= P; ++k1) r = fma(w1[k1], lv[k1], r);
+          R[tid] = r;
+        }
+        __syncthreads();
+        const double* Rg = R + (g2 > g2base ? g2 - g2base : 0);  // (inactive threads: clamped, unused)
+        double sres = 0.0;
+#pragma unroll
+        for (int k2 = 0; k2 <= P; ++k2) sres = fma(w2[k2], Rg[k2], sres);
+        Tw[u] = active ? sres : 0.0;
+        rbuf ^= 1;
+        ++abase;
+        fetch_window(abase + P + 1);
+      } else {
+        Tw[u] = active ? reduce_plane() : 0.0;  // plane abase + P + 1 replaces plane abase
+        ++abase;
+        if (active) fetch_plane(abase + P + 1);
+      }
     }
   }
   // CTA reduction -> partial[blockIdx]
@@ -1629,7 +1675,7 @@ struct DecodeSweepLaunch {
   template <int D, int S>
   static void go(const DecodeSweepArgs& a, const CUtensorMap& map, const TmaGeom& g, cudaStream_t s) {
     const StageLayout SL = stage_layout(kFitR, g.B1 * g.B2, P);
-    const size_t smem = static_cast<size_t>(S) * SL.stage_bytes + S * 8;
+    const size_t smem = static_cast<size_t>(S) * SL.stage_bytes + S * 8 + 2 * static_cast<size_t>(g.lt_cap) * 8;
     dim3 grid(a.ntile1 * a.ntile2, a.nrange);
     static const int mb = std::getenv("MFADD_DEC_MINB") ? std::atoi(std::getenv("MFADD_DEC_MINB")) : 1;
     if (mb >= 4) {
