@@ -732,6 +732,7 @@ struct mfadd_solver {
 
   DBuf<int2> hr;
   DBuf<int> slist, clist, own_coord, pair_slot, unit_g0;
+  DBuf<long long> rowbase;  // k_assemble: P offset per (lattice row, last-dim owner block)
   DBuf<double> unit_vals;
   DBuf<std::int64_t> poff;
   std::int64_t hr_off[3] = {0, 0, 0}, s_off[3] = {0, 0, 0}, c_off[3] = {0, 0, 0}, oc_off[3] = {0, 0, 0};
@@ -1326,6 +1327,34 @@ std::unique_ptr<mfadd_solver> create_solver(mfadd_context* ctx, const mfadd_deco
     for (int b = s->srange.blo; b < s->srange.bhi; ++b)
       po[static_cast<std::size_t>(b)] = wl.blocks[static_cast<std::size_t>(b - s->srange.blo)].poff;
     s->poff.upload(po, st);
+    {  // assemble_owned's P offset of every lattice row in each last-dim owner block (k_assemble)
+      const int dl = D - 1;
+      std::int64_t rows = 1;
+      for (int k = 0; k < dl; ++k) rows *= d.n_ctrl[k];
+      const int Bl = d.blocks[dl];
+      std::vector<long long> rb(static_cast<std::size_t>(rows * Bl), 0);
+      for (std::int64_t r = 0; r < rows; ++r) {
+        std::int64_t rr = r, il[3] = {0, 0, 0};
+        int cl[3] = {0, 0, 0};
+        for (int k = dl - 1; k >= 0; --k) {
+          il[k] = rr % d.n_ctrl[k];
+          rr /= d.n_ctrl[k];
+          cl[k] = oc[static_cast<std::size_t>(s->oc_off[k] + il[k])];
+        }
+        int lead = 0;
+        for (int k = 0; k < dl; ++k) lead = lead * d.blocks[k] + cl[k];
+        for (int c = 0; c < Bl; ++c) {
+          std::int64_t o = 0;
+          for (int k = 0; k < dl; ++k) {
+            const AxisProb& pk = wl.probs[static_cast<std::size_t>(s->axbase[k] + cl[k])];
+            o = o * pk.n + (il[k] - pk.col_lo);
+          }
+          const AxisProb& pl = wl.probs[static_cast<std::size_t>(s->axbase[dl] + c)];
+          rb[static_cast<std::size_t>(r * Bl + c)] = po[static_cast<std::size_t>(lead * Bl + c)] + o * pl.n - pl.col_lo;
+        }
+      }
+      s->rowbase.upload(rb, st);
+    }
     // final-jump pair slots in the reference's order (solver.cpp:170-174)
     std::vector<int> ps(static_cast<std::size_t>(d.nblocks) * 27, -1);
     for (int a = 0; a < d.nblocks; ++a)
@@ -1754,6 +1783,7 @@ int enqueue_solve(mfadd_solver* s, const double* dfield) {
     aa.axbase[k] = s->axbase[k];
   }
   aa.own_coord = s->own_coord.p;
+  aa.rowbase = s->rowbase.p;
   aa.probs = wl.d_probs.p;
   aa.poff = s->poff.p;
   aa.P = wl.P.p;
@@ -2016,6 +2046,7 @@ int shard_assemble_decode(mfadd_solver* s, const double* dfield) {
     aa.axbase[k] = s->axbase[k];
   }
   aa.own_coord = s->own_coord.p;
+  aa.rowbase = s->rowbase.p;
   aa.probs = wl.d_probs.p;
   aa.poff = s->poff.p;
   aa.P = wl.P.p;

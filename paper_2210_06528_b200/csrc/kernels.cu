@@ -1516,28 +1516,10 @@ __global__ void __launch_bounds__(256) k_assemble(AssembleArgs a) {
     for (int i = threadIdx.x; i < Nl; i += blockDim.x) s_own[i] = static_cast<short>(__ldg(a.own_coord + a.oc_off[dl] + i));
   const std::int64_t r0 = static_cast<std::int64_t>(blockIdx.x) * kAsmRows;
   const int nr = static_cast<int>(a.nrows - r0 < kAsmRows ? a.nrows - r0 : kAsmRows);
-  // lead coordinates of each row; s_base per (row, last-dim block coordinate)
+  // s_base per (row, last-dim block coordinate): the plan's row-base table
   for (int e = threadIdx.x; e < nr * Bl; e += blockDim.x) {
     const int r = e / Bl, c = e - r * Bl;
-    std::int64_t row = a.row0 + r0 + r;
-    int cl[3] = {0, 0, 0};
-    std::int64_t il[3] = {0, 0, 0};
-    for (int k = dl - 1; k >= 0; --k) {
-      il[k] = row % a.N[k];
-      row /= a.N[k];
-      cl[k] = a.own_coord[a.oc_off[k] + il[k]];
-    }
-    int lead_id = 0;
-    for (int k = 0; k < dl; ++k) lead_id = lead_id * a.B[k] + cl[k];
-    const int id = lead_id * Bl + c;
-    // local row index within block id: row-major over the lead dims, then x n_last
-    std::int64_t o = 0;
-    for (int k = 0; k < dl; ++k) {
-      const AxisProb& pk = a.probs[a.axbase[k] + cl[k]];
-      o = o * pk.n + (il[k] - pk.col_lo);
-    }
-    const AxisProb& pl = a.probs[a.axbase[dl] + c];
-    s_base[r][c] = a.poff[id] + o * pl.n - pl.col_lo;
+    s_base[r][c] = __ldg(a.rowbase + (a.row0 + r0 + r) * Bl + c);
   }
   __syncthreads();
   const int i0 = static_cast<int>(a.col0), i1 = static_cast<int>(a.col0 + a.ncols);

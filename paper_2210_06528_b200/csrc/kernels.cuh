@@ -199,6 +199,7 @@ struct AssembleArgs {
   const AxisProb* probs;
   int axbase[3];
   const std::int64_t* poff;
+  const long long* rowbase;  // P offset of each lattice row in each last-dim owner block, minus its col_lo
   const double* P;
   double* lattice;
   std::int64_t row0, nrows;  // lattice rows (all dims but the last) to assemble
