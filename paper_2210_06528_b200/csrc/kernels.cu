@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -47,6 +48,11 @@ __device__ int g_mfb_debug_line = 0;
 #endif
 
 namespace mfb {
+
+bool pdl_enabled() {
+  static const bool on = std::getenv("MFADD_NO_PDL") == nullptr;
+  return on;
+}
 
 namespace {
 
@@ -89,6 +95,7 @@ __device__ __forceinline__ unsigned long long block_umax(unsigned long long v, u
 // ------------------------------------------------------------------- K1
 template <int P>
 __global__ void __launch_bounds__(256) k_basis_rows(RowsArgs a) {
+  pdl_enter();
   const int pid = a.prob0 + static_cast<int>(blockIdx.y);
   const AxisProb pr = a.probs[pid];
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1234,6 +1241,7 @@ __global__ void __launch_bounds__(kRegionThreads, MAXNS == 8 ? 2 : 3) k_epoch_re
   __shared__ unsigned long long s_red[32];
   __shared__ int s_last;
   __shared__ TileDev s_T;
+  pdl_enter();
   constexpr int kWords = static_cast<int>(sizeof(TileDev) / 4);
   static_assert(kWords <= kRegionThreads, "one descriptor word per thread");
   const int iter = a.mode < 0 ? a.st->iter + 1 : (a.mode == 4 ? 1 : 0);
@@ -1318,6 +1326,7 @@ __device__ __forceinline__ void region_pairs(const EpochRegionArgs& a, const Reg
 }
 
 __global__ void __launch_bounds__(kRegionThreads) k_pair_jumps_regions(EpochRegionArgs a) {
+  pdl_enter();
   __shared__ double s_w[2 * kRegionMaxHolders + 1][kRegionWarps];
   if (a.st->last_iter >= 2) return;  // after a mode-2 epoch all copies agree bitwise
   for (int tb = blockIdx.x; tb < a.ntiles; tb += gridDim.x) {
@@ -1507,6 +1516,7 @@ constexpr int kAsmMaxB = 256;
 constexpr int kAsmRows = 4;  // lattice rows per CTA (owner table loaded once)
 
 __global__ void __launch_bounds__(256) k_assemble(AssembleArgs a) {
+  pdl_enter();
   __shared__ short s_own[kAsmMaxLast];
   __shared__ long long s_base[kAsmRows][kAsmMaxB];  // P offset of the row in block (lead, c) minus col_lo
   const int D = a.D, dl = D - 1;
@@ -1689,7 +1699,7 @@ struct RowsLaunch {
   static int run(const RowsArgs& a, cudaStream_t s) {
     if (a.nprobs == 0 || a.max_m == 0) return 0;
     dim3 grid((a.max_m + 255) / 256, a.nprobs);
-    k_basis_rows<P><<<grid, 256, 0, s>>>(a);
+    launch_pdl(k_basis_rows<P>, grid, dim3(256), 0, s, a);
     return 1;
   }
 };
@@ -1922,14 +1932,14 @@ int launch_epoch_regions(const EpochRegionArgs& a, cudaStream_t s) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   if (a.mode == 3)  // persistent over the tiles: one wave (usually it exits at once)
-    k_pair_jumps_regions<<<a.ntiles < 2 * sms ? a.ntiles : 2 * sms, kRegionThreads, 0, s>>>(a);
+    launch_pdl(k_pair_jumps_regions, dim3(a.ntiles < 2 * sms ? a.ntiles : 2 * sms), dim3(kRegionThreads), 0, s, a);
   else {
     const int per_sm = a.max_ns > 4 ? 2 : 3;  // __launch_bounds__ residency
     const int grid = a.ntiles < sms * per_sm ? a.ntiles : sms * per_sm;
     if (a.max_ns > 4)
-      k_epoch_regions<8><<<grid, kRegionThreads, 0, s>>>(a);
+      launch_pdl(k_epoch_regions<8>, dim3(grid), dim3(kRegionThreads), 0, s, a);
     else
-      k_epoch_regions<4><<<grid, kRegionThreads, 0, s>>>(a);
+      launch_pdl(k_epoch_regions<4>, dim3(grid), dim3(kRegionThreads), 0, s, a);
   }
   return 1;
 }
@@ -1942,7 +1952,7 @@ int launch_dp(const DpArgs& a, cudaStream_t s) {
 int launch_assemble(const AssembleArgs& a, cudaStream_t s) {
   if (a.B[a.D - 1] > kAsmMaxB) return -1;  // host validates blocks_per_dim first
   if (a.nrows <= 0) return 0;
-  k_assemble<<<static_cast<unsigned>((a.nrows + kAsmRows - 1) / kAsmRows), 256, 0, s>>>(a);
+  launch_pdl(k_assemble, dim3(static_cast<unsigned>((a.nrows + kAsmRows - 1) / kAsmRows)), dim3(256), 0, s, a);
   return 1;
 }
 

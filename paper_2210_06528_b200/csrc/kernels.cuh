@@ -10,6 +10,33 @@
 
 namespace mfb {
 
+// Programmatic dependent launch on the solve's critical chain: each kernel
+// of the chain lets its successor launch as soon as it starts
+// (griddepcontrol.launch_dependents) and waits for its predecessor's grid to
+// complete and flush before touching anything (griddepcontrol.wait), so the
+// successor's launch and CTA rasterisation overlap the predecessor's tail.
+// Memory semantics are those of plain stream order.  MFADD_NO_PDL disables it.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, static_cast<Args&&>(args)...);
+}
+
 // Source line of the first failed device bounds check (debug builds), else 0.
 int debug_fail_line();
 int debug_fail_line_tma();  // stream_tma.cu lines (debug builds)

@@ -88,6 +88,7 @@ constexpr int kFitR = 8;  // rows per TMA stage (fit axis 0)
 template <int P, int S, int NC, bool MID, bool BACK = true, bool FWD = true>
 __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __grid_constant__ CUtensorMap map,
                                                        const TmaGeom geo) {
+  pdl_enter();
   constexpr int R = kFitR;
   extern __shared__ __align__(1024) unsigned char sm_raw[];
   const int b = blockIdx.y;
@@ -374,6 +375,7 @@ __host__ __device__ inline int last_stage_bytes(int LT, int P) {
 template <int P>
 __global__ void __launch_bounds__(256) k_last_contract_tma(const FitArgs a, const __grid_constant__ CUtensorMap map,
                                                            const int LT) {
+  pdl_enter();
   extern __shared__ __align__(1024) unsigned char sm_raw[];
   constexpr int S = kLastS, CW = kLastCW, PADC = P + 1;
   const int D = a.D, d = D - 1;
@@ -1209,6 +1211,7 @@ __device__ __forceinline__ unsigned stage_rl_tables(const FitArgs& a, const Axis
 
 template <int P>
 __global__ void __launch_bounds__(kSolve2dThreads) k_solve2d(const FitArgs a) {
+  pdl_enter();
   extern __shared__ __align__(128) double s2d[];
   __shared__ unsigned long long s_red[32];
   constexpr int PADC = P + 1, W = RL<P>::W;
@@ -1336,6 +1339,7 @@ struct BacksubLaunch {
 template <int P, int D, int S, int MB = 1, bool ERR = true>
 __global__ void __launch_bounds__(256, MB) k_decode_tma(const DecodeSweepArgs a, const __grid_constant__ CUtensorMap map,
                                                     const TmaGeom geo) {
+  pdl_enter();
   extern __shared__ __align__(1024) unsigned char sm_raw[];
   __shared__ double s_red[64];
   constexpr int R = kFitR;  // same row stages as the fit pass
@@ -1648,15 +1652,15 @@ struct Axis0Launch {
       const size_t smem_c = static_cast<size_t>(S) * SL.stage_bytes + 128;
       cudaFuncSetAttribute(k_fit_axis0_tma<P, S, NC, MID, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(smem_c));
-      k_fit_axis0_tma<P, S, NC, MID, false, false><<<grid, g.B1 * g.B2 / NC, smem_c, s>>>(a, map, g);
+      launch_pdl(k_fit_axis0_tma<P, S, NC, MID, false, false>, grid, dim3(g.B1 * g.B2 / NC), smem_c, s, a, map, g);
     } else if (!MID && a.defer_back) {
       cudaFuncSetAttribute(k_fit_axis0_tma<P, S, NC, MID, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(smem));
-      k_fit_axis0_tma<P, S, NC, MID, false><<<grid, g.B1 * g.B2 / NC, smem, s>>>(a, map, g);
+      launch_pdl(k_fit_axis0_tma<P, S, NC, MID, false>, grid, dim3(g.B1 * g.B2 / NC), smem, s, a, map, g);
     } else {
       cudaFuncSetAttribute(k_fit_axis0_tma<P, S, NC, MID>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(smem));
-      k_fit_axis0_tma<P, S, NC, MID><<<grid, g.B1 * g.B2 / NC, smem, s>>>(a, map, g);
+      launch_pdl(k_fit_axis0_tma<P, S, NC, MID>, grid, dim3(g.B1 * g.B2 / NC), smem, s, a, map, g);
     }
   }
   static int run(const FitArgs& a, const CUtensorMap& map, const TmaGeom& g, int ntiles, cudaStream_t s) {
@@ -1680,17 +1684,17 @@ struct DecodeSweepLaunch {
     static const int mb = std::getenv("MFADD_DEC_MINB") ? std::atoi(std::getenv("MFADD_DEC_MINB")) : 1;
     if (mb >= 4) {
       cudaFuncSetAttribute(k_decode_tma<P, D, S, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      k_decode_tma<P, D, S, 4><<<grid, g.B1 * g.B2, smem, s>>>(a, map, g);
+      launch_pdl(k_decode_tma<P, D, S, 4>, grid, dim3(g.B1 * g.B2), smem, s, a, map, g);
       return;
     }
     if (!a.err) {  // no error field: L2 / L-inf only
       cudaFuncSetAttribute(k_decode_tma<P, D, S, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(smem));
-      k_decode_tma<P, D, S, 1, false><<<grid, g.B1 * g.B2, smem, s>>>(a, map, g);
+      launch_pdl(k_decode_tma<P, D, S, 1, false>, grid, dim3(g.B1 * g.B2), smem, s, a, map, g);
       return;
     }
     cudaFuncSetAttribute(k_decode_tma<P, D, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    k_decode_tma<P, D, S><<<grid, g.B1 * g.B2, smem, s>>>(a, map, g);
+    launch_pdl(k_decode_tma<P, D, S>, grid, dim3(g.B1 * g.B2), smem, s, a, map, g);
   }
   static int run(const DecodeSweepArgs& a, const CUtensorMap& map, const TmaGeom& g, cudaStream_t s) {
     if (a.D == 2)
@@ -1723,13 +1727,13 @@ struct LastLaunch {
     const size_t smem = static_cast<size_t>(kLastS) * last_stage_bytes(LT, P) + 128;
     cudaFuncSetAttribute(k_last_contract_tma<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     dim3 grid((a.max_lines_last + LT - 1) / LT, a.nblocks, kseg);
-    k_last_contract_tma<P><<<grid, LT, smem, s>>>(a, map, LT);
+    launch_pdl(k_last_contract_tma<P>, grid, dim3(LT), smem, s, a, map, LT);
     // the contraction needs no factor: the Gram/Cholesky side stream joins here
     if (a.join_event) cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(a.join_event), 0);
     if (a.fuse2d) {
       const size_t sm2 = solve2d_smem_bytes(a.max_n0, a.max_n1, a.max_zl, P, kseg);
       cudaFuncSetAttribute(k_solve2d<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm2));
-      k_solve2d<P><<<a.nblocks, kSolve2dThreads, sm2, s>>>(a);
+      launch_pdl(k_solve2d<P>, dim3(a.nblocks), dim3(kSolve2dThreads), sm2, s, a);
       return 2;
     }
     constexpr int T2 = 64, F = (P + 2) & ~1;
