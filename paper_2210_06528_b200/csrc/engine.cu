@@ -1718,6 +1718,7 @@ int enqueue_solve(mfadd_solver* s, const double* dfield) {
     const cudaGraphConditionalHandle h = make_loop_handle(st);
     mfb::EpochRegionArgs a = region_args(s, 4);
     a.cond = static_cast<unsigned long long>(h);
+    a.zero_pairs = static_cast<int>(s->pair_jumps.n);  // cleared here instead of by a memset node
     s->tl.begin("epoch");
     launches += mfb::launch_epoch_regions(a, st);
     s->tl.end();
@@ -1767,7 +1768,8 @@ int enqueue_solve(mfadd_solver* s, const double* dfield) {
   // epoch all copies of each control are bit-identical and every per-pair
   // jump is exactly 0 (the kernel checks the last iteration on the device).
   if (s->npairs > 0) {
-    CK(cudaMemsetAsync(s->pair_jumps.p, 0, s->pair_jumps.n * sizeof(unsigned long long), st));
+    if (!fuse01)  // (the fused epoch's finalize cleared them)
+      CK(cudaMemsetAsync(s->pair_jumps.p, 0, s->pair_jumps.n * sizeof(unsigned long long), st));
     s->tl.begin("pair_jumps");
     launches += regions ? mfb::launch_epoch_regions(region_args(s, 3), st)
                         : mfb::launch_epoch(epoch_args(s, 3), st);

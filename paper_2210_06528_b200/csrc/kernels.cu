@@ -1206,6 +1206,7 @@ __device__ void epoch_finalize(const EpochRegionArgs& a, int mode, int slot, uns
     a.change[b] = 0ull;
     a.linf_sh[b] = 0ull;
   }
+  for (int q = threadIdx.x; q < a.zero_pairs; q += blockDim.x) a.pair_jumps[q] = 0ull;
   dp = block_umax(dp, s_red);
   if (threadIdx.x == 0) {
     const double dpv = mode == 0 ? 0.0 : __longlong_as_double(static_cast<long long>(dp));  // record_epoch(0, 0.0)

@@ -174,6 +174,7 @@ struct EpochRegionArgs {
   int max_ns;               // largest region n_s (selects the kernel form)
   const double* recv;       // sharded: remote holders' copies (RegionDev::rmask)
   int finalize;             // 1: the last CTA computes dp and writes epoch_out (else k_epoch_finalize)
+  int zero_pairs;           // > 0: the finalize also clears pair_jumps[0, zero_pairs) (no memset node in the chain)
   int slot;                 // epoch_out slot when finalize is done separately
 };
 int launch_epoch_regions(const EpochRegionArgs& a, cudaStream_t s);
