@@ -750,7 +750,7 @@ struct mfadd_solver {
   int max_holders = 1;
   // log_errors: per-epoch block residuals
   DBuf<double> res_partial, block_errs;
-  int res_ntile = 0;
+  int res_ntile = 0, res_max_m0 = 0;
   std::vector<double> h_block_errs;
   // shard: rank of nranks owns blocks [srange.blo, srange.bhi)
   int rank = 0, nranks = 1;
@@ -968,6 +968,7 @@ mfb::BlockResArgs res_args(mfadd_solver* s, const double* dfield, const mfb::Epo
   a.nglobal = s->dec.nblocks;
   a.boff = s->srange.blo;
   a.expect_iter = -1;
+  a.max_m0 = s->res_max_m0;
   return a;
 }
 
@@ -1477,6 +1478,7 @@ std::unique_ptr<mfadd_solver> create_solver(mfadd_context* ctx, const mfadd_deco
       int mx = 1;
       for (const auto& b : wl.blocks) {
         const int m0 = wl.probs[static_cast<std::size_t>(b.ax[0])].m;
+        s->res_max_m0 = std::max(s->res_max_m0, m0);
         int tr = 1;
         for (int k = 1; k < D; ++k) tr *= wl.probs[static_cast<std::size_t>(b.ax[k])].m;
         mx = std::max(mx, D == 1 ? m0 : tr);

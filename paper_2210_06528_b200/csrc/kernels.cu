@@ -1450,6 +1450,149 @@ __global__ void __launch_bounds__(kResThreads) k_block_residual(BlockResArgs a) 
   }
 }
 
+// D = 2, 3 form of K9 with the block's axis-0 row table staged in shared
+// memory (broadcast reads: no global load on the per-row chain), the next
+// control plane's lattice values fetched one advance ahead (the decode's
+// scheme, k_decode_tma) and the field rows RB at a time ahead of use.  Same
+// arithmetic, in the same order, as k_block_residual.
+template <int P, int D>
+__global__ void __launch_bounds__(kResThreads) k_block_residual_staged(BlockResArgs a) {
+  extern __shared__ __align__(16) double s_rows[];  // m0 x (P+1) basis values, then m0 first columns
+  __shared__ double s_red[2][kResThreads / 32];
+  if (a.expect_iter >= 0 && a.st->iter != a.expect_iter) return;  // its epoch did not run
+  const int b = blockIdx.y;
+  const BlockDev& blk = a.blocks[b];
+  const AxisProb p0 = a.probs[blk.ax[0]], p1 = a.probs[blk.ax[1]];
+  const AxisProb p2 = D == 3 ? a.probs[blk.ax[2]] : p1;
+  const int m0 = p0.m, n0 = p0.n, m1 = p1.m, n1 = p1.n;
+  const int m2 = D == 3 ? p2.m : 1, n2 = D == 3 ? p2.n : 1;
+  double* sv = s_rows;
+  int* sg = reinterpret_cast<int*>(s_rows + m0 * (P + 1));
+  {
+    const double* v00 = a.vals + p0.row_off * (P + 1);
+    const int* g00 = a.g0 + p0.row_off;
+    for (int e = threadIdx.x; e < m0 * (P + 1); e += kResThreads) sv[e] = __ldg(v00 + e);
+    for (int e = threadIdx.x; e < m0; e += kResThreads) sg[e] = __ldg(g00 + e);
+  }
+  __syncthreads();
+  const double* Pb = a.P + blk.poff;
+  double l2 = 0.0, li = 0.0;
+  auto clampi = [](int i, int n) { return i < 0 ? 0 : (i >= n ? n - 1 : i); };
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < m1 * m2) {
+    const int j1 = D == 3 ? t / m2 : t, j2 = D == 3 ? t - (t / m2) * m2 : 0;
+    double w1[P + 1], w2[P + 1];
+    int r1[P + 1], c2[P + 1];  // clamped lattice row / column offsets of this point's window
+    const int g1 = __ldg(a.g0 + p1.row_off + j1);
+    const int g2 = D == 3 ? __ldg(a.g0 + p2.row_off + j2) : 0;
+#pragma unroll
+    for (int k = 0; k <= P; ++k) {
+      w1[k] = __ldg(a.vals + (p1.row_off + j1) * (P + 1) + k);
+      w2[k] = D == 3 ? __ldg(a.vals + (p2.row_off + j2) * (P + 1) + k) : 0.0;
+      r1[k] = clampi(g1 + k, n1) * n2;
+      c2[k] = D == 3 ? clampi(g2 + k, n2) : 0;
+    }
+    const std::int64_t plane_sz = static_cast<std::int64_t>(n1) * n2;
+    constexpr int NV = D == 2 ? (P + 1) : (P + 1) * (P + 1);
+    double nxt[NV];  // raw lattice values of the plane after the window
+    auto fetch = [&](int ai) {
+      const double* L0 = Pb + static_cast<std::int64_t>(clampi(ai, n0)) * plane_sz;
+#pragma unroll
+      for (int k1 = 0; k1 <= P; ++k1) {
+        if (D == 2) {
+          nxt[k1] = L0[r1[k1]];
+        } else {
+#pragma unroll
+          for (int k2 = 0; k2 <= P; ++k2) nxt[(k1 * (P + 1) + k2) % NV] = L0[r1[k1] + c2[k2]];
+        }
+      }
+    };
+    auto reduce = [&]() -> double {  // plane() of k_block_residual on the fetched values
+      double s = 0.0;
+#pragma unroll
+      for (int k1 = 0; k1 <= P; ++k1) {
+        if (D == 2) {
+          s = fma(w1[k1], nxt[k1], s);
+        } else {
+          double r = 0.0;
+#pragma unroll
+          for (int k2 = 0; k2 <= P; ++k2) r = fma(w2[k2], nxt[(k1 * (P + 1) + k2) % NV], r);
+          s = fma(w1[k1], r, s);
+        }
+      }
+      return s;
+    };
+    int abase = sg[0];
+    double Tw[P + 1];
+#pragma unroll
+    for (int k = 0; k <= P; ++k) {
+      fetch(abase + k);
+      Tw[k] = reduce();
+    }
+    // D = 2: the next plane's P+1 values ride along in registers; D = 3 would
+    // hold (P+1)^2 of them across the row loop, so it fetches at the advance
+    constexpr bool AHEAD = D == 2;
+    if (AHEAD) fetch(abase + P + 1);
+    const double* q = a.field + blk.fbase + j1 * a.fs[1] + (D == 3 ? j2 * a.fs[2] : 0);
+    const std::int64_t fs0 = a.fs[0];
+    constexpr int RB = 4;
+    double qn[RB];
+#pragma unroll
+    for (int u = 0; u < RB; ++u) qn[u] = u < m0 ? __ldcs(q + u * fs0) : 0.0;
+    for (int j0 = 0; j0 < m0; j0 += RB) {
+      double qc[RB];
+#pragma unroll
+      for (int u = 0; u < RB; ++u) {
+        qc[u] = qn[u];
+        const int jn = j0 + RB + u;
+        qn[u] = jn < m0 ? __ldcs(q + jn * fs0) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < RB; ++u) {
+        const int j = j0 + u;
+        if (j < m0) {
+          const int g = sg[j];
+          while (abase < g) {
+#pragma unroll
+            for (int k = 0; k < P; ++k) Tw[k] = Tw[k + 1];
+            ++abase;
+            if (!AHEAD) fetch(abase + P);
+            Tw[P] = reduce();  // plane abase + P
+            if (AHEAD) fetch(abase + P + 1);
+          }
+          const double* vr = sv + j * (P + 1);
+          double s = 0.0;
+#pragma unroll
+          for (int k = 0; k <= P; ++k) s = fma(vr[k], Tw[k], s);
+          const double e = qc[u] - s;
+          l2 = fma(e, e, l2);
+          li = fmax(li, fabs(e));
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    l2 += __shfl_xor_sync(kFull, l2, o);
+    li = fmax(li, __shfl_xor_sync(kFull, li, o));
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    s_red[0][w] = l2;
+    s_red[1][w] = li;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sl = 0.0, sm = 0.0;
+    for (int i = 0; i < kResThreads / 32; ++i) {
+      sl += s_red[0][i];
+      sm = fmax(sm, s_red[1][i]);
+    }
+    a.partial[2 * (static_cast<std::int64_t>(b) * a.ntile + blockIdx.x)] = sl;
+    a.partial[2 * (static_cast<std::int64_t>(b) * a.ntile + blockIdx.x) + 1] = sm;
+  }
+}
+
 // Fixed-order reduction of the per-tile partials: errs[slot][b] = {sqrt(sum), max}.
 __global__ void k_block_residual_reduce(BlockResArgs a) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1470,7 +1613,17 @@ template <int P>
 struct BlockResLaunch {
   static int run(const BlockResArgs& a, cudaStream_t s) {
     dim3 grid(a.ntile, a.nblocks);
-    k_block_residual<P><<<grid, kResThreads, 0, s>>>(a);
+    const size_t smem = static_cast<size_t>(a.max_m0) * ((P + 1) * 8 + 4) + 16;
+    static const bool plain = std::getenv("MFADD_RES_PLAIN") != nullptr;  // A/B: the unstaged kernel
+    // D = 3 stays on the unstaged kernel (the staged form holds about 30% more
+    // registers there; not measured faster)
+    if (a.D == 2 && !plain && smem <= 160 * 1024) {
+      cudaFuncSetAttribute(k_block_residual_staged<P, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem));
+      k_block_residual_staged<P, 2><<<grid, kResThreads, smem, s>>>(a);
+    } else {
+      k_block_residual<P><<<grid, kResThreads, 0, s>>>(a);
+    }
     k_block_residual_reduce<<<(a.nblocks + 127) / 128, 128, 0, s>>>(a);
     return 2;
   }

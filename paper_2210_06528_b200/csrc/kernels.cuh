@@ -202,6 +202,7 @@ struct BlockResArgs {
   int slot;
   int expect_iter;             // >= 0: no-op unless st->iter == expect_iter (after a predicated epoch)
   int nglobal, boff;           // all blocks; global id of local block 0
+  int max_m0;                  // longest axis-0 row table of a local block (shared-memory staging)
 };
 int launch_block_residual(int degree, const BlockResArgs& a, cudaStream_t s);
 
