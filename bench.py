@@ -17,7 +17,20 @@ explicit flush is needed between timed steps.
 
 --impl reference: the reference's own CPU implementation (oracle/_ref, built
 from the unmodified /root/reference sources) on all host threads, same config,
-each step one full solve.  Under torchrun only rank 0 runs it.
+each step one full solve, timed around mfadd::solve() only (C++ steady_clock
+inside the driver: the Field build and the result copies are outside, as
+BASELINE.md §3 asks); the line reports the median step.  Under torchrun only
+rank 0 runs it.
+
+--gpus N without torchrun: the bench relaunches itself under
+torch.distributed.run with N ranks (one per GPU, 127.0.0.1 rendezvous).
+--scaling weak (default): each rank solves one config-sized slab of block rows
+(the global problem grows with N); strong: the config's global problem is
+split over the N ranks.
+
+`other_configs` (N = 1): the other BASELINE configs through the same path —
+graph-replay ms/solve, pts/s, the step's roofline fraction and parity against
+the reference (oracle/_ref) on the same field.
 """
 from __future__ import annotations
 
@@ -46,7 +59,56 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-log-errors", action="store_true")
+    ap.add_argument("--no-other", action="store_true", help="skip the other_configs pass")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     return ap.parse_args()
+
+
+def relaunch_distributed(args):
+    """--gpus N > 1 outside torchrun: run this script under torch.distributed.run
+    with N ranks and pass its output and exit status through."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def global_config(cfg, world, scaling):
+    from paper_2210_06528_b200 import workloads as W
+    return W.weak(cfg, world) if scaling == "weak" else cfg
+
+
+def bench_field_host(cfg):
+    """The bench's input field on the host: the device generator when a GPU is
+    present (the buffer our arm solves), else the host generator."""
+    from paper_2210_06528_b200 import workloads as W
+    try:
+        import torch
+        if torch.cuda.is_available():
+            f = W.make_field_torch(cfg).cpu().numpy()
+            torch.cuda.empty_cache()
+            return f, "device generator (the buffer the GPU arm solves)"
+    except Exception:
+        pass
+    return W.make_field_numpy(cfg), "host generator"
+
+
+def ref_time_solves(cfg, values, n, workers, log_errors=False):
+    """n reference solves on `values`: solve()-only seconds (steady_clock inside
+    the driver) of each, and the last result."""
+    from oracle import ref
+    dec = ref.RefDecomposition(cfg.grid, cfg.blocks, cfg.degree, cfg.nctrl, cfg.overlap,
+                               bounds=[list(b) for b in cfg.bounds])
+    ts, r = [], None
+    for _ in range(n):
+        r = ref.solve(dec, values, cfg.max_iters, cfg.tolerance, workers=workers, log_errors=log_errors,
+                      want_blocks=False)
+        ts.append(r.timings["solve_s"])
+    return ts, r
 
 
 def workload_desc(cfg):
@@ -156,50 +218,52 @@ def run_reference(args, cfg, rank):
     if rank != 0:
         return
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1:  # the same (weak-scaled) global problem as our arm
-        from paper_2210_06528_b200 import workloads as W
-        cfg = W.weak(cfg, world)
+    n = world if world > 1 else args.gpus
+    cfg = global_config(cfg, n, args.scaling)  # the same global problem as our arm
     if not ref.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libmfadd_ref.so not built"}))
         return
-    from paper_2210_06528_b200 import workloads as W
-    values = W.make_field_numpy(cfg)
-    dec = ref.RefDecomposition(cfg.grid, cfg.blocks, cfg.degree, cfg.nctrl, cfg.overlap,
-                               bounds=[list(b) for b in cfg.bounds])
+    values, src = bench_field_host(cfg)
     cores = os.cpu_count() or 1
-    for _ in range(args.warmup):
-        ref.solve(dec, values, cfg.max_iters, cfg.tolerance, workers=cores, log_errors=False, want_blocks=False)
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        ref.solve(dec, values, cfg.max_iters, cfg.tolerance, workers=cores, log_errors=False, want_blocks=False)
-        times.append(time.perf_counter() - t0)
-    t = sum(times) / len(times)
+    ref_time_solves(cfg, values, args.warmup, cores)
+    times, r = ref_time_solves(cfg, values, args.steps, cores)
+    t = statistics.median(times)
     v = cfg.points / t
-    sample = f"full {cfg.name} solve per step ({cfg.points} pts), log_errors=false, workers={cores}"
+    extra = {}
+    if not args.no_log_errors:  # the reference's default mode (solver.hpp:20), one solve
+        tl, _ = ref_time_solves(cfg, values, 1, cores, log_errors=True)
+        extra["log_errors_true"] = {"value": cfg.points / tl[0], "unit": UNIT, "ms_per_step": tl[0] * 1e3,
+                                    "workers": cores}
+    sample = (f"full {cfg.name} solve per step ({cfg.points} pts), log_errors=false, workers={cores}; "
+              f"solve() only (steady_clock), median of {args.steps}")
     print(json.dumps({
-        "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded, BASELINE shapes)", "impl": "reference",
-        "config": {"workload": workload_desc(cfg), "parallelism": f"{cores} host threads (reference thread pool)"},
+        "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": n, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+        "dtype": "f64", "data": f"synthetic (seeded, BASELINE shapes; {src})", "impl": "reference",
+        "config": {"workload": workload_desc(cfg), "parallelism": f"{cores} host threads (reference thread pool)",
+                   "timing": "mfadd::solve() only, C++ steady_clock; median over the K steps",
+                   "ms_per_step_min": min(times) * 1e3, "ms_per_step_max": max(times) * 1e3},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        **extra,
     }))
 
 
 def cpu_baseline(cfg, values_host):
-    """The reference (oracle/_ref) on this host's cores, one bounded full solve."""
+    """The reference (oracle/_ref) on this host: median of 3 solve()-only runs on
+    all cores, one run on 1 worker, one log_errors=true run."""
     from oracle import ref
     cores = os.cpu_count() or 1
     if ref.available():
-        dec = ref.RefDecomposition(cfg.grid, cfg.blocks, cfg.degree, cfg.nctrl, cfg.overlap,
-                                   bounds=[list(b) for b in cfg.bounds])
-        t0 = time.perf_counter()
-        r = ref.solve(dec, values_host, cfg.max_iters, cfg.tolerance, workers=cores, log_errors=False,
-                      want_blocks=False)
-        t = time.perf_counter() - t0
+        ts, r = ref_time_solves(cfg, values_host, 3, cores)
+        t = statistics.median(ts)
+        t1, _ = ref_time_solves(cfg, values_host, 1, 1)
+        tl, _ = ref_time_solves(cfg, values_host, 1, cores, log_errors=True)
         return {"value": cfg.points / t, "unit": UNIT, "cores": cores, "kind": "reference",
-                "sample": f"1 full {cfg.name} solve ({cfg.points} pts) in {t:.2f} s, workers={cores}"}, r
+                "sample": f"{cfg.name} full solves ({cfg.points} pts): median of 3 at workers={cores} "
+                          f"({t:.2f} s, solve() only), 1 at workers=1, 1 with log_errors=true",
+                "workers_1": {"value": cfg.points / t1[0], "ms_per_step": t1[0] * 1e3, "cores": 1},
+                "log_errors_true": {"value": cfg.points / tl[0], "ms_per_step": tl[0] * 1e3, "cores": cores}}, r
     from oracle import orc
     dec = orc.Decomposition(cfg.grid, cfg.blocks, cfg.degree, cfg.nctrl, cfg.overlap)
     t0 = time.perf_counter()
@@ -209,10 +273,85 @@ def cpu_baseline(cfg, values_host):
             "sample": f"1 full {cfg.name} solve ({cfg.points} pts) in {t:.2f} s, C restatement"}, r
 
 
+def parity_vs_ref(ours, r):
+    """Solve parity figures against a reference SolveResult."""
+    import numpy as np
+    scale = max(1.0, float(np.abs(r.controls).max()))
+    return {"max_abs_dP_rel": float(np.abs(ours.model.controls - r.controls).max()) / scale,
+            "iters_equal": ours.constraint_iterations == r.constraint_iterations,
+            "converged_equal": ours.converged == r.converged,
+            "l2_rel": abs(ours.global_l2 - r.global_l2) / max(1.0, r.global_l2),
+            "linf_rel": abs(ours.global_linf - r.global_linf) / max(1.0, r.global_linf),
+            "epochs_equal": len(ours.epochs) == len(r.epochs),
+            "dp_max_abs": max([abs(a.dp_max - float(b[1])) for a, b in zip(ours.epochs, r.epochs)] or [0.0])}
+
+
+def other_config(name, args, ctx, stream):
+    """One other BASELINE config through the same path: graph-replay ms/solve,
+    step roofline fraction, log_errors=true ms/solve, parity vs the reference."""
+    import numpy as np
+    import torch
+    import paper_2210_06528_b200 as m
+    from paper_2210_06528_b200 import workloads as W
+    from oracle import ref
+    cfg = W.CONFIGS[name]
+    field = W.make_field_torch(cfg)
+    torch.cuda.synchronize()
+    dec = m.partition(cfg.grid, cfg.bounds, cfg.blocks, cfg.degree, cfg.nctrl, cfg.overlap)
+    out = {"workload": workload_desc(cfg)}
+
+    def timed(log_errors):
+        s = m.Solver(dec, m.SolverConfig(max_outer_iterations=cfg.max_iters, tolerance=cfg.tolerance,
+                                         log_errors=log_errors, store_error=True), ctx)
+        for _ in range(3):
+            s.run(field, on_device=True)
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k = max(3, args.steps)
+        a0.record(stream)
+        for _ in range(k):
+            s.run(field, on_device=True)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        return s, a0.elapsed_time(a1) / k
+
+    s, ms = timed(False)
+    res = s.result(want_blocks=False, want_error=False)
+    ab = W.algorithmic_bytes(cfg, dec, len(res.epochs) - 1, store_error=True)
+    peak, _ = measured_peaks()
+    out.update({"ms_per_step": ms, "value": cfg.points / (ms * 1e-3), "unit": UNIT,
+                "epochs": len(res.epochs), "constraint_iterations": res.constraint_iterations,
+                "step_algorithmic_bytes": ab["bytes"], "step_frac": ab["bytes"] / (ms * 1e-3) / 1e9 / peak,
+                "roofline_ms": ab["bytes"] / (peak * 1e9) * 1e3})
+    if not args.no_log_errors:
+        sl, lms = timed(True)
+        out["log_errors_true"] = {"ms_per_step": lms, "value": cfg.points / (lms * 1e-3)}
+        rl = sl.result(want_blocks=False, want_error=False)
+        sl.close()
+    s.close()
+    if ref.available() and not args.no_cpu_baseline:
+        host = field.cpu().numpy()
+        del field
+        torch.cuda.empty_cache()
+        cores = os.cpu_count() or 1
+        ts, r = ref_time_solves(cfg, host, 1, cores, log_errors=not args.no_log_errors)
+        par = parity_vs_ref(res, r)
+        if not args.no_log_errors:
+            be = [max(abs(a - b) / max(1.0, abs(b)) for ga, rb in zip(e.block_errors, np.asarray(r.block_errors[i]))
+                      for a, b in zip(ga, rb)) for i, e in enumerate(rl.epochs)]
+            par["block_errors_max_rel"] = float(max(be)) if be else 0.0
+        out["parity_vs_reference"] = par
+        out["reference_ms_per_step"] = ts[0] * 1e3
+        out["reference_note"] = f"oracle/_ref solve() only, workers={cores}, log_errors={not args.no_log_errors}"
+    return out
+
+
 def main():
     args = parse()
     from paper_2210_06528_b200 import workloads as W
     cfg = W.CONFIGS[args.config]
+    if args.impl != "reference" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_distributed(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -230,9 +369,10 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        # weak scaling: the global problem grows with N, each rank solves one
-        # cfg-sized slab of block rows (block-sharded solve, NCCL exchanges)
-        cfg = W.weak(cfg, world)
+        # weak: the global problem grows with N, each rank solves one cfg-sized
+        # slab of block rows; strong: cfg itself split over the ranks
+        # (block-sharded solve, NCCL exchanges)
+        cfg = global_config(cfg, world, args.scaling)
     field = W.make_field_torch(cfg)
     torch.cuda.synchronize()
     dec = m.partition(cfg.grid, cfg.bounds, cfg.blocks, cfg.degree, cfg.nctrl, cfg.overlap)
@@ -284,7 +424,7 @@ def main():
 
     # ---------------- the reference's default mode, log_errors=true
     log_mode = None
-    if not args.no_e2e:
+    if not args.no_log_errors:
         lcfg = m.SolverConfig(max_outer_iterations=cfg.max_iters, tolerance=cfg.tolerance, log_errors=True,
                               store_error=True)
         lsolver = m.Solver(dec, lcfg, ctx, comm=comm)
@@ -382,10 +522,13 @@ def main():
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded generator on device, BASELINE shapes)",
-        "config": {"workload": workload_desc(cfg), "parallelism": (f"block-sharded x{world} (NCCL exchange per epoch, weak scaling: "
-                                   f"{world} x {args.config} slabs)") if world > 1 else "1 GPU",
+        "config": {"workload": workload_desc(cfg),
+                   "parallelism": ((f"block-sharded x{world} (NCCL exchange per epoch, weak scaling: "
+                                    f"{world} x {args.config} slabs)") if args.scaling == "weak" else
+                                   f"block-sharded x{world} (NCCL exchange per epoch, strong scaling of {args.config})")
+                   if world > 1 else "1 GPU",
                    "l2_flush": "input 8*prod(M) bytes > 126 MB L2 (no explicit flush)",
                    "timing": "value: K whole-solve graph replays between CUDA events; kernels/roofline: a second "
                              "pass of K solves with an event pair around every launch",
@@ -404,10 +547,25 @@ def main():
         host = field.cpu().numpy()
         cb, r = cpu_baseline(cfg, host)
         ours = solver.result(want_blocks=False, want_error=False)
-        scale = max(1.0, float(np.abs(r.controls).max()))
-        cb["parity_max_abs_dP_rel"] = float(np.abs(ours.model.controls - r.controls).max()) / scale
-        cb["parity_iters_equal"] = ours.constraint_iterations == r.constraint_iterations
+        par = parity_vs_ref(ours, r)
+        cb["parity_max_abs_dP_rel"] = par["max_abs_dP_rel"]
+        cb["parity_iters_equal"] = par["iters_equal"]
+        cb["parity"] = par
         out["cpu_baseline"] = cb
+    if rank == 0 and world == 1 and not args.no_other:
+        solver.close()
+        del field
+        torch.cuda.empty_cache()
+        others = {}
+        for nm in ("C1", "C2", "C3", "C4", "C5"):
+            if nm == args.config:
+                continue
+            try:
+                others[nm] = other_config(nm, args, ctx, stream)
+            except Exception as ex:  # reported, never silently dropped
+                others[nm] = {"error": f"{type(ex).__name__}: {ex}"}
+            torch.cuda.empty_cache()
+        out["other_configs"] = others
     if rank == 0:
         print(json.dumps(out))
     if dist:

@@ -69,6 +69,8 @@ void mfadd_dec_holder_ranges(const mfadd_decomposition* dec, int dim, int* out /
 void mfadd_dec_exchange_volume(const mfadd_decomposition* dec, int64_t* out);
 double mfadd_dec_compression_ratio(const mfadd_decomposition* dec); /* layout.hpp:114 */
 int mfadd_dec_any_shared(const mfadd_decomposition* dec);           /* SharedDofMap::any_shared */
+/* GlobalLayout::n_input (layout.hpp:86-96): the field extents the decomposition expects */
+void mfadd_dec_grid_dims(const mfadd_decomposition* dec, int64_t* out /* rank */);
 
 /* ----------------------------------------------------------------- device */
 typedef struct mfadd_context mfadd_context;
@@ -203,6 +205,29 @@ int mfadd_collocation(mfadd_context* ctx, const double* knots, int nknots, int d
 int mfadd_fit_unconstrained(mfadd_context* ctx, int rank, int degree, const double* knots, const int64_t* kn_off,
                             const double* params, const int64_t* pm_off, const int64_t* col_lo,
                             const int64_t* col_hi, const double* q, double* out_p);
+
+/* ResidualStats residual_error(const LocalProblem&, const Tensor& controls)
+ *                                                   lsq.hpp:35-41, lsq.cpp:66-85
+ * The local problem as in mfadd_fit_unconstrained; controls has extents
+ * col_hi[d]-col_lo[d].  out_pointwise (nullable) = q - decode(controls) with the
+ * window-clipped rows, bitwise equal to the reference; l2 = sqrt(sum e^2)
+ * (device reduction: equal within rounding), linf = max |e|. */
+int mfadd_residual_error(mfadd_context* ctx, int rank, int degree, const double* knots, const int64_t* kn_off,
+                         const double* params, const int64_t* pm_off, const int64_t* col_lo, const int64_t* col_hi,
+                         const double* q, const double* controls, double* out_pointwise, double* out_l2,
+                         double* out_linf);
+
+/* int find_span(const KnotVector&, double)                        knots.hpp:36
+ * SpanBasis basis_funs(const KnotVector&, int span, double u)     knots.hpp:53
+ * SpanBasis basis_derivs(const KnotVector&, int span, double u, int k)  knots.hpp:56
+ * n evaluations on the GPU.  spans == NULL: span = find_span(u) (ERANGE for
+ * u outside the evaluable range, the reference's message); else the given
+ * spans (one-sided limits), which must satisfy p <= span < nknots - p - 1
+ * (EINVAL).  orders = k >= 0 (EINVAL if k > p); out: n x (k+1) x (p+1)
+ * values, row 0 = basis_funs, row r = the r-th derivatives (bitwise equal to
+ * the reference); out_spans (nullable) receives the spans used. */
+int mfadd_basis_funs(mfadd_context* ctx, const double* knots, int nknots, int degree, int64_t n, const double* u,
+                     const int* spans, int orders, int* out_spans, double* out);
 
 /* Tensor decode(controls, kvs, params, col_offset)  decode.hpp:20-22 */
 int mfadd_decode(mfadd_context* ctx, int rank, int degree, const double* knots, const int64_t* kn_off,

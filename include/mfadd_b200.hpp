@@ -174,6 +174,7 @@ class Decomposition {
 
   std::vector<KnotVector> kvs;          // GlobalLayout::kvs
   std::vector<std::int64_t> n_ctrl;     // GlobalLayout::n_ctrl
+  std::vector<std::int64_t> n_input;    // GlobalLayout::n_input (field extents)
   std::vector<BlockLayout> blocks;      // Decomposition::blocks
 
  private:
@@ -183,6 +184,8 @@ class Decomposition {
     const int nb = mfadd_dec_block_count(d);
     n_ctrl.assign(static_cast<std::size_t>(rank_), 0);
     mfadd_dec_nctrl(d, n_ctrl.data());
+    n_input.assign(static_cast<std::size_t>(rank_), 0);
+    mfadd_dec_grid_dims(d, n_input.data());
     int degree = 0;
     for (int k = 0; k < rank_; ++k) {
       KnotVector kv;
@@ -477,8 +480,7 @@ class Solver {
   }
   // Host field in, host results out (H2D + solve + D2H).
   SolveResult run(const Field& field, bool want_blocks = true) {
-    if (field.values.size() != Tensor::count(field.dims))
-      throw std::invalid_argument("solve: field values do not match dims");
+    check_field(field);
     SolveResult r;
     r.model.controls = Tensor(dec_.n_ctrl);
     r.global_error = Tensor(field.dims);
@@ -489,6 +491,7 @@ class Solver {
   }
   // Device-resident field (a device pointer on the context's GPU).
   SolveResult run_device(const double* field_dev, const Field& meta, bool want_blocks = false) {
+    if (meta.dims != dec_.n_input) throw std::invalid_argument("solve: field extents disagree with the decomposition");
     SolveResult r;
     mfadd_solve_summary sm{};
     check(mfadd_solve(h_.get(), field_dev, 1, &sm));
@@ -502,6 +505,12 @@ class Solver {
   mfadd_solver* get() const { return h_.get(); }
 
  private:
+  // solver.cpp:333-338: the field must match the decomposition's input extents
+  void check_field(const Field& field) const {
+    if (field.dims != dec_.n_input) throw std::invalid_argument("solve: field extents disagree with the decomposition");
+    if (field.values.size() != Tensor::count(field.dims))
+      throw std::invalid_argument("solve: field values do not match dims");
+  }
   void fill(SolveResult& r, const mfadd_solve_summary& sm, const Field& field, bool want_blocks) const {
     r.converged = sm.converged != 0;
     r.constraint_iterations = sm.constraint_iterations;
@@ -619,6 +628,75 @@ inline Tensor fit_unconstrained(const LocalProblem& problem, Context& ctx = defa
   check(mfadd_fit_unconstrained(ctx.get(), rank, problem.r[0].kv.degree, knots.data(), kn_off.data(), params.data(),
                                 pm_off.data(), lo.data(), hi.data(), problem.q.data(), out.data()));
   return out;
+}
+
+// ResidualStats / residual_error (lsq.hpp:35-41)
+struct ResidualStats {
+  double l2 = 0.0;
+  double linf = 0.0;
+  Tensor pointwise;
+};
+
+inline ResidualStats residual_error(const LocalProblem& problem, const Tensor& controls,
+                                    Context& ctx = default_context()) {
+  const int rank = static_cast<int>(problem.r.size());
+  if (rank == 0 || problem.q.rank() != rank || controls.rank() != rank)
+    throw std::invalid_argument("residual_error: rank mismatch");
+  std::vector<double> knots, params;
+  std::vector<std::int64_t> kn_off{0}, pm_off{0}, lo, hi;
+  for (int d = 0; d < rank; ++d) {
+    const auto& c = problem.r[static_cast<std::size_t>(d)];
+    if (controls.extent(d) != c.col_hi - c.col_lo) throw std::invalid_argument("residual_error: control extents");
+    knots.insert(knots.end(), c.kv.knots.begin(), c.kv.knots.end());
+    params.insert(params.end(), c.params.begin(), c.params.end());
+    kn_off.push_back(static_cast<std::int64_t>(knots.size()));
+    pm_off.push_back(static_cast<std::int64_t>(params.size()));
+    lo.push_back(c.col_lo);
+    hi.push_back(c.col_hi);
+  }
+  ResidualStats st;
+  st.pointwise = Tensor(problem.q.extents());
+  check(mfadd_residual_error(ctx.get(), rank, problem.r[0].kv.degree, knots.data(), kn_off.data(), params.data(),
+                             pm_off.data(), lo.data(), hi.data(), problem.q.data(), controls.data(),
+                             st.pointwise.data(), &st.l2, &st.linf));
+  return st;
+}
+
+// SpanBasis (knots.hpp:39-50)
+struct SpanBasis {
+  int span = 0;
+  int orders = 0;
+  std::vector<double> values;       // p+1 values, N_{span-p..span}
+  std::vector<double> derivatives;  // (orders+1) x (p+1), row 0 = values
+  double deriv(int k, int j) const {
+    return derivatives[static_cast<std::size_t>(k * static_cast<int>(values.size()) + j)];
+  }
+};
+
+// find_span (knots.hpp:36)
+inline int find_span(const KnotVector& kv, double u, Context& ctx = default_context()) {
+  std::vector<double> v(static_cast<std::size_t>(kv.degree + 1));
+  int span = 0;
+  check(mfadd_basis_funs(ctx.get(), kv.knots.data(), static_cast<int>(kv.knots.size()), kv.degree, 1, &u, nullptr, 0,
+                         &span, v.data()));
+  return span;
+}
+
+// basis_derivs (knots.hpp:56); basis_funs (knots.hpp:53) is its k = 0 row
+inline SpanBasis basis_derivs(const KnotVector& kv, int span, double u, int k, Context& ctx = default_context()) {
+  SpanBasis b;
+  b.span = span;
+  b.orders = k;
+  const std::size_t w = static_cast<std::size_t>(kv.degree + 1);
+  b.derivatives.resize(w * static_cast<std::size_t>(k + 1));
+  int sp = span;
+  check(mfadd_basis_funs(ctx.get(), kv.knots.data(), static_cast<int>(kv.knots.size()), kv.degree, 1, &u, &span, k,
+                         &sp, b.derivatives.data()));
+  b.values.assign(b.derivatives.begin(), b.derivatives.begin() + static_cast<std::ptrdiff_t>(w));
+  return b;
+}
+inline SpanBasis basis_funs(const KnotVector& kv, int span, double u, Context& ctx = default_context()) {
+  return basis_derivs(kv, span, u, 0, ctx);
 }
 
 // decode (decode.hpp:20-22)

@@ -281,6 +281,8 @@ def solve(dec: RefDecomposition, values, max_outer_iterations=10, tolerance=1e-1
         ints = np.zeros(4, np.int32)
         dbl = np.zeros(8, np.float64)
         L.ref_result_scalars(h, _ptr(ints, _ip), _ptr(dbl, _dp))
+        L.ref_last_solve_seconds.restype = C.c_double
+        solve_s = float(L.ref_last_solve_seconds())
         ep = np.zeros((int(ints[2]), 4), np.float64)
         L.ref_result_epochs(h, _ptr(ep, _dp))
         fj = np.zeros((int(ints[3]), 4), np.float64)
@@ -306,7 +308,7 @@ def solve(dec: RefDecomposition, values, max_outer_iterations=10, tolerance=1e-1
         return RefSolveResult(bool(ints[0]), int(ints[1]), float(dbl[0]), float(dbl[1]), float(dbl[2]), ep, fj,
                               ctrl, err, blocks,
                               dict(setup=dbl[3], local_solve=dbl[4], exchange=dbl[5], constraint=dbl[6],
-                                   decode=dbl[7]), berr)
+                                   decode=dbl[7], solve_s=solve_s), berr)
     finally:
         L.ref_result_free(h)
 

@@ -11,6 +11,7 @@
 //   0 ok, 1 std::invalid_argument, 2 std::out_of_range, 3 SingularFitError,
 //   4 std::runtime_error, 5 std::logic_error, 9 anything else.
 #include <cstdint>
+#include <chrono>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -304,6 +305,8 @@ double ref_dec_compression_ratio(void* h) { return compression_ratio(static_cast
 int ref_dec_any_shared(void* h) { return static_cast<RefDec*>(h)->dec.shared.any_shared() ? 1 : 0; }
 
 // ---- solver.hpp: solve --------------------------------------------------
+static double g_last_solve_s = 0.0;
+
 int ref_solve(void* dec_handle, const double* field_values, const double* bounds, int max_outer_iterations,
               double tolerance, int workers, int log_errors, int enforce_continuity, void** out_result) {
   return guarded([&] {
@@ -321,10 +324,17 @@ int ref_solve(void* dec_handle, const double* field_values, const double* bounds
     cfg.log_errors = log_errors != 0;
     cfg.enforce_continuity = enforce_continuity != 0;
     auto r = std::make_unique<RefResult>();
+    // the timed region is mfadd::solve() only (the Field
+    // build above and the result copies afterwards are outside it)
+    const auto t0 = std::chrono::steady_clock::now();
     r->res = solve(f, dec, cfg);
+    g_last_solve_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     *out_result = r.release();
   });
 }
+
+// Wall seconds of the last ref_solve's solve() call (steady_clock).
+double ref_last_solve_seconds(void) { return g_last_solve_s; }
 
 void ref_result_free(void* h) { delete static_cast<RefResult*>(h); }
 

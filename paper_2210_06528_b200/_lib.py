@@ -66,6 +66,7 @@ _SIGS = {
     "mfadd_dec_exchange_volume": (None, [C.c_void_p, c_lp]),
     "mfadd_dec_compression_ratio": (C.c_double, [C.c_void_p]),
     "mfadd_dec_any_shared": (C.c_int, [C.c_void_p]),
+    "mfadd_dec_grid_dims": (None, [C.c_void_p, c_lp]),
     "mfadd_context_create": (C.c_int, [C.c_int, C.c_void_p, C.POINTER(C.c_void_p)]),
     "mfadd_context_free": (None, [C.c_void_p]),
     "mfadd_context_launch_count": (C.c_int64, [C.c_void_p]),
@@ -89,6 +90,9 @@ _SIGS = {
                                     c_lp, c_ip, c_dp]),
     "mfadd_fit_unconstrained": (C.c_int, [C.c_void_p, C.c_int, C.c_int, c_dp, c_lp, c_dp, c_lp, c_lp, c_lp, c_dp,
                                           c_dp]),
+    "mfadd_residual_error": (C.c_int, [C.c_void_p, C.c_int, C.c_int, c_dp, c_lp, c_dp, c_lp, c_lp, c_lp, c_dp, c_dp,
+                                       c_dp, c_dp, c_dp]),
+    "mfadd_basis_funs": (C.c_int, [C.c_void_p, c_dp, C.c_int, C.c_int, C.c_int64, c_dp, c_ip, C.c_int, c_ip, c_dp]),
     "mfadd_decode": (C.c_int, [C.c_void_p, C.c_int, C.c_int, c_dp, c_lp, c_dp, c_lp, c_lp, c_lp, c_dp, c_dp]),
     "mfadd_eval_points": (C.c_int, [C.c_void_p, C.c_int, c_ip, c_dp, c_lp, c_lp, c_lp, c_dp, C.c_int64, c_dp, c_ip,
                                     C.c_int, C.c_int, c_dp]),

@@ -207,10 +207,50 @@ def collocation_matrix(kv: KnotVector, params, col_lo: int = 0, col_hi: Optional
 
 
 def find_span(kv: KnotVector, u: float, ctx: Optional[Context] = None) -> int:
-    """find_span (knots.hpp:36) via a one-row collocation on the GPU."""
-    bc = collocation_matrix(kv, [u], 0, kv.basis_count(), ctx)
-    return int(bc.first_col[0]) + kv.degree if bc.count[0] == kv.degree + 1 else \
-        int(bc.first_col[0]) + int(bc.count[0]) - 1
+    """find_span (knots.hpp:36) on the GPU (mfadd_basis_funs)."""
+    return basis_funs_batch(kv, [u], ctx=ctx)[0][0]
+
+
+@dataclass
+class SpanBasis:
+    """SpanBasis (knots.hpp:39-50): span, p+1 values, (orders+1) x (p+1) derivative rows (row 0 = values)."""
+    span: int
+    orders: int
+    values: np.ndarray
+    derivatives: np.ndarray
+
+    def deriv(self, k, j):
+        return float(self.derivatives[k, j])
+
+
+def basis_funs_batch(kv: KnotVector, us, spans=None, orders: int = 0, ctx: Optional[Context] = None):
+    """find_span + basis_funs / basis_derivs for many parameters in one GPU call:
+    returns (spans[n], values[n, orders+1, p+1])."""
+    ctx = ctx or default_context()
+    kn = np.ascontiguousarray(kv.knots, np.float64)
+    u = np.ascontiguousarray(us, np.float64).reshape(-1)
+    n = len(u)
+    out = np.zeros((n, orders + 1, kv.degree + 1), np.float64)
+    sp_out = np.zeros(n, np.int32)
+    sp_in = None if spans is None else np.ascontiguousarray(spans, np.int32).reshape(-1)
+    if sp_in is not None and len(sp_in) != n:
+        raise InvalidArgument("basis_funs: spans and parameters differ in length")
+    _check(L.load().mfadd_basis_funs(ctx._h, _dp(kn), len(kn), kv.degree, n, _dp(u),
+                                     None if sp_in is None else _ip(sp_in), orders, _ip(sp_out), _dp(out)))
+    return [int(x) for x in sp_out], out
+
+
+def basis_funs(kv: KnotVector, span: int, u: float, ctx: Optional[Context] = None) -> SpanBasis:
+    """basis_funs (knots.hpp:53): Cox-de Boor values at `span` (a neighbouring
+    span gives the one-sided polynomial piece)."""
+    sp, v = basis_funs_batch(kv, [u], spans=[span], ctx=ctx)
+    return SpanBasis(sp[0], 0, v[0, 0].copy(), v[0].copy())
+
+
+def basis_derivs(kv: KnotVector, span: int, u: float, k: int, ctx: Optional[Context] = None) -> SpanBasis:
+    """basis_derivs (knots.hpp:56): derivative rows 0..k (row 0 = basis_funs)."""
+    sp, v = basis_funs_batch(kv, [u], spans=[span], orders=k, ctx=ctx)
+    return SpanBasis(sp[0], k, v[0, 0].copy(), v[0].copy())
 
 
 # ------------------------------------------------------------------ lsq / decode
@@ -249,6 +289,38 @@ def fit_unconstrained(problem: LocalProblem, ctx: Optional[Context] = None) -> n
     _check(L.load().mfadd_fit_unconstrained(ctx._h, len(problem.kvs), degree, _dp(kn), _lp(ko), _dp(pm), _lp(po),
                                             _lp(lo), _lp(hi), _dp(q), _dp(out)))
     return out
+
+
+@dataclass
+class ResidualStats:
+    """ResidualStats (lsq.hpp:35-39)."""
+    l2: float
+    linf: float
+    pointwise: Optional[np.ndarray]
+
+
+def residual_error(problem: LocalProblem, controls, want_pointwise: bool = True,
+                   ctx: Optional[Context] = None) -> ResidualStats:
+    """residual_error (lsq.hpp:41, lsq.cpp:66-85) on the GPU: decode of the
+    window-clipped rows, pointwise q - decode bitwise equal to the reference."""
+    ctx = ctx or default_context()
+    degree = problem.kvs[0].degree
+    kn, ko, pm, po = _pack(problem.kvs, problem.params)
+    lo = np.array([w[0] for w in problem.windows], np.int64)
+    hi = np.array([w[1] for w in problem.windows], np.int64)
+    q = np.ascontiguousarray(problem.q, np.float64)
+    if q.shape != tuple(len(p) for p in problem.params):
+        raise InvalidArgument("LocalProblem: row count mismatch")
+    c = np.ascontiguousarray(controls, np.float64)
+    if c.shape != tuple(int(h - l) for l, h in zip(lo, hi)):
+        raise InvalidArgument("residual_error: control extents do not match the column windows")
+    pw = np.zeros(q.shape, np.float64) if want_pointwise else None
+    l2 = C.c_double()
+    li = C.c_double()
+    _check(L.load().mfadd_residual_error(ctx._h, len(problem.kvs), degree, _dp(kn), _lp(ko), _dp(pm), _lp(po),
+                                         _lp(lo), _lp(hi), _dp(q), _dp(c), None if pw is None else _dp(pw),
+                                         C.byref(l2), C.byref(li)))
+    return ResidualStats(l2.value, li.value, pw)
 
 
 def decode(controls, kvs: Sequence[KnotVector], params, col_offset=None, ctx: Optional[Context] = None):
@@ -872,37 +944,75 @@ class Solver:
         except Exception:
             pass
 
-    # field: numpy array (host) or an object with data_ptr() on the device
+    # Buffer checks before any pointer crosses the C ABI (the ABI takes plain
+    # pointers and sizes; the reference throws invalid_argument for a field
+    # whose extents disagree with the decomposition, solver.cpp:335-338).
+    def _buf(self, a, n, what, device, shape=None):
+        """Address of a float64, C-contiguous buffer of n elements on the right side
+        (a multi-dimensional buffer must also have `shape`, e.g. the grid extents)."""
+        sh = getattr(a, "shape", None)
+        if shape is not None and sh is not None and len(sh) > 1 and tuple(int(x) for x in sh) != tuple(shape):
+            raise InvalidArgument("solve: field extents disagree with the decomposition")
+        if isinstance(a, np.ndarray):
+            if device:
+                raise InvalidArgument(f"{what}: expected a device buffer, got a host numpy array")
+            if a.dtype != np.float64 or not a.flags["C_CONTIGUOUS"]:
+                raise InvalidArgument(f"{what}: expected a C-contiguous float64 array")
+            if a.size != n:
+                raise InvalidArgument(f"{what}: {a.size} elements, expected {n}")
+            return a.ctypes.data
+        dt = getattr(a, "dtype", None)
+        if dt is not None and str(dt) not in ("torch.float64", "float64"):
+            raise InvalidArgument(f"{what}: expected float64, got {dt}")
+        if hasattr(a, "is_contiguous") and not a.is_contiguous():
+            raise InvalidArgument(f"{what}: expected a contiguous tensor")
+        numel = a.numel() if hasattr(a, "numel") else None
+        if numel is not None and numel != n:
+            raise InvalidArgument(f"{what}: {numel} elements, expected {n}")
+        is_cuda = getattr(a, "is_cuda", None)
+        if is_cuda is not None and bool(is_cuda) != bool(device):
+            raise InvalidArgument(f"{what}: expected a {'device' if device else 'host'} buffer")
+        if device and is_cuda and getattr(a, "device", None) is not None and a.device.index not in (None, self.ctx.device):
+            raise InvalidArgument(f"{what}: tensor on cuda:{a.device.index}, solver on cuda:{self.ctx.device}")
+        return a.data_ptr()
+
+    def _field_n(self):
+        return self.dec.total_inputs()
+
+    def _ctrl_n(self):
+        return int(np.prod(self.dec.n_ctrl))
+
+    # field: numpy array (host) or a torch tensor (host or, with on_device, device)
     def run(self, values, on_device: bool = False):
         lib = L.load()
         if on_device:
-            _check(lib.mfadd_solve(self._h, C.c_void_p(values.data_ptr()), 1, C.byref(self.summary)))
+            ptr = self._buf(values, self._field_n(), "solve: field", True, self.dec.grid_dims)
+            _check(lib.mfadd_solve(self._h, C.c_void_p(ptr), 1, C.byref(self.summary)))
         else:
             v = np.ascontiguousarray(values, np.float64)
-            if v.size != self.dec.total_inputs():
+            if v.size != self.dec.total_inputs() or (v.ndim > 1 and v.shape != tuple(self.dec.grid_dims)):
                 raise InvalidArgument("solve: field extents disagree with the decomposition")
             _check(lib.mfadd_solve(self._h, v.ctypes.data_as(C.c_void_p), 0, C.byref(self.summary)))
         return self.summary
 
     def run_host(self, values, out_controls, out_error=None):
         """mfadd_solve_host: H2D + solve + D2H in one call (the e2e path)."""
-        _check(L.load().mfadd_solve_host(
-            self._h, C.c_void_p(values.ctypes.data if isinstance(values, np.ndarray) else values.data_ptr()),
-            C.c_void_p(out_controls.ctypes.data if isinstance(out_controls, np.ndarray) else out_controls.data_ptr()),
-            None if out_error is None else C.c_void_p(out_error.ctypes.data if isinstance(out_error, np.ndarray)
-                                                      else out_error.data_ptr()),
-            C.byref(self.summary)))
+        fp = self._buf(values, self._field_n(), "solve: field", False, self.dec.grid_dims)
+        cp = self._buf(out_controls, self._ctrl_n(), "solve: out_controls", False)
+        ep = None if out_error is None else C.c_void_p(self._buf(out_error, self._field_n(), "solve: out_error", False))
+        _check(L.load().mfadd_solve_host(self._h, C.c_void_p(fp), C.c_void_p(cp), ep, C.byref(self.summary)))
         return self.summary
 
     def run_host_batch(self, fields, out_controls, out_errors=None):
         """mfadd_solve_host_batch: a stream of solves on host buffers with the
         copies of neighbouring steps overlapped.  Returns the n summaries."""
-        def ptr(a):
-            return a.ctypes.data if isinstance(a, np.ndarray) else a.data_ptr()
         n = len(fields)
-        fp = (C.c_void_p * n)(*[ptr(f) for f in fields])
-        cp = (C.c_void_p * n)(*[ptr(o) for o in out_controls])
-        ep = None if out_errors is None else (C.c_void_p * n)(*[ptr(o) for o in out_errors])
+        if len(out_controls) != n or (out_errors is not None and len(out_errors) != n):
+            raise InvalidArgument("solve_host_batch: fields and outputs differ in length")
+        fp = (C.c_void_p * n)(*[self._buf(f, self._field_n(), "solve: field", False, self.dec.grid_dims) for f in fields])
+        cp = (C.c_void_p * n)(*[self._buf(o, self._ctrl_n(), "solve: out_controls", False) for o in out_controls])
+        ep = None if out_errors is None else \
+            (C.c_void_p * n)(*[self._buf(o, self._field_n(), "solve: out_error", False) for o in out_errors])
         sums = (L.SolveSummaryC * n)()
         _check(L.load().mfadd_solve_host_batch(self._h, n, fp, cp, ep, sums))
         self.summary = sums[n - 1]

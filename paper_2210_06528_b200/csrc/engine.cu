@@ -751,6 +751,11 @@ struct mfadd_solver {
   // log_errors: per-epoch block residuals
   DBuf<double> res_partial, block_errs;
   int res_ntile = 0, res_max_m0 = 0;
+  // one-pass form (residual_tma.cu): epoch snapshots of the shared copies,
+  // every epoch's residuals after the loop
+  bool res_snap = false;
+  DBuf<double> snap, res_part2;
+  int res_W = 0, res_ntc = 0, res_nrr = 1, res_threads = 0, res_ltcap = 0, res_nacap = 0, res_eg = 1;
   std::vector<double> h_block_errs;
   // shard: rank of nranks owns blocks [srange.blo, srange.bhi)
   int rank = 0, nranks = 1;
@@ -870,6 +875,9 @@ MFB_API double mfadd_dec_compression_ratio(const mfadd_decomposition* dec) {
   return static_cast<double>(dec->d.total_inputs()) / static_cast<double>(dec->d.total_ctrl());
 }
 MFB_API int mfadd_dec_any_shared(const mfadd_decomposition* dec) { return dec->d.any_shared ? 1 : 0; }
+MFB_API void mfadd_dec_grid_dims(const mfadd_decomposition* dec, int64_t* out) {
+  for (int k = 0; k < dec->d.rank; ++k) out[k] = dec->d.grid[k];
+}
 
 // ---------------------------------------------------------------- context
 MFB_API int mfadd_context_create(int device, void* stream, mfadd_context** out) {
@@ -946,6 +954,8 @@ mfb::EpochRegionArgs region_args(mfadd_solver* s, int mode) {
   a.tol = s->cfg.tolerance;
   a.max_ns = s->max_holders;
   a.finalize = 1;  // the last CTA computes dp (and ends the graph loop)
+  a.snap = s->res_snap ? s->snap.p : nullptr;
+  a.snap_stride = s->wl.total_p;
   return a;
 }
 
@@ -972,9 +982,54 @@ mfb::BlockResArgs res_args(mfadd_solver* s, const double* dfield, const mfb::Epo
   return a;
 }
 
+// record_epoch's block residuals (solver.cpp:357-364) of every recorded
+// epoch in one pass after the loop (snapshot form; st->iter + 1 epochs).
+int launch_residuals_all(mfadd_solver* s, const double* dfield, cudaStream_t cs) {
+  const Decomp& d = s->dec;
+  const Workload& wl = s->wl;
+  mfb::ResTmaArgs a{};
+  a.D = d.rank;
+  a.nblocks = static_cast<int>(wl.blocks.size());
+  a.blocks = wl.d_blocks.p;
+  a.probs = wl.d_probs.p;
+  a.g0 = wl.g0.p;
+  a.vals = wl.vals.p;
+  a.P = wl.P.p;
+  a.snap = s->snap.p;
+  a.snap_stride = wl.total_p;
+  a.sflag = wl.sflag.p;
+  for (int k = 0; k < 3; ++k) a.sflag_off[k] = wl.sflag_off[k];
+  a.st = s->est.p;
+  a.W = s->res_W;
+  a.ntc = s->res_ntc;
+  a.nrr = s->res_nrr;
+  a.lt_cap = s->res_ltcap;
+  a.na_cap = s->res_nacap;
+  a.eg = s->res_eg;
+  a.partial = s->res_part2.p;
+  a.errs = s->block_errs.p;
+  a.nglobal = d.nblocks;
+  a.boff = s->srange.blo;
+  std::uint64_t dims[3];
+  std::uint32_t box[3];
+  for (int k = 0; k < d.rank; ++k) dims[k] = static_cast<std::uint64_t>(d.grid[d.rank - 1 - k]);
+  box[0] = static_cast<std::uint32_t>(s->res_W);
+  if (d.rank == 2) {
+    box[1] = 8u;
+  } else {
+    box[1] = 1u;
+    box[2] = 8u;
+  }
+  const CUtensorMap map = make_tmap(dfield, d.rank, dims, box);
+  s->tl.begin("residual");
+  const int l = mfb::launch_residual_tma(wl.p, a, map, s->res_threads, cs);
+  s->tl.end();
+  return l;
+}
+
 // record_epoch's block residuals (solver.cpp:357-364) when log_errors.
 int launch_residuals(mfadd_solver* s, const double* dfield, const mfb::EpochState* st, int slot, cudaStream_t cs) {
-  if (!s->cfg.log_errors) return 0;
+  if (!s->cfg.log_errors || s->res_snap) return 0;
   s->tl.begin("residual");
   const int l = mfb::launch_block_residual(s->wl.p, res_args(s, dfield, st, slot), cs);
   s->tl.end();
@@ -1134,7 +1189,7 @@ void build_loop_graph(mfadd_solver* s, const double* dfield) {
   mfb::EpochRegionArgs a = region_args(s, -1);
   a.cond = static_cast<unsigned long long>(h);
   mfb::launch_epoch_regions(a, cs);
-  if (s->cfg.log_errors) mfb::launch_block_residual(s->wl.p, res_args(s, dfield, s->est.p, 0), cs);
+  if (s->cfg.log_errors && !s->res_snap) mfb::launch_block_residual(s->wl.p, res_args(s, dfield, s->est.p, 0), cs);
   CK(cudaStreamEndCapture(cs, &body));
   CK(cudaGraphInstantiate(&s->loop_exec, s->loop_graph, 0));
 }
@@ -1171,7 +1226,7 @@ void add_loop_node(mfadd_solver* s, cudaStream_t st, const double* dfield, cudaG
   mfb::EpochRegionArgs a = region_args(s, -1);
   a.cond = static_cast<unsigned long long>(h);
   mfb::launch_epoch_regions(a, bs);
-  if (s->cfg.log_errors) mfb::launch_block_residual(s->wl.p, res_args(s, dfield, s->est.p, 0), bs);
+  if (s->cfg.log_errors && !s->res_snap) mfb::launch_block_residual(s->wl.p, res_args(s, dfield, s->est.p, 0), bs);
   CK(cudaStreamEndCapture(bs, &body));
   CK(cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies));
 }
@@ -1180,6 +1235,101 @@ void add_loop_node(mfadd_solver* s, cudaStream_t st, const double* dfield, cudaG
 
 // ---------------------------------------------------------------- solver
 namespace {
+
+// Geometry of the one-pass residual kernel (residual_tma.cu): column tiles
+// (D = 2) or rows j1 (D = 3) x row ranges per block, and the exact sizes of
+// the staged windows (planes per row range, window columns per CTA) computed
+// from the same spans the device row tables hold.  Picks the most epochs per
+// pass (4, 2, 1) whose staging fits the shared-memory budget.
+void plan_residual_tma(mfadd_solver* s) {
+  const Decomp& d = s->dec;
+  Workload& wl = s->wl;
+  const int D = d.rank, p = d.degree;
+  auto g0_of = [&](const AxisProb& pr, int j) {  // the device row table's g0 (span - p - col_lo)
+    const double u = static_cast<double>(pr.in_lo + j) / static_cast<double>(pr.M - 1);
+    return host_find_span(d.knots[static_cast<std::size_t>(pr.dim)], p, u) - p - static_cast<int>(pr.col_lo);
+  };
+  int mxm1 = 0, mxm2 = 0, mnm0 = 1 << 30;
+  for (const auto& b : wl.blocks) {
+    mnm0 = std::min(mnm0, wl.probs[static_cast<std::size_t>(b.ax[0])].m);
+    mxm1 = std::max(mxm1, wl.probs[static_cast<std::size_t>(b.ax[1])].m);
+    if (D == 3) mxm2 = std::max(mxm2, wl.probs[static_cast<std::size_t>(b.ax[2])].m);
+  }
+  int cols = 0;
+  if (D == 2) {  // column tiles of W - 2 columns (W <= 256: the TMA box limit)
+    const int nt = (mxm1 + 253) / 254;
+    cols = round_up((mxm1 + nt - 1) / nt, 2);
+    s->res_W = cols + 2;
+    s->res_ntc = (mxm1 + cols - 1) / cols;
+  } else {  // one row j1 per CTA, the block's whole axis-2 extent in one box
+    s->res_W = round_up(mxm2 + 1, 2);
+    s->res_ntc = mxm1;
+    if (s->res_W > 256) return;
+  }
+  // widest lattice window of a CTA (distinct axis problems only)
+  int ltc = 1;
+  std::vector<char> seen(wl.probs.size(), 0);
+  for (const auto& b : wl.blocks) {
+    const int pid = b.ax[D == 2 ? 1 : 2];
+    if (seen[static_cast<std::size_t>(pid)]) continue;
+    seen[static_cast<std::size_t>(pid)] = 1;
+    const AxisProb& pr = wl.probs[static_cast<std::size_t>(pid)];
+    if (D == 2) {
+      for (int jf = 0; jf < pr.m; jf += cols)
+        ltc = std::max(ltc, g0_of(pr, std::min(pr.m - 1, jf + cols - 1)) - g0_of(pr, jf) + p + 1);
+    } else {
+      ltc = std::max(ltc, g0_of(pr, pr.m - 1) - g0_of(pr, 0) + p + 1);
+    }
+  }
+  s->res_ltcap = ltc;
+  s->res_threads = round_up(s->res_W, 32);
+  // planes touched by one row range (distinct axis-0 problems), per nrr
+  auto na_for = [&](int nrr) {
+    int na = 1;
+    std::vector<char> seen0(wl.probs.size(), 0);
+    for (const auto& b : wl.blocks) {
+      const int pid = b.ax[0];
+      if (seen0[static_cast<std::size_t>(pid)]) continue;
+      seen0[static_cast<std::size_t>(pid)] = 1;
+      const AxisProb& pr = wl.probs[static_cast<std::size_t>(pid)];
+      const int nch = (pr.m + 7) / 8, cpr = (nch + nrr - 1) / nrr;
+      for (int c0 = 0; c0 < nch; c0 += cpr) {
+        const int y0 = c0 * 8, y1 = std::min(pr.m, (c0 + cpr) * 8);
+        const int lo = std::min(std::max(g0_of(pr, y0), 0), pr.n - 1);
+        const int hi = std::min(std::max(g0_of(pr, y1 - 1) + p, 0), pr.n - 1);
+        na = std::max(na, hi - lo + 1);
+      }
+    }
+    return na;
+  };
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->ctx->device);
+  const std::int64_t ctas = static_cast<std::int64_t>(s->res_ntc) * static_cast<std::int64_t>(wl.blocks.size());
+  const int want = static_cast<int>((6LL * sms + ctas - 1) / ctas);  // ~6 CTAs of work per SM
+  const int maxr = std::max(1, (mnm0 / 8) / 4);                     // >= 4 chunks per row range
+  const std::size_t budget = static_cast<std::size_t>(env_int("MFADD_RES_SMEM_KB", 110)) * 1024;
+  const int eg_force = env_int("MFADD_RES_EG", 0), nrr_force = env_int("MFADD_RES_NRR", 0);
+  bool ok = false;
+  for (int eg : {4, 2, 1}) {
+    if (eg_force && eg != eg_force) continue;
+    for (int nrr = std::max(1, std::min(want, maxr)); nrr <= std::max(maxr, 1) && !ok; ++nrr) {
+      if (nrr_force && nrr != nrr_force) continue;
+      const int na = na_for(nrr);
+      if (mfb::residual_tma_smem(p, s->res_W, eg, na, s->res_ltcap) <= budget) {
+        s->res_eg = eg;
+        s->res_nrr = nrr;
+        s->res_nacap = na;
+        ok = true;
+      }
+    }
+    if (ok) break;
+  }
+  if (!ok) return;  // the per-epoch kernels stay
+  s->res_snap = true;
+  s->snap.alloc(static_cast<std::size_t>(s->cfg.max_outer_iterations + 1) * static_cast<std::size_t>(wl.total_p));
+  s->res_part2.alloc(static_cast<std::size_t>(s->cfg.max_outer_iterations + 1) * wl.blocks.size() *
+                     static_cast<std::size_t>(s->res_ntc) * s->res_nrr * 2);
+}
 
 // Solver construction for rank `rank` of `nranks` (1: the whole decomposition).
 std::unique_ptr<mfadd_solver> create_solver(mfadd_context* ctx, const mfadd_decomposition* dech,
@@ -1468,7 +1618,6 @@ std::unique_ptr<mfadd_solver> create_solver(mfadd_context* ctx, const mfadd_deco
       if (s->max_holders > 8)
         throw std::invalid_argument("mfadd_b200: a sharded solve needs at most two holders per axis");
     }
-    if (nranks == 1 && s->ntiles > 0 && cfg->enforce_continuity) build_loop_graph(s.get(), nullptr);
     s->hres_eo = 4;
     s->hres_es = s->hres_eo + s->epoch_out.n;
     s->hres_pj = s->hres_es + (sizeof(mfb::EpochState) + 7) / 8;
@@ -1483,10 +1632,17 @@ std::unique_ptr<mfadd_solver> create_solver(mfadd_context* ctx, const mfadd_deco
         for (int k = 1; k < D; ++k) tr *= wl.probs[static_cast<std::size_t>(b.ax[k])].m;
         mx = std::max(mx, D == 1 ? m0 : tr);
       }
-      s->res_ntile = std::min(4096, (mx + 127) / 128);
+      s->res_ntile = (mx + 127) / 128;  // one thread per trailing point (no cap: every point is counted)
       s->res_partial.alloc(wl.blocks.size() * static_cast<std::size_t>(s->res_ntile) * 2);
       s->block_errs.alloc(static_cast<std::size_t>(cfg->max_outer_iterations + 1) * d.nblocks * 2);
+      // one-pass snapshot form (residual_tma.cu) where the epochs run as
+      // region kernels on one device and the field rows are 16-B aligned
+      const bool regions_ok = s->ntiles > 0 || !d.any_shared;
+      if (D >= 2 && nranks == 1 && regions_ok && d.grid[D - 1] % 2 == 0 && !std::getenv("MFADD_RES_LEGACY"))
+        plan_residual_tma(s.get());
     }
+    // (after the log_errors plan: the loop body writes the epoch snapshots)
+    if (nranks == 1 && s->ntiles > 0 && cfg->enforce_continuity) build_loop_graph(s.get(), nullptr);
     CK(cudaStreamSynchronize(st));
     return s;
 }
@@ -1735,7 +1891,7 @@ int enqueue_solve(mfadd_solver* s, const double* dfield) {
       s->tl.begin("epoch");
       launches += mfb::launch_epoch_regions(b, st);
       s->tl.end();
-      if (s->cfg.log_errors) {
+      if (s->cfg.log_errors && !s->res_snap) {
         mfb::BlockResArgs ra = res_args(s, dfield, s->est.p, 0);
         ra.expect_iter = 2 + u;  // skipped with its epoch
         launches += mfb::launch_block_residual(s->wl.p, ra, st);
@@ -1760,11 +1916,13 @@ int enqueue_solve(mfadd_solver* s, const double* dfield) {
     if (captured)
       add_loop_node(s, st, dfield, make_loop_handle(st));
     else {
-      if (!s->loop_exec || (s->cfg.log_errors && s->loop_field != dfield)) build_loop_graph(s, dfield);
+      if (!s->loop_exec || (s->cfg.log_errors && !s->res_snap && s->loop_field != dfield)) build_loop_graph(s, dfield);
       CK(cudaGraphLaunch(s->loop_exec, st));
     }
     s->tl.end();
   }
+  // ---- every epoch's block residuals in one pass (log_errors, snapshot form)
+  if (s->cfg.log_errors && s->res_snap) launches += launch_residuals_all(s, dfield, st);
   CK(cudaEventRecord(s->ev[3], st));
   // ---- final jumps per neighbour pair (solver.cpp:416).  After a mode-2
   // epoch all copies of each control are bit-identical and every per-pair
@@ -2132,6 +2290,12 @@ void solve_group(std::vector<mfadd_solver*>& g, const std::vector<const double*>
     }
   }
   tmark("jumps", 0);
+  if (s0->cfg.log_errors && s0->res_snap && g.size() == 1) {  // the host-driven loop of one device
+    mfb::EpochState es{};
+    es.iter = last;
+    CK(cudaMemcpyAsync(s0->est.p, &es, sizeof es, cudaMemcpyHostToDevice, s0->ctx->stream));
+    launches[0] += launch_residuals_all(s0, fields[0], s0->ctx->stream);
+  }
   for (std::size_t r = 0; r < g.size(); ++r) launches[r] += shard_assemble_decode(g[r], fields[r]);
   tr.gather_lattice(g);
   tmark("assembled", 0);
@@ -2647,6 +2811,87 @@ MFB_API int mfadd_fit_unconstrained(mfadd_context* ctx, int rank, int degree, co
     CK(cudaMemcpyAsync(out_p, wl.P.p, static_cast<std::size_t>(wl.total_p) * sizeof(double), cudaMemcpyDeviceToHost,
                        st));
     CK(cudaStreamSynchronize(st));
+  });
+}
+
+MFB_API int mfadd_residual_error(mfadd_context* ctx, int rank, int degree, const double* knots, const int64_t* kn_off,
+                                 const double* params, const int64_t* pm_off, const int64_t* col_lo,
+                                 const int64_t* col_hi, const double* q, const double* controls,
+                                 double* out_pointwise, double* out_l2, double* out_linf) {
+  return guarded([&] {
+    ContextScope scope(ctx);
+    if (rank < 1 || rank > 3) throw std::invalid_argument("residual_error: rank must be 1..3");
+    if (degree < 1 || degree > mfb::kMaxDegree) throw std::invalid_argument("residual_error: unsupported degree");
+    Workload wl;
+    wl.D = rank;
+    wl.p = degree;
+    std::int64_t qn = 1, pn = 1;
+    for (int k = 0; k < rank; ++k) {
+      const std::int64_t m = pm_off[k + 1] - pm_off[k];
+      check_params_ascending(params + pm_off[k], m);
+      check_window(static_cast<int>(kn_off[k + 1] - kn_off[k]), degree, col_lo[k], col_hi[k]);
+      AxisProb pr{};
+      pr.dim = k;
+      pr.m = static_cast<int>(m);
+      pr.n = static_cast<int>(col_hi[k] - col_lo[k]);
+      pr.col_lo = col_lo[k];
+      pr.M = -1;
+      pr.param_off = pm_off[k];
+      pr.knot_off = kn_off[k];
+      pr.nknots = static_cast<int>(kn_off[k + 1] - kn_off[k]);
+      wl.probs.push_back(pr);
+      qn *= m;
+      pn *= pr.n;
+    }
+    wl.layout_tables();
+    cudaStream_t st = ctx->stream;
+    wl.d_probs.upload(wl.probs, st);
+    wl.knots.upload(std::vector<double>(knots, knots + kn_off[rank]), st);
+    wl.params.upload(std::vector<double>(params, params + pm_off[rank]), st);
+    wl.g0.alloc(static_cast<std::size_t>(wl.total_rows));
+    wl.first_col.alloc(static_cast<std::size_t>(wl.total_rows));
+    wl.count.alloc(static_cast<std::size_t>(wl.total_rows));
+    wl.vals.alloc(static_cast<std::size_t>(wl.total_rows) * (degree + 1));
+    mfb::RowsArgs ra{wl.d_probs.p, rank, wl.max_m, wl.knots.p, wl.params.p, wl.g0.p, wl.first_col.p, wl.count.p,
+                     wl.vals.p, ctx->d_status};
+    ctx->launches += mfb::launch_basis_rows(degree, ra, st);
+    DBuf<double> dq, dp, dout, dpart, dred;
+    dq.upload(std::vector<double>(q, q + qn), st);
+    dp.upload(std::vector<double>(controls, controls + pn), st);
+    if (out_pointwise) dout.alloc(static_cast<std::size_t>(qn));
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+    const int ctas = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>((qn + 255) / 256, 8 * sms)));
+    dpart.alloc(static_cast<std::size_t>(ctas) * 2);
+    dred.alloc(2);
+    mfb::ResidualArgs a{};
+    a.D = rank;
+    for (int k = 0; k < 3; ++k) {
+      const int kk = k < rank ? k : 0;
+      const AxisProb& pr = wl.probs[static_cast<std::size_t>(kk)];
+      a.m[k] = k < rank ? pr.m : 1;
+      a.n[k] = k < rank ? pr.n : 1;
+      a.g0[k] = wl.g0.p + pr.row_off;
+      a.vals[k] = wl.vals.p + pr.row_off * (degree + 1);
+    }
+    a.controls = dp.p;
+    a.q = dq.p;
+    a.pointwise = out_pointwise ? dout.p : nullptr;
+    a.partial = dpart.p;
+    a.total = qn;
+    ctx->launches += mfb::launch_residual_points(degree, a, ctas, st);
+    ctx->launches += mfb::launch_reduce_partials(dpart.p, ctas, dred.p, st);
+    CK(cudaGetLastError());
+    const mfb::DevStatus stt = read_status(ctx);
+    wl.raise_status(stt, "");
+    double red[2] = {0.0, 0.0};
+    CK(cudaMemcpyAsync(red, dred.p, sizeof red, cudaMemcpyDeviceToHost, st));
+    if (out_pointwise)
+      CK(cudaMemcpyAsync(out_pointwise, dout.p, static_cast<std::size_t>(qn) * sizeof(double), cudaMemcpyDeviceToHost,
+                         st));
+    CK(cudaStreamSynchronize(st));
+    if (out_l2) *out_l2 = std::sqrt(red[0]);
+    if (out_linf) *out_linf = red[1];
   });
 }
 

@@ -1009,9 +1009,9 @@ __device__ __forceinline__ void divmod_nb(int n, int d, float rcp, int& q, int& 
 // arithmetic, and for FLAT boxes (ext[0] == 1: every 1-D/2-D region) a single
 // division.  Elements past the tile are loaded at a clamped index and not
 // used.  Same arithmetic and reduction as region_tile.
-template <int NS, bool FLAT>
+template <int NS, bool FLAT, bool SNAP>
 __device__ __forceinline__ void region_tile_local(const EpochRegionArgs& a, const RegionDev& R, const TileDev& t,
-                                                  int mode, double (*s_w)[kRegionWarps]) {
+                                                  int mode, int se, double (*s_w)[kRegionWarps]) {
   constexpr int PT = NS == 2 ? 4 : (NS == 4 ? 2 : 1);
   // mode 4 = epoch 0 fused with iteration 1: as mode 1, plus the pre-average
   // SS jump of the n_s == 2 controls (epoch 0's measurement)
@@ -1027,6 +1027,10 @@ __device__ __forceinline__ void region_tile_local(const EpochRegionArgs& a, cons
   const int e1 = R.ext[1], e2 = R.ext[2];
   const float rc1 = 1.0f / static_cast<float>(e1), rc2 = 1.0f / static_cast<float>(e2);
   double* __restrict__ P = a.P;
+  // log_errors snapshots (residual_tma.cu): epoch se's value of every copy,
+  // and in mode 4 also epoch 0's (the pre-average value)
+  double* __restrict__ snap = (SNAP && se >= 0) ? a.snap + static_cast<long long>(se) * a.snap_stride : nullptr;
+  double* __restrict__ snap0 = (SNAP && se >= 0 && mode == 4) ? a.snap : nullptr;
   unsigned long long red[NS + 2];  // [NS + 1]: mode 4's pre-average jump
 #pragma unroll
   for (int j = 0; j <= NS + 1; ++j) red[j] = 0ull;
@@ -1070,6 +1074,8 @@ __device__ __forceinline__ void region_tile_local(const EpochRegionArgs& a, cons
           for (int h = 0; h < NS; ++h) {
             red[h] = umax(red[h], dbits(fabs(avg - v[u][h])));
             P[off[u][h]] = avg;
+            if (SNAP && snap) snap[off[u][h]] = avg;
+            if (SNAP && snap0) snap0[off[u][h]] = v[u][h];
           }
           red[NS] = umax(red[NS], dbits(fabs(avg)));
         } else {
@@ -1079,6 +1085,8 @@ __device__ __forceinline__ void region_tile_local(const EpochRegionArgs& a, cons
             mn = fmin(mn, v[u][h]);
             mx = fmax(mx, v[u][h]);
             red[h] = umax(red[h], dbits(fabs(v[u][h])));
+            if (SNAP && snap) snap[off[u][h]] = v[u][h];
+            if (SNAP && snap0) snap0[off[u][h]] = v[u][h];
           }
           red[NS] = umax(red[NS], dbits(mx - mn));
         }
@@ -1183,15 +1191,15 @@ __device__ __forceinline__ void region_tile(const EpochRegionArgs& a, const Regi
   __syncthreads();  // s_w and the tile descriptor are reused by the next tile
 }
 
-template <int NS>
-__device__ __forceinline__ void region_tile_any(const EpochRegionArgs& a, const TileDev& t, int mode,
+template <int NS, bool SNAP>
+__device__ __forceinline__ void region_tile_any(const EpochRegionArgs& a, const TileDev& t, int mode, int se,
                                                 double (*s_w)[kRegionWarps]) {
   if (t.r.rmask != 0)
-    region_tile<NS>(a, t.r, t, mode, s_w);
+    region_tile<NS>(a, t.r, t, mode, s_w);  // (sharded solves keep no snapshots)
   else if (t.r.ext[0] == 1)
-    region_tile_local<NS, true>(a, t.r, t, mode, s_w);
+    region_tile_local<NS, true, SNAP>(a, t.r, t, mode, se, s_w);
   else
-    region_tile_local<NS, false>(a, t.r, t, mode, s_w);
+    region_tile_local<NS, false, SNAP>(a, t.r, t, mode, se, s_w);
 }
 
 // dp = max_b change_b / max(1, ||P_b||_inf) (solver.cpp:398-405) into
@@ -1236,7 +1244,9 @@ __device__ void epoch_finalize(const EpochRegionArgs& a, int mode, int slot, uns
 
 // MAXNS = 4 for 1-D/2-D decompositions (tighter register budget, 3 CTAs/SM),
 // 8 for 3-D.
-template <int MAXNS>
+// SNAP: the log_errors form that also writes the epoch snapshots of the
+// shared copies (residual_tma.cu); the plain form is the solve's hot epoch.
+template <int MAXNS, bool SNAP>
 __global__ void __launch_bounds__(kRegionThreads, MAXNS == 8 ? 2 : 3) k_epoch_regions(EpochRegionArgs a) {
   __shared__ double s_w[2 * kRegionMaxHolders + 1][kRegionWarps];
   __shared__ unsigned long long s_red[32];
@@ -1251,6 +1261,9 @@ __global__ void __launch_bounds__(kRegionThreads, MAXNS == 8 ? 2 : 3) k_epoch_re
   // previous epoch converged or the iteration budget is spent (its finalize
   // then already cleared the WHILE condition)
   if (a.predicated && (a.st->converged || iter > a.max_iter)) return;
+  // log_errors snapshot slot of this epoch (explicit-mode launches of the
+  // host-driven loop name their epoch in a.slot)
+  const int se = (a.snap && mode != 3) ? ((a.mode < 0 || a.mode == 4) ? iter : a.slot) : -1;
   // persistent CTAs: the next tile's descriptor is fetched while this one runs
   const int tid = threadIdx.x;
   int w = 0;
@@ -1263,9 +1276,9 @@ __global__ void __launch_bounds__(kRegionThreads, MAXNS == 8 ? 2 : 3) k_epoch_re
     if (tid < kWords && tn < a.ntiles) w = __ldg(reinterpret_cast<const int*>(a.tiles + tn) + tid);
     const TileDev& t = s_T;
     switch (t.r.ns) {
-      case 2: region_tile_any<2>(a, t, mode, s_w); break;
-      case 4: region_tile_any<4>(a, t, mode, s_w); break;
-      default: region_tile_any<MAXNS>(a, t, mode, s_w); break;
+      case 2: region_tile_any<2, SNAP>(a, t, mode, se, s_w); break;
+      case 4: region_tile_any<4, SNAP>(a, t, mode, se, s_w); break;
+      default: region_tile_any<MAXNS, SNAP>(a, t, mode, se, s_w); break;
     }
   }
   if (!a.finalize) return;
@@ -1808,6 +1821,85 @@ __global__ void __launch_bounds__(kDecodeThreads) k_decode(DecodeArgs a) {
   }
 }
 
+// residual_error of one local problem (lsq.cpp:66-85): the decode of
+// apply_along_axis over d = 0..D-1 (apply_line, collocation.cpp:37-45: acc +=
+// v * x from 0.0, no FMA in the reference build) at one point, q - decoded.
+// Out-of-window basis entries are exact zeros and add exact zeros, so the
+// clipped row of the reference and the aligned row here sum identically.
+constexpr int kResPtThreads = 256;
+template <int P>
+__global__ void __launch_bounds__(kResPtThreads) k_residual_points(ResidualArgs a) {
+  __shared__ double s_red[2][kResPtThreads / 32];
+  auto clampi = [](int i, int n) { return i < 0 ? 0 : (i >= n ? n - 1 : i); };
+  double l2 = 0.0, li = 0.0;
+  const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+  for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < a.total; i += stride) {
+    int j[3] = {0, 0, 0};
+    {
+      std::int64_t r = i;
+      for (int k = a.D - 1; k >= 0; --k) {
+        j[k] = static_cast<int>(r % a.m[k]);
+        r /= a.m[k];
+      }
+    }
+    int g[3] = {0, 0, 0};
+    double v[3][P + 1];
+    for (int k = 0; k < 3; ++k) {
+      if (k < a.D) {
+        g[k] = a.g0[k][j[k]];
+#pragma unroll
+        for (int t = 0; t <= P; ++t) v[k][t] = a.vals[k][static_cast<std::int64_t>(j[k]) * (P + 1) + t];
+      } else {
+#pragma unroll
+        for (int t = 0; t <= P; ++t) v[k][t] = t == 0 ? 1.0 : 0.0;
+      }
+    }
+    const int n1 = a.D >= 2 ? a.n[1] : 1, n2 = a.D >= 3 ? a.n[2] : 1;
+    const int K1 = a.D >= 2 ? P : 0, K2 = a.D >= 3 ? P : 0;
+    double acc2 = 0.0;  // outermost: the last axis applied
+    for (int k2 = 0; k2 <= K2; ++k2) {
+      const int c2 = a.D >= 3 ? clampi(g[2] + k2, n2) : 0;
+      double acc1 = 0.0;
+      for (int k1 = 0; k1 <= K1; ++k1) {
+        const int c1 = a.D >= 2 ? clampi(g[1] + k1, n1) : 0;
+        double acc0 = 0.0;
+#pragma unroll
+        for (int k0 = 0; k0 <= P; ++k0) {
+          const int c0 = clampi(g[0] + k0, a.n[0]);
+          const double x = a.controls[(static_cast<std::int64_t>(c0) * n1 + c1) * n2 + c2];
+          acc0 = __dadd_rn(acc0, __dmul_rn(v[0][k0], x));
+        }
+        acc1 = a.D >= 2 ? __dadd_rn(acc1, __dmul_rn(v[1][k1], acc0)) : acc0;
+      }
+      acc2 = a.D >= 3 ? __dadd_rn(acc2, __dmul_rn(v[2][k2], acc1)) : acc1;
+    }
+    const double e = __dsub_rn(a.q[i], acc2);
+    if (a.pointwise) a.pointwise[i] = e;
+    l2 = fma(e, e, l2);
+    li = fmax(li, fabs(e));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    l2 += __shfl_xor_sync(kFull, l2, o);
+    li = fmax(li, __shfl_xor_sync(kFull, li, o));
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    s_red[0][w] = l2;
+    s_red[1][w] = li;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sl = 0.0, sm = 0.0;
+    for (int t = 0; t < kResPtThreads / 32; ++t) {
+      sl += s_red[0][t];
+      sm = fmax(sm, s_red[1][t]);
+    }
+    a.partial[2 * blockIdx.x] = sl;
+    a.partial[2 * blockIdx.x + 1] = sm;
+  }
+}
+
 __global__ void __launch_bounds__(1024) k_reduce_partials(const double* p, std::int64_t n, double* out) {
   __shared__ double s_l2[1024], s_li[1024];
   double l2 = 0.0, li = 0.0;
@@ -1847,6 +1939,14 @@ int dispatch_degree(int p, Args&&... args) {
     default: return -1;
   }
 }
+
+template <int P>
+struct ResidualPointsLaunch {
+  static int run(const ResidualArgs& a, int ctas, cudaStream_t s) {
+    k_residual_points<P><<<ctas, kResPtThreads, 0, s>>>(a);
+    return 1;
+  }
+};
 
 template <int P>
 struct RowsLaunch {
@@ -2013,6 +2113,9 @@ int debug_fail_line() {
 #endif
 }
 
+int launch_residual_points(int degree, const ResidualArgs& a, int ctas, cudaStream_t s) {
+  return dispatch_degree<ResidualPointsLaunch>(degree, a, ctas, s);
+}
 int launch_basis_rows(int degree, const RowsArgs& a, cudaStream_t s) {
   return dispatch_degree<RowsLaunch>(degree, a, s);
 }
@@ -2091,9 +2194,11 @@ int launch_epoch_regions(const EpochRegionArgs& a, cudaStream_t s) {
     const int per_sm = a.max_ns > 4 ? 2 : 3;  // __launch_bounds__ residency
     const int grid = a.ntiles < sms * per_sm ? a.ntiles : sms * per_sm;
     if (a.max_ns > 4)
-      launch_pdl(k_epoch_regions<8>, dim3(grid), dim3(kRegionThreads), 0, s, a);
+      a.snap ? launch_pdl(k_epoch_regions<8, true>, dim3(grid), dim3(kRegionThreads), 0, s, a)
+             : launch_pdl(k_epoch_regions<8, false>, dim3(grid), dim3(kRegionThreads), 0, s, a);
     else
-      launch_pdl(k_epoch_regions<4>, dim3(grid), dim3(kRegionThreads), 0, s, a);
+      a.snap ? launch_pdl(k_epoch_regions<4, true>, dim3(grid), dim3(kRegionThreads), 0, s, a)
+             : launch_pdl(k_epoch_regions<4, false>, dim3(grid), dim3(kRegionThreads), 0, s, a);
   }
   return 1;
 }

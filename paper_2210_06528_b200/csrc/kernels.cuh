@@ -176,6 +176,8 @@ struct EpochRegionArgs {
   int finalize;             // 1: the last CTA computes dp and writes epoch_out (else k_epoch_finalize)
   int zero_pairs;           // > 0: the finalize also clears pair_jumps[0, zero_pairs) (no memset node in the chain)
   int slot;                 // epoch_out slot when finalize is done separately
+  double* snap;             // log_errors: per-epoch snapshots of the shared copies (null: none)
+  long long snap_stride;    // doubles per snapshot (= the held lattices' size)
 };
 int launch_epoch_regions(const EpochRegionArgs& a, cudaStream_t s);
 // dp / jumps of the epoch into epoch_out[3*slot] and accumulator reset (one CTA).
@@ -205,6 +207,34 @@ struct BlockResArgs {
   int max_m0;                  // longest axis-0 row table of a local block (shared-memory staging)
 };
 int launch_block_residual(int degree, const BlockResArgs& a, cudaStream_t s);
+
+// K9 one-pass form (residual_tma.cu): every recorded epoch's block residuals
+// after the loop, from the held lattices P (non-shared controls) and the
+// epoch snapshots of the shared copies, Q_loc streamed once per EG epochs.
+struct ResTmaArgs {
+  int D;
+  int nblocks;                       // grid.y (local blocks)
+  const BlockDev* blocks;
+  const AxisProb* probs;
+  const int* g0;
+  const double* vals;
+  const double* P;
+  const double* snap;                // snapshot e at snap + e * snap_stride (same layout as P)
+  long long snap_stride;
+  const unsigned char* sflag;        // per dim concatenated: 1 if the global control index is shared
+  std::int64_t sflag_off[3];
+  const EpochState* st;              // epochs recorded = st->iter + 1 (null: 1)
+  int W;                             // TMA box inner width (even, one spare column)
+  int ntc, nrr;                      // column tiles (D = 3: rows j1) x row ranges per block: grid.x = ntc * nrr
+  int lt_cap;                        // window columns per staged plane (>= the widest CTA window)
+  int na_cap;                        // staged planes per epoch (>= the most planes a row range touches)
+  int eg;                            // epochs per pass (1, 2 or 4; the staged windows scale with it)
+  double* partial;                   // [epoch][block][ntc * nrr] x {sum e^2, max |e|}
+  double* errs;                      // [(max_iter + 1)][nglobal] x {l2, linf}
+  int nglobal, boff;
+};
+int launch_residual_tma(int degree, const ResTmaArgs& a, const CUtensorMap& map, int threads, cudaStream_t s);
+size_t residual_tma_smem(int degree, int W, int eg, int na_cap, int lt_cap);
 
 // K5: dp = max_b change_b / max(1, ||P_b||_inf) and epoch bookkeeping.
 struct DpArgs {
@@ -294,6 +324,23 @@ struct DecodeSweepArgs {
 };
 int launch_decode_tma(int degree, const DecodeSweepArgs& a, const CUtensorMap& map, const TmaGeom& g,
                       cudaStream_t s);
+
+// residual_error (lsq.cpp:66-85) of ONE local problem (the unit sub-boundary,
+// lsq.hpp:41): thread per point, decode of the window-clipped rows in the
+// reference's axis order with explicit RN operations (bitwise equal pointwise
+// errors), per-CTA {sum e^2, max |e|} partials.
+struct ResidualArgs {
+  int D;
+  int m[3], n[3];          // rows / window columns per dim
+  const int* g0[3];        // local unclipped first column per row
+  const double* vals[3];   // (p+1) per row, out-of-window entries zero
+  const double* controls;  // n0 x n1 x n2 row-major
+  const double* q;         // m0 x m1 x m2 row-major
+  double* pointwise;       // nullable
+  double* partial;         // 2 per CTA
+  std::int64_t total;
+};
+int launch_residual_points(int degree, const ResidualArgs& a, int ctas, cudaStream_t s);
 
 // K7b: deterministic reduction of the tile partials.
 int launch_reduce_partials(const double* partial, std::int64_t n, double* out2, cudaStream_t s);

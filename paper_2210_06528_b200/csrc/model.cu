@@ -202,6 +202,32 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval_points(EvalArgs a) {
   a.err[i] = 0;
 }
 
+// find_span / basis_funs / basis_derivs (knots.cpp:83-203) per parameter:
+// out row 0 = basis_funs, rows 1..k = basis_derivs rows; err per item (1: u
+// outside the evaluable range).
+__global__ void __launch_bounds__(kEvalThreads) k_basis_points(const double* kn, int p, int nb, std::int64_t n,
+                                                               const double* u, const int* spans, int k,
+                                                               int* out_spans, double* out, int* err) {
+  const std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double x = u[i];
+  int s;
+  if (spans) {
+    s = spans[i];
+  } else {
+    if (x < kn[p] || x > kn[nb]) {
+      err[i] = 1;
+      return;
+    }
+    s = dev_find_span(kn, p, nb, x);
+  }
+  err[i] = 0;
+  out_spans[i] = s;
+  double* o = out + i * static_cast<std::int64_t>(k + 1) * (p + 1);
+  dev_basis_funs(kn, p, s, x, o);
+  for (int r = 1; r <= k; ++r) dev_basis_deriv_row(kn, p, s, x, r, o + r * (p + 1));
+}
+
 // field.cpp:170-185: float32 / float64, optional byte swap, widened to fp64
 __global__ void k_raw_to_f64(const unsigned char* raw, std::int64_t n, int width, int swap, double* out) {
   const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
@@ -485,6 +511,45 @@ MFB_API int mfadd_eval_points(mfadd_context* ctx, int rank, const int* degrees, 
     std::vector<double> vals;
     mfb::eval_items_device(ctx, rank, degrees, knots, kn_off, dc.p, {L}, items, vals);
     std::memcpy(out, vals.data(), vals.size() * sizeof(double));
+  });
+}
+
+MFB_API int mfadd_basis_funs(mfadd_context* ctx, const double* knots, int nknots, int degree, int64_t n,
+                             const double* u, const int* spans, int orders, int* out_spans, double* out) {
+  return guarded([&] {
+    ContextScope scope(ctx);
+    if (degree < 1 || degree > mfb::kMaxDegree)
+      throw std::invalid_argument("basis_funs: degree must be in [1, " + std::to_string(mfb::kMaxDegree) + "]");
+    if (nknots < 2 * (degree + 1)) throw std::invalid_argument("KnotVector: too few knots");
+    if (orders < 0 || orders > degree)  // knots.cpp:133-134
+      throw std::invalid_argument("basis_derivs: order must satisfy 0 <= k <= p (got " + std::to_string(orders) + ")");
+    const int nb = nknots - degree - 1;
+    if (spans)
+      for (std::int64_t i = 0; i < n; ++i)
+        if (spans[i] < degree || spans[i] >= nb)
+          throw std::invalid_argument("basis_funs: span " + std::to_string(spans[i]) + " outside [" +
+                                      std::to_string(degree) + ", " + std::to_string(nb) + ")");
+    if (n <= 0) return;
+    cudaStream_t st = ctx->stream;
+    const std::size_t nv = static_cast<std::size_t>(n) * (orders + 1) * (degree + 1);
+    DevVec<double> dk(static_cast<std::size_t>(nknots)), du(static_cast<std::size_t>(n)), dout(nv);
+    DevVec<int> dsp(static_cast<std::size_t>(n)), dspo(static_cast<std::size_t>(n)), derr(static_cast<std::size_t>(n));
+    h2d(dk.p, knots, static_cast<std::size_t>(nknots), st);
+    h2d(du.p, u, static_cast<std::size_t>(n), st);
+    if (spans) h2d(dsp.p, spans, static_cast<std::size_t>(n), st);
+    mfb::k_basis_points<<<static_cast<unsigned>((n + mfb::kEvalThreads - 1) / mfb::kEvalThreads), mfb::kEvalThreads,
+                          0, st>>>(dk.p, degree, nb, n, du.p, spans ? dsp.p : nullptr, orders, dspo.p, dout.p, derr.p);
+    ctx->launches += 1;
+    CK(cudaGetLastError());
+    std::vector<int> err(static_cast<std::size_t>(n));
+    CK(cudaMemcpyAsync(err.data(), derr.p, err.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(out, dout.p, nv * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (out_spans) CK(cudaMemcpyAsync(out_spans, dspo.p, err.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (std::int64_t i = 0; i < n; ++i)  // first failing parameter (knots.cpp:88-90)
+      if (err[static_cast<std::size_t>(i)])
+        throw std::out_of_range("find_span: parameter " + std::to_string(u[i]) + " outside evaluable range [" +
+                                std::to_string(knots[degree]) + ", " + std::to_string(knots[nb]) + "]");
   });
 }
 

@@ -107,6 +107,43 @@ static void gpu_cases() {
   double e = 0.0;
   for (std::int64_t i = 0; i < back.size(); ++i) e = std::fmax(e, std::fabs(back[i] - lp.q[i]));
   EXPECT(e < 1e-9);
+  // residual_error (lsq.hpp:41) of the fit: pointwise = q - decode(P)
+  const auto rs = mfadd::residual_error(lp, P);
+  double rl2 = 0.0, rli = 0.0, rmx = 0.0;
+  for (std::int64_t i = 0; i < rs.pointwise.size(); ++i) {
+    rl2 += rs.pointwise[i] * rs.pointwise[i];
+    rli = std::fmax(rli, std::fabs(rs.pointwise[i]));
+    rmx = std::fmax(rmx, std::fabs(rs.pointwise[i] - (lp.q[i] - back[i])));
+  }
+  EXPECT(rmx < 1e-13 && rli == rs.linf && std::fabs(std::sqrt(rl2) - rs.l2) <= 1e-12 * std::fmax(rs.l2, 1e-300));
+  // find_span / basis_funs / basis_derivs (knots.hpp:36-56)
+  const int sp = mfadd::find_span(kv, 0.5);
+  EXPECT(kv.knots[static_cast<std::size_t>(sp)] <= 0.5 && 0.5 < kv.knots[static_cast<std::size_t>(sp) + 1]);
+  const auto bf = mfadd::basis_funs(kv, sp, 0.5);
+  double pu = 0.0;
+  for (double v : bf.values) pu += v;
+  EXPECT(bf.values.size() == 4 && std::fabs(pu - 1.0) < 1e-14);
+  const auto bd = mfadd::basis_derivs(kv, sp, 0.5, 2);
+  double d1 = 0.0;
+  for (int j = 0; j < 4; ++j) d1 += bd.deriv(1, j);
+  EXPECT(bd.values == bf.values && std::fabs(d1) < 1e-9);
+  bool range = false;
+  try {
+    mfadd::find_span(kv, 1.5);
+  } catch (const std::out_of_range&) {
+    range = true;
+  }
+  EXPECT(range);
+  // solver.cpp:335-338: a field whose extents disagree with the decomposition
+  bool extents = false;
+  try {
+    mfadd::Field ft = sinc2d(64, 64);
+    ft.dims = {32, 128};
+    mfadd::solve(ft, dec, cfg);
+  } catch (const std::invalid_argument&) {
+    extents = true;
+  }
+  EXPECT(extents);
   // SingularFitError{dim, span} through the shim (lsq.cpp:46-55)
   bool singular = false;
   try {
@@ -119,7 +156,7 @@ static void gpu_cases() {
     bad.q = mfadd::Tensor({40});
     mfadd::fit_unconstrained(bad);
   } catch (const mfadd::SingularFitError& ex) {
-    singular = ex.dim == 0 && ex.span >= 0;
+    singular = ex.dim == 0 && ex.span == 4;  // columns 0..3 supported (one knot span of data)
   }
   EXPECT(singular);
   // MfaModel output path (model.hpp): MFDD round trip, decode_grid, eval and
