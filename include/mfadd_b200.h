@@ -168,12 +168,21 @@ int mfadd_nccl_unique_id(unsigned char* out128);
 int mfadd_comm_create(mfadd_context* ctx, const unsigned char* id128, int rank, int nranks, mfadd_comm** out);
 void mfadd_comm_free(mfadd_comm* comm);
 /* A solver for the calling rank's shard; mfadd_solve()/mfadd_solve_host() then
- * take the full global field and run collectively on every rank. */
+ * run collectively on every rank.  The field argument keeps the global
+ * layout, but a host field is read only in the rank's slab (the axis-0 input
+ * rows its blocks touch, mfadd_shard_range's box) and a device field must
+ * hold valid data there; mfadd_solve_host's out_error receives the input
+ * rows the rank decoded ([in_lo, in_hi)), out_controls the whole gathered
+ * lattice.  An asynchronous NCCL error, or no progress for
+ * MFADD_NCCL_TIMEOUT_S seconds (default 600), aborts the communicator and
+ * returns MFADD_ECUDA (later calls on it fail fast). */
 int mfadd_solver_create_sharded(mfadd_context* ctx, const mfadd_decomposition* dec, const mfadd_solver_config* cfg,
                                 mfadd_comm* comm, mfadd_solver** out);
 /* Host-side shard plan: block ids [blo, bhi) and own input rows [in_lo, in_hi). */
 int mfadd_shard_range(const mfadd_decomposition* dec, int rank, int nranks, int* blo, int* bhi, int64_t* in_lo,
                       int64_t* in_hi);
+/* The axis-0 input rows [box_lo, box_hi) a rank's solve reads (its slab). */
+int mfadd_shard_box(const mfadd_decomposition* dec, int rank, int nranks, int64_t* box_lo, int64_t* box_hi);
 /* Per-epoch exchange layout with one peer (recv=0: what `rank` sends, 1: what it
  * receives): entries (holder block, i0, i1, i2) in buffer order.  Returns the
  * entry count (out may be NULL), or -status on error. */

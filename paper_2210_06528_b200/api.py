@@ -874,6 +874,13 @@ def shard_range(dec: "Decomposition", rank: int, nranks: int):
     return blo.value, bhi.value, ilo.value, ihi.value
 
 
+def shard_box(dec: "Decomposition", rank: int, nranks: int):
+    """(box_lo, box_hi): the axis-0 input rows `rank`'s sharded solve reads (its slab)."""
+    lo, hi = C.c_int64(), C.c_int64()
+    _check(L.load().mfadd_shard_box(dec._h, rank, nranks, C.byref(lo), C.byref(hi)))
+    return lo.value, hi.value
+
+
 def shard_exchange(dec: "Decomposition", rank: int, nranks: int, peer: int, recv: bool) -> np.ndarray:
     """Per-epoch exchange layout of `rank` with `peer`: rows (holder block, i0, i1, i2) in buffer order."""
     lib = L.load()

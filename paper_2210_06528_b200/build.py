@@ -60,9 +60,12 @@ def build(force: bool = False, verbose: bool = False, debug: bool = False) -> st
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
+    headers = [d for d in deps if not d.endswith((".cu", ".cpp"))]
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         objs.append(obj)
+        if not force and not _stale(obj, [src] + headers):  # per-object: only changed units recompile
+            continue
         ncl = _nccl_dir()
         inc = ["-I", os.path.join(ncl, "include")] if ncl else []
         cmd = [NVCC, *ARCH, *FLAGS, *extra, *inc, "-I", CSRC, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]

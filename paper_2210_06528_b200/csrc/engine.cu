@@ -14,6 +14,8 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <chrono>
+#include <thread>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -710,6 +712,7 @@ struct DecodePlan {
 struct mfadd_comm {
   ncclComm_t comm = nullptr;
   int rank = 0, nranks = 1;
+  bool aborted = false;  // after an NCCL error or a timeout: every later call fails fast
 };
 
 struct ShardPeer {
@@ -729,6 +732,7 @@ struct mfadd_solver {
   bool tma_decode = false;
   mfb::TmaGeom dgeo{1, 1, 16, 4, 0};
   int dnt1 = 1, dnt2 = 1, dnrange = 1, dH = 1;
+  bool dwin = false;  // D = 3: window-only decode kernel form
 
   DBuf<int2> hr;
   DBuf<int> slist, clist, own_coord, pair_slot, unit_g0;
@@ -755,7 +759,7 @@ struct mfadd_solver {
   // every epoch's residuals after the loop
   bool res_snap = false;
   DBuf<double> snap, res_part2;
-  int res_W = 0, res_ntc = 0, res_nrr = 1, res_threads = 0, res_ltcap = 0, res_nacap = 0, res_eg = 1;
+  int res_W = 0, res_ntc = 0, res_nrr = 1, res_threads = 0, res_ltcap = 0, res_nacap = 0, res_eg = 1, res_dense = 0;
   std::vector<double> h_block_errs;
   // shard: rank of nranks owns blocks [srange.blo, srange.bhi)
   int rank = 0, nranks = 1;
@@ -1006,6 +1010,7 @@ int launch_residuals_all(mfadd_solver* s, const double* dfield, cudaStream_t cs)
   a.lt_cap = s->res_ltcap;
   a.na_cap = s->res_nacap;
   a.eg = s->res_eg;
+  a.dense_a = s->res_dense;
   a.partial = s->res_part2.p;
   a.errs = s->block_errs.p;
   a.nglobal = d.nblocks;
@@ -1325,6 +1330,19 @@ void plan_residual_tma(mfadd_solver* s) {
     if (ok) break;
   }
   if (!ok) return;  // the per-epoch kernels stay
+  // dense chunk sweep: the most plane advances within one 8-row chunk
+  {
+    int adv = 0;
+    std::vector<char> seen0(wl.probs.size(), 0);
+    for (const auto& b : wl.blocks) {
+      const int pid = b.ax[0];
+      if (seen0[static_cast<std::size_t>(pid)]) continue;
+      seen0[static_cast<std::size_t>(pid)] = 1;
+      const AxisProb& pr = wl.probs[static_cast<std::size_t>(pid)];
+      for (int y = 0; y < pr.m; y += 8) adv = std::max(adv, g0_of(pr, std::min(pr.m - 1, y + 7)) - g0_of(pr, y));
+    }
+    s->res_dense = (s->res_eg == 4 && p <= 6 && adv <= 3 && !std::getenv("MFADD_RES_ROWS")) ? std::max(1, adv) : 0;
+  }
   s->res_snap = true;
   s->snap.alloc(static_cast<std::size_t>(s->cfg.max_outer_iterations + 1) * static_cast<std::size_t>(wl.total_p));
   s->res_part2.alloc(static_cast<std::size_t>(s->cfg.max_outer_iterations + 1) * wl.blocks.size() *
@@ -1601,6 +1619,16 @@ std::unique_ptr<mfadd_solver> create_solver(mfadd_context* ctx, const mfadd_deco
       s->dnrange = (M0 + s->dH - 1) / s->dH;
       s->tma_decode = true;
       npart = std::max(npart, static_cast<std::size_t>(s->dnt1) * s->dnt2 * s->dnrange);
+      if (D == 3 && s->dgeo.B1 == 1 && s->dgeo.lt_cap > 0) {  // every tile's axis-2 window fits: window-only kernel
+        const std::vector<double>& kn2 = d.knots[2];
+        auto g0 = [&](int j) { return host_find_span(kn2, p, static_cast<double>(j) / static_cast<double>(M2 - 1)) - p; };
+        int mrw = 0;
+        for (int tx = 0; tx < s->dnt2; ++tx) {
+          const int jf = tx * s->dgeo.B2, jl = std::min(M2 - 1, jf + s->dgeo.B2 - 1);
+          mrw = std::max(mrw, g0(jl) - g0(jf) + p + 1);
+        }
+        s->dwin = mrw <= s->dgeo.lt_cap && mrw <= s->dgeo.B2;
+      }
     }
     s->partial.alloc(npart * 2);
     s->red2.alloc(2);
@@ -1820,6 +1848,7 @@ int enqueue_decode(mfadd_solver* s, const double* dfield) {
     }
     ds.ticket = s->ticket.p;
     ds.red2 = s->red2.p;
+    ds.win = s->dwin ? 1 : 0;
     const CUtensorMap map = make_tmap(dfield, d.rank, dims, box);
     launches += mfb::launch_decode_tma(wl.p, ds, map, s->dgeo, st);
     nparts = 0;  // reduced by the decode's last CTA
@@ -2187,10 +2216,48 @@ int shard_compute(mfadd_solver* s, int mode, int slot) {
   return l;
 }
 
+// Wait for the context stream of a sharded solver while polling the
+// communicator: an asynchronous NCCL error (a lost peer, a failed
+// connection) or no progress within MFADD_NCCL_TIMEOUT_S seconds (default
+// 600) aborts the communicator and raises MFADD_ECUDA instead of hanging
+// (the reference's workers are threads of one process and cannot be lost).
+void sync_sharded(mfadd_solver* s) {
+  cudaStream_t st = s->ctx->stream;
+  mfadd_comm* c = s->comm;
+  if (!c) {
+    CK(cudaStreamSynchronize(st));
+    return;
+  }
+  if (c->aborted) throw ApiError(MFADD_ECUDA, "mfadd: the NCCL communicator was aborted by an earlier failure");
+  static const double limit = std::getenv("MFADD_NCCL_TIMEOUT_S") ? std::atof(std::getenv("MFADD_NCCL_TIMEOUT_S")) : 600.0;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t e = cudaStreamQuery(st);
+    if (e == cudaSuccess) return;
+    if (e != cudaErrorNotReady) CK(e);
+    ncclResult_t ae = ncclSuccess;
+    ncclCommGetAsyncError(c->comm, &ae);
+    const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (ae != ncclSuccess && ae != ncclInProgress) {
+      ncclCommAbort(c->comm);
+      c->aborted = true;
+      throw ApiError(MFADD_ECUDA, std::string("NCCL asynchronous error on rank ") + std::to_string(c->rank) + ": " +
+                                      ncclGetErrorString(ae) + " (communicator aborted)");
+    }
+    if (el > limit) {
+      ncclCommAbort(c->comm);
+      c->aborted = true;
+      throw ApiError(MFADD_ECUDA, "NCCL: no progress for " + std::to_string(static_cast<int>(limit)) + " s on rank " +
+                                      std::to_string(c->rank) + " (communicator aborted; MFADD_NCCL_TIMEOUT_S)");
+    }
+    std::this_thread::yield();
+  }
+}
+
 double read_epoch_dp(mfadd_solver* s, int slot) {
   double v = 0.0;
   CK(cudaMemcpyAsync(&v, s->epoch_out.p + 3 * slot, sizeof v, cudaMemcpyDeviceToHost, s->ctx->stream));
-  CK(cudaStreamSynchronize(s->ctx->stream));
+  sync_sharded(s);
   return v;
 }
 
@@ -2319,7 +2386,7 @@ void solve_group(std::vector<mfadd_solver*>& g, const std::vector<const double*>
     es.iter = last;
     es.last_iter = last;
     es.converged = converged ? 1 : 0;
-    CK(cudaStreamSynchronize(st));
+    sync_sharded(s);
     std::memcpy(hr + s->hres_es, &es, sizeof es);
     finish_solve(s, launches[r] - (loop ? last : 0));  // finish_solve adds one launch per iteration
   }
@@ -2387,6 +2454,39 @@ void solve_impl(mfadd_solver* s, const double* dfield) {
 
 }  // namespace
 
+namespace {
+// Host field -> device for one solve.  A sharded solver reads only its slab:
+// the axis-0 input rows [box_lo, box_hi) its blocks' fits (and its own decode
+// rows, a subset) touch, at their global offsets (each GPU
+// uploads the union of its blocks' input boxes).  Returns the bytes copied.
+std::size_t upload_field(mfadd_solver* s, const double* host, double* dev, cudaStream_t st) {
+  const Decomp& d = s->dec;
+  std::int64_t row = 1;
+  for (int k = 1; k < d.rank; ++k) row *= d.grid[k];
+  std::int64_t lo = 0, hi = d.grid[0];
+  if (s->nranks > 1 && s->tma_decode) {  // (the generic decode path decodes every row on every rank)
+    lo = s->srange.box_lo;
+    hi = s->srange.box_hi;
+  }
+  const std::size_t n = static_cast<std::size_t>((hi - lo) * row);
+  CK(cudaMemcpyAsync(dev + lo * row, host + lo * row, n * sizeof(double), cudaMemcpyHostToDevice, st));
+  return n * sizeof(double);
+}
+// Error field -> host: a sharded solver returns the input rows it decoded.
+void download_error(mfadd_solver* s, double* host, cudaStream_t st) {
+  const Decomp& d = s->dec;
+  std::int64_t row = 1;
+  for (int k = 1; k < d.rank; ++k) row *= d.grid[k];
+  std::int64_t lo = 0, hi = d.grid[0];
+  if (s->nranks > 1 && s->tma_decode) {  // (the generic decode path decodes every row on every rank)
+    lo = s->srange.in_lo;
+    hi = s->srange.in_hi;
+  }
+  CK(cudaMemcpyAsync(host + lo * row, s->error.p + lo * row, static_cast<std::size_t>((hi - lo) * row) * sizeof(double),
+                     cudaMemcpyDeviceToHost, st));
+}
+}  // namespace
+
 MFB_API int mfadd_solve(mfadd_solver* s, const double* field, int field_on_device, mfadd_solve_summary* out) {
   return guarded([&] {
     ContextScope scope(s->ctx);
@@ -2395,7 +2495,7 @@ MFB_API int mfadd_solve(mfadd_solver* s, const double* field, int field_on_devic
     if (!field_on_device) {
       const std::size_t n = static_cast<std::size_t>(s->dec.total_inputs());
       if (s->field_buf.n != n) s->field_buf.alloc(n);
-      CK(cudaMemcpyAsync(s->field_buf.p, field, n * sizeof(double), cudaMemcpyHostToDevice, s->ctx->stream));
+      upload_field(s, field, s->field_buf.p, s->ctx->stream);
       df = s->field_buf.p;
     }
     solve_impl(s, df);
@@ -2413,12 +2513,11 @@ MFB_API int mfadd_solve_host(mfadd_solver* s, const double* field_host, double* 
     const std::size_t n = static_cast<std::size_t>(s->dec.total_inputs());
     if (s->field_buf.n != n) s->field_buf.alloc(n);
     cudaStream_t st = s->ctx->stream;
-    CK(cudaMemcpyAsync(s->field_buf.p, field_host, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    upload_field(s, field_host, s->field_buf.p, st);
     solve_impl(s, s->field_buf.p);
     if (out_controls_host)
       CK(cudaMemcpyAsync(out_controls_host, s->lattice.p, s->lattice.n * sizeof(double), cudaMemcpyDeviceToHost, st));
-    if (out_error_host)
-      CK(cudaMemcpyAsync(out_error_host, s->error.p, s->error.n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (out_error_host) download_error(s, out_error_host, st);
     CK(cudaStreamSynchronize(st));
     if (out) *out = s->summary;
   });
@@ -2443,13 +2542,13 @@ MFB_API int mfadd_solve_host_batch(mfadd_solver* s, int n, const double* const* 
     if (s->nranks > 1 || s->tl.on || s->tl.sync_check) {  // no overlap: one call per step
       for (int i = 0; i < n; ++i) {
         if (s->field_buf.n != nf) s->field_buf.alloc(nf);
-        CK(cudaMemcpyAsync(s->field_buf.p, fields_host[i], nf * sizeof(double), cudaMemcpyHostToDevice,
-                           s->ctx->stream));
+        upload_field(s, fields_host[i], s->field_buf.p, s->ctx->stream);
         solve_impl(s, s->field_buf.p);
         if (out_controls_host && out_controls_host[i])
-          CK(cudaMemcpy(out_controls_host[i], s->lattice.p, s->lattice.n * sizeof(double), cudaMemcpyDeviceToHost));
-        if (out_errors_host && out_errors_host[i])
-          CK(cudaMemcpy(out_errors_host[i], s->error.p, s->error.n * sizeof(double), cudaMemcpyDeviceToHost));
+          CK(cudaMemcpyAsync(out_controls_host[i], s->lattice.p, s->lattice.n * sizeof(double), cudaMemcpyDeviceToHost,
+                             s->ctx->stream));
+        if (out_errors_host && out_errors_host[i]) download_error(s, out_errors_host[i], s->ctx->stream);
+        CK(cudaStreamSynchronize(s->ctx->stream));
         if (out) out[i] = s->summary;
       }
       return;
@@ -3028,6 +3127,14 @@ MFB_API int mfadd_shard_range(const mfadd_decomposition* dec, int rank, int nran
   });
 }
 
+MFB_API int mfadd_shard_box(const mfadd_decomposition* dec, int rank, int nranks, int64_t* box_lo, int64_t* box_hi) {
+  return guarded([&] {
+    const mfb::ShardRange r = mfb::shard_range(dec->d, rank, nranks);
+    *box_lo = r.box_lo;
+    *box_hi = r.box_hi;
+  });
+}
+
 MFB_API int mfadd_shard_exchange(const mfadd_decomposition* dec, int rank, int nranks, int peer, int recv,
                                  int64_t* out, int64_t cap) {
   int64_t count = -1;
@@ -3068,11 +3175,17 @@ MFB_API int mfadd_solve_loopback(mfadd_context* ctx, const mfadd_decomposition* 
       own.push_back(create_solver(ctx, dec, cfg, r, nranks, nullptr));
       g.push_back(own.back().get());
     }
+    // one field buffer per rank, NaN outside the rank's slab (upload_field):
+    // any read outside the slab would show in the results
     const std::size_t n = static_cast<std::size_t>(dec->d.total_inputs());
-    DBuf<double> f;
-    f.alloc(n);
-    CK(cudaMemcpyAsync(f.p, field_host, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-    std::vector<const double*> fields(g.size(), f.p);
+    std::vector<DBuf<double>> fb(g.size());
+    std::vector<const double*> fields;
+    for (std::size_t r = 0; r < g.size(); ++r) {
+      fb[r].alloc(n);
+      CK(cudaMemsetAsync(fb[r].p, 0xff, n * sizeof(double), ctx->stream));
+      upload_field(g[r], field_host, fb[r].p, ctx->stream);
+      fields.push_back(fb[r].p);
+    }
     LoopbackTransport tr;
     solve_group(g, fields, tr);
     mfadd_solver* s0 = g[0];

@@ -229,6 +229,7 @@ struct ResTmaArgs {
   int lt_cap;                        // window columns per staged plane (>= the widest CTA window)
   int na_cap;                        // staged planes per epoch (>= the most planes a row range touches)
   int eg;                            // epochs per pass (1, 2 or 4; the staged windows scale with it)
+  int dense_a;                       // 1..3: dense chunk sweep (EG = 4, P <= 6; max plane advances within a chunk), 0: per row
   double* partial;                   // [epoch][block][ntc * nrr] x {sum e^2, max |e|}
   double* errs;                      // [(max_iter + 1)][nglobal] x {l2, linf}
   int nglobal, boff;
@@ -321,6 +322,7 @@ struct DecodeSweepArgs {
   double* partial;  // per CTA {l2sq, linf}
   unsigned* ticket; // CTA completion counter (zero between launches)
   double* red2;     // {sum l2sq, max linf}, written by the last CTA
+  int win;          // D = 3: every CTA's axis-2 window fits (host-checked): the window-only kernel form
 };
 int launch_decode_tma(int degree, const DecodeSweepArgs& a, const CUtensorMap& map, const TmaGeom& g,
                       cudaStream_t s);

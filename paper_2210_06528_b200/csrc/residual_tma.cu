@@ -51,10 +51,16 @@ __host__ __device__ inline ResStage res_stage(int nbox, int P) {
 
 __host__ __device__ inline size_t res_tma_smem(int P, int W, int EG, int na_cap, int lt_cap, int S) {
   return static_cast<size_t>(S) * res_stage(W, P).stage_bytes + S * 8 + 8 +
-         static_cast<size_t>(EG) * na_cap * lt_cap * 8;
+         static_cast<size_t>(EG) * na_cap * lt_cap * 8 + 2 * kResR * (P + 4) * 8;  // (+ the dense sweep's rows)
 }
 
-template <int P, int D, int EG, int S>
+// A > 0: the dense chunk sweep.  A window of NW = P+1+A planes per epoch
+// covers every row of an 8-row chunk (the host checks that no chunk's rows
+// span more than A plane advances); each chunk's basis rows are expanded to
+// NW columns (zeros outside the row's P+1) in shared memory, so the 8 rows
+// are decoded fully unrolled with static register indices and no per-row
+// control flow.  A = 0: the per-row sweep with a P+1 plane window.
+template <int P, int D, int EG, int S, int A>
 __global__ void __launch_bounds__(256) k_residual_tma(const ResTmaArgs a, const __grid_constant__ CUtensorMap map) {
   extern __shared__ __align__(1024) unsigned char sm_raw[];
   __shared__ double s_red[2 * EG][8];
@@ -242,6 +248,77 @@ __global__ void __launch_bounds__(256) k_residual_tma(const ResTmaArgs a, const 
           Tw[q][slot] = sacc;
         }
       };
+      if constexpr (A > 0) {
+        constexpr int NW = P + 1 + A;
+        double Tn[EG][NW];
+        auto plane_into = [&](int slot, int ai) {
+          const double* Ub = sR + (clampi(ai, n0) - a_lo) * a.lt_cap + wo;
+#pragma unroll
+          for (int q = 0; q < EG; ++q) {
+            double sacc = 0.0;
+#pragma unroll
+            for (int k = 0; k <= P; ++k) sacc = fma(wk[k], Ub[q * a.na_cap * a.lt_cap + k], sacc);
+            Tn[q][slot] = sacc;
+          }
+        };
+        int abase = __ldg(g0g + ybeg);
+#pragma unroll
+        for (int k = 0; k < NW; ++k) plane_into(k, abase + k);
+        double* sVp = reinterpret_cast<double*>(sm_raw + S * SL.stage_bytes + S * 8 + 8) +
+                      static_cast<std::int64_t>(EG) * a.na_cap * a.lt_cap;  // [2][kResR][NW]
+        const int col = tid < W ? tid : 0;
+        for (int c = 0; c < nchunks; ++c, ++g) {
+          const int st = g % S;
+          const unsigned char* base = sm_raw + st * SL.stage_bytes;
+          const double* sq = reinterpret_cast<const double*>(base) + col;
+          const double* sv = reinterpret_cast<const double*>(base + SL.v_off);
+          const int* sg = reinterpret_cast<const int*>(base + SL.g_off);
+          const int yc = (ch0 + c) * kResR;
+          const int jn = (m0 - yc) < kResR ? (m0 - yc) : kResR;
+          mbar_wait(&bars[st], (g / S) & 1);
+          // slide the window to the chunk's first row (CTA-uniform)
+          const int gf = sg[0];
+          while (abase < gf) {
+#pragma unroll
+            for (int q = 0; q < EG; ++q)
+#pragma unroll
+              for (int k = 0; k + 1 < NW; ++k) Tn[q][k] = Tn[q][k + 1];
+            plane_into(NW - 1, abase + NW);
+            ++abase;
+          }
+          // the chunk's basis rows expanded to the window's NW columns
+          double* Vb = sVp + (c & 1) * kResR * NW;
+          for (int i = tid; i < kResR * NW; i += nthr) {
+            const int j = i / NW, sidx = i - j * NW;
+            const int k = j < jn ? sidx - (sg[j] - abase) : -1;
+            Vb[i] = (k >= 0 && k <= P) ? sv[j * (P + 1) + k] : 0.0;
+          }
+          __syncthreads();  // Vb visible; every thread is done with the previous chunk's stage
+          if (tid == 0 && g >= 1 && g - 1 + S < gtotal) {
+            fence_proxy_async();
+            issue(g - 1 + S);
+          }
+#pragma unroll
+          for (int j = 0; j < kResR; ++j) {
+            if (j < jn) {  // CTA-uniform
+              const double qv = sq[j * W];
+              double v[NW];
+#pragma unroll
+              for (int k = 0; k < NW; ++k) v[k] = Vb[j * NW + k];
+#pragma unroll
+              for (int q = 0; q < EG; ++q) {
+                double e = qv;
+#pragma unroll
+                for (int k = 0; k < NW; ++k) e = fma(-v[k], Tn[q][k], e);
+                l2[q] = fma(e, e, l2[q]);
+                const unsigned long long eb =
+                    static_cast<unsigned long long>(__double_as_longlong(e)) & 0x7fffffffffffffffull;
+                li[q] = li[q] > eb ? li[q] : eb;
+              }
+            }
+          }
+        }
+      } else {
       int abase = __ldg(g0g + ybeg);
 #pragma unroll
       for (int k = 0; k <= P; ++k) reduce_into(k, abase + k);
@@ -283,22 +360,51 @@ __global__ void __launch_bounds__(256) k_residual_tma(const ResTmaArgs a, const 
 #pragma unroll
         for (int u = 0; u <= P; ++u) {
           while (gnext == abase) {  // CTA-uniform
-            const double* vr = sv + jl * (P + 1);
-            double v[P + 1];
-#pragma unroll
-            for (int k = 0; k <= P; ++k) v[k] = vr[k];
-            const double qv = sq[jl * W];
             // e = q - sum_k v_k T_k as one FMA chain from q; L-inf as integer
             // max of |e|'s bit pattern (off the FP64 pipe); inactive (padding)
-            // threads compute on finite staged values and are zeroed at the end
+            // threads compute on finite staged values and are zeroed at the
+            // end.  Two rows of the same window per step when the chunk has
+            // them (twice the independent chains per thread).
+            const bool two = jl + 1 < jn && sg[jl + 1] == abase;  // CTA-uniform
+            const double* vr = sv + jl * (P + 1);
+            if (two) {
+              double v0[P + 1], v1[P + 1];
 #pragma unroll
-            for (int q = 0; q < EG; ++q) {
-              double e = qv;
+              for (int k = 0; k <= P; ++k) {
+                v0[k] = vr[k];
+                v1[k] = vr[P + 1 + k];
+              }
+              const double q0 = sq[jl * W], q1 = sq[(jl + 1) * W];
 #pragma unroll
-              for (int k = 0; k <= P; ++k) e = fma(-v[k], Tw[q][(u + k) % (P + 1)], e);
-              l2[q] = fma(e, e, l2[q]);
-              const unsigned long long eb = static_cast<unsigned long long>(__double_as_longlong(e)) & 0x7fffffffffffffffull;
-              li[q] = li[q] > eb ? li[q] : eb;
+              for (int q = 0; q < EG; ++q) {
+                double e = q0, f = q1;
+#pragma unroll
+                for (int k = 0; k <= P; ++k) {
+                  e = fma(-v0[k], Tw[q][(u + k) % (P + 1)], e);
+                  f = fma(-v1[k], Tw[q][(u + k) % (P + 1)], f);
+                }
+                l2[q] = fma(e, e, l2[q]);
+                l2[q] = fma(f, f, l2[q]);
+                const unsigned long long eb = static_cast<unsigned long long>(__double_as_longlong(e)) & 0x7fffffffffffffffull;
+                const unsigned long long fb = static_cast<unsigned long long>(__double_as_longlong(f)) & 0x7fffffffffffffffull;
+                const unsigned long long mb = eb > fb ? eb : fb;
+                li[q] = li[q] > mb ? li[q] : mb;
+              }
+              ++jl;  // (jl + 1 < jn: still inside the chunk)
+            } else {
+              double v[P + 1];
+#pragma unroll
+              for (int k = 0; k <= P; ++k) v[k] = vr[k];
+              const double qv = sq[jl * W];
+#pragma unroll
+              for (int q = 0; q < EG; ++q) {
+                double e = qv;
+#pragma unroll
+                for (int k = 0; k <= P; ++k) e = fma(-v[k], Tw[q][(u + k) % (P + 1)], e);
+                l2[q] = fma(e, e, l2[q]);
+                const unsigned long long eb = static_cast<unsigned long long>(__double_as_longlong(e)) & 0x7fffffffffffffffull;
+                li[q] = li[q] > eb ? li[q] : eb;
+              }
             }
             advance();
           }
@@ -308,6 +414,7 @@ __global__ void __launch_bounds__(256) k_residual_tma(const ResTmaArgs a, const 
         }
       }
     }
+      }
     // ---- CTA partials of this pass's epochs
     double lif[EG];
 #pragma unroll
@@ -367,23 +474,34 @@ __global__ void k_res_reduce(const ResTmaArgs a, int nblocks, int ctas) {
 
 template <int P>
 struct ResTmaLaunch {
-  template <int D, int EG>
+  template <int D, int EG, int A>
   static void go(const ResTmaArgs& a, const CUtensorMap& map, int threads, cudaStream_t s) {
     constexpr int S = 3;
-    const ResStage SL = res_stage(a.W, P);
     const size_t smem = res_tma_smem(P, a.W, EG, a.na_cap, a.lt_cap, S);
-    cudaFuncSetAttribute(k_residual_tma<P, D, EG, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_residual_tma<P, D, EG, S, A>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
     dim3 grid(a.ntc * a.nrr, a.nblocks);
-    k_residual_tma<P, D, EG, S><<<grid, threads, smem, s>>>(a, map);
+    k_residual_tma<P, D, EG, S, A><<<grid, threads, smem, s>>>(a, map);
     k_res_reduce<<<(a.nblocks + 127) / 128, 128, 0, s>>>(a, a.nblocks, a.ntc * a.nrr);
+  }
+  template <int D>
+  static void dense(const ResTmaArgs& a, const CUtensorMap& map, int threads, cudaStream_t s) {
+    if constexpr (P <= 6) {
+      switch (a.dense_a) {
+        case 1: go<D, 4, 1>(a, map, threads, s); return;
+        case 2: go<D, 4, 2>(a, map, threads, s); return;
+        case 3: go<D, 4, 3>(a, map, threads, s); return;
+        default: break;
+      }
+    }
+    go<D, 4, 0>(a, map, threads, s);
   }
   static int run(const ResTmaArgs& a, const CUtensorMap& map, int threads, cudaStream_t s) {
     const int eg = a.eg;
     if (a.D == 2)
-      eg >= 4 ? go<2, 4>(a, map, threads, s) : (eg >= 2 ? go<2, 2>(a, map, threads, s) : go<2, 1>(a, map, threads, s));
+      eg >= 4 ? dense<2>(a, map, threads, s) : (eg >= 2 ? go<2, 2, 0>(a, map, threads, s) : go<2, 1, 0>(a, map, threads, s));
     else
-      eg >= 4 ? go<3, 4>(a, map, threads, s) : (eg >= 2 ? go<3, 2>(a, map, threads, s) : go<3, 1>(a, map, threads, s));
+      eg >= 4 ? dense<3>(a, map, threads, s) : (eg >= 2 ? go<3, 2, 0>(a, map, threads, s) : go<3, 1, 0>(a, map, threads, s));
     return 2;
   }
 };

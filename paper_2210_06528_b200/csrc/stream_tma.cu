@@ -1336,7 +1336,10 @@ struct BacksubLaunch {
 };
 
 // ---------------------------------------------------------------- decode
-template <int P, int D, int S, int MB = 1, bool ERR = true>
+// WIN (D = 3): the host has checked that every CTA's axis-2 window fits, so
+// only the shared-window form is compiled (no (P+1)^2 per-thread plane
+// registers: higher occupancy).
+template <int P, int D, int S, int MB = 1, bool ERR = true, bool WIN = false>
 __global__ void __launch_bounds__(256, MB) k_decode_tma(const DecodeSweepArgs a, const __grid_constant__ CUtensorMap map,
                                                     const TmaGeom geo) {
   pdl_enter();
@@ -1436,8 +1439,8 @@ __global__ void __launch_bounds__(256, MB) k_decode_tma(const DecodeSweepArgs a,
   int abase = __ldg(a.g0_0 + y0);
   double Tw[P + 1];
 #pragma unroll
-  for (int k = 0; k <= P; ++k) Tw[k] = active ? plane(abase + k) : 0.0;
-  constexpr int NV = D == 2 ? (P + 1) : (P + 1) * (P + 1);
+  for (int k = 0; k <= P; ++k) Tw[k] = (active && !WIN) ? plane(abase + k) : 0.0;
+  constexpr int NV = D == 2 ? (P + 1) : (WIN ? 1 : (P + 1) * (P + 1));
   double nxt[NV];
   auto fetch_plane = [&](int ai) {
     const int a2 = ai < a.N0 ? ai : a.N0 - 1;
@@ -1482,7 +1485,7 @@ __global__ void __launch_bounds__(256, MB) k_decode_tma(const DecodeSweepArgs a,
     g2base = __ldg(a.g0_2 + jf);
     rw = __ldg(a.g0_2 + jl) - g2base + P + 1;
   }
-  const bool win = D == 3 && B1 == 1 && rw <= geo.lt_cap && rw <= nthr;  // CTA-uniform
+  const bool win = WIN || (D == 3 && B1 == 1 && rw <= geo.lt_cap && rw <= nthr);  // CTA-uniform
   double lv[P + 1];  // this thread's window column of the plane after next (raw lattice values)
   int rbuf = 0;
   auto fetch_window = [&](int ai) {
@@ -1493,6 +1496,26 @@ __global__ void __launch_bounds__(256, MB) k_decode_tma(const DecodeSweepArgs a,
       for (int k1 = 0; k1 <= P; ++k1) lv[k1] = __ldg(L0 + static_cast<std::int64_t>(g1 + k1) * a.N2);
     }
   };
+  if (WIN) {  // the initial window planes through the shared window as well
+#pragma unroll
+    for (int k = 0; k <= P; ++k) {
+      fetch_window(abase + k);
+      double* R = sR + rbuf * geo.lt_cap;
+      if (tid < rw) {
+        double r = 0.0;
+#pragma unroll
+        for (int k1 = 0; k1 <= P; ++k1) r = fma(w1[k1], lv[k1], r);
+        R[tid] = r;
+      }
+      __syncthreads();
+      const double* Rg = R + (g2 > g2base ? g2 - g2base : 0);
+      double sres = 0.0;
+#pragma unroll
+      for (int k2 = 0; k2 <= P; ++k2) sres = fma(w2[k2], Rg[k2], sres);
+      Tw[k] = active ? sres : 0.0;
+      rbuf ^= 1;
+    }
+  }
   if (win)
     fetch_window(abase + P + 1);
   else if (active)
@@ -1685,6 +1708,12 @@ struct DecodeSweepLaunch {
     if (mb >= 4) {
       cudaFuncSetAttribute(k_decode_tma<P, D, S, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
       launch_pdl(k_decode_tma<P, D, S, 4>, grid, dim3(g.B1 * g.B2), smem, s, a, map, g);
+      return;
+    }
+    if (D == 3 && a.win && a.err) {
+      cudaFuncSetAttribute(k_decode_tma<P, D, S, 1, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem));
+      launch_pdl(k_decode_tma<P, D, S, 1, true, true>, grid, dim3(g.B1 * g.B2), smem, s, a, map, g);
       return;
     }
     if (!a.err) {  // no error field: L2 / L-inf only

@@ -173,3 +173,17 @@ def test_knot_vectors_bit_exact():
     for i in range(int(g["nkv"][0])):
         p, n, cl, cr = (int(x) for x in g[f"kv{i}_meta"])
         assert np.array_equal(m.make_knot_vector(p, n, 0.0, 1.0, bool(cl), bool(cr)).knots, g[f"kv{i}_knots"])
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 8])
+def test_shard_box_covers_its_blocks(n):
+    """The slab a sharded rank uploads (mfadd_shard_box) is exactly the union of
+    its blocks' input rows along axis 0 and contains the rows it decodes."""
+    dec = m.partition((4096, 512), [(0, 1), (0, 1)], (16, 4), 5, (32, 32), 5)
+    bd = dec.block_dims_array()
+    for r in range(n):
+        blo, bhi, ilo, ihi = m.shard_range(dec, r, n)
+        lo, hi = m.shard_box(dec, r, n)
+        assert lo == min(int(bd[b, 0, 12]) for b in range(blo, bhi))
+        assert hi == max(int(bd[b, 0, 13]) for b in range(blo, bhi))
+        assert lo <= ilo < ihi <= hi
