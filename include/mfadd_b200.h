@@ -172,8 +172,11 @@ void mfadd_comm_free(mfadd_comm* comm);
  * layout, but a host field is read only in the rank's slab (the axis-0 input
  * rows its blocks touch, mfadd_shard_range's box) and a device field must
  * hold valid data there; mfadd_solve_host's out_error receives the input
- * rows the rank decoded ([in_lo, in_hi)), out_controls the whole gathered
- * lattice.  An asynchronous NCCL error, or no progress for
+ * rows the rank decoded ([in_lo, in_hi)) and out_controls the lattice rows
+ * the rank owns (mfadd_shard_ctrl_rows): only the halo rows a neighbour's
+ * decode reads cross NVLink, never the whole lattice.  Call
+ * mfadd_solver_gather_controls (collective) when every rank needs the whole
+ * lattice (mfadd_solver_controls / device_controls then hold all of it).  An asynchronous NCCL error, or no progress for
  * MFADD_NCCL_TIMEOUT_S seconds (default 600), aborts the communicator and
  * returns MFADD_ECUDA (later calls on it fail fast). */
 int mfadd_solver_create_sharded(mfadd_context* ctx, const mfadd_decomposition* dec, const mfadd_solver_config* cfg,
@@ -181,6 +184,11 @@ int mfadd_solver_create_sharded(mfadd_context* ctx, const mfadd_decomposition* d
 /* Host-side shard plan: block ids [blo, bhi) and own input rows [in_lo, in_hi). */
 int mfadd_shard_range(const mfadd_decomposition* dec, int rank, int nranks, int* blo, int* bhi, int64_t* in_lo,
                       int64_t* in_hi);
+/* The lattice rows [own_lo, own_hi) along axis 0 a rank owns. */
+int mfadd_shard_ctrl_rows(const mfadd_decomposition* dec, int rank, int nranks, int64_t* own_lo, int64_t* own_hi);
+/* Collective over a sharded solver's communicator: every rank's owned lattice
+ * rows to every rank (no-op for a one-device solver). */
+int mfadd_solver_gather_controls(mfadd_solver* s);
 /* The axis-0 input rows [box_lo, box_hi) a rank's solve reads (its slab). */
 int mfadd_shard_box(const mfadd_decomposition* dec, int rank, int nranks, int64_t* box_lo, int64_t* box_hi);
 /* Per-epoch exchange layout with one peer (recv=0: what `rank` sends, 1: what it

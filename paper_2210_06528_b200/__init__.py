@@ -9,7 +9,7 @@ from .api import (BandedCollocation, BlockDim, BlockLayout, BlockState, Context,
                   MfaddError, OutOfRange, PhaseTimings, RuntimeFault, SharedDofMap, SingularFitError, SolveResult,
                   Solver, SolverConfig, collocation_matrix, compression_ratio, decode, default_context, delta_width,
                   exchange_volume, find_span, fit_unconstrained, make_knot_vector, partition, solve, Comm,
-                  shard_range, shard_box, shard_exchange, solve_loopback, Side, eval_points, eval_deriv, eval_deriv_sided,
+                  shard_range, shard_box, shard_ctrl_rows, shard_exchange, solve_loopback, Side, eval_points, eval_deriv, eval_deriv_sided,
                   continuity_jumps, write_mfa, read_mfa, RawScalar, RawByteOrder, read_raw_grid,
                   ResidualStats, residual_error, SpanBasis, basis_funs, basis_derivs, basis_funs_batch)
 

@@ -112,6 +112,8 @@ _SIGS = {
                                               C.POINTER(C.c_void_p)]),
     "mfadd_shard_range": (C.c_int, [C.c_void_p, C.c_int, C.c_int, c_ip, c_ip, c_lp, c_lp]),
     "mfadd_shard_box": (C.c_int, [C.c_void_p, C.c_int, C.c_int, c_lp, c_lp]),
+    "mfadd_shard_ctrl_rows": (C.c_int, [C.c_void_p, C.c_int, C.c_int, c_lp, c_lp]),
+    "mfadd_solver_gather_controls": (C.c_int, [C.c_void_p]),
     "mfadd_shard_exchange": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, c_lp, C.c_int64]),
     "mfadd_solve_loopback": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(SolverConfigC), C.c_int, C.c_void_p,
                                        C.c_void_p, C.c_void_p, C.POINTER(SolveSummaryC), C.POINTER(EpochStatsC),

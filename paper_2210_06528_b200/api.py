@@ -881,6 +881,13 @@ def shard_box(dec: "Decomposition", rank: int, nranks: int):
     return lo.value, hi.value
 
 
+def shard_ctrl_rows(dec: "Decomposition", rank: int, nranks: int):
+    """(own_lo, own_hi): the lattice rows along axis 0 `rank` owns."""
+    lo, hi = C.c_int64(), C.c_int64()
+    _check(L.load().mfadd_shard_ctrl_rows(dec._h, rank, nranks, C.byref(lo), C.byref(hi)))
+    return lo.value, hi.value
+
+
 def shard_exchange(dec: "Decomposition", rank: int, nranks: int, peer: int, recv: bool) -> np.ndarray:
     """Per-epoch exchange layout of `rank` with `peer`: rows (holder block, i0, i1, i2) in buffer order."""
     lib = L.load()
@@ -1024,6 +1031,10 @@ class Solver:
         _check(L.load().mfadd_solve_host_batch(self._h, n, fp, cp, ep, sums))
         self.summary = sums[n - 1]
         return list(sums)
+
+    def gather_controls(self):
+        """Collective (sharded solver): every rank's owned lattice rows to every rank."""
+        _check(L.load().mfadd_solver_gather_controls(self._h))
 
     def set_profiling(self, on: bool = True):
         _check(L.load().mfadd_solver_set_profiling(self._h, int(on)))

@@ -763,6 +763,9 @@ struct mfadd_solver {
   std::vector<double> h_block_errs;
   // shard: rank of nranks owns blocks [srange.blo, srange.bhi)
   int rank = 0, nranks = 1;
+  // lattice rows (axis 0) this rank's decode reads: its own rows plus a halo
+  // of at most P rows per side from the neighbouring ranks
+  std::int64_t need_lo = 0, need_hi = 0;
   mfb::ShardRange srange;
   std::vector<int> local_of;  // global block id -> local index (-1: other rank)
   mfadd_comm* comm = nullptr;
@@ -1341,7 +1344,8 @@ void plan_residual_tma(mfadd_solver* s) {
       const AxisProb& pr = wl.probs[static_cast<std::size_t>(pid)];
       for (int y = 0; y < pr.m; y += 8) adv = std::max(adv, g0_of(pr, std::min(pr.m - 1, y + 7)) - g0_of(pr, y));
     }
-    s->res_dense = (s->res_eg == 4 && p <= 6 && adv <= 3 && !std::getenv("MFADD_RES_ROWS")) ? std::max(1, adv) : 0;
+    // (the dense sweep is built only with -DMFB_RES_DENSE: measured slower)
+    s->res_dense = (s->res_eg == 4 && p <= 6 && adv <= 3 && std::getenv("MFADD_RES_DENSE")) ? std::max(1, adv) : 0;
   }
   s->res_snap = true;
   s->snap.alloc(static_cast<std::size_t>(s->cfg.max_outer_iterations + 1) * static_cast<std::size_t>(wl.total_p));
@@ -1632,6 +1636,16 @@ std::unique_ptr<mfadd_solver> create_solver(mfadd_context* ctx, const mfadd_deco
     }
     s->partial.alloc(npart * 2);
     s->red2.alloc(2);
+    s->need_lo = 0;
+    s->need_hi = d.n_ctrl[0];
+    if (nranks > 1 && s->tma_decode) {  // spans of the rank's first / last own input row (decode.cpp:63-79)
+      const std::vector<double>& kn0 = d.knots[0];
+      auto span = [&](std::int64_t j) {
+        return host_find_span(kn0, p, static_cast<double>(j) / static_cast<double>(d.grid[0] - 1));
+      };
+      s->need_lo = std::max<std::int64_t>(0, span(s->srange.in_lo) - p);
+      s->need_hi = std::min<std::int64_t>(d.n_ctrl[0], span(s->srange.in_hi - 1) + 1);
+    }
     s->ticket.alloc(1);
     CK(cudaMemsetAsync(s->ticket.p, 0, sizeof(unsigned), st));
     s->unit_g0.upload(std::vector<int>{0}, st);
@@ -2067,7 +2081,8 @@ struct Transport {
   virtual ~Transport() = default;
   virtual void exchange(std::vector<mfadd_solver*>& g) = 0;               // send -> recv buffers
   virtual void max_u64(std::vector<mfadd_solver*>& g, std::size_t off, std::size_t n, bool pairs) = 0;
-  virtual void gather_lattice(std::vector<mfadd_solver*>& g) = 0;         // owned rows to every rank
+  // owned lattice rows to the ranks whose decode reads them (full: to every rank)
+  virtual void gather_lattice(std::vector<mfadd_solver*>& g, bool full) = 0;
   // elementwise sum of a device array that every rank filled at its own entries
   using ArrayOf = std::pair<double*, std::size_t> (*)(mfadd_solver*);
   virtual void sum_f64(std::vector<mfadd_solver*>& g, ArrayOf arr) = 0;
@@ -2075,6 +2090,21 @@ struct Transport {
   // rank decoded all rows (generic decode path: identical values), max linf
   virtual void reduce_err(std::vector<mfadd_solver*>& g, bool sum_l2) = 0;
 };
+
+// The lattice rows rank q's decode reads (mfadd_solver::need_lo/need_hi of q).
+void lattice_need(const mfadd_solver* s, int q, std::int64_t& lo, std::int64_t& hi) {
+  const Decomp& d = s->dec;
+  lo = 0;
+  hi = d.n_ctrl[0];
+  if (!s->tma_decode) return;
+  const mfb::ShardRange r = mfb::shard_range(d, q, s->nranks);
+  const int p = d.degree;
+  auto span = [&](std::int64_t j) {
+    return host_find_span(d.knots[0], p, static_cast<double>(j) / static_cast<double>(d.grid[0] - 1));
+  };
+  lo = std::max<std::int64_t>(0, span(r.in_lo) - p);
+  hi = std::min<std::int64_t>(d.n_ctrl[0], span(r.in_hi - 1) + 1);
+}
 
 std::int64_t lattice_row_elems(const Decomp& d) {
   std::int64_t r = 1;
@@ -2103,7 +2133,7 @@ struct NcclTransport : Transport {
     const auto a = arr(g[0]);
     NCK(ncclAllReduce(a.first, a.first, a.second, ncclFloat64, ncclSum, g[0]->comm->comm, g[0]->ctx->stream));
   }
-  void gather_lattice(std::vector<mfadd_solver*>& g) override {
+  void gather_lattice(std::vector<mfadd_solver*>& g, bool full) override {
     mfadd_solver* s = g[0];
     const Decomp& d = s->dec;
     const std::int64_t row = lattice_row_elems(d);
@@ -2111,10 +2141,15 @@ struct NcclTransport : Transport {
     for (int q = 0; q < s->nranks; ++q) {
       if (q == s->rank) continue;
       const mfb::ShardRange mine = s->srange, theirs = mfb::shard_range(d, q, s->nranks);
-      NCK(ncclSend(s->lattice.p + mine.own_lo * row, (mine.own_hi - mine.own_lo) * row, ncclFloat64, q, s->comm->comm,
-                   s->ctx->stream));
-      NCK(ncclRecv(s->lattice.p + theirs.own_lo * row, (theirs.own_hi - theirs.own_lo) * row, ncclFloat64, q,
-                   s->comm->comm, s->ctx->stream));
+      std::int64_t qlo = 0, qhi = d.n_ctrl[0];  // rows q's decode reads (full: all)
+      if (!full) lattice_need(s, q, qlo, qhi);
+      const std::int64_t s0 = std::max(mine.own_lo, qlo), s1 = std::min(mine.own_hi, qhi);
+      const std::int64_t r0 = std::max(theirs.own_lo, full ? std::int64_t{0} : s->need_lo),
+                         r1 = std::min(theirs.own_hi, full ? d.n_ctrl[0] : s->need_hi);
+      if (s1 > s0)
+        NCK(ncclSend(s->lattice.p + s0 * row, (s1 - s0) * row, ncclFloat64, q, s->comm->comm, s->ctx->stream));
+      if (r1 > r0)
+        NCK(ncclRecv(s->lattice.p + r0 * row, (r1 - r0) * row, ncclFloat64, q, s->comm->comm, s->ctx->stream));
     }
     NCK(ncclGroupEnd());
   }
@@ -2165,15 +2200,18 @@ struct LoopbackTransport : Transport {
     }
     for (mfadd_solver* s : g) CK(cudaMemcpy(arr(s).first, acc.data(), n * sizeof(double), cudaMemcpyHostToDevice));
   }
-  void gather_lattice(std::vector<mfadd_solver*>& g) override {
+  void gather_lattice(std::vector<mfadd_solver*>& g, bool full) override {
     const Decomp& d = g[0]->dec;
     const std::int64_t row = lattice_row_elems(d);
     for (mfadd_solver* q : g)
-      for (mfadd_solver* r : g)
-        if (q != r)
-          CK(cudaMemcpyAsync(r->lattice.p + q->srange.own_lo * row, q->lattice.p + q->srange.own_lo * row,
-                             (q->srange.own_hi - q->srange.own_lo) * row * sizeof(double), cudaMemcpyDeviceToDevice,
-                             r->ctx->stream));
+      for (mfadd_solver* r : g) {
+        if (q == r) continue;
+        const std::int64_t r0 = std::max(q->srange.own_lo, full ? std::int64_t{0} : r->need_lo),
+                           r1 = std::min(q->srange.own_hi, full ? d.n_ctrl[0] : r->need_hi);
+        if (r1 > r0)
+          CK(cudaMemcpyAsync(r->lattice.p + r0 * row, q->lattice.p + r0 * row, (r1 - r0) * row * sizeof(double),
+                             cudaMemcpyDeviceToDevice, r->ctx->stream));
+      }
   }
   void reduce_err(std::vector<mfadd_solver*>& g, bool sum_l2) override {
     double l2 = 0.0, li = 0.0, v[2];
@@ -2364,7 +2402,7 @@ void solve_group(std::vector<mfadd_solver*>& g, const std::vector<const double*>
     launches[0] += launch_residuals_all(s0, fields[0], s0->ctx->stream);
   }
   for (std::size_t r = 0; r < g.size(); ++r) launches[r] += shard_assemble_decode(g[r], fields[r]);
-  tr.gather_lattice(g);
+  tr.gather_lattice(g, false);  // the halo rows each rank's decode reads (no all-gather)
   tmark("assembled", 0);
   for (std::size_t r = 0; r < g.size(); ++r) launches[r] += shard_decode(g[r], fields[r]);
   tr.reduce_err(g, s0->tma_decode);
@@ -2472,6 +2510,20 @@ std::size_t upload_field(mfadd_solver* s, const double* host, double* dev, cudaS
   CK(cudaMemcpyAsync(dev + lo * row, host + lo * row, n * sizeof(double), cudaMemcpyHostToDevice, st));
   return n * sizeof(double);
 }
+// Lattice -> host: a sharded solver returns the lattice rows it owns (its
+// blocks' owned controls; mfadd_solver_gather_controls assembles the rest).
+void download_controls(mfadd_solver* s, double* host, cudaStream_t st) {
+  const Decomp& d = s->dec;
+  std::int64_t row = 1;
+  for (int k = 1; k < d.rank; ++k) row *= d.n_ctrl[k];
+  std::int64_t lo = 0, hi = d.n_ctrl[0];
+  if (s->nranks > 1) {
+    lo = s->srange.own_lo;
+    hi = s->srange.own_hi;
+  }
+  CK(cudaMemcpyAsync(host + lo * row, s->lattice.p + lo * row, static_cast<std::size_t>((hi - lo) * row) * sizeof(double),
+                     cudaMemcpyDeviceToHost, st));
+}
 // Error field -> host: a sharded solver returns the input rows it decoded.
 void download_error(mfadd_solver* s, double* host, cudaStream_t st) {
   const Decomp& d = s->dec;
@@ -2515,8 +2567,7 @@ MFB_API int mfadd_solve_host(mfadd_solver* s, const double* field_host, double* 
     cudaStream_t st = s->ctx->stream;
     upload_field(s, field_host, s->field_buf.p, st);
     solve_impl(s, s->field_buf.p);
-    if (out_controls_host)
-      CK(cudaMemcpyAsync(out_controls_host, s->lattice.p, s->lattice.n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (out_controls_host) download_controls(s, out_controls_host, st);
     if (out_error_host) download_error(s, out_error_host, st);
     CK(cudaStreamSynchronize(st));
     if (out) *out = s->summary;
@@ -2544,9 +2595,7 @@ MFB_API int mfadd_solve_host_batch(mfadd_solver* s, int n, const double* const* 
         if (s->field_buf.n != nf) s->field_buf.alloc(nf);
         upload_field(s, fields_host[i], s->field_buf.p, s->ctx->stream);
         solve_impl(s, s->field_buf.p);
-        if (out_controls_host && out_controls_host[i])
-          CK(cudaMemcpyAsync(out_controls_host[i], s->lattice.p, s->lattice.n * sizeof(double), cudaMemcpyDeviceToHost,
-                             s->ctx->stream));
+        if (out_controls_host && out_controls_host[i]) download_controls(s, out_controls_host[i], s->ctx->stream);
         if (out_errors_host && out_errors_host[i]) download_error(s, out_errors_host[i], s->ctx->stream);
         CK(cudaStreamSynchronize(s->ctx->stream));
         if (out) out[i] = s->summary;
@@ -2752,6 +2801,17 @@ MFB_API int mfadd_solver_block_errors(const mfadd_solver* s, int epoch, double* 
 }
 
 MFB_API const double* mfadd_solver_device_controls(const mfadd_solver* s) { return s->lattice.p; }
+
+MFB_API int mfadd_solver_gather_controls(mfadd_solver* s) {
+  return guarded([&] {
+    if (s->nranks <= 1) return;
+    ContextScope scope(s->ctx);
+    std::vector<mfadd_solver*> g{s};
+    NcclTransport tr;
+    tr.gather_lattice(g, true);
+    sync_sharded(s);
+  });
+}
 
 MFB_API int mfadd_solver_set_profiling(mfadd_solver* s, int on) {
   s->tl.on = on != 0;
@@ -3127,6 +3187,15 @@ MFB_API int mfadd_shard_range(const mfadd_decomposition* dec, int rank, int nran
   });
 }
 
+MFB_API int mfadd_shard_ctrl_rows(const mfadd_decomposition* dec, int rank, int nranks, int64_t* own_lo,
+                                  int64_t* own_hi) {
+  return guarded([&] {
+    const mfb::ShardRange r = mfb::shard_range(dec->d, rank, nranks);
+    *own_lo = r.own_lo;
+    *own_hi = r.own_hi;
+  });
+}
+
 MFB_API int mfadd_shard_box(const mfadd_decomposition* dec, int rank, int nranks, int64_t* box_lo, int64_t* box_hi) {
   return guarded([&] {
     const mfb::ShardRange r = mfb::shard_range(dec->d, rank, nranks);
@@ -3189,8 +3258,9 @@ MFB_API int mfadd_solve_loopback(mfadd_context* ctx, const mfadd_decomposition* 
     LoopbackTransport tr;
     solve_group(g, fields, tr);
     mfadd_solver* s0 = g[0];
-    if (out_controls)
-      CK(cudaMemcpy(out_controls, s0->lattice.p, s0->lattice.n * sizeof(double), cudaMemcpyDeviceToHost));
+    if (out_controls)  // each rank's owned lattice rows
+      for (mfadd_solver* s : g) download_controls(s, out_controls, s->ctx->stream);
+    CK(cudaStreamSynchronize(ctx->stream));
     if (out_error) {  // each rank's own input rows
       const mfb::Decomp& d = dec->d;
       std::int64_t row = 1;

@@ -35,6 +35,10 @@ namespace {
 
 constexpr unsigned kFullMask = 0xffffffffu;
 constexpr int kResR = 8;  // rows per TMA stage
+#ifndef MFB_RES_S
+#define MFB_RES_S 3
+#endif
+constexpr int kResS = MFB_RES_S;  // TMA ring stages
 
 struct ResStage {
   int q_bytes, v_off, g_off, stage_bytes;
@@ -252,7 +256,10 @@ __global__ void __launch_bounds__(256) k_residual_tma(const ResTmaArgs a, const 
         constexpr int NW = P + 1 + A;
         double Tn[EG][NW];
         auto plane_into = [&](int slot, int ai) {
-          const double* Ub = sR + (clampi(ai, n0) - a_lo) * a.lt_cap + wo;
+          // planes past the range's last one only meet zero coefficients;
+          // clamp them onto staged (finite) data
+          const int ac = min(clampi(ai, n0), a_hi);
+          const double* Ub = sR + (ac - a_lo) * a.lt_cap + wo;
 #pragma unroll
           for (int q = 0; q < EG; ++q) {
             double sacc = 0.0;
@@ -476,7 +483,7 @@ template <int P>
 struct ResTmaLaunch {
   template <int D, int EG, int A>
   static void go(const ResTmaArgs& a, const CUtensorMap& map, int threads, cudaStream_t s) {
-    constexpr int S = 3;
+    constexpr int S = kResS;
     const size_t smem = res_tma_smem(P, a.W, EG, a.na_cap, a.lt_cap, S);
     cudaFuncSetAttribute(k_residual_tma<P, D, EG, S, A>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
@@ -486,6 +493,7 @@ struct ResTmaLaunch {
   }
   template <int D>
   static void dense(const ResTmaArgs& a, const CUtensorMap& map, int threads, cudaStream_t s) {
+#ifdef MFB_RES_DENSE  // measured slower than the per-row sweep on C3/C4/C5: not built by default
     if constexpr (P <= 6) {
       switch (a.dense_a) {
         case 1: go<D, 4, 1>(a, map, threads, s); return;
@@ -494,6 +502,7 @@ struct ResTmaLaunch {
         default: break;
       }
     }
+#endif
     go<D, 4, 0>(a, map, threads, s);
   }
   static int run(const ResTmaArgs& a, const CUtensorMap& map, int threads, cudaStream_t s) {
@@ -525,7 +534,7 @@ int dispatch_res(int p, Args&&... args) {
 }  // namespace
 
 size_t residual_tma_smem(int degree, int W, int eg, int na_cap, int lt_cap) {
-  return res_tma_smem(degree, W, eg, na_cap, lt_cap, 3);
+  return res_tma_smem(degree, W, eg, na_cap, lt_cap, kResS);
 }
 
 int launch_residual_tma(int degree, const ResTmaArgs& a, const CUtensorMap& map, int threads, cudaStream_t s) {
