@@ -213,6 +213,44 @@ def kernel_bytes(cfg, dec, ab):
     return out
 
 
+def kernel_flops(cfg, dec, ab, epochs_exchanged):
+    """Algorithmic FP64 flops per launch of each kernel group (banded
+    arithmetic): the FP64 side of every kernel's roofline."""
+    import numpy as np
+    bd = dec.block_dims_array()
+    D, p = dec.rank, dec.degree
+    m = (bd[:, :, 13] - bd[:, :, 12]).astype(np.float64)
+    n = (bd[:, :, 9] - bd[:, :, 8]).astype(np.float64)
+    q = float(ab["q_loc"])
+    rows = float(sum(m[b, k] for b in range(dec.nblocks) for k in range(D))) + float(sum(cfg.grid))
+    out = {"basis_rows": 3.0 * p * (p + 1) * rows,
+           "gram_chol": float(sum(2 * (m[b, k] + n[b, k]) * (p + 1) ** 2 for b in range(dec.nblocks) for k in range(D))),
+           "epoch": 2.0 * ab["ns_total"],
+           "decode": 2.0 * (p + 1) * ab["points"] * (1.0 + float(dec.n_ctrl[0]) / cfg.grid[0]) + 4.0 * ab["points"],
+           "residual": (epochs_exchanged + 1) * 2.0 * (p + 1) * q * 1.3}
+    if D >= 2:
+        t1 = float(sum(n[b, 0] * np.prod(m[b, 1:]) for b in range(dec.nblocks)))
+        out["fit_axis0"] = 2.0 * (p + 1) * q
+        if D == 3:
+            t2 = float(sum(n[b, 0] * n[b, 1] * m[b, 2] for b in range(dec.nblocks)))
+            out["fit_axis1"] = 2.0 * (p + 1) * t1
+            out["fit_last"] = 2.0 * (p + 1) * t2 + 4.0 * (2 * p + 1) * ab["p_held"]
+            out["fit_backsub0"] = 4.0 * (2 * p + 1) * ab["p_held"]
+        else:
+            out["fit_last"] = 2.0 * (p + 1) * t1 + 8.0 * (2 * p + 1) * ab["p_held"]
+    else:
+        out["fit_last"] = 2.0 * (p + 1) * q + 4.0 * (2 * p + 1) * ab["p_held"]
+    return out
+
+
+def fp64_peak():
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_fp64_peak.json")) as f:
+            return float(json.load(f)["fp64_tflops"]) * 1e12, "measured (profiles/r02_fp64_peak.json)"
+    except Exception:
+        return 37.0e12, "fallback (B200 FP64 spec)"
+
+
 def run_reference(args, cfg, rank):
     from oracle import ref
     if rank != 0:
@@ -496,8 +534,11 @@ def main():
     # ---------------- roofline of the dominant kernel (live CUDA events)
     ab = W.algorithmic_bytes(cfg, dec, epochs_exchanged, store_error=True)
     kb = kernel_bytes(cfg, dec, ab)
+    kf = kernel_flops(cfg, dec, ab, epochs_exchanged)
+    f64, f64_src = fp64_peak()
     if world > 1:  # per-rank share of the global problem (equal block slabs)
         kb = {k: v / world for k, v in kb.items()}
+        kf = {k: v / world for k, v in kf.items()}
         ab = dict(ab, bytes=ab["bytes"] / world)
     per = {}
     for name, t in ktimes:
@@ -514,10 +555,20 @@ def main():
             "algorithmic_bytes_per_launch": kb[dom], "avg_launch_ms": avg_ms,
             "step_share": shares[dom] / tot,
             "step_algorithmic_bytes": ab["bytes"],
-            "step_frac": ab["bytes"] / (ms * 1e-3) / 1e9 / peak}
-    kern = {k: {"ms_per_step": shares[k] / args.steps, "launches_per_step": len(per[k]) / args.steps,
-                **({"GBps": kb[k] * len(per[k]) / (shares[k] * 1e-3) / 1e9} if k in kb else {})}
-            for k in shares}
+            "step_frac": ab["bytes"] / (ms * 1e-3) / 1e9 / peak,
+            "fp64_peak_tflops": f64 / 1e12, "fp64_peak_source": f64_src}
+
+    def kentry(k):
+        t = shares[k] * 1e-3 / args.steps  # seconds per step
+        e = {"ms_per_step": shares[k] / args.steps, "launches_per_step": len(per[k]) / args.steps}
+        if k in kb and t > 0:  # HBM side: algorithmic bytes per step / time
+            e["GBps"] = kb[k] * len(per[k]) / args.steps / t / 1e9
+            e["hbm_frac"] = e["GBps"] / peak
+        if k in kf and t > 0:  # FP64 side: algorithmic flops per step / time
+            e["fp64_frac"] = kf[k] * len(per[k]) / args.steps / t / f64
+        e["bound"] = "hbm" if k in kb else "latency"
+        return e
+    kern = {k: kentry(k) for k in shares}
 
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -732,7 +732,8 @@ struct mfadd_solver {
   bool tma_decode = false;
   mfb::TmaGeom dgeo{1, 1, 16, 4, 0};
   int dnt1 = 1, dnt2 = 1, dnrange = 1, dH = 1;
-  bool dwin = false;  // D = 3: window-only decode kernel form
+  bool dwin = false;  // D = 3: staged-window decode kernel form
+  int dna_cap = 0;    // its staged planes per row range
 
   DBuf<int2> hr;
   DBuf<int> slist, clist, own_coord, pair_slot, unit_g0;
@@ -1632,6 +1633,30 @@ std::unique_ptr<mfadd_solver> create_solver(mfadd_context* ctx, const mfadd_deco
           mrw = std::max(mrw, g0(jl) - g0(jf) + p + 1);
         }
         s->dwin = mrw <= s->dgeo.lt_cap && mrw <= s->dgeo.B2;
+        if (s->dwin) {  // staged windows: row ranges short enough that their planes fit the budget
+          s->dgeo.lt_cap = mrw;
+          const std::vector<double>& kn0 = d.knots[0];
+          auto g00 = [&](std::int64_t j) {
+            return host_find_span(kn0, p, static_cast<double>(j) / static_cast<double>(d.grid[0] - 1)) - p;
+          };
+          const std::int64_t ybeg = s->srange.in_lo, yend = s->srange.in_hi;
+          auto na_for = [&](int H) {
+            int na = 1;
+            for (std::int64_t y0 = ybeg; y0 < yend; y0 += H) {
+              const std::int64_t y1 = std::min<std::int64_t>(yend, y0 + H);
+              const int hi = static_cast<int>(std::min<std::int64_t>(g00(y1 - 1) + p, d.n_ctrl[0] - 1));
+              na = std::max(na, hi - g00(y0) + 1);
+            }
+            return na;
+          };
+          const std::size_t budget = static_cast<std::size_t>(env_int("MFADD_DEC_STAGE_KB", 24)) * 1024;
+          int H = s->dH;
+          while (H > 8 && static_cast<std::size_t>(na_for(H)) * mrw * 8 > budget) H -= 8;
+          s->dH = H;
+          s->dnrange = static_cast<int>((M0 + H - 1) / H);
+          s->dna_cap = na_for(H);
+          npart = std::max(npart, static_cast<std::size_t>(s->dnt1) * s->dnt2 * s->dnrange);
+        }
       }
     }
     s->partial.alloc(npart * 2);
@@ -1863,6 +1888,7 @@ int enqueue_decode(mfadd_solver* s, const double* dfield) {
     ds.ticket = s->ticket.p;
     ds.red2 = s->red2.p;
     ds.win = s->dwin ? 1 : 0;
+    ds.na_cap = s->dna_cap;
     const CUtensorMap map = make_tmap(dfield, d.rank, dims, box);
     launches += mfb::launch_decode_tma(wl.p, ds, map, s->dgeo, st);
     nparts = 0;  // reduced by the decode's last CTA

@@ -322,7 +322,8 @@ struct DecodeSweepArgs {
   double* partial;  // per CTA {l2sq, linf}
   unsigned* ticket; // CTA completion counter (zero between launches)
   double* red2;     // {sum l2sq, max linf}, written by the last CTA
-  int win;          // D = 3: every CTA's axis-2 window fits (host-checked): the window-only kernel form
+  int win;          // D = 3: every CTA's axis-2 window fits (host-checked): the staged-window kernel form
+  int na_cap;       // D = 3 win: staged control planes per row range (host-sized exactly)
 };
 int launch_decode_tma(int degree, const DecodeSweepArgs& a, const CUtensorMap& map, const TmaGeom& g,
                       cudaStream_t s);

@@ -1496,31 +1496,50 @@ __global__ void __launch_bounds__(256, MB) k_decode_tma(const DecodeSweepArgs a,
       for (int k1 = 0; k1 <= P; ++k1) lv[k1] = __ldg(L0 + static_cast<std::int64_t>(g1 + k1) * a.N2);
     }
   };
-  if (WIN) {  // the initial window planes through the shared window as well
+  // WIN: the CTA's axis-1-contracted window of every control plane its row
+  // range touches, U[a - a_lo][t], staged once up front (independent loads,
+  // no per-advance loads or barriers in the sweep)
+  const int a_lo = WIN ? __ldg(a.g0_0 + y0) : 0;
+  const int y1c = y1 > y0 ? y1 - 1 : y0;
+  const int a_hi = WIN ? min(__ldg(a.g0_0 + y1c) + P, a.N0 - 1) : 0;
+  const int na = a_hi - a_lo + 1;
+  const int wo = g2 > g2base ? g2 - g2base : 0;  // (inactive threads: clamped, unused)
+  bool wfits = true;
+  if (WIN) {
+    const bool fits = rw <= geo.lt_cap && na <= a.na_cap;  // host-sized exactly
+    wfits = fits;
+    if (fits && rw > 0) {
+      const int tr = nthr / rw > 0 ? nthr / rw : 1;
+      const int t = tid % rw, r0 = tid / rw;
+      if (r0 < tr) {
+        const double* Lc = a.lattice + g2base + t;
+#pragma unroll 4
+        for (int ai = r0; ai < na; ai += tr) {
+          const double* L0 = Lc + static_cast<std::int64_t>(a_lo + ai) * N12;
+          double r = 0.0;
+#pragma unroll
+          for (int k1 = 0; k1 <= P; ++k1) r = fma(w1[k1], __ldg(L0 + static_cast<std::int64_t>(g1 + k1) * a.N2), r);
+          sR[ai * geo.lt_cap + t] = r;
+        }
+      }
+    }
+    __syncthreads();
 #pragma unroll
     for (int k = 0; k <= P; ++k) {
-      fetch_window(abase + k);
-      double* R = sR + rbuf * geo.lt_cap;
-      if (tid < rw) {
-        double r = 0.0;
-#pragma unroll
-        for (int k1 = 0; k1 <= P; ++k1) r = fma(w1[k1], lv[k1], r);
-        R[tid] = r;
-      }
-      __syncthreads();
-      const double* Rg = R + (g2 > g2base ? g2 - g2base : 0);
+      const double* Rg = sR + min(abase + k - a_lo, na - 1) * geo.lt_cap + wo;
       double sres = 0.0;
 #pragma unroll
       for (int k2 = 0; k2 <= P; ++k2) sres = fma(w2[k2], Rg[k2], sres);
-      Tw[k] = active ? sres : 0.0;
-      rbuf ^= 1;
+      Tw[k] = (active && fits) ? sres : 0.0;
     }
   }
-  if (win)
-    fetch_window(abase + P + 1);
-  else if (active)
-    fetch_plane(abase + P + 1);
-  double l2 = 0.0;
+  if (!WIN) {
+    if (win)
+      fetch_window(abase + P + 1);
+    else if (active)
+      fetch_plane(abase + P + 1);
+  }
+  double l2 = wfits ? 0.0 : __longlong_as_double(0x7ff8000000000000LL);  // NaN: never a silent wrong answer
   unsigned long long li = 0ull;  // L-inf as the bit pattern of |e| (ordered like the value)
   // error of the current row (ERR: the error field is stored); inactive
   // threads point at their clamped column and never store
@@ -1579,7 +1598,14 @@ __global__ void __launch_bounds__(256, MB) k_decode_tma(const DecodeSweepArgs a,
         advance();
       }
       if (gnext == 0x7fffffff) break;
-      if (win) {  // plane abase + P + 1 replaces plane abase, through the shared window
+      if (WIN) {  // plane abase + P + 1 replaces plane abase, from the staged windows
+        const double* Rg = sR + min(abase + P + 1 - a_lo, na - 1) * geo.lt_cap + wo;
+        double sres = 0.0;
+#pragma unroll
+        for (int k2 = 0; k2 <= P; ++k2) sres = fma(w2[k2], Rg[k2], sres);
+        Tw[u] = active ? sres : 0.0;
+        ++abase;
+      } else if (win) {  // plane abase + P + 1 replaces plane abase, through the shared window
         double* R = sR + rbuf * geo.lt_cap;
         if (tid < rw) {
           double r = 0.0;
@@ -1702,7 +1728,8 @@ struct DecodeSweepLaunch {
   template <int D, int S>
   static void go(const DecodeSweepArgs& a, const CUtensorMap& map, const TmaGeom& g, cudaStream_t s) {
     const StageLayout SL = stage_layout(kFitR, g.B1 * g.B2, P);
-    const size_t smem = static_cast<size_t>(S) * SL.stage_bytes + S * 8 + 2 * static_cast<size_t>(g.lt_cap) * 8;
+    const size_t smem = static_cast<size_t>(S) * SL.stage_bytes + S * 8 +
+                        (D == 3 && a.win ? static_cast<size_t>(a.na_cap) : 2) * static_cast<size_t>(g.lt_cap) * 8;
     dim3 grid(a.ntile1 * a.ntile2, a.nrange);
     static const int mb = std::getenv("MFADD_DEC_MINB") ? std::atoi(std::getenv("MFADD_DEC_MINB")) : 1;
     if (mb >= 4) {
