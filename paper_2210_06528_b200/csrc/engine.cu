@@ -760,7 +760,7 @@ struct mfadd_solver {
   // every epoch's residuals after the loop
   bool res_snap = false;
   DBuf<double> snap, res_part2;
-  int res_W = 0, res_ntc = 0, res_nrr = 1, res_threads = 0, res_ltcap = 0, res_nacap = 0, res_eg = 1, res_dense = 0;
+  int res_W = 0, res_ntc = 0, res_nrr = 1, res_threads = 0, res_ltcap = 0, res_nacap = 0, res_eg = 1, res_ng = 1;
   std::vector<double> h_block_errs;
   // shard: rank of nranks owns blocks [srange.blo, srange.bhi)
   int rank = 0, nranks = 1;
@@ -1014,7 +1014,7 @@ int launch_residuals_all(mfadd_solver* s, const double* dfield, cudaStream_t cs)
   a.lt_cap = s->res_ltcap;
   a.na_cap = s->res_nacap;
   a.eg = s->res_eg;
-  a.dense_a = s->res_dense;
+  a.ng = s->res_ng;
   a.partial = s->res_part2.p;
   a.errs = s->block_errs.p;
   a.nglobal = d.nblocks;
@@ -1334,20 +1334,7 @@ void plan_residual_tma(mfadd_solver* s) {
     if (ok) break;
   }
   if (!ok) return;  // the per-epoch kernels stay
-  // dense chunk sweep: the most plane advances within one 8-row chunk
-  {
-    int adv = 0;
-    std::vector<char> seen0(wl.probs.size(), 0);
-    for (const auto& b : wl.blocks) {
-      const int pid = b.ax[0];
-      if (seen0[static_cast<std::size_t>(pid)]) continue;
-      seen0[static_cast<std::size_t>(pid)] = 1;
-      const AxisProb& pr = wl.probs[static_cast<std::size_t>(pid)];
-      for (int y = 0; y < pr.m; y += 8) adv = std::max(adv, g0_of(pr, std::min(pr.m - 1, y + 7)) - g0_of(pr, y));
-    }
-    // (the dense sweep is built only with -DMFB_RES_DENSE: measured slower)
-    s->res_dense = (s->res_eg == 4 && p <= 6 && adv <= 3 && std::getenv("MFADD_RES_DENSE")) ? std::max(1, adv) : 0;
-  }
+  s->res_ng = (s->res_eg == 4 && s->res_threads * 2 <= 512) ? env_int("MFADD_RES_NG", 2) : 1;
   s->res_snap = true;
   s->snap.alloc(static_cast<std::size_t>(s->cfg.max_outer_iterations + 1) * static_cast<std::size_t>(wl.total_p));
   s->res_part2.alloc(static_cast<std::size_t>(s->cfg.max_outer_iterations + 1) * wl.blocks.size() *

@@ -55,19 +55,16 @@ __host__ __device__ inline ResStage res_stage(int nbox, int P) {
 
 __host__ __device__ inline size_t res_tma_smem(int P, int W, int EG, int na_cap, int lt_cap, int S) {
   return static_cast<size_t>(S) * res_stage(W, P).stage_bytes + S * 8 + 8 +
-         static_cast<size_t>(EG) * na_cap * lt_cap * 8 + 2 * kResR * (P + 4) * 8;  // (+ the dense sweep's rows)
+         static_cast<size_t>(EG) * na_cap * lt_cap * 8;
 }
 
-// A > 0: the dense chunk sweep.  A window of NW = P+1+A planes per epoch
-// covers every row of an 8-row chunk (the host checks that no chunk's rows
-// span more than A plane advances); each chunk's basis rows are expanded to
-// NW columns (zeros outside the row's P+1) in shared memory, so the 8 rows
-// are decoded fully unrolled with static register indices and no per-row
-// control flow.  A = 0: the per-row sweep with a P+1 plane window.
-template <int P, int D, int EG, int S, int A>
-__global__ void __launch_bounds__(256) k_residual_tma(const ResTmaArgs a, const __grid_constant__ CUtensorMap map) {
+// NG epoch groups: the CTA runs NG threads per point, each decoding EG / NG
+// of the pass's epochs from the same staged rows (Q is still read once per
+// pass; twice the warps per SM at half the registers per thread).
+template <int P, int D, int EG, int S, int NG>
+__global__ void __maxnreg__(NG == 2 ? 84 : 128) k_residual_tma(const ResTmaArgs a, const __grid_constant__ CUtensorMap map) {
   extern __shared__ __align__(1024) unsigned char sm_raw[];
-  __shared__ double s_red[2 * EG][8];
+  __shared__ double s_red[2 * EG][16];
   const int b = blockIdx.y;
   const BlockDev blk = a.blocks[b];
   const AxisProb p0 = a.probs[blk.ax[0]], p1 = a.probs[blk.ax[1]];
@@ -75,6 +72,9 @@ __global__ void __launch_bounds__(256) k_residual_tma(const ResTmaArgs a, const 
   const int m0 = p0.m, n0 = p0.n, m1 = p1.m, n1 = p1.n;
   const int m2 = D == 3 ? p2.m : 1, n2 = D == 3 ? p2.n : 1;
   const int W = a.W, tid = threadIdx.x, nthr = blockDim.x;
+  constexpr int EGT = EG / NG;                   // epochs per thread
+  const int Wt = nthr / NG;                      // threads per epoch group
+  const int grp = tid / Wt, ct = tid - grp * Wt;  // epoch group, column thread
   const int ne = a.st ? a.st->iter + 1 : 1;  // epochs recorded (0 .. iter)
   // ---- this thread's point and the CTA's box origin
   const int tcol = blockIdx.x % a.ntc, rr = blockIdx.x / a.ntc;  // column tile, row range
@@ -84,17 +84,17 @@ __global__ void __launch_bounds__(256) k_residual_tma(const ResTmaArgs a, const 
     const int cols = W - 2;
     const int first = static_cast<int>(p1.in_lo) + tcol * cols;
     c_inner = first & ~1;  // 16-B aligned box start; the column map is shifted by its parity
-    j1 = tcol * cols + tid - (first - c_inner);
+    j1 = tcol * cols + ct - (first - c_inner);
     live = tcol * cols < m1;
-    act = live && tid < W && j1 >= tcol * cols && j1 < tcol * cols + cols && j1 < m1;
+    act = live && ct < W && j1 >= tcol * cols && j1 < tcol * cols + cols && j1 < m1;
   } else {
     j1 = tcol;
     live = j1 < m1;
     const int in2 = static_cast<int>(p2.in_lo);
     c_inner = in2 & ~1;
     c_mid = static_cast<int>(p1.in_lo) + (live ? j1 : 0);
-    j2 = tid - (in2 - c_inner);
-    act = live && tid < W && j2 >= 0 && j2 < m2;
+    j2 = ct - (in2 - c_inner);
+    act = live && ct < W && j2 >= 0 && j2 < m2;
   }
   // row range of this CTA (chunk-aligned)
   const int nch_all = (m0 + kResR - 1) / kResR;
@@ -185,10 +185,10 @@ __global__ void __launch_bounds__(256) k_residual_tma(const ResTmaArgs a, const 
   int g = 0;  // global chunk cursor
   for (int pass = 0; pass < npass; ++pass) {
     const int e0 = pass * EG;
-    double l2[EG];
-    unsigned long long li[EG];  // max |e| as bit patterns (ordered like the values)
+    double l2[EGT];
+    unsigned long long li[EGT];  // max |e| as bit patterns (ordered like the values)
 #pragma unroll
-    for (int q = 0; q < EG; ++q) {
+    for (int q = 0; q < EGT; ++q) {
       l2[q] = 0.0;
       li[q] = 0ull;
     }
@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(256) k_residual_tma(const ResTmaArgs a, const 
       const bool fits = rw <= a.lt_cap && na <= a.na_cap;  // (the host sizes the caps exactly)
       if (!fits)
 #pragma unroll
-        for (int q = 0; q < EG; ++q) l2[q] = __longlong_as_double(0x7ff8000000000000LL);  // NaN: never silent
+        for (int q = 0; q < EGT; ++q) l2[q] = __longlong_as_double(0x7ff8000000000000LL);  // NaN: never silent
       if (fits) {
         // thread -> (window column t, plane phase r0): one division per thread
         const int tr = nthr / rw > 0 ? nthr / rw : 1;
@@ -240,92 +240,18 @@ __global__ void __launch_bounds__(256) k_residual_tma(const ResTmaArgs a, const 
       }
       __syncthreads();
       // trailing contraction of plane ai for every epoch -> Tw slot
-      double Tw[EG][P + 1];
+      double Tw[EGT][P + 1];
       const double* wk = D == 2 ? w1 : w2;
       auto reduce_into = [&](int slot, int ai) {
-        const double* Ub = sR + (clampi(ai, n0) - a_lo) * a.lt_cap + wo;
+        const double* Ub = sR + (static_cast<std::int64_t>(grp) * EGT * a.na_cap + clampi(ai, n0) - a_lo) * a.lt_cap + wo;
 #pragma unroll
-        for (int q = 0; q < EG; ++q) {
+        for (int q = 0; q < EGT; ++q) {
           double sacc = 0.0;
 #pragma unroll
           for (int k = 0; k <= P; ++k) sacc = fma(wk[k], Ub[q * a.na_cap * a.lt_cap + k], sacc);
           Tw[q][slot] = sacc;
         }
       };
-      if constexpr (A > 0) {
-        constexpr int NW = P + 1 + A;
-        double Tn[EG][NW];
-        auto plane_into = [&](int slot, int ai) {
-          // planes past the range's last one only meet zero coefficients;
-          // clamp them onto staged (finite) data
-          const int ac = min(clampi(ai, n0), a_hi);
-          const double* Ub = sR + (ac - a_lo) * a.lt_cap + wo;
-#pragma unroll
-          for (int q = 0; q < EG; ++q) {
-            double sacc = 0.0;
-#pragma unroll
-            for (int k = 0; k <= P; ++k) sacc = fma(wk[k], Ub[q * a.na_cap * a.lt_cap + k], sacc);
-            Tn[q][slot] = sacc;
-          }
-        };
-        int abase = __ldg(g0g + ybeg);
-#pragma unroll
-        for (int k = 0; k < NW; ++k) plane_into(k, abase + k);
-        double* sVp = reinterpret_cast<double*>(sm_raw + S * SL.stage_bytes + S * 8 + 8) +
-                      static_cast<std::int64_t>(EG) * a.na_cap * a.lt_cap;  // [2][kResR][NW]
-        const int col = tid < W ? tid : 0;
-        for (int c = 0; c < nchunks; ++c, ++g) {
-          const int st = g % S;
-          const unsigned char* base = sm_raw + st * SL.stage_bytes;
-          const double* sq = reinterpret_cast<const double*>(base) + col;
-          const double* sv = reinterpret_cast<const double*>(base + SL.v_off);
-          const int* sg = reinterpret_cast<const int*>(base + SL.g_off);
-          const int yc = (ch0 + c) * kResR;
-          const int jn = (m0 - yc) < kResR ? (m0 - yc) : kResR;
-          mbar_wait(&bars[st], (g / S) & 1);
-          // slide the window to the chunk's first row (CTA-uniform)
-          const int gf = sg[0];
-          while (abase < gf) {
-#pragma unroll
-            for (int q = 0; q < EG; ++q)
-#pragma unroll
-              for (int k = 0; k + 1 < NW; ++k) Tn[q][k] = Tn[q][k + 1];
-            plane_into(NW - 1, abase + NW);
-            ++abase;
-          }
-          // the chunk's basis rows expanded to the window's NW columns
-          double* Vb = sVp + (c & 1) * kResR * NW;
-          for (int i = tid; i < kResR * NW; i += nthr) {
-            const int j = i / NW, sidx = i - j * NW;
-            const int k = j < jn ? sidx - (sg[j] - abase) : -1;
-            Vb[i] = (k >= 0 && k <= P) ? sv[j * (P + 1) + k] : 0.0;
-          }
-          __syncthreads();  // Vb visible; every thread is done with the previous chunk's stage
-          if (tid == 0 && g >= 1 && g - 1 + S < gtotal) {
-            fence_proxy_async();
-            issue(g - 1 + S);
-          }
-#pragma unroll
-          for (int j = 0; j < kResR; ++j) {
-            if (j < jn) {  // CTA-uniform
-              const double qv = sq[j * W];
-              double v[NW];
-#pragma unroll
-              for (int k = 0; k < NW; ++k) v[k] = Vb[j * NW + k];
-#pragma unroll
-              for (int q = 0; q < EG; ++q) {
-                double e = qv;
-#pragma unroll
-                for (int k = 0; k < NW; ++k) e = fma(-v[k], Tn[q][k], e);
-                l2[q] = fma(e, e, l2[q]);
-                const unsigned long long eb =
-                    static_cast<unsigned long long>(__double_as_longlong(e)) & 0x7fffffffffffffffull;
-                li[q] = li[q] > eb ? li[q] : eb;
-              }
-            }
-          }
-        }
-      } else {
       int abase = __ldg(g0g + ybeg);
 #pragma unroll
       for (int k = 0; k <= P; ++k) reduce_into(k, abase + k);
@@ -337,7 +263,7 @@ __global__ void __launch_bounds__(256) k_residual_tma(const ResTmaArgs a, const 
       auto open_chunk = [&]() {
         const int st = g % S;
         const unsigned char* base = sm_raw + st * SL.stage_bytes;
-        sq = reinterpret_cast<const double*>(base) + (tid < W ? tid : 0);
+        sq = reinterpret_cast<const double*>(base) + (ct < W ? ct : 0);
         sv = reinterpret_cast<const double*>(base + SL.v_off);
         sg = reinterpret_cast<const int*>(base + SL.g_off);
         const int yc = (ch0 + c) * kResR;
@@ -383,7 +309,7 @@ __global__ void __launch_bounds__(256) k_residual_tma(const ResTmaArgs a, const 
               }
               const double q0 = sq[jl * W], q1 = sq[(jl + 1) * W];
 #pragma unroll
-              for (int q = 0; q < EG; ++q) {
+              for (int q = 0; q < EGT; ++q) {
                 double e = q0, f = q1;
 #pragma unroll
                 for (int k = 0; k <= P; ++k) {
@@ -404,7 +330,7 @@ __global__ void __launch_bounds__(256) k_residual_tma(const ResTmaArgs a, const 
               for (int k = 0; k <= P; ++k) v[k] = vr[k];
               const double qv = sq[jl * W];
 #pragma unroll
-              for (int q = 0; q < EG; ++q) {
+              for (int q = 0; q < EGT; ++q) {
                 double e = qv;
 #pragma unroll
                 for (int k = 0; k <= P; ++k) e = fma(-v[k], Tw[q][(u + k) % (P + 1)], e);
@@ -421,11 +347,10 @@ __global__ void __launch_bounds__(256) k_residual_tma(const ResTmaArgs a, const 
         }
       }
     }
-      }
-    // ---- CTA partials of this pass's epochs
-    double lif[EG];
+    // ---- CTA partials of this pass's epochs (group grp holds epochs grp*EGT ..)
+    double lif[EGT];
 #pragma unroll
-    for (int q = 0; q < EG; ++q) {
+    for (int q = 0; q < EGT; ++q) {
       if (!act) {
         l2[q] = 0.0;
         li[q] = 0ull;
@@ -437,17 +362,17 @@ __global__ void __launch_bounds__(256) k_residual_tma(const ResTmaArgs a, const 
         lif[q] = fmax(lif[q], __shfl_xor_sync(kFullMask, lif[q], o));
       }
     }
-    const int wid = tid >> 5;
+    const int wg = ct >> 5;  // warp within the group
     if ((tid & 31) == 0)
 #pragma unroll
-      for (int q = 0; q < EG; ++q) {
-        s_red[2 * q][wid] = l2[q];
-        s_red[2 * q + 1][wid] = lif[q];
+      for (int q = 0; q < EGT; ++q) {
+        s_red[2 * (grp * EGT + q)][wg] = l2[q];
+        s_red[2 * (grp * EGT + q) + 1][wg] = lif[q];
       }
     __syncthreads();
     if (tid < EG && e0 + tid < ne) {
       double sl = 0.0, sm = 0.0;
-      for (int w = 0; w < (nthr + 31) / 32; ++w) {
+      for (int w = 0; w < (Wt + 31) / 32; ++w) {
         sl += s_red[2 * tid][w];
         sm = fmax(sm, s_red[2 * tid + 1][w]);
       }
@@ -481,36 +406,30 @@ __global__ void k_res_reduce(const ResTmaArgs a, int nblocks, int ctas) {
 
 template <int P>
 struct ResTmaLaunch {
-  template <int D, int EG, int A>
+  template <int D, int EG, int NG>
   static void go(const ResTmaArgs& a, const CUtensorMap& map, int threads, cudaStream_t s) {
     constexpr int S = kResS;
     const size_t smem = res_tma_smem(P, a.W, EG, a.na_cap, a.lt_cap, S);
-    cudaFuncSetAttribute(k_residual_tma<P, D, EG, S, A>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_residual_tma<P, D, EG, S, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
     dim3 grid(a.ntc * a.nrr, a.nblocks);
-    k_residual_tma<P, D, EG, S, A><<<grid, threads, smem, s>>>(a, map);
+    k_residual_tma<P, D, EG, S, NG><<<grid, threads * NG, smem, s>>>(a, map);
     k_res_reduce<<<(a.nblocks + 127) / 128, 128, 0, s>>>(a, a.nblocks, a.ntc * a.nrr);
-  }
-  template <int D>
-  static void dense(const ResTmaArgs& a, const CUtensorMap& map, int threads, cudaStream_t s) {
-#ifdef MFB_RES_DENSE  // measured slower than the per-row sweep on C3/C4/C5: not built by default
-    if constexpr (P <= 6) {
-      switch (a.dense_a) {
-        case 1: go<D, 4, 1>(a, map, threads, s); return;
-        case 2: go<D, 4, 2>(a, map, threads, s); return;
-        case 3: go<D, 4, 3>(a, map, threads, s); return;
-        default: break;
-      }
-    }
-#endif
-    go<D, 4, 0>(a, map, threads, s);
   }
   static int run(const ResTmaArgs& a, const CUtensorMap& map, int threads, cudaStream_t s) {
     const int eg = a.eg;
-    if (a.D == 2)
-      eg >= 4 ? dense<2>(a, map, threads, s) : (eg >= 2 ? go<2, 2, 0>(a, map, threads, s) : go<2, 1, 0>(a, map, threads, s));
-    else
-      eg >= 4 ? dense<3>(a, map, threads, s) : (eg >= 2 ? go<3, 2, 0>(a, map, threads, s) : go<3, 1, 0>(a, map, threads, s));
+    const bool two = a.ng == 2 && threads * 2 <= 512;
+    if (a.D == 2) {
+      if (eg >= 4)
+        two ? go<2, 4, 2>(a, map, threads, s) : go<2, 4, 1>(a, map, threads, s);
+      else
+        eg >= 2 ? go<2, 2, 1>(a, map, threads, s) : go<2, 1, 1>(a, map, threads, s);
+    } else {
+      if (eg >= 4)
+        two ? go<3, 4, 2>(a, map, threads, s) : go<3, 4, 1>(a, map, threads, s);
+      else
+        eg >= 2 ? go<3, 2, 1>(a, map, threads, s) : go<3, 1, 1>(a, map, threads, s);
+    }
     return 2;
   }
 };
