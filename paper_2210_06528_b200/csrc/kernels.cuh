@@ -229,7 +229,7 @@ struct ResTmaArgs {
   int lt_cap;                        // window columns per staged plane (>= the widest CTA window)
   int na_cap;                        // staged planes per epoch (>= the most planes a row range touches)
   int eg;                            // epochs per pass (1, 2 or 4; the staged windows scale with it)
-  int dense_a;                       // 1..3: dense chunk sweep (EG = 4, P <= 6; max plane advances within a chunk), 0: per row
+  int ng;                            // threads per point (2: each decodes half of the pass's epochs)
   double* partial;                   // [epoch][block][ntc * nrr] x {sum e^2, max |e|}
   double* errs;                      // [(max_iter + 1)][nglobal] x {l2, linf}
   int nglobal, boff;
