@@ -1334,7 +1334,7 @@ void plan_residual_tma(mfadd_solver* s) {
     if (ok) break;
   }
   if (!ok) return;  // the per-epoch kernels stay
-  s->res_ng = (s->res_eg == 4 && s->res_threads * 2 <= 512) ? env_int("MFADD_RES_NG", 2) : 1;
+  s->res_ng = (s->res_eg == 4 && s->res_threads * 2 <= 512) ? env_int("MFADD_RES_NG", 1) : 1;
   s->res_snap = true;
   s->snap.alloc(static_cast<std::size_t>(s->cfg.max_outer_iterations + 1) * static_cast<std::size_t>(wl.total_p));
   s->res_part2.alloc(static_cast<std::size_t>(s->cfg.max_outer_iterations + 1) * wl.blocks.size() *
