@@ -231,10 +231,14 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
     mbar_wait(&bars[st], (c / S) & 1);
     gnext = sg[0];
   };
+  // the staged-row stride in a register (the compiler otherwise re-derives
+  // it from the kernel parameters on every row)
+  int nbox_r = nbox;
+  asm volatile("" : "+r"(nbox_r));
   auto advance = [&]() {
     if (++jl < jn) {
       gnext = sg[jl];
-      sq += nbox;  // this thread's column in the next staged row
+      sq += nbox_r;  // this thread's column in the next staged row
       return;
     }
     __syncthreads();  // every column is done with chunk c: refill its stage
@@ -252,6 +256,19 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
 #pragma unroll
     for (int u = 0; u <= P; ++u) {
       while (gnext == cbase) {  // CTA-uniform
+        if (NC == 1 && jl + 1 < jn && sg[jl + 1] == cbase) {  // two rows of the same column run (CTA-uniform)
+          const double q0 = sq[0], q1 = sq[nbox_r];
+          const double* vr = sv + jl * (P + 1);
+#pragma unroll
+          for (int k = 0; k <= P; ++k) {
+            const double v0 = vr[k], v1 = vr[P + 1 + k];
+            acc[0][(u + k) % (P + 1)] = fma(v1, q1, fma(v0, q0, acc[0][(u + k) % (P + 1)]));
+          }
+          ++jl;
+          sq += nbox_r;
+          advance();
+          continue;
+        }
         double q[NC];
         if (NC == 2) {
           const double2 q2 = *reinterpret_cast<const double2*>(sq);
