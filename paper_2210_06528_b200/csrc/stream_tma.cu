@@ -1103,13 +1103,18 @@ __device__ __forceinline__ void rl_load_step(const double* row, double (&cf)[RL<
   }
 }
 
-// cf holds step t0's table row on entry and step t0 + U's on exit: each
-// step's coefficients are loaded one step ahead, off the dependent chain.
+// cf holds the table rows of steps t0 .. t0+PF-1 on entry and of steps
+// t0+U .. t0+U+PF-1 on exit: each step's coefficients are loaded PF steps
+// ahead (MFB_RL_PF), off the dependent chain and past the shared-memory
+// latency with one warp per scheduler.
+#ifndef MFB_RL_PF
+#define MFB_RL_PF 1
+#endif
 template <int P, bool TAIL, bool FINAL>
 __device__ __forceinline__ void rl_batch(double* __restrict__ x0, const int ds, const int n, const int t0,
                                          const double* __restrict__ tab, double (&acc)[P], double (&zin)[RL<P>::U],
-                                         double (&cf)[RL<P>::W], RLFinal& fin) {
-  constexpr int U = RL<P>::U, W = RL<P>::W;
+                                         double (&cf)[MFB_RL_PF][RL<P>::W], RLFinal& fin) {
+  constexpr int U = RL<P>::U, W = RL<P>::W, PF = MFB_RL_PF;
   double znx[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
@@ -1120,11 +1125,11 @@ __device__ __forceinline__ void rl_batch(double* __restrict__ x0, const int ds, 
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     double cfn[W];
-    rl_load_step<P>(tb + (u + 1) * W, cfn);  // the next step's row (tables are padded past the line)
+    rl_load_step<P>(tb + (u + PF) * W, cfn);  // the row PF steps ahead (tables are padded past the line)
     const double y = acc[u % P];
 #pragma unroll
-    for (int k = 1; k < P; ++k) acc[(u + k) % P] = fma(-cf[k - 1], y, acc[(u + k) % P]);
-    acc[u % P] = fma(-cf[P - 1], y, zin[u] * cf[P]);
+    for (int k = 1; k < P; ++k) acc[(u + k) % P] = fma(-cf[0][k - 1], y, acc[(u + k) % P]);
+    acc[u % P] = fma(-cf[0][P - 1], y, zin[u] * cf[0][P]);
     const int t = t0 + u;
     if (!TAIL || t < n) {
       x0[t * ds] = y;
@@ -1137,7 +1142,11 @@ __device__ __forceinline__ void rl_batch(double* __restrict__ x0, const int ds, 
       }
     }
 #pragma unroll
-    for (int k = 0; k < W; ++k) cf[k] = cfn[k];
+    for (int q = 0; q + 1 < PF; ++q)
+#pragma unroll
+      for (int k = 0; k < W; ++k) cf[q][k] = cf[q + 1][k];
+#pragma unroll
+    for (int k = 0; k < W; ++k) cf[PF - 1][k] = cfn[k];
   }
 #pragma unroll
   for (int u = 0; u < U; ++u) zin[u] = znx[u];
@@ -1146,14 +1155,15 @@ __device__ __forceinline__ void rl_batch(double* __restrict__ x0, const int ds, 
 template <int P, bool FINAL>
 __device__ __forceinline__ void rl_pass(double* __restrict__ x0, const int ds, const int n,
                                         const double* __restrict__ tab, RLFinal& fin) {
-  constexpr int U = RL<P>::U, W = RL<P>::W;
+  constexpr int U = RL<P>::U, W = RL<P>::W, PF = MFB_RL_PF;
   double acc[P], zin[U];
 #pragma unroll
   for (int k = 0; k < P; ++k) acc[k] = (k < n ? x0[k * ds] : 0.0) * tab[(k - P) * W + P];
 #pragma unroll
   for (int u = 0; u < U; ++u) zin[u] = P + u < n ? x0[(P + u) * ds] : 0.0;
-  double cf[W];
-  rl_load_step<P>(tab, cf);
+  double cf[PF][W];
+#pragma unroll
+  for (int q = 0; q < PF; ++q) rl_load_step<P>(tab + q * W, cf[q]);
   int t0 = 0;
   for (; t0 + 2 * U + P <= n; t0 += U) rl_batch<P, false, FINAL>(x0, ds, n, t0, tab, acc, zin, cf, fin);
   for (; t0 < n; t0 += U) rl_batch<P, true, FINAL>(x0, ds, n, t0, tab, acc, zin, cf, fin);
