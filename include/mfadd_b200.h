@@ -156,11 +156,17 @@ int mfadd_solver_set_profiling(mfadd_solver* s, int on);
 int mfadd_solver_kernel_times(const mfadd_solver* s, char* names, int name_len, double* ms, int cap);
 
 /* ------------------------------------------------------------- multi-GPU
- * The path shards by blocks: rank r of n owns the block rows
- * [r*B0/n, (r+1)*B0/n) along axis 0.  Each epoch exchanges the copies of the
- * controls shared across ranks (ncclSend/ncclRecv with the adjacent ranks, the
- * runtime.cpp:123-158 exchange) and max-reduces dp; the lattice rows are
- * all-gathered and every rank decodes its own input rows.  Results equal the
+ * The path shards by blocks: rank r of n owns contiguous block
+ * ids.  With n <= B0 these are the block rows [r*B0/n, (r+1)*B0/n) along axis
+ * 0; with n > B0 (D >= 2, n <= the block count) they are the id ranges
+ * [r*nblocks/n, (r+1)*nblocks/n), which may cut a block row (the reference
+ * deals any block count to any number of workers, runtime.cpp:115-121).  Each
+ * epoch exchanges the copies of the controls shared across ranks
+ * (ncclSend/ncclRecv with every rank that holds a copy, the
+ * runtime.cpp:123-158 exchange) and max-reduces dp.  Block-row shards send
+ * only the lattice halo rows a neighbour's decode reads; finer shards combine
+ * the lattice with one all-reduce (u64 sum: every entry has one owner, +0.0
+ * elsewhere).  Every rank decodes its own input rows.  Results equal the
  * single-device solve (bitwise for the lattice). */
 typedef struct mfadd_comm mfadd_comm;
 /* ncclGetUniqueId on one rank; the 128 bytes are then broadcast by the caller. */
@@ -181,15 +187,19 @@ void mfadd_comm_free(mfadd_comm* comm);
  * returns MFADD_ECUDA (later calls on it fail fast). */
 int mfadd_solver_create_sharded(mfadd_context* ctx, const mfadd_decomposition* dec, const mfadd_solver_config* cfg,
                                 mfadd_comm* comm, mfadd_solver** out);
-/* Host-side shard plan: block ids [blo, bhi) and own input rows [in_lo, in_hi). */
+/* Host-side shard plan: block ids [blo, bhi) and own input rows [in_lo, in_hi)
+ * (the rows the rank decodes: its block rows' own inputs, or an even split of
+ * the grid's rows when the ranges are finer than block rows). */
 int mfadd_shard_range(const mfadd_decomposition* dec, int rank, int nranks, int* blo, int* bhi, int64_t* in_lo,
                       int64_t* in_hi);
-/* The lattice rows [own_lo, own_hi) along axis 0 a rank owns. */
+/* The lattice rows [own_lo, own_hi) along axis 0 a rank's blocks own entries of
+ * (all of them for block-row shards). */
 int mfadd_shard_ctrl_rows(const mfadd_decomposition* dec, int rank, int nranks, int64_t* own_lo, int64_t* own_hi);
 /* Collective over a sharded solver's communicator: every rank's owned lattice
  * rows to every rank (no-op for a one-device solver). */
 int mfadd_solver_gather_controls(mfadd_solver* s);
-/* The axis-0 input rows [box_lo, box_hi) a rank's solve reads (its slab). */
+/* The axis-0 input rows [box_lo, box_hi) a rank's solve reads (its slab: the
+ * rows its blocks' fits touch and the rows it decodes). */
 int mfadd_shard_box(const mfadd_decomposition* dec, int rank, int nranks, int64_t* box_lo, int64_t* box_hi);
 /* Per-epoch exchange layout with one peer (recv=0: what `rank` sends, 1: what it
  * receives): entries (holder block, i0, i1, i2) in buffer order.  Returns the

@@ -768,6 +768,7 @@ struct mfadd_solver {
   // of at most P rows per side from the neighbouring ranks
   std::int64_t need_lo = 0, need_hi = 0;
   mfb::ShardRange srange;
+  bool lattice_complete = false;  // partial ranges: the lattice has been summed over the ranks since the last assembly
   std::vector<int> local_of;  // global block id -> local index (-1: other rank)
   mfadd_comm* comm = nullptr;
   std::vector<ShardPeer> peers;
@@ -1484,7 +1485,7 @@ std::unique_ptr<mfadd_solver> create_solver(mfadd_context* ctx, const mfadd_deco
     s->slist.upload(sl.empty() ? std::vector<int>{0} : sl, st);
     s->clist.upload(cl.empty() ? std::vector<int>{0} : cl, st);
     s->own_coord.upload(oc, st);
-    std::vector<std::int64_t> po(static_cast<std::size_t>(d.nblocks), 0);  // by global id (local blocks only)
+    std::vector<std::int64_t> po(static_cast<std::size_t>(d.nblocks), -1);  // by global id (-1: another rank's block)
     for (int b = s->srange.blo; b < s->srange.bhi; ++b)
       po[static_cast<std::size_t>(b)] = wl.blocks[static_cast<std::size_t>(b - s->srange.blo)].poff;
     s->poff.upload(po, st);
@@ -1511,7 +1512,8 @@ std::unique_ptr<mfadd_solver> create_solver(mfadd_context* ctx, const mfadd_deco
             o = o * pk.n + (il[k] - pk.col_lo);
           }
           const AxisProb& pl = wl.probs[static_cast<std::size_t>(s->axbase[dl] + c)];
-          rb[static_cast<std::size_t>(r * Bl + c)] = po[static_cast<std::size_t>(lead * Bl + c)] + o * pl.n - pl.col_lo;
+          const std::int64_t pb = po[static_cast<std::size_t>(lead * Bl + c)];
+          rb[static_cast<std::size_t>(r * Bl + c)] = pb < 0 ? mfb::kAsmOtherRank : pb + o * pl.n - pl.col_lo;
         }
       }
       s->rowbase.upload(rb, st);
@@ -2149,6 +2151,14 @@ struct NcclTransport : Transport {
   void gather_lattice(std::vector<mfadd_solver*>& g, bool full) override {
     mfadd_solver* s = g[0];
     const Decomp& d = s->dec;
+    if (s->srange.partial) {
+      // every entry is owned by exactly one rank and +0.0 elsewhere: the sum
+      // of the 64-bit patterns is the owner's value, bit for bit
+      if (!s->lattice_complete)
+        NCK(ncclAllReduce(s->lattice.p, s->lattice.p, s->lattice.n, ncclUint64, ncclSum, s->comm->comm, s->ctx->stream));
+      s->lattice_complete = true;
+      return;
+    }
     const std::int64_t row = lattice_row_elems(d);
     NCK(ncclGroupStart());
     for (int q = 0; q < s->nranks; ++q) {
@@ -2215,6 +2225,22 @@ struct LoopbackTransport : Transport {
   }
   void gather_lattice(std::vector<mfadd_solver*>& g, bool full) override {
     const Decomp& d = g[0]->dec;
+    if (g[0]->srange.partial) {  // the u64 sum of NcclTransport, on the host
+      if (g[0]->lattice_complete) return;
+      const std::size_t n = g[0]->lattice.n;
+      std::vector<unsigned long long> acc(n, 0ull), v(n);
+      for (mfadd_solver* s : g) {
+        CK(cudaMemcpyAsync(v.data(), s->lattice.p, n * 8, cudaMemcpyDeviceToHost, s->ctx->stream));
+        CK(cudaStreamSynchronize(s->ctx->stream));
+        for (std::size_t i = 0; i < n; ++i) acc[i] += v[i];
+      }
+      for (mfadd_solver* s : g) {
+        CK(cudaMemcpyAsync(s->lattice.p, acc.data(), n * 8, cudaMemcpyHostToDevice, s->ctx->stream));
+        CK(cudaStreamSynchronize(s->ctx->stream));
+        s->lattice_complete = true;
+      }
+      return;
+    }
     const std::int64_t row = lattice_row_elems(d);
     for (mfadd_solver* q : g)
       for (mfadd_solver* r : g) {
@@ -2332,6 +2358,12 @@ int shard_assemble_decode(mfadd_solver* s, const double* dfield) {
   aa.P = wl.P.p;
   aa.lattice = s->lattice.p;
   set_assemble_range(s, aa);
+  // block-id ranges finer than block rows: the lattice is combined by a sum
+  // over ranks of bit patterns, so every entry this rank does not own is +0.0
+  if (s->srange.partial) {
+    CK(cudaMemsetAsync(s->lattice.p, 0, s->lattice.n * sizeof(double), st));
+    s->lattice_complete = false;
+  }
   l += mfb::launch_assemble(aa, st);
   return l;
 }

@@ -1706,7 +1706,7 @@ __global__ void __launch_bounds__(256) k_assemble(AssembleArgs a) {
     const int c = own_smem ? s_own[i] : a.own_coord[a.oc_off[dl] + i];
     double v[kAsmRows];
 #pragma unroll
-    for (int r = 0; r < kAsmRows; ++r) v[r] = r < nr ? a.P[s_base[r][c] + i] : 0.0;
+    for (int r = 0; r < kAsmRows; ++r) v[r] = (r < nr && s_base[r][c] != kAsmOtherRank) ? a.P[s_base[r][c] + i] : 0.0;
 #pragma unroll
     for (int r = 0; r < kAsmRows; ++r)
       if (r < nr) out[static_cast<std::int64_t>(r) * Nl + i] = v[r];

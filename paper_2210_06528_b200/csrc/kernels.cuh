@@ -250,6 +250,7 @@ struct DpArgs {
 int launch_dp(const DpArgs& a, cudaStream_t s);
 
 // K6: assemble_owned (solver.cpp:281-294).
+constexpr long long kAsmOtherRank = -(1ll << 62);
 struct AssembleArgs {
   int D;
   int B[3];
@@ -260,6 +261,7 @@ struct AssembleArgs {
   int axbase[3];
   const std::int64_t* poff;
   const long long* rowbase;  // P offset of each lattice row in each last-dim owner block, minus its col_lo
+                             // (kAsmOtherRank: the owner block lives on another rank, entry written as +0.0)
   const double* P;
   double* lattice;
   std::int64_t row0, nrows;  // lattice rows (all dims but the last) to assemble

@@ -294,31 +294,46 @@ std::vector<Region> enumerate_regions(const Decomp& d) {
 ShardRange shard_range(const Decomp& d, int rank, int nranks) {
   if (nranks < 1 || rank < 0 || rank >= nranks) throw std::invalid_argument("shard_range: bad rank");
   const int B0 = d.blocks[0];
-  if (nranks > B0)
-    throw std::invalid_argument("shard_range: " + std::to_string(nranks) + " ranks for " + std::to_string(B0) +
-                                " block rows along axis 0");
   ShardRange s;
-  s.row_lo = static_cast<int>(static_cast<std::int64_t>(rank) * B0 / nranks);
-  s.row_hi = static_cast<int>(static_cast<std::int64_t>(rank + 1) * B0 / nranks);
-  const int per_row = d.nblocks / B0;
-  s.blo = s.row_lo * per_row;
-  s.bhi = s.row_hi * per_row;
-  s.in_lo = d.dim_field(0, s.row_lo, OWNIN_LO);
-  s.in_hi = d.dim_field(0, s.row_hi - 1, OWNIN_HI);
+  if (nranks > B0) {  // contiguous block-id ranges finer than block rows
+    if (d.rank < 2 || nranks > d.nblocks || nranks > d.grid[0])
+      throw std::invalid_argument("shard_range: " + std::to_string(nranks) + " ranks for " + std::to_string(d.nblocks) +
+                                  " blocks (" + std::to_string(B0) + " block rows along axis 0)");
+    s.partial = true;
+    s.blo = static_cast<int>(static_cast<std::int64_t>(rank) * d.nblocks / nranks);
+    s.bhi = static_cast<int>(static_cast<std::int64_t>(rank + 1) * d.nblocks / nranks);
+    s.row_lo = d.coords[static_cast<std::size_t>(s.blo)][0];
+    s.row_hi = d.coords[static_cast<std::size_t>(s.bhi - 1)][0] + 1;
+    s.in_lo = static_cast<std::int64_t>(rank) * d.grid[0] / nranks;
+    s.in_hi = static_cast<std::int64_t>(rank + 1) * d.grid[0] / nranks;
+  } else {
+    s.row_lo = static_cast<int>(static_cast<std::int64_t>(rank) * B0 / nranks);
+    s.row_hi = static_cast<int>(static_cast<std::int64_t>(rank + 1) * B0 / nranks);
+    const int per_row = d.nblocks / B0;
+    s.blo = s.row_lo * per_row;
+    s.bhi = s.row_hi * per_row;
+    s.in_lo = d.dim_field(0, s.row_lo, OWNIN_LO);
+    s.in_hi = d.dim_field(0, s.row_hi - 1, OWNIN_HI);
+  }
   s.own_lo = d.dim_field(0, s.row_lo, OWN_LO);
   s.own_hi = d.dim_field(0, s.row_hi - 1, OWN_HI);
-  s.box_lo = d.dim_field(0, s.row_lo, IN_LO);
-  s.box_hi = d.dim_field(0, s.row_hi - 1, IN_HI);
+  s.box_lo = std::min(d.dim_field(0, s.row_lo, IN_LO), s.in_lo);
+  s.box_hi = std::max(d.dim_field(0, s.row_hi - 1, IN_HI), s.in_hi);
   return s;
 }
 
 int shard_of_block(const Decomp& d, int nranks, int block) {
-  const int B0 = d.blocks[0], row = d.coords[static_cast<std::size_t>(block)][0];
-  // inverse of row_lo(r) = r*B0/n: the largest r with row_lo(r) <= row
-  int r = static_cast<int>((static_cast<std::int64_t>(row) * nranks + nranks - 1) / B0);
-  while (r > 0 && static_cast<std::int64_t>(r) * B0 / nranks > row) --r;
-  while (r + 1 < nranks && static_cast<std::int64_t>(r + 1) * B0 / nranks <= row) ++r;
-  return r;
+  const int B0 = d.blocks[0];
+  // inverse of lo(r) = r*N/n: the largest r with lo(r) <= x
+  auto inv = [nranks](std::int64_t x, std::int64_t N) {
+    int r = static_cast<int>((x * nranks + nranks - 1) / N);
+    if (r >= nranks) r = nranks - 1;
+    while (r > 0 && static_cast<std::int64_t>(r) * N / nranks > x) --r;
+    while (r + 1 < nranks && static_cast<std::int64_t>(r + 1) * N / nranks <= x) ++r;
+    return r;
+  };
+  if (nranks > B0) return inv(block, d.nblocks);
+  return inv(d.coords[static_cast<std::size_t>(block)][0], B0);
 }
 
 std::vector<PeerLayout> shard_peers(const Decomp& d, const std::vector<Region>& regions, int rank, int nranks) {

@@ -88,15 +88,22 @@ struct Region {
 std::vector<Region> enumerate_regions(const Decomp& d);
 
 // ------------------------------------------------------------ sharding
-// Rank r of n owns block rows [row_lo, row_hi) along axis 0 (block ids are
-// lexicographic with axis 0 slowest, layout.cpp:320-323), i.e. the contiguous
-// block ids [blo, bhi).  A shared control then has holders on at most two
-// adjacent ranks.
+// Rank r of n owns the contiguous block ids [blo, bhi) (ids are lexicographic
+// with axis 0 slowest, layout.cpp:320-323).  With n <= B0 the ranges are whole
+// block rows [row_lo, row_hi) along axis 0 (r*B0/n .. (r+1)*B0/n): a shared
+// control then has holders on at most two adjacent ranks, and a rank decodes
+// the input rows its block rows own.  With n > B0 (D >= 2, n <= nblocks) the
+// ranges are [r*nblocks/n, (r+1)*nblocks/n) and may cut a block row
+// (`partial`): holders then sit on any of the neighbouring ranks, the owned
+// lattice entries are a subset of the rows [own_lo, own_hi), and the input
+// rows are split evenly over the ranks for the decode (the reference deals any
+// block count to any number of workers, runtime.cpp:115-121).
 struct ShardRange {
   int row_lo = 0, row_hi = 0, blo = 0, bhi = 0;
+  bool partial = false;                 // block-id ranges finer than block rows
   std::int64_t in_lo = 0, in_hi = 0;    // own input rows along axis 0 (decode)
-  std::int64_t own_lo = 0, own_hi = 0;  // owned control indices along axis 0 (assembly)
-  std::int64_t box_lo = 0, box_hi = 0;  // input rows touched by the local blocks' fits
+  std::int64_t own_lo = 0, own_hi = 0;  // control rows along axis 0 the local blocks own entries of (assembly)
+  std::int64_t box_lo = 0, box_hi = 0;  // input rows the rank reads: its blocks' fits and its decode rows
 };
 ShardRange shard_range(const Decomp& d, int rank, int nranks);
 int shard_of_block(const Decomp& d, int nranks, int block);

@@ -187,3 +187,30 @@ def test_shard_box_covers_its_blocks(n):
         assert lo == min(int(bd[b, 0, 12]) for b in range(blo, bhi))
         assert hi == max(int(bd[b, 0, 13]) for b in range(blo, bhi))
         assert lo <= ilo < ihi <= hi
+
+
+@pytest.mark.parametrize("n", [5, 8, 16])
+def test_shard_ranges_finer_than_block_rows(n):
+    """More ranks than block rows along axis 0: contiguous block-id ranges
+    (runtime.cpp:115-121 deals any block count to any worker count), input rows
+    split evenly for the decode, slab = fit rows and decode rows."""
+    dec = m.partition((96, 100, 104), [(0, 1)] * 3, (4, 4, 4), 3, (12, 12, 13), 3)
+    bd = dec.block_dims_array()
+    nxt_b, nxt_i = 0, 0
+    for r in range(n):
+        blo, bhi, ilo, ihi = m.shard_range(dec, r, n)
+        lo, hi = m.shard_box(dec, r, n)
+        olo, ohi = m.shard_ctrl_rows(dec, r, n)
+        assert (blo, ilo) == (nxt_b, nxt_i) and bhi > blo and ihi > ilo
+        nxt_b, nxt_i = bhi, ihi
+        assert lo == min(min(int(bd[b, 0, 12]) for b in range(blo, bhi)), ilo)
+        assert hi == max(max(int(bd[b, 0, 13]) for b in range(blo, bhi)), ihi)
+        assert olo == min(int(bd[b, 0, 10]) for b in range(blo, bhi))
+        assert ohi == max(int(bd[b, 0, 11]) for b in range(blo, bhi))
+        # every exchange plan is symmetric: what r sends to q is what q receives from r
+        for q in range(n):
+            if q != r:
+                assert np.array_equal(m.shard_exchange(dec, r, n, q, False), m.shard_exchange(dec, q, n, r, True))
+    assert (nxt_b, nxt_i) == (64, 96)
+    with pytest.raises(ValueError):
+        m.shard_range(dec, 0, 65)

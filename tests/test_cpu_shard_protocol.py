@@ -120,7 +120,7 @@ def _worker(rank, nranks, port, case, out):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("case,nranks", [("2d", 2), ("2d", 3), ("3d", 2)])
+@pytest.mark.parametrize("case,nranks", [("2d", 2), ("2d", 3), ("3d", 2), ("2d", 5)])
 def test_gloo_shard_protocol_matches_reference(case, nranks):
     mgr = mp.get_context("spawn").Manager()
     out = mgr.dict()
