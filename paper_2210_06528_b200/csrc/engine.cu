@@ -227,8 +227,9 @@ struct Workload {
   DBuf<AxisProb> d_probs;
   DBuf<BlockDev> d_blocks;
   DBuf<int> d_factor, g0, first_col, count;
-  DBuf<double> vals, ltab, t1, t2, P, Y, rlt;
-  std::int64_t rlt_stride = 0;
+  DBuf<double> vals, ltab, t1, t2, P, Y, rlt, twf;
+  std::int64_t rlt_stride = 0, twf_stride = 0;
+  bool tw2d = false;  // k_solve2d runs the twisted (two-sided) passes
   DBuf<unsigned long long> linf_int;
   DBuf<unsigned char> sflag;
   std::int64_t sflag_off[3] = {0, 0, 0};
@@ -437,8 +438,27 @@ struct Workload {
     count.alloc(static_cast<std::size_t>(total_rows));
     vals.alloc(static_cast<std::size_t>(total_rows * (p + 1)));
     ltab.alloc(static_cast<std::size_t>(std::max<std::int64_t>(total_cols, 1) * (2 * p + 1)));
-    rlt_stride = (mfb::rl_table_doubles(p, max_n_factor) + 1) / 2 * 2;  // even: 16-B aligned per problem
+    // k_solve2d's twisted passes (MFADD_TWIST=1; measured slower than the plain
+    // passes on C5, see k_solve2d_tw): every factored extent long enough and
+    // the CTA's tile + side buffers within shared memory
+    tw2d = false;
+    if (D == 2 && tma_last && std::getenv("MFADD_TWIST") && !std::getenv("MFADD_NO_FUSE2D")) {
+      int mn0 = 0, mn1 = 0, mzl = 0;
+      bool ok = !blocks.empty();
+      for (const auto& b : blocks) {
+        mn0 = std::max(mn0, probs[static_cast<std::size_t>(b.ax[0])].n);
+        mn1 = std::max(mn1, probs[static_cast<std::size_t>(b.ax[1])].n);
+        mzl = std::max(mzl, b.zl);
+      }
+      for (int id : factor_ids) ok = ok && mfb::tw_ok(probs[static_cast<std::size_t>(id)].n, p);
+      tw2d = ok && mfb::solve2d_smem(p, mn0, mn1, mzl, last_kseg, true) > 0;
+    }
+    rlt_stride = (mfb::rl_table_doubles(p, max_n_factor, tw2d) + 1) / 2 * 2;  // even: 16-B aligned per problem
     rlt.alloc(static_cast<std::size_t>(probs.size() * rlt_stride));
+    if (tw2d) {
+      twf_stride = 2 * static_cast<std::int64_t>(max_n_factor) * (p + 1);
+      twf.alloc(static_cast<std::size_t>(probs.size() * twf_stride));
+    }
     t1.alloc(static_cast<std::size_t>(total_t1));
     t2.alloc(static_cast<std::size_t>(total_t2));
     P.alloc(static_cast<std::size_t>(total_p));
@@ -482,6 +502,10 @@ struct Workload {
     for (int id : factor_ids) max_m_factor = std::max(max_m_factor, probs[static_cast<std::size_t>(id)].m);
     mfb::CholArgs ca{d_probs.p, d_factor.p, static_cast<int>(factor_ids.size()), max_n_factor, max_m_factor, 0, 0,
                      g0.p, vals.p, ltab.p, ctx->d_status};
+    if (tw2d) {
+      ca.tw = twf.p;
+      ca.tw_stride = twf_stride;
+    }
     if (fork) {  // the factorizations run beside the axis-0 sweep
       if (!side) {
         CK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
@@ -501,14 +525,14 @@ struct Workload {
         CK(cudaEventRecord(ev_rows2, side));
       }
       l += mfb::launch_gram_chol(p, ca, side);
-      if (D == 2 && tma_last) l += mfb::launch_rl_tables(p, ca, rlt.p, rlt_stride, side);
+      if (D == 2 && tma_last) l += mfb::launch_rl_tables(p, ca, rlt.p, rlt_stride, side, tw2d);
       tl->end();
       tl->st = main_st;
       CK(cudaEventRecord(ev_chol, side));
     } else {
       tl->begin("gram_chol");
       l += mfb::launch_gram_chol(p, ca, ctx->stream);
-      if (D == 2 && tma_last) l += mfb::launch_rl_tables(p, ca, rlt.p, rlt_stride, ctx->stream);
+      if (D == 2 && tma_last) l += mfb::launch_rl_tables(p, ca, rlt.p, rlt_stride, ctx->stream, tw2d);
       tl->end();
     }
     CK(cudaGetLastError());
@@ -589,7 +613,8 @@ struct Workload {
         fa.max_n1 = std::max(fa.max_n1, probs[static_cast<std::size_t>(b.ax[1])].n);
         fa.max_zl = std::max(fa.max_zl, b.zl);
       }
-      fa.fuse2d = mfb::solve2d_smem(p, fa.max_n0, fa.max_n1, fa.max_zl, last_kseg) > 0 ? 1 : 0;
+      fa.fuse2d = mfb::solve2d_smem(p, fa.max_n0, fa.max_n1, fa.max_zl, last_kseg, tw2d) > 0 ? 1 : 0;
+      fa.tw2d = fa.fuse2d && tw2d ? 1 : 0;
     }
     if (rows_split && D == 2) CK(cudaStreamWaitEvent(ctx->stream, ev_rows2, 0));  // last-axis + decode rows
     if (D == 2 && defer_mode == 2 && tma_last) fa.join_event = ev_chol;

@@ -177,6 +177,75 @@ __global__ void __launch_bounds__(256) k_basis_rows(RowsArgs a) {
   }
 }
 
+// Banded Cholesky (the Eigen LLT of lsq.cpp:46-49 restricted to the band: L
+// has no fill outside it) by one thread, right-looking within each row: as
+// soon as L(c,c-k) is known it is applied to the pending sums of the entries
+// left of it and to the diagonal, so the dependent chain per entry is one
+// multiply and one FMA.  The last P rows sit in a register ring with
+// compile-time slots (row j in slot j mod P; the column loop is unrolled by
+// P), so the next row's first entries overlap this row's rsqrt.  src row c
+// holds [G(c,c), G(c,c-1), .., G(c,c-P)] (zero where c-k < 0); row c of dst
+// becomes [1/L(c,c), L(c,c-1), .., L(c,c-P)] (dst may be src).  FLIP: the
+// factor of the index-reversed matrix, G'(c,c-k) = G(n-1-c+k, n-1-c) read from
+// src.  Rows [0, rows) are factored.  Returns the first non-positive pivot's
+// row (Eigen LLT NumericalIssue -> SingularFitError) or -1.
+template <int P, bool FLIP>
+__device__ __forceinline__ int banded_chol(const double* src, double* dst, const int n, const int rows) {
+  double R[P][P + 1];  // R[j mod P] = [1/L(j,j), L(j,j-1), .., L(j,j-P)]
+#pragma unroll
+  for (int r = 0; r < P; ++r)
+#pragma unroll
+    for (int k = 0; k <= P; ++k) R[r][k] = 0.0;
+  // Branch-free body (the tail past `rows` reads row 0 and is not stored), so
+  // the compiler can overlap a row's first entries with the previous row's
+  // reciprocal square root.
+  int bad = -1;
+  for (int c0 = 0; c0 < rows; c0 += P) {
+#pragma unroll
+    for (int u = 0; u < P; ++u) {
+      const int c = c0 + u;
+      const bool in = c < rows;
+      double g[P + 1];
+#pragma unroll
+      for (int k = 0; k <= P; ++k) {
+        if (FLIP) {
+          const bool ok = in && k <= c;  // row n-1-c+k < n
+          const double gv = src[(ok ? n - 1 - c + k : 0) * (P + 1) + k];
+          g[k] = ok ? gv : (in ? 0.0 : 1.0);
+        } else {
+          g[k] = in ? src[c * (P + 1) + k] : 1.0;
+        }
+      }
+      double Lc[P + 1];
+#pragma unroll
+      for (int k = P; k >= 1; --k) {
+        const int sj = (u - k + P) % P;  // row c-k
+        const double lk = g[k] * R[sj][0];
+        Lc[k] = lk;
+#pragma unroll
+        for (int k2 = k - 1; k2 >= 1; --k2) g[k2] = fma(-lk, R[(u - k2 + P) % P][k - k2], g[k2]);
+        g[0] = fma(-lk, lk, g[0]);
+      }
+      double dg = g[0];
+      const bool sing = !(dg > 0.0);
+      bad = (sing && in && bad < 0) ? c : bad;
+      dg = sing ? 1.0 : dg;
+      // 1/sqrt(dg): fp32 estimate + two Newton steps (no slow-path branch)
+      double y = static_cast<double>(rsqrtf(static_cast<float>(dg)));
+      y = y * fma(-0.5 * dg, y * y, 1.5);
+      y = y * fma(-0.5 * dg, y * y, 1.5);
+      Lc[0] = y;
+      double* Gc = dst + (in ? c : 0) * (P + 1);
+#pragma unroll
+      for (int k = 0; k <= P; ++k) {
+        if (in) Gc[k] = Lc[k];
+        R[u % P][k] = Lc[k];
+      }
+    }
+  }
+  return bad;
+}
+
 // ------------------------------------------------------------------- K2
 template <int P>
 __global__ void __launch_bounds__(256) k_gram_chol(CholArgs a) {
@@ -187,6 +256,10 @@ __global__ void __launch_bounds__(256) k_gram_chol(CholArgs a) {
   const int* g0 = a.g0 + pr.row_off;
   const double* v = a.vals + pr.row_off * (P + 1);
   double* band = a.ltab + pr.col_off * (2 * P + 1);  // light mode: the Gram band between the two launches
+  // twisted solves: a pristine copy of the band (sm2) and the factor of the
+  // index-reversed matrix (sm3), behind everything else in shared memory
+  double* sm2 = a.tw ? sm + a.max_n * (P + 1) + (a.stage_rows ? a.max_m * (P + 1) + (a.max_m + 1) / 2 : 0) : nullptr;
+  double* sm3 = a.tw ? sm2 + a.max_n * (P + 1) : nullptr;
   if (a.light == 2) {  // Cholesky-only launch: the band written by the Gram-only launch
     constexpr int B = 8;  // independent loads in flight per thread (one warp)
     const int nv = n * (P + 1), nt = static_cast<int>(blockDim.x);
@@ -196,7 +269,10 @@ __global__ void __launch_bounds__(256) k_gram_chol(CholArgs a) {
       for (int u = 0; u < B; ++u) t[u] = e0 + u * nt < nv ? band[e0 + u * nt] : 0.0;
 #pragma unroll
       for (int u = 0; u < B; ++u)
-        if (e0 + u * nt < nv) sm[e0 + u * nt] = t[u];
+        if (e0 + u * nt < nv) {
+          sm[e0 + u * nt] = t[u];
+          if (sm2) sm2[e0 + u * nt] = t[u];
+        }
     }
     __syncthreads();
   } else {
@@ -247,6 +323,7 @@ __global__ void __launch_bounds__(256) k_gram_chol(CholArgs a) {
       }
     }
     sm[e] = s;
+    if (sm2) sm2[e] = s;
   }
   if (a.light == 1) {  // Gram-only launch
     for (int e = threadIdx.x; e < n * (P + 1); e += blockDim.x) band[e] = sm[e];
@@ -254,60 +331,15 @@ __global__ void __launch_bounds__(256) k_gram_chol(CholArgs a) {
   }
   __syncthreads();
   }
+  // Banded Cholesky by thread 0; twisted solves: the first thread of warp 1
+  // factors the index-reversed matrix beside it (its own warp: neither
+  // instruction stream waits for the other), only as far as the bottom half
+  // of the twisted solve reaches.
   if (threadIdx.x == 0) {
-    // Banded Cholesky (the Eigen LLT of lsq.cpp:46-49 restricted to the band:
-    // L has no fill outside it), right-looking within each row: as soon as
-    // L(c,c-k) is known it is applied to the pending sums of the entries
-    // left of it and to the diagonal, so the dependent chain per entry is one
-    // multiply and one FMA.  The last P rows sit in a register ring with
-    // compile-time slots (row j in slot j mod P; the column loop is unrolled
-    // by P), so the next row's first entries overlap this row's rsqrt.  Row c
-    // is written back over sm[c*(P+1)..]: [1/L(c,c), L(c,c-1), .., L(c,c-P)].
-    double R[P][P + 1];  // R[j mod P] = [1/L(j,j), L(j,j-1), .., L(j,j-P)]
-#pragma unroll
-    for (int r = 0; r < P; ++r)
-#pragma unroll
-      for (int k = 0; k <= P; ++k) R[r][k] = 0.0;
-    // Branch-free body (the tail past n reads the zero-padded Gram rows and is
-    // not stored), so the compiler can overlap a row's first entries with the
-    // previous row's reciprocal square root.
-    int bad = -1;
-    for (int c0 = 0; c0 < n; c0 += P) {
-#pragma unroll
-      for (int u = 0; u < P; ++u) {
-        const int c = c0 + u;
-        const bool in = c < n;
-        double* Gc = sm + (in ? c : 0) * (P + 1);
-        double g[P + 1];
-#pragma unroll
-        for (int k = 0; k <= P; ++k) g[k] = in ? Gc[k] : 1.0;  // G(c,c), G(c,c-k); zero where c-k < 0
-        double Lc[P + 1];
-#pragma unroll
-        for (int k = P; k >= 1; --k) {
-          const int sj = (u - k + P) % P;  // row c-k
-          const double lk = g[k] * R[sj][0];
-          Lc[k] = lk;
-#pragma unroll
-          for (int k2 = k - 1; k2 >= 1; --k2) g[k2] = fma(-lk, R[(u - k2 + P) % P][k - k2], g[k2]);
-          g[0] = fma(-lk, lk, g[0]);
-        }
-        double dg = g[0];
-        const bool sing = !(dg > 0.0);  // Eigen LLT NumericalIssue -> SingularFitError
-        bad = (sing && in && bad < 0) ? c : bad;
-        dg = sing ? 1.0 : dg;
-        // 1/sqrt(dg): fp32 estimate + two Newton steps (no slow-path branch)
-        double y = static_cast<double>(rsqrtf(static_cast<float>(dg)));
-        y = y * fma(-0.5 * dg, y * y, 1.5);
-        y = y * fma(-0.5 * dg, y * y, 1.5);
-        Lc[0] = y;
-#pragma unroll
-        for (int k = 0; k <= P; ++k) {
-          if (in) Gc[k] = Lc[k];
-          R[u % P][k] = Lc[k];
-        }
-      }
-    }
+    const int bad = banded_chol<P, false>(sm, sm, n, n);
     if (bad >= 0) set_status(a.status, 3, pid, bad);
+  } else if (a.tw && threadIdx.x == 32) {
+    banded_chol<P, true>(sm2, sm3, n, n - (n - P) / 2);  // nb + P rows (tw_bot)
   }
   __syncthreads();
   // table per column: [1/L(c,c), L(c,c-k) k=1..P, L(c+k,c) k=1..P]
@@ -324,6 +356,14 @@ __global__ void __launch_bounds__(256) k_gram_chol(CholArgs a) {
       val = (c + k < n) ? sm[(c + k) * (P + 1) + k] : 0.0;
     }
     out[e] = val;
+  }
+  if (a.tw) {  // reversed factor, then the Gram band
+    double* tw = a.tw + static_cast<std::int64_t>(pid) * a.tw_stride;
+    const int fr = (n - (n - P) / 2) * (P + 1);  // factored rows of the reversed matrix
+    for (int e = threadIdx.x; e < n * (P + 1); e += blockDim.x) {
+      tw[e] = e < fr ? sm3[e] : 0.0;
+      tw[n * (P + 1) + e] = sm2[e];
+    }
   }
 }
 
@@ -1964,9 +2004,13 @@ struct CholLaunch {
     if (a.nfactor == 0) return 0;
     CholArgs b = a;
     size_t smem = static_cast<size_t>(a.max_n) * (P + 1) * sizeof(double);
-    const size_t staged = smem + static_cast<size_t>(a.max_m) * ((P + 1) * sizeof(double) + sizeof(int));
-    b.stage_rows = !a.light && staged <= 200 * 1024;
+    const size_t twb = a.tw ? 2 * smem : 0;  // pristine band + reversed factor
+    // staged rows: vals, then g0 as ints (rounded up to whole doubles)
+    const size_t staged = smem + static_cast<size_t>(a.max_m) * (P + 1) * sizeof(double) +
+                          static_cast<size_t>((a.max_m + 1) / 2) * sizeof(double);
+    b.stage_rows = !a.light && staged + twb <= 200 * 1024;
     if (b.stage_rows) smem = staged;
+    smem += twb;
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_gram_chol<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (!a.light) {
       k_gram_chol<P><<<a.nfactor, 256, smem, s>>>(b);
@@ -1978,10 +2022,11 @@ struct CholLaunch {
     // full CTA's resources for the length of the dependent chain
     b.light = 1;
     b.stage_rows = 0;  // rows through L1: no shared-memory footprint beyond the band
-    k_gram_chol<P><<<a.nfactor, 256, static_cast<size_t>(a.max_n) * (P + 1) * sizeof(double), s>>>(b);
+    const size_t band = static_cast<size_t>(a.max_n) * (P + 1) * sizeof(double);
+    k_gram_chol<P><<<a.nfactor, 256, band + twb, s>>>(b);
     b.light = 2;
     b.stage_rows = 0;
-    k_gram_chol<P><<<a.nfactor, 32, static_cast<size_t>(a.max_n) * (P + 1) * sizeof(double), s>>>(b);
+    k_gram_chol<P><<<a.nfactor, a.tw ? 64 : 32, band + twb, s>>>(b);
     return 2;
     return 1;
   }

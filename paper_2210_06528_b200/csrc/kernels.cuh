@@ -72,12 +72,22 @@ struct CholArgs {
   const double* vals;
   double* ltab;
   DevStatus* status;
+  // Twisted (two-sided) solves of k_solve2d: per problem, the Cholesky factor
+  // of the index-reversed Gram matrix ([n][P+1], same row format as the band)
+  // followed by the Gram band itself; null when unused.
+  double* tw = nullptr;
+  std::int64_t tw_stride = 0;
 };
+// Twisted solve of an extent-n problem: rows [0, a) are eliminated from the
+// top, rows [a+P, n) from the bottom, the P rows between last (a dense P x P
+// Schur complement).  Needs at least P rows in each outer part.
+inline bool tw_ok(int n, int P) { return n >= 4 * P + 2; }
 int launch_gram_chol(int degree, const CholArgs& a, cudaStream_t s);
 // The solve kernels' right-looking step tables of every factored problem,
 // once per solve after the factorizations: rlt + problem id * stride.
-int launch_rl_tables(int degree, const CholArgs& a, double* rlt, std::int64_t stride, cudaStream_t s);
-std::int64_t rl_table_doubles(int degree, int n);  // forward + backward table of an extent-n problem
+int launch_rl_tables(int degree, const CholArgs& a, double* rlt, std::int64_t stride, cudaStream_t s, bool tw = false);
+// forward + backward table of an extent-n problem, or its twisted table set
+std::int64_t rl_table_doubles(int degree, int n, bool tw = false);
 
 // K3: per-axis fit passes (lsq.cpp:57-61 fused: R^T contraction in row order
 // + forward substitution + back substitution).
@@ -110,12 +120,13 @@ struct FitArgs {
   const double* rlt;                 // right-looking step tables per axis problem (k_rl_tables), or null
   std::int64_t rlt_stride;           // doubles per axis problem in rlt (forward then backward table)
   int max_n0, max_n1, max_zl;        // largest held extents / Z pitch (k_solve2d shared-memory size)
+  int tw2d;                          // k_solve2d: twisted passes (rlt holds the twisted table sets)
   void* join_event;                  // cudaEvent_t the last-axis solve waits for (factorizations on a side stream)
 };
 int launch_fit_strided(int degree, const FitArgs& a, int axis, cudaStream_t s);  // axis < D-1
 int launch_fit_last(int degree, const FitArgs& a, cudaStream_t s);
 // Shared-memory bytes of k_solve2d for held extents n0 x n1 (0 if it does not fit one CTA).
-size_t solve2d_smem(int degree, int n0, int n1, int zl, int kseg);
+size_t solve2d_smem(int degree, int n0, int n1, int zl, int kseg, bool tw = false);
 
 // D = 1: CTA per block, column-parallel R^T q + serial banded solve (smem: max_n x (2P+2) doubles).
 int launch_fit_1d(int degree, const FitArgs& a, int max_n, cudaStream_t s);

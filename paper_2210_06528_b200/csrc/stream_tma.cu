@@ -14,6 +14,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 
@@ -1093,11 +1094,23 @@ struct RLFinal {  // last pass of a tile: results also go to HBM (+ L-inf)
   unsigned long long lmax;
 };
 
+// MFB_RL_GTAB=1 (measurement knob): the plain passes read the step tables from
+// global memory through L1 instead of staging them in shared memory.  Measured
+// slower on C5 (fit_last 193 us against 121 us; 181 / 177 us with the rows
+// loaded 2 / 3 steps ahead): a broadcast 16-byte load costs four shared-memory
+// wavefronts, but the L1 path's latency costs more.
+#ifndef MFB_RL_GTAB
+#define MFB_RL_GTAB 0
+#endif
 template <int P>
 __device__ __forceinline__ void rl_load_step(const double* row, double (&cf)[RL<P>::W]) {
 #pragma unroll
   for (int h = 0; h < RL<P>::W / 2; ++h) {
+#if MFB_RL_GTAB
+    const double2 v = __ldg(reinterpret_cast<const double2*>(row) + h);
+#else
     const double2 v = reinterpret_cast<const double2*>(row)[h];
+#endif
     cf[2 * h] = v.x;
     cf[2 * h + 1] = v.y;
   }
@@ -1110,10 +1123,17 @@ __device__ __forceinline__ void rl_load_step(const double* row, double (&cf)[RL<
 #ifndef MFB_RL_PF
 #define MFB_RL_PF 1
 #endif
-template <int P, bool TAIL, bool FINAL>
+// SIDE (twisted forward passes): steps [side_e, n) hold the pending sums of
+// the middle rows, which go to side[(t - side_e) * side_stride] instead of the
+// line (the other half of the line still reads those rows).
+struct RLSide {
+  double* side;
+  int stride, e;
+};
+template <int P, bool TAIL, bool FINAL, bool SIDE = false>
 __device__ __forceinline__ void rl_batch(double* __restrict__ x0, const int ds, const int n, const int t0,
                                          const double* __restrict__ tab, double (&acc)[P], double (&zin)[RL<P>::U],
-                                         double (&cf)[MFB_RL_PF][RL<P>::W], RLFinal& fin) {
+                                         double (&cf)[MFB_RL_PF][RL<P>::W], RLFinal& fin, const RLSide sd = RLSide{}) {
   constexpr int U = RL<P>::U, W = RL<P>::W, PF = MFB_RL_PF;
   double znx[U];
 #pragma unroll
@@ -1132,7 +1152,10 @@ __device__ __forceinline__ void rl_batch(double* __restrict__ x0, const int ds, 
     acc[u % P] = fma(-cf[0][P - 1], y, zin[u] * cf[0][P]);
     const int t = t0 + u;
     if (!TAIL || t < n) {
-      x0[t * ds] = y;
+      if (SIDE && TAIL && t >= sd.e)  // (a full batch ends U + P steps before n: below sd.e)
+        sd.side[(t - sd.e) * sd.stride] = y;
+      else
+        x0[t * ds] = y;
       if (FINAL) {
         fin.dst[t * fin.dstride] = y;
         if (!fin.line_shared && t >= fin.t_lo && t < fin.t_hi) {  // no shared-memory flag on the chain
@@ -1152,28 +1175,161 @@ __device__ __forceinline__ void rl_batch(double* __restrict__ x0, const int ds, 
   for (int u = 0; u < U; ++u) zin[u] = znx[u];
 }
 
-template <int P, bool FINAL>
+// init (twisted backward passes): the first P values come from registers
+// instead of the line.
+template <int P, bool FINAL, bool SIDE = false, bool INIT = false>
 __device__ __forceinline__ void rl_pass(double* __restrict__ x0, const int ds, const int n,
-                                        const double* __restrict__ tab, RLFinal& fin) {
+                                        const double* __restrict__ tab, RLFinal& fin, const RLSide sd = RLSide{},
+                                        const double* init = nullptr) {
   constexpr int U = RL<P>::U, W = RL<P>::W, PF = MFB_RL_PF;
   double acc[P], zin[U];
 #pragma unroll
-  for (int k = 0; k < P; ++k) acc[k] = (k < n ? x0[k * ds] : 0.0) * tab[(k - P) * W + P];
+  for (int k = 0; k < P; ++k)
+    acc[k] = (INIT ? init[k] : (k < n ? x0[k * ds] : 0.0)) * (MFB_RL_GTAB ? __ldg(tab + (k - P) * W + P) : tab[(k - P) * W + P]);
 #pragma unroll
   for (int u = 0; u < U; ++u) zin[u] = P + u < n ? x0[(P + u) * ds] : 0.0;
   double cf[PF][W];
 #pragma unroll
   for (int q = 0; q < PF; ++q) rl_load_step<P>(tab + q * W, cf[q]);
   int t0 = 0;
-  for (; t0 + 2 * U + P <= n; t0 += U) rl_batch<P, false, FINAL>(x0, ds, n, t0, tab, acc, zin, cf, fin);
-  for (; t0 < n; t0 += U) rl_batch<P, true, FINAL>(x0, ds, n, t0, tab, acc, zin, cf, fin);
+  for (; t0 + 2 * U + P <= n; t0 += U) rl_batch<P, false, FINAL, SIDE>(x0, ds, n, t0, tab, acc, zin, cf, fin, sd);
+  for (; t0 < n; t0 += U) rl_batch<P, true, FINAL, SIDE>(x0, ds, n, t0, tab, acc, zin, cf, fin, sd);
 }
 
-__host__ __device__ inline size_t solve2d_smem_bytes(int n0, int n1, int zl, int P, int kseg) {
+// ---- twisted (two-sided) solve of one banded SPD system G x = z
+// Rows [0, a) are eliminated from the top with the standard factor L, rows
+// [a+P, n) from the bottom with the factor L' of the index-reversed matrix,
+// and the P rows between them last, through the explicit inverse of their
+// dense Schur complement S.  Two threads share a line: each runs a forward
+// pass over its outer part (leaving its contribution to the middle rows'
+// right-hand side in a side buffer), both form x_M = S^-1 r, and each runs the
+// backward pass of its part outwards from the middle.  The arithmetic per row
+// is that of lsq.cpp:59-60 with another elimination order (1e-10 contract);
+// the dependent chain is n/2 + P steps per pass instead of n.
+// Table set of one problem: [TF | TB | BF | BB | S^-1 (P*P, padded even)],
+// step tables in the layout of rl_pass over a + P (top) / nb + P (bottom)
+// steps, the last P forward steps (first P backward steps) being the middle
+// rows.
+__host__ __device__ inline int tw_top(int n, int P) { return (n - P) / 2; }
+__host__ __device__ inline int tw_bot(int n, int P) { return n - P - (n - P) / 2; }
+__host__ __device__ inline int tw_table_doubles(int n, int P) {
   const int W = (P + 2) & ~1;
-  return 128 + (static_cast<size_t>(n1) * zl + static_cast<size_t>(kseg > 1 ? kseg - 1 : 0) * (P + 1) * zl +
-                2 * static_cast<size_t>(rl_rows(n0, P) + rl_rows(n1, P)) * W) *
-                   8 +
+  return 2 * (rl_rows(tw_top(n, P) + P, P) + rl_rows(tw_bot(n, P) + P, P)) * W + ((P * P + 1) & ~1);
+}
+
+// Forward / backward step tables of one half.  rec(i, 0) = 1/Lh(i,i) and
+// rec(i, k) = Lh(i, i-k) in the half's own index space (bottom: reversed),
+// e = rows eliminated by the half, top = the half whose forward pass carries
+// the middle rows' own right-hand side.
+template <int P, class Rec>
+__device__ __forceinline__ void build_tw_half(Rec rec, int e, bool top, double* f, double* b, int tid, int nthr) {
+  constexpr int W = RL<P>::W;
+  const int rows = rl_rows(e + P, P);
+  for (int i = tid; i < rows * W; i += nthr) {
+    const int t = i / W - P, k = i - (t + P) * W;
+    double fv = 0.0, bv = 0.0;
+    if (k < P) {
+      const int j = k + 1;
+      if (t >= 0 && t < e) fv = rec(t + j, j) * (t + j < e ? rec(t + j, 0) : 1.0);
+      if (t >= 0 && t < e + P) {
+        const int rho = e + P - 1 - t, tgt = rho - j;
+        if (tgt >= 0 && tgt < e) bv = rec(rho, j) * rec(tgt, 0);
+      }
+    } else if (k == P) {
+      const int te = t + P;  // the step whose value enters here
+      fv = te < e ? rec(te, 0) : (te < e + P ? (top ? 1.0 : 0.0) : 0.0);
+      const int r = e - 1 - t;
+      bv = t < 0 ? 1.0 : (r >= 0 ? rec(r, 0) : 0.0);
+    }
+    f[i] = fv;
+    b[i] = bv;
+  }
+}
+
+// lt: standard factor table (2P+1 per column), rv: reversed factor ([n][P+1]),
+// gb: Gram band ([n][P+1]); out: the problem's table set.
+template <int P>
+__device__ void build_tw_tables(const double* lt, const double* rv, const double* gb, int n, double* out, int tid,
+                                int nthr) {
+  constexpr int LW = 2 * P + 1, W = RL<P>::W;
+  const int a = tw_top(n, P), nb = tw_bot(n, P);
+  double* tf = out;
+  double* tb = tf + rl_rows(a + P, P) * W;
+  double* bf = tb + rl_rows(a + P, P) * W;
+  double* bb = bf + rl_rows(nb + P, P) * W;
+  double* sinv = bb + rl_rows(nb + P, P) * W;
+  auto rt = [lt](int i, int k) { return __ldg(lt + i * LW + k); };
+  auto rb = [rv](int i, int k) { return __ldg(rv + i * (P + 1) + k); };
+  build_tw_half<P>(rt, a, true, tf + 0, tb + 0, tid, nthr);
+  build_tw_half<P>(rb, nb, false, bf + 0, bb + 0, tid, nthr);
+  if (tid == nthr - 1) {
+    // S = S_top + S_bot - G_MM with S_top = L_MM L_MM^T (what is left of the
+    // middle block after the top eliminations), S_bot likewise from below.
+    // Everything in registers (compile-time indices).
+    double Lt[P][P], Lb[P][P];  // Lh(base+i, base+j), j <= i
+#pragma unroll
+    for (int i = 0; i < P; ++i)
+#pragma unroll
+      for (int j = 0; j < P; ++j) {
+        Lt[i][j] = j > i ? 0.0 : (i == j ? 1.0 / rt(a + i, 0) : rt(a + i, i - j));
+        Lb[i][j] = j > i ? 0.0 : (i == j ? 1.0 / rb(nb + i, 0) : rb(nb + i, i - j));
+      }
+    double S[P][P], I[P][P];
+#pragma unroll
+    for (int i = 0; i < P; ++i)
+#pragma unroll
+      for (int j = 0; j < P; ++j) {
+        if (j > i) continue;  // actual rows (a+i, a+j)
+        double st = 0.0, sb = 0.0;
+#pragma unroll
+        for (int m = 0; m < P; ++m)
+          if (m <= j) st = fma(Lt[i][m], Lt[j][m], st);
+        // reversed middle indices: row a+i <-> nb + (P-1-i), so (i, j) is the
+        // reversed block's entry (P-1-j, P-1-i) with P-1-j >= P-1-i
+#pragma unroll
+        for (int m = 0; m < P; ++m)
+          if (m <= P - 1 - i) sb = fma(Lb[P - 1 - j][m], Lb[P - 1 - i][m], sb);
+        const double g = __ldg(gb + (a + i) * (P + 1) + (i - j));
+        S[i][j] = st + sb - g;
+        S[j][i] = S[i][j];
+      }
+#pragma unroll
+    for (int i = 0; i < P; ++i)
+#pragma unroll
+      for (int j = 0; j < P; ++j) I[i][j] = i == j ? 1.0 : 0.0;
+#pragma unroll
+    for (int c = 0; c < P; ++c) {  // Gauss-Jordan (S is SPD: no pivoting)
+      const double pv = 1.0 / S[c][c];
+#pragma unroll
+      for (int j = 0; j < P; ++j) {
+        S[c][j] *= pv;
+        I[c][j] *= pv;
+      }
+#pragma unroll
+      for (int r = 0; r < P; ++r) {
+        if (r == c) continue;
+        const double fct = S[r][c];
+#pragma unroll
+        for (int j = 0; j < P; ++j) {
+          S[r][j] = fma(-fct, S[c][j], S[r][j]);
+          I[r][j] = fma(-fct, I[c][j], I[r][j]);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < P; ++i)
+#pragma unroll
+      for (int j = 0; j < P; ++j) sinv[i * P + j] = I[i][j];
+    if ((P * P) & 1) sinv[P * P] = 0.0;
+  }
+}
+
+__host__ __device__ inline size_t solve2d_smem_bytes(int n0, int n1, int zl, int P, int kseg, bool tw = false) {
+  const int W = (P + 2) & ~1;
+  // step tables (only when staged in shared memory) / the twisted passes' two side buffers
+  const size_t tabs = tw ? 2 * static_cast<size_t>(P) * (kSolve2dThreads / 2)
+                         : (MFB_RL_GTAB ? 0 : 2 * static_cast<size_t>(rl_rows(n0, P) + rl_rows(n1, P)) * W);
+  return 128 + (static_cast<size_t>(n1) * zl + static_cast<size_t>(kseg > 1 ? kseg - 1 : 0) * (P + 1) * zl + tabs) * 8 +
          static_cast<size_t>(n0 + n1 + 16);
 }
 
@@ -1209,11 +1365,16 @@ __device__ __forceinline__ void build_rl_tables(const double* lt, int n, double*
 // solve after the factorizations (the solve kernels bulk-copy them instead of
 // deriving them from the Cholesky table in every CTA).
 template <int P>
-__global__ void __launch_bounds__(256) k_rl_tables(const CholArgs a, double* rlt, std::int64_t stride) {
+__global__ void __launch_bounds__(256) k_rl_tables(const CholArgs a, double* rlt, std::int64_t stride, int tw) {
   constexpr int W = RL<P>::W;
   const int pid = a.prob_ids[blockIdx.x];
   const AxisProb pr = a.probs[pid];
   double* f = rlt + static_cast<std::int64_t>(pid) * stride;
+  if (tw) {
+    const double* twp = a.tw + static_cast<std::int64_t>(pid) * a.tw_stride;
+    build_tw_tables<P>(a.ltab + pr.col_off * (2 * P + 1), twp, twp + pr.n * (P + 1), pr.n, f, threadIdx.x, blockDim.x);
+    return;
+  }
   build_rl_tables<P>(a.ltab + pr.col_off * (2 * P + 1), pr.n, f, f + rl_rows(pr.n, P) * W, threadIdx.x, blockDim.x);
 }
 
@@ -1253,18 +1414,29 @@ __global__ void __launch_bounds__(kSolve2dThreads) k_solve2d(const FitArgs a) {
   std::uint64_t* bar = reinterpret_cast<std::uint64_t*>(s2d);
   double* X = s2d + 16;                                   // [n1][zl]
   double* C = X + static_cast<std::int64_t>(n1) * zl;     // [(K-1)(P+1)][zl] carries
+#if MFB_RL_GTAB
+  // the step tables stay in global memory (k_rl_tables), read through L1
+  const double* f0 = a.rlt + static_cast<std::int64_t>(blk.ax[0]) * a.rlt_stride;
+  const double* b0 = f0 + rl_rows(n0, P) * W;
+  const double* f1 = a.rlt + static_cast<std::int64_t>(blk.ax[1]) * a.rlt_stride;
+  const double* b1 = f1 + rl_rows(n1, P) * W;
+  unsigned char* sf0 = reinterpret_cast<unsigned char*>(C + static_cast<std::int64_t>(K - 1) * PADC * zl);
+#else
   double* f0 = C + static_cast<std::int64_t>(K - 1) * PADC * zl;
   double* b0 = f0 + rl_rows(n0, P) * W;
   double* f1 = b0 + rl_rows(n0, P) * W;
   double* b1 = f1 + rl_rows(n1, P) * W;
   unsigned char* sf0 = reinterpret_cast<unsigned char*>(b1 + rl_rows(n1, P) * W);  // n0: axis-0 index shared
+#endif
   unsigned char* sf1 = sf0 + n0;                                                   // n1: axis-1 index shared
   const double* zb = a.Y + blk.zoff + static_cast<std::int64_t>(PADC) * zl;
   if (tid == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
     unsigned bytes = static_cast<unsigned>(n1) * zl * 8 + static_cast<unsigned>(K - 1) * PADC * zl * 8;
+#if !MFB_RL_GTAB
     if (a.rlt) bytes += 2 * static_cast<unsigned>((rl_rows(n0, P) + rl_rows(n1, P)) * W) * 8;
+#endif
     mbar_arrive_expect_tx(bar, bytes);
     int cs = 0;
     for (int sg = 0; sg < K; ++sg) {  // segment sg owns columns [cs_sg, cs_sg+1) in parity sg & 1
@@ -1277,8 +1449,10 @@ __global__ void __launch_bounds__(kSolve2dThreads) k_solve2d(const FitArgs a) {
       cs = ce;
     }
   }
+#if !MFB_RL_GTAB
   stage_rl_tables<P>(a, p0, blk.ax[0], f0, b0, bar, tid, nthr);
   stage_rl_tables<P>(a, p1, blk.ax[1], f1, b1, bar, tid, nthr);
+#endif
   for (int c = tid; c < n1; c += nthr) sf1[c] = a.shared_flag[a.sflag_off[1] + p1.col_lo + c];
   __shared__ int s_ns[2];  // non-shared axis-0 indices: [s_ns[0], s_ns[1])
   if (tid == 0) {
@@ -1305,6 +1479,7 @@ __global__ void __launch_bounds__(kSolve2dThreads) k_solve2d(const FitArgs a) {
   }
   __syncthreads();
   RLFinal fin{};
+  double* Pb = a.P + blk.poff;
   // G1^-1 along the rows (thread per row; stride zl)
   for (int i = tid; i < n0; i += nthr) {
     rl_pass<P, false>(X + i, zl, n1, f1 + P * W, fin);
@@ -1314,7 +1489,6 @@ __global__ void __launch_bounds__(kSolve2dThreads) k_solve2d(const FitArgs a) {
   // G0^-1 along the columns (thread per column); the backward pass writes
   // P_b[i][c] (coalesced over the warp's columns) and the L-inf over
   // non-shared controls.
-  double* Pb = a.P + blk.poff;
   for (int c = tid; c < n1; c += nthr) {
     double* xc = X + static_cast<std::int64_t>(c) * zl;
     rl_pass<P, false>(xc, 1, n0, f0 + P * W, fin);
@@ -1326,6 +1500,262 @@ __global__ void __launch_bounds__(kSolve2dThreads) k_solve2d(const FitArgs a) {
     rl_pass<P, true>(xc + (n0 - 1), -1, n0, b0 + P * W, fin);
   }
   unsigned long long lmax = fin.lmax;
+  const int lane = tid & 31, warp = tid >> 5, nw = nthr >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long t2 = __shfl_xor_sync(kFullMask, lmax, o);
+    lmax = lmax > t2 ? lmax : t2;
+  }
+  if (lane == 0) s_red[warp] = lmax;
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long mx = 0ull;
+    for (int w2 = 0; w2 < nw; ++w2) mx = mx > s_red[w2] ? mx : s_red[w2];
+    if (mx) atomicMax(a.linf_int + bid, mx);
+  }
+}
+
+// ---- k_solve2d_tw: the fused 2-D solve with twisted passes (MFADD_TWIST=1)
+// Measured on C5 (round 2): 104 us as four inlined pass instantiations (a
+// quarter of the issue slots waited for instructions), 119 us in this compact
+// form (53 instructions per step against the plain kernel's 32, and the same
+// 0.27 instructions per cycle per scheduler with twice the warps: a third of
+// the warp time is spent at the per-pass barriers), against 70 us for
+// k_solve2d.  Parity-green (the whole GPU suite passes with it), kept as a
+// measurement knob, off by default.
+// Same tile, carries and outputs as k_solve2d; a thread pair per line (top /
+// bottom half).  All four passes of a thread (forward and backward, along the
+// rows then along the columns) run the SAME compiled loop, tw_pass, whose
+// per-pass differences are run-time values: the kernel body executes once per
+// block, so its instruction footprint, not its branch count, is what matters
+// (the four-instantiation form spent a quarter of its issue slots waiting for
+// instructions).  Addresses are 32-bit shared-memory byte offsets.
+__device__ __forceinline__ double lds_f64(std::uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts_f64(std::uint32_t addr, double v) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+__device__ __forceinline__ double2 lds_f64x2(std::uint32_t addr) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
+}
+
+template <int P>
+struct TwPass {
+  std::uint32_t x0;   // byte address of step 0's line element
+  int dsb;            // byte stride per step (signed)
+  int S;              // steps
+  int e;              // steps [e, S) are stored to the side column (forward pass; S: none)
+  const double* tab;  // the step table's row 0 (global memory, read through L1)
+  std::uint32_t side; // byte address of the side column
+  int sstb;           // its byte stride
+  int use_init;       // backward pass: the first P values are init[]
+  double init[P];
+  double* gdst;       // final pass: global destination of step 0 (null: none)
+  std::int64_t gstride;
+  int t_lo, t_hi;     // steps that count towards the L-inf (empty: none)
+};
+
+template <int P>
+__device__ __noinline__ unsigned long long tw_pass(const TwPass<P> q, unsigned long long lmax) {
+  constexpr int U = RL<P>::U, W = RL<P>::W;
+  const int S = q.S;
+  double acc[P], zin[U], cf[W];
+#pragma unroll
+  for (int k = 0; k < P; ++k) {
+    const double v = q.use_init ? q.init[k] : (k < S ? lds_f64(q.x0 + k * q.dsb) : 0.0);
+    acc[k] = v * __ldg(q.tab + (k - P) * W + P);
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) zin[u] = P + u < S ? lds_f64(q.x0 + (P + u) * q.dsb) : 0.0;
+#pragma unroll
+  for (int h = 0; h < W / 2; ++h) {
+    const double2 v = __ldg(reinterpret_cast<const double2*>(q.tab) + h);
+    cf[2 * h] = v.x;
+    cf[2 * h + 1] = v.y;
+  }
+  std::uint32_t xa = q.x0;           // line element of step t0
+  const double* ta = q.tab + W;  // table row of step t0 + 1
+  double* gp = q.gdst;
+#pragma unroll 1
+  for (int t0 = 0; t0 < S; t0 += U) {
+    double znx[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int te = t0 + U + P + u;
+      znx[u] = te < S ? lds_f64(xa + (U + P + u) * q.dsb) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      double cfn[W];
+#pragma unroll
+      for (int h = 0; h < W / 2; ++h) {  // the next step's row (tables are padded past the line)
+        const double2 v = __ldg(reinterpret_cast<const double2*>(ta + u * W) + h);
+        cfn[2 * h] = v.x;
+        cfn[2 * h + 1] = v.y;
+      }
+      const double y = acc[u % P];
+#pragma unroll
+      for (int k = 1; k < P; ++k) acc[(u + k) % P] = fma(-cf[k - 1], y, acc[(u + k) % P]);
+      acc[u % P] = fma(-cf[P - 1], y, zin[u] * cf[P]);
+      const int t = t0 + u;
+      if (t < S) {
+        sts_f64(t < q.e ? xa + u * q.dsb : q.side + (t - q.e) * q.sstb, y);
+        if (gp) {
+          gp[u * q.gstride] = y;
+          if (t >= q.t_lo && t < q.t_hi) {
+            const unsigned long long bits = dbits_s(fabs(y));
+            lmax = lmax > bits ? lmax : bits;
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < W; ++k) cf[k] = cfn[k];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) zin[u] = znx[u];
+    xa += U * q.dsb;
+    ta += U * W;
+    if (gp) gp += U * q.gstride;
+  }
+  return lmax;
+}
+
+template <int P>
+__global__ void __launch_bounds__(kSolve2dThreads) k_solve2d_tw(const FitArgs a) {
+  pdl_enter();
+  extern __shared__ __align__(128) double s2d[];
+  __shared__ unsigned long long s_red[32];
+  __shared__ int s_ns[2];  // non-shared axis-0 indices: [s_ns[0], s_ns[1])
+  constexpr int PADC = P + 1, W = RL<P>::W, HALF = kSolve2dThreads / 2;
+  const int bid = blockIdx.x;
+  const BlockDev& blk = a.blocks[bid];
+  const AxisProb p0 = a.probs[blk.ax[0]], p1 = a.probs[blk.ax[1]];
+  const int n0 = p0.n, n1 = p1.n, zl = blk.zl;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int* seg = a.segtab + blk.ax[1] * kSegStride;
+  const int K = seg[0];
+  const int* g0g = a.g0 + p1.row_off;
+  std::uint64_t* bar = reinterpret_cast<std::uint64_t*>(s2d);
+  double* X = s2d + 16;                                   // [n1][zl]
+  double* C = X + static_cast<std::int64_t>(n1) * zl;     // [(K-1)(P+1)][zl] carries
+  // the problems' table sets stay in global memory (k_rl_tables), read through L1
+  const double* tab0 = a.rlt + static_cast<std::int64_t>(blk.ax[0]) * a.rlt_stride;
+  const double* tab1 = a.rlt + static_cast<std::int64_t>(blk.ax[1]) * a.rlt_stride;
+  double* mtop = C + static_cast<std::int64_t>(K - 1) * PADC * zl;  // side buffers [P][HALF]
+  double* mbot = mtop + P * HALF;
+  unsigned char* sf1 = reinterpret_cast<unsigned char*>(mbot + P * HALF);  // n1: axis-1 index shared
+  const double* zb = a.Y + blk.zoff + static_cast<std::int64_t>(PADC) * zl;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(bar, static_cast<unsigned>(n1) * zl * 8 + static_cast<unsigned>(K - 1) * PADC * zl * 8);
+    int cs = 0;
+    for (int sg = 0; sg < K; ++sg) {  // segment sg owns columns [cs_sg, cs_sg+1) in parity sg & 1
+      const int ce = sg + 1 < K ? __ldg(g0g + seg[2 + sg]) : n1;
+      const double* src = zb + (sg & 1) * a.zhalf + static_cast<std::int64_t>(cs) * zl;
+      if (ce > cs) bulk_load_1d(X + static_cast<std::int64_t>(cs) * zl, src, static_cast<unsigned>(ce - cs) * zl * 8, bar);
+      if (sg + 1 < K)  // its partial sums of the next segment's first P+1 columns
+        bulk_load_1d(C + static_cast<std::int64_t>(sg) * PADC * zl, zb + (sg & 1) * a.zhalf + static_cast<std::int64_t>(ce) * zl,
+                     static_cast<unsigned>(PADC) * zl * 8, bar);
+      cs = ce;
+    }
+    s_ns[0] = n0;
+    s_ns[1] = 0;
+  }
+  for (int c = tid; c < n1; c += nthr) sf1[c] = a.shared_flag[a.sflag_off[1] + p1.col_lo + c];
+  __syncthreads();
+  for (int i = tid; i < n0; i += nthr)
+    if (!a.shared_flag[a.sflag_off[0] + p0.col_lo + i]) {
+      atomicMin(&s_ns[0], i);
+      atomicMax(&s_ns[1], i + 1);
+    }
+  __syncthreads();  // barrier init visible before any wait
+  mbar_wait(bar, 0);
+  // carries: X[cs_s + k] += C[s-1][k] for boundaries s = 1..K-1
+  for (int e = tid; e < (K - 1) * PADC * n0; e += nthr) {
+    const int r = e / n0, i = e - r * n0;  // r = (s-1)*(P+1) + k
+    const int sb = r / PADC + 1, k = r - (sb - 1) * PADC;
+    const int c = __ldg(g0g + seg[1 + sb]) + k;
+    X[static_cast<std::int64_t>(c) * zl + i] += C[static_cast<std::int64_t>(r) * zl + i];
+  }
+  __syncthreads();
+  const int role = tid >= HALF ? 1 : 0, pr = tid - role * HALF;
+  const std::uint32_t xs = smem_u32(X), mts = smem_u32(mtop + pr), mbs = smem_u32(mbot + pr);
+  double* Pb = a.P + blk.poff;
+  unsigned long long lmax = 0ull;
+  // phase 0: G1^-1 along the rows (line i: X[.][i], stride zl);
+  // phase 1: G0^-1 along the columns (line c: X[c][.], stride 1), whose
+  // backward passes write P_b[i][c] and the L-inf over non-shared controls
+#pragma unroll 1
+  for (int ph = 0; ph < 2; ++ph) {
+    const int n = ph ? n0 : n1, nl = ph ? n1 : n0;   // line length, line count
+    const int stb = (ph ? 1 : zl) * 8;               // byte stride along a line
+    const double* tb = ph ? tab0 : tab1;
+    const int ta = tw_top(n, P), nb = tw_bot(n, P);
+    const int rt = rl_rows(ta + P, P) * W, rb = rl_rows(nb + P, P) * W;
+    const double* fwd = tb + (role ? 2 * rt : 0) + P * W;
+    const double* bwd = tb + (role ? 2 * rt + rb : rt) + P * W;
+    const double* sinv = tb + 2 * rt + 2 * rb;
+    const int e = role ? nb : ta, S = e + P;
+#pragma unroll 1
+    for (int l0 = 0; l0 < nl; l0 += HALF) {
+      const int l = l0 + pr;
+      const bool act = l < nl;
+      const std::uint32_t line = xs + static_cast<std::uint32_t>(act ? l : 0) * (ph ? zl * 8 : 8);
+      TwPass<P> q;
+      q.S = S;
+      q.tab = fwd;
+      q.side = role ? mbs : mts;
+      q.sstb = HALF * 8;
+      q.gdst = nullptr;
+      q.gstride = 0;
+      q.t_lo = q.t_hi = 0;
+      // forward: top walks rows 0, 1, ..; bottom rows n-1, n-2, ..
+      q.x0 = role ? line + static_cast<std::uint32_t>(n - 1) * stb : line;
+      q.dsb = role ? -stb : stb;
+      q.e = e;
+      q.use_init = 0;
+#pragma unroll
+      for (int k = 0; k < P; ++k) q.init[k] = 0.0;
+      if (act) lmax = tw_pass<P>(q, lmax);
+      __syncthreads();
+      if (act) {
+        double r[P];
+#pragma unroll
+        for (int j = 0; j < P; ++j) r[j] = mtop[j * HALF + pr] + mbot[(P - 1 - j) * HALF + pr];  // row ta+j
+        // x_M = S^-1 r; backward: top walks rows ta+P-1 down to 0, bottom
+        // rows ta up to n-1; the first P steps are the middle rows in the
+        // pass's own order
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+          double sacc = 0.0;
+#pragma unroll
+          for (int j = 0; j < P; ++j) sacc = fma(__ldg(sinv + i * P + j), r[j], sacc);
+          q.init[role ? i : P - 1 - i] = sacc;
+        }
+        q.use_init = 1;
+        q.tab = bwd;
+        q.e = S;
+        q.x0 = line + static_cast<std::uint32_t>(role ? ta : ta + P - 1) * stb;
+        q.dsb = role ? stb : -stb;
+        if (ph) {
+          q.gdst = Pb + static_cast<std::int64_t>(role ? ta : ta + P - 1) * n1 + l;
+          q.gstride = role ? n1 : -n1;
+          if (!sf1[l]) {  // step t <-> row ta + t (bottom) / ta + P - 1 - t (top)
+            q.t_lo = role ? s_ns[0] - ta : ta + P - s_ns[1];
+            q.t_hi = role ? s_ns[1] - ta : ta + P - s_ns[0];
+          }
+        }
+        lmax = tw_pass<P>(q, lmax);
+      }
+      __syncthreads();
+    }
+  }
   const int lane = tid & 31, warp = tid >> 5, nw = nthr >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -1814,7 +2244,12 @@ struct LastLaunch {
     // the contraction needs no factor: the Gram/Cholesky side stream joins here
     if (a.join_event) cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(a.join_event), 0);
     if (a.fuse2d) {
-      const size_t sm2 = solve2d_smem_bytes(a.max_n0, a.max_n1, a.max_zl, P, kseg);
+      const size_t sm2 = solve2d_smem_bytes(a.max_n0, a.max_n1, a.max_zl, P, kseg, a.tw2d != 0);
+      if (a.tw2d) {
+        cudaFuncSetAttribute(k_solve2d_tw<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm2));
+        launch_pdl(k_solve2d_tw<P>, dim3(a.nblocks), dim3(kSolve2dThreads), sm2, s, a);
+        return 2;
+      }
       cudaFuncSetAttribute(k_solve2d<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm2));
       launch_pdl(k_solve2d<P>, dim3(a.nblocks), dim3(kSolve2dThreads), sm2, s, a);
       return 2;
@@ -1843,38 +2278,41 @@ int debug_fail_line_tma() {
 namespace {
 template <int P>
 struct RlTablesLaunch {
-  static int run(const CholArgs& a, double* rlt, std::int64_t stride, cudaStream_t s) {
+  static int run(const CholArgs& a, double* rlt, std::int64_t stride, cudaStream_t s, bool tw) {
     if (a.nfactor == 0) return 0;
-    k_rl_tables<P><<<a.nfactor, 256, 0, s>>>(a, rlt, stride);
+    k_rl_tables<P><<<a.nfactor, 256, 0, s>>>(a, rlt, stride, tw ? 1 : 0);
     return 1;
   }
 };
 template <int P>
 struct RlDoubles {
-  static std::int64_t run(int n) { return 2 * static_cast<std::int64_t>(rl_rows(n, P)) * RL<P>::W; }
+  static std::int64_t run(int n, bool tw) {
+    const std::int64_t plain = 2 * static_cast<std::int64_t>(rl_rows(n, P)) * RL<P>::W;
+    return tw && tw_ok(n, P) ? std::max<std::int64_t>(plain, tw_table_doubles(n, P)) : plain;
+  }
 };
 }  // namespace
 
-int launch_rl_tables(int degree, const CholArgs& a, double* rlt, std::int64_t stride, cudaStream_t s) {
-  return dispatch_p<RlTablesLaunch>(degree, a, rlt, stride, s);
+int launch_rl_tables(int degree, const CholArgs& a, double* rlt, std::int64_t stride, cudaStream_t s, bool tw) {
+  return dispatch_p<RlTablesLaunch>(degree, a, rlt, stride, s, tw);
 }
-std::int64_t rl_table_doubles(int degree, int n) {
+std::int64_t rl_table_doubles(int degree, int n, bool tw) {
   switch (degree) {
-    case 1: return RlDoubles<1>::run(n);
-    case 2: return RlDoubles<2>::run(n);
-    case 3: return RlDoubles<3>::run(n);
-    case 4: return RlDoubles<4>::run(n);
-    case 5: return RlDoubles<5>::run(n);
-    case 6: return RlDoubles<6>::run(n);
-    case 7: return RlDoubles<7>::run(n);
-    case 8: return RlDoubles<8>::run(n);
-    case 9: return RlDoubles<9>::run(n);
+    case 1: return RlDoubles<1>::run(n, tw);
+    case 2: return RlDoubles<2>::run(n, tw);
+    case 3: return RlDoubles<3>::run(n, tw);
+    case 4: return RlDoubles<4>::run(n, tw);
+    case 5: return RlDoubles<5>::run(n, tw);
+    case 6: return RlDoubles<6>::run(n, tw);
+    case 7: return RlDoubles<7>::run(n, tw);
+    case 8: return RlDoubles<8>::run(n, tw);
+    case 9: return RlDoubles<9>::run(n, tw);
     default: return 0;
   }
 }
 
-size_t solve2d_smem(int degree, int n0, int n1, int zl, int kseg) {
-  const size_t b = solve2d_smem_bytes(n0, n1, zl, degree, kseg);
+size_t solve2d_smem(int degree, int n0, int n1, int zl, int kseg, bool tw) {
+  const size_t b = solve2d_smem_bytes(n0, n1, zl, degree, kseg, tw);
   return b <= 227 * 1024 - 512 ? b : 0;
 }
 

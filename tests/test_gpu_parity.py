@@ -402,6 +402,20 @@ def test_tma_and_generic_paths_agree(ctx, monkeypatch):
         assert np.max(np.abs(bt.p - bg.p)) <= 1e-12 * max(1.0, np.max(np.abs(bg.p)))
 
 
+@pytest.mark.parametrize("name", ["C2", "C5s"])
+def test_twisted_solve2d_knob(ctx, monkeypatch, name):
+    """MFADD_TWIST=1: the fused 2-D solve with two-sided (twisted) banded
+    passes, another elimination order of lsq.cpp:59-60: same contract."""
+    cfg = SMALL[name]
+    values = W.make_field_numpy(cfg)
+    g_plain, o, _ = run_both(cfg, values)
+    monkeypatch.setenv("MFADD_TWIST", "1")
+    g_tw, _, _ = run_both(cfg, values)
+    assert_solve_parity(g_tw, o)
+    for bt, bg in zip(g_tw.blocks, g_plain.blocks):
+        assert np.max(np.abs(bt.p - bg.p)) <= 1e-11 * max(1.0, np.max(np.abs(bg.p)))
+
+
 def test_graph_replay_matches_direct(ctx, monkeypatch):
     """The first solve on a field pointer runs direct launches, the second
     captures the whole solve into a CUDA graph, later ones replay it: all must
