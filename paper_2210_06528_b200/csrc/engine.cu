@@ -230,6 +230,9 @@ struct Workload {
   DBuf<double> vals, ltab, t1, t2, P, Y, rlt, twf;
   std::int64_t rlt_stride = 0, twf_stride = 0;
   bool tw2d = false;  // k_solve2d runs the twisted (two-sided) passes
+  // D = 3: every pass a pure contraction and one CTA per block solves all three axes (k_solve3d)
+  bool fuse3d = false;
+  int s3_n[3] = {0, 0, 0}, s3_zs = 0, s3_threads = 0, s3_slab = 0, s3_nslab = 0;
   DBuf<unsigned long long> linf_int;
   DBuf<unsigned char> sflag;
   std::int64_t sflag_off[3] = {0, 0, 0};
@@ -453,6 +456,39 @@ struct Workload {
       for (int id : factor_ids) ok = ok && mfb::tw_ok(probs[static_cast<std::size_t>(id)].n, p);
       tw2d = ok && mfb::solve2d_smem(p, mn0, mn1, mzl, last_kseg, true) > 0;
     }
+    fuse3d = false;
+    if (D == 3 && defer_mode == 2 && tma_last && tma_mid && tma_axis0 && !blocks.empty() &&
+        !std::getenv("MFADD_NO_FUSE3D")) {
+      s3_n[0] = s3_n[1] = s3_n[2] = 0;
+      bool n1_odd = false;
+      for (const auto& b : blocks)
+        for (int k = 0; k < 3; ++k) {
+          const int nk = probs[static_cast<std::size_t>(b.ax[k])].n;
+          s3_n[k] = std::max(s3_n[k], nk);
+          if (k == 1 && (nk & 1)) n1_odd = true;
+        }
+      // slab = axis-0 indices per CTA: the whole block when it fits one CTA,
+      // else ~224 lines (column runs start 16-B aligned: an even line count)
+      auto pitch = [&](int slab) { return (slab * s3_n[1] + 1) / 4 * 4 + 2; };
+      auto fits = [&](int slab, std::size_t cap) {
+        const std::size_t b = mfb::solve3d_smem(p, s3_n[0], s3_n[1], s3_n[2], pitch(slab), last_kseg);
+        return b > 0 && b <= cap;
+      };
+      int slab = s3_n[0];
+      if (!fits(slab, 227 * 1024) || std::getenv("MFADD_S3_SLAB")) {
+        slab = std::max(1, env_int("MFADD_S3_SLAB", std::max(1, 224 / s3_n[1])));
+        if (n1_odd) slab = std::max(2, slab & ~1);
+        while (slab > (n1_odd ? 2 : 1) && !fits(slab, static_cast<std::size_t>(env_int("MFADD_S3_KB", 75)) * 1024))
+          slab -= n1_odd ? 2 : 1;
+      }
+      slab = std::min(slab, s3_n[0]);
+      fuse3d = fits(slab, 227 * 1024) && (slab == s3_n[0] || !n1_odd || slab % 2 == 0);
+      s3_slab = slab;
+      s3_nslab = (s3_n[0] + slab - 1) / slab;
+      s3_zs = pitch(slab);
+      const int lines = std::max({slab * s3_n[1], slab * s3_n[2], s3_nslab == 1 ? s3_n[1] * s3_n[2] : 1});
+      s3_threads = std::min(640, std::max(128, (lines + 31) / 32 * 32));
+    }
     rlt_stride = (mfb::rl_table_doubles(p, max_n_factor, tw2d) + 1) / 2 * 2;  // even: 16-B aligned per problem
     rlt.alloc(static_cast<std::size_t>(probs.size() * rlt_stride));
     if (tw2d) {
@@ -525,14 +561,14 @@ struct Workload {
         CK(cudaEventRecord(ev_rows2, side));
       }
       l += mfb::launch_gram_chol(p, ca, side);
-      if (D == 2 && tma_last) l += mfb::launch_rl_tables(p, ca, rlt.p, rlt_stride, side, tw2d);
+      if ((D == 2 && tma_last) || fuse3d) l += mfb::launch_rl_tables(p, ca, rlt.p, rlt_stride, side, tw2d);
       tl->end();
       tl->st = main_st;
       CK(cudaEventRecord(ev_chol, side));
     } else {
       tl->begin("gram_chol");
       l += mfb::launch_gram_chol(p, ca, ctx->stream);
-      if (D == 2 && tma_last) l += mfb::launch_rl_tables(p, ca, rlt.p, rlt_stride, ctx->stream, tw2d);
+      if ((D == 2 && tma_last) || fuse3d) l += mfb::launch_rl_tables(p, ca, rlt.p, rlt_stride, ctx->stream, tw2d);
       tl->end();
     }
     CK(cudaGetLastError());
@@ -577,6 +613,16 @@ struct Workload {
     fa.n_P = total_p;
     static const char* kNames[2] = {"fit_axis0", "fit_axis1"};
     int l = 0;
+    if (fuse3d) {
+      fa.fuse3d = 1;
+      fa.max_n0 = s3_n[0];
+      fa.max_n1 = s3_n[1];
+      fa.max_n2 = s3_n[2];
+      fa.s3_slab = s3_slab;
+      fa.s3_nslab = s3_nslab;
+      fa.s3_zs = s3_zs;
+      fa.solve3d_threads = s3_threads;
+    }
     for (int d = 0; d + 1 < D; ++d) {
       tl->begin(kNames[d]);
       if (d == 0 && tma_axis0) {
@@ -604,7 +650,13 @@ struct Workload {
       tl->end();
       // join the factorizations (D = 2 with the TMA last axis: inside the
       // last-axis launch, after its contraction, which needs no factor)
-      if (d == 0 && defer_mode == 2 && !(D == 2 && tma_last)) CK(cudaStreamWaitEvent(ctx->stream, ev_chol, 0));
+      // (D = 3 fused solve: the contractions need only the basis rows; the
+      // factors join inside the last-axis launch as well)
+      if (d == 0 && defer_mode == 2 && fuse3d) {
+        if (rows_split) CK(cudaStreamWaitEvent(ctx->stream, ev_rows2, 0));
+      } else if (d == 0 && defer_mode == 2 && !(D == 2 && tma_last)) {
+        CK(cudaStreamWaitEvent(ctx->stream, ev_chol, 0));
+      }
     }
     if (D == 1 && defer_mode == 2) CK(cudaStreamWaitEvent(ctx->stream, ev_chol, 0));
     if (D == 2 && defer_mode == 2 && tma_last && !std::getenv("MFADD_NO_FUSE2D")) {
@@ -617,8 +669,8 @@ struct Workload {
       fa.tw2d = fa.fuse2d && tw2d ? 1 : 0;
     }
     if (rows_split && D == 2) CK(cudaStreamWaitEvent(ctx->stream, ev_rows2, 0));  // last-axis + decode rows
-    if (D == 2 && defer_mode == 2 && tma_last) fa.join_event = ev_chol;
-    if (D == 2 && tma_last) {
+    if ((D == 2 && defer_mode == 2 && tma_last) || fuse3d) fa.join_event = ev_chol;
+    if ((D == 2 && tma_last) || fuse3d) {
       fa.rlt = rlt.p;
       fa.rlt_stride = rlt_stride;
     }
@@ -636,7 +688,7 @@ struct Workload {
       l += mfb::launch_fit_last(p, fa, ctx->stream);
     }
     tl->end();
-    if (fa.defer_back && !fa.fuse2d) {
+    if (fa.defer_back && !fa.fuse2d && !(fa.fuse3d && fa.s3_nslab == 1)) {
       int mxn0 = 0;
       std::int64_t mxr = 1;
       fa.min_n0 = 1 << 30;

@@ -121,12 +121,17 @@ struct FitArgs {
   std::int64_t rlt_stride;           // doubles per axis problem in rlt (forward then backward table)
   int max_n0, max_n1, max_zl;        // largest held extents / Z pitch (k_solve2d shared-memory size)
   int tw2d;                          // k_solve2d: twisted passes (rlt holds the twisted table sets)
+  int fuse3d;                        // D = 3: every pass a pure contraction, k_solve3d solves axes 2 and 1 (and 0) in smem
+  int max_n2, solve3d_threads;       // k_solve3d: largest axis-2 held extent, CTA size
+  int s3_slab, s3_nslab, s3_zs;      // k_solve3d: axis-0 indices per slab, slabs per block, tile column pitch
   void* join_event;                  // cudaEvent_t the last-axis solve waits for (factorizations on a side stream)
 };
 int launch_fit_strided(int degree, const FitArgs& a, int axis, cudaStream_t s);  // axis < D-1
 int launch_fit_last(int degree, const FitArgs& a, cudaStream_t s);
 // Shared-memory bytes of k_solve2d for held extents n0 x n1 (0 if it does not fit one CTA).
 size_t solve2d_smem(int degree, int n0, int n1, int zl, int kseg, bool tw = false);
+// Shared-memory bytes of k_solve3d for held extents n0 x n1 x n2 and a tile column pitch zs (0 if over the CTA limit).
+size_t solve3d_smem(int degree, int n0, int n1, int n2, int zs, int kseg);
 
 // D = 1: CTA per block, column-parallel R^T q + serial banded solve (smem: max_n x (2P+2) doubles).
 int launch_fit_1d(int degree, const FitArgs& a, int max_n, cudaStream_t s);

@@ -1771,6 +1771,187 @@ __global__ void __launch_bounds__(kSolve2dThreads) k_solve2d_tw(const FitArgs a)
   }
 }
 
+// ------------------------------------------- fused 3-D solve (CTA per slab)
+// D = 3 with all three passes as pure contractions (FitArgs::fuse3d): after
+// k_last_contract_tma the block's right-hand side Z = Q_b x0 R0 x1 R1 x2 R2 is
+// n0 n1 n2 values in the layout Z[c][l], l = i0 n1 + i1 (column pitch zl).  A
+// CTA takes the slab i0 in [i0a, i0b) of one block (FitArgs::s3_slab indices;
+// C4: 36^3 controls per block, slabs of 6 = 61 KB), pulls its n2 column runs
+// in with 1-D bulk copies into X[c][ls] (pitch s3_zs), and applies G2^-1 along
+// c (a thread per line ls) and G1^-1 along i1 (a thread per (i0, c)) with the
+// right-looking passes of k_solve2d (lsq.cpp:59-60 on each axis; the axis
+// operators commute).  With several slabs per block the axis-1 backward pass
+// writes P_b and the axis-0 solve follows on the held lattices
+// (k_axis0_backsub / k_axis0_solve_part, which also take the L-inf).  When the
+// whole block is one slab, G0^-1 along i0 (a thread per (i1, c)) runs here
+// too, its backward pass writing P_b and the per-block L-inf over non-shared
+// controls (solver.cpp:97-101).  Replaces the middle pass's in-place solve on
+// T2 and k_last_solve (strided walks over HBM-resident intermediates).
+constexpr int kSolve3dMaxThreads = 640;
+
+// Shared memory: the slab tile, the segment carries, two step-table slots
+// (each a forward + backward table of the largest extent: axis 2's and axis
+// 1's tables arrive with the tile, axis 0's replaces axis 2's during the
+// axis-1 phase) and the shared-index flags.
+__host__ __device__ inline size_t solve3d_smem_bytes(int n0, int n1, int n2, int zs, int P, int kseg) {
+  const int W = (P + 2) & ~1;
+  const int nm = n0 > n1 ? (n0 > n2 ? n0 : n2) : (n1 > n2 ? n1 : n2);
+  return 128 + (static_cast<size_t>(n2) * zs + static_cast<size_t>(kseg > 1 ? kseg - 1 : 0) * (P + 1) * zs +
+                4 * static_cast<size_t>(rl_rows(nm, P)) * W) *
+                   8 +
+         static_cast<size_t>(n0 + n1 + n2 + 16);
+}
+
+template <int P>
+__global__ void __launch_bounds__(kSolve3dMaxThreads) k_solve3d(const FitArgs a) {
+  pdl_enter();
+  extern __shared__ __align__(128) double s2d[];
+  __shared__ unsigned long long s_red[32];
+  __shared__ int s_ns[2];  // non-shared axis-0 indices: [s_ns[0], s_ns[1])
+  constexpr int PADC = P + 1, W = RL<P>::W;
+  const int bid = blockIdx.x;
+  const BlockDev& blk = a.blocks[bid];
+  const AxisProb p0 = a.probs[blk.ax[0]], p1 = a.probs[blk.ax[1]], p2 = a.probs[blk.ax[2]];
+  const int n0 = p0.n, n1 = p1.n, n2 = p2.n, zl = blk.zl, zs = a.s3_zs;
+  const int i0a = static_cast<int>(blockIdx.y) * a.s3_slab;
+  if (i0a >= n0) return;
+  const int i0b = i0a + a.s3_slab < n0 ? i0a + a.s3_slab : n0;
+  const int S0 = i0b - i0a, L = S0 * n1, l_off = i0a * n1;
+  const bool whole = a.s3_nslab == 1;  // the block is one slab: axis 0 is solved here too
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int* seg = a.segtab + blk.ax[2] * kSegStride;
+  const int K = seg[0];
+  const int* g0g = a.g0 + p2.row_off;
+  std::uint64_t* bar = reinterpret_cast<std::uint64_t*>(s2d);
+  double* X = s2d + 16;                                   // [n2][zs]
+  double* C = X + static_cast<std::int64_t>(n2) * zs;     // [(K-1)(P+1)][zs] carries
+  const int slot = 2 * rl_rows(a.max_n0 > a.max_n1 ? (a.max_n0 > a.max_n2 ? a.max_n0 : a.max_n2)
+                                                     : (a.max_n1 > a.max_n2 ? a.max_n1 : a.max_n2), P) * W;
+  double* f2 = C + static_cast<std::int64_t>(K - 1) * PADC * zs;  // slot 0: axis 2, later axis 0
+  double* b2 = f2 + rl_rows(n2, P) * W;
+  double* f0 = f2;
+  double* b0 = f0 + rl_rows(n0, P) * W;
+  double* f1 = f2 + slot;                                         // slot 1: axis 1
+  double* b1 = f1 + rl_rows(n1, P) * W;
+  unsigned char* sf0 = reinterpret_cast<unsigned char*>(f1 + slot);  // n0: axis-0 index shared
+  unsigned char* sf1 = sf0 + n0;
+  unsigned char* sf2 = sf1 + n1;
+  const double* zb = a.Y + blk.zoff + static_cast<std::int64_t>(PADC) * zl + l_off;
+  // bytes of one column run, rounded up to a 16-B multiple (an odd line count
+  // copies one more value: inside Z's column pitch and the tile's)
+  const unsigned run = static_cast<unsigned>((L + 1) & ~1) * 8;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+    fence_mbar_init();
+    unsigned bytes = static_cast<unsigned>(n2 + (K - 1) * PADC) * run;
+    bytes += 2 * static_cast<unsigned>((rl_rows(n1, P) + rl_rows(n2, P)) * W) * 8;
+    mbar_arrive_expect_tx(bar, bytes);
+    s_ns[0] = n0;
+    s_ns[1] = 0;
+  }
+  __syncthreads();  // barrier init visible before the copies are issued by other threads
+  {
+    // column c's run comes from the parity buffer of the segment that owns it;
+    // carry column (s, k) = segment s-1's partial sums of column cs_s + k
+    for (int c = tid; c < n2 + (K - 1) * PADC; c += nthr) {
+      if (c < n2) {
+        int own = 0;
+        for (int s2 = 1; s2 < K; ++s2)
+          if (c >= __ldg(g0g + seg[1 + s2])) own = s2;
+        bulk_load_1d(X + static_cast<std::int64_t>(c) * zs, zb + (own & 1) * a.zhalf + static_cast<std::int64_t>(c) * zl, run, bar);
+      } else {
+        const int r = c - n2, sb = r / PADC + 1, k = r - (sb - 1) * PADC;
+        const int col = __ldg(g0g + seg[1 + sb]) + k;
+        bulk_load_1d(C + static_cast<std::int64_t>(r) * zs, zb + ((sb - 1) & 1) * a.zhalf + static_cast<std::int64_t>(col) * zl, run, bar);
+      }
+    }
+  }
+  stage_rl_tables<P>(a, p1, blk.ax[1], f1, b1, bar, tid, nthr);
+  stage_rl_tables<P>(a, p2, blk.ax[2], f2, b2, bar, tid, nthr);
+  for (int c = tid; c < n1; c += nthr) sf1[c] = a.shared_flag[a.sflag_off[1] + p1.col_lo + c];
+  for (int c = tid; c < n2; c += nthr) sf2[c] = a.shared_flag[a.sflag_off[2] + p2.col_lo + c];
+  for (int i = tid; i < n0; i += nthr) {
+    const unsigned char f = a.shared_flag[a.sflag_off[0] + p0.col_lo + i];
+    sf0[i] = f;
+    if (!f) {
+      atomicMin(&s_ns[0], i);
+      atomicMax(&s_ns[1], i + 1);
+    }
+  }
+  __syncthreads();
+  mbar_wait(bar, 0);
+  // carries: X[cs_s + k] += C[s-1][k] for boundaries s = 1..K-1
+  for (int e = tid; e < (K - 1) * PADC * L; e += nthr) {
+    const int r = e / L, i = e - r * L;  // r = (s-1)*(P+1) + k
+    const int sb = r / PADC + 1, k = r - (sb - 1) * PADC;
+    const int c = __ldg(g0g + seg[1 + sb]) + k;
+    X[static_cast<std::int64_t>(c) * zs + i] += C[static_cast<std::int64_t>(r) * zs + i];
+  }
+  __syncthreads();
+  RLFinal fin{};
+  // G2^-1 along c (thread per line ls; stride zs)
+  for (int l = tid; l < L; l += nthr) {
+    rl_pass<P, false>(X + l, zs, n2, f2 + P * W, fin);
+    rl_pass<P, false>(X + l + (n2 - 1) * zs, -zs, n2, b2 + P * W, fin);
+  }
+  __syncthreads();
+  if (whole) {  // axis 0's tables over axis 2's, behind the axis-1 phase
+    if (tid == 0) {
+      fence_proxy_async();
+      mbar_arrive_expect_tx(bar + 1, 2 * static_cast<unsigned>(rl_rows(n0, P) * W) * 8);
+    }
+    stage_rl_tables<P>(a, p0, blk.ax[0], f0, b0, bar + 1, tid, nthr);
+  }
+  // G1^-1 along i1 (thread per (i0, c), c fastest; stride 1).  Several slabs:
+  // the backward pass writes P_b[i0][i1][c] (coalesced over the warp's c).
+  double* Pb = a.P + blk.poff;
+  for (int q = tid; q < S0 * n2; q += nthr) {
+    const int i0r = q / n2, c = q - i0r * n2;
+    double* x = X + static_cast<std::int64_t>(c) * zs + i0r * n1;
+    rl_pass<P, false>(x, 1, n1, f1 + P * W, fin);
+    if (whole) {
+      rl_pass<P, false>(x + (n1 - 1), -1, n1, b1 + P * W, fin);
+    } else {
+      fin.dst = Pb + (static_cast<std::int64_t>(i0a + i0r) * n1 + (n1 - 1)) * n2 + c;
+      fin.dstride = -n2;
+      fin.t_lo = fin.t_hi = 0;
+      fin.line_shared = true;  // (the L-inf is taken by the axis-0 solve)
+      rl_pass<P, true>(x + (n1 - 1), -1, n1, b1 + P * W, fin);
+    }
+  }
+  if (!whole) return;
+  __syncthreads();
+  mbar_wait(bar + 1, 0);
+  // G0^-1 along i0 (thread per (i1, c), c fastest; stride n1); the backward
+  // pass writes P_b[i0][i1][c] and the L-inf over non-shared controls
+  for (int q = tid; q < n1 * n2; q += nthr) {
+    const int i1 = q / n2, c = q - i1 * n2;
+    double* x = X + static_cast<std::int64_t>(c) * zs + i1;
+    rl_pass<P, false>(x, n1, n0, f0 + P * W, fin);
+    fin.dst = Pb + (static_cast<std::int64_t>(n0 - 1) * n1 + i1) * n2 + c;
+    fin.dstride = -static_cast<std::int64_t>(n1) * n2;
+    fin.t_lo = n0 - s_ns[1];  // step t is axis-0 index n0 - 1 - t
+    fin.t_hi = n0 - s_ns[0];
+    fin.line_shared = (sf1[i1] | sf2[c]) != 0;
+    rl_pass<P, true>(x + (n0 - 1) * n1, -n1, n0, b0 + P * W, fin);
+  }
+  unsigned long long lmax = fin.lmax;
+  const int lane = tid & 31, warp = tid >> 5, nw = (nthr + 31) >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long t2 = __shfl_xor_sync(kFullMask, lmax, o);
+    lmax = lmax > t2 ? lmax : t2;
+  }
+  if (lane == 0) s_red[warp] = lmax;
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long mx = 0ull;
+    for (int w2 = 0; w2 < nw; ++w2) mx = mx > s_red[w2] ? mx : s_red[w2];
+    if (mx) atomicMax(a.linf_int + bid, mx);
+  }
+}
+
 template <int P>
 struct BacksubLaunch {
   static int run(const FitArgs& a, int max_n0, std::int64_t max_rest, cudaStream_t s) {
@@ -2154,7 +2335,7 @@ struct Axis0Launch {
     const StageLayout SL = stage_layout(kFitR, g.B1 * g.B2, P);
     const size_t smem = static_cast<size_t>(S) * SL.stage_bytes + 128 + static_cast<size_t>(g.lt_cap) * 8;
     dim3 grid(ntiles, a.nblocks, zdim);
-    if (!MID && a.defer_back == 2) {  // contraction only: no factor table in smem
+    if ((!MID && a.defer_back == 2) || (MID && a.fuse3d)) {  // contraction only: no factor table in smem
       const size_t smem_c = static_cast<size_t>(S) * SL.stage_bytes + 128;
       cudaFuncSetAttribute(k_fit_axis0_tma<P, S, NC, MID, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(smem_c));
@@ -2243,6 +2424,12 @@ struct LastLaunch {
     launch_pdl(k_last_contract_tma<P>, grid, dim3(LT), smem, s, a, map, LT);
     // the contraction needs no factor: the Gram/Cholesky side stream joins here
     if (a.join_event) cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(a.join_event), 0);
+    if (a.fuse3d) {
+      const size_t sm3 = solve3d_smem_bytes(a.max_n0, a.max_n1, a.max_n2, a.s3_zs, P, kseg);
+      cudaFuncSetAttribute(k_solve3d<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm3));
+      launch_pdl(k_solve3d<P>, dim3(a.nblocks, a.s3_nslab), dim3(a.solve3d_threads), sm3, s, a);
+      return 2;
+    }
     if (a.fuse2d) {
       const size_t sm2 = solve2d_smem_bytes(a.max_n0, a.max_n1, a.max_zl, P, kseg, a.tw2d != 0);
       if (a.tw2d) {
@@ -2309,6 +2496,11 @@ std::int64_t rl_table_doubles(int degree, int n, bool tw) {
     case 9: return RlDoubles<9>::run(n, tw);
     default: return 0;
   }
+}
+
+size_t solve3d_smem(int degree, int n0, int n1, int n2, int zs, int kseg) {
+  const size_t b = solve3d_smem_bytes(n0, n1, n2, zs, degree, kseg);
+  return b <= 227 * 1024 - 512 ? b : 0;
 }
 
 size_t solve2d_smem(int degree, int n0, int n1, int zl, int kseg, bool tw) {
