@@ -232,7 +232,7 @@ struct Workload {
   bool tw2d = false;  // k_solve2d runs the twisted (two-sided) passes
   // D = 3: every pass a pure contraction and one CTA per block solves all three axes (k_solve3d)
   bool fuse3d = false;
-  int s3_n[3] = {0, 0, 0}, s3_zs = 0, s3_threads = 0, s3_slab = 0, s3_nslab = 0;
+  int s3_n[3] = {0, 0, 0}, s3_zs = 0, s3_threads = 0, s3_slab = 0, s3_nslab = 0, s3_nl = 1;
   DBuf<unsigned long long> linf_int;
   DBuf<unsigned char> sflag;
   std::int64_t sflag_off[3] = {0, 0, 0};
@@ -488,6 +488,11 @@ struct Workload {
       s3_zs = pitch(slab);
       const int lines = std::max({slab * s3_n[1], slab * s3_n[2], s3_nslab == 1 ? s3_n[1] * s3_n[2] : 1});
       s3_threads = std::min(640, std::max(128, (lines + 31) / 32 * 32));
+      // four lines per thread where the slabs fill the GPU many times over
+      std::int64_t all_lines = 0;
+      for (const auto& b : blocks)
+        all_lines += static_cast<std::int64_t>(probs[static_cast<std::size_t>(b.ax[0])].n) * probs[static_cast<std::size_t>(b.ax[1])].n;
+      s3_nl = env_int("MFADD_S3_NL", all_lines >= 2048 * 148 ? 4 : 1);
     }
     rlt_stride = (mfb::rl_table_doubles(p, max_n_factor, tw2d) + 1) / 2 * 2;  // even: 16-B aligned per problem
     rlt.alloc(static_cast<std::size_t>(probs.size() * rlt_stride));
@@ -621,6 +626,7 @@ struct Workload {
       fa.s3_slab = s3_slab;
       fa.s3_nslab = s3_nslab;
       fa.s3_zs = s3_zs;
+      fa.s3_nl = s3_nl;
       fa.solve3d_threads = s3_threads;
     }
     for (int d = 0; d + 1 < D; ++d) {

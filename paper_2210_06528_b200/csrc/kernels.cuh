@@ -124,6 +124,7 @@ struct FitArgs {
   int fuse3d;                        // D = 3: every pass a pure contraction, k_solve3d solves axes 2 and 1 (and 0) in smem
   int max_n2, solve3d_threads;       // k_solve3d: largest axis-2 held extent, CTA size
   int s3_slab, s3_nslab, s3_zs;      // k_solve3d: axis-0 indices per slab, slabs per block, tile column pitch
+  int s3_nl;                         // k_solve3d: lines per thread (1 or 4)
   void* join_event;                  // cudaEvent_t the last-axis solve waits for (factorizations on a side stream)
 };
 int launch_fit_strided(int degree, const FitArgs& a, int axis, cudaStream_t s);  // axis < D-1

@@ -1324,6 +1324,93 @@ __device__ void build_tw_tables(const double* lt, const double* rv, const double
   }
 }
 
+// ---- NL lines per thread
+// The step-table row of a pass is the same for every line, and a broadcast
+// 16-byte shared-memory load still costs four wavefronts: with one line per
+// thread 12 of a step's 16 wavefronts are table reads, and the passes run
+// against the shared-memory pipe (k_solve3d: 66% of its peak).  A thread that
+// carries NL lines through the same steps reads each row once for all of
+// them and has NL independent chains in flight.  Line j of a thread sits at
+// element offset lo[j] from x0 (callers interleave the lines over the
+// threads, so a warp's accesses to line j stay contiguous); lines past the
+// end alias the thread's line 0 (same values, same stores).
+template <int P, int NL>
+struct RLN {
+  static constexpr int UB = NL >= 4 ? 4 : 8;
+  static constexpr int U = P * ((UB + P - 1) / P);  // <= RL<P>::U: the tables' padding covers it
+};
+template <int NL>
+struct RLFinalN {         // last pass of a tile: results also go to HBM (+ L-inf)
+  double* dst[NL];        // global base of each line's outputs
+  std::int64_t dstride;   // global stride per step (signed)
+  int t_lo, t_hi;         // steps [t_lo, t_hi) hold non-shared entries
+  bool line_shared[NL];
+  unsigned long long lmax;
+};
+
+template <int P, int NL, bool TAIL, bool FINAL>
+__device__ __forceinline__ void rln_batch(double* __restrict__ x0, const int (&lo)[NL], const int ds, const int n,
+                                          const int t0, const double* __restrict__ tab, double (&acc)[NL][P],
+                                          double (&zin)[NL][RLN<P, NL>::U], double (&cf)[RL<P>::W], RLFinalN<NL>& fin) {
+  constexpr int U = RLN<P, NL>::U, W = RL<P>::W;
+  double znx[NL][U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int te = t0 + U + P + u;
+#pragma unroll
+    for (int j = 0; j < NL; ++j) znx[j][u] = (!TAIL || te < n) ? x0[te * ds + lo[j]] : 0.0;
+  }
+  const double* tb = tab + t0 * W;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    double cfn[W];
+    rl_load_step<P>(tb + (u + 1) * W, cfn);  // the next step's row (tables are padded past the line)
+    const int t = t0 + u;
+#pragma unroll
+    for (int j = 0; j < NL; ++j) {
+      const double y = acc[j][u % P];
+#pragma unroll
+      for (int k = 1; k < P; ++k) acc[j][(u + k) % P] = fma(-cf[k - 1], y, acc[j][(u + k) % P]);
+      acc[j][u % P] = fma(-cf[P - 1], y, zin[j][u] * cf[P]);
+      if (!TAIL || t < n) {
+        x0[t * ds + lo[j]] = y;
+        if (FINAL) {
+          fin.dst[j][t * fin.dstride] = y;
+          if (!fin.line_shared[j] && t >= fin.t_lo && t < fin.t_hi) {
+            const unsigned long long bits = dbits_s(fabs(y));
+            fin.lmax = fin.lmax > bits ? fin.lmax : bits;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < W; ++k) cf[k] = cfn[k];
+  }
+#pragma unroll
+  for (int j = 0; j < NL; ++j)
+#pragma unroll
+    for (int u = 0; u < U; ++u) zin[j][u] = znx[j][u];
+}
+
+template <int P, int NL, bool FINAL>
+__device__ __forceinline__ void rln_pass(double* __restrict__ x0, const int (&lo)[NL], const int ds, const int n,
+                                         const double* __restrict__ tab, RLFinalN<NL>& fin) {
+  constexpr int U = RLN<P, NL>::U, W = RL<P>::W;
+  double acc[NL][P], zin[NL][U];
+#pragma unroll
+  for (int j = 0; j < NL; ++j) {
+#pragma unroll
+    for (int k = 0; k < P; ++k) acc[j][k] = (k < n ? x0[k * ds + lo[j]] : 0.0) * tab[(k - P) * W + P];
+#pragma unroll
+    for (int u = 0; u < U; ++u) zin[j][u] = P + u < n ? x0[(P + u) * ds + lo[j]] : 0.0;
+  }
+  double cf[W];
+  rl_load_step<P>(tab, cf);
+  int t0 = 0;
+  for (; t0 + 2 * U + P <= n; t0 += U) rln_batch<P, NL, false, FINAL>(x0, lo, ds, n, t0, tab, acc, zin, cf, fin);
+  for (; t0 < n; t0 += U) rln_batch<P, NL, true, FINAL>(x0, lo, ds, n, t0, tab, acc, zin, cf, fin);
+}
+
 __host__ __device__ inline size_t solve2d_smem_bytes(int n0, int n1, int zl, int P, int kseg, bool tw = false) {
   const int W = (P + 2) & ~1;
   // step tables (only when staged in shared memory) / the twisted passes' two side buffers
@@ -1397,6 +1484,9 @@ __device__ __forceinline__ unsigned stage_rl_tables(const FitArgs& a, const Axis
   return 0;
 }
 
+#ifndef MFB_S2_NL
+#define MFB_S2_NL 1  // lines per thread of k_solve2d's passes
+#endif
 template <int P>
 __global__ void __launch_bounds__(kSolve2dThreads) k_solve2d(const FitArgs a) {
   pdl_enter();
@@ -1478,8 +1568,42 @@ __global__ void __launch_bounds__(kSolve2dThreads) k_solve2d(const FitArgs a) {
     X[static_cast<std::int64_t>(c) * zl + i] += C[static_cast<std::int64_t>(r) * zl + i];
   }
   __syncthreads();
-  RLFinal fin{};
   double* Pb = a.P + blk.poff;
+#if MFB_S2_NL > 1
+  // NL lines per thread (rln_pass): a thread's lines are T apart
+  constexpr int NL = MFB_S2_NL;
+  RLFinalN<NL> fin{};
+  int lo[NL];
+  {  // G1^-1 along the rows (line i: X[.][i], stride zl)
+    const int T = (n0 + NL - 1) / NL;
+    for (int i = tid; i < T; i += nthr) {
+#pragma unroll
+      for (int j = 0; j < NL; ++j) lo[j] = i + j * T < n0 ? j * T : 0;
+      rln_pass<P, NL, false>(X + i, lo, zl, n1, f1 + P * W, fin);
+      rln_pass<P, NL, false>(X + i + (n1 - 1) * zl, lo, -zl, n1, b1 + P * W, fin);
+    }
+  }
+  __syncthreads();
+  {  // G0^-1 along the columns (line c: X[c][.], stride 1), P_b and the L-inf from the backward pass
+    const int T = (n1 + NL - 1) / NL;
+    for (int c = tid; c < T; c += nthr) {
+#pragma unroll
+      for (int j = 0; j < NL; ++j) {
+        const int cj = c + j * T < n1 ? c + j * T : c;
+        lo[j] = (cj - c) * zl;
+        fin.dst[j] = Pb + static_cast<std::int64_t>(n0 - 1) * n1 + cj;
+        fin.line_shared[j] = sf1[cj] != 0;
+      }
+      double* xc = X + static_cast<std::int64_t>(c) * zl;
+      rln_pass<P, NL, false>(xc, lo, 1, n0, f0 + P * W, fin);
+      fin.dstride = -n1;
+      fin.t_lo = n0 - s_ns[1];  // step t is axis-0 index n0 - 1 - t
+      fin.t_hi = n0 - s_ns[0];
+      rln_pass<P, NL, true>(xc + (n0 - 1), lo, -1, n0, b0 + P * W, fin);
+    }
+  }
+#else
+  RLFinal fin{};
   // G1^-1 along the rows (thread per row; stride zl)
   for (int i = tid; i < n0; i += nthr) {
     rl_pass<P, false>(X + i, zl, n1, f1 + P * W, fin);
@@ -1499,6 +1623,7 @@ __global__ void __launch_bounds__(kSolve2dThreads) k_solve2d(const FitArgs a) {
     fin.line_shared = sf1[c] != 0;
     rl_pass<P, true>(xc + (n0 - 1), -1, n0, b0 + P * W, fin);
   }
+#endif
   unsigned long long lmax = fin.lmax;
   const int lane = tid & 31, warp = tid >> 5, nw = nthr >> 5;
 #pragma unroll
@@ -1788,6 +1913,9 @@ __global__ void __launch_bounds__(kSolve2dThreads) k_solve2d_tw(const FitArgs a)
 // controls (solver.cpp:97-101).  Replaces the middle pass's in-place solve on
 // T2 and k_last_solve (strided walks over HBM-resident intermediates).
 constexpr int kSolve3dMaxThreads = 640;
+// Lines per thread of k_solve3d's passes (FitArgs::s3_nl): 4 where the grid
+// fills the GPU many times over (C4: 3072 slabs; 271 vs 320 us for the
+// last-axis group), 1 where CTAs are scarce (C3: 512 slabs; 62 vs 81 us).
 
 // Shared memory: the slab tile, the segment carries, two step-table slots
 // (each a forward + backward table of the largest extent: axis 2's and axis
@@ -1802,8 +1930,8 @@ __host__ __device__ inline size_t solve3d_smem_bytes(int n0, int n1, int n2, int
          static_cast<size_t>(n0 + n1 + n2 + 16);
 }
 
-template <int P>
-__global__ void __launch_bounds__(kSolve3dMaxThreads) k_solve3d(const FitArgs a) {
+template <int P, int NL>
+__global__ void __launch_bounds__((kSolve3dMaxThreads / NL + 31) / 32 * 32) k_solve3d(const FitArgs a) {
   pdl_enter();
   extern __shared__ __align__(128) double s2d[];
   __shared__ unsigned long long s_red[32];
@@ -1889,11 +2017,17 @@ __global__ void __launch_bounds__(kSolve3dMaxThreads) k_solve3d(const FitArgs a)
     X[static_cast<std::int64_t>(c) * zs + i] += C[static_cast<std::int64_t>(r) * zs + i];
   }
   __syncthreads();
-  RLFinal fin{};
-  // G2^-1 along c (thread per line ls; stride zs)
-  for (int l = tid; l < L; l += nthr) {
-    rl_pass<P, false>(X + l, zs, n2, f2 + P * W, fin);
-    rl_pass<P, false>(X + l + (n2 - 1) * zs, -zs, n2, b2 + P * W, fin);
+  RLFinalN<NL> fin{};
+  int lo[NL];
+  // G2^-1 along c (line ls: X[.][ls], stride zs); a thread's lines are T apart
+  {
+    const int T = (L + NL - 1) / NL;
+    for (int l = tid; l < T; l += nthr) {
+#pragma unroll
+      for (int j = 0; j < NL; ++j) lo[j] = l + j * T < L ? j * T : 0;
+      rln_pass<P, NL, false>(X + l, lo, zs, n2, f2 + P * W, fin);
+      rln_pass<P, NL, false>(X + l + (n2 - 1) * zs, lo, -zs, n2, b2 + P * W, fin);
+    }
   }
   __syncthreads();
   if (whole) {  // axis 0's tables over axis 2's, behind the axis-1 phase
@@ -1903,21 +2037,32 @@ __global__ void __launch_bounds__(kSolve3dMaxThreads) k_solve3d(const FitArgs a)
     }
     stage_rl_tables<P>(a, p0, blk.ax[0], f0, b0, bar + 1, tid, nthr);
   }
-  // G1^-1 along i1 (thread per (i0, c), c fastest; stride 1).  Several slabs:
-  // the backward pass writes P_b[i0][i1][c] (coalesced over the warp's c).
+  // G1^-1 along i1 (line (i0, c), c fastest: X[c][i0 n1 + .], stride 1).
+  // Several slabs: the backward pass writes P_b[i0][i1][c] (coalesced over
+  // the warp's c).
   double* Pb = a.P + blk.poff;
-  for (int q = tid; q < S0 * n2; q += nthr) {
-    const int i0r = q / n2, c = q - i0r * n2;
-    double* x = X + static_cast<std::int64_t>(c) * zs + i0r * n1;
-    rl_pass<P, false>(x, 1, n1, f1 + P * W, fin);
-    if (whole) {
-      rl_pass<P, false>(x + (n1 - 1), -1, n1, b1 + P * W, fin);
-    } else {
-      fin.dst = Pb + (static_cast<std::int64_t>(i0a + i0r) * n1 + (n1 - 1)) * n2 + c;
-      fin.dstride = -n2;
-      fin.t_lo = fin.t_hi = 0;
-      fin.line_shared = true;  // (the L-inf is taken by the axis-0 solve)
-      rl_pass<P, true>(x + (n1 - 1), -1, n1, b1 + P * W, fin);
+  {
+    const int NQ = S0 * n2, T = (NQ + NL - 1) / NL;
+    for (int q0 = tid; q0 < T; q0 += nthr) {
+      double* x = nullptr;
+#pragma unroll
+      for (int j = 0; j < NL; ++j) {
+        const int q = q0 + j * T < NQ ? q0 + j * T : q0;
+        const int i0r = q / n2, c = q - i0r * n2;
+        double* xj = X + static_cast<std::int64_t>(c) * zs + i0r * n1;
+        if (j == 0) x = xj;
+        lo[j] = static_cast<int>(xj - x);
+        fin.dst[j] = Pb + (static_cast<std::int64_t>(i0a + i0r) * n1 + (n1 - 1)) * n2 + c;
+        fin.line_shared[j] = true;  // (the L-inf is taken by the axis-0 solve)
+      }
+      rln_pass<P, NL, false>(x, lo, 1, n1, f1 + P * W, fin);
+      if (whole) {
+        rln_pass<P, NL, false>(x + (n1 - 1), lo, -1, n1, b1 + P * W, fin);
+      } else {
+        fin.dstride = -n2;
+        fin.t_lo = fin.t_hi = 0;
+        rln_pass<P, NL, true>(x + (n1 - 1), lo, -1, n1, b1 + P * W, fin);
+      }
     }
   }
   if (!whole) return;
@@ -1925,16 +2070,26 @@ __global__ void __launch_bounds__(kSolve3dMaxThreads) k_solve3d(const FitArgs a)
   mbar_wait(bar + 1, 0);
   // G0^-1 along i0 (thread per (i1, c), c fastest; stride n1); the backward
   // pass writes P_b[i0][i1][c] and the L-inf over non-shared controls
-  for (int q = tid; q < n1 * n2; q += nthr) {
-    const int i1 = q / n2, c = q - i1 * n2;
-    double* x = X + static_cast<std::int64_t>(c) * zs + i1;
-    rl_pass<P, false>(x, n1, n0, f0 + P * W, fin);
-    fin.dst = Pb + (static_cast<std::int64_t>(n0 - 1) * n1 + i1) * n2 + c;
-    fin.dstride = -static_cast<std::int64_t>(n1) * n2;
-    fin.t_lo = n0 - s_ns[1];  // step t is axis-0 index n0 - 1 - t
-    fin.t_hi = n0 - s_ns[0];
-    fin.line_shared = (sf1[i1] | sf2[c]) != 0;
-    rl_pass<P, true>(x + (n0 - 1) * n1, -n1, n0, b0 + P * W, fin);
+  {
+    const int NQ = n1 * n2, T = (NQ + NL - 1) / NL;
+    for (int q0 = tid; q0 < T; q0 += nthr) {
+      double* x = nullptr;
+#pragma unroll
+      for (int j = 0; j < NL; ++j) {
+        const int q = q0 + j * T < NQ ? q0 + j * T : q0;
+        const int i1 = q / n2, c = q - i1 * n2;
+        double* xj = X + static_cast<std::int64_t>(c) * zs + i1;
+        if (j == 0) x = xj;
+        lo[j] = static_cast<int>(xj - x);
+        fin.dst[j] = Pb + (static_cast<std::int64_t>(n0 - 1) * n1 + i1) * n2 + c;
+        fin.line_shared[j] = (sf1[i1] | sf2[c]) != 0;
+      }
+      rln_pass<P, NL, false>(x, lo, n1, n0, f0 + P * W, fin);
+      fin.dstride = -static_cast<std::int64_t>(n1) * n2;
+      fin.t_lo = n0 - s_ns[1];  // step t is axis-0 index n0 - 1 - t
+      fin.t_hi = n0 - s_ns[0];
+      rln_pass<P, NL, true>(x + (n0 - 1) * n1, lo, -n1, n0, b0 + P * W, fin);
+    }
   }
   unsigned long long lmax = fin.lmax;
   const int lane = tid & 31, warp = tid >> 5, nw = (nthr + 31) >> 5;
@@ -2426,8 +2581,15 @@ struct LastLaunch {
     if (a.join_event) cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(a.join_event), 0);
     if (a.fuse3d) {
       const size_t sm3 = solve3d_smem_bytes(a.max_n0, a.max_n1, a.max_n2, a.s3_zs, P, kseg);
-      cudaFuncSetAttribute(k_solve3d<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm3));
-      launch_pdl(k_solve3d<P>, dim3(a.nblocks, a.s3_nslab), dim3(a.solve3d_threads), sm3, s, a);
+      const int nl = a.s3_nl >= 4 ? 4 : 1;
+      const int thr3 = std::max(64, ((a.solve3d_threads + nl - 1) / nl + 31) / 32 * 32);
+      if (nl == 4) {
+        cudaFuncSetAttribute(k_solve3d<P, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm3));
+        launch_pdl(k_solve3d<P, 4>, dim3(a.nblocks, a.s3_nslab), dim3(thr3), sm3, s, a);
+      } else {
+        cudaFuncSetAttribute(k_solve3d<P, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm3));
+        launch_pdl(k_solve3d<P, 1>, dim3(a.nblocks, a.s3_nslab), dim3(thr3), sm3, s, a);
+      }
       return 2;
     }
     if (a.fuse2d) {
