@@ -232,7 +232,7 @@ struct Workload {
   bool tw2d = false;  // k_solve2d runs the twisted (two-sided) passes
   // D = 3: every pass a pure contraction and one CTA per block solves all three axes (k_solve3d)
   bool fuse3d = false;
-  int s3_n[3] = {0, 0, 0}, s3_zs = 0, s3_threads = 0, s3_slab = 0, s3_nslab = 0, s3_nl = 1;
+  int s3_n[3] = {0, 0, 0}, s3_zs = 0, s3_threads = 0, s3_slab = 0, s3_nslab = 0, s3_nl = 1, a0_slab = 0, a0_zr = 0;
   DBuf<unsigned long long> linf_int;
   DBuf<unsigned char> sflag;
   std::int64_t sflag_off[3] = {0, 0, 0};
@@ -493,6 +493,20 @@ struct Workload {
       for (const auto& b : blocks)
         all_lines += static_cast<std::int64_t>(probs[static_cast<std::size_t>(b.ax[0])].n) * probs[static_cast<std::size_t>(b.ax[1])].n;
       s3_nl = env_int("MFADD_S3_NL", all_lines >= 2048 * 148 ? 4 : 1);
+      // the axis-0 solve on i1 slabs of ~224 lines in place of the strided
+      // walkers where slabs are scarce (C3: 91.7 vs 95.9 us for the group; on
+      // C4 the walkers win, 439 vs 474 us); MFADD_A0_SLAB / MFADD_NO_A0_SLAB force it
+      a0_slab = 0;
+      if (fuse3d && s3_nslab > 1 && !std::getenv("MFADD_NO_A0_SLAB") && (s3_nl == 1 || std::getenv("MFADD_A0_SLAB"))) {
+        int sl = std::min(s3_n[1], std::max(1, env_int("MFADD_A0_SLAB", std::max(1, 224 / s3_n[2]))));
+        while (sl > 1 && (mfb::axis0_slab_smem(p, s3_n[0], sl * s3_n[2]) == 0 ||
+                          mfb::axis0_slab_smem(p, s3_n[0], sl * s3_n[2]) > static_cast<std::size_t>(env_int("MFADD_S3_KB", 75)) * 1024))
+          --sl;
+        if (mfb::axis0_slab_smem(p, s3_n[0], sl * s3_n[2]) > 0) {
+          a0_slab = sl;
+          a0_zr = (sl * s3_n[2] + 1) & ~1;
+        }
+      }
     }
     rlt_stride = (mfb::rl_table_doubles(p, max_n_factor, tw2d) + 1) / 2 * 2;  // even: 16-B aligned per problem
     rlt.alloc(static_cast<std::size_t>(probs.size() * rlt_stride));
@@ -627,6 +641,8 @@ struct Workload {
       fa.s3_nslab = s3_nslab;
       fa.s3_zs = s3_zs;
       fa.s3_nl = s3_nl;
+      fa.a0_slab = a0_slab;
+      fa.a0_zr = a0_zr;
       fa.solve3d_threads = s3_threads;
     }
     for (int d = 0; d + 1 < D; ++d) {
@@ -694,7 +710,7 @@ struct Workload {
       l += mfb::launch_fit_last(p, fa, ctx->stream);
     }
     tl->end();
-    if (fa.defer_back && !fa.fuse2d && !(fa.fuse3d && fa.s3_nslab == 1)) {
+    if (fa.defer_back && !fa.fuse2d && !(fa.fuse3d && (fa.s3_nslab == 1 || fa.a0_slab > 0))) {
       int mxn0 = 0;
       std::int64_t mxr = 1;
       fa.min_n0 = 1 << 30;

@@ -125,6 +125,7 @@ struct FitArgs {
   int max_n2, solve3d_threads;       // k_solve3d: largest axis-2 held extent, CTA size
   int s3_slab, s3_nslab, s3_zs;      // k_solve3d: axis-0 indices per slab, slabs per block, tile column pitch
   int s3_nl;                         // k_solve3d: lines per thread (1 or 4)
+  int a0_slab, a0_zr;                // k_axis0_slab: axis-1 indices per slab (0: k_axis0_backsub instead), tile row pitch
   void* join_event;                  // cudaEvent_t the last-axis solve waits for (factorizations on a side stream)
 };
 int launch_fit_strided(int degree, const FitArgs& a, int axis, cudaStream_t s);  // axis < D-1
@@ -133,6 +134,8 @@ int launch_fit_last(int degree, const FitArgs& a, cudaStream_t s);
 size_t solve2d_smem(int degree, int n0, int n1, int zl, int kseg, bool tw = false);
 // Shared-memory bytes of k_solve3d for held extents n0 x n1 x n2 and a tile column pitch zs (0 if over the CTA limit).
 size_t solve3d_smem(int degree, int n0, int n1, int n2, int zs, int kseg);
+// Shared-memory bytes of k_axis0_slab for an axis-0 extent n0 and `lines` lines per slab (0 if over the CTA limit).
+size_t axis0_slab_smem(int degree, int n0, int lines);
 
 // D = 1: CTA per block, column-parallel R^T q + serial banded solve (smem: max_n x (2P+2) doubles).
 int launch_fit_1d(int degree, const FitArgs& a, int max_n, cudaStream_t s);

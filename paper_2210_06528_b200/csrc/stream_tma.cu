@@ -2107,6 +2107,104 @@ __global__ void __launch_bounds__((kSolve3dMaxThreads / NL + 31) / 32 * 32) k_so
   }
 }
 
+// ------------------------------- axis-0 solve on shared-memory slabs (D = 3)
+// After k_solve3d's slabs, P_b holds G2^-1 G1^-1 Z; this kernel applies G0^-1
+// along i0 (lsq.cpp:59-60 on axis 0).  A CTA takes the slab i1 in [i1a, i1b) of
+// one block: for every i0 the values P_b[i0][i1a..i1b)[.] are one contiguous
+// run, copied (coalesced loads) into X[i0][r], r = (i1 - i1a) n2 + c.  The
+// passes walk i0 with the tile's row pitch (a warp's lines are consecutive r:
+// conflict-free); the backward pass writes P_b back in place (coalesced) and
+// takes the per-block L-inf over non-shared controls (solver.cpp:97-101).
+// Replaces k_axis0_backsub / k_axis0_solve_part, whose threads walk the
+// HBM-resident lattice with a stride of n1 n2 values.
+__host__ __device__ inline size_t axis0_slab_smem_bytes(int n0, int lines, int P) {
+  const int W = (P + 2) & ~1;
+  return 128 + (static_cast<size_t>(n0) * ((lines + 1) & ~1) + 2 * static_cast<size_t>(rl_rows(n0, P)) * W) * 8 + 64;
+}
+
+template <int P, int NL>
+__global__ void __launch_bounds__((kSolve3dMaxThreads / NL + 31) / 32 * 32) k_axis0_slab(const FitArgs a) {
+  pdl_enter();
+  extern __shared__ __align__(128) double s2d[];
+  __shared__ unsigned long long s_red[32];
+  __shared__ int s_ns[2];  // non-shared axis-0 indices: [s_ns[0], s_ns[1])
+  constexpr int W = RL<P>::W;
+  const int bid = blockIdx.x;
+  const BlockDev& blk = a.blocks[bid];
+  const AxisProb p0 = a.probs[blk.ax[0]], p1 = a.probs[blk.ax[1]], p2 = a.probs[blk.ax[2]];
+  const int n0 = p0.n, n1 = p1.n, n2 = p2.n;
+  const int i1a = static_cast<int>(blockIdx.y) * a.a0_slab;
+  if (i1a >= n1) return;
+  const int i1b = i1a + a.a0_slab < n1 ? i1a + a.a0_slab : n1;
+  const int L = (i1b - i1a) * n2, zr = a.a0_zr;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  std::uint64_t* bar = reinterpret_cast<std::uint64_t*>(s2d);
+  double* X = s2d + 16;  // [n0][zr]
+  double* f0 = X + static_cast<std::int64_t>(n0) * zr;
+  double* b0 = f0 + rl_rows(n0, P) * W;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(bar, 2 * static_cast<unsigned>(rl_rows(n0, P) * W) * 8);
+    s_ns[0] = n0;
+    s_ns[1] = 0;
+  }
+  stage_rl_tables<P>(a, p0, blk.ax[0], f0, b0, bar, tid, nthr);
+  double* Pb = a.P + blk.poff + static_cast<std::int64_t>(i1a) * n2;
+  const std::int64_t grow = static_cast<std::int64_t>(n1) * n2;  // P_b values per i0
+  {  // tile load, 4 rows of every line in flight
+    for (int i0 = 0; i0 < n0; i0 += 4)
+      for (int r = tid; r < L; r += nthr) {
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = i0 + u < n0 ? Pb[(i0 + u) * grow + r] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (i0 + u < n0) X[(i0 + u) * zr + r] = v[u];
+      }
+  }
+  __syncthreads();
+  for (int i = tid; i < n0; i += nthr)
+    if (!a.shared_flag[a.sflag_off[0] + p0.col_lo + i]) {
+      atomicMin(&s_ns[0], i);
+      atomicMax(&s_ns[1], i + 1);
+    }
+  __syncthreads();
+  mbar_wait(bar, 0);
+  RLFinalN<NL> fin{};
+  int lo[NL];
+  const int T = (L + NL - 1) / NL;
+  for (int r0 = tid; r0 < T; r0 += nthr) {
+#pragma unroll
+    for (int j = 0; j < NL; ++j) {
+      const int r = r0 + j * T < L ? r0 + j * T : r0;
+      const int i1 = i1a + r / n2, c = r - (r / n2) * n2;
+      lo[j] = r - r0;
+      fin.dst[j] = Pb + static_cast<std::int64_t>(n0 - 1) * grow + r;
+      fin.line_shared[j] = (a.shared_flag[a.sflag_off[1] + p1.col_lo + i1] | a.shared_flag[a.sflag_off[2] + p2.col_lo + c]) != 0;
+    }
+    rln_pass<P, NL, false>(X + r0, lo, zr, n0, f0 + P * W, fin);
+    fin.dstride = -grow;
+    fin.t_lo = n0 - s_ns[1];  // step t is axis-0 index n0 - 1 - t
+    fin.t_hi = n0 - s_ns[0];
+    rln_pass<P, NL, true>(X + r0 + static_cast<std::int64_t>(n0 - 1) * zr, lo, -zr, n0, b0 + P * W, fin);
+  }
+  unsigned long long lmax = fin.lmax;
+  const int lane = tid & 31, warp = tid >> 5, nw = (nthr + 31) >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long t2 = __shfl_xor_sync(kFullMask, lmax, o);
+    lmax = lmax > t2 ? lmax : t2;
+  }
+  if (lane == 0) s_red[warp] = lmax;
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long mx = 0ull;
+    for (int w2 = 0; w2 < nw; ++w2) mx = mx > s_red[w2] ? mx : s_red[w2];
+    if (mx) atomicMax(a.linf_int + bid, mx);
+  }
+}
+
 template <int P>
 struct BacksubLaunch {
   static int run(const FitArgs& a, int max_n0, std::int64_t max_rest, cudaStream_t s) {
@@ -2590,6 +2688,20 @@ struct LastLaunch {
         cudaFuncSetAttribute(k_solve3d<P, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm3));
         launch_pdl(k_solve3d<P, 1>, dim3(a.nblocks, a.s3_nslab), dim3(thr3), sm3, s, a);
       }
+      if (a.s3_nslab > 1 && a.a0_slab > 0) {  // the axis-0 solve on i1 slabs
+        const int lines = a.a0_slab * a.max_n2;
+        const size_t sma = axis0_slab_smem_bytes(a.max_n0, lines, P);
+        const int thra = std::max(64, ((std::min(lines, kSolve3dMaxThreads) + nl - 1) / nl + 31) / 32 * 32);
+        const dim3 ga(a.nblocks, (a.max_n1 + a.a0_slab - 1) / a.a0_slab);
+        if (nl == 4) {
+          cudaFuncSetAttribute(k_axis0_slab<P, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sma));
+          launch_pdl(k_axis0_slab<P, 4>, ga, dim3(thra), sma, s, a);
+        } else {
+          cudaFuncSetAttribute(k_axis0_slab<P, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sma));
+          launch_pdl(k_axis0_slab<P, 1>, ga, dim3(thra), sma, s, a);
+        }
+        return 3;
+      }
       return 2;
     }
     if (a.fuse2d) {
@@ -2658,6 +2770,11 @@ std::int64_t rl_table_doubles(int degree, int n, bool tw) {
     case 9: return RlDoubles<9>::run(n, tw);
     default: return 0;
   }
+}
+
+size_t axis0_slab_smem(int degree, int n0, int lines) {
+  const size_t b = axis0_slab_smem_bytes(n0, lines, degree);
+  return b <= 227 * 1024 - 512 ? b : 0;
 }
 
 size_t solve3d_smem(int degree, int n0, int n1, int n2, int zs, int kseg) {
