@@ -2604,8 +2604,10 @@ struct Axis0Launch {
     }
   }
   static int run(const FitArgs& a, const CUtensorMap& map, const TmaGeom& g, int ntiles, cudaStream_t s) {
-    // NC = 2 (two columns per thread) measured slower on C5 (331 vs 233 us): fewer resident warps
-    static const int nc = std::getenv("MFADD_FIT_NC") ? std::atoi(std::getenv("MFADD_FIT_NC")) : 1;
+    // NC = 2 (two columns per thread, one LDS.128 per row): slower on C5 (331 vs
+    // 233 us: fewer resident warps), faster for D = 3 (C4 902 -> 798 us, C3 59.6 -> 55.5 us)
+    static const int nc_env = std::getenv("MFADD_FIT_NC") ? std::atoi(std::getenv("MFADD_FIT_NC")) : 0;
+    const int nc = nc_env > 0 ? nc_env : (a.D == 3 ? 2 : 1);
     if (nc == 1)
       g.S == 3 ? go<3, 1>(a, map, g, ntiles, s) : go<4, 1>(a, map, g, ntiles, s);
     else
@@ -2805,7 +2807,11 @@ namespace {
 template <int P>
 struct MidLaunch {
   static int run(const FitArgs& a, const CUtensorMap& map, const TmaGeom& g, int ntiles, int max_n0, cudaStream_t s) {
-    Axis0Launch<P>::template go<4, 1, true>(a, map, g, ntiles, s, max_n0);
+    static const int nc = std::getenv("MFADD_MID_NC") ? std::atoi(std::getenv("MFADD_MID_NC")) : 1;
+    if (nc == 2)
+      Axis0Launch<P>::template go<4, 2, true>(a, map, g, ntiles, s, max_n0);
+    else
+      Axis0Launch<P>::template go<4, 1, true>(a, map, g, ntiles, s, max_n0);
     return 1;
   }
 };
