@@ -1286,8 +1286,11 @@ __device__ void epoch_finalize(const EpochRegionArgs& a, int mode, int slot, uns
 // 8 for 3-D.
 // SNAP: the log_errors form that also writes the epoch snapshots of the
 // shared copies (residual_tma.cu); the plain form is the solve's hot epoch.
+#ifndef MFB_EPOCH8_CTAS
+#define MFB_EPOCH8_CTAS 3  // resident CTAs per SM of the n_s = 8 (3-D) form (3: C4 epochs 347 -> 327 us, C3 82 -> 80 us)
+#endif
 template <int MAXNS, bool SNAP>
-__global__ void __launch_bounds__(kRegionThreads, MAXNS == 8 ? 2 : 3) k_epoch_regions(EpochRegionArgs a) {
+__global__ void __launch_bounds__(kRegionThreads, MAXNS == 8 ? MFB_EPOCH8_CTAS : 3) k_epoch_regions(EpochRegionArgs a) {
   __shared__ double s_w[2 * kRegionMaxHolders + 1][kRegionWarps];
   __shared__ unsigned long long s_red[32];
   __shared__ int s_last;
@@ -2236,7 +2239,7 @@ int launch_epoch_regions(const EpochRegionArgs& a, cudaStream_t s) {
   if (a.mode == 3)  // persistent over the tiles: one wave (usually it exits at once)
     launch_pdl(k_pair_jumps_regions, dim3(a.ntiles < 2 * sms ? a.ntiles : 2 * sms), dim3(kRegionThreads), 0, s, a);
   else {
-    const int per_sm = a.max_ns > 4 ? 2 : 3;  // __launch_bounds__ residency
+    const int per_sm = a.max_ns > 4 ? MFB_EPOCH8_CTAS : 3;  // __launch_bounds__ residency
     const int grid = a.ntiles < sms * per_sm ? a.ntiles : sms * per_sm;
     if (a.max_ns > 4)
       a.snap ? launch_pdl(k_epoch_regions<8, true>, dim3(grid), dim3(kRegionThreads), 0, s, a)

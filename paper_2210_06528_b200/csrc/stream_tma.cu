@@ -271,7 +271,13 @@ __global__ void __launch_bounds__(256) k_fit_axis0_tma(const FitArgs a, const __
           continue;
         }
         double q[NC];
-        if (NC == 2) {
+        if (NC == 4) {
+          const double2 qa = *reinterpret_cast<const double2*>(sq), qb = *reinterpret_cast<const double2*>(sq + 2);
+          q[0] = qa.x;
+          q[1 % NC] = qa.y;
+          q[2 % NC] = qb.x;
+          q[NC - 1] = qb.y;
+        } else if (NC == 2) {
           const double2 q2 = *reinterpret_cast<const double2*>(sq);
           q[0] = q2.x;
           q[NC - 1] = q2.y;
@@ -2610,6 +2616,8 @@ struct Axis0Launch {
     const int nc = nc_env > 0 ? nc_env : (a.D == 3 ? 2 : 1);
     if (nc == 1)
       g.S == 3 ? go<3, 1>(a, map, g, ntiles, s) : go<4, 1>(a, map, g, ntiles, s);
+    else if (nc == 4 && g.B2 % 4 == 0 && a.D == 3)
+      g.S == 3 ? go<3, 4>(a, map, g, ntiles, s) : go<4, 4>(a, map, g, ntiles, s);
     else
       g.S == 3 ? go<3, 2>(a, map, g, ntiles, s) : go<4, 2>(a, map, g, ntiles, s);
     return 1;
