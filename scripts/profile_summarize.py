@@ -1,8 +1,10 @@
 """Turn scripts/profile_round.sh outputs (gpurun_out/prof_*) into profiles/:
 
-  profiles/r01_launches.csv   launch list (kernel, us) of the bench command
-  profiles/r01_ncu_full.csv   one line per kernel of one solve (ncu --set full)
-  profiles/ncu_traffic.json   DRAM bytes per launch per bench kernel group (roofline.traffic)
+  profiles/<round>_launches.csv   launch list (kernel, us) of the bench command
+  profiles/<round>_ncu_full.csv   one line per kernel of one solve (ncu --set full)
+  profiles/ncu_traffic.json       DRAM bytes per launch per bench kernel group (roofline.traffic)
+
+    python scripts/profile_summarize.py [round tag, default r02]
 """
 import csv
 import json
@@ -11,6 +13,7 @@ import re
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+TAG = sys.argv[1] if len(sys.argv) > 1 else "r02"
 G = os.path.join(ROOT, "gpurun_out")
 P = os.path.join(ROOT, "profiles")
 
@@ -37,7 +40,7 @@ def launches():
         v = float(r[vi].replace(",", ""))
         v = v / 1000.0 if r[ui] == "nsecond" or r[ui] == "ns" else (v if r[ui] in ("usecond", "us") else v * 1000.0)
         out.append((short(r[ki]), v))
-    with open(os.path.join(P, "r01_launches.csv"), "w") as f:
+    with open(os.path.join(P, TAG + "_launches.csv"), "w") as f:
         f.write("# ncu --metrics gpu__time_duration.sum --clock-control none -c 400 -- python bench.py --steps 2 "
                 "--warmup 3 --no-cpu-baseline --no-e2e (C5); cold-cache, serialised per launch; graph-replayed "
                 "solves show only their first direct launches\n")
@@ -71,7 +74,7 @@ def full():
             rec[nm] = v * SCALE.get(units[i], 1.0)
         recs.append(rec)
     cols = ["kernel"] + [nm for _, nm in WANT]
-    with open(os.path.join(P, "r01_ncu_full.csv"), "w") as f:
+    with open(os.path.join(P, TAG + "_ncu_full.csv"), "w") as f:
         f.write(",".join(cols) + "\n")
         for rec in recs:
             f.write(",".join(str(round(rec[c], 3)) if isinstance(rec.get(c), float) else str(rec.get(c, ""))
@@ -86,7 +89,7 @@ def full():
                 tot += rec.get("dram_read_B", 0.0) + rec.get("dram_write_B", 0.0)
         if seen:
             traffic[g] = tot
-    traffic["_source"] = ("profiles/r01_ncu_full.csv: ncu --set full (C5, one solve, MFADD_HOST_LOOP=1 direct "
+    traffic["_source"] = ("profiles/" + TAG + "_ncu_full.csv: ncu --set full (C5, one solve, MFADD_HOST_LOOP=1 direct "
                           "launches), dram__bytes_read.sum + dram__bytes_write.sum per launch, summed over the "
                           "kernels of each bench.py group")
     with open(os.path.join(P, "ncu_traffic.json"), "w") as f:
