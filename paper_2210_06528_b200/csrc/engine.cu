@@ -494,10 +494,10 @@ struct Workload {
         all_lines += static_cast<std::int64_t>(probs[static_cast<std::size_t>(b.ax[0])].n) * probs[static_cast<std::size_t>(b.ax[1])].n;
       s3_nl = env_int("MFADD_S3_NL", all_lines >= 2048 * 148 ? 4 : 1);
       // the axis-0 solve on i1 slabs of ~224 lines in place of the strided
-      // walkers where slabs are scarce (C3: 91.7 vs 95.9 us for the group; on
-      // C4 the walkers win, 439 vs 474 us); MFADD_A0_SLAB / MFADD_NO_A0_SLAB force it
+      // walkers (C4: last-axis group 440 -> 402 us, C3 95.9 -> 91.2 us);
+      // MFADD_A0_SLAB sets the slab, MFADD_NO_A0_SLAB keeps the walkers
       a0_slab = 0;
-      if (fuse3d && s3_nslab > 1 && !std::getenv("MFADD_NO_A0_SLAB") && (s3_nl == 1 || std::getenv("MFADD_A0_SLAB"))) {
+      if (fuse3d && s3_nslab > 1 && !std::getenv("MFADD_NO_A0_SLAB")) {
         int sl = std::min(s3_n[1], std::max(1, env_int("MFADD_A0_SLAB", std::max(1, 224 / s3_n[2]))));
         while (sl > 1 && (mfb::axis0_slab_smem(p, s3_n[0], sl * s3_n[2]) == 0 ||
                           mfb::axis0_slab_smem(p, s3_n[0], sl * s3_n[2]) > static_cast<std::size_t>(env_int("MFADD_S3_KB", 75)) * 1024))

@@ -2158,16 +2158,16 @@ __global__ void __launch_bounds__((kSolve3dMaxThreads / NL + 31) / 32 * 32) k_ax
   stage_rl_tables<P>(a, p0, blk.ax[0], f0, b0, bar, tid, nthr);
   double* Pb = a.P + blk.poff + static_cast<std::int64_t>(i1a) * n2;
   const std::int64_t grow = static_cast<std::int64_t>(n1) * n2;  // P_b values per i0
-  {  // tile load, 4 rows of every line in flight
-    for (int i0 = 0; i0 < n0; i0 += 4)
-      for (int r = tid; r < L; r += nthr) {
-        double v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = i0 + u < n0 ? Pb[(i0 + u) * grow + r] : 0.0;
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (i0 + u < n0) X[(i0 + u) * zr + r] = v[u];
-      }
+  {  // tile load: 8-byte asynchronous copies, all of a thread's in flight at once
+     // (P_b rows are only 8-B aligned in general, and the CTA has few threads:
+     // plain loads spent 45% of the kernel waiting on their round trips)
+    const std::uint32_t xs = smem_u32(X);
+    for (int i0 = 0; i0 < n0; ++i0)
+      for (int r = tid; r < L; r += nthr)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(xs + static_cast<std::uint32_t>(i0 * zr + r) * 8u),
+                     "l"(Pb + i0 * grow + r)
+                     : "memory");
+    asm volatile("cp.async.wait_all;" ::: "memory");
   }
   __syncthreads();
   for (int i = tid; i < n0; i += nthr)
