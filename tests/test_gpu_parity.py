@@ -416,6 +416,33 @@ def test_twisted_solve2d_knob(ctx, monkeypatch, name):
         assert np.max(np.abs(bt.p - bg.p)) <= 1e-11 * max(1.0, np.max(np.abs(bg.p)))
 
 
+FUSE3D_CASES = {
+    "C3s": SMALL["C3s"],
+    "C4s": SMALL["C4s"],
+    # odd held extents along every axis, long last axis (two row segments: the
+    # carries of the last-axis contraction reach k_solve3d)
+    "long2": W.Config("long2", (44, 46, 300), (2, 2, 2), 2, (7, 8, 41), 2, "sinc_radial"),
+}
+
+
+@pytest.mark.parametrize("env", [{}, {"MFADD_S3_SLAB": "2"}, {"MFADD_S3_SLAB": "2", "MFADD_S3_NL": "4"},
+                                 {"MFADD_S3_SLAB": "4", "MFADD_NO_A0_SLAB": "1"}, {"MFADD_S3_NL": "4"},
+                                 {"MFADD_NO_FUSE3D": "1"}],
+                         ids=["default", "slab2", "slab2-nl4", "slab4-walkers", "nl4", "unfused"])
+@pytest.mark.parametrize("name", list(FUSE3D_CASES))
+def test_fused_3d_solve_forms(ctx, monkeypatch, name, env):
+    """Every form of the 3-D fit's solve stage against the oracle: the whole
+    block in one k_solve3d CTA, axis-0 slabs + k_axis0_slab or the strided
+    walkers, one or four lines per thread, and the unfused passes
+    (lsq.cpp:57-61 in any order of the commuting axis operators)."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    cfg = FUSE3D_CASES[name]
+    values = W.make_field_numpy(cfg)
+    g, o, _ = run_both(cfg, values)
+    assert_solve_parity(g, o)
+
+
 def test_graph_replay_matches_direct(ctx, monkeypatch):
     """The first solve on a field pointer runs direct launches, the second
     captures the whole solve into a CUDA graph, later ones replay it: all must
