@@ -894,6 +894,10 @@ struct mfadd_solver {
   };
   std::vector<SolveGraph> graphs;
   cudaStream_t aux_stream = nullptr;  // captures conditional-node bodies
+  // log_errors: the one-pass residual kernel (FP64 / latency-bound) runs on its
+  // own stream beside the assembly and the decode (HBM-bound)
+  cudaStream_t res_stream = nullptr;
+  cudaEvent_t ev_res_fork = nullptr, ev_res_join = nullptr;
   // mfadd_solve_host_batch: second field / output slot, copy streams, events
   DBuf<double> field_buf2, lattice_alt, error_alt;
   cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
@@ -922,6 +926,9 @@ struct mfadd_solver {
     for (auto& e : bev)
       if (e) cudaEventDestroy(e);
     if (aux_stream) cudaStreamDestroy(aux_stream);
+    if (res_stream) cudaStreamDestroy(res_stream);
+    if (ev_res_fork) cudaEventDestroy(ev_res_fork);
+    if (ev_res_join) cudaEventDestroy(ev_res_join);
     if (h2d_stream) cudaStreamDestroy(h2d_stream);
     if (d2h_stream) cudaStreamDestroy(d2h_stream);
     if (hres) cudaFreeHost(hres);
@@ -1769,6 +1776,9 @@ std::unique_ptr<mfadd_solver> create_solver(mfadd_context* ctx, const mfadd_deco
     CK(cudaMemsetAsync(s->acc.p, 0, sizeof(mfb::EpochAcc), st));
     CK(cudaMemsetAsync(s->est.p, 0, sizeof(mfb::EpochState), st));
     CK(cudaStreamCreateWithFlags(&s->aux_stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&s->res_stream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&s->ev_res_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&s->ev_res_join, cudaEventDisableTiming));
     if (nranks > 1) {
       if (s->max_holders > 8)
         throw std::invalid_argument("mfadd_b200: a sharded solve needs at most two holders per axis");
@@ -2079,7 +2089,18 @@ int enqueue_solve(mfadd_solver* s, const double* dfield) {
     s->tl.end();
   }
   // ---- every epoch's block residuals in one pass (log_errors, snapshot form)
-  if (s->cfg.log_errors && s->res_snap) launches += launch_residuals_all(s, dfield, st);
+  // (beside the assembly and the decode on res_stream, joined before the
+  // results are read back; on the solve's own stream when kernels are timed)
+  static const bool res_inline = std::getenv("MFADD_RES_INLINE") != nullptr;
+  const bool res_side = s->cfg.log_errors && s->res_snap && !s->tl.on && !s->tl.sync_check && !res_inline;
+  if (res_side) {
+    CK(cudaEventRecord(s->ev_res_fork, st));
+    CK(cudaStreamWaitEvent(s->res_stream, s->ev_res_fork, 0));
+    launches += launch_residuals_all(s, dfield, s->res_stream);
+    CK(cudaEventRecord(s->ev_res_join, s->res_stream));
+  } else if (s->cfg.log_errors && s->res_snap) {
+    launches += launch_residuals_all(s, dfield, st);
+  }
   CK(cudaEventRecord(s->ev[3], st));
   // ---- final jumps per neighbour pair (solver.cpp:416).  After a mode-2
   // epoch all copies of each control are bit-identical and every per-pair
@@ -2113,6 +2134,7 @@ int enqueue_solve(mfadd_solver* s, const double* dfield) {
   s->tl.end();
   // ---- block_error_slab over every block == global decode (solver.cpp:425-438)
   launches += enqueue_decode(s, dfield);
+  if (res_side) CK(cudaStreamWaitEvent(st, s->ev_res_join, 0));
   CK(cudaGetLastError());
   double* hr = s->hres;
   CK(cudaMemcpyAsync(hr, s->red2.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
