@@ -2395,10 +2395,11 @@ int shard_pack(mfadd_solver* s) {
 }
 
 // One epoch's averaging/measurement on this rank after the exchange.
-int shard_compute(mfadd_solver* s, int mode, int slot) {
+int shard_compute(mfadd_solver* s, int mode, int slot, bool predicated = false) {
   cudaStream_t st = s->ctx->stream;
   int l = 0;
   mfb::EpochRegionArgs a = region_args(s, mode);
+  a.predicated = predicated ? 1 : 0;  // no-op once an earlier epoch of the chunk converged
   a.finalize = 0;
   a.recv = s->recvbuf.p;
   a.slot = slot;
@@ -2450,13 +2451,6 @@ void sync_sharded(mfadd_solver* s) {
     }
     std::this_thread::yield();
   }
-}
-
-double read_epoch_dp(mfadd_solver* s, int slot) {
-  double v = 0.0;
-  CK(cudaMemcpyAsync(&v, s->epoch_out.p + 3 * slot, sizeof v, cudaMemcpyDeviceToHost, s->ctx->stream));
-  sync_sharded(s);
-  return v;
 }
 
 int shard_assemble_decode(mfadd_solver* s, const double* dfield) {
@@ -2520,33 +2514,55 @@ void solve_group(std::vector<mfadd_solver*>& g, const std::vector<const double*>
     CK(cudaEventRecord(s->ev[2], s->ctx->stream));
     CK(cudaMemsetAsync(s->est.p, 0, sizeof(mfb::EpochState), s->ctx->stream));
   }
-  auto epoch = [&](int mode, int slot) {
+  // One epoch on every rank.  The loop bookkeeping runs on the device
+  // (k_shard_advance, after dp is max-reduced over the ranks), and an
+  // iteration enqueued behind an unread one is predicated on st->converged, so
+  // the host reads the loop state once per chunk of iterations, not per epoch.
+  auto epoch = [&](int mode, int slot, bool predicated) {
     for (std::size_t r = 0; r < g.size(); ++r) launches[r] += shard_pack(g[r]);
     tr.exchange(g);
-    for (std::size_t r = 0; r < g.size(); ++r) {
-      launches[r] += shard_compute(g[r], mode, slot);
-      launches[r] += launch_residuals(g[r], fields[r], nullptr, slot, g[r]->ctx->stream);
-    }
+    for (std::size_t r = 0; r < g.size(); ++r) launches[r] += shard_compute(g[r], mode, slot, predicated);
     tr.max_u64(g, static_cast<std::size_t>(3 * slot), 3, false);
+    for (std::size_t r = 0; r < g.size(); ++r) {
+      mfadd_solver* s = g[r];
+      launches[r] += mfb::launch_shard_advance(s->est.p, s->epoch_out.p, slot, s->cfg.tolerance, s->ctx->stream);
+      if (s->cfg.log_errors && !s->res_snap) {  // record_epoch's block errors, skipped with a skipped epoch
+        s->tl.begin("residual");
+        mfb::BlockResArgs ra = res_args(s, fields[r], s->est.p, slot);
+        ra.expect_iter = slot;
+        launches[r] += mfb::launch_block_residual(s->wl.p, ra, s->ctx->stream);
+        s->tl.end();
+      }
+    }
+  };
+  auto read_state = [&](mfadd_solver* s) {  // identical on every rank after the max
+    mfb::EpochState es{};
+    CK(cudaMemcpyAsync(&es, s->est.p, sizeof es, cudaMemcpyDeviceToHost, s->ctx->stream));
+    sync_sharded(s);
+    return es;
   };
   if (s0->cfg.log_errors)
     for (mfadd_solver* s : g)
       CK(cudaMemsetAsync(s->block_errs.p, 0, s->block_errs.n * sizeof(double), s->ctx->stream));
   tmark("fit done", 0);
-  epoch(0, 0);  // record_epoch(0, 0.0)
+  epoch(0, 0, false);  // record_epoch(0, 0.0)
   tmark("epoch", 0);
   int last = 0;
   bool converged = true;
   if (loop) {
     converged = false;
-    for (int it = 1; it <= s0->cfg.max_outer_iterations; ++it) {
-      epoch(it >= 2 ? 2 : 1, it);
-      tmark("epoch", it);
-      last = it;
-      if (read_epoch_dp(s0, it) < s0->cfg.tolerance) {  // identical on every rank after the max
-        converged = true;
-        break;
+    static const int chunk = std::max(1, env_int("MFADD_SHARD_CHUNK", 3));  // iterations per host sync
+    for (int it = 1; it <= s0->cfg.max_outer_iterations && !converged;) {
+      const int hi = std::min(s0->cfg.max_outer_iterations, it + chunk - 1);
+      for (int j = it; j <= hi; ++j) {
+        epoch(j >= 2 ? 2 : 1, j, j > it);
+        tmark("epoch", j);
       }
+      mfb::EpochState es{};
+      for (mfadd_solver* s : g) es = read_state(s);
+      last = es.last_iter;
+      converged = es.converged != 0;
+      it = hi + 1;
     }
   }
   for (mfadd_solver* s : g) CK(cudaEventRecord(s->ev[3], s->ctx->stream));

@@ -1339,7 +1339,18 @@ __global__ void __launch_bounds__(kRegionThreads, MAXNS == 8 ? MFB_EPOCH8_CTAS :
 // sharded path, where dp is then max-reduced across ranks).
 __global__ void __launch_bounds__(kRegionThreads) k_epoch_finalize(EpochRegionArgs a) {
   __shared__ unsigned long long s_red[32];
+  if (a.predicated && a.st->converged) return;  // a speculated epoch after convergence
   epoch_finalize(a, a.mode, a.slot, s_red);
+}
+
+// Sharded solve: the loop bookkeeping of epoch `slot` (solver.cpp:406-412) on
+// the device, after dp has been max-reduced over the ranks, so that the host
+// can enqueue several iterations (predicated on st->converged) per sync.
+__global__ void k_shard_advance(EpochState* st, const double* epoch_out, int slot, double tol) {
+  if (st->converged) return;
+  st->iter = slot;
+  st->last_iter = slot;
+  if (slot >= 1 && epoch_out[3 * slot] < tol) st->converged = 1;
 }
 
 // Final per-pair jumps (solver.cpp:416 -> :166-193): L-inf of |P_a - P_b| per
@@ -2225,6 +2236,10 @@ int launch_pack(const PackTile* tiles, int ntiles, const double* P, double* send
 
 int launch_epoch_finalize(const EpochRegionArgs& a, cudaStream_t s) {
   k_epoch_finalize<<<1, kRegionThreads, 0, s>>>(a);
+  return 1;
+}
+int launch_shard_advance(EpochState* st, const double* epoch_out, int slot, double tol, cudaStream_t s) {
+  k_shard_advance<<<1, 1, 0, s>>>(st, epoch_out, slot, tol);
   return 1;
 }
 

@@ -202,6 +202,8 @@ struct EpochRegionArgs {
 int launch_epoch_regions(const EpochRegionArgs& a, cudaStream_t s);
 // dp / jumps of the epoch into epoch_out[3*slot] and accumulator reset (one CTA).
 int launch_epoch_finalize(const EpochRegionArgs& a, cudaStream_t s);
+// Sharded solve: epoch `slot`'s loop bookkeeping on the device (after the dp max-reduction over ranks).
+int launch_shard_advance(EpochState* st, const double* epoch_out, int slot, double tol, cudaStream_t s);
 // Sharded solve: gather holder copies into the send buffer.
 int launch_pack(const PackTile* tiles, int ntiles, const double* P, double* send, cudaStream_t s);
 
