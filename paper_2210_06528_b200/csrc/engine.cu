@@ -287,7 +287,7 @@ struct Workload {
     } else {
       if (mx2 + 1 > 256) return;
       axis0_geo.B2 = round_up(mx2 + 1, 2);
-      axis0_geo.B1 = std::max(1, 256 / axis0_geo.B2);
+      axis0_geo.B1 = std::max(1, env_int("MFADD_AX0_B1", 256 / axis0_geo.B2));
       axis0_tiles = (mx1 + axis0_geo.B1 - 1) / axis0_geo.B1;
     }
     axis0_geo.R = 8;
