@@ -1712,11 +1712,13 @@ std::unique_ptr<mfadd_solver> create_solver(mfadd_context* ctx, const mfadd_deco
       int sms = 148;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
       const int M0 = static_cast<int>(s->srange.in_hi - s->srange.in_lo);  // this rank's input rows
-      const int per_sm = env_int("MFADD_DEC_CTAS", 8);  // CTAs per SM the row ranges aim at
-      const int want = std::max(1, (per_sm * sms + s->dnt1 * s->dnt2 - 1) / (s->dnt1 * s->dnt2));
-      const int nr = std::max(1, std::min(want, (M0 + s->dgeo.R - 1) / s->dgeo.R));
-      s->dH = round_up((M0 + nr - 1) / nr, s->dgeo.R);
-      s->dnrange = (M0 + s->dH - 1) / s->dH;
+      auto plan_rows = [&](int per_sm) {  // per_sm: CTAs per SM the row ranges aim at
+        const int want = std::max(1, (per_sm * sms + s->dnt1 * s->dnt2 - 1) / (s->dnt1 * s->dnt2));
+        const int nr = std::max(1, std::min(want, (M0 + s->dgeo.R - 1) / s->dgeo.R));
+        s->dH = round_up((M0 + nr - 1) / nr, s->dgeo.R);
+        s->dnrange = (M0 + s->dH - 1) / s->dH;
+      };
+      plan_rows(env_int("MFADD_DEC_CTAS", 8));
       s->tma_decode = true;
       npart = std::max(npart, static_cast<std::size_t>(s->dnt1) * s->dnt2 * s->dnrange);
       if (D == 3 && s->dgeo.B1 == 1 && s->dgeo.lt_cap > 0) {  // every tile's axis-2 window fits: window-only kernel
@@ -1744,7 +1746,12 @@ std::unique_ptr<mfadd_solver> create_solver(mfadd_context* ctx, const mfadd_deco
             }
             return na;
           };
-          const std::size_t budget = static_cast<std::size_t>(env_int("MFADD_DEC_STAGE_KB", 24)) * 1024;
+          // wide windows (C3: ~135 columns per CTA against C4's ~70): longer row
+          // ranges amortise the staging, 48 KB of windows and ~4 CTAs per SM
+          // (C3 decode 92.7 -> 78.3 us; C4 is fastest at 24 KB / 8: 693 vs 784 us)
+          const bool wide = static_cast<std::size_t>(mrw) * 8 * 48 > 36 * 1024;
+          if (wide) plan_rows(env_int("MFADD_DEC_CTAS", 4));
+          const std::size_t budget = static_cast<std::size_t>(env_int("MFADD_DEC_STAGE_KB", wide ? 48 : 24)) * 1024;
           int H = s->dH;
           while (H > 8 && static_cast<std::size_t>(na_for(H)) * mrw * 8 > budget) H -= 8;
           s->dH = H;
