@@ -1669,12 +1669,6 @@ __device__ __forceinline__ double lds_f64(std::uint32_t addr) {
 __device__ __forceinline__ void sts_f64(std::uint32_t addr, double v) {
   asm volatile("st.shared.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
 }
-__device__ __forceinline__ double2 lds_f64x2(std::uint32_t addr) {
-  double2 v;
-  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
-  return v;
-}
-
 template <int P>
 struct TwPass {
   std::uint32_t x0;   // byte address of step 0's line element
