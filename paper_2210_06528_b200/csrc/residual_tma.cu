@@ -61,8 +61,11 @@ __host__ __device__ inline size_t res_tma_smem(int P, int W, int EG, int na_cap,
 // NG epoch groups: the CTA runs NG threads per point, each decoding EG / NG
 // of the pass's epochs from the same staged rows (Q is still read once per
 // pass; twice the warps per SM at half the registers per thread).
+#ifndef MFB_RES_MAXREG
+#define MFB_RES_MAXREG 128  // registers per thread of the one-thread-per-point form
+#endif
 template <int P, int D, int EG, int S, int NG>
-__global__ void __maxnreg__(NG == 2 ? 84 : 128) k_residual_tma(const ResTmaArgs a, const __grid_constant__ CUtensorMap map) {
+__global__ void __maxnreg__(NG == 2 ? 84 : MFB_RES_MAXREG) k_residual_tma(const ResTmaArgs a, const __grid_constant__ CUtensorMap map) {
   extern __shared__ __align__(1024) unsigned char sm_raw[];
   __shared__ double s_red[2 * EG][16];
   const int b = blockIdx.y;
