@@ -2744,6 +2744,18 @@ MFB_API int mfadd_solve(mfadd_solver* s, const double* field, int field_on_devic
   });
 }
 
+// Measurement aid (not part of the boundary): the cached whole-solve graph of
+// one device field n times back to back, one host read-back at the end: what
+// a solve costs on the device without the host round trip between solves.
+extern "C" __attribute__((visibility("default"))) int mfadd_debug_solve_repeat(mfadd_solver* s, const double* dfield, int n) {
+  return guarded([&] {
+    ContextScope scope(s->ctx);
+    int launches = 0;
+    for (int i = 0; i < n; ++i) launches = enqueue_cached(s, dfield);
+    finish_solve(s, launches);
+  });
+}
+
 MFB_API int mfadd_solve_host(mfadd_solver* s, const double* field_host, double* out_controls_host,
                              double* out_error_host, mfadd_solve_summary* out) {
   return guarded([&] {
