@@ -132,6 +132,8 @@ int launch_fit_strided(int degree, const FitArgs& a, int axis, cudaStream_t s); 
 int launch_fit_last(int degree, const FitArgs& a, cudaStream_t s);
 // Shared-memory bytes of k_solve2d for held extents n0 x n1 (0 if it does not fit one CTA).
 size_t solve2d_smem(int degree, int n0, int n1, int zl, int kseg, bool tw = false);
+// The solve stage after the last-axis contraction (FitArgs::fuse2d / fuse3d; solve_tma.cu); returns its launches.
+int launch_solve_stage(int degree, const FitArgs& a, int kseg, cudaStream_t s);
 // Shared-memory bytes of k_solve3d for held extents n0 x n1 x n2 and a tile column pitch zs (0 if over the CTA limit).
 size_t solve3d_smem(int degree, int n0, int n1, int n2, int zs, int kseg);
 // Shared-memory bytes of k_axis0_slab for an axis-0 extent n0 and `lines` lines per slab (0 if over the CTA limit).
