@@ -2558,7 +2558,7 @@ void solve_group(std::vector<mfadd_solver*>& g, const std::vector<const double*>
   bool converged = true;
   if (loop) {
     converged = false;
-    static const int chunk = std::max(1, env_int("MFADD_SHARD_CHUNK", 3));  // iterations per host sync
+    const int chunk = std::max(1, env_int("MFADD_SHARD_CHUNK", 3));  // iterations per host sync
     for (int it = 1; it <= s0->cfg.max_outer_iterations && !converged;) {
       const int hi = std::min(s0->cfg.max_outer_iterations, it + chunk - 1);
       for (int j = it; j <= hi; ++j) {

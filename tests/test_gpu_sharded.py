@@ -41,6 +41,29 @@ def test_loopback_matches_single_device(ctx, name, cfg, ranks):
         assert r.global_linf == ref.global_linf
 
 
+@pytest.mark.parametrize("max_iters", [1, 2, 4])
+def test_loopback_iteration_budget(ctx, max_iters, monkeypatch):
+    """The chunked epoch loop (iterations enqueued ahead of the host's read of
+    the loop state, predicated on convergence) stops where the single-device
+    loop stops: out of budget before convergence, or converged inside a chunk
+    (solver.cpp:394-413)."""
+    cfg = W.scaled(W.CONFIGS["C2"], (400, 380), (20, 18))
+    values = W.make_field_numpy(cfg)
+    dec = m.partition(cfg.grid, cfg.bounds, cfg.blocks, cfg.degree, cfg.nctrl, cfg.overlap)
+    f = m.Field(list(cfg.grid), list(cfg.bounds), values)
+    scfg = m.SolverConfig(max_outer_iterations=max_iters, tolerance=cfg.tolerance, log_errors=False)
+    ref = m.solve(f, dec, scfg)
+    for chunk in ("1", "3"):
+        monkeypatch.setenv("MFADD_SHARD_CHUNK", chunk)
+        for n in (2, 8):
+            r = m.solve_loopback(f, dec, n, scfg)
+            assert (r.converged, r.constraint_iterations, len(r.epochs)) == \
+                   (ref.converged, ref.constraint_iterations, len(ref.epochs)), (max_iters, chunk, n)
+            assert [e.dp_max for e in r.epochs] == [e.dp_max for e in ref.epochs]
+            assert np.array_equal(r.model.controls, ref.model.controls)
+            assert [(j.linf_ss, j.linf_ms) for j in r.final_jumps] == [(j.linf_ss, j.linf_ms) for j in ref.final_jumps]
+
+
 def test_loopback_enforce_off_and_1d(ctx):
     # decoupled fits (no exchange epochs) still need the final cross-rank jumps
     cfg = W.scaled(W.CONFIGS["C2"], (400, 380), (20, 18))
