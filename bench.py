@@ -436,15 +436,16 @@ def main():
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    launches = 0
     for _ in range(args.steps):
         solver.run(field, on_device=True)
-        launches += solver.last_launches()
     e1.record(stream)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     clk = clocks.stop()
+    # every step solves the same field: the same launches per step (read once,
+    # outside the timed loop, whose host gaps count against the device time)
+    launches = args.steps * solver.last_launches()
     ms = e0.elapsed_time(e1) / args.steps
     # ---------------- per-kernel CUDA events: a second pass of the same K steps
     # with direct launches and an event pair around every kernel
